@@ -1,0 +1,600 @@
+/*
+ * cwb_oracle.c -- plain fp64 CPU oracle for binned componentwise boosting
+ * (arXiv 2110.03513).  TEST INFRASTRUCTURE ONLY (see cwb_oracle.h).
+ *
+ * Written from PAPER.md alone, step by step in the paper's order, with the
+ * plain definition wherever the paper has a faster equivalent.  No blocking,
+ * fusion or reordering.  Compiled with -O2 -ffp-contract=off (no FMA
+ * contraction, so every product and sum is rounded as written).
+ *
+ * Parity pins for every function live in tests/test_oracle_*.py.
+ */
+#include "cwb_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ bins */
+
+/* "n* = sqrt(n)" (Wood), rounded up (reading G1); n^(1/4). */
+int orc_n_star(int64_t n, int rule, int fixed) {
+    if (n < 1) return ORC_EINVAL;
+    if (rule == 2) return fixed >= 2 ? fixed : ORC_EINVAL;
+    if (rule == 0) {
+        int64_t s = (int64_t)ceil(sqrt((double)n));
+        while (s > 1 && (s - 1) * (s - 1) >= n) s--;
+        while (s * s < n) s++;
+        return s < 2 ? 2 : (int)s;
+    }
+    if (rule == 1) {
+        int64_t s = (int64_t)ceil(pow((double)n, 0.25));
+        while (s > 1 && (s - 1) * (s - 1) * (s - 1) * (s - 1) >= n) s--;
+        while (s * s * s * s < n) s++;
+        return s < 2 ? 2 : (int)s;
+    }
+    return ORC_EINVAL;
+}
+
+/* z_l = min(x) + (l-1)/(n*-1) (max(x) - min(x)), l = 1..n*, evaluated
+ * left to right as printed; the last point is forced to max(x) (reading G18).
+ * x goes to design point l if x in (z_l - m1, z_l + m2], m = half the
+ * distance to the neighbour; the first interval is closed on the left.  A
+ * value on a boundary goes to the lower bin (reading G2).  Boundaries are
+ * bnd_l = z_l + (z_{l+1} - z_l)/2; idx(x) = smallest l with x <= bnd_l, else
+ * the last bin.  Found by binary search over bnd (no arithmetic rounding). */
+int orc_build_bins(const double* x, int64_t n, int n_star, double* z, double* bnd, int32_t* idx) {
+    if (n < 1 || n_star < 2) return ORC_EINVAL;
+    double lo = x[0], hi = x[0];
+    for (int64_t i = 0; i < n; i++) {
+        if (!isfinite(x[i])) return ORC_ENONFINITE;
+        if (x[i] < lo) lo = x[i];
+        if (x[i] > hi) hi = x[i];
+    }
+    if (!(lo < hi)) return ORC_EDEGENERATE;
+    for (int l = 0; l < n_star; l++) {
+        double t = (double)l / (double)(n_star - 1);
+        z[l] = lo + t * (hi - lo);
+    }
+    z[n_star - 1] = hi;
+    for (int l = 0; l < n_star - 1; l++) bnd[l] = z[l] + (z[l + 1] - z[l]) / 2.0;
+    for (int64_t i = 0; i < n; i++) {
+        int a = 0, b = n_star - 1; /* answer in [a, b]; b = n*-1 means "none" */
+        while (a < b) {
+            int mid = a + (b - a) / 2;
+            if (x[i] <= bnd[mid]) b = mid;
+            else a = mid + 1;
+        }
+        idx[i] = a;
+    }
+    return ORC_OK;
+}
+
+/* ----------------------------------------------------------------- basis */
+
+/* "20 knots and degree 3" -> 20 inner knots, d = n_knots + degree + 1
+ * (reading G5). */
+int orc_basis_dim(int degree, int n_knots) { return n_knots + degree + 1; }
+
+/* P:L822 g_k(x) = (B_1(x), ..., B_d(x)): B-splines (P-splines, Eilers & Marx).
+ * Knots equidistant over [lo, hi] extended by `degree` knots on each side
+ * (reading G6): t_q = lo + (q - degree) h, h = (hi - lo)/(n_knots + 1),
+ * q = 0 .. n_knots + 2 degree + 1.  Cox-de Boor recursion:
+ *   B_{q,0}(x) = 1{t_q <= x < t_{q+1}}
+ *   B_{q,p}(x) = (x - t_q)/(t_{q+p} - t_q) B_{q,p-1}(x)
+ *              + (t_{q+p+1} - x)/(t_{q+p+1} - t_{q+1}) B_{q+1,p-1}(x). */
+int orc_bspline_basis(const double* x, int64_t m, double lo, double hi, int degree, int n_knots,
+                      double* out) {
+    if (degree < 0 || n_knots < 0 || !(lo < hi)) return ORC_EINVAL;
+    int nk = n_knots + 2 * degree + 2;
+    int d = orc_basis_dim(degree, n_knots);
+    double* t = (double*)malloc(sizeof(double) * nk);
+    double* N = (double*)malloc(sizeof(double) * nk);
+    if (!t || !N) { free(t); free(N); return ORC_ENOMEM; }
+    double h = (hi - lo) / (double)(n_knots + 1);
+    for (int q = 0; q < nk; q++) t[q] = lo + (double)(q - degree) * h;
+    for (int64_t i = 0; i < m; i++) {
+        double xi = x[i];
+        for (int q = 0; q < nk - 1; q++) N[q] = (t[q] <= xi && xi < t[q + 1]) ? 1.0 : 0.0;
+        for (int p = 1; p <= degree; p++) {
+            for (int q = 0; q < nk - 1 - p; q++) {
+                double a = (xi - t[q]) / (t[q + p] - t[q]) * N[q];
+                double b = (t[q + p + 1] - xi) / (t[q + p + 1] - t[q + 1]) * N[q + 1];
+                N[q] = a + b;
+            }
+        }
+        for (int j = 0; j < d; j++) out[i * d + j] = N[j];
+    }
+    free(t);
+    free(N);
+    return ORC_OK;
+}
+
+/* Supp. P:L312: D^{1/2}(i) = (0..0, 1, -2, 1, 0..0) in R^{(d-2) x d}; D = D^{1/2 T} D^{1/2}. */
+void orc_penalty(int d, double* D) {
+    int r = d - 2;
+    double* Dl = (double*)calloc((size_t)(r > 0 ? r : 1) * d, sizeof(double));
+    for (int i = 0; i < r; i++) {
+        Dl[i * d + i] = 1.0;
+        Dl[i * d + i + 1] = -2.0;
+        Dl[i * d + i + 2] = 1.0;
+    }
+    for (int a = 0; a < d; a++)
+        for (int b = 0; b < d; b++) {
+            double s = 0.0;
+            for (int i = 0; i < r; i++) s += Dl[i * d + a] * Dl[i * d + b];
+            D[a * d + b] = s;
+        }
+    free(Dl);
+}
+
+/* ------------------------------------------------- binned matrix products */
+
+/* Algorithm binMatMat, P:L887-892 (reading G3/G4: w_i is the observation
+ * weight; column idx(i) of the d x n* matrix U receives w_i Zb(idx(i))^T). */
+void orc_bin_mat_mat(const double* Zb, int n_star, int d, const int32_t* idx, const double* w,
+                     int64_t n, double* out) {
+    double* U = (double*)calloc((size_t)d * n_star, sizeof(double)); /* U = 0_{d x n*} */
+    for (int64_t i = 0; i < n; i++) {
+        int l = idx[i];
+        double wi = w ? w[i] : 1.0;
+        for (int j = 0; j < d; j++) U[j * n_star + l] += wi * Zb[l * d + j];
+    }
+    for (int a = 0; a < d; a++) /* return U Zb */
+        for (int b = 0; b < d; b++) {
+            double s = 0.0;
+            for (int l = 0; l < n_star; l++) s += U[a * n_star + l] * Zb[l * d + b];
+            out[a * d + b] = s;
+        }
+    free(U);
+}
+
+/* Algorithm binMatVec. */
+void orc_bin_mat_vec(const double* Zb, int n_star, int d, const int32_t* idx, const double* w,
+                     const double* r, int64_t n, double* out) {
+    double* u = (double*)calloc((size_t)n_star, sizeof(double)); /* u = 0_{n*} */
+    for (int64_t i = 0; i < n; i++) u[idx[i]] += (w ? w[i] : 1.0) * r[i];
+    for (int j = 0; j < d; j++) { /* return Zb^T u */
+        double s = 0.0;
+        for (int l = 0; l < n_star; l++) s += Zb[l * d + j] * u[l];
+        out[j] = s;
+    }
+    free(u);
+}
+
+/* Row i of the materialised design matrix: rows[idx[i]] or rows[i]. */
+static inline const double* zrow(const double* rows, const int32_t* idx, int d, int64_t i) {
+    return rows + (size_t)d * (size_t)(idx ? idx[i] : i);
+}
+
+static void dense_ztwz_rows(const double* rows, const int32_t* idx, int d, const double* w,
+                            int64_t n, double* out) {
+    for (int a = 0; a < d * d; a++) out[a] = 0.0;
+    for (int64_t i = 0; i < n; i++) {
+        const double* zi = zrow(rows, idx, d, i);
+        double wi = w ? w[i] : 1.0;
+        for (int a = 0; a < d; a++)
+            for (int b = 0; b < d; b++) out[a * d + b] += zi[a] * wi * zi[b];
+    }
+}
+
+static void dense_ztwr_rows(const double* rows, const int32_t* idx, int d, const double* w,
+                            const double* r, int64_t n, double* out) {
+    for (int a = 0; a < d; a++) out[a] = 0.0;
+    for (int64_t i = 0; i < n; i++) {
+        const double* zi = zrow(rows, idx, d, i);
+        double wr = (w ? w[i] : 1.0) * r[i];
+        for (int a = 0; a < d; a++) out[a] += zi[a] * wr;
+    }
+}
+
+void orc_dense_ztwz(const double* Zb, int d, const int32_t* idx, const double* w, int64_t n,
+                    double* out) {
+    dense_ztwz_rows(Zb, idx, d, w, n, out);
+}
+
+void orc_dense_ztwr(const double* Zb, int d, const int32_t* idx, const double* w,
+                    const double* r, int64_t n, double* out) {
+    dense_ztwr_rows(Zb, idx, d, w, r, n, out);
+}
+
+/* ------------------------------------------------------- linear algebra */
+
+/* Z^T Z = L L^T. */
+int orc_cholesky(const double* A, int d, double* L) {
+    for (int a = 0; a < d * d; a++) L[a] = 0.0;
+    for (int i = 0; i < d; i++)
+        for (int j = 0; j <= i; j++) {
+            double s = A[i * d + j];
+            for (int q = 0; q < j; q++) s -= L[i * d + q] * L[j * d + q];
+            if (i == j) {
+                if (!(s > 0.0)) return ORC_EINVAL;
+                L[i * d + i] = sqrt(s);
+            } else {
+                L[i * d + j] = s / L[j * d + j];
+            }
+        }
+    return ORC_OK;
+}
+
+/* P:L843 forward/backward solving with the factor. */
+static void chol_fb(const double* L, int d, const double* b, double* x) {
+    for (int i = 0; i < d; i++) { /* L y = b */
+        double s = b[i];
+        for (int q = 0; q < i; q++) s -= L[i * d + q] * x[q];
+        x[i] = s / L[i * d + i];
+    }
+    for (int i = d - 1; i >= 0; i--) { /* L^T x = y */
+        double s = x[i];
+        for (int q = i + 1; q < d; q++) s -= L[q * d + i] * x[q];
+        x[i] = s / L[i * d + i];
+    }
+}
+
+int orc_chol_solve(const double* A, int d, const double* b, double* x) {
+    double* L = (double*)malloc(sizeof(double) * d * d);
+    int st = orc_cholesky(A, d, L);
+    if (st == ORC_OK) chol_fb(L, d, b, x);
+    free(L);
+    return st;
+}
+
+/* ---------------------------------------------------- degrees of freedom */
+
+/* Supp. P:L307-318: H = Z (Z^T W Z + lambda D)^-1 Z^T W (W = I here),
+ * df1 = tr H, df2 = tr(2H - H H).  With A = G + lambda D, G = Z^T Z and the
+ * cyclic trace identity, tr H = tr(A^-1 G) and tr(H H) = tr(A^-1 G A^-1 G). */
+int orc_df(const double* G, const double* D, int d, double lambda, int kind, double* df_out) {
+    double* A = (double*)malloc(sizeof(double) * d * d);
+    double* L = (double*)malloc(sizeof(double) * d * d);
+    double* X = (double*)malloc(sizeof(double) * d * d); /* X = A^-1 G */
+    double* col = (double*)malloc(sizeof(double) * d);
+    double* sol = (double*)malloc(sizeof(double) * d);
+    for (int a = 0; a < d * d; a++) A[a] = G[a] + lambda * D[a];
+    int st = orc_cholesky(A, d, L);
+    if (st == ORC_OK) {
+        for (int c = 0; c < d; c++) {
+            for (int r = 0; r < d; r++) col[r] = G[r * d + c];
+            chol_fb(L, d, col, sol);
+            for (int r = 0; r < d; r++) X[r * d + c] = sol[r];
+        }
+        double tr = 0.0;
+        for (int j = 0; j < d; j++) tr += X[j * d + j];
+        if (kind == 2) {
+            double tr2 = 0.0;
+            for (int a = 0; a < d; a++)
+                for (int b = 0; b < d; b++) tr2 += X[a * d + b] * X[b * d + a];
+            *df_out = 2.0 * tr - tr2;
+        } else {
+            *df_out = tr;
+        }
+    }
+    free(A); free(L); free(X); free(col); free(sol);
+    return st;
+}
+
+/* Supp. P:L316-319: equal df for every learner; "no analytic solution ...
+ * must be solved numerically".  df(lambda) is decreasing in lambda: bracket
+ * by doubling/halving, then bisect to the resolution of double. */
+int orc_df_to_lambda(const double* G, const double* D, int d, double target, int kind,
+                     double* lambda_out) {
+    if (!(target > 0.0) || target > (double)d) return ORC_ECALIB;
+    double v;
+    double hi = 1.0;
+    for (;;) {
+        if (orc_df(G, D, d, hi, kind, &v) != ORC_OK) return ORC_ECALIB;
+        if (v <= target) break;
+        hi *= 2.0;
+        if (hi > 1e300) return ORC_ECALIB;
+    }
+    if (v == target) { *lambda_out = hi; return ORC_OK; }
+    double lo = hi / 2.0;
+    for (;;) {
+        if (lo < 1e-300) return ORC_ECALIB;
+        if (orc_df(G, D, d, lo, kind, &v) != ORC_OK) return ORC_ECALIB;
+        if (v > target) break;
+        hi = lo;
+        lo /= 2.0;
+    }
+    for (int it = 0; it < 400; it++) {
+        double mid = lo + (hi - lo) / 2.0;
+        if (!(mid > lo && mid < hi)) break;
+        if (orc_df(G, D, d, mid, kind, &v) != ORC_OK) return ORC_ECALIB;
+        if (v > target) lo = mid;
+        else hi = mid;
+    }
+    *lambda_out = lo + (hi - lo) / 2.0;
+    if (orc_df(G, D, d, *lambda_out, kind, &v) != ORC_OK) return ORC_ECALIB;
+    if (fabs(v - target) > 1e-9) return ORC_ECALIB;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ pool */
+
+void orc_pool_free(orc_pool* p) {
+    if (!p) return;
+    free(p->lo); free(p->hi); free(p->z); free(p->bnd); free(p->idx); free(p->Zb);
+    free(p->Zx); free(p->G); free(p->D); free(p->lambda); free(p->L);
+    free(p);
+}
+
+/* Pool construction ("each base learner that uses binning
+ * individually calculates the bin values z, the reduced design matrix Zb and
+ * the index vector idx"; P:L846 caching; supp. P:L316-319 df calibration). */
+int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int mode, orc_pool** out) {
+    if (K < 1) return ORC_EEMPTY;
+    if (n < 2 || !cfg || mode < 0 || mode > 2) return ORC_EINVAL;
+    int n_star = orc_n_star(n, cfg->n_star_rule, cfg->n_star_fixed);
+    if (n_star < 0) return n_star;
+    int d = orc_basis_dim(cfg->degree, cfg->n_knots);
+    orc_pool* p = (orc_pool*)calloc(1, sizeof(orc_pool));
+    p->K = K; p->n = n; p->n_star = n_star; p->d = d; p->mode = mode;
+    p->lo = (double*)malloc(sizeof(double) * K);
+    p->hi = (double*)malloc(sizeof(double) * K);
+    p->z = (double*)malloc(sizeof(double) * K * n_star);
+    p->bnd = (double*)malloc(sizeof(double) * K * (n_star - 1));
+    p->idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)K * n);
+    p->Zb = (double*)malloc(sizeof(double) * (size_t)K * n_star * d);
+    p->G = (double*)malloc(sizeof(double) * K * d * d);
+    p->D = (double*)malloc(sizeof(double) * d * d);
+    p->lambda = (double*)malloc(sizeof(double) * K);
+    p->L = (double*)malloc(sizeof(double) * K * d * d);
+    if (mode == ORC_MODE_UNBINNED) p->Zx = (double*)malloc(sizeof(double) * (size_t)K * n * d);
+    if (!p->lo || !p->hi || !p->z || !p->bnd || !p->idx || !p->Zb || !p->G || !p->D || !p->lambda ||
+        !p->L || (mode == ORC_MODE_UNBINNED && !p->Zx)) {
+        orc_pool_free(p);
+        return ORC_ENOMEM;
+    }
+    orc_penalty(d, p->D);
+    int st = ORC_OK;
+    for (int k = 0; k < K && st == ORC_OK; k++) {
+        const double* x = X + (size_t)k * n;
+        double* z = p->z + (size_t)k * n_star;
+        st = orc_build_bins(x, n, n_star, z, p->bnd + (size_t)k * (n_star - 1), p->idx + (size_t)k * n);
+        if (st != ORC_OK) break;
+        p->lo[k] = z[0];
+        p->hi[k] = z[n_star - 1];
+        double* Zb = p->Zb + (size_t)k * n_star * d;
+        st = orc_bspline_basis(z, n_star, p->lo[k], p->hi[k], cfg->degree, cfg->n_knots, Zb);
+        if (st != ORC_OK) break;
+        double* G = p->G + (size_t)k * d * d;
+        if (mode == ORC_MODE_BINNED) {
+            orc_bin_mat_mat(Zb, n_star, d, p->idx + (size_t)k * n, NULL, n, G);
+        } else if (mode == ORC_MODE_DENSE) {
+            dense_ztwz_rows(Zb, p->idx + (size_t)k * n, d, NULL, n, G);
+        } else {
+            double* Zx = p->Zx + (size_t)k * n * d;
+            st = orc_bspline_basis(x, n, p->lo[k], p->hi[k], cfg->degree, cfg->n_knots, Zx);
+            if (st != ORC_OK) break;
+            dense_ztwz_rows(Zx, NULL, d, NULL, n, G);
+        }
+        st = orc_df_to_lambda(G, p->D, d, cfg->df, cfg->df_kind, &p->lambda[k]);
+        if (st != ORC_OK) break;
+        double* A = (double*)malloc(sizeof(double) * d * d);
+        for (int a = 0; a < d * d; a++) A[a] = G[a] + p->lambda[k] * p->D[a];
+        st = orc_cholesky(A, d, p->L + (size_t)k * d * d);
+        free(A);
+        if (st != ORC_OK) st = ORC_ECALIB;
+    }
+    if (st != ORC_OK) { orc_pool_free(p); return st; }
+    *out = p;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------ find best */
+
+typedef struct {
+    double *s, *theta, *fz, *A;
+} scratch;
+
+static void scratch_init(scratch* w, int d, int n_star) {
+    w->s = (double*)malloc(sizeof(double) * d);
+    w->theta = (double*)malloc(sizeof(double) * d);
+    w->fz = (double*)malloc(sizeof(double) * (n_star > 0 ? n_star : 1));
+    w->A = (double*)malloc(sizeof(double) * d * d);
+}
+
+static void scratch_free(scratch* w) { free(w->s); free(w->theta); free(w->fz); free(w->A); }
+
+/* Fit learner k to r (supp. eq. pen-regr): theta = (G + lambda D)^-1 Z^T r,
+ * and its SSE = sum_i (r_i - Z(i) theta)^2 (unpenalised, reading G12). */
+static double fit_one(const orc_pool* p, int k, const double* r, scratch* w, double* theta) {
+    int d = p->d, n_star = p->n_star;
+    int64_t n = p->n;
+    const int32_t* idx = p->idx + (size_t)k * n;
+    const double* Zb = p->Zb + (size_t)k * n_star * d;
+    const double* G = p->G + (size_t)k * d * d;
+    double sse = 0.0;
+    if (p->mode == ORC_MODE_BINNED) {
+        orc_bin_mat_vec(Zb, n_star, d, idx, NULL, r, n, w->s); /* P:L915 binMatVec */
+        chol_fb(p->L + (size_t)k * d * d, d, w->s, theta);    /* P:L846 cached factor */
+        for (int l = 0; l < n_star; l++) {
+            double v = 0.0;
+            for (int j = 0; j < d; j++) v += Zb[l * d + j] * theta[j];
+            w->fz[l] = v;
+        }
+        for (int64_t i = 0; i < n; i++) {
+            double e = r[i] - w->fz[idx[i]];
+            sse += e * e;
+        }
+        return sse;
+    }
+    const double* rows = (p->mode == ORC_MODE_DENSE) ? Zb : p->Zx + (size_t)k * n * d;
+    const int32_t* ridx = (p->mode == ORC_MODE_DENSE) ? idx : NULL;
+    dense_ztwr_rows(rows, ridx, d, NULL, r, n, w->s);
+    for (int a = 0; a < d * d; a++) w->A[a] = G[a] + p->lambda[k] * p->D[a];
+    orc_chol_solve(w->A, d, w->s, theta);
+    for (int64_t i = 0; i < n; i++) {
+        const double* zi = zrow(rows, ridx, d, i);
+        double v = 0.0;
+        for (int j = 0; j < d; j++) v += zi[j] * theta[j];
+        double e = r[i] - v;
+        sse += e * e;
+    }
+    return sse;
+}
+
+static void find_best_ws(const orc_pool* p, const double* r, scratch* w, int32_t* k_out,
+                         double* theta_out, double* sse_out, double* sse_all, double* gap_out) {
+    int d = p->d;
+    int best = -1;
+    double best_sse = 0.0, second = INFINITY;
+    for (int k = 0; k < p->K; k++) {
+        double sse = fit_one(p, k, r, w, w->theta);
+        if (sse_all) sse_all[k] = sse;
+        if (best < 0 || sse < best_sse) { /* strict: lowest k wins ties */
+            if (best >= 0) second = best_sse;
+            best = k;
+            best_sse = sse;
+            for (int j = 0; j < d; j++) theta_out[j] = w->theta[j];
+        } else if (sse < second) {
+            second = sse;
+        }
+    }
+    *k_out = best;
+    *sse_out = best_sse;
+    if (gap_out) *gap_out = second - best_sse;
+}
+
+int orc_find_best(const orc_pool* p, const double* r, int32_t* k_out, double* theta_out,
+                  double* sse_out, double* sse_all_out, double* gap_out) {
+    if (!p || p->K < 1) return ORC_EEMPTY;
+    for (int64_t i = 0; i < p->n; i++)
+        if (!isfinite(r[i])) return ORC_ENONFINITE;
+    scratch w;
+    scratch_init(&w, p->d, p->n_star);
+    find_best_ws(p, r, &w, k_out, theta_out, sse_out, sse_all_out, gap_out);
+    scratch_free(&w);
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------- train */
+
+typedef struct {
+    const orc_pool* p;
+    const double* Y;
+    int B, M, tid, nth;
+    double nu;
+    double *offset, *theta_agg, *sse_trace, *risk_trace, *gap_trace, *f_out;
+    int32_t* k_trace;
+} train_job;
+
+/* Alg. 1 supp., one replication at a time. */
+static void train_one(const train_job* J, int b, scratch* w, double* f, double* r, double* theta) {
+    const orc_pool* p = J->p;
+    int64_t n = p->n;
+    int d = p->d, K = p->K, B = J->B;
+    const double* y = J->Y + (size_t)b * n;
+    /* line 2: f0 = argmin_c R_emp(c) = mean(y) for L2 (S:L319 reading) */
+    double sy = 0.0;
+    for (int64_t i = 0; i < n; i++) sy += y[i];
+    double f0 = sy / (double)n;
+    J->offset[b] = f0;
+    for (int64_t i = 0; i < n; i++) f[i] = f0;
+    double* agg = J->theta_agg + (size_t)b * K * d;
+    for (int a = 0; a < K * d; a++) agg[a] = 0.0;
+    for (int m = 0; m < J->M; m++) {
+        /* line 4: pseudo residuals r = -dL/df = y - f for L = 1/2 (y - f)^2 (G9) */
+        for (int64_t i = 0; i < n; i++) r[i] = y[i] - f[i];
+        /* lines 5-9: fit every learner, SSE, argmin */
+        int32_t ks;
+        double sse, gap;
+        find_best_ws(p, r, w, &ks, theta, &sse, NULL, &gap);
+        /* line 10: f += nu b_{k*}(x, theta) */
+        const double* Zb = p->Zb + (size_t)ks * p->n_star * d;
+        const int32_t* idx = p->idx + (size_t)ks * n;
+        const double* rows = (p->mode == ORC_MODE_UNBINNED) ? p->Zx + (size_t)ks * n * d : Zb;
+        for (int64_t i = 0; i < n; i++) {
+            const double* zi = (p->mode == ORC_MODE_UNBINNED) ? rows + (size_t)i * d : Zb + (size_t)idx[i] * d;
+            double v = 0.0;
+            for (int j = 0; j < d; j++) v += zi[j] * theta[j];
+            f[i] = f[i] + J->nu * v;
+        }
+        /* P:L838 aggregation (with nu, reading G10) */
+        for (int j = 0; j < d; j++) agg[ks * d + j] += J->nu * theta[j];
+        double rs = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            double e = y[i] - f[i];
+            rs += 0.5 * e * e;
+        }
+        J->k_trace[(size_t)m * B + b] = ks;
+        J->sse_trace[(size_t)m * B + b] = sse;
+        J->risk_trace[(size_t)m * B + b] = rs / (double)n;
+        if (J->gap_trace) J->gap_trace[(size_t)m * B + b] = gap;
+    }
+    if (J->f_out)
+        for (int64_t i = 0; i < n; i++) J->f_out[(size_t)b * n + i] = f[i];
+}
+
+static void* train_worker(void* arg) {
+    train_job* J = (train_job*)arg;
+    int64_t n = J->p->n;
+    scratch w;
+    scratch_init(&w, J->p->d, J->p->n_star);
+    double* f = (double*)malloc(sizeof(double) * n);
+    double* r = (double*)malloc(sizeof(double) * n);
+    double* theta = (double*)malloc(sizeof(double) * J->p->d);
+    for (int b = J->tid; b < J->B; b += J->nth) train_one(J, b, &w, f, r, theta);
+    free(f); free(r); free(theta);
+    scratch_free(&w);
+    return NULL;
+}
+
+int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n_threads,
+              double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
+              double* risk_trace, double* gap_trace, double* f_out) {
+    if (!p || p->K < 1) return ORC_EEMPTY;
+    if (B < 1 || M < 0 || !(nu >= 0.0)) return ORC_EINVAL;
+    for (int64_t a = 0; a < (int64_t)B * p->n; a++)
+        if (!isfinite(Y[a])) return ORC_ENONFINITE;
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > B) n_threads = B;
+    train_job* jobs = (train_job*)malloc(sizeof(train_job) * n_threads);
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) {
+        train_job J = {p, Y, B, M, t, n_threads, nu, offset, theta_agg, sse_trace,
+                       risk_trace, gap_trace, f_out, k_trace};
+        jobs[t] = J;
+    }
+    for (int t = 1; t < n_threads; t++) pthread_create(&th[t], NULL, train_worker, &jobs[t]);
+    train_worker(&jobs[0]);
+    for (int t = 1; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(jobs);
+    free(th);
+    return ORC_OK;
+}
+
+/* -------------------------------------------------------------- predict */
+
+int orc_predict(const orc_pool* p, const double* Xnew, int64_t m, const double* offset,
+                const double* theta_agg, int B, double* out) {
+    int d = p->d, K = p->K, n_star = p->n_star;
+    int32_t* lix = (int32_t*)malloc(sizeof(int32_t) * (size_t)K * (m > 0 ? m : 1));
+    for (int k = 0; k < K; k++) {
+        const double* bnd = p->bnd + (size_t)k * (n_star - 1);
+        for (int64_t i = 0; i < m; i++) {
+            double x = Xnew[(size_t)k * m + i];
+            if (!isfinite(x)) { free(lix); return ORC_ENONFINITE; }
+            int a = 0, b = n_star - 1;
+            while (a < b) {
+                int mid = a + (b - a) / 2;
+                if (x <= bnd[mid]) b = mid;
+                else a = mid + 1;
+            }
+            lix[(size_t)k * m + i] = a;
+        }
+    }
+    for (int bb = 0; bb < B; bb++)
+        for (int64_t i = 0; i < m; i++) {
+            double v = offset[bb];
+            for (int k = 0; k < K; k++) {
+                const double* zr = p->Zb + ((size_t)k * n_star + lix[(size_t)k * m + i]) * d;
+                const double* th = theta_agg + ((size_t)bb * K + k) * d;
+                for (int j = 0; j < d; j++) v += zr[j] * th[j];
+            }
+            out[(size_t)bb * m + i] = v;
+        }
+    free(lix);
+    return ORC_OK;
+}

@@ -1,0 +1,142 @@
+/*
+ * cwb_oracle.h -- plain, slow, obviously-correct fp64 CPU oracle for binned
+ * componentwise gradient boosting (CWB), arXiv 2110.03513.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2110_03513_b200/) never links, imports or calls it,
+ * and it shares no code, header, table or constant generator with the CUDA
+ * path.
+ *
+ * Citations: "P:L<n>" = line n of PAPER.md (the paper body starts at L751,
+ * its supplement is L246-751).  Every function below names the passage it
+ * follows.  Readings of garbled / silent passages are listed in DESIGN.md
+ * ("Readings") and repeated at the function.
+ *
+ * Conventions: row-major arrays, 0-based indices, int32 bin indices.
+ * Learner k uses feature column k (univariate base learners).
+ * Return codes mirror include/cwb.h statuses but are defined independently.
+ */
+#ifndef CWB_ORACLE_H
+#define CWB_ORACLE_H
+#include <stdint.h>
+
+#define ORC_OK 0
+#define ORC_EINVAL (-1)
+#define ORC_EDEGENERATE (-2)
+#define ORC_ECALIB (-3)
+#define ORC_ENONFINITE (-4)
+#define ORC_EEMPTY (-5)
+#define ORC_ENOMEM (-8)
+
+#define ORC_MODE_DENSE 0    /* materialised rows Z(i)=Zb(idx(i)), fresh Cholesky per fit   */
+#define ORC_MODE_BINNED 1   /* Algorithm binMatVec literally, cached Cholesky */
+#define ORC_MODE_UNBINNED 2 /* basis evaluated at x itself, no discretisation            */
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* n* rule: 0 = ceil(sqrt n) ("n* = sqrt(n)"), 1 = ceil(n^(1/4)),
+ * 2 = fixed.  Returns n* or a negative status. */
+int orc_n_star(int64_t n, int rule, int fixed);
+
+/* P:L859-861 design points + index vector.  z[n_star], bnd[n_star-1], idx[n]. */
+int orc_build_bins(const double* x, int64_t n, int n_star, double* z, double* bnd, int32_t* idx);
+
+/* Basis dimension of a degree-`degree` P-spline with n_knots inner knots. */
+int orc_basis_dim(int degree, int n_knots);
+
+/* Cox-de Boor B-spline basis (P-splines of Eilers & Marx) on the
+ * extended equidistant knots over [lo, hi].  out is m x d. */
+int orc_bspline_basis(const double* x, int64_t m, double lo, double hi, int degree, int n_knots,
+                      double* out);
+
+/* Second-order difference penalty D = Delta^T Delta (supp. P:L312). out d x d. */
+void orc_penalty(int d, double* D);
+
+/* Algorithm binMatMat: U(idx(i)) += w_i Zb(idx(i)); return U Zb.
+ * w == NULL means ones.  out d x d. */
+void orc_bin_mat_mat(const double* Zb, int n_star, int d, const int32_t* idx, const double* w,
+                     int64_t n, double* out);
+
+/* Algorithm binMatVec: u(idx(i)) += w_i r_i; return Zb^T u.  out d. */
+void orc_bin_mat_vec(const double* Zb, int n_star, int d, const int32_t* idx, const double* w,
+                     const double* r, int64_t n, double* out);
+
+/* Plain dense products over the materialised discretised design matrix
+ * Z(i) = Zb(idx(i)): the definitions binMatMat/binMatVec reach faster. */
+void orc_dense_ztwz(const double* Zb, int d, const int32_t* idx, const double* w, int64_t n,
+                    double* out);
+void orc_dense_ztwr(const double* Zb, int d, const int32_t* idx, const double* w,
+                    const double* r, int64_t n, double* out);
+
+/* Plain Cholesky A = L L^T (lower, row-major).  ORC_EINVAL if not SPD. */
+int orc_cholesky(const double* A, int d, double* L);
+/* Solve A x = b with a fresh Cholesky factorisation. */
+int orc_chol_solve(const double* A, int d, const double* b, double* x);
+
+/* Degrees of freedom (supp. P:L314-318) by their definition: df1 = tr(H),
+ * df2 = tr(2H - H^2), H = Z (G + lambda D)^-1 Z^T, evaluated with the cyclic
+ * trace identity tr(H) = tr((G+lambda D)^-1 G).  kind in {1,2}. */
+int orc_df(const double* G, const double* D, int d, double lambda, int kind, double* df_out);
+
+/* Solve df(lambda) = target by bracketing + bisection on the definition
+ * (supp. P:L316-319: "must be solved numerically"). */
+int orc_df_to_lambda(const double* G, const double* D, int d, double target, int kind,
+                     double* lambda_out);
+
+typedef struct {
+    int32_t n_star_rule, n_star_fixed, degree, n_knots;
+    double df;
+    int32_t df_kind;
+} orc_config;
+
+/* A pool of K univariate binned P-spline base learners built from X (K x n,
+ * feature-major).  Owned by the caller through orc_pool_new / orc_pool_free. */
+typedef struct {
+    int K, n_star, d, mode;
+    int64_t n;
+    double* lo;     /* K */
+    double* hi;     /* K */
+    double* z;      /* K x n_star */
+    double* bnd;    /* K x (n_star-1) */
+    int32_t* idx;   /* K x n */
+    double* Zb;     /* K x n_star x d   (binned / dense modes) */
+    double* Zx;     /* K x n x d        (unbinned mode only)   */
+    double* G;      /* K x d x d   Z^T Z */
+    double* D;      /* d x d */
+    double* lambda; /* K */
+    double* L;      /* K x d x d   Cholesky of G + lambda D (binned mode cache) */
+} orc_pool;
+
+int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int mode, orc_pool** out);
+void orc_pool_free(orc_pool* p);
+
+/* findBestBaselearner (Alg. 1 supp. lines 5-9) on one
+ * residual vector r (n).  Fits every learner, SSE_k = sum_i (r_i - Z_k(i) theta_k)^2
+ * (unpenalised), argmin with the lowest k on ties.  gap_out (optional)
+ * = SSE of the second best minus SSE of the best. */
+int orc_find_best(const orc_pool* p, const double* r, int32_t* k_out, double* theta_out,
+                  double* sse_out, double* sse_all_out, double* gap_out);
+
+/* Vanilla CWB, Alg. 1 supp., L2 loss with the 1/2 convention
+ * (r = y - f), for B independent target vectors Y (B x n) sharing X.
+ * Outputs: offset[B], theta_agg[B][K][d] (theta_k = sum_m 1{k=k[m]} nu theta[m],
+ * P:L838 with nu), k_trace/sse_trace/risk_trace/gap_trace[M][B] (risk after
+ * the update of iteration m, R_emp = mean 1/2 (y-f)^2), f_out[B][n]
+ * (optional final fit).  n_threads >= 1 threads over replications. */
+int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n_threads,
+              double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
+              double* risk_trace, double* gap_trace, double* f_out);
+
+/* Prediction with the aggregated parameters (P:L822-826 additivity):
+ * f(x) = offset + sum_k g_k(z(x))^T theta_k, x hashed into the training bins
+ * (clamped to the end bins outside [lo, hi]).  Xnew K x m; out B x m. */
+int orc_predict(const orc_pool* p, const double* Xnew, int64_t m, const double* offset,
+                const double* theta_agg, int B, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,483 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+Each test names the passage (PAPER.md "P:L<n>", SPEC.md "S:L<n>") or the
+closed form it checks.  None of them re-types the oracle's formula: they use
+worked examples (tests/golden/spec_examples.json), exact rational arithmetic,
+closed forms, invariants, independent library routines (scipy BSpline, numpy
+dense linear algebra) or brute force.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ----------------------------------------------------------------- n* rule
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 21, 1331, 20000, 200000, 1000000, 99, 100, 101])
+def test_n_star_sqrt_is_integer_ceiling(n):
+    # P:L859 n* = sqrt(n), rounded up (reading G1): smallest s with s^2 >= n
+    s = math.isqrt(n - 1) + 1 if n > 1 else 1
+    assert O.n_star(n, 0) == max(s, 2)
+
+
+@pytest.mark.parametrize("n,expect", [(16, 2), (17, 3), (81, 3), (82, 4), (1000000, 32)])
+def test_n_star_fourth_root(n, expect):
+    # P:L445 n* = n^(1/4) variant
+    assert O.n_star(n, 1) == expect
+
+
+def test_ladder_bin_counts():
+    # SURVEY/BASELINE table: R1 37, R2 142, R3 448, R4 1000
+    assert [O.n_star(n) for n in (1331, 20000, 200000, 1000000)] == [37, 142, 448, 1000]
+
+
+# -------------------------------------------------------------------- bins
+
+def test_build_bins_spec_example():
+    g = GOLD["build_bins"]
+    z, bnd, idx = O.build_bins(np.array(g["x"], float), g["n_star"])
+    assert z.tolist() == g["z"]
+    assert idx.tolist() == g["idx"]
+    assert bnd.tolist() == [1.0, 3.0]
+
+
+def test_build_bins_identity_discretisation():
+    # x already equal to equally spaced design points -> identity index
+    x = np.arange(50, dtype=float) * 3.0 - 7.0
+    rng = np.random.default_rng(1)
+    perm = rng.permutation(50)
+    z, bnd, idx = O.build_bins(x[perm], 50)
+    assert (idx == perm).all()
+    assert np.abs(z - x).max() <= 1e-12
+
+
+def _exact_nearest(xs, ns):
+    lo, hi = Fraction(min(xs)), Fraction(max(xs))
+    zs = [lo + Fraction(l, ns - 1) * (hi - lo) for l in range(ns)]
+    out = []
+    for x in xs:
+        xf = Fraction(x)
+        dist = [abs(xf - zz) for zz in zs]
+        m = min(dist)
+        out.append(dist.index(m))  # tie -> lower bin (P:L861 closed-right intervals)
+    return zs, out
+
+
+@pytest.mark.parametrize("seed,ns", [(0, 7), (1, 2), (2, 13), (3, 37)])
+def test_build_bins_brute_force_nearest(seed, ns):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-5, 11, size=200)
+    zs, want = _exact_nearest(x.tolist(), ns)
+    z, bnd, idx = O.build_bins(x, ns)
+    assert idx.tolist() == want
+    for a, b in zip(z, zs):  # design points within 1 ulp-ish of the exact grid
+        assert abs(Fraction(a) - b) <= Fraction(abs(float(b)) + 1) * Fraction(1, 2**50)
+    assert z[-1] == x.max() and z[0] == x.min()
+
+
+def test_build_bins_ties_go_to_lower_bin():
+    # boundary between 0 and 2 is 1, between 2 and 4 is 3 -> lower bin
+    z, bnd, idx = O.build_bins(np.array([4.0, 0.0, 1.0, 3.0, 1.0000000000000002]), 3)
+    assert idx.tolist() == [2, 0, 0, 1, 1]
+
+
+@pytest.mark.parametrize("x,ns,err", [([2.0, 2.0, 2.0], 3, "EDEGENERATE"),
+                                      ([0.0, 1.0, float("nan")], 3, "ENONFINITE"),
+                                      ([0.0, 1.0, 2.0], 1, "EINVAL")])
+def test_build_bins_errors(x, ns, err):
+    with pytest.raises(O.OracleError) as e:
+        O.build_bins(np.array(x), ns)
+    assert e.value.name == err
+
+
+# ------------------------------------------------------------------- basis
+
+def _knots(lo, hi, degree, n_knots):
+    h = (hi - lo) / (n_knots + 1)
+    return np.array([lo + (q - degree) * h for q in range(n_knots + 2 * degree + 2)])
+
+
+@pytest.mark.parametrize("degree,n_knots", [(3, 20), (3, 4), (2, 7), (1, 0), (3, 10)])
+def test_bspline_matches_scipy(degree, n_knots):
+    from scipy.interpolate import BSpline
+    lo, hi = -3.25, 17.5
+    rng = np.random.default_rng(degree * 100 + n_knots)
+    x = np.concatenate([[lo, hi], rng.uniform(lo, hi, 300)])
+    B = O.bspline_basis(x, lo, hi, degree, n_knots)
+    assert B.shape == (len(x), n_knots + degree + 1)
+    t = _knots(lo, hi, degree, n_knots)
+    ref = BSpline.design_matrix(x, t, degree, extrapolate=False).toarray()
+    assert np.abs(B - ref).max() <= 1e-14
+    assert np.abs(B.sum(1) - 1.0).max() <= 1e-14     # partition of unity on [lo, hi]
+    assert (B >= -1e-16).all()
+    assert ((B > 0).sum(1) <= degree + 1).all()      # local support
+
+
+def test_uniform_cubic_values_at_knots():
+    g = GOLD["uniform_cubic_bspline_at_knot"]["values"]
+    B = O.bspline_basis(np.array([0.0, 5.0, 10.0]), 0.0, 10.0, 3, 1)  # knots spacing 5
+    # at x = lo the three non-zero cubic B-splines are 1/6, 2/3, 1/6
+    nz = B[0][B[0] > 1e-15]
+    assert np.allclose(nz, g, rtol=0, atol=1e-15)
+    nz_hi = B[2][B[2] > 1e-15]
+    assert np.allclose(nz_hi, g, rtol=0, atol=1e-15)
+
+
+def test_basis_dimension():
+    # reading G5: 20 inner knots, degree 3 -> d = 24
+    assert O.basis_dim(3, 20) == 24
+
+
+# ----------------------------------------------------------------- penalty
+
+def test_penalty_d4_spec():
+    assert O.penalty(4).tolist() == GOLD["penalty_d4"]["D"]
+
+
+@pytest.mark.parametrize("d", [5, 8, 24])
+def test_penalty_nullspace(d):
+    D = O.penalty(d)
+    assert np.allclose(D, D.T)
+    assert np.abs(D @ np.ones(d)).max() == 0.0
+    assert np.abs(D @ np.arange(d, dtype=float)).max() == 0.0
+    ev = np.linalg.eigvalsh(D)
+    assert (ev > -1e-12).all() and (np.abs(ev) < 1e-10).sum() == 2
+
+
+# ---------------------------------------------------- binMatMat / binMatVec
+
+def test_bin_mat_mat_spec_examples():
+    for g in GOLD["bin_mat_mat"]:
+        out = O.bin_mat_mat(np.array(g["Zb"], float), np.array(g["idx"]), np.array(g["w"], float))
+        assert out.tolist() == g["out"], g["cite"]
+
+
+def test_bin_mat_vec_spec_examples():
+    for g in GOLD["bin_mat_vec"]:
+        out = O.bin_mat_vec(np.array(g["Zb"], float), np.array(g["idx"]), np.array(g["r"], float))
+        assert out.tolist() == g["out"], g["cite"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_binned_products_equal_dense_expansion(seed):
+    # binned products equal dense products on the expanded Z
+    rng = np.random.default_rng(seed)
+    n, ns, d = int(rng.integers(5, 2000)), int(rng.integers(2, 60)), int(rng.integers(1, 25))
+    Zb = rng.standard_normal((ns, d))
+    idx = rng.integers(0, ns, n).astype(np.int32)
+    w = rng.uniform(0, 2, n) if seed % 2 else None
+    r = rng.standard_normal(n)
+    Z = Zb[idx]
+    W = np.ones(n) if w is None else w
+    ref_mm = Z.T @ (W[:, None] * Z)
+    ref_mv = Z.T @ (W * r)
+    mm = O.bin_mat_mat(Zb, idx, w)
+    mv = O.bin_mat_vec(Zb, idx, r, w)
+    scale_mm = np.abs(Z).T @ (W[:, None] * np.abs(Z))
+    scale_mv = np.abs(Z).T @ (W * np.abs(r))
+    assert (np.abs(mm - ref_mm) <= 1e-12 * scale_mm + 1e-300).all()
+    assert (np.abs(mv - ref_mv) <= 1e-12 * scale_mv + 1e-300).all()
+    assert np.allclose(O.dense_ztwz(Zb, idx, w), ref_mm, rtol=1e-12, atol=1e-12)
+    assert np.allclose(O.dense_ztwr(Zb, idx, r, w), ref_mv, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------- linear algebra
+
+def test_linear_ls_spec():
+    g = GOLD["linear_ls"]
+    Z = np.array(g["Z"], float)
+    r = np.array(g["r"], float)
+    th = O.chol_solve(Z.T @ Z, Z.T @ r)
+    assert np.allclose(th, g["theta"], rtol=0, atol=1e-13)
+
+
+def test_cholesky_residual_and_error():
+    rng = np.random.default_rng(5)
+    A0 = rng.standard_normal((24, 24))
+    A = A0 @ A0.T + 24 * np.eye(24)
+    L = O.cholesky(A)
+    assert np.allclose(np.tril(L), L)
+    assert np.abs(L @ L.T - A).max() <= 1e-12 * np.abs(A).max()
+    b = rng.standard_normal(24)
+    x = O.chol_solve(A, b)
+    assert np.abs(A @ x - b).max() <= 1e-10 * (1 + np.abs(b).max())
+    with pytest.raises(O.OracleError):
+        O.cholesky(-np.eye(3))
+
+
+# ---------------------------------------------------------------------- df
+
+def test_df_diag_spec():
+    g = GOLD["df_diag"]
+    G, D = np.array(g["G"], float), np.array(g["D"], float)
+    assert abs(O.df(G, D, 1.0, 1) - g["df1_num"] / g["df1_den"]) <= 1e-15
+    assert abs(O.df(G, D, 1.0, 2) - g["df2"]) <= 1e-15
+    assert abs(O.df(G, D, 0.0, 1) - 2.0) <= 1e-15           # lambda = 0 -> d
+    assert O.df(G, D, 1e15, 1) < 1e-14                        # nullity(I) = 0
+
+
+def test_df_to_lambda_diag_spec():
+    g = GOLD["df_to_lambda_diag"]
+    lam = O.df_to_lambda(np.array(g["G"], float), np.array(g["D"], float),
+                         g["target_num"] / g["target_den"], 1)
+    assert abs(lam - g["lambda"]) <= 1e-12
+
+
+def _hat(Z, D, lam):
+    return Z @ np.linalg.solve(Z.T @ Z + lam * D, Z.T)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_df_equals_dense_hat_trace(seed):
+    # supp. P:L314-318 by explicit n x n hat matrix (numpy), rank-deficient cases included
+    rng = np.random.default_rng(seed)
+    n, ns = 40, [30, 5, 12, 40][seed]
+    x = rng.uniform(0, 1, n)
+    z, _, idx = O.build_bins(x, ns)
+    Zb = O.bspline_basis(z, z[0], z[-1], 3, 6)
+    Z = Zb[idx]
+    D = O.penalty(Z.shape[1])
+    G = Z.T @ Z
+    for lam in [1e-3, 0.7, 13.0, 1e4]:
+        H = _hat(Z, D, lam)
+        assert abs(O.df(G, D, lam, 1) - np.trace(H)) <= 1e-9
+        assert abs(O.df(G, D, lam, 2) - np.trace(2 * H - H @ H)) <= 1e-9
+        assert O.df(G, D, lam, 2) >= O.df(G, D, lam, 1) - 1e-12
+
+
+def test_df_monotone_and_limits():
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 10, 500)
+    z, _, idx = O.build_bins(x, 23)
+    Zb = O.bspline_basis(z, z[0], z[-1], 3, 20)
+    G = O.bin_mat_mat(Zb, idx)
+    D = O.penalty(24)
+    lams = np.logspace(-6, 9, 40)
+    dfs = [O.df(G, D, l, 1) for l in lams]
+    assert all(a > b for a, b in zip(dfs, dfs[1:]))
+    assert abs(O.df(G, D, 1e-13, 1) - 23.0) < 1e-3            # lambda -> 0: rank(G) = n* = 23 < d
+    assert abs(dfs[-1] - 2.0) < 1e-4                          # nullity of D
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_df_to_lambda_calibrates(kind):
+    rng = np.random.default_rng(10 + kind)
+    x = rng.standard_normal(1331)
+    z, _, idx = O.build_bins(x, 37)
+    Zb = O.bspline_basis(z, z[0], z[-1], 3, 20)
+    G = O.bin_mat_mat(Zb, idx)
+    D = O.penalty(24)
+    lam = O.df_to_lambda(G, D, 5.0, kind)
+    Z = Zb[idx]
+    H = _hat(Z, D, lam)
+    val = np.trace(H) if kind == 1 else np.trace(2 * H - H @ H)
+    assert abs(val - 5.0) <= 1e-8
+
+
+def test_df_to_lambda_errors():
+    G, D = np.diag([2.0, 3.0, 5.0]), O.penalty(3)   # nullity of D = 2
+    with pytest.raises(O.OracleError) as e:
+        O.df_to_lambda(G, D, 1.5, 1)                 # below nullity
+    assert e.value.name == "ECALIB"
+    with pytest.raises(O.OracleError):
+        O.df_to_lambda(G, D, 3.5, 1)                 # above d
+
+
+# ------------------------------------------------------------ find best
+
+def _pool(X, **kw):
+    return O.Pool(np.asarray(X, float), O.Config(**kw), O.MODE_BINNED)
+
+
+def test_find_best_singleton():
+    rng = np.random.default_rng(0)
+    p = _pool(rng.uniform(0, 1, (1, 100)), n_knots=5)
+    k, th, sse, sse_all, gap = p.find_best(rng.standard_normal(100))
+    assert k == 0 and math.isinf(gap)
+
+
+def test_find_best_tie_lowest_index():
+    rng = np.random.default_rng(1)
+    x = rng.uniform(0, 1, 100)
+    p = _pool(np.stack([x, x, x]), n_knots=5)
+    k, th, sse, sse_all, gap = p.find_best(rng.standard_normal(100))
+    assert k == 0 and gap == 0.0 and sse_all[0] == sse_all[1] == sse_all[2]
+
+
+def test_find_best_orthogonal_residual():
+    # r orthogonal to learner A's column space but not B's -> B
+    rng = np.random.default_rng(2)
+    n = 300
+    X = np.stack([rng.uniform(0, 1, n), rng.uniform(0, 1, n)])
+    p = _pool(X, n_knots=5)
+    ZA = p.Zb[0][p.idx[0]]
+    ZB = p.Zb[1][p.idx[1]]
+    v = ZB @ rng.standard_normal(p.d)
+    r = v - ZA @ np.linalg.lstsq(ZA, v, rcond=None)[0]
+    k, th, sse, sse_all, gap = p.find_best(r)
+    assert k == 1
+    assert abs(sse_all[0] - r @ r) <= 1e-9 * (r @ r)
+    assert sse_all[1] < r @ r
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_find_best_exhaustive(seed):
+    # brute force: every learner fitted by numpy dense solve, SSE by full pass
+    rng = np.random.default_rng(100 + seed)
+    n, K = int(rng.integers(30, 400)), int(rng.integers(1, 7))
+    X = rng.uniform(-2, 3, (K, n))
+    p = _pool(X, n_knots=int(rng.integers(3, 12)))
+    r = rng.standard_normal(n)
+    sses, thetas = [], []
+    for k in range(K):
+        Z = p.Zb[k][p.idx[k]]
+        th = np.linalg.solve(Z.T @ Z + p.lam[k] * p.D, Z.T @ r)
+        e = r - Z @ th
+        sses.append(e @ e)
+        thetas.append(th)
+        # SSE identity rr - 2 theta^T s + theta^T G theta (exact algebra)
+        s = Z.T @ r
+        assert abs((r @ r - 2 * th @ s + th @ (Z.T @ Z) @ th) - e @ e) <= 1e-9 * (r @ r)
+    k, th, sse, sse_all, gap = p.find_best(r)
+    assert k == int(np.argmin(sses))
+    assert np.allclose(sse_all, sses, rtol=1e-11, atol=0)
+    assert np.allclose(th, thetas[k], rtol=1e-9, atol=1e-12)
+
+
+def test_pool_df_calibrated_against_dense_hat():
+    # every learner of the pool has df1 = 5 by the explicit hat matrix
+    rng = np.random.default_rng(7)
+    X = np.stack([rng.uniform(0, 50, 400), rng.standard_normal(400), rng.uniform(3, 4, 400)])
+    p = _pool(X)
+    for k in range(3):
+        Z = p.Zb[k][p.idx[k]]
+        assert abs(np.trace(_hat(Z, p.D, p.lam[k])) - 5.0) <= 1e-8
+
+
+# ------------------------------------------------------------------- train
+
+def test_train_linear_m1_spec():
+    g = GOLD["train_linear_m1"]
+    x = np.array([g["x"]], float)
+    p = O.Pool(x, O.Config(n_star_rule=2, n_star_fixed=3, degree=1, n_knots=0, df=2.0), O.MODE_BINNED)
+    res = p.train(np.array([g["y"]], float), nu=1.0, M=1)
+    assert abs(res.offset[0] - g["offset"]) <= 1e-15
+    assert np.allclose(res.f[0], g["f"], rtol=0, atol=1e-13)
+    assert abs(res.risk_trace[0, 0] - g["risk"]) <= 1e-25
+
+
+def test_train_nu_zero_is_offset_only():
+    rng = np.random.default_rng(4)
+    p = _pool(rng.uniform(0, 1, (3, 200)), n_knots=6)
+    y = rng.standard_normal((2, 200))
+    res = p.train(y, nu=0.0, M=7)
+    assert (res.theta_agg == 0).all()
+    assert np.allclose(res.f, y.mean(1, keepdims=True) * np.ones((1, 200)), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("nu,M", [(0.05, 60), (0.3, 25), (1.0, 3)])
+def test_train_single_learner_closed_form(nu, M):
+    # K = 1: r^[m] = (I - nu H)^m r^[0], H = Z (Z^T Z + lambda D)^-1 Z^T (Alg. 1 supp. with K = 1)
+    rng = np.random.default_rng(11)
+    n = 150
+    x = rng.uniform(0, 1, n)
+    y = np.sin(6 * x) + 0.3 * rng.standard_normal(n)
+    p = _pool(x[None], n_knots=8)
+    res = p.train(y[None], nu=nu, M=M)
+    Z = p.Zb[0][p.idx[0]]
+    H = _hat(Z, p.D, p.lam[0])
+    r0 = y - y.mean()
+    rM = np.linalg.matrix_power(np.eye(n) - nu * H, M) @ r0
+    assert np.abs((y - res.f[0]) - rM).max() <= 1e-11 * np.abs(r0).max()
+    # risk trace = (1/n) sum 1/2 r^2 after each update
+    rm = r0.copy()
+    A = Z.T @ Z + p.lam[0] * p.D
+    agg = np.zeros(p.d)
+    for m in range(M):
+        th = np.linalg.solve(A, Z.T @ rm)
+        e = rm - Z @ th
+        assert abs(res.sse_trace[m, 0] - e @ e) <= 1e-11 * (r0 @ r0)     # SSE of the fit at m
+        agg += nu * th
+        rm = rm - nu * H @ rm
+        assert abs(res.risk_trace[m, 0] - 0.5 * (rm @ rm) / n) <= 1e-11 * (0.5 * (r0 @ r0) / n)
+    assert np.abs(res.theta_agg[0, 0] - agg).max() <= 1e-10 * np.abs(agg).max()   # P:L838 with nu
+    assert (res.k_trace == 0).all()
+
+
+def test_train_invariants_r0():
+    import cwb_synth as S
+    ds = S.make("R0")
+    c = ds.cfg
+    cfg = O.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots)
+    p = O.Pool(ds.X, cfg, O.MODE_BINNED)
+    res = p.train(ds.Y, nu=c.nu, M=c.M, threads=3)
+    # train risk non-increasing
+    assert (np.diff(res.risk_trace, axis=0) <= 1e-12).all()
+    # aggregation: offset + sum_k Z_k theta_agg_k equals the accumulated fit
+    pred = p.predict(ds.X, res.offset, res.theta_agg)
+    assert np.abs(pred - res.f).max() <= 1e-10 * np.abs(ds.Y).max()
+    # SSE_m of the fitted learner never exceeds r^T r before the update: with
+    # A = G + lambda D >= G, theta^T G theta <= theta^T s, so SSE <= rr - theta^T s <= rr
+    n = ds.cfg.n
+    rr_before = np.vstack([0.5 * ((ds.Y - ds.Y.mean(1, keepdims=True)) ** 2).sum(1) / n,
+                           res.risk_trace[:-1]]) * 2 * n
+    assert (res.sse_trace <= rr_before * (1 + 1e-12)).all()
+    # determinism across thread counts
+    res1 = p.train(ds.Y, nu=c.nu, M=c.M, threads=1)
+    assert (res1.theta_agg == res.theta_agg).all() and (res1.k_trace == res.k_trace).all()
+
+
+def test_binned_equals_unbinned_on_grid_features():
+    # features that coincide with their design points -> identical fits.
+    # The grid is built with the design-point expression of P:L859 so x == z exactly.
+    n = 41
+    lo, hi = -1.0, 1.0
+    grid = np.array([lo + (l / (n - 1)) * (hi - lo) for l in range(n)])
+    grid[-1] = hi
+    rng = np.random.default_rng(9)
+    X = np.stack([grid, grid[rng.permutation(n)], grid[rng.permutation(n)]])
+    Y = np.stack([np.sin(3 * X[0]) + X[1] ** 2 + 0.1 * rng.standard_normal(n) for _ in range(3)])
+    cfg = O.Config(n_star_rule=2, n_star_fixed=n, n_knots=6)
+    pb = O.Pool(X, cfg, O.MODE_BINNED)
+    pu = O.Pool(X, cfg, O.MODE_UNBINNED)
+    assert (pb.idx == np.stack([np.argsort(np.argsort(x)) for x in X])).all()
+    rb = pb.train(Y, nu=0.1, M=40)
+    ru = pu.train(Y, nu=0.1, M=40)
+    assert (rb.k_trace == ru.k_trace).all()
+    assert np.allclose(rb.theta_agg, ru.theta_agg, rtol=1e-10, atol=1e-12)
+
+
+def test_binned_mode_equals_dense_mode():
+    # Algorithm binMatVec reaches the dense definition's result
+    import cwb_synth as S
+    ds = S.make("R1", reps=range(6))
+    X = ds.X
+    pb = O.Pool(X, O.Config(), O.MODE_BINNED)
+    pd = O.Pool(X, O.Config(), O.MODE_DENSE)
+    assert np.allclose(pb.lam, pd.lam, rtol=1e-12)
+    rb = pb.train(ds.Y, nu=0.05, M=60, threads=6)
+    rd = pd.train(ds.Y, nu=0.05, M=60, threads=6)
+    assert (rb.k_trace == rd.k_trace).all()
+    assert np.allclose(rb.theta_agg, rd.theta_agg, rtol=1e-10, atol=1e-12)
+    assert np.allclose(rb.sse_trace, rd.sse_trace, rtol=1e-11)
+
+
+def test_unbinned_pool_is_penalised_regression_on_x():
+    # NEXT-3 basis at x itself: find_best equals numpy penalised LS with g(x)
+    rng = np.random.default_rng(13)
+    X = rng.uniform(0, 1, (2, 120))
+    p = O.Pool(X, O.Config(n_knots=7), O.MODE_UNBINNED)
+    r = rng.standard_normal(120)
+    k, th, sse, sse_all, gap = p.find_best(r)
+    for kk in range(2):
+        Z = O.bspline_basis(X[kk], X[kk].min(), X[kk].max(), 3, 7)
+        t = np.linalg.solve(Z.T @ Z + p.lam[kk] * p.D, Z.T @ r)
+        assert abs(sse_all[kk] - ((r - Z @ t) ** 2).sum()) <= 1e-10 * (r @ r)
