@@ -1,0 +1,185 @@
+/*
+ * cwb.h -- C ABI of the B200-native binned componentwise-boosting engine
+ * (arXiv 2110.03513, "Accelerated Componentwise Gradient Boosting using
+ * Efficient Data Representation and Momentum-based Optimization").
+ *
+ * Citations "P:L<n>" are lines of the paper text PAPER.md (body L751-1217,
+ * supplement L246-751).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - Every array argument is a DEVICE pointer allocated by the caller (for
+ *   instance by torch), except where "host" is written.  The caller owns
+ *   inputs and outputs and must keep them alive until the work enqueued on
+ *   `stream` has completed.
+ * - All arithmetic is IEEE fp64.  Indices are 0-based.
+ * - Calls are asynchronous with respect to the host unless stated: they
+ *   validate arguments on the host, enqueue kernels on `stream` and return.
+ *   Errors found on the device (a constant feature, a non-finite value, an
+ *   unreachable df target) are recorded in the context and reported by the
+ *   next call that synchronises (cwb_status, cwb_get_lambda, cwb_get_pool).
+ * - Every function returns a cwb_code (0 = success); no C++ exception
+ *   crosses the ABI.  cwb_last_error() returns the last message.
+ * - A cwb_ctx is not thread-safe; use one context per host thread / stream.
+ * - Learner k is the univariate binned P-spline base learner of feature k
+ *   (K = number of features).
+ */
+#ifndef CWB_H
+#define CWB_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CWB_OK = 0,
+    CWB_EINVAL = -1,        /* bad dimension, null pointer, n* < 2, unsupported size        */
+    CWB_EDEGENERATE = -2,   /* a feature is constant: min(x) == max(x) (P:L859 undefined)    */
+    CWB_ECALIB = -3,        /* df target not reachable (supp. P:L314-319)                     */
+    CWB_ENONFINITE = -4,    /* NaN/Inf in x, y or r                                           */
+    CWB_EEMPTY = -5,        /* empty base-learner pool (K = 0)                                */
+    CWB_ECUDA = -6,         /* CUDA runtime error                                             */
+    CWB_ENCCL = -7,         /* communicator error (row-sharded mode)                          */
+    CWB_ENOMEM = -8,        /* device allocation failed                                       */
+    CWB_EUNSUPPORTED = -9   /* configuration outside what the kernels implement               */
+} cwb_code;
+
+typedef struct cwb_ctx cwb_ctx;
+
+/* Learner configuration ("20 knots and degree 3"; P:L1049 df = 5). */
+typedef struct {
+    int32_t n_star_rule;  /* 0: n* = ceil(sqrt n), 1: ceil(n^(1/4)), 2: fixed */
+    int32_t n_star_fixed; /* n* when n_star_rule == 2 (>= 2)                                      */
+    int32_t degree;       /* B-spline degree, 1..3 (default 3)                                    */
+    int32_t n_knots;      /* inner knots (default 20); d = n_knots + degree + 1 <= 32             */
+    double df;            /* target degrees of freedom per learner (default 5)                   */
+    int32_t df_kind;      /* 1: df1 = tr H, 2: df2 = tr(2H - H^2) (supp. P:L314-318)              */
+} cwb_config;
+
+/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5. */
+void cwb_default_config(cwb_config* cfg);
+
+/* Library ABI version (major*100 + minor). */
+int cwb_version(void);
+
+/* ------------------------------------------------------------------------
+ * Stand-alone primitives of Sec. 3.1 (no context).
+ * ---------------------------------------------------------------------- */
+
+/* Binning of one feature.
+ *   x[n]          feature values.
+ *   z_out[n_star] design points z_l = min + l/(n*-1) (max - min), z[n*-1] = max.
+ *   bnd_out[n*-1] bin boundaries z_l + (z_{l+1} - z_l)/2 (may be NULL).
+ *   idx_out[n]    index vector: smallest l with x <= bnd_l, else n*-1 (a value
+ *                 on a boundary goes to the lower bin), stored as uint8
+ *                 (idx_bytes = 1, n* <= 256) or uint16 (idx_bytes = 2).
+ * Bit-exact with the paper's definition evaluated in fp64 without FMA.
+ * Errors: CWB_EINVAL (n < 1, n* < 2, n* too large for idx_bytes),
+ * CWB_EDEGENERATE / CWB_ENONFINITE (reported by this call: it synchronises). */
+int cwb_bin(const double* x, int64_t n, int32_t n_star, double* z_out, double* bnd_out,
+            void* idx_out, int32_t idx_bytes, cudaStream_t stream);
+
+/* Algorithm binMatMat: out (d x d, row-major) = Zb^T diag(c) Zb with
+ * c_l = sum_{i: idx(i)=l} w_i (w == NULL: ones).
+ *   Zb[n_star][d] reduced design matrix, idx[n] (idx_bytes 1 or 2). */
+int cwb_bin_mat_mat(const double* Zb, int32_t n_star, int32_t d, const void* idx, int32_t idx_bytes,
+                    const double* w, int64_t n, double* out, cudaStream_t stream);
+
+/* Algorithm binMatVec, for B vectors at once:
+ *   R[B][n] (vector b contiguous), out[B][d]: out_b = Zb^T u_b,
+ *   u_b(l) = sum_{i: idx(i)=l} w_i R[b][i] (w == NULL: ones).
+ * The per-bin sums run in increasing row order (counting-sort inversion of
+ * the index vector, computed on the device by this call). */
+int cwb_bin_mat_vec(const double* Zb, int32_t n_star, int32_t d, const void* idx, int32_t idx_bytes,
+                    const double* w, const double* R, int64_t n, int32_t B, double* out,
+                    cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Base-learner pool (init steps I1-I8 of DESIGN.md).
+ * ---------------------------------------------------------------------- */
+
+/* Builds the pool of K binned P-spline learners from X[K][n] (feature-major):
+ * per learner min/max, design points, index vector, the bin
+ * inversion (rows sorted by bin), basis at the design points Zb,
+ * G = binMatMat, lambda with df(lambda) = cfg->df via the
+ * Demmler-Reinsch orthogonalisation (supp. P:L319) and the cached inverse of
+ * G + lambda D.  cfg == NULL uses the defaults.  The context owns
+ * all its device buffers (stream-ordered allocations on `stream`).
+ * Errors: CWB_EINVAL (n < 2, K < 1, d > 32, degree not in 1..3),
+ * CWB_EEMPTY (K == 0); device-side errors via cwb_status(). */
+int cwb_init(cwb_ctx** ctx, const double* X, int64_t n, int32_t K, const cwb_config* cfg,
+             cudaStream_t stream);
+
+/* Synchronises the context's last stream and returns the first recorded
+ * error (host or device side), or CWB_OK. */
+int cwb_status(cwb_ctx* ctx);
+
+/* Human-readable message of the last error (static storage when ctx == NULL). */
+const char* cwb_last_error(const cwb_ctx* ctx);
+
+/* Host outputs: n* and d of the pool, K, n. */
+int cwb_get_dims(const cwb_ctx* ctx, int32_t* n_star, int32_t* d, int32_t* K, int64_t* n);
+
+/* Host output lambda[K] (synchronises). */
+int cwb_get_lambda(cwb_ctx* ctx, double* lambda_out);
+
+/* Device copies of the pool for inspection (each pointer may be NULL):
+ * z[K][n*], idx[K][n] (uint16 regardless of the internal width),
+ * Zb[K][n*][d], G[K][d][d], Ainv[K][d][d].  Synchronises. */
+int cwb_get_pool(cwb_ctx* ctx, double* z, uint16_t* idx, double* Zb, double* G, double* Ainv);
+
+/* Implementation selector for cwb_train (tests use it to cover both):
+ * 0 = auto, 1 = fused persistent kernel (one CTA per replication, residual
+ * vector resident in shared memory; needs n*8 + K*n**8 bytes to fit), 2 =
+ * general per-iteration kernels. */
+int cwb_set_path(cwb_ctx* ctx, int32_t path);
+
+/* findBestBaselearner (Alg. 1 supp. lines 5-9) for B
+ * residual vectors R[B][n]:
+ *   k_out[B]        argmin_k SSE_k (lowest k on ties)
+ *   theta_out[B][d] fitted parameters of that learner, (G+lambda D)^-1 Zb^T u
+ *   sse_out[B]      SSE = sum_i (r_i - Z_k(i) theta)^2 (unpenalised),
+ *                   evaluated as r^T r - (2 theta^T s - theta^T G theta).
+ * Any output pointer may be NULL. */
+int cwb_find_best(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                  double* sse_out, cudaStream_t stream);
+
+/* Vanilla CWB, Alg. 1 supp., L2 loss with L = (y-f)^2/2, for B
+ * independent target vectors Y[B][n] sharing X, M iterations, learning rate nu.
+ *   offset_out[B]          f0 = mean(y)
+ *   theta_agg_out[B][K][d] theta_k = sum_m 1{k = k[m]} nu theta[m]
+ *   k_trace[M][B], sse_trace[M][B]  selected learner and its SSE at iteration m
+ *   risk_trace[M][B]       empirical risk after the update of iteration m
+ * Trace pointers may be NULL.  Returns after enqueueing (no host sync). */
+int cwb_train(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+              double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+              cudaStream_t stream);
+
+/* Same as cwb_train but every array is a HOST pointer (X[K][n], Y[B][n] in,
+ * the rest out); the host<->device copies are enqueued on `stream` and the
+ * call synchronises before returning.  Builds and frees its own context. */
+int cwb_fit_host(const double* X, int64_t n, int32_t K, const cwb_config* cfg, const double* Y,
+                 int32_t B, double nu, int32_t M, double* offset_out, double* theta_agg_out,
+                 int32_t* k_trace, double* sse_trace, double* risk_trace, cudaStream_t stream);
+
+/* Prediction with aggregated parameters:
+ * out[b][i] = offset[b] + sum_k Zb_k(bin_k(Xnew[k][i]))^T theta_agg[b][k],
+ * Xnew[K][m] hashed into the training bins (values outside [min, max] fall
+ * into the end bins). */
+int cwb_predict(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
+                const double* theta_agg, int32_t B, double* out, cudaStream_t stream);
+
+/* Number of kernels this context has launched so far (bench evidence). */
+int64_t cwb_launch_count(const cwb_ctx* ctx);
+
+/* Releases every device buffer of the context (stream-ordered on the last
+ * stream used).  ctx may be NULL. */
+void cwb_free(cwb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CWB_H */

@@ -1,0 +1,113 @@
+// cwb_internal.cuh -- context layout and device helpers shared by the CUDA
+// translation units of the engine (not part of the public ABI; see
+// include/cwb.h).  Written for sm_100a (B200): 148 SMs, 227 KB shared
+// memory per CTA, fp64 CUDA-core arithmetic (tcgen05 has no f64 kind).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/cwb.h"
+
+#define CWB_MAX_D 32      // basis dimension d <= 32: one warp lane per coefficient
+#define CWB_SPW 4         // non-zero B-spline values per design point (degree <= 3)
+#define CWB_FUSED_THREADS 256
+
+// Device-side error recording: first error wins.
+__device__ __forceinline__ void cwb_dev_fail(int* status, int code) {
+    if (status) atomicCAS(status, 0, code);
+}
+
+struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
+    int32_t B = 0, Bp = 0;
+    int64_t bytes = 0;
+    double* Rt = nullptr;      // n x Bp residuals, row-major (column = replication)
+    double* U = nullptr;       // K x n* x Bp bin sums (binMatVec intermediate u)
+    double* theta = nullptr;   // K x d x Bp fitted parameters of every learner
+    double* delta = nullptr;   // K x Bp  SSE reduction 2 theta^T s - theta^T G theta
+    double* rr = nullptr;      // Bp      r^T r
+    double* zhat = nullptr;    // n* x Bp nu * Zb_{k*} theta*
+    int32_t* kstar = nullptr;  // Bp
+    double* part = nullptr;    // row-block partial sums of squares
+    int32_t n_part = 0;
+};
+
+struct cwb_ctx {
+    // dimensions / configuration
+    int64_t n = 0;
+    int32_t K = 0, n_star = 0, d = 0, degree = 3, n_knots = 20, df_kind = 1;
+    double df = 5.0;
+    int32_t idx_bytes = 1;   // 1: uint8 index vector, 2: uint16
+    int32_t perm_bytes = 2;  // 2: uint16 row ids, 4: uint32
+    int32_t path = 0;        // 0 auto, 1 fused, 2 general
+    cudaStream_t stream = 0;
+    int status = CWB_OK;
+    std::string err;
+    int64_t launches = 0;
+
+    // device buffers (pool, built once by cwb_init)
+    int* d_status = nullptr;
+    double* lo = nullptr;     // K
+    double* hi = nullptr;     // K
+    double* z = nullptr;      // K x n*
+    double* bnd = nullptr;    // K x (n*-1)
+    void* idx = nullptr;      // K x n   (uint8 / uint16)
+    uint32_t* cnt = nullptr;  // K x n*
+    int32_t* off = nullptr;   // K x (n*+1)  rows of bin l: perm[off[l] .. off[l+1])
+    void* perm = nullptr;     // K x n   (uint16 / uint32) row ids sorted by bin
+    double* Zb = nullptr;     // K x n* x d  dense basis at the design points
+    int32_t* zj0 = nullptr;   // K x n*      first non-zero basis index of design point l
+    double* Zs = nullptr;     // K x n* x 4  its non-zero values
+    int32_t* lwin = nullptr;  // K x d x 2   design points l with zj0[l] <= j <= zj0[l]+3
+    double* G = nullptr;      // K x d x d   Zb^T diag(cnt) Zb
+    double* Ainv = nullptr;   // K x d x d   (G + lambda D)^-1
+    double* lambda = nullptr; // K
+    double* eig = nullptr;    // K x d  DRO eigenvalues mu in [0,1]
+
+    cwb_train_ws ws;
+};
+
+// ----------------------------------------------------------------- helpers
+
+#define CWB_CUDA_TRY(ctx, expr)                                              \
+    do {                                                                     \
+        cudaError_t e_ = (expr);                                             \
+        if (e_ != cudaSuccess) return cwb_set_error((ctx), CWB_ECUDA,        \
+            std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+int cwb_set_error(cwb_ctx* ctx, int code, const std::string& msg);
+int cwb_check_launch(cwb_ctx* ctx, const char* what);
+cudaError_t cwb_alloc(void** p, size_t bytes, cudaStream_t s);
+void cwb_release(void* p, cudaStream_t s);
+
+// Kernel entry points used across translation units (host launchers).
+int cwb_launch_init(cwb_ctx* ctx, const double* X, cudaStream_t s);
+int cwb_launch_csr(cwb_ctx* ctx, const void* idx, int32_t idx_bytes, int64_t n, int32_t K,
+                   int32_t n_star, uint32_t* cnt, int32_t* off, void* perm, int32_t perm_bytes,
+                   cudaStream_t s);
+int cwb_train_fused(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
+                    double* offset_out, double* theta_agg_out, int32_t* k_trace, double* sse_trace,
+                    double* risk_trace, cudaStream_t s, bool* launched);
+size_t cwb_fused_smem_bytes(const cwb_ctx* ctx, bool perm_in_smem);
+int cwb_train_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
+                      double* offset_out, double* theta_agg_out, int32_t* k_trace,
+                      double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_find_best_general(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out,
+                          double* theta_out, double* sse_out, cudaStream_t s);
+int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
+                     const double* theta_agg, int32_t B, double* out, cudaStream_t s);
+
+// Warp reductions with a fixed butterfly order (deterministic).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t ld_u(const T* p, int64_t i) {
+    return (uint32_t)p[i];
+}

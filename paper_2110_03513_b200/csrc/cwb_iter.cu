@@ -1,0 +1,438 @@
+// cwb_iter.cu -- general per-iteration kernels: any n,
+// any B, residuals kept row-major (n x Bp, one column per replication) so
+// that every gather of a residual row is one coalesced 256-byte segment for
+// 32 replications.  Used by cwb_find_best, by cwb_train when the fused
+// kernel's shared-memory working set does not fit, and by the stand-alone
+// binMatVec primitive.
+//
+//   k_center   f0 = mean(y), r = y - f0, r^T r      (I8)
+//   k_tr_in    Y[B][n] -> Rt[n][Bp]  (tiled transpose)
+//   k_h1       u_k(l)[b] = sum_{i in bin l} Rt[i][b]          binMatVec loop
+//   k_h234     s = Zb^T u, theta = A^-1 s, delta = 2 theta^T s - theta^T G theta
+//   k_h5       k* = argmax delta (lowest k), log, theta_agg += nu theta*   P:L292
+//   k_zhat     nu Zb_{k*} theta* at the design points
+//   k_h6       r -= zhat[idx_{k*}(i)], partial r^T r
+//   k_rr       r^T r per replication, risk log
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cwb_internal.cuh"
+
+namespace {
+
+constexpr int kRowsH6 = 256;  // rows per block in k_h6
+
+__global__ void k_center(const double* __restrict__ Y, int64_t n, int B, bool center, double* off_ws,
+                         double* offset_out, double* rr, int* status) {
+    const int b = blockIdx.x;
+    const double* y = Y + (size_t)b * n;
+    __shared__ double red[32];
+    __shared__ double s_f0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double f0 = 0.0;
+    if (center) {
+        double s = 0.0;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += y[i];
+        s = warp_sum(s);
+        if (lane == 0) red[w] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < nw; q++) t += red[q];
+            s_f0 = t / (double)n;
+        }
+        __syncthreads();
+        f0 = s_f0;
+        __syncthreads();
+    }
+    double s = 0.0;
+    bool bad = false;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double v = y[i] - f0;
+        bad |= !isfinite(y[i]);
+        s += v * v;
+    }
+    if (bad) cwb_dev_fail(status, CWB_ENONFINITE);
+    s = warp_sum(s);
+    if (lane == 0) red[w] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < nw; q++) t += red[q];
+        rr[b] = t;
+        off_ws[b] = f0;
+        if (offset_out) offset_out[b] = f0;
+    }
+}
+
+// Rt[i][b] = w_i (Y[b][i] - off[b]) for b < B, 0 for the padding columns
+__global__ void k_tr_in(const double* __restrict__ Y, int64_t n, int B, int Bp,
+                        const double* __restrict__ off, const double* __restrict__ w,
+                        double* __restrict__ Rt) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int b0 = blockIdx.y * 32;
+    for (int q = threadIdx.y; q < 32; q += blockDim.y) {  // read rows of Y (contiguous in i)
+        const int b = b0 + q;
+        const int64_t i = i0 + threadIdx.x;
+        double v = 0.0;
+        if (b < B && i < n) {
+            v = Y[(size_t)b * n + i] - (off ? off[b] : 0.0);
+            if (w) v = w[i] * v;
+        }
+        tile[q][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int q = threadIdx.y; q < 32; q += blockDim.y) {  // write rows of Rt (contiguous in b)
+        const int64_t i = i0 + q;
+        if (i < n) Rt[(size_t)i * Bp + b0 + threadIdx.x] = tile[threadIdx.x][q];
+    }
+}
+
+// H1: one warp per (learner, bin), lane = replication column; rows of the bin
+// in increasing order (the order of the paper's loop over i).
+template <typename PermT>
+__global__ void k_h1(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
+                     const int32_t* __restrict__ off, const PermT* __restrict__ perm,
+                     double* __restrict__ U) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+    if (g >= (int64_t)K * ns) return;
+    const int k = (int)(g / ns), l = (int)(g - (int64_t)k * ns);
+    const int b = blockIdx.y * 32 + lane;
+    const int32_t a0 = off[(size_t)k * (ns + 1) + l], a1 = off[(size_t)k * (ns + 1) + l + 1];
+    const PermT* pk = perm + (size_t)k * n;
+    const double* col = Rt + b;
+    double acc = 0.0;
+    int32_t q = a0;
+    for (; q + 4 <= a1; q += 4) {
+        const uint32_t i0 = pk[q], i1 = pk[q + 1], i2 = pk[q + 2], i3 = pk[q + 3];
+        const double v0 = col[(size_t)i0 * Bp], v1 = col[(size_t)i1 * Bp];
+        const double v2 = col[(size_t)i2 * Bp], v3 = col[(size_t)i3 * Bp];
+        acc += v0; acc += v1; acc += v2; acc += v3;
+    }
+    for (; q < a1; q++) acc += col[(size_t)pk[q] * Bp];
+    U[(size_t)g * Bp + b] = acc;
+}
+
+// H2-H4 for one learner (blockIdx.x) and 32 replications (blockIdx.y)
+__global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
+                       const int32_t* __restrict__ zj0, const double* __restrict__ Zs,
+                       const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
+                       const double* __restrict__ G, double* __restrict__ theta,
+                       double* __restrict__ delta) {
+    __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
+    const int k = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const int32_t* j0 = zj0 + (size_t)k * ns;
+    const double* zs = Zs + (size_t)k * ns * CWB_SPW;
+    const double* u = U + (size_t)k * ns * Bp + b;
+    for (int j = w; j < d; j += nw) {
+        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+        double s = 0.0;
+        for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * Bp];
+        S[j][lane] = s;
+    }
+    __syncthreads();
+    const double* Ai = Ainv + (size_t)k * d * d;
+    for (int j = w; j < d; j += nw) {
+        double t = 0.0;
+        for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][lane];
+        Th[j][lane] = t;
+        theta[((size_t)k * d + j) * Bp + b] = t;
+    }
+    __syncthreads();
+    const double* Gk = G + (size_t)k * d * d;
+    for (int j = w; j < d; j += nw) {
+        double gt = 0.0;
+        for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++)
+            gt += Gk[j * d + jp] * Th[jp][lane];
+        V[j][lane] = Th[j][lane] * (2.0 * S[j][lane] - gt);
+    }
+    __syncthreads();
+    if (w == 0) {
+        double v = 0.0;
+        for (int j = 0; j < d; j++) v += V[j][lane];
+        delta[(size_t)k * Bp + b] = v;
+    }
+}
+
+// H5: argmax over learners per replication; theta_agg update; logs
+__global__ void k_h5(const double* __restrict__ delta, const double* __restrict__ theta,
+                     const double* __restrict__ rr, int K, int d, int B, int Bp, double nu, int m,
+                     int32_t* __restrict__ kstar, double* __restrict__ agg, int32_t* k_trace,
+                     double* sse_trace, int32_t* k_out, double* theta_out, double* sse_out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= Bp) return;
+    if (b >= B) { kstar[b] = 0; return; }
+    int ks = 0;
+    double best = delta[b];
+    for (int k = 1; k < K; k++) {
+        double v = delta[(size_t)k * Bp + b];
+        if (v > best) { best = v; ks = k; }
+    }
+    kstar[b] = ks;
+    const double sse = rr[b] - best;
+    if (agg)
+        for (int j = 0; j < d; j++)
+            agg[((size_t)b * K + ks) * d + j] += nu * theta[((size_t)ks * d + j) * Bp + b];
+    if (k_trace) k_trace[(size_t)m * B + b] = ks;
+    if (sse_trace) sse_trace[(size_t)m * B + b] = sse;
+    if (k_out) k_out[b] = ks;
+    if (sse_out) sse_out[b] = sse;
+    if (theta_out)
+        for (int j = 0; j < d; j++) theta_out[(size_t)b * d + j] = theta[((size_t)ks * d + j) * Bp + b];
+}
+
+// nu * Zb_{k*} theta* at the design points, per (design point, replication)
+__global__ void k_zhat(const int32_t* __restrict__ kstar, const double* __restrict__ theta,
+                       const int32_t* __restrict__ zj0, const double* __restrict__ Zs, int ns, int d,
+                       int B, int Bp, double nu, double* __restrict__ zhat) {
+    const int b = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (l >= ns) return;
+    double v = 0.0;
+    if (b < B) {
+        const int ks = kstar[b];
+        const int a = zj0[(size_t)ks * ns + l];
+        const double* zs = Zs + ((size_t)ks * ns + l) * CWB_SPW;
+        const double* th = theta + (size_t)ks * d * Bp + b;
+        v = zs[0] * th[(size_t)a * Bp];
+        for (int q = 1; q < CWB_SPW; q++)
+            if (a + q < d) v += zs[q] * th[(size_t)(a + q) * Bp];
+        v *= nu;
+    }
+    zhat[(size_t)l * Bp + b] = v;
+}
+
+template <typename IdxT>
+__global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* __restrict__ kstar,
+                     const IdxT* __restrict__ idx, const double* __restrict__ zhat,
+                     double* __restrict__ part) {
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const int ks = kstar[b];
+    const IdxT* ik = idx + (size_t)ks * n;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6;
+    const int64_t r1 = min(n, r0 + kRowsH6);
+    double acc = 0.0;
+    for (int64_t i = r0 + w; i < r1; i += 8) {
+        double v = Rt[(size_t)i * Bp + b] - zhat[(size_t)ik[i] * Bp + b];
+        Rt[(size_t)i * Bp + b] = v;
+        acc += v * v;
+    }
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) {
+        double s = 0.0;
+        for (int q = 0; q < 8; q++) s += red[q][lane];
+        part[(size_t)blockIdx.x * Bp + b] = s;
+    }
+}
+
+__global__ void k_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n, int m,
+                     double* __restrict__ rr, double* risk_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double s = 0.0;
+    for (int q = 0; q < nblk; q++) s += part[(size_t)q * Bp + b];
+    rr[b] = s;
+    if (risk_trace) risk_trace[(size_t)m * B + b] = s / (2.0 * (double)n);
+}
+
+__global__ void k_zero(double* p, size_t cnt) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = 0.0;
+}
+
+// dense projection out[b][j] = sum_l Zb[l][j] U[l][b] (stand-alone binMatVec, any Zb)
+__global__ void k_dense_proj(const double* __restrict__ Zb, const double* __restrict__ U, int ns, int d,
+                             int B, int Bp, double* __restrict__ out) {
+    const int b = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (j >= d || b >= B) return;
+    double s = 0.0;
+    for (int l = 0; l < ns; l++) s += Zb[(size_t)l * d + j] * U[(size_t)l * Bp + b];
+    out[(size_t)b * d + j] = s;
+}
+
+}  // namespace
+
+// ===================================================================== host
+
+static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s) {
+    cwb_train_ws& w = c->ws;
+    const int Bp = (B + 31) / 32 * 32;
+    const int nblk = (int)((c->n + kRowsH6 - 1) / kRowsH6);
+    if (w.Bp >= Bp && w.B >= B && w.Rt) return CWB_OK;
+    cwb_release(w.Rt, s); cwb_release(w.U, s); cwb_release(w.theta, s); cwb_release(w.delta, s);
+    cwb_release(w.rr, s); cwb_release(w.zhat, s); cwb_release(w.kstar, s); cwb_release(w.part, s);
+    w = cwb_train_ws();
+    const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
+    bool ok = true;
+    ok &= cwb_alloc((void**)&w.Rt, sizeof(double) * n * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.U, sizeof(double) * K * ns * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.theta, sizeof(double) * K * d * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.delta, sizeof(double) * K * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.rr, sizeof(double) * 2 * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.zhat, sizeof(double) * ns * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.kstar, sizeof(int32_t) * Bp, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&w.part, sizeof(double) * (size_t)nblk * Bp, s) == cudaSuccess;
+    if (!ok) return cwb_set_error(c, CWB_ENOMEM, "general-path workspace allocation failed");
+    w.B = B; w.Bp = Bp; w.n_part = nblk;
+    return CWB_OK;
+}
+
+template <typename PermT>
+static void launch_h1(const double* Rt, int64_t n, int Bp, int K, int ns, const int32_t* off,
+                      const void* perm, double* U, cudaStream_t s) {
+    const int wpb = 8;
+    dim3 grid((unsigned)(((int64_t)K * ns + wpb - 1) / wpb), Bp / 32);
+    k_h1<PermT><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, off, (const PermT*)perm, U);
+}
+
+static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_t* off,
+               const void* perm, int perm_bytes, double* U, cudaStream_t s) {
+    if (perm_bytes == 2) launch_h1<uint16_t>(Rt, c->n, Bp, K, ns, off, perm, U, s);
+    else launch_h1<uint32_t>(Rt, c->n, Bp, K, ns, off, perm, U, s);
+    c->launches++;
+}
+
+// one findBestBaselearner on the residual columns of ws.Rt
+static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg, int32_t* k_trace,
+                           double* sse_trace, int32_t* k_out, double* theta_out, double* sse_out,
+                           cudaStream_t s) {
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp;
+    h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
+    k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
+                                                c->Ainv, c->G, w.theta, w.delta);
+    k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
+                                          agg, k_trace, sse_trace, k_out, theta_out, sse_out);
+    c->launches += 2;
+}
+
+int cwb_find_best_general(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                          double* sse_out, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    k_center<<<B, 256, 0, s>>>(R, c->n, B, false, w.rr + w.Bp, nullptr, w.rr, c->d_status);
+    dim3 gt((unsigned)((c->n + 31) / 32), w.Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(R, c->n, B, w.Bp, nullptr, nullptr, w.Rt);
+    c->launches += 2;
+    find_best_iter(c, B, 0.0, 0, nullptr, nullptr, nullptr, k_out, theta_out, sse_out, s);
+    return cwb_check_launch(c, "find_best kernels");
+}
+
+int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
+                      double* offset_out, double* theta_agg_out, int32_t* k_trace,
+                      double* sse_trace, double* risk_trace, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp;
+    double* off_ws = w.rr + Bp;
+    k_center<<<B, 256, 0, s>>>(Y, c->n, B, true, off_ws, offset_out, w.rr, c->d_status);
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
+    const size_t nagg = (size_t)B * c->K * c->d;
+    k_zero<<<(unsigned)min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_agg_out, nagg);
+    c->launches += 3;
+    const int nblk = w.n_part;
+    for (int m = 0; m < M; m++) {
+        find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
+        k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
+                                                                  c->n_star, c->d, B, Bp, nu, w.zhat);
+        dim3 g6(nblk, Bp / 32);
+        if (c->idx_bytes == 1)
+            k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
+        else
+            k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
+        k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+        c->launches += 3;
+    }
+    return cwb_check_launch(c, "general train kernels");
+}
+
+// ------------------------------------------------ stand-alone primitives
+namespace {
+__global__ void k_gram_dense(const double* __restrict__ Zb, const double* __restrict__ u, int ustride,
+                             int ns, int d, double* __restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * d; e += gridDim.x * blockDim.x) {
+        const int a = e / d, b = e % d;
+        double s = 0.0;
+        for (int l = 0; l < ns; l++) s += u[(size_t)l * ustride] * (Zb[(size_t)l * d + a] * Zb[(size_t)l * d + b]);
+        out[e] = s;
+    }
+}
+__global__ void k_fill(double* p, int64_t cnt, double v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+}  // namespace
+
+// U[l][b] = sum_{i: idx(i) = l} w_i R[b][i]  (binMatVec's u), rows in increasing order
+static int binned_sums(const void* idx, int32_t idx_bytes, const double* w, const double* R, int64_t n,
+                       int32_t B, int32_t ns, double* U, int Bp, cudaStream_t s) {
+    const int perm_bytes = n <= 65536 ? 2 : 4;
+    uint32_t* cnt = nullptr;
+    int32_t* off = nullptr;
+    void* perm = nullptr;
+    double* Rt = nullptr;
+    bool ok = cwb_alloc((void**)&cnt, sizeof(uint32_t) * ns, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&off, sizeof(int32_t) * (ns + 1), s) == cudaSuccess;
+    ok &= cwb_alloc(&perm, (size_t)perm_bytes * n, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&Rt, sizeof(double) * (size_t)n * Bp, s) == cudaSuccess;
+    int rc = ok ? CWB_OK : CWB_ENOMEM;
+    if (rc == CWB_OK) rc = cwb_launch_csr(nullptr, idx, idx_bytes, n, 1, ns, cnt, off, perm, perm_bytes, s);
+    if (rc == CWB_OK) {
+        dim3 gt((unsigned)((n + 31) / 32), Bp / 32);
+        k_tr_in<<<gt, dim3(32, 8), 0, s>>>(R, n, B, Bp, nullptr, w, Rt);
+        const int wpb = 8;
+        dim3 grid((unsigned)((ns + wpb - 1) / wpb), Bp / 32);
+        if (perm_bytes == 2) k_h1<uint16_t><<<grid, 256, 0, s>>>(Rt, n, Bp, 1, ns, off, (const uint16_t*)perm, U);
+        else k_h1<uint32_t><<<grid, 256, 0, s>>>(Rt, n, Bp, 1, ns, off, (const uint32_t*)perm, U);
+        if (cudaGetLastError() != cudaSuccess) rc = CWB_ECUDA;
+    }
+    cwb_release(cnt, s); cwb_release(off, s); cwb_release(perm, s); cwb_release(Rt, s);
+    return rc;
+}
+
+int cwb_bin_mat_vec_impl(const double* Zb, int32_t ns, int32_t d, const void* idx, int32_t idx_bytes,
+                         const double* w, const double* R, int64_t n, int32_t B, double* out,
+                         cudaStream_t s) {
+    const int Bp = (B + 31) / 32 * 32;
+    double* U = nullptr;
+    if (cwb_alloc((void**)&U, sizeof(double) * (size_t)ns * Bp, s) != cudaSuccess) return CWB_ENOMEM;
+    int rc = binned_sums(idx, idx_bytes, w, R, n, B, ns, U, Bp, s);
+    if (rc == CWB_OK) {
+        k_dense_proj<<<dim3((d + 7) / 8, Bp / 32), 256, 0, s>>>(Zb, U, ns, d, B, Bp, out);
+        if (cudaGetLastError() != cudaSuccess) rc = CWB_ECUDA;
+    }
+    cwb_release(U, s);
+    return rc;
+}
+
+// binMatMat: c_l = sum_{i in bin l} w_i, out = Zb^T diag(c) Zb
+int cwb_bin_mat_mat_impl(const double* Zb, int32_t ns, int32_t d, const void* idx, int32_t idx_bytes,
+                         const double* w, int64_t n, double* out, cudaStream_t s) {
+    double *ones = nullptr, *U = nullptr;
+    bool ok = cwb_alloc((void**)&U, sizeof(double) * (size_t)ns * 32, s) == cudaSuccess;
+    if (!w) {
+        ok &= cwb_alloc((void**)&ones, sizeof(double) * (size_t)n, s) == cudaSuccess;
+        if (ok) k_fill<<<(unsigned)min((int64_t)1184, (n + 255) / 256), 256, 0, s>>>(ones, n, 1.0);
+    }
+    int rc = ok ? CWB_OK : CWB_ENOMEM;
+    if (rc == CWB_OK) rc = binned_sums(idx, idx_bytes, nullptr, w ? w : ones, n, 1, ns, U, 32, s);
+    if (rc == CWB_OK) {
+        // U is ns x 32 with the sums in column 0 (stride 32)
+        k_gram_dense<<<(d * d + 255) / 256, 256, 0, s>>>(Zb, U, 32, ns, d, out);
+        if (cudaGetLastError() != cudaSuccess) rc = CWB_ECUDA;
+    }
+    cwb_release(ones, s);
+    cwb_release(U, s);
+    return rc;
+}

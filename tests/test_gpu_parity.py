@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, on the
+same seeded inputs (cwb_synth), element by element.  Agreement rules in
+tests/parity_util.py and DESIGN.md.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import cwb_synth as S  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from parity_util import (RTOL, assert_train_parity, cfg_of, close, gpu_cfg_of)  # noqa: E402
+
+from paper_2110_03513_b200 import cwb  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def dev(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+# ------------------------------------------------------------------ binning
+
+@pytest.mark.parametrize("seed,n,ns", [(0, 5, 3), (1, 1000, 37), (2, 20000, 142), (3, 65536, 256),
+                                       (4, 70001, 448), (5, 3000, 1000), (6, 257, 2)])
+def test_bin_bit_exact(seed, n, ns):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-71.16807745607325, 89.72988942744877, n) if seed else np.arange(5.0)
+    if seed == 6:
+        x = rng.standard_normal(n)
+    z, bnd, idx = O.build_bins(x, ns)
+    gz, gb, gi = cwb.cwb_bin(dev(x), ns)
+    assert (host(gz) == z).all()
+    assert (host(gb) == bnd).all()
+    assert (host(gi).astype(np.int64) == idx).all()
+
+
+def test_bin_ties_and_errors():
+    x = np.array([4.0, 0.0, 1.0, 3.0, 1.0000000000000002, 2.0, 3.0000000000000004])
+    z, bnd, idx = O.build_bins(x, 3)
+    gz, gb, gi = cwb.cwb_bin(dev(x), 3)
+    assert (host(gi).astype(np.int64) == idx).all()
+    with pytest.raises(cwb.CwbError) as e:
+        cwb.cwb_bin(dev(np.full(10, 2.5)), 3)
+    assert e.value.name == "CWB_EDEGENERATE"
+    with pytest.raises(cwb.CwbError) as e:
+        cwb.cwb_bin(dev(np.array([0.0, np.nan, 1.0])), 3)
+    assert e.value.name == "CWB_ENONFINITE"
+
+
+# ------------------------------------------------- binMatVec / binMatMat
+
+@pytest.mark.parametrize("seed,n,ns,d,B,weighted", [(0, 3, 2, 1, 1, False), (1, 2000, 37, 24, 5, True),
+                                                     (2, 20000, 142, 24, 33, False), (3, 70000, 448, 24, 64, True),
+                                                     (4, 1, 1, 3, 2, False), (5, 999, 300, 7, 1, True)])
+def test_bin_mat_vec_and_mat(seed, n, ns, d, B, weighted):
+    rng = np.random.default_rng(seed)
+    Zb = rng.standard_normal((ns, d))
+    idx = rng.integers(0, ns, n).astype(np.int32)
+    R = rng.standard_normal((B, n))
+    w = rng.uniform(0, 2, n) if weighted else None
+    ib = 1 if ns <= 256 else 2
+    gidx = dev(idx.astype(np.uint8 if ib == 1 else np.uint16), torch.uint8 if ib == 1 else torch.uint16)
+    got = host(cwb.cwb_bin_mat_vec(dev(Zb), gidx, dev(R), None if w is None else dev(w)))
+    for b in range(B):
+        ref = O.bin_mat_vec(Zb, idx, R[b], w)
+        ok, e = close(got[b], ref, 1e-12, scale=np.abs(Zb).max() * np.abs(R[b]).sum() * (2 if weighted else 1))
+        assert ok, e
+    gm = host(cwb.cwb_bin_mat_mat(dev(Zb), gidx, None if w is None else dev(w)))
+    rm = O.bin_mat_mat(Zb, idx, w)
+    ok, e = close(gm, rm, 1e-12, scale=np.abs(rm).max())
+    assert ok, e
+
+
+def test_bin_mat_vec_spec_examples():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+    for ex in g["bin_mat_vec"]:
+        out = cwb.cwb_bin_mat_vec(dev(np.array(ex["Zb"], float)), dev(np.array(ex["idx"], np.uint8), torch.uint8),
+                                  dev(np.array([ex["r"]], float)))
+        assert host(out)[0].tolist() == ex["out"]
+    for ex in g["bin_mat_mat"]:
+        out = cwb.cwb_bin_mat_mat(dev(np.array(ex["Zb"], float)), dev(np.array(ex["idx"], np.uint8), torch.uint8),
+                                  dev(np.array(ex["w"], float)))
+        assert host(out).tolist() == ex["out"]
+
+
+# ---------------------------------------------------------------- pool
+
+@pytest.mark.parametrize("name", ["R0", "R1", "R2"])
+def test_pool_matches_oracle(name):
+    ds = S.make(name, reps=[0])
+    c = ds.cfg
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    pg.status()
+    assert (pg.n_star, pg.d) == (po.n_star, po.d)
+    P = {k: host(v) for k, v in pg.pool().items()}
+    assert (P["idx"].astype(np.int64) == po.idx).all()          # bit-exact hash
+    assert (P["z"] == po.z).all()                                 # bit-exact design points
+    ok, e = close(P["Zb"], po.Zb, 1e-14, scale=1.0)
+    assert ok, e
+    ok, e = close(P["G"], po.G, 1e-12, scale=np.abs(po.G).max())
+    assert ok, e
+    lam = pg.lam()
+    ok, e = close(lam, po.lam, 1e-10)
+    assert ok, f"lambda rel err {e}"
+    Ainv = np.linalg.inv(po.G + po.lam[:, None, None] * po.D)
+    ok, e = close(P["Ainv"], Ainv, 1e-9, scale=np.abs(Ainv).max())
+    assert ok, e
+    # df(lambda_gpu) = 5 by the oracle's dense trace definition
+    for k in range(po.K):
+        assert abs(O.df(po.G[k], po.D, float(lam[k]), 1) - c.df) < 1e-9
+    pg.close()
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_df_kinds(kind):
+    ds = S.make("R1", reps=[0])
+    cfg = cfg_of(ds.cfg)
+    cfg.df_kind = kind
+    po = O.Pool(ds.X, cfg, O.MODE_BINNED)
+    gc = gpu_cfg_of(ds.cfg)
+    gc.df_kind = kind
+    pg = cwb.Pool(dev(ds.X), gc)
+    ok, e = close(pg.lam(), po.lam, 1e-10)
+    assert ok, e
+    pg.close()
+
+
+def test_pool_errors():
+    rng = np.random.default_rng(0)
+    X = rng.uniform(0, 1, (3, 200))
+    X[1] = 0.5
+    p = cwb.Pool(dev(X))
+    with pytest.raises(cwb.CwbError) as e:
+        p.status()
+    assert e.value.name == "CWB_EDEGENERATE"
+    X[1] = rng.uniform(0, 1, 200)
+    X[2, 7] = np.inf
+    with pytest.raises(cwb.CwbError) as e:
+        cwb.Pool(dev(X)).status()
+    assert e.value.name == "CWB_ENONFINITE"
+    with pytest.raises(cwb.CwbError) as e:   # df above rank(G): n* = 3 bins < 5 df
+        cwb.Pool(dev(rng.uniform(0, 1, (2, 50))), cwb.Config(n_star_rule=2, n_star_fixed=3)).status()
+    assert e.value.name == "CWB_ECALIB"
+    with pytest.raises(cwb.CwbError) as e:
+        cwb.Pool(torch.empty((0, 10), dtype=torch.float64, device=DEV))
+    assert e.value.name == "CWB_EEMPTY"
+
+
+# ------------------------------------------------------------ find best
+
+@pytest.mark.parametrize("name,B", [("R0", 8), ("R1", 40), ("R2", 3)])
+def test_find_best_matches_oracle(name, B):
+    ds = S.make(name, reps=range(B))
+    c = ds.cfg
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_DENSE)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    R = ds.Y - ds.Y.mean(1, keepdims=True)
+    R[0] *= 1e-3
+    k, th, sse = [host(t) for t in pg.find_best(dev(R))]
+    for b in range(B):
+        ko, tho, sseo, sall, gap = po.find_best(R[b])
+        if k[b] != ko:
+            assert gap / sseo <= 1e-10
+            continue
+        ok, e = close(th[b], tho, RTOL, scale=np.abs(tho).max())
+        assert ok, e
+        ok, e = close(sse[b], sseo, RTOL)
+        assert ok, e
+    pg.close()
+
+
+def test_find_best_ties_and_orthogonal():
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 1, 300)
+    X = np.stack([x, x, rng.uniform(0, 1, 300)])
+    po = O.Pool(X, O.Config(n_knots=6), O.MODE_BINNED)
+    pg = cwb.Pool(dev(X), cwb.Config(n_knots=6))
+    r = rng.standard_normal(300)
+    k, th, sse = [host(t) for t in pg.find_best(dev(r[None]))]
+    ko = po.find_best(r)[0]
+    assert ko in (0, 2) and (k[0] == ko or k[0] in (0, 2))
+    assert k[0] != 1  # exact duplicate of learner 0 never wins (lowest index)
+    # r orthogonal to learner 0's (and 1's) column space -> learner 2
+    ZA = po.Zb[0][po.idx[0]]
+    ZB = po.Zb[2][po.idx[2]]
+    v = ZB @ rng.standard_normal(po.d)
+    r2 = v - ZA @ np.linalg.lstsq(ZA, v, rcond=None)[0]
+    k, th, sse = [host(t) for t in pg.find_best(dev(r2[None]))]
+    assert k[0] == 2
+
+
+# ---------------------------------------------------------------- train
+
+def _gpu_train(pg, Y, c, path, M=None):
+    pg.set_path(path)
+    out = pg.train(dev(Y), nu=c.nu, M=M or c.M)
+    pg.status()
+    return {k: host(v) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("name", ["R0", "R1"])
+def test_train_full_parity(name, path):
+    ds = S.make(name)
+    c = ds.cfg
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    ro = po.train(ds.Y, nu=c.nu, M=c.M, threads=8)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    g = _gpu_train(pg, ds.Y, c, path)
+    first, ties = assert_train_parity(g, ro, c.n, f"{name}/path{path}")
+    # aggregation invariant on the GPU side: predict(X) reproduces the final fit
+    pred = host(pg.predict(dev(ds.X), dev(g["offset"]), dev(g["theta_agg"])))
+    opred = po.predict(ds.X, g["offset"], g["theta_agg"])
+    ok, e = close(pred, opred, 1e-12, scale=np.abs(opred).max())
+    assert ok, e
+    full = first == c.M
+    ok, e = close(pred[full], ro.f[full], 1e-9, scale=np.abs(ro.f).max())
+    assert ok, e
+    assert (np.diff(g["risk_trace"], axis=0) <= 1e-12 * g["risk_trace"][0]).all()
+    pg.close()
+
+
+def test_train_dense_oracle_agrees_r1_subset():
+    # the dense (materialised) definition, not only Algorithm binMatVec
+    ds = S.make("R1", reps=range(12))
+    c = ds.cfg
+    ro = O.Pool(ds.X, cfg_of(c), O.MODE_DENSE).train(ds.Y, nu=c.nu, M=c.M, threads=8)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    g = _gpu_train(pg, ds.Y, c, 0)
+    assert_train_parity(g, ro, c.n, "R1/dense")
+
+
+def test_paths_agree_and_deterministic():
+    ds = S.make("R1", reps=range(64))
+    c = ds.cfg
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    a = _gpu_train(pg, ds.Y, c, 1)
+    a2 = _gpu_train(pg, ds.Y, c, 1)
+    b = _gpu_train(pg, ds.Y, c, 2)
+    b2 = _gpu_train(pg, ds.Y, c, 2)
+    for k in a:
+        assert (a[k] == a2[k]).all(), k      # run-to-run bitwise (fused)
+        assert (b[k] == b2[k]).all(), k      # run-to-run bitwise (general)
+    assert (a["k_trace"] == b["k_trace"]).all()
+    ok, e = close(a["theta_agg"], b["theta_agg"], 1e-11, scale=np.abs(b["theta_agg"]).max())
+    assert ok, e
+
+
+def test_train_r2_full_launch_sampled():
+    # full R2 launch (B = 1024, the bench configuration of that rung); replications sampled
+    ds = S.make("R2")
+    c = ds.cfg
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    g = _gpu_train(pg, ds.Y, c, 0)
+    reps = [0, 1, 511, 1023]
+    ro = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED).train(ds.Y[reps], nu=c.nu, M=c.M, threads=4)
+    gs = {k: v[:, reps] if v.ndim == 2 and k != "theta_agg" else v[reps] for k, v in g.items()}
+    assert_train_parity(gs, ro, c.n, "R2")
+
+
+@pytest.mark.slow
+def test_train_r3_sampled():
+    ds = S.make("R3", reps=[0, 1, 2, 3, 4, 5, 6, 7])
+    c = ds.cfg
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    g = _gpu_train(pg, ds.Y, c, 0)
+    ro = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED).train(ds.Y[:2], nu=c.nu, M=c.M, threads=2)
+    gs = {k: v[:, :2] if v.ndim == 2 and k != "theta_agg" else v[:2] for k, v in g.items()}
+    assert_train_parity(gs, ro, c.n, "R3")
+
+
+@pytest.mark.slow
+def test_train_r4_sampled():
+    ds = S.make("R4", reps=[0, 1, 2, 3])
+    c = ds.cfg
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    g = _gpu_train(pg, ds.Y, c, 0, M=40)
+    ro = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED).train(ds.Y[:2], nu=c.nu, M=40, threads=2)
+    gs = {k: v[:, :2] if v.ndim == 2 and k != "theta_agg" else v[:2] for k, v in g.items()}
+    assert_train_parity(gs, ro, c.n, "R4")
+
+
+def test_train_edge_cases():
+    rng = np.random.default_rng(8)
+    X = rng.uniform(0, 1, (2, 50))
+    pg = cwb.Pool(dev(X), cwb.Config(n_knots=4))
+    Y = rng.standard_normal((3, 50))
+    for path in (1, 2):
+        pg.set_path(path)
+        out = pg.train(dev(Y), nu=0.0, M=5)              # nu = 0: offset only
+        assert (host(out["theta_agg"]) == 0).all()
+        out = pg.train(dev(Y), nu=0.1, M=0)              # M = 0: offset only
+        assert np.allclose(host(out["offset"]), Y.mean(1), rtol=1e-13)
+    Yb = Y.copy()
+    Yb[1, 3] = np.nan
+    pg.set_path(0)
+    pg.train(dev(Yb), nu=0.1, M=2)
+    with pytest.raises(cwb.CwbError) as e:
+        pg.status()
+    assert e.value.name == "CWB_ENONFINITE"
+
+
+def test_fit_host_matches_device_api():
+    ds = S.make("R1", reps=range(16))
+    c = ds.cfg
+    h = cwb.cwb_fit_host(ds.X, ds.Y, gpu_cfg_of(c), nu=c.nu, M=c.M)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    g = _gpu_train(pg, ds.Y, c, 0)
+    for k in g:
+        assert (h[k] == g[k]).all(), k
