@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 binned-CWB engine (arXiv 2110.03513).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config R1] [--impl ours|reference]
+
+One STEP = the whole hot path on one batch: cwb_init (binning, bin inversion,
+basis, G, df->lambda, cached inverse) + cwb_train (M boosting iterations for
+the B replications of the workload), inputs resident in HBM.  Metric (the
+reshaped BASELINE.json metric): learner-row evaluations per
+second = K*n*B*M / step time (one evaluation = one (learner, row,
+replication) contribution of the binMatVec scatter of P:L899-901).
+
+Timing: W warm-up steps, then K steps, each bracketed by CUDA events on the
+launching stream; L2 is flushed (256 MiB write) between steps outside the
+events; barrier + synchronize around the timed region; max over ranks.
+N > 1 (torchrun): replications are sharded (weak scaling, every rank its own
+B replications, no collective on the data path).
+
+--impl reference times the CPU oracle (oracle/, plain fp64 C) on a bounded
+sample of the same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import cwb_synth as S  # noqa: E402
+
+METRIC = "learner-row evaluations/s (K*n*B per boosting iteration) and boosting iterations/s"
+UNIT = "evals/s"
+
+
+def alg_ops_per_rep_iter(c, n_star, d):
+    """FP64 add/FMA instructions per replication-iteration of the fused path."""
+    K, n = c.K, c.n
+    h1 = K * n                      # binMatVec scatter: one add per (learner, row)
+    h2 = 4 * K * n_star             # s = Zb^T u, 4 non-zeros per design point
+    h3 = K * d * d                  # theta = A^-1 s
+    h4 = K * (7 * d + 3 * d)        # G theta on the band, v = theta (2 s - G theta), reduction
+    h6 = 4 * n_star + 2 * n         # zhat, r update, r^T r
+    return h1 + h2 + h3 + h4 + h6
+
+
+def fp64_peak_ops(peaks):
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    return 148 * 64 * mhz * 1e6      # 148 SMs x 64 FP64 lanes/clk (B200), one add or FMA each
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _names(self, mask):
+        N = self.N
+        table = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+                 "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                 "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
+        return {k for k, v in table.items() if mask & v}
+
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                self.reasons |= self._names(N.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_sample(cfg, seconds_target=12.0, threads=None):
+    """Time the oracle (binned mode = the paper's Algorithm, as it stands) on a bounded sample."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    c = cfg
+    oc = O.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots,
+                  degree=c.degree, df=c.df)
+    # probe: one replication, a few iterations
+    ds = S.make(c, reps=range(min(c.B, threads)))
+    t0 = time.perf_counter()
+    pool = O.Pool(ds.X, oc, O.MODE_BINNED)
+    t_init = time.perf_counter() - t0
+    M_probe = max(1, min(c.M, 5))
+    t0 = time.perf_counter()
+    pool.train(ds.Y[:1], nu=c.nu, M=M_probe, threads=1)
+    per_rep_iter = (time.perf_counter() - t0) / M_probe
+    reps = int(max(1, min(c.B, seconds_target * threads / max(per_rep_iter * c.M, 1e-9))))
+    reps = max(min(reps, c.B), 1)
+    ds = S.make(c, reps=range(reps))
+    t0 = time.perf_counter()
+    pool = O.Pool(ds.X, oc, O.MODE_BINNED)
+    pool.train(ds.Y, nu=c.nu, M=c.M, threads=threads)
+    dt = time.perf_counter() - t0
+    evals = c.K * c.n * reps * c.M
+    return {"value": evals / dt, "unit": UNIT, "cores": min(threads, reps), "kind": "oracle",
+            "sample": f"{c.name}: {reps} of {c.B} replications x M={c.M} iterations, oracle binned mode "
+                      f"(Algorithm binMatVec, P:L898-904), pool build included; {dt:.2f} s",
+            "seconds": dt, "init_s": t_init}
+
+
+def run_reference(args, cfg):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    res = []
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(cfg, seconds_target=args.ref_seconds, threads=threads)
+        if i >= args.warmup:
+            res.append(r)
+    v = float(np.mean([r["value"] for r in res]))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean([r["seconds"] for r in res]) * 1e3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (paper Sec. 4.1.1 generator, seeded)",
+            "config": workload_config(cfg, None, None),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": res[0]["cores"], "kind": "oracle",
+                             "sample": res[0]["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(c, n_star, d):
+    return {"workload": c.name, "n": c.n, "K": c.K, "B_per_gpu": c.B, "M": c.M, "nu": c.nu,
+            "n_star": n_star, "d": d, "df": c.df, "degree": c.degree, "n_knots": c.n_knots,
+            "step": "cwb_init + cwb_train (all M iterations for B replications)",
+            "l2": "flushed between steps (256 MiB write), flush outside the timed events"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="R1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 fused, 2 general")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_SHORT"), \
+        "timing rules: at least 3 warm-up steps"
+    cfg = S.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    devname = f"cuda:{local}"
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(devname))
+    from paper_2110_03513_b200 import cwb
+
+    # this rank's replications (weak scaling): rank r owns [r*B, (r+1)*B)
+    reps = range(rank * cfg.B, (rank + 1) * cfg.B)
+    ds = S.make(cfg, reps=reps)
+    X = torch.as_tensor(ds.X, device=devname)
+    Y = torch.as_tensor(ds.Y, device=devname)
+    gcfg = cwb.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots,
+                      degree=cfg.degree, df=cfg.df)
+    B, K, n, M = cfg.B, cfg.K, cfg.n, cfg.M
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=devname)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps + args.warmup)]
+    outs = None
+    launches = []
+
+    def step(i):
+        nonlocal outs
+        a, b, c_ = ev[i]
+        a.record(stream)
+        pool = cwb.Pool(X, gcfg)
+        if args.path:
+            pool.set_path(args.path)
+        b.record(stream)
+        outs = pool.train(Y, nu=cfg.nu, M=M, out=outs)
+        c_.record(stream)
+        launches.append(pool.launches())
+        pool.close()
+
+    for i in range(args.warmup):
+        step(i)
+        flush.fill_(float(i))
+    torch.cuda.synchronize()
+    pool = cwb.Pool(X, gcfg)
+    pool.status()
+    n_star, d = pool.n_star, pool.d
+    pool.close()
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    launches.clear()
+    clk = ClockSampler(local)
+    barrier()
+    with clk:
+        for i in range(args.warmup, args.warmup + args.steps):
+            flush.fill_(float(i))
+            step(i)
+        barrier()
+    step_ms = np.array([ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)])
+    train_ms = np.array([ev[i][1].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)])
+    init_ms = step_ms - train_ms
+    total_ms = float(step_ms.sum())
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=devname)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    evals = K * n * B * M * ws
+    value = evals / (ms_per_step * 1e-3)
+
+    # ---- end-to-end through the host-pointer C-ABI call (pinned host buffers)
+    Xh = torch.as_tensor(ds.X).pin_memory()
+    Yh = torch.as_tensor(ds.Y).pin_memory()
+    outh = {"offset": torch.empty(B, dtype=torch.float64).pin_memory(),
+            "theta_agg": torch.empty((B, K, d), dtype=torch.float64).pin_memory(),
+            "k_trace": torch.empty((M, B), dtype=torch.int32).pin_memory(),
+            "sse_trace": torch.empty((M, B), dtype=torch.float64).pin_memory(),
+            "risk_trace": torch.empty((M, B), dtype=torch.float64).pin_memory()}
+    lib = cwb.load()
+    import ctypes as C
+    ccfg = gcfg.c()
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+
+    def e2e_step():
+        rc = lib.cwb_fit_host(P(Xh), n, K, C.byref(ccfg), P(Yh), B, float(cfg.nu), M, P(outh["offset"]),
+                              P(outh["theta_agg"]), P(outh["k_trace"]), P(outh["sse_trace"]),
+                              P(outh["risk_trace"]), C.c_void_p(stream.cuda_stream))
+        if rc:
+            raise cwb.CwbError(rc, lib.cwb_last_error(None).decode())
+
+    for i in range(3):
+        e2e_step()
+    e_ms = []
+    for i in range(max(3, min(args.steps, 10))):
+        flush.fill_(float(i))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        e_ms.append(e0.elapsed_time(e1))
+    e2e_ms = float(np.mean(e_ms))
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=devname)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = ds.X.nbytes + ds.Y.nbytes
+    d2h = sum(v.numel() * v.element_size() for v in outh.values())
+
+    if rank == 0:
+        peaks, src = load_peaks()
+        ops = alg_ops_per_rep_iter(cfg, n_star, d) * B * M
+        train_s = float(np.mean(train_ms)) * 1e-3
+        achieved = ops / train_s
+        peak = fp64_peak_ops(peaks)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(cfg.name)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (paper Sec. 4.1.1 generator, seeded; OpenML sets not available)",
+            "config": workload_config(cfg, n_star, d),
+            "iters_per_s": M / (ms_per_step * 1e-3),
+            "phase_ms": {"init": float(np.mean(init_ms)), "train": float(np.mean(train_ms))},
+            "roofline": {"bound": "alu", "kernel": "k_train_fused" if args.path != 2 else "general path",
+                         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "note": ("fp64 add/FMA instructions per launch (DESIGN.md Sec. 5) / mean train-event "
+                                  f"time; peak = 148 SM x 64 fp64 lanes x {peaks.get('sm_max_mhz', 1965)} MHz "
+                                  f"({src} clock)")},
+            "e2e": {"value": evals / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+                    "api": "cwb_fit_host (pinned host buffers, copies + init + train + sync)"},
+            "clocks": clk.summary(),
+            "gpu_launches": int(sum(launches)),
+        }
+        if not args.no_cpu_baseline and ws == 1:
+            try:
+                line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg).items()
+                                        if k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:  # keep the GPU line even if the host leg fails
+                line["cpu_baseline"] = {"error": str(e)}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -110,7 +110,8 @@ def make(cfg: SynthConfig | str, reps=None) -> Dataset:
         cfg = CONFIGS[cfg]
     X, root = make_X(cfg)
     reps = np.arange(cfg.B) if reps is None else np.asarray(reps, dtype=np.int64)
-    children = root.spawn(cfg.B)
+    # children are indexed: spawning more than B leaves the first B unchanged
+    children = root.spawn(max(cfg.B, int(reps.max()) + 1 if len(reps) else cfg.B))
     n, p = cfg.n, cfg.p_inf
     bases = [_sim_basis(X[j]) for j in range(p)]
     nb = len(reps)

@@ -456,22 +456,71 @@ __global__ void k_dro(const double* __restrict__ Gall, int d, double target, int
     }
     __syncthreads();
     if (fail) return;
-    const double lam = s_lambda;
-    if (tid == 0) lambda_out[k] = lam;
-    // A = G + lambda D -> Cholesky -> A^{-1} = L^{-T} L^{-1}  (cached)
-    for (int e = tid; e < d * d; e += nthr) { const int a = e / d, b = e % d; P[a][b] = G[a][b] + lam * Dm[a][b]; }
-    __syncthreads();
-    blk_cholesky(P, d, &fail);
-    if (fail) { if (tid == 0) cwb_dev_fail(status, CWB_ECALIB); return; }
-    blk_tri_inverse(P, W, d);
-    for (int e = tid; e < d * d; e += nthr) {
-        const int i = e / d, c = e % d;
-        if (c <= i) {
-            double s = 0.0;
-            for (int q = i; q < d; q++) s += W[q][i] * W[q][c];
-            Ainv_out[((size_t)k * d + i) * d + c] = s;
-            Ainv_out[((size_t)k * d + c) * d + i] = s;
+    // Newton polish of the DRO root on the definition df(lambda) = tr(A^-1 G)
+    // (supp. P:L316): the whitened eigenvalues carry cond(G + D) * eps error,
+    // the dense trace only cond(A) * eps.  Two steps, then the cached inverse.
+    __shared__ double red[32];
+    for (int it = 0; it <= 2; it++) {
+        const double lam = s_lambda;
+        // A = G + lambda D -> Cholesky -> A^{-1} = L^{-T} L^{-1}  (cached)
+        for (int e = tid; e < d * d; e += nthr) { const int a = e / d, b = e % d; P[a][b] = G[a][b] + lam * Dm[a][b]; }
+        __syncthreads();
+        blk_cholesky(P, d, &fail);
+        if (fail) { if (tid == 0) cwb_dev_fail(status, CWB_ECALIB); return; }
+        blk_tri_inverse(P, W, d);
+        for (int e = tid; e < d * d; e += nthr) {  // P <- A^{-1} (symmetric)
+            const int i = e / d, c = e % d;
+            if (c <= i) {
+                double s = 0.0;
+                for (int q = i; q < d; q++) s += W[q][i] * W[q][c];
+                P[i][c] = s;
+                P[c][i] = s;
+            }
         }
+        __syncthreads();
+        if (it == 2) {
+            for (int e = tid; e < d * d; e += nthr) Ainv_out[(size_t)k * d * d + e] = P[e / d][e % d];
+            if (tid == 0) lambda_out[k] = lam;
+            break;
+        }
+        for (int e = tid; e < d * d; e += nthr) {  // M <- X = A^-1 G,  W <- A^-1 D
+            const int i = e / d, c = e % d;
+            double x = 0.0, y = 0.0;
+            for (int q = 0; q < d; q++) { x += P[i][q] * G[q][c]; y += P[i][q] * Dm[q][c]; }
+            M[i][c] = x;
+            W[i][c] = y;
+        }
+        __syncthreads();
+        // f = df - target, f' = d df / d lambda  (dX/dlambda = -A^-1 D X)
+        double tX = 0.0, tXX = 0.0, tYX = 0.0, tXYX = 0.0;
+        for (int e = tid; e < d * d; e += nthr) {
+            const int i = e / d, c = e % d;
+            if (i == c) tX += M[i][i];
+            tXX += M[i][c] * M[c][i];
+            double yx = 0.0, xy = 0.0;
+            for (int q = 0; q < d; q++) { yx += W[i][q] * M[q][c]; xy += M[i][q] * W[q][c]; }
+            if (i == c) tYX += yx;
+            tXYX += xy * M[c][i];
+        }
+        double vals[4] = {tX, tXX, tYX, tXYX};
+        double tot[4];
+        for (int q = 0; q < 4; q++) {
+            double v = warp_sum(vals[q]);
+            if ((tid & 31) == 0) red[tid >> 5] = v;
+            __syncthreads();
+            double t = 0.0;
+            for (int w = 0; w < (nthr >> 5); w++) t += red[w];
+            tot[q] = t;
+            __syncthreads();
+        }
+        double f, fp;
+        if (kind == 2) { f = 2.0 * tot[0] - tot[1] - target; fp = -2.0 * tot[2] + 2.0 * tot[3]; }
+        else { f = tot[0] - target; fp = -tot[2]; }
+        if (tid == 0) {
+            double nl = lam - f / fp;
+            if (isfinite(nl) && nl > 0.5 * lam && nl < 2.0 * lam) s_lambda = nl;
+        }
+        __syncthreads();
     }
 }
 
