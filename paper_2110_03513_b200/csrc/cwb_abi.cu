@@ -156,8 +156,8 @@ void cwb_free(cwb_ctx* c) {
     if (!c) return;
     cudaStream_t s = c->stream;
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
-                    c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->eig, c->ws.Rt, c->ws.U,
-                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part};
+                    c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
+                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->plan, c->permt};
     for (void* p : bufs) cwb_release(p, s);
     delete c;
 }
@@ -194,7 +194,7 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     ok &= cwb_alloc(&c->idx, (size_t)c->idx_bytes * Ks * nn, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->cnt, 4 * Ks * nss, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->off, 4 * Ks * (nss + 1), s) == cudaSuccess;
-    ok &= cwb_alloc(&c->perm, (size_t)c->perm_bytes * Ks * nn, s) == cudaSuccess;
+    ok &= cwb_alloc(&c->perm, (size_t)c->perm_bytes * (Ks * nn + 8), s) == cudaSuccess;  // +8: vector-load padding
     ok &= cwb_alloc((void**)&c->Zb, 8 * Ks * nss * dd, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->zj0, 4 * Ks * nss, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->Zs, 8 * Ks * nss * CWB_SPW, s) == cudaSuccess;
@@ -202,12 +202,12 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     ok &= cwb_alloc((void**)&c->G, 8 * Ks * dd * dd, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->Ainv, 8 * Ks * dd * dd, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->lambda, 8 * Ks, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->eig, 8 * Ks * dd, s) == cudaSuccess;
     if (!ok) {
         cwb_free(c);
         return cwb_set_error(nullptr, CWB_ENOMEM, "cwb_init: device allocation failed");
     }
     cudaMemsetAsync(c->d_status, 0, sizeof(int), s);
+    cudaMemsetAsync(c->perm, 0, (size_t)c->perm_bytes * (Ks * nn + 8), s);
     int rc = cwb_launch_init(c, X, s);
     if (rc) {
         std::string m = c->err;

@@ -6,7 +6,7 @@
 //   I4 k_csr      bin inversion: rows of every bin, ascending      (binning as a hash map)
 //   I5 k_basis    cubic B-spline basis at the design points
 //   I6 k_gram     G = Zb^T diag(cnt) Zb  (binMatMat, w = 1)
-//   I7 k_dro      Demmler-Reinsch df -> lambda, (G + lambda D)^-1  supp. P:L314-319
+//   I7 k_lambda   df(lambda) = df by Newton on the definition, (G + lambda D)^-1   supp. P:L314-319
 //
 // Everything here runs once per data set and is shared by all B
 // replications.  Bit-exactness with the paper's fp64 definitions matters for
@@ -291,237 +291,170 @@ __global__ void k_gram(const double* __restrict__ Zb, const uint32_t* __restrict
     }
 }
 
-// --------------------------------------------------- I7 DRO, lambda, inverse
+// ------------------------------------------- I7 df -> lambda, cached inverse
+// One warp per learner (no block barriers).  df(lambda) is evaluated by its
+// definition (supp.): A = G + lambda D, df1 = tr(A^-1 G),
+// df2 = tr(2 A^-1 G - (A^-1 G)^2), with its exact derivative
+// d tr(A^-1 G)/d lambda = -tr(A^-1 D A^-1 G).  The root of df(lambda) = df
+// ("must be solved numerically") is found by safeguarded Newton
+// in t = log(lambda).  The paper's Demmler-Reinsch route makes each
+// df evaluation O(d) after an O(d^3) eigen-decomposition, a CPU trade-off; a
+// warp evaluates the O(d^3) definition in a few microseconds and Newton needs
+// a handful of steps, so the eigen-decomposition is not used.
+// The inverse of the final A is cached for the iterations.
 #define DS 33  // padded shared row stride
 
-__device__ void blk_cholesky(double (*P)[DS], int d, int* fail) {
-    // in place: lower triangle of P becomes L with P = L L^T
-    for (int j = 0; j < d; j++) {
-        if (threadIdx.x == 0) {
-            double v = P[j][j];
-            if (!(v > 0.0)) *fail = 1;
-            P[j][j] = sqrt(fmax(v, 1e-300));
+__device__ __forceinline__ double dpen(int a, int b, int d) {
+    // D = Delta^T Delta, Delta rows (.., 1, -2, 1, ..)  (supp. P:L312)
+    double v = 0.0;
+    for (int i = max(0, max(a, b) - 2); i <= min(a, b) && i + 2 < d; i++) {
+        const double ca = (a == i) ? 1.0 : (a == i + 1) ? -2.0 : 1.0;
+        const double cb = (b == i) ? 1.0 : (b == i + 1) ? -2.0 : 1.0;
+        v += ca * cb;
+    }
+    return v;
+}
+
+struct LamEval { double f, fp; bool ok; };
+
+#define BW 3  // half-bandwidth of G (cubic B-splines overlap 4 design windows) and of D (2)
+
+// Banded Cholesky of A = G + lambda D (lane 0), then lane c solves A x = b_c
+// for the columns of G (-> X = A^-1 G) and of D (-> Y = A^-1 D).
+// f(t) = df(e^t) - target, f'(t) = lambda d df / d lambda,
+// d tr(X)/d lambda = -tr(Y X), d tr(X^2)/d lambda = -2 tr(X Y X).
+__device__ void band_factor(double lam, int d, double (*Gs)[DS], double (*Dm)[DS], double* Lb, double* inv,
+                            bool* ok_out) {
+    if ((threadIdx.x & 31) == 0) {
+        bool ok = true;
+        for (int j = 0; j < d; j++) {
+            for (int q = min(j, BW); q >= 1; q--) {  // L[j][c], c = j - q
+                const int c = j - q;
+                double v = Gs[j][c] + lam * Dm[j][c];
+                for (int p = max(0, j - BW); p < c; p++) v -= Lb[j * 4 + (j - p)] * Lb[c * 4 + (c - p)];
+                Lb[j * 4 + q] = v * inv[c];
+            }
+            double v = Gs[j][j] + lam * Dm[j][j];
+            for (int p = max(0, j - BW); p < j; p++) v -= Lb[j * 4 + (j - p)] * Lb[j * 4 + (j - p)];
+            ok &= v > 0.0;
+            const double l = sqrt(fmax(v, 1e-300));
+            Lb[j * 4] = l;
+            inv[j] = 1.0 / l;
         }
-        __syncthreads();
-        for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) P[i][j] /= P[j][j];
-        __syncthreads();
-        for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-            const int i = e / d, c = e % d;
-            if (c > j && i >= c) P[i][c] -= P[i][j] * P[c][j];
-        }
-        __syncthreads();
+        *ok_out = ok;
+    }
+    __syncwarp();
+}
+
+// x = A^-1 b for b = column c of B (read through the functor), result in column c of Xs
+template <typename Fb>
+__device__ __forceinline__ void band_solve(int d, const double* Lb, const double* inv, Fb b, double (*Xs)[DS], int c) {
+    for (int j = 0; j < d; j++) {  // L z = b
+        double v = b(j);
+        for (int p = max(0, j - BW); p < j; p++) v -= Lb[j * 4 + (j - p)] * Xs[p][c];
+        Xs[j][c] = v * inv[j];
+    }
+    for (int j = d - 1; j >= 0; j--) {  // L^T x = z
+        double v = Xs[j][c];
+        for (int p = j + 1; p <= min(d - 1, j + BW); p++) v -= Lb[p * 4 + (p - j)] * Xs[p][c];
+        Xs[j][c] = v * inv[j];
     }
 }
 
-__device__ void blk_tri_inverse(double (*L)[DS], double (*W)[DS], int d) {
-    // W = L^{-1} (lower triangular), one column per thread
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        for (int i = 0; i < d; i++) {
-            if (i < c) { W[i][c] = 0.0; continue; }
-            double s = (i == c) ? 1.0 : 0.0;
-            for (int q = c; q < i; q++) s -= L[i][q] * W[q][c];
-            W[i][c] = s / L[i][i];
+__device__ LamEval lam_eval(double t, int d, double target, int kind, double (*Gs)[DS], double (*Dm)[DS],
+                            double (*Xs)[DS], double (*Ys)[DS], double* Lb, double* inv) {
+    const int i = threadIdx.x & 31;
+    const double lam = exp(t);
+    __shared__ bool s_ok;
+    band_factor(lam, d, Gs, Dm, Lb, inv, &s_ok);
+    if (i < d) {
+        band_solve(d, Lb, inv, [&](int j) { return Gs[j][i]; }, Xs, i);
+        band_solve(d, Lb, inv, [&](int j) { return Dm[j][i]; }, Ys, i);
+    }
+    __syncwarp();
+    double tX = 0.0, tYX = 0.0, tXX = 0.0, tXYX = 0.0;
+    if (i < d) {
+        tX = Xs[i][i];
+        for (int j = 0; j < d; j++) {
+            tYX += Ys[i][j] * Xs[j][i];
+            if (kind == 2) {
+                tXX += Xs[i][j] * Xs[j][i];
+                double xy = 0.0;
+                for (int q = 0; q < d; q++) xy += Xs[i][q] * Ys[q][j];
+                tXYX += xy * Xs[j][i];
+            }
         }
     }
-    __syncthreads();
+    tX = warp_sum(tX);
+    tYX = warp_sum(tYX);
+    tXX = warp_sum(tXX);
+    tXYX = warp_sum(tXYX);
+    __syncwarp();
+    LamEval e;
+    e.ok = s_ok;
+    if (kind == 2) { e.f = 2.0 * tX - tXX - target; e.fp = lam * (-2.0 * tYX + 2.0 * tXYX); }
+    else { e.f = tX - target; e.fp = -lam * tYX; }
+    return e;
 }
 
-__device__ __forceinline__ double df_term(double mu, double lam, int kind) {
-    // eigenvalue of the hat matrix in the DRO basis: h = mu / (mu + lam (1 - mu))
-    double den = mu + lam * (1.0 - mu);
-    if (!(den > 0.0)) return 0.0;
-    double h = mu / den;
-    return kind == 2 ? h * (2.0 - h) : h;
-}
-
-__global__ void k_dro(const double* __restrict__ Gall, int d, double target, int kind,
-                      double* lambda_out, double* Ainv_out, double* eig_out, int* status) {
-    __shared__ double G[CWB_MAX_D][DS], P[CWB_MAX_D][DS], W[CWB_MAX_D][DS], T[CWB_MAX_D][DS];
-    __shared__ double cs[CWB_MAX_D / 2][2];
-    __shared__ int pq[CWB_MAX_D / 2][2];
-    __shared__ int fail;
-    __shared__ double s_lambda, s_off;
+__global__ void k_lambda(const double* __restrict__ Gall, int d, double target, int kind,
+                         double* lambda_out, double* Ainv_out, int* status) {
+    __shared__ double Gs[CWB_MAX_D][DS], Dm[CWB_MAX_D][DS], Xs[CWB_MAX_D][DS], Ys[CWB_MAX_D][DS];
+    __shared__ double Lb[CWB_MAX_D * 4], inv[CWB_MAX_D];
     if (status && *status) return;
-    const int k = blockIdx.x;
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    if (tid == 0) fail = 0;
-    for (int e = tid; e < d * d; e += nthr) {
-        const int a = e / d, b = e % d;
-        const double g = Gall[((size_t)k * d + a) * d + b];
-        // D = Delta^T Delta, Delta rows (.., 1, -2, 1, ..)  (supp. P:L312)
-        double dv = 0.0;
-        for (int i = 0; i + 2 < d; i++) {
-            double ca = (a == i) ? 1.0 : (a == i + 1) ? -2.0 : (a == i + 2) ? 1.0 : 0.0;
-            double cb = (b == i) ? 1.0 : (b == i + 1) ? -2.0 : (b == i + 2) ? 1.0 : 0.0;
-            dv += ca * cb;
+    const int k = blockIdx.x, i = threadIdx.x;
+    if (i < d)
+        for (int c = 0; c < d; c++) {
+            Gs[i][c] = Gall[((size_t)k * d + i) * d + c];
+            Dm[i][c] = dpen(i, c, d);
         }
-        G[a][b] = g;
-        T[a][b] = dv;          // keep D in T until it is needed again
-        P[a][b] = g + dv;      // whitening matrix G + D (PD, reading G19)
-    }
-    __syncthreads();
-    blk_cholesky(P, d, &fail);
-    if (fail) { if (tid == 0) cwb_dev_fail(status, CWB_ECALIB); return; }
-    blk_tri_inverse(P, W, d);  // W = R^{-1},  G + D = R R^T
-    // M = W G W^T  (symmetric, eigenvalues mu in [0, 1])
-    double (*Dm)[DS] = T;
-    __shared__ double M[CWB_MAX_D][DS];
-    for (int e = tid; e < d * d; e += nthr) {  // P <- W G
-        const int i = e / d, c = e % d;
-        double s = 0.0;
-        for (int q = 0; q <= i; q++) s += W[i][q] * G[q][c];
-        P[i][c] = s;
-    }
-    __syncthreads();
-    for (int e = tid; e < d * d; e += nthr) {  // M <- (W G) W^T, lower half mirrored
-        const int i = e / d, c = e % d;
-        if (c <= i) {
-            double s = 0.0;
-            for (int q = 0; q <= c; q++) s += P[i][q] * W[c][q];
-            M[i][c] = s;
-            M[c][i] = s;
+    __syncwarp();
+    const double trG = warp_sum(i < d ? Gs[i][i] : 0.0);
+    const double trD = warp_sum(i < d ? Dm[i][i] : 0.0);
+    double t = log(fmax(trG, 1e-300) / fmax(trD, 1e-300));
+    double tlo = -INFINITY, thi = INFINITY;  // f(tlo) > 0 > f(thi)
+    bool done = false, fail = false;
+    int it = 0;
+    for (; it < 80 && !done; it++) {
+        LamEval e = lam_eval(t, d, target, kind, Gs, Dm, Xs, Ys, Lb, inv);
+#ifdef CWB_DEBUG_LAMBDA
+        if (i == 0) printf("k=%d it=%d t=%.17g f=%.3e fp=%.3e ok=%d\n", k, it, t, e.f, e.fp, (int)e.ok);
+#endif
+        if (!e.ok || !isfinite(e.f)) {  // A not numerically SPD at this lambda: move up
+            tlo = t;
+            t = isfinite(thi) ? 0.5 * (t + thi) : t + 4.0;
+            if (t > 120.0) { fail = true; break; }
+            continue;
         }
-    }
-    __syncthreads();
-    // cyclic parallel Jacobi (round-robin pairs; disjoint rotations commute)
-    const int m = d + (d & 1);
-    for (int sweep = 0; sweep < 40; sweep++) {
-        if (tid < 32) {
-            double o = 0.0;
-            for (int e = tid; e < d * d; e += 32) { const int i = e / d, c = e % d; if (i != c) o += M[i][c] * M[i][c]; }
-            o = warp_sum(o);
-            if (tid == 0) s_off = o;
+        if (fabs(e.f) <= 1e-13 * target) { done = true; break; }
+        if (e.f > 0.0) tlo = t; else thi = t;
+        double tn = t - e.f / e.fp;
+        const bool inside = isfinite(tn) && tn > tlo && tn < thi;
+        if (!inside) {
+            if (isfinite(tlo) && isfinite(thi)) tn = 0.5 * (tlo + thi);
+            else tn = (e.f > 0.0) ? t + 4.0 : t - 4.0;
         }
-        __syncthreads();
-        if (s_off < 1e-34) break;
-        for (int st = 0; st < m - 1; st++) {
-            if (tid < m / 2) {
-                int a0 = (tid == 0) ? 0 : 1 + ((tid - 1 + st) % (m - 1));
-                int b0 = 1 + ((m - 1 - tid - 1 + st) % (m - 1));
-                int p = min(a0, b0), q = max(a0, b0);
-                double c = 1.0, s = 0.0;
-                if (q < d && M[p][q] != 0.0) {
-                    double tau = (M[q][q] - M[p][p]) / (2.0 * M[p][q]);
-                    double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = 1.0 / sqrt(1.0 + t * t);
-                    s = t * c;
-                }
-                cs[tid][0] = c; cs[tid][1] = s;
-                pq[tid][0] = p; pq[tid][1] = (q < d) ? q : -1;
-            }
-            __syncthreads();
-            for (int e = tid; e < (m / 2) * d; e += nthr) {  // rows: M <- J^T M
-                const int pr = e / d, j = e % d;
-                const int p = pq[pr][0], q = pq[pr][1];
-                if (q >= 0) {
-                    const double c = cs[pr][0], s = cs[pr][1];
-                    const double ap = M[p][j], aq = M[q][j];
-                    M[p][j] = c * ap - s * aq;
-                    M[q][j] = s * ap + c * aq;
-                }
-            }
-            __syncthreads();
-            for (int e = tid; e < (m / 2) * d; e += nthr) {  // columns: M <- M J
-                const int pr = e / d, j = e % d;
-                const int p = pq[pr][0], q = pq[pr][1];
-                if (q >= 0) {
-                    const double c = cs[pr][0], s = cs[pr][1];
-                    const double ap = M[j][p], aq = M[j][q];
-                    M[j][p] = c * ap - s * aq;
-                    M[j][q] = s * ap + c * aq;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // lambda: df(lambda) = target, bisection on log2(lambda) (df decreasing)
-    if (tid < 32) {
-        double mu = 0.0;
-        if (tid < d) mu = fmin(1.0, fmax(0.0, M[tid][tid]));
-        if (tid < d) eig_out[(size_t)k * d + tid] = mu;
-        double elo = -150.0, ehi = 150.0;
-        double dlo = warp_sum(tid < d ? df_term(mu, exp2(elo), kind) : 0.0);
-        double dhi = warp_sum(tid < d ? df_term(mu, exp2(ehi), kind) : 0.0);
-        bool ok = (dlo > target) && (dhi < target);
-        for (int it = 0; it < 80 && ok; it++) {
-            double mid = 0.5 * (elo + ehi);
-            double v = warp_sum(tid < d ? df_term(mu, exp2(mid), kind) : 0.0);
-            if (v > target) elo = mid;
-            else ehi = mid;
-        }
-        if (tid == 0) {
-            if (!ok) { fail = 1; cwb_dev_fail(status, CWB_ECALIB); }
-            s_lambda = exp2(0.5 * (elo + ehi));
-        }
-    }
-    __syncthreads();
-    if (fail) return;
-    // Newton polish of the DRO root on the definition df(lambda) = tr(A^-1 G)
-    // (supp. P:L316): the whitened eigenvalues carry cond(G + D) * eps error,
-    // the dense trace only cond(A) * eps.  Two steps, then the cached inverse.
-    __shared__ double red[32];
-    for (int it = 0; it <= 2; it++) {
-        const double lam = s_lambda;
-        // A = G + lambda D -> Cholesky -> A^{-1} = L^{-T} L^{-1}  (cached)
-        for (int e = tid; e < d * d; e += nthr) { const int a = e / d, b = e % d; P[a][b] = G[a][b] + lam * Dm[a][b]; }
-        __syncthreads();
-        blk_cholesky(P, d, &fail);
-        if (fail) { if (tid == 0) cwb_dev_fail(status, CWB_ECALIB); return; }
-        blk_tri_inverse(P, W, d);
-        for (int e = tid; e < d * d; e += nthr) {  // P <- A^{-1} (symmetric)
-            const int i = e / d, c = e % d;
-            if (c <= i) {
-                double s = 0.0;
-                for (int q = i; q < d; q++) s += W[q][i] * W[q][c];
-                P[i][c] = s;
-                P[c][i] = s;
-            }
-        }
-        __syncthreads();
-        if (it == 2) {
-            for (int e = tid; e < d * d; e += nthr) Ainv_out[(size_t)k * d * d + e] = P[e / d][e % d];
-            if (tid == 0) lambda_out[k] = lam;
+        if (fabs(tn - t) <= 1e-15 * fmax(1.0, fabs(t))) {  // step below resolution: stop at tn
+            t = tn;
+            e = lam_eval(t, d, target, kind, Gs, Dm, Xs, Ys, Lb, inv);
+            done = e.ok;
+            fail = !e.ok || fabs(e.f) > 1e-9;
             break;
         }
-        for (int e = tid; e < d * d; e += nthr) {  // M <- X = A^-1 G,  W <- A^-1 D
-            const int i = e / d, c = e % d;
-            double x = 0.0, y = 0.0;
-            for (int q = 0; q < d; q++) { x += P[i][q] * G[q][c]; y += P[i][q] * Dm[q][c]; }
-            M[i][c] = x;
-            W[i][c] = y;
-        }
-        __syncthreads();
-        // f = df - target, f' = d df / d lambda  (dX/dlambda = -A^-1 D X)
-        double tX = 0.0, tXX = 0.0, tYX = 0.0, tXYX = 0.0;
-        for (int e = tid; e < d * d; e += nthr) {
-            const int i = e / d, c = e % d;
-            if (i == c) tX += M[i][i];
-            tXX += M[i][c] * M[c][i];
-            double yx = 0.0, xy = 0.0;
-            for (int q = 0; q < d; q++) { yx += W[i][q] * M[q][c]; xy += M[i][q] * W[q][c]; }
-            if (i == c) tYX += yx;
-            tXYX += xy * M[c][i];
-        }
-        double vals[4] = {tX, tXX, tYX, tXYX};
-        double tot[4];
-        for (int q = 0; q < 4; q++) {
-            double v = warp_sum(vals[q]);
-            if ((tid & 31) == 0) red[tid >> 5] = v;
-            __syncthreads();
-            double t = 0.0;
-            for (int w = 0; w < (nthr >> 5); w++) t += red[w];
-            tot[q] = t;
-            __syncthreads();
-        }
-        double f, fp;
-        if (kind == 2) { f = 2.0 * tot[0] - tot[1] - target; fp = -2.0 * tot[2] + 2.0 * tot[3]; }
-        else { f = tot[0] - target; fp = -tot[2]; }
-        if (tid == 0) {
-            double nl = lam - f / fp;
-            if (isfinite(nl) && nl > 0.5 * lam && nl < 2.0 * lam) s_lambda = nl;
-        }
-        __syncthreads();
+        if (tn < -120.0 || tn > 120.0) { fail = true; break; }
+        t = tn;
     }
+    if (!done || fail) {
+        if (i == 0) cwb_dev_fail(status, CWB_ECALIB);
+        return;
+    }
+    // cached inverse: columns of A^-1 by banded solves, symmetrised
+    if (i < d) band_solve(d, Lb, inv, [&](int j) { return j == i ? 1.0 : 0.0; }, Xs, i);
+    __syncwarp();
+    if (i == 0) lambda_out[k] = exp(t);
+    if (i < d)
+        for (int c = 0; c < d; c++)
+            Ainv_out[((size_t)k * d + i) * d + c] = 0.5 * (Xs[i][c] + Xs[c][i]);
 }
 
 }  // namespace
@@ -590,10 +523,12 @@ int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
     rc = cwb_launch_csr(c, c->idx, c->idx_bytes, c->n, K, ns, c->cnt, c->off, c->perm,
                         c->perm_bytes, s);
     if (rc) return rc;
+    rc = cwb_fused_plan(c, s);
+    if (rc) return rc;
     k_basis<<<K, 128, sizeof(int32_t) * ns, s>>>(c->z, c->lo, c->hi, ns, c->degree, c->n_knots, d,
                                                  c->Zb, c->zj0, c->Zs, c->lwin, c->d_status);
     k_gram<<<K, 256, 0, s>>>(c->Zb, c->cnt, ns, d, c->lwin, c->G, c->d_status);
-    k_dro<<<K, 256, 0, s>>>(c->G, d, c->df, c->df_kind, c->lambda, c->Ainv, c->eig, c->d_status);
+    k_lambda<<<K, 32, 0, s>>>(c->G, d, c->df, c->df_kind, c->lambda, c->Ainv, c->d_status);
     c->launches += 3;
     return cwb_check_launch(c, "pool kernels");
 }

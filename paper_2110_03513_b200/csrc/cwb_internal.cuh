@@ -64,7 +64,13 @@ struct cwb_ctx {
     double* G = nullptr;      // K x d x d   Zb^T diag(cnt) Zb
     double* Ainv = nullptr;   // K x d x d   (G + lambda D)^-1
     double* lambda = nullptr; // K
-    double* eig = nullptr;    // K x d  DRO eigenvalues mu in [0,1]
+
+    // fused-kernel plan (k_fused_plan): threads per CTA, positions per thread
+    int32_t* plan = nullptr;
+    void* permt = nullptr;       // step-major task row ids (uint16 / uint32)
+    int32_t permt_bytes = 2;
+    int32_t fused_T = 0, fused_chunk = 0;
+    size_t fused_smem = 0;
 
     cwb_train_ws ws;
 };
@@ -91,7 +97,8 @@ int cwb_launch_csr(cwb_ctx* ctx, const void* idx, int32_t idx_bytes, int64_t n, 
 int cwb_train_fused(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
                     double* offset_out, double* theta_agg_out, int32_t* k_trace, double* sse_trace,
                     double* risk_trace, cudaStream_t s, bool* launched);
-size_t cwb_fused_smem_bytes(const cwb_ctx* ctx, bool perm_in_smem);
+size_t cwb_fused_smem_bytes(const cwb_ctx* ctx);
+int cwb_fused_plan(cwb_ctx* ctx, cudaStream_t s);
 int cwb_train_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
                       double* offset_out, double* theta_agg_out, int32_t* k_trace,
                       double* sse_trace, double* risk_trace, cudaStream_t s);
