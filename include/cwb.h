@@ -172,6 +172,13 @@ int cwb_fit_host(const double* X, int64_t n, int32_t K, const cwb_config* cfg, c
 int cwb_predict(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
                 const double* theta_agg, int32_t B, double* out, cudaStream_t stream);
 
+/* Profiling hook: when cycles4 (a DEVICE buffer of 4 int64) is non-NULL, every
+ * later fused cwb_train launch writes the clock64() cycles its CTA 0 spent in
+ * the four phases of an iteration (A: binMatVec sums, B: per-learner
+ * selection criterion, C: argmax + parameters, D: residual update), summed over
+ * the M iterations.  NULL switches it off (default). */
+int cwb_set_phase_timing(cwb_ctx* ctx, int64_t* cycles4);
+
 /* Number of kernels this context has launched so far (bench evidence). */
 int64_t cwb_launch_count(const cwb_ctx* ctx);
 

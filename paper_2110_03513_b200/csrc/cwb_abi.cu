@@ -157,7 +157,8 @@ void cwb_free(cwb_ctx* c) {
     cudaStream_t s = c->stream;
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
-                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->plan, c->permt};
+                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->plan, c->permt,
+                    c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
     delete c;
 }
@@ -202,6 +203,11 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     ok &= cwb_alloc((void**)&c->G, 8 * Ks * dd * dd, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->Ainv, 8 * Ks * dd * dd, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->lambda, 8 * Ks, s) == cudaSuccess;
+    c->nsp = (int32_t)((ns + 1) / 2 * 2);
+    // design points in the support of one B-spline ((degree+1) knot intervals), +2 for rounding
+    c->W = (int32_t)std::min<int64_t>(ns, ((int64_t)(cfg.degree + 1) * (ns - 1)) / (cfg.n_knots + 1) + 2);
+    ok &= cwb_alloc((void**)&c->Cb, 8 * Ks * dd * 4, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&c->ZT, 8 * Ks * (size_t)c->W * dd, s) == cudaSuccess;
     if (!ok) {
         cwb_free(c);
         return cwb_set_error(nullptr, CWB_ENOMEM, "cwb_init: device allocation failed");
@@ -356,6 +362,12 @@ int cwb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offset,
 }
 
 int64_t cwb_launch_count(const cwb_ctx* c) { return c ? c->launches : 0; }
+
+int cwb_set_phase_timing(cwb_ctx* c, int64_t* cycles4) {
+    if (!c) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_set_phase_timing: NULL context");
+    c->timing = reinterpret_cast<long long*>(cycles4);
+    return CWB_OK;
+}
 
 }  // extern "C"
 

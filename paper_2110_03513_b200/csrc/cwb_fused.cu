@@ -1,31 +1,32 @@
-// cwb_fused.cu -- the whole CWB loop (Alg. 1 supp.) for one
-// replication per CTA, all M iterations in one launch.
+// cwb_fused.cu -- the whole CWB loop (Alg. 1 supp.) for RB = 1 or
+// 2 replications per CTA, all M iterations in one launch.
 //
 // Replications are independent boosting runs that share the binned pool, so
 // a CTA never waits for another CTA: no grid barrier, no atomics, no host
-// round trip between iterations.  The residual vector r (n doubles) and the
-// bin sums u (K x n* doubles) stay in shared memory for all M iterations;
-// the pool (task table, basis, cached inverse) is read-only and L1/L2
-// resident.  Per iteration m:
+// round trip between iterations.  The residuals r (n x RB doubles, the RB
+// replications of a row side by side) and the bin sums u (K x n* x RB) stay
+// in shared memory for all M iterations; when it fits, the read-only pool
+// tables used every iteration (gather schedule, basis windows, cached
+// inverses, selection factors) are staged in shared memory too, otherwise
+// they are read through L1/L2.  Four block barriers per iteration m:
 //
-//   H1  u_k(l) = sum_{i in bin l of learner k} r_i      binMatVec loop
-//       The K*n* bins are cut into tasks of at most P rows (P ~ K n / T),
-//       sorted by length and dealt to the T threads in snake order by a plan
-//       built once per data set (k_fused_plan).  The row ids of the 32 tasks
-//       of a warp are stored step-major ([step][lane], padded with a zero
-//       row), so each step is one coalesced index load and one gather, with
-//       no per-row branch; rows inside a task are ordered by shared-memory
-//       bank (rotated per lane) so that the gathers of a step spread over the
-//       banks.  A bin cut into several tasks is completed by a fixed-order
-//       combine.
-//   H2  s_k = Zb_k^T u_k  (4 non-zeros per design point)
-//   H3  theta_k = (G_k + lambda_k D)^-1 s_k (cached)
-//   H4  delta_k = 2 theta_k^T s_k - theta_k^T G_k theta_k,  SSE_k = r^T r - delta_k
-//   H5  k* = argmin SSE_k = argmax delta_k, lowest k on ties
-//   H6  r -= nu Zb_{k*}(idx_{k*}(i)) theta*;  theta_agg[k*] += nu theta*;  r^T r
-//
-// One warp per learner runs H2-H4 (lane j = coefficient j), so the solve and
-// the SSE reduction use register shuffles instead of shared-memory passes.
+//   A  H1  u_k(l) = sum_{i in bin l of learner k} r_i      binMatVec loop
+//          The K*n* bins are cut into tasks, sorted by length and dealt to the
+//          T threads in snake order by a plan built once per (data set, RB, T)
+//          (k_fused_plan).  For each warp the plan holds a gather schedule of
+//          byte offsets ([step/4][lane][4]) in which the lanes of a shared-
+//          memory wavefront always hit distinct bank groups; one 8- or 16-byte
+//          load fetches 4 offsets and each offset addresses the RB residuals of
+//          a row directly.  Zero padding rows r[n..n+15] absorb ragged ends; a
+//          bin cut into several tasks is completed by a fixed-order combine.
+//   B  H2-H4  one warp per learner, lane j = coefficient j:
+//          s = Zb^T u over the design-point window of basis j,
+//          theta = (G + lambda D)^-1 s with the cached inverse,
+//          delta = |C^T theta|^2 = 2 theta^T s - theta^T G theta with C C^T = G + 2 lambda D
+//          banded, so SSE_k = r^T r - delta_k.
+//   C  H5  warp q (replication q): k* = argmax delta_k, lowest k on ties;
+//          zhat = nu Zb_k* theta_k* at the design points; theta_agg[k*] += nu theta* (P:L838).
+//   D  H6  r_i -= zhat[idx_k*(i)], r^T r per warp.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,43 +37,56 @@
 namespace {
 
 constexpr int kDiscard = INT32_MIN;
+constexpr int kPadRows = 16;  // zero rows after the n residual rows, one per bank group
 
 struct FusedParams {
-    int n, K, ns, d, M, B, T, n_multi;
+    int n, K, ns, nsp, d, M, B, n_multi, W;
+    int permt_cap;  // entries of permt staged in shared memory (POOL)
+    int ztab;       // Zs / zj0 staged in shared memory
     double nu;
+    double inv2n;  // 1 / (2n): risk = r^T r / (2n) without a division on the critical path
     const double* Y;
     const void* idx;
     const void* permt;
     const int32_t* plan;
     const int32_t* zj0;
     const double* Zs;
-    const double* Zb;
-    const int32_t* lwin;
-    const double* Ainv;
-    const double* G;
+    const double* ZT;     // K x W x d  basis windows
+    const int32_t* lwin;  // K x d x 2  window starts
+    const double* Ainv;   // K x d x d
+    const double* Cb;     // K x d x 4
     double* offset_out;
     double* agg_out;
     int32_t* k_trace;
     double* sse_trace;
     double* risk_trace;
+    long long* timing;  // optional: cycles per phase (CTA 0, thread 0), summed over iterations
     int* status;
 };
 
 __host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 
 struct SmemLayout {
-    size_t r, U, th, delta, zhat, agg, pc, red, total;
-    __host__ __device__ SmemLayout(int n, int K, int ns, int d, int T, int n_multi) {
-        const size_t KS = (size_t)K * ns;
+    size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, total;
+    __host__ __device__ SmemLayout(int n, int K, int nsp, int d, int W, int n_multi, int RB, int NW, bool pool,
+                                   size_t permt_bytes, bool ztab) {
         size_t o = 0;
-        r = o; o = align16(o + sizeof(double) * (n + 1));  // r[n] = 0: padding row
-        U = o; o = align16(o + sizeof(double) * KS);
-        th = o; o = align16(o + sizeof(double) * (size_t)K * 32);
-        delta = o; o = align16(o + sizeof(double) * K);
-        zhat = o; o = align16(o + sizeof(double) * ns);
-        agg = o; o = align16(o + sizeof(double) * (size_t)K * d);
-        pc = o; o = align16(o + sizeof(double) * (n_multi > 0 ? n_multi : 1));
-        red = o; o = align16(o + sizeof(double) * 32);
+        r = o; o = align16(o + sizeof(double) * RB * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
+        U = o; o = align16(o + sizeof(double) * RB * ((size_t)K * nsp + W));  // +W: window overrun pad
+        delta = o; o = align16(o + sizeof(double) * RB * K);
+        th = o; o = align16(o + sizeof(double) * RB * (size_t)K * 32);        // theta_k of every learner
+        ss = o; o = align16(o + sizeof(double) * RB * (size_t)NW * 32);       // per-warp s = Zb^T u
+        zhat = o; o = align16(o + sizeof(double) * RB * (size_t)nsp);
+        agg = o; o = align16(o + sizeof(double) * RB * (size_t)K * d);
+        pc = o; o = align16(o + sizeof(double) * RB * (n_multi > 0 ? n_multi : 1));
+        red = o; o = align16(o + sizeof(double) * 2 * RB * (size_t)NW * 32);  // double-buffered per-thread r^T r
+        permt = o; if (pool) o = align16(o + permt_bytes);
+        zt = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * W * d);
+        ai = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * d * d);
+        cb = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * d * 4);
+        lw = o; if (pool) o = align16(o + sizeof(int32_t) * (size_t)K * d);
+        zs = o; if (ztab) o = align16(o + sizeof(double) * (size_t)K * nsp * CWB_SPW);
+        zj = o; if (ztab) o = align16(o + sizeof(int32_t) * (size_t)K * nsp);
         total = o;
     }
 };
@@ -82,7 +96,7 @@ struct SmemLayout {
 //   tt_dest[R*T]   destination of thread t's task in round r (>= 0: u index,
 //                  < 0: piece slot -dest-1, INT32_MIN: no task)
 //   wl[R*NW]       steps of warp w in round r (multiple of 4, 0: none)
-//   wb[R*NW]       offset of that block in permt ([step][lane] row ids)
+//   wb[R*NW]       offset of that block in permt ([step/4][lane][4] byte offsets)
 //   comb_g[KS] comb_first[KS] comb_cnt[KS]   bins cut into several pieces
 __host__ __device__ __forceinline__ int plan_rounds_max(int KS, int T) { return (KS + 2 * T) / T + 1; }
 __host__ __device__ __forceinline__ size_t plan_ints(int KS, int T) {
@@ -93,27 +107,102 @@ __host__ __device__ __forceinline__ size_t permt_bound(int KS, int T, int P) {
     return (size_t)plan_rounds_max(KS, T) * T * (size_t)((P + 3) / 4 * 4);
 }
 
-template <typename IdxT, typename PermT, int MAXT, int MINB>
+template <int RB> struct RV;  // RB residuals of one row
+template <> struct RV<1> {
+    double x;
+    __device__ __forceinline__ static RV ld(const unsigned char* base, uint32_t off) {
+        RV v; v.x = *reinterpret_cast<const double*>(base + off); return v;
+    }
+    __device__ __forceinline__ double operator[](int) const { return x; }
+};
+template <> struct RV<2> {
+    double x, y;
+    __device__ __forceinline__ static RV ld(const unsigned char* base, uint32_t off) {
+        const double2 t = *reinterpret_cast<const double2*>(base + off); RV v; v.x = t.x; v.y = t.y; return v;
+    }
+    __device__ __forceinline__ double operator[](int q) const { return q ? y : x; }
+};
+
+// 4 byte offsets of consecutive steps of this lane
+template <typename PermT> struct Off4;
+template <> struct Off4<uint16_t> {
+    uint32_t o0, o1, o2, o3;
+    template <bool SM> __device__ __forceinline__ static Off4 ld(const uint16_t* p) {
+        const uint2 v = SM ? *reinterpret_cast<const uint2*>(p) : __ldg(reinterpret_cast<const uint2*>(p));
+        Off4 o; o.o0 = v.x & 0xffffu; o.o1 = v.x >> 16; o.o2 = v.y & 0xffffu; o.o3 = v.y >> 16; return o;
+    }
+};
+template <> struct Off4<uint32_t> {
+    uint32_t o0, o1, o2, o3;
+    template <bool SM> __device__ __forceinline__ static Off4 ld(const uint32_t* p) {
+        const uint4 v = SM ? *reinterpret_cast<const uint4*>(p) : __ldg(reinterpret_cast<const uint4*>(p));
+        Off4 o; o.o0 = v.x; o.o1 = v.y; o.o2 = v.z; o.o3 = v.w; return o;
+    }
+};
+
+template <bool SM> __device__ __forceinline__ double2 ld2(const double2* p) { return SM ? *p : __ldg(p); }
+
+__device__ __forceinline__ long long phase_mark(long long* acc, long long t0, bool on) {
+    if (!on) return 0;
+    const long long t = clock64();
+    *acc += t - t0;
+    return t;
+}
+
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int T = blockDim.x, NW = T >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.x;
+    const int b0 = blockIdx.x * RB;
     const int n = p.n;
-    const int K = p.K, ns = p.ns, d = p.d, KS = K * ns;
-    const SmemLayout L(n, K, ns, d, T, p.n_multi);
-    double* r = (double*)(smem + L.r);
-    double* U = (double*)(smem + L.U);
-    double* th = (double*)(smem + L.th);
+    const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns;
+    const int W = p.W;
+    const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab != 0);
+    double* r = (double*)(smem + L.r);  // r[i * RB + q]
+    const unsigned char* rb = smem + L.r;
+    double* U = (double*)(smem + L.U);  // U[g * RB + q], g = k * nsp + l
     double* delta = (double*)(smem + L.delta);
-    double* zhat = (double*)(smem + L.zhat);
+    double* thall = (double*)(smem + L.th);  // thall[(k * RB + q) * 32 + j]
+    double* zhat = (double*)(smem + L.zhat);  // zhat[q * nsp + l]
     double* agg = (double*)(smem + L.agg);
     double* pc = (double*)(smem + L.pc);
-    double* red = (double*)(smem + L.red);
-    const PermT* permt = (const PermT*)p.permt;
+    double* red = (double*)(smem + L.red);  // red[(parity * RB + q) * T + tid]: per-thread r^T r partials
+    const PermT* permt = POOL ? (const PermT*)(smem + L.permt) : (const PermT*)p.permt;
+    const double* ZTc = POOL ? (const double*)(smem + L.zt) : p.ZT;
+    const double* Ac = POOL ? (const double*)(smem + L.ai) : p.Ainv;
+    const double* Cbc = POOL ? (const double*)(smem + L.cb) : p.Cb;
+    double* sS = (double*)(smem + L.ss) + (size_t)warp * RB * 32;
+    const double* Zs_c = p.ztab ? (const double*)(smem + L.zs) : p.Zs;
+    const int32_t* zj0_c = p.ztab ? (const int32_t*)(smem + L.zj) : p.zj0;
+    const int zstride = p.ztab ? nsp : ns;  // row stride of Zs / zj0 per learner
     const IdxT* idx = (const IdxT*)p.idx;
+    const bool timed = p.timing && blockIdx.x == 0 && tid == 0;
+    long long tA = 0, tB = 0, tC = 0, tD = 0, tm = 0;
+    __shared__ int ks_sh[2];
+    __shared__ double best_sh[2];
 
-    // ---- prologue: plan tables, I8 offset f0 = mean(y) ---------------
+    // ---- prologue: pool staging, plan tables, I8 offset f0 = mean(y) --------
+    if (POOL) {
+        const uint4* src = (const uint4*)p.permt;
+        uint4* dst = (uint4*)(smem + L.permt);
+        const int nv = (int)((sizeof(PermT) * (size_t)p.permt_cap) / 16);
+        for (int a = tid; a < nv; a += T) dst[a] = __ldg(src + a);
+        for (int a = tid; a < K * W * d; a += T) ((double*)(smem + L.zt))[a] = __ldg(p.ZT + a);
+        for (int a = tid; a < K * d * d; a += T) ((double*)(smem + L.ai))[a] = __ldg(p.Ainv + a);
+        for (int a = tid; a < K * d * 4; a += T) ((double*)(smem + L.cb))[a] = __ldg(p.Cb + a);
+        for (int a = tid; a < K * d; a += T) ((int32_t*)(smem + L.lw))[a] = __ldg(p.lwin + 2 * a);
+    }
+    if (p.ztab) {
+        double* zd = (double*)(smem + L.zs);
+        int32_t* jd = (int32_t*)(smem + L.zj);
+        for (int a = tid; a < K * ns; a += T) {
+            const int k = a / ns, l = a - k * ns;
+#pragma unroll
+            for (int q = 0; q < CWB_SPW; q++) zd[((size_t)k * nsp + l) * CWB_SPW + q] = __ldg(p.Zs + (size_t)a * CWB_SPW + q);
+            jd[k * nsp + l] = __ldg(p.zj0 + a);
+        }
+    }
     const int32_t* pl = p.plan;
     const int rounds = pl[1], n_comb = pl[2];
     const int RM = plan_rounds_max(KS, T);
@@ -123,158 +212,267 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     const int32_t* comb_g = wb + RM * NW;
     const int32_t* comb_first = comb_g + KS;
     const int32_t* comb_cnt = comb_first + KS;
-    for (int a = tid; a < KS; a += T) U[a] = 0.0;  // empty bins keep u = 0
-    for (int a = tid; a < K * d; a += T) agg[a] = 0.0;
-    if (tid == 0) r[n] = 0.0;
+    for (int a = tid; a < RB * (K * nsp + W); a += T) U[a] = 0.0;  // empty / padding bins keep u = 0
+    for (int a = tid; a < RB * K * d; a += T) agg[a] = 0.0;
+    for (int a = tid; a < RB * kPadRows; a += T) r[n * RB + a] = 0.0;
 
-    const double* y = p.Y + (size_t)b * n;
-    double part = 0.0;
-    bool bad = false;
-    for (int i = tid; i < n; i += T) {
-        double v = y[i];
-        bad |= !isfinite(v);
-        r[i] = v;
-        part += v;
+    double f0[RB];
+    {
+        double part[RB];
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < RB; q++) part[q] = 0.0;
+        for (int i = tid; i < n; i += T) {
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const double v = (b0 + q < p.B) ? p.Y[(size_t)(b0 + q) * n + i] : 0.0;
+                bad |= !isfinite(v);
+                r[i * RB + q] = v;
+                part[q] += v;
+            }
+        }
+        if (bad) cwb_dev_fail(p.status, CWB_ENONFINITE);
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+            part[q] = warp_sum(part[q]);
+            if (lane == 0) red[q * 32 + warp] = part[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+            double sy = 0.0;
+            for (int w = 0; w < NW; w++) sy += red[q * 32 + w];
+            f0[q] = sy / (double)n;
+            part[q] = 0.0;
+        }
+        for (int i = tid; i < n; i += T) {
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const double v = r[i * RB + q] - f0[q];
+                r[i * RB + q] = v;
+                part[q] += v * v;
+            }
+        }
+        __syncthreads();  // everyone has read red[] for f0
+#pragma unroll
+        for (int q = 0; q < RB; q++) red[(RB + q) * T + tid] = part[q];  // rr_0 -> parity 1
+        __syncthreads();
     }
-    if (bad) cwb_dev_fail(p.status, CWB_ENONFINITE);
-    part = warp_sum(part);
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    double sy = 0.0;
-    for (int w = 0; w < NW; w++) sy += red[w];
-    const double f0 = sy / (double)n;
-    part = 0.0;
-    for (int i = tid; i < n; i += T) {
-        double v = r[i] - f0;
-        r[i] = v;
-        part += v * v;
-    }
-    part = warp_sum(part);
-    __syncthreads();  // everyone has read red[] for f0
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    double rr = 0.0;
-    for (int w = 0; w < NW; w++) rr += red[w];
+    if (timed) tm = clock64();
+
+    // Bookkeeping of iteration mp for replication q (one warp): theta_agg[k*] += nu theta*
+    // (P:L838), traces k*, SSE = rr_mp - delta* and risk = rr_(mp+1) / (2n), with rr_m the
+    // per-thread partials of r^T r before the update of iteration m (parity (m+1) & 1).
+    // Runs in phase A of iteration mp + 1 on the last warps (least H1 work), off the
+    // critical path.
+    auto bookkeeping = [&](int mp, int q) {
+        const int b = b0 + q, kb = ks_sh[q];
+        if (lane < d) agg[(q * K + kb) * d + lane] += p.nu * thall[(kb * RB + q) * 32 + lane];
+        double s0 = 0.0, s1 = 0.0;
+        for (int t = lane; t < T; t += 32) {
+            s0 += red[((mp + 1) & 1) * RB * T + q * T + t];
+            s1 += red[(mp & 1) * RB * T + q * T + t];
+        }
+        const double rr0 = warp_sum(s0), rr1 = warp_sum(s1);
+        if (lane == 0 && b < p.B) {
+            if (p.k_trace) p.k_trace[(size_t)mp * p.B + b] = kb;
+            if (p.sse_trace) p.sse_trace[(size_t)mp * p.B + b] = rr0 - best_sh[q];
+            if (p.risk_trace) p.risk_trace[(size_t)mp * p.B + b] = rr1 * p.inv2n;
+        }
+    };
 
     for (int m = 0; m < p.M; m++) {
-        // ---- H1: each lane sums its task, one coalesced index load per step -------
+        if (m > 0 && warp >= NW - RB) bookkeeping(m - 1, NW - 1 - warp);
+        // ---- A / H1: each lane sums its task, 4 steps per offset load ------------------
         for (int rd = 0; rd < rounds; rd++) {
             const int steps = __ldg(wl + rd * NW + warp);  // warp-uniform
             if (steps == 0) continue;
-            const PermT* pt = permt + __ldg(wb + rd * NW + warp) + lane;
-            double acc = 0.0;
+            const PermT* pt = permt + __ldg(wb + rd * NW + warp) + lane * 4;
+            double a0[RB], a1[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) { a0[q] = 0.0; a1[q] = 0.0; }
+#pragma unroll 2
             for (int j = 0; j < steps; j += 4) {
-                const uint32_t i0 = __ldg(pt + (j + 0) * 32), i1 = __ldg(pt + (j + 1) * 32);
-                const uint32_t i2 = __ldg(pt + (j + 2) * 32), i3 = __ldg(pt + (j + 3) * 32);
-                const double v0 = r[i0], v1 = r[i1], v2 = r[i2], v3 = r[i3];
-                acc += v0; acc += v1; acc += v2; acc += v3;
+                const Off4<PermT> o = Off4<PermT>::template ld<POOL>(pt + j * 32);
+                const RV<RB> v0 = RV<RB>::ld(rb, o.o0), v1 = RV<RB>::ld(rb, o.o1);
+                const RV<RB> v2 = RV<RB>::ld(rb, o.o2), v3 = RV<RB>::ld(rb, o.o3);
+#pragma unroll
+                for (int q = 0; q < RB; q++) {
+                    a0[q] += v0[q]; a1[q] += v1[q]; a0[q] += v2[q]; a1[q] += v3[q];
+                }
             }
             const int dest = __ldg(tt_dest + rd * T + tid);
-            if (dest >= 0) U[dest] = acc;
-            else if (dest != kDiscard) pc[-dest - 1] = acc;
+            double* dp = dest >= 0 ? U + (size_t)dest * RB : (dest != kDiscard ? pc + (size_t)(-dest - 1) * RB : nullptr);
+            if (dp) {
+                if (RB == 2) *reinterpret_cast<double2*>(dp) = make_double2(a0[0] + a1[0], a0[RB - 1] + a1[RB - 1]);
+                else dp[0] = a0[0] + a1[0];
+            }
         }
         if (n_comb) {  // bins cut into pieces: combine in piece order
             __syncthreads();
             for (int c = tid; c < n_comb; c += T) {
-                const int f = __ldg(comb_first + c), cnt = __ldg(comb_cnt + c);
-                double v = pc[f];
-                for (int q = 1; q < cnt; q++) v += pc[f + q];
-                U[__ldg(comb_g + c)] = v;
-            }
-        }
-        __syncthreads();
-        // ---- H2-H4: one warp per learner, lane j = coefficient j -------------------
-        for (int k = warp; k < K; k += NW) {
-            // s_j = sum_l Zb[l][j] u[l] over the design points where B_j != 0
-            double s0 = 0.0, s1 = 0.0;
-            if (lane < d) {
-                const int lb = __ldg(p.lwin + (k * d + lane) * 2), le = __ldg(p.lwin + (k * d + lane) * 2 + 1);
-                const double* zc = p.Zb + (size_t)k * ns * d + lane;
-                const double* u = U + k * ns;
-                int l = lb;
-                for (; l + 2 <= le; l += 2) {
-                    s0 += __ldg(zc + (size_t)l * d) * u[l];
-                    s1 += __ldg(zc + (size_t)(l + 1) * d) * u[l + 1];
+                const int f = __ldg(comb_first + c), cnt = __ldg(comb_cnt + c), g = __ldg(comb_g + c);
+#pragma unroll
+                for (int q = 0; q < RB; q++) {
+                    double v = pc[f * RB + q];
+                    for (int e = 1; e < cnt; e++) v += pc[(f + e) * RB + q];
+                    U[g * RB + q] = v;
                 }
-                if (l < le) s0 += __ldg(zc + (size_t)l * d) * u[l];
-            }
-            const double s = s0 + s1;
-            // theta = A^-1 s (A^-1 symmetric: lane j reads column j of row j'), 4 chains
-            const int jl = lane < d ? lane : 0;
-            const double* Aj = p.Ainv + (size_t)k * d * d + jl;
-            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-            int jp = 0;
-            for (; jp + 4 <= d; jp += 4) {
-                const double a0 = __ldg(Aj + (jp + 0) * d), a1 = __ldg(Aj + (jp + 1) * d);
-                const double a2 = __ldg(Aj + (jp + 2) * d), a3 = __ldg(Aj + (jp + 3) * d);
-                t0 += a0 * __shfl_sync(0xffffffffu, s, jp + 0);
-                t1 += a1 * __shfl_sync(0xffffffffu, s, jp + 1);
-                t2 += a2 * __shfl_sync(0xffffffffu, s, jp + 2);
-                t3 += a3 * __shfl_sync(0xffffffffu, s, jp + 3);
-            }
-            for (; jp < d; jp++) t0 += __ldg(Aj + jp * d) * __shfl_sync(0xffffffffu, s, jp);
-            const double t = lane < d ? (t0 + t1) + (t2 + t3) : 0.0;
-            // G theta on the band |j - j'| <= 3 (G is exactly banded)
-            const double* Gk = p.G + (size_t)k * d * d;
-            double gt = 0.0;
-#pragma unroll
-            for (int o = -(CWB_SPW - 1); o <= CWB_SPW - 1; o++) {
-                const double to = __shfl_sync(0xffffffffu, t, (lane + o) & 31);
-                const int jq = lane + o;
-                if (lane < d && jq >= 0 && jq < d) gt += __ldg(Gk + jq * d + lane) * to;
-            }
-            double v = lane < d ? t * (2.0 * s - gt) : 0.0;
-            v = warp_sum(v);
-            th[k * 32 + lane] = t;
-            if (lane == 0) delta[k] = v;
-        }
-        __syncthreads();
-        // ---- H5: argmax delta (every thread, identical result) --------------------
-        int ks = 0;
-        double best = delta[0];
-        for (int k = 1; k < K; k++) {
-            const double v = delta[k];
-            if (v > best) { best = v; ks = k; }
-        }
-        // ---- H6a: fitted values at the design points, aggregation, log ------------
-        {
-            const int32_t* j0 = p.zj0 + (size_t)ks * ns;
-            const double* zs = p.Zs + (size_t)ks * ns * CWB_SPW;
-            const double* tk = th + ks * 32;
-            for (int l = tid; l < ns; l += T) {
-                const int a = __ldg(j0 + l);
-                double v = __ldg(zs + l * CWB_SPW) * tk[a];
-#pragma unroll
-                for (int q = 1; q < CWB_SPW; q++) v += __ldg(zs + l * CWB_SPW + q) * tk[a + q];
-                zhat[l] = p.nu * v;
-            }
-            for (int j = tid; j < d; j += T) agg[ks * d + j] += p.nu * tk[j];
-            if (tid == 0) {
-                if (p.k_trace) p.k_trace[(size_t)m * p.B + b] = ks;
-                if (p.sse_trace) p.sse_trace[(size_t)m * p.B + b] = rr - best;
             }
         }
         __syncthreads();
-        // ---- H6b: residual update and r^T r ----------------------------------------
-        {
-            const IdxT* ik = idx + (size_t)ks * n;
-            double acc = 0.0;
-            for (int i = tid; i < n; i += T) {
-                const double v = r[i] - zhat[__ldg(ik + i)];
-                r[i] = v;
-                acc += v * v;
+        if (timed) tm = phase_mark(&tA, tm, true);
+        // ---- B / H2-H4, one warp per learner, lane j = coefficient j:
+        //      s = Zb^T u (window of basis j), theta = (G + lambda D)^-1 s (cached inverse,
+        //      P:L846), c = C^T theta, delta = |c|^2 = 2 theta^T s - theta^T G theta ------
+        for (int k = warp; k < K; k += NW) {
+            double sv[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) sv[q] = 0.0;
+            __syncwarp();  // sS reuse
+            if (lane < d) {
+                const double* zt = ZTc + (size_t)k * W * d + lane;
+                const int lb = POOL ? ((const int32_t*)(smem + L.lw))[k * d + lane] : __ldg(p.lwin + 2 * (k * d + lane));
+                const double* uk = U + ((size_t)k * nsp + lb) * RB;
+#pragma unroll 4
+                for (int w = 0; w < W; w++) {
+                    const double z = POOL ? zt[w * d] : __ldg(zt + w * d);
+#pragma unroll
+                    for (int q = 0; q < RB; q++) sv[q] = fma(z, uk[w * RB + q], sv[q]);
+                }
             }
-            acc = warp_sum(acc);
-            if (lane == 0) red[warp] = acc;
-            __syncthreads();
-            rr = 0.0;
-            for (int w = 0; w < NW; w++) rr += red[w];
-            if (tid == 0 && p.risk_trace) p.risk_trace[(size_t)m * p.B + b] = rr / (2.0 * (double)n);
+#pragma unroll
+            for (int q = 0; q < RB; q++) sS[q * 32 + lane] = sv[q];  // lanes >= d store 0
+            __syncwarp();
+            double t0[RB], t1[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) { t0[q] = 0.0; t1[q] = 0.0; }
+            if (lane < d) {
+                const double* Ak = Ac + (size_t)k * d * d + lane;  // A^-1 symmetric: column j = row j
+                int jp = 0;
+#pragma unroll 4
+                for (; jp + 2 <= d; jp += 2) {
+                    const double a0 = POOL ? Ak[jp * d] : __ldg(Ak + jp * d);
+                    const double a1 = POOL ? Ak[(jp + 1) * d] : __ldg(Ak + (jp + 1) * d);
+#pragma unroll
+                    for (int q = 0; q < RB; q++) {
+                        const double2 s2 = *reinterpret_cast<const double2*>(sS + q * 32 + jp);
+                        t0[q] = fma(a0, s2.x, t0[q]);
+                        t1[q] = fma(a1, s2.y, t1[q]);
+                    }
+                }
+                if (jp < d) {
+                    const double a0 = POOL ? Ak[jp * d] : __ldg(Ak + jp * d);
+#pragma unroll
+                    for (int q = 0; q < RB; q++) t0[q] = fma(a0, sS[q * 32 + jp], t0[q]);
+                }
+            }
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+            if (lane < d) {
+                const double* cbj = Cbc + ((size_t)k * d + lane) * 4;
+                c0 = cbj[0]; c1 = cbj[1]; c2 = cbj[2]; c3 = cbj[3];
+            }
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const double th = t0[q] + t1[q];  // 0 on lanes >= d
+                const double h1 = __shfl_down_sync(0xffffffffu, th, 1);
+                const double h2 = __shfl_down_sync(0xffffffffu, th, 2);
+                const double h3 = __shfl_down_sync(0xffffffffu, th, 3);
+                const double c = fma(c3, h3, fma(c2, h2, fma(c1, h1, c0 * th)));
+                const double v = warp_sum(c * c);
+                thall[(k * RB + q) * 32 + lane] = th;
+                if (lane == 0) delta[k * RB + q] = v;
+            }
         }
-        __syncthreads();  // red[] / r / zhat reuse in the next iteration
+        __syncthreads();
+        if (timed) tm = phase_mark(&tB, tm, true);
+        // ---- C / H5: job (q, slice): k* = argmax delta (lowest k on ties) for
+        //      replication q, then zhat = nu Zb_k* theta_k* on design points slice*32 + lane ------
+        {
+            const int nslice = (ns + 31) >> 5;
+            for (int job = warp; job < RB * nslice; job += NW) {
+                const int q = job % RB, sl = job / RB;
+                double best = -INFINITY;
+                int kb = 0;
+                for (int k = lane; k < K; k += 32) {
+                    const double v = delta[k * RB + q];
+                    if (v > best) { best = v; kb = k; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
+                    if (ob > best || (ob == best && ok < kb)) { best = ob; kb = ok; }
+                }
+                const int l = sl * 32 + lane;
+                if (l < ns) {
+                    const double* tk = thall + (kb * RB + q) * 32;
+                    const int a = zj0_c[(size_t)kb * zstride + l];
+                    const double2* zs = reinterpret_cast<const double2*>(Zs_c + ((size_t)kb * zstride + l) * CWB_SPW);
+                    const double2 za = zs[0], zb = zs[1];
+                    double v = za.x * tk[a];
+                    if (a + 1 < d) v += za.y * tk[a + 1];
+                    if (a + 2 < d) v += zb.x * tk[a + 2];
+                    if (a + 3 < d) v += zb.y * tk[a + 3];
+                    zhat[q * nsp + l] = p.nu * v;
+                }
+                if (sl == 0 && lane == 0) { ks_sh[q] = kb; best_sh[q] = best; }
+            }
+        }
+        __syncthreads();
+        if (timed) tm = phase_mark(&tC, tm, true);
+        // ---- D / H6: r_i -= zhat[idx_k*(i)], per-thread r^T r partials -------------
+        {
+            const int parw = m & 1;
+            const IdxT* ik0 = idx + (size_t)ks_sh[0] * n;
+            const IdxT* ik1 = idx + (size_t)ks_sh[RB - 1] * n;
+            double acc[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) acc[q] = 0.0;
+            for (int i0 = tid; i0 < n; i0 += 4 * T) {
+                uint32_t j0[4], j1[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const int i = i0 + e * T;
+                    j0[e] = i < n ? (uint32_t)__ldg(ik0 + i) : 0u;
+                    j1[e] = (RB == 2 && i < n) ? (uint32_t)__ldg(ik1 + i) : 0u;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const int i = i0 + e * T;
+                    if (i < n) {
+                        if (RB == 1) {
+                            const double v = r[i] - zhat[j0[e]];
+                            r[i] = v;
+                            acc[0] = fma(v, v, acc[0]);
+                        } else {
+                            double2 v = *reinterpret_cast<double2*>(r + 2 * i);
+                            v.x -= zhat[j0[e]];
+                            v.y -= zhat[nsp + j1[e]];
+                            *reinterpret_cast<double2*>(r + 2 * i) = v;
+                            acc[0] = fma(v.x, v.x, acc[0]);
+                            acc[RB - 1] = fma(v.y, v.y, acc[RB - 1]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RB; q++) red[(parw * RB + q) * T + tid] = acc[q];
+        }
+        __syncthreads();
+        if (timed) tm = phase_mark(&tD, tm, true);
     }
-    for (int a = tid; a < K * d; a += T) p.agg_out[(size_t)b * K * d + a] = agg[a];
-    if (tid == 0 && p.offset_out) p.offset_out[b] = f0;
+    if (p.M > 0 && warp >= NW - RB) bookkeeping(p.M - 1, NW - 1 - warp);
+    __syncthreads();  // agg complete
+#pragma unroll
+    for (int q = 0; q < RB; q++)
+        if (b0 + q < p.B) {
+            for (int a = tid; a < K * d; a += T) p.agg_out[(size_t)(b0 + q) * K * d + a] = agg[q * K * d + a];
+            if (tid == 0 && p.offset_out) p.offset_out[b0 + q] = f0[q];
+        }
+    if (timed) {
+        p.timing[0] = tA; p.timing[1] = tB; p.timing[2] = tC; p.timing[3] = tD;
+    }
 }
 
 // ------------------------------------------------------------- plan kernel
@@ -317,14 +515,81 @@ __device__ int block_scan_excl(int* a, int N, int* wsum) {
     return total;
 }
 
+// Greedy bank-conflict-free schedule of one lane group (G lanes that share a
+// shared-memory wavefront: G = 16 for 8-byte rows, 8 for 16-byte rows).  Colour
+// of a row = its bank group (row mod G).  Every step each lane emits one row
+// of its task or a zero padding row, and the G rows of a step have distinct
+// colours, so each gather instruction is conflict-free.  Lanes are served
+// longest-remaining first; a lane takes the free colour it holds most rows
+// of.  The longest lane always gets a row, so the step count is the longest
+// task of the group.  write = false only counts the steps.
+template <typename PermT>
+__device__ int schedule_group(int G, int rd, int th0, int T, int n, int stride, bool write, int steps_total,
+                              const int32_t* s_tos, const int32_t* s_start, const int32_t* cs,
+                              const int32_t* srt, const int32_t* wb, PermT* permt) {
+    int task[16], tot[16];
+    int rem[16][16];
+    const int NW = T / 32;
+    for (int L = 0; L < G; L++) {
+        const int t = s_tos[rd * T + th0 + L];
+        task[L] = t;
+        tot[L] = 0;
+        for (int c = 0; c < G; c++) {
+            rem[L][c] = t >= 0 ? cs[t * 17 + c + 1] - cs[t * 17 + c] : 0;
+            tot[L] += rem[L][c];
+        }
+    }
+    int steps = 0;
+    for (;;) {
+        bool any = false;
+        for (int L = 0; L < G; L++) any |= tot[L] > 0;
+        if (!any && (!write || steps >= steps_total)) break;
+        unsigned freec = (1u << G) - 1u, picked = 0u;
+        int row_of[16];
+        for (int L = 0; L < G; L++) row_of[L] = -1;
+        for (int it = 0; it < G && any; it++) {
+            int bl = -1, bv = 0;
+            for (int L = 0; L < G; L++)
+                if (!((picked >> L) & 1u) && tot[L] > bv) { bv = tot[L]; bl = L; }
+            if (bl < 0) break;
+            picked |= 1u << bl;
+            int bc = -1, bn = 0;
+            for (int c = 0; c < G; c++)
+                if (((freec >> c) & 1u) && rem[bl][c] > bn) { bn = rem[bl][c]; bc = c; }
+            if (bc < 0) continue;  // only taken colours left: padding this step
+            freec &= ~(1u << bc);
+            const int t = task[bl];
+            const int cnt = cs[t * 17 + bc + 1] - cs[t * 17 + bc];
+            row_of[bl] = srt[s_start[t] + cs[t * 17 + bc] + (cnt - rem[bl][bc])];
+            rem[bl][bc]--;
+            tot[bl]--;
+        }
+        if (write) {
+            for (int L = 0; L < G; L++) {
+                int row = row_of[L];
+                if (row < 0) {  // zero padding row of a free colour
+                    const int c = __ffs(freec) - 1;
+                    freec &= freec - 1u;
+                    row = n + (((c - n) % G) + G) % G;
+                }
+                const int th = th0 + L, w = th >> 5, ln = th & 31;
+                permt[(size_t)wb[rd * NW + w] + (size_t)(steps >> 2) * 128 + ln * 4 + (steps & 3)] = (PermT)(stride * row);
+            }
+        }
+        steps++;
+    }
+    return steps;
+}
+
 // One block.  Cuts every non-empty bin into ceil(count / P) tasks, sorts the
 // tasks by length (descending, ties by bin order; coarse buckets), deals them
-// to the T threads of the fused kernel in snake order and writes the row ids
-// of every warp's 32 tasks step-major into permt.  Deterministic; runs once
-// per data set inside cwb_init.
+// to the T threads of the fused kernel in snake order, and writes for every
+// warp and round a conflict-free gather schedule (schedule_group) of byte
+// offsets into permt ([step/4][lane][4]).  Deterministic; runs once per
+// (data set, RB, T).
 template <typename PermT, typename SrcPermT>
 __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __restrict__ perm, int K, int ns,
-                             int n, int T, int P, size_t permt_cap, int32_t* __restrict__ plan,
+                             int nsp, int n, int T, int P, int stride, int G, int32_t* __restrict__ plan,
                              int32_t* __restrict__ scratch, PermT* __restrict__ permt, const int* status) {
     extern __shared__ int psm[];
     __shared__ int wsum[33];
@@ -349,6 +614,9 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
     int32_t* s_dest = s_len + n_tasks_max;
     int32_t* s_bkt = s_dest + n_tasks_max;
     int32_t* s_slot = s_bkt + n_tasks_max;  // rd * T + thread of each task
+    int32_t* s_tos = s_slot + n_tasks_max;  // task of each (rd, thread) slot, -1: none
+    int32_t* cs = s_tos + RM * T;           // per task: 17 colour offsets
+    int32_t* srt = cs + 17 * (size_t)n_tasks_max;  // task rows sorted by colour (K*n)
     for (int g = tid; g < KS; g += nthr) {
         const int k = g / ns, l = g - k * ns;
         const int c = off[k * (ns + 1) + l + 1] - off[k * (ns + 1) + l];
@@ -358,9 +626,8 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
         slot[g] = pc > 1 ? pc : 0;
         cidx[g] = pc > 1 ? 1 : 0;
     }
-    for (int e = tid; e < RM * T; e += nthr) tt_dest[e] = kDiscard;
+    for (int e = tid; e < RM * T; e += nthr) { tt_dest[e] = kDiscard; s_tos[e] = -1; }
     for (int e = tid; e < 2 * RM * NW; e += nthr) wl[e] = 0;
-    for (size_t e = tid; e < permt_cap; e += nthr) permt[e] = (PermT)n;  // padding row
     for (int e = tid; e < 1024; e += nthr) { hist[e] = 0; run_b[e] = 0; }
     __syncthreads();
     const int n_tasks = block_scan_excl(first, KS, wsum);
@@ -371,8 +638,9 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
         const int pc = pcs[g];
         if (pc == 0) continue;
         const int a0 = off[k * (ns + 1) + l], c = off[k * (ns + 1) + l + 1] - a0;
+        const int ug = k * nsp + l;  // u index (rows of U padded to nsp)
         if (pc > 1) {
-            comb_g[cidx[g]] = g;
+            comb_g[cidx[g]] = ug;
             comb_first[cidx[g]] = slot[g];
             comb_cnt[cidx[g]] = pc;
         }
@@ -383,13 +651,25 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
             const int t = first[g] + q;
             s_start[t] = st;
             s_len[t] = len;
-            s_dest[t] = pc == 1 ? g : -(slot[g] + q) - 1;
+            s_dest[t] = pc == 1 ? ug : -(slot[g] + q) - 1;
             const int bk = (int)(((long long)len * 1024) / (P + 1));
             s_bkt[t] = 1023 - min(1023, bk);  // ascending key = descending length
             st += len;
         }
     }
     __syncthreads();
+    for (int t = tid; t < n_tasks; t += nthr) {  // rows of every task grouped by colour (stable)
+        const int st = s_start[t], len = s_len[t];
+        int cnt[17];
+        for (int c = 0; c <= G; c++) cnt[c] = 0;
+        for (int q = 0; q < len; q++) cnt[(int)perm[st + q] % G + 1]++;
+        for (int c = 0; c < G; c++) cnt[c + 1] += cnt[c];
+        for (int c = 0; c <= G; c++) cs[t * 17 + c] = cnt[c];
+        for (int q = 0; q < len; q++) {
+            const int row = (int)perm[st + q];
+            srt[st + cnt[row % G]++] = row;
+        }
+    }
     for (int t = tid; t < n_tasks; t += nthr) atomicAdd(&hist[s_bkt[t]], 1u);
     __syncthreads();
     if (tid < 32) {  // exclusive scan of the 1024 bucket counts (one warp, 32 per lane)
@@ -416,17 +696,25 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
             const unsigned mask = __match_any_sync(0xffffffffu, bk);
             const unsigned lt = mask & ((1u << tid) - 1u);
             if (valid) {
-                const int srt = (int)(hist[bk] + run_b[bk] + __popc(lt));
-                const int rd = srt / T, i = srt - rd * T;
+                const int srk = (int)(hist[bk] + run_b[bk] + __popc(lt));
+                const int rd = srk / T, i = srk - rd * T;
                 const int th = (rd & 1) ? (T - 1 - i) : i;
                 tt_dest[rd * T + th] = s_dest[t];
                 s_slot[t] = rd * T + th;
-                atomicMax(&wl[rd * NW + th / 32], (s_len[t] + 3) / 4 * 4);
+                s_tos[rd * T + th] = t;
             }
             __syncwarp();
             if (valid && lt == 0) run_b[bk] += __popc(mask);
             __syncwarp();
         }
+    }
+    __syncthreads();
+    const int groups = RM * T / G;
+    for (int gi = tid; gi < groups; gi += nthr) {  // steps per lane group -> per warp
+        const int rd = gi / (T / G), th0 = (gi - rd * (T / G)) * G;
+        const int st = schedule_group<PermT>(G, rd, th0, T, n, stride, false, 0, s_tos, s_start, cs, srt, wb,
+                                             permt);
+        if (st) atomicMax(&wl[rd * NW + th0 / 32], (st + 3) / 4 * 4);
     }
     __syncthreads();
     if (tid == 0) {  // block offsets, round count
@@ -445,126 +733,189 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
         plan[6] = plan[7] = 0;
     }
     __syncthreads();
-    // row ids step-major; inside a task rows are ordered by shared-memory bank
-    // pair (row mod 16) rotated by the lane, ties by bin-sorted position
-    for (int t = tid; t < n_tasks; t += nthr) {
-        const int sl = s_slot[t], rd = sl / T, thd = sl - rd * T, ln = thd & 31;
-        PermT* out = permt + wb[rd * NW + thd / 32] + ln;
-        const int st = s_start[t], len = s_len[t];
-        int pos[16];
-        for (int q = 0; q < 16; q++) pos[q] = 0;
-        for (int q = 0; q < len; q++) pos[(((int)perm[st + q] & 15) - (ln & 15)) & 15]++;
-        for (int q = 0, run = 0; q < 16; q++) { const int c = pos[q]; pos[q] = run; run += c; }
-        for (int q = 0; q < len; q++) {  // stable counting sort by rotated bank pair
-            const int row = (int)perm[st + q];
-            out[(size_t)(pos[((row & 15) - (ln & 15)) & 15]++) * 32] = (PermT)row;
-        }
+    for (int gi = tid; gi < groups; gi += nthr) {  // write the schedules
+        const int rd = gi / (T / G), th0 = (gi - rd * (T / G)) * G;
+        const int w = th0 / 32;
+        if (wl[rd * NW + w] == 0) continue;
+        schedule_group<PermT>(G, rd, th0, T, n, stride, true, wl[rd * NW + w], s_tos, s_start, cs, srt, wb, permt);
     }
 }
 
-template <typename IdxT, typename PermT, int MAXT, int MINB>
-int launch_t(const FusedParams& fp, size_t smem, cudaStream_t s) {
-    auto kern = k_train_fused<IdxT, PermT, MAXT, MINB>;
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB>
+int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
+    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -1;
-    kern<<<fp.B, fp.T, smem, s>>>(fp);
+    const int grid = (fp.B + RB - 1) / RB;
+    kern<<<grid, T, smem, s>>>(fp);
     return 0;
 }
 
 template <typename IdxT, typename PermT>
-int launch_sel(const FusedParams& fp, size_t smem, cudaStream_t s) {
-    if (fp.T <= 384) return launch_t<IdxT, PermT, 384, 2>(fp, smem, s);
-    return launch_t<IdxT, PermT, 768, 1>(fp, smem, s);
+int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s) {
+    if (RB == 2) {
+        if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1>(fp, T, smem, s);
+        return launch_t<IdxT, PermT, 2, false, 512, 1>(fp, T, smem, s);
+    }
+    if (T <= 384) {
+        if (pool) return launch_t<IdxT, PermT, 1, true, 384, 2>(fp, T, smem, s);
+        return launch_t<IdxT, PermT, 1, false, 384, 2>(fp, T, smem, s);
+    }
+    if (pool) return launch_t<IdxT, PermT, 1, true, 768, 1>(fp, T, smem, s);
+    return launch_t<IdxT, PermT, 1, false, 768, 1>(fp, T, smem, s);
 }
 
 }  // namespace
 
 static const size_t kMaxSmem = 227 * 1024;
-static const size_t kTwoCtaSmem = 112 * 1024;
+static const size_t kTwoCtaSmem = 113 * 1024;
 
-// Threads per CTA; false when the fused kernel cannot hold the working set.
-static bool fused_shape(const cwb_ctx* c, int* T_out, size_t* smem_out) {
+struct FusedShape {
+    int RB = 0, T = 0, P = 0, permt_bytes = 2;
+    bool pool = false;
+    size_t cap = 0, smem = 0;
+};
+
+// Launch shape for B replications: RB replications per CTA, T threads, pool
+// tables in shared memory or not.  false when the residuals do not fit.
+static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
     if ((int64_t)c->K * c->n + 8 > INT32_MAX) return false;
     if ((int64_t)c->K * c->n_star * 16 > 200 * 1024) return false;  // plan kernel shared memory
-    const int T_small = std::min(384, std::max(256, 32 * c->K));
-    const int T_large = std::min(768, std::max(256, 32 * c->K));
-    for (int pass = 0; pass < 2; pass++) {
-        const int T = pass == 0 ? T_small : T_large;
-        SmemLayout L((int)c->n, c->K, c->n_star, c->d, T, 2 * T);
-        const size_t lim = pass == 0 ? kTwoCtaSmem : kMaxSmem;
-        if (L.total <= lim) {
-            *T_out = T;
-            *smem_out = L.total;
-            return true;
+    const int KS = c->K * c->n_star;
+    struct Cand { int RB, T; size_t lim; };
+    Cand cands[4];
+    int nc = 0;
+    const int nsm = 148;
+    if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};                     // ~2 replications per SM: one CTA
+    if (B > nsm) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
+    cands[nc++] = {1, c->n >= 8192 ? 768 : 512, kMaxSmem};
+    for (int i = 0; i < nc; i++) {
+        FusedShape f;
+        f.RB = cands[i].RB;
+        f.T = cands[i].T;
+        const int64_t stride = 8 * f.RB;
+        f.permt_bytes = stride * (c->n + kPadRows) <= 65535 ? 2 : 4;
+        // task size: balance the K*n rows over T threads, but do not cut bins of up to
+        // 1.6x the mean bin size (a cut bin costs a combine pass)
+        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
+        f.cap = permt_bound(KS, f.T, f.P);
+        for (int pool = 1; pool >= 0; pool--) {
+            SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, false);
+            if (L.total <= cands[i].lim) {
+                f.pool = pool != 0;
+                f.smem = L.total;
+                *out = f;
+                return true;
+            }
         }
     }
     return false;
 }
 
 size_t cwb_fused_smem_bytes(const cwb_ctx* c) {
-    int T;
-    size_t smem;
-    return fused_shape(c, &T, &smem) ? smem : (size_t)-1;
+    FusedShape f;
+    return fused_shape(c, 1, &f) ? f.smem : (size_t)-1;
 }
 
-int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
-    int T;
-    size_t smem;
+// (Re)builds the H1 task plan for the shape of a B-replication launch.
+static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
+    if (c->fused_T == f.T && c->fused_rb == f.RB && c->plan) return CWB_OK;
+    cwb_release(c->plan, s);
+    cwb_release(c->permt, s);
+    c->plan = nullptr;
+    c->permt = nullptr;
     c->fused_T = 0;
-    if (!fused_shape(c, &T, &smem)) return CWB_OK;
-    const int KS = c->K * c->n_star;
-    const int total = (int)(c->K * c->n);
-    const int P = std::max(4, (total + T - 1) / T);
-    const size_t scratch_ints = 5 * (size_t)(KS + 2 * T);
-    const size_t cap = permt_bound(KS, T, P);
-    c->permt_bytes = c->n <= 65534 ? 2 : 4;
+    const int KS = c->K * c->n_star, T = f.T;
+    const size_t scratch_ints = 22 * (size_t)(KS + 2 * T) + (size_t)plan_rounds_max(KS, T) * T + (size_t)c->K * c->n;
     if (cwb_alloc((void**)&c->plan, sizeof(int32_t) * (plan_ints(KS, T) + scratch_ints), s) != cudaSuccess ||
-        cwb_alloc(&c->permt, (size_t)c->permt_bytes * cap, s) != cudaSuccess)
+        cwb_alloc(&c->permt, (size_t)f.permt_bytes * f.cap + 16, s) != cudaSuccess)
         return cwb_set_error(c, CWB_ENOMEM, "fused plan allocation failed");
     const size_t psmem = sizeof(int) * 4 * (size_t)KS;
     int32_t* scratch = c->plan + plan_ints(KS, T);
-#define PLAN_CASE(PT, ST)                                                                              \
-    {                                                                                                  \
-        auto kern = k_fused_plan<PT, ST>;                                                              \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);           \
-        kern<<<1, 1024, psmem, s>>>(c->off, (const ST*)c->perm, c->K, c->n_star, (int)c->n, T, P, cap, \
-                                    c->plan, scratch, (PT*)c->permt, c->d_status);                      \
+    const int stride = 8 * f.RB;
+#define PLAN_CASE(PT, ST)                                                                                \
+    {                                                                                                    \
+        auto kern = k_fused_plan<PT, ST>;                                                                \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);             \
+        kern<<<1, 1024, psmem, s>>>(c->off, (const ST*)c->perm, c->K, c->n_star, c->nsp, (int)c->n, T, f.P, \
+                                    stride, 16 / f.RB, c->plan, scratch, (PT*)c->permt, c->d_status);    \
     }
-    if (c->permt_bytes == 2 && c->perm_bytes == 2) PLAN_CASE(uint16_t, uint16_t)
-    else if (c->permt_bytes == 2) PLAN_CASE(uint16_t, uint32_t)
+    if (f.permt_bytes == 2 && c->perm_bytes == 2) PLAN_CASE(uint16_t, uint16_t)
+    else if (f.permt_bytes == 2) PLAN_CASE(uint16_t, uint32_t)
     else if (c->perm_bytes == 2) PLAN_CASE(uint32_t, uint16_t)
     else PLAN_CASE(uint32_t, uint32_t)
 #undef PLAN_CASE
     c->launches++;
+    int rc = cwb_check_launch(c, "k_fused_plan");
+    if (rc) return rc;
+    // exact schedule size (one host sync per plan build): sizes the shared-memory copy
+    int32_t hdr[8] = {0};
+    int dev_status = 0;
+    CWB_CUDA_TRY(c, cudaMemcpyAsync(hdr, c->plan, sizeof(hdr), cudaMemcpyDeviceToHost, s));
+    CWB_CUDA_TRY(c, cudaMemcpyAsync(&dev_status, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CWB_CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (dev_status) return CWB_OK;  // reported by cwb_status
+    if ((size_t)hdr[5] > f.cap) return cwb_set_error(c, CWB_ECUDA, "fused plan exceeds its bound");
     c->fused_T = T;
-    c->fused_chunk = P;
-    c->fused_smem = smem;
-    return cwb_check_launch(c, "k_fused_plan");
+    c->fused_rb = f.RB;
+    c->permt_bytes = f.permt_bytes;
+    c->permt_entries = hdr[5];
+    c->plan_multi = hdr[3];
+    return CWB_OK;
+}
+
+int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
+    // built lazily by the first cwb_train (the shape depends on B)
+    (void)c; (void)s;
+    return CWB_OK;
 }
 
 int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
                     double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
                     cudaStream_t s, bool* launched) {
     *launched = false;
-    if (c->fused_T == 0) return CWB_OK;  // does not fit: caller uses the general path
+    FusedShape f;
+    if (!fused_shape(c, B, &f)) return CWB_OK;  // does not fit: caller uses the general path
+    int rc = fused_plan(c, f, s);
+    if (rc) return rc;
+    if (c->fused_T != f.T) return CWB_OK;  // plan failed on the device: cwb_status reports it
+    // pool staging levels with the exact schedule size: schedule + B tables, then Zs / zj0
+    const size_t lim = (f.RB == 1 && f.T <= 384) ? kTwoCtaSmem : kMaxSmem;
+    const size_t pbytes = ((size_t)c->permt_entries * f.permt_bytes + 15) / 16 * 16;
+    f.pool = false;
+    const int nm = c->plan_multi;
+    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, false).total;
+    bool ztab = false;
+    for (int lvl = 2; lvl >= 1; lvl--) {
+        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, lvl == 2);
+        if (L1.total <= lim) {
+            f.pool = true;
+            ztab = lvl == 2;
+            f.smem = L1.total;
+            break;
+        }
+    }
     FusedParams fp;
-    fp.n = (int)c->n; fp.K = c->K; fp.ns = c->n_star; fp.d = c->d; fp.M = M; fp.B = B; fp.nu = nu;
-    fp.T = c->fused_T;
-    fp.n_multi = 2 * c->fused_T;
+    fp.n = (int)c->n; fp.K = c->K; fp.ns = c->n_star; fp.nsp = c->nsp; fp.d = c->d; fp.M = M; fp.B = B; fp.nu = nu;
+    fp.n_multi = c->plan_multi;
+    fp.ztab = ztab ? 1 : 0;
+    fp.permt_cap = (int)(pbytes / f.permt_bytes);
     fp.Y = Y; fp.idx = c->idx; fp.permt = c->permt; fp.plan = c->plan; fp.zj0 = c->zj0; fp.Zs = c->Zs;
-    fp.Zb = c->Zb; fp.lwin = c->lwin; fp.Ainv = c->Ainv; fp.G = c->G;
+    fp.inv2n = 1.0 / (2.0 * (double)c->n);
+    fp.ZT = c->ZT; fp.lwin = c->lwin; fp.Ainv = c->Ainv; fp.Cb = c->Cb; fp.W = c->W;
     fp.offset_out = offset_out; fp.agg_out = theta_agg_out;
     fp.k_trace = k_trace; fp.sse_trace = sse_trace; fp.risk_trace = risk_trace;
+    fp.timing = c->timing;
     fp.status = c->d_status;
-    const size_t smem = c->fused_smem;
-    int rc;
-    const bool i8 = c->idx_bytes == 1, p16 = c->permt_bytes == 2;
-    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, smem, s);
-    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, smem, s);
-    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, smem, s);
-    else rc = launch_sel<uint16_t, uint32_t>(fp, smem, s);
+    const bool i8 = c->idx_bytes == 1, p16 = f.permt_bytes == 2;
+    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s);
     if (rc) return cwb_set_error(c, CWB_ECUDA, "fused kernel: cannot set shared memory size");
     c->launches++;
+    c->fused_smem = f.smem;
+    c->fused_pool = f.pool;
     *launched = true;
     return cwb_check_launch(c, "k_train_fused");
 }

@@ -398,7 +398,7 @@ __device__ LamEval lam_eval(double t, int d, double target, int kind, double (*G
 }
 
 __global__ void k_lambda(const double* __restrict__ Gall, int d, double target, int kind,
-                         double* lambda_out, double* Ainv_out, int* status) {
+                         double* lambda_out, double* Ainv_out, double* Cb_out, int* status) {
     __shared__ double Gs[CWB_MAX_D][DS], Dm[CWB_MAX_D][DS], Xs[CWB_MAX_D][DS], Ys[CWB_MAX_D][DS];
     __shared__ double Lb[CWB_MAX_D * 4], inv[CWB_MAX_D];
     if (status && *status) return;
@@ -451,10 +451,36 @@ __global__ void k_lambda(const double* __restrict__ Gall, int d, double target, 
     // cached inverse: columns of A^-1 by banded solves, symmetrised
     if (i < d) band_solve(d, Lb, inv, [&](int j) { return j == i ? 1.0 : 0.0; }, Xs, i);
     __syncwarp();
-    if (i == 0) lambda_out[k] = exp(t);
+    const double lam = exp(t);
+    if (i == 0) lambda_out[k] = lam;
     if (i < d)
         for (int c = 0; c < d; c++)
             Ainv_out[((size_t)k * d + i) * d + c] = 0.5 * (Xs[i][c] + Xs[c][i]);
+    // Selection factor: C C^T = G + 2 lambda D (banded Cholesky), so that for theta = A^-1 s
+    // 2 theta^T s - theta^T G theta = theta^T (2A - G) theta = |C^T theta|^2.
+    __shared__ bool s_ok2;
+    band_factor(2.0 * lam, d, Gs, Dm, Lb, inv, &s_ok2);
+    if (!s_ok2) {
+        if (i == 0) cwb_dev_fail(status, CWB_ECALIB);
+        return;
+    }
+    if (i < d)
+        for (int q = 0; q < 4; q++)  // Cb[j][q] = C[j+q][j] (Lb[row*4 + q] = C[row][row-q])
+            Cb_out[((size_t)k * d + i) * 4 + q] = (q <= BW && i + q < d) ? Lb[(i + q) * 4 + q] : 0.0;
+}
+
+// Windows of the basis functions: ZT[k][w][j] = Zb[k][lb_j + w][j] for the design points
+// lb_j <= l < le_j where B_j(z_l) can be non-zero (lwin), zero-padded to W.
+__global__ void k_zt(const double* __restrict__ Zb, const int32_t* __restrict__ lwin, int ns, int d, int W,
+                     double* __restrict__ ZT, int* status) {
+    if (status && *status) return;
+    const int k = blockIdx.x;
+    for (int e = threadIdx.x; e < W * d; e += blockDim.x) {
+        const int w = e / d, j = e - w * d;
+        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+        if (w == 0 && le - lb > W) cwb_dev_fail(status, CWB_EUNSUPPORTED);
+        ZT[((size_t)k * W + w) * d + j] = (lb + w < le) ? Zb[((size_t)k * ns + lb + w) * d + j] : 0.0;
+    }
 }
 
 }  // namespace
@@ -528,7 +554,8 @@ int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
     k_basis<<<K, 128, sizeof(int32_t) * ns, s>>>(c->z, c->lo, c->hi, ns, c->degree, c->n_knots, d,
                                                  c->Zb, c->zj0, c->Zs, c->lwin, c->d_status);
     k_gram<<<K, 256, 0, s>>>(c->Zb, c->cnt, ns, d, c->lwin, c->G, c->d_status);
-    k_lambda<<<K, 32, 0, s>>>(c->G, d, c->df, c->df_kind, c->lambda, c->Ainv, c->d_status);
-    c->launches += 3;
+    k_lambda<<<K, 32, 0, s>>>(c->G, d, c->df, c->df_kind, c->lambda, c->Ainv, c->Cb, c->d_status);
+    k_zt<<<K, 256, 0, s>>>(c->Zb, c->lwin, ns, d, c->W, c->ZT, c->d_status);
+    c->launches += 4;
     return cwb_check_launch(c, "pool kernels");
 }

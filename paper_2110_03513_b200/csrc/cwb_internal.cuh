@@ -64,13 +64,21 @@ struct cwb_ctx {
     double* G = nullptr;      // K x d x d   Zb^T diag(cnt) Zb
     double* Ainv = nullptr;   // K x d x d   (G + lambda D)^-1
     double* lambda = nullptr; // K
+    // selection tables: with C C^T = G + 2 lambda D (banded Cholesky),
+    //   s = Zb^T u,  theta = (G + lambda D)^-1 s,  delta = 2 theta^T s - theta^T G theta = |C^T theta|^2
+    double* Cb = nullptr;     // K x d x 4   Cb[k][j][i] = C[j+i][j]
+    double* ZT = nullptr;     // K x W x d   ZT[k][w][j] = Zb[k][lb_j + w][j] (basis j's window)
+    int32_t W = 0;            // window length bound
+    int32_t nsp = 0;
 
     // fused-kernel plan (k_fused_plan): threads per CTA, positions per thread
     int32_t* plan = nullptr;
     void* permt = nullptr;       // step-major task row ids (uint16 / uint32)
     int32_t permt_bytes = 2;
-    int32_t fused_T = 0, fused_chunk = 0;
+    int32_t fused_T = 0, fused_rb = 0, permt_entries = 0, plan_multi = 0;
+    bool fused_pool = false;
     size_t fused_smem = 0;
+    long long* timing = nullptr;  // optional device buffer: fused-kernel phase cycles (cwb_set_timing)
 
     cwb_train_ws ws;
 };

@@ -22,7 +22,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
            "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_fit_host", "cwb_predict",
-           "cwb_launch_count", "cwb_free"]
+           "cwb_launch_count", "cwb_set_phase_timing", "cwb_free"]
 
 
 class CwbError(RuntimeError):
@@ -83,6 +83,7 @@ def load() -> C.CDLL:
     L.cwb_fit_host.argtypes = [_vp, _i64, _i32, C.POINTER(cwb_config), _vp, _i32, _f64, _i32,
                                _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_predict.argtypes = [_vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp]
+    L.cwb_set_phase_timing.argtypes = [_vp, _vp]
     L.cwb_launch_count.argtypes = [_vp]
     L.cwb_launch_count.restype = C.c_int64
     L.cwb_free.argtypes = [_vp]
@@ -283,6 +284,11 @@ def cwb_launch_count(ctx) -> int:
     return int(load().cwb_launch_count(ctx))
 
 
+def cwb_set_phase_timing(ctx, cycles4=None) -> None:
+    """cycles4: int64 CUDA tensor of 4 elements (or None to switch off)."""
+    _chk(load().cwb_set_phase_timing(ctx, _ptr(cycles4)), ctx)
+
+
 def cwb_free(ctx) -> None:
     if ctx:
         load().cwb_free(ctx)
@@ -315,6 +321,9 @@ class Pool:
 
     def pool(self):
         return cwb_get_pool(self.ctx)
+
+    def set_phase_timing(self, cycles4=None):
+        cwb_set_phase_timing(self.ctx, cycles4)
 
     def launches(self):
         return cwb_launch_count(self.ctx)
