@@ -291,15 +291,32 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             double a0[RB], a1[RB];
 #pragma unroll
             for (int q = 0; q < RB; q++) { a0[q] = 0.0; a1[q] = 0.0; }
-#pragma unroll 2
-            for (int j = 0; j < steps; j += 4) {
-                const Off4<PermT> o = Off4<PermT>::template ld<POOL>(pt + j * 32);
-                const RV<RB> v0 = RV<RB>::ld(rb, o.o0), v1 = RV<RB>::ld(rb, o.o1);
-                const RV<RB> v2 = RV<RB>::ld(rb, o.o2), v3 = RV<RB>::ld(rb, o.o3);
+            // software pipeline: the offsets of groups g+2, g+3 load while groups g, g+1 gather
+            const int ng = steps >> 2;  // groups of 4 steps
+            Off4<PermT> oa = Off4<PermT>::template ld<POOL>(pt);
+            Off4<PermT> ob = ng > 1 ? Off4<PermT>::template ld<POOL>(pt + 128) : oa;
+            for (int g = 0; g < ng; g += 2) {
+                Off4<PermT> na = oa, nb = ob;
+                if (g + 2 < ng) na = Off4<PermT>::template ld<POOL>(pt + (g + 2) * 128);
+                if (g + 3 < ng) nb = Off4<PermT>::template ld<POOL>(pt + (g + 3) * 128);
+                const RV<RB> v0 = RV<RB>::ld(rb, oa.o0), v1 = RV<RB>::ld(rb, oa.o1);
+                const RV<RB> v2 = RV<RB>::ld(rb, oa.o2), v3 = RV<RB>::ld(rb, oa.o3);
+                if (g + 1 < ng) {
+                    const RV<RB> v4 = RV<RB>::ld(rb, ob.o0), v5 = RV<RB>::ld(rb, ob.o1);
+                    const RV<RB> v6 = RV<RB>::ld(rb, ob.o2), v7 = RV<RB>::ld(rb, ob.o3);
 #pragma unroll
-                for (int q = 0; q < RB; q++) {
-                    a0[q] += v0[q]; a1[q] += v1[q]; a0[q] += v2[q]; a1[q] += v3[q];
+                    for (int q = 0; q < RB; q++) {
+                        a0[q] += v0[q]; a1[q] += v1[q]; a0[q] += v2[q]; a1[q] += v3[q];
+                        a0[q] += v4[q]; a1[q] += v5[q]; a0[q] += v6[q]; a1[q] += v7[q];
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < RB; q++) {
+                        a0[q] += v0[q]; a1[q] += v1[q]; a0[q] += v2[q]; a1[q] += v3[q];
+                    }
                 }
+                oa = na;
+                ob = nb;
             }
             const int dest = __ldg(tt_dest + rd * T + tid);
             double* dp = dest >= 0 ? U + (size_t)dest * RB : (dest != kDiscard ? pc + (size_t)(-dest - 1) * RB : nullptr);
