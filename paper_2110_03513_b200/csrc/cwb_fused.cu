@@ -532,82 +532,15 @@ __device__ int block_scan_excl(int* a, int N, int* wsum) {
     return total;
 }
 
-// Greedy bank-conflict-free schedule of one lane group (G lanes that share a
-// shared-memory wavefront: G = 16 for 8-byte rows, 8 for 16-byte rows).  Colour
-// of a row = its bank group (row mod G).  Every step each lane emits one row
-// of its task or a zero padding row, and the G rows of a step have distinct
-// colours, so each gather instruction is conflict-free.  Lanes are served
-// longest-remaining first; a lane takes the free colour it holds most rows
-// of.  The longest lane always gets a row, so the step count is the longest
-// task of the group.  write = false only counts the steps.
-template <typename PermT>
-__device__ int schedule_group(int G, int rd, int th0, int T, int n, int stride, bool write, int steps_total,
-                              const int32_t* s_tos, const int32_t* s_start, const int32_t* cs,
-                              const int32_t* srt, const int32_t* wb, PermT* permt) {
-    int task[16], tot[16];
-    int rem[16][16];
-    const int NW = T / 32;
-    for (int L = 0; L < G; L++) {
-        const int t = s_tos[rd * T + th0 + L];
-        task[L] = t;
-        tot[L] = 0;
-        for (int c = 0; c < G; c++) {
-            rem[L][c] = t >= 0 ? cs[t * 17 + c + 1] - cs[t * 17 + c] : 0;
-            tot[L] += rem[L][c];
-        }
-    }
-    int steps = 0;
-    for (;;) {
-        bool any = false;
-        for (int L = 0; L < G; L++) any |= tot[L] > 0;
-        if (!any && (!write || steps >= steps_total)) break;
-        unsigned freec = (1u << G) - 1u, picked = 0u;
-        int row_of[16];
-        for (int L = 0; L < G; L++) row_of[L] = -1;
-        for (int it = 0; it < G && any; it++) {
-            int bl = -1, bv = 0;
-            for (int L = 0; L < G; L++)
-                if (!((picked >> L) & 1u) && tot[L] > bv) { bv = tot[L]; bl = L; }
-            if (bl < 0) break;
-            picked |= 1u << bl;
-            int bc = -1, bn = 0;
-            for (int c = 0; c < G; c++)
-                if (((freec >> c) & 1u) && rem[bl][c] > bn) { bn = rem[bl][c]; bc = c; }
-            if (bc < 0) continue;  // only taken colours left: padding this step
-            freec &= ~(1u << bc);
-            const int t = task[bl];
-            const int cnt = cs[t * 17 + bc + 1] - cs[t * 17 + bc];
-            row_of[bl] = srt[s_start[t] + cs[t * 17 + bc] + (cnt - rem[bl][bc])];
-            rem[bl][bc]--;
-            tot[bl]--;
-        }
-        if (write) {
-            for (int L = 0; L < G; L++) {
-                int row = row_of[L];
-                if (row < 0) {  // zero padding row of a free colour
-                    const int c = __ffs(freec) - 1;
-                    freec &= freec - 1u;
-                    row = n + (((c - n) % G) + G) % G;
-                }
-                const int th = th0 + L, w = th >> 5, ln = th & 31;
-                permt[(size_t)wb[rd * NW + w] + (size_t)(steps >> 2) * 128 + ln * 4 + (steps & 3)] = (PermT)(stride * row);
-            }
-        }
-        steps++;
-    }
-    return steps;
-}
-
-// One block.  Cuts every non-empty bin into ceil(count / P) tasks, sorts the
-// tasks by length (descending, ties by bin order; coarse buckets), deals them
-// to the T threads of the fused kernel in snake order, and writes for every
-// warp and round a conflict-free gather schedule (schedule_group) of byte
-// offsets into permt ([step/4][lane][4]).  Deterministic; runs once per
-// (data set, RB, T).
-template <typename PermT, typename SrcPermT>
+// Plan, step 1 (one block).  Cuts every non-empty bin into ceil(count / P)
+// tasks, sorts the tasks by length (descending, ties by bin order; coarse
+// buckets), deals them to the T threads of the fused kernel in snake order and
+// groups the rows of every task by colour (bank group, row mod G) for the
+// scheduler.  Deterministic; runs once per (data set, RB, T).
+template <typename SrcPermT>
 __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __restrict__ perm, int K, int ns,
-                             int nsp, int n, int T, int P, int stride, int G, int32_t* __restrict__ plan,
-                             int32_t* __restrict__ scratch, PermT* __restrict__ permt, const int* status) {
+                             int nsp, int n, int T, int P, int G, int32_t* __restrict__ plan,
+                             int32_t* __restrict__ scratch, const int* status) {
     extern __shared__ int psm[];
     __shared__ int wsum[33];
     __shared__ unsigned hist[1024], run_b[1024];
@@ -726,35 +659,156 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
         }
     }
     __syncthreads();
-    const int groups = RM * T / G;
-    for (int gi = tid; gi < groups; gi += nthr) {  // steps per lane group -> per warp
+    if (tid == 0) {
+        plan[0] = n_tasks;
+        plan[2] = n_comb;
+        plan[3] = n_multi;
+        plan[4] = P;
+    }
+}
+
+// Plan, step 2: conflict-free gather schedule of one lane group (the G lanes that
+// share a shared-memory wavefront: G = 16 for 8-byte rows, 8 for 16-byte rows).
+// Colour of a row = its bank group (row mod G).  Every step each lane emits one
+// row of its task or a zero padding row, and the G rows of a step have distinct
+// colours, so each gather instruction is conflict-free.  The G lanes cooperate
+// through segmented shuffles; each keeps its colour counts in registers.  Per
+// step the lane with the most rows left picks first (so the longest task makes
+// progress every step), then the others in rotated lane order; a lane takes the
+// free colour it holds most rows of; lanes without a pick get the remaining free
+// colours as padding rows.  The schedule goes to scratch ([group][step][G]).
+template <int G>
+__global__ void k_fused_sched(const int32_t* __restrict__ plan, const int32_t* __restrict__ scratch, int T, int KS,
+                              int SB, int n_groups, int32_t* __restrict__ sched, int32_t* __restrict__ gsteps,
+                              int* status) {
+    if (status && *status) return;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gi = gt / G, L = gt % G, lane = threadIdx.x & 31;
+    const int RM = plan_rounds_max(KS, T);
+    const int n_tasks_max = KS + 2 * T;
+    const int32_t* s_start = scratch;
+    const int32_t* s_tos = scratch + 5 * (size_t)n_tasks_max;
+    const int32_t* cs = s_tos + RM * T;
+    const bool valid = gi < n_groups;
+    int t = -1;
+    if (valid) {
         const int rd = gi / (T / G), th0 = (gi - rd * (T / G)) * G;
-        const int st = schedule_group<PermT>(G, rd, th0, T, n, stride, false, 0, s_tos, s_start, cs, srt, wb,
-                                             permt);
-        if (st) atomicMax(&wl[rd * NW + th0 / 32], (st + 3) / 4 * 4);
+        t = s_tos[rd * T + th0 + L];
+    }
+    int rem[G], nxt[G], tot = 0;  // rows left per colour, next srt index per colour
+#pragma unroll
+    for (int c = 0; c < G; c++) {
+        const int c0 = t >= 0 ? cs[t * 17 + c] : 0;
+        const int c1 = t >= 0 ? cs[t * 17 + c + 1] : 0;
+        rem[c] = c1 - c0;
+        nxt[c] = (t >= 0 ? s_start[t] : 0) + c0;
+        tot += rem[c];
+    }
+    const unsigned seg = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
+    int step = 0, gst = 0;
+    for (;;) {
+        const unsigned act = __ballot_sync(0xffffffffu, tot > 0);
+        if (!act) break;  // warp-uniform loop: shuffles stay convergent
+        const bool seg_active = (act & seg) != 0u;
+        // first pick: most rows left, ties lowest lane
+        int key = tot > 0 ? (tot << 5) | (31 - L) : -1;
+        for (int o = 1; o < G; o <<= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o, G));
+        const int first = key >= 0 ? 31 - (key & 31) : 0;
+        unsigned taken = 0u;
+        int mycol = -1;
+#pragma unroll 1
+        for (int e = 0; e < G; e++) {
+            const int cur = (first + e) % G;
+            int pick = -1;
+            if (L == cur && tot > 0) {
+                int bv = 0;
+#pragma unroll
+                for (int c = 0; c < G; c++)
+                    if (!((taken >> c) & 1u) && rem[c] > bv) { bv = rem[c]; pick = c; }
+            }
+            pick = __shfl_sync(0xffffffffu, pick, cur, G);
+            if (pick >= 0) {
+                taken |= 1u << pick;
+                if (L == cur) mycol = pick;
+            }
+        }
+        int mypick = -1;  // -> srt index of the row
+        if (mycol >= 0) {
+#pragma unroll
+            for (int c = 0; c < G; c++)
+                if (c == mycol) { rem[c]--; mypick = nxt[c]++; }
+            tot--;
+        }
+        // padding for lanes without a pick: the free colours in lane order (entry -1 - colour)
+        const unsigned nop = __ballot_sync(0xffffffffu, mypick < 0) & seg;
+        int entry = mypick;  // srt index of the row (resolved by k_fused_pack)
+        if (mypick < 0) {
+            int rank = __popc(nop & ((1u << lane) - 1u) & seg);
+            unsigned freec = ~taken & ((1u << G) - 1u);
+            for (; rank > 0; rank--) freec &= freec - 1u;
+            entry = -__ffs(freec);  // -1 - colour
+        }
+        if (seg_active) {
+            if (valid && step < SB) sched[((size_t)gi * SB + step) * G + L] = entry;
+            if (valid && step >= SB && L == 0) cwb_dev_fail(status, CWB_ECUDA);  // bound exceeded
+            gst = step + 1;
+        }
+        step += 1;
+        if (step >= SB + 1) break;
+    }
+    if (valid && L == 0) gsteps[gi] = gst;  // steps of this group
+}
+
+// Plan, step 3 (one block): steps per warp and round (max over its lane groups,
+// rounded up to 4), block offsets of the schedule, round count and size.
+__global__ void k_fused_wl(int32_t* __restrict__ plan, const int32_t* __restrict__ gsteps, int KS, int T, int G,
+                           const int* status) {
+    if (status && *status) return;
+    const int RM = plan_rounds_max(KS, T), NW = T / 32, gpw = 32 / G;
+    int32_t* wl = plan + 8 + RM * T;
+    int32_t* wb = wl + RM * NW;
+    for (int e = threadIdx.x; e < RM * NW; e += blockDim.x) {
+        int st = 0;
+        for (int g = 0; g < gpw; g++) st = max(st, gsteps[e * gpw + g]);
+        wl[e] = (st + 3) / 4 * 4;
     }
     __syncthreads();
-    if (tid == 0) {  // block offsets, round count
+    if (threadIdx.x == 0) {
         int o = 0, rounds = 0;
         for (int e = 0; e < RM * NW; e++) {
             wb[e] = o;
             o += 32 * wl[e];
             if (wl[e]) rounds = e / NW + 1;
         }
-        plan[0] = n_tasks;
         plan[1] = rounds;
-        plan[2] = n_comb;
-        plan[3] = n_multi;
-        plan[4] = P;
         plan[5] = o;
-        plan[6] = plan[7] = 0;
     }
-    __syncthreads();
-    for (int gi = tid; gi < groups; gi += nthr) {  // write the schedules
-        const int rd = gi / (T / G), th0 = (gi - rd * (T / G)) * G;
-        const int w = th0 / 32;
-        if (wl[rd * NW + w] == 0) continue;
-        schedule_group<PermT>(G, rd, th0, T, n, stride, true, wl[rd * NW + w], s_tos, s_start, cs, srt, wb, permt);
+}
+
+// Plan, step 4: the schedule in the kernel's layout ([step/4][lane][4] per warp
+// and round block), padding steps beyond a group's schedule with zero rows of
+// distinct colours.
+template <typename PermT>
+__global__ void k_fused_pack(const int32_t* __restrict__ plan, const int32_t* __restrict__ scratch,
+                             const int32_t* __restrict__ sched, const int32_t* __restrict__ gsteps, int KS, int T,
+                             int G, int SB, int n, int stride, PermT* __restrict__ permt, const int* status) {
+    if (status && *status) return;
+    const int RM = plan_rounds_max(KS, T), NW = T / 32;
+    const int32_t* srt = scratch + 22 * (size_t)(KS + 2 * T) + (size_t)RM * T;  // task rows by colour
+    const int32_t* wl = plan + 8 + RM * T;
+    const int32_t* wb = wl + RM * NW;
+    const int rounds = plan[1];
+    for (int e = blockIdx.x; e < rounds * NW; e += gridDim.x) {
+        const int steps = wl[e];
+        for (int x = threadIdx.x; x < steps * 32; x += blockDim.x) {
+            const int st = x >> 5, ln = x & 31;
+            const int gi = e * (32 / G) + ln / G, L = ln % G;
+            int v;
+            const int x2 = st < gsteps[gi] ? sched[((size_t)gi * SB + st) * G + L] : -1 - L;
+            const int row = x2 >= 0 ? srt[x2] : n + (((-1 - x2 - n) % G) + G) % G;
+            v = stride * row;
+            permt[(size_t)wb[e] + (size_t)(st >> 2) * 128 + ln * 4 + (st & 3)] = (PermT)v;
+        }
     }
 }
 
@@ -842,37 +896,61 @@ static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
     c->plan = nullptr;
     c->permt = nullptr;
     c->fused_T = 0;
-    const int KS = c->K * c->n_star, T = f.T;
-    const size_t scratch_ints = 22 * (size_t)(KS + 2 * T) + (size_t)plan_rounds_max(KS, T) * T + (size_t)c->K * c->n;
-    if (cwb_alloc((void**)&c->plan, sizeof(int32_t) * (plan_ints(KS, T) + scratch_ints), s) != cudaSuccess ||
-        cwb_alloc(&c->permt, (size_t)f.permt_bytes * f.cap + 16, s) != cudaSuccess)
+    const int KS = c->K * c->n_star, T = f.T, G = 16 / f.RB;
+    const int RM = plan_rounds_max(KS, T);
+    const int n_groups = RM * T / G;
+    const int SB = 2 * ((f.P + 3) / 4 * 4) + G;  // schedule steps bound per group
+    const size_t scratch_ints = 22 * (size_t)(KS + 2 * T) + (size_t)RM * T + (size_t)c->K * c->n;
+    const size_t sched_ints = (size_t)n_groups * SB * G + n_groups;
+    if (cwb_alloc((void**)&c->plan, sizeof(int32_t) * (plan_ints(KS, T) + scratch_ints + sched_ints), s) != cudaSuccess)
         return cwb_set_error(c, CWB_ENOMEM, "fused plan allocation failed");
-    const size_t psmem = sizeof(int) * 4 * (size_t)KS;
     int32_t* scratch = c->plan + plan_ints(KS, T);
+    int32_t* sched = scratch + scratch_ints;
+    int32_t* gsteps = sched + (size_t)n_groups * SB * G;
+    const size_t psmem = sizeof(int) * 4 * (size_t)KS;
     const int stride = 8 * f.RB;
-#define PLAN_CASE(PT, ST)                                                                                \
-    {                                                                                                    \
-        auto kern = k_fused_plan<PT, ST>;                                                                \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);             \
-        kern<<<1, 1024, psmem, s>>>(c->off, (const ST*)c->perm, c->K, c->n_star, c->nsp, (int)c->n, T, f.P, \
-                                    stride, 16 / f.RB, c->plan, scratch, (PT*)c->permt, c->d_status);    \
+    if (c->perm_bytes == 2) {
+        auto kern = k_fused_plan<uint16_t>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        kern<<<1, 1024, psmem, s>>>(c->off, (const uint16_t*)c->perm, c->K, c->n_star, c->nsp, (int)c->n, T, f.P, G,
+                                    c->plan, scratch, c->d_status);
+    } else {
+        auto kern = k_fused_plan<uint32_t>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        kern<<<1, 1024, psmem, s>>>(c->off, (const uint32_t*)c->perm, c->K, c->n_star, c->nsp, (int)c->n, T, f.P, G,
+                                    c->plan, scratch, c->d_status);
     }
-    if (f.permt_bytes == 2 && c->perm_bytes == 2) PLAN_CASE(uint16_t, uint16_t)
-    else if (f.permt_bytes == 2) PLAN_CASE(uint16_t, uint32_t)
-    else if (c->perm_bytes == 2) PLAN_CASE(uint32_t, uint16_t)
-    else PLAN_CASE(uint32_t, uint32_t)
-#undef PLAN_CASE
-    c->launches++;
-    int rc = cwb_check_launch(c, "k_fused_plan");
+    const int sthreads = n_groups * G;  // one warp per block: spread the latency-bound groups over the SMs
+    if (G == 8)
+        k_fused_sched<8><<<(sthreads + 31) / 32, 32, 0, s>>>(c->plan, scratch, T, KS, SB, n_groups, sched, gsteps,
+                                                             c->d_status);
+    else
+        k_fused_sched<16><<<(sthreads + 31) / 32, 32, 0, s>>>(c->plan, scratch, T, KS, SB, n_groups, sched, gsteps,
+                                                              c->d_status);
+    k_fused_wl<<<1, 256, 0, s>>>(c->plan, gsteps, KS, T, G, c->d_status);
+    c->launches += 3;
+    int rc = cwb_check_launch(c, "fused plan kernels");
     if (rc) return rc;
-    // exact schedule size (one host sync per plan build): sizes the shared-memory copy
+    // exact schedule size (one host sync per plan build): sizes the schedule buffer and
+    // its shared-memory copy
     int32_t hdr[8] = {0};
     int dev_status = 0;
     CWB_CUDA_TRY(c, cudaMemcpyAsync(hdr, c->plan, sizeof(hdr), cudaMemcpyDeviceToHost, s));
     CWB_CUDA_TRY(c, cudaMemcpyAsync(&dev_status, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CWB_CUDA_TRY(c, cudaStreamSynchronize(s));
     if (dev_status) return CWB_OK;  // reported by cwb_status
-    if ((size_t)hdr[5] > f.cap) return cwb_set_error(c, CWB_ECUDA, "fused plan exceeds its bound");
+    if (cwb_alloc(&c->permt, (size_t)f.permt_bytes * hdr[5] + 64, s) != cudaSuccess)
+        return cwb_set_error(c, CWB_ENOMEM, "fused plan allocation failed");
+    const int blocks = std::max(1, std::min(hdr[1] * (T / 32), 1184));
+    if (f.permt_bytes == 2)
+        k_fused_pack<uint16_t><<<blocks, 256, 0, s>>>(c->plan, scratch, sched, gsteps, KS, T, G, SB, (int)c->n,
+                                                      stride, (uint16_t*)c->permt, c->d_status);
+    else
+        k_fused_pack<uint32_t><<<blocks, 256, 0, s>>>(c->plan, scratch, sched, gsteps, KS, T, G, SB, (int)c->n,
+                                                      stride, (uint32_t*)c->permt, c->d_status);
+    c->launches++;
+    rc = cwb_check_launch(c, "k_fused_pack");
+    if (rc) return rc;
     c->fused_T = T;
     c->fused_rb = f.RB;
     c->permt_bytes = f.permt_bytes;

@@ -323,23 +323,35 @@ struct LamEval { double f, fp; bool ok; };
 // for the columns of G (-> X = A^-1 G) and of D (-> Y = A^-1 D).
 // f(t) = df(e^t) - target, f'(t) = lambda d df / d lambda,
 // d tr(X)/d lambda = -tr(Y X), d tr(X^2)/d lambda = -2 tr(X Y X).
+// The factor keeps the last three rows in registers (no shared-memory round trip
+// in the dependency chain) and uses rsqrt for the pivots (no division).
+// Lb[j*4 + q] = L[j][j-q] (q = 0..3), inv[j] = 1 / L[j][j]; Lb is zero beyond row d.
 __device__ void band_factor(double lam, int d, double (*Gs)[DS], double (*Dm)[DS], double* Lb, double* inv,
                             bool* ok_out) {
     if ((threadIdx.x & 31) == 0) {
         bool ok = true;
+        double r1_1 = 0.0, r1_2 = 0.0, r2_1 = 0.0;  // L[j-1][j-2], L[j-1][j-3], L[j-2][j-3]
+        double i1 = 0.0, i2 = 0.0, i3 = 0.0;        // inverse pivots of rows j-1, j-2, j-3
         for (int j = 0; j < d; j++) {
-            for (int q = min(j, BW); q >= 1; q--) {  // L[j][c], c = j - q
-                const int c = j - q;
-                double v = Gs[j][c] + lam * Dm[j][c];
-                for (int p = max(0, j - BW); p < c; p++) v -= Lb[j * 4 + (j - p)] * Lb[c * 4 + (c - p)];
-                Lb[j * 4 + q] = v * inv[c];
-            }
-            double v = Gs[j][j] + lam * Dm[j][j];
-            for (int p = max(0, j - BW); p < j; p++) v -= Lb[j * 4 + (j - p)] * Lb[j * 4 + (j - p)];
+            const double a0 = Gs[j][j] + lam * Dm[j][j];
+            const double a1 = j >= 1 ? Gs[j][j - 1] + lam * Dm[j][j - 1] : 0.0;
+            const double a2 = j >= 2 ? Gs[j][j - 2] + lam * Dm[j][j - 2] : 0.0;
+            const double a3 = j >= 3 ? Gs[j][j - 3] + lam * Dm[j][j - 3] : 0.0;
+            const double x3 = a3 * i3;
+            const double x2 = (a2 - x3 * r2_1) * i2;
+            const double x1 = (a1 - x3 * r1_2 - x2 * r1_1) * i1;
+            const double v = a0 - x3 * x3 - x2 * x2 - x1 * x1;
             ok &= v > 0.0;
-            const double l = sqrt(fmax(v, 1e-300));
-            Lb[j * 4] = l;
-            inv[j] = 1.0 / l;
+            const double vi = rsqrt(fmax(v, 1e-300));
+            Lb[j * 4 + 0] = v * vi;
+            Lb[j * 4 + 1] = x1;
+            Lb[j * 4 + 2] = x2;
+            Lb[j * 4 + 3] = x3;
+            inv[j] = vi;
+            r2_1 = r1_1;  // row j-1 becomes row j-2: its L[.][.-1]
+            r1_1 = x1;
+            r1_2 = x2;
+            i3 = i2; i2 = i1; i1 = vi;
         }
         *ok_out = ok;
     }
@@ -349,15 +361,19 @@ __device__ void band_factor(double lam, int d, double (*Gs)[DS], double (*Dm)[DS
 // x = A^-1 b for b = column c of B (read through the functor), result in column c of Xs
 template <typename Fb>
 __device__ __forceinline__ void band_solve(int d, const double* Lb, const double* inv, Fb b, double (*Xs)[DS], int c) {
+    double z1 = 0.0, z2 = 0.0, z3 = 0.0;
     for (int j = 0; j < d; j++) {  // L z = b
-        double v = b(j);
-        for (int p = max(0, j - BW); p < j; p++) v -= Lb[j * 4 + (j - p)] * Xs[p][c];
-        Xs[j][c] = v * inv[j];
+        const double v = b(j) - Lb[j * 4 + 1] * z1 - Lb[j * 4 + 2] * z2 - Lb[j * 4 + 3] * z3;
+        const double z = v * inv[j];
+        Xs[j][c] = z;
+        z3 = z2; z2 = z1; z1 = z;
     }
-    for (int j = d - 1; j >= 0; j--) {  // L^T x = z
-        double v = Xs[j][c];
-        for (int p = j + 1; p <= min(d - 1, j + BW); p++) v -= Lb[p * 4 + (p - j)] * Xs[p][c];
-        Xs[j][c] = v * inv[j];
+    double x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    for (int j = d - 1; j >= 0; j--) {  // L^T x = z (Lb rows beyond d are zero)
+        const double v = Xs[j][c] - Lb[(j + 1) * 4 + 1] * x1 - Lb[(j + 2) * 4 + 2] * x2 - Lb[(j + 3) * 4 + 3] * x3;
+        const double x = v * inv[j];
+        Xs[j][c] = x;
+        x3 = x2; x2 = x1; x1 = x;
     }
 }
 
@@ -400,9 +416,10 @@ __device__ LamEval lam_eval(double t, int d, double target, int kind, double (*G
 __global__ void k_lambda(const double* __restrict__ Gall, int d, double target, int kind,
                          double* lambda_out, double* Ainv_out, double* Cb_out, int* status) {
     __shared__ double Gs[CWB_MAX_D][DS], Dm[CWB_MAX_D][DS], Xs[CWB_MAX_D][DS], Ys[CWB_MAX_D][DS];
-    __shared__ double Lb[CWB_MAX_D * 4], inv[CWB_MAX_D];
+    __shared__ double Lb[(CWB_MAX_D + 4) * 4], inv[CWB_MAX_D];
     if (status && *status) return;
     const int k = blockIdx.x, i = threadIdx.x;
+    for (int e = i; e < (CWB_MAX_D + 4) * 4; e += 32) Lb[e] = 0.0;  // zero band beyond row d
     if (i < d)
         for (int c = 0; c < d; c++) {
             Gs[i][c] = Gall[((size_t)k * d + i) * d + c];
