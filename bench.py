@@ -40,14 +40,19 @@ UNIT = "evals/s"
 
 
 def alg_ops_per_rep_iter(c, n_star, d):
-    """FP64 add/FMA instructions per replication-iteration of the fused path."""
+    """Algorithmic fp64 add/FMA operations per replication-iteration of the fused kernel."""
     K, n = c.K, c.n
-    h1 = K * n                      # binMatVec scatter: one add per (learner, row)
+    h1 = K * n                      # binMatVec sums: one add per (learner, row)
     h2 = 4 * K * n_star             # s = Zb^T u, 4 non-zeros per design point
     h3 = K * d * d                  # theta = A^-1 s
-    h4 = K * (7 * d + 3 * d)        # G theta on the band, v = theta (2 s - G theta), reduction
-    h6 = 4 * n_star + 2 * n         # zhat, r update, r^T r
+    h4 = 5 * K * d                  # c = C^T theta (4 per coefficient), |c|^2
+    h6 = 4 * n_star + 2 * n + d     # zhat, r update + r^T r, theta_agg
     return h1 + h2 + h3 + h4 + h6
+
+
+# measured conflict-free shared-memory gather ceiling (profiles/ubench_smem_gather.txt):
+# 16-byte lane-loads (RB = 2 replications per row) and 8-byte lane-loads (RB = 1) per clock per SM
+GATHER_LANE_LOADS_PER_CLK = {2: 7.1, 1: 12.7}
 
 
 def fp64_peak_ops(peaks):
@@ -117,10 +122,9 @@ class ClockSampler:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    from paper_2110_03513_b200 import dist as D
+    w = D.world_from_env()
+    return w.size, w.rank, w.local_rank
 
 
 def oracle_sample(cfg, seconds_target=12.0, threads=None):
@@ -203,16 +207,16 @@ def main():
         return
 
     import torch
-    ws, rank, local = dist_env()
+    from paper_2110_03513_b200 import dist as D
+    w = D.world_from_env()
+    ws, rank, local = w.size, w.rank, w.local_rank
     torch.cuda.set_device(local)
     devname = f"cuda:{local}"
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(devname))
+    D.init_process_group(w, "nccl", torch.device(devname))
     from paper_2110_03513_b200 import cwb
 
     # this rank's replications (weak scaling): rank r owns [r*B, (r+1)*B)
-    reps = range(rank * cfg.B, (rank + 1) * cfg.B)
+    reps = D.replication_block(cfg.B, rank)
     ds = S.make(cfg, reps=reps)
     X = torch.as_tensor(ds.X, device=devname)
     Y = torch.as_tensor(ds.Y, device=devname)
@@ -249,9 +253,7 @@ def main():
     pool.close()
 
     def barrier():
-        if ws > 1:
-            import torch.distributed as dist
-            dist.barrier()
+        D.barrier(w)
         torch.cuda.synchronize()
 
     launches.clear()
@@ -265,12 +267,7 @@ def main():
     step_ms = np.array([ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)])
     train_ms = np.array([ev[i][1].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)])
     init_ms = step_ms - train_ms
-    total_ms = float(step_ms.sum())
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=devname)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = D.max_over_ranks(float(step_ms.sum()), w, devname)
     ms_per_step = total_ms / args.steps
     evals = K * n * B * M * ws
     value = evals / (ms_per_step * 1e-3)
@@ -306,20 +303,34 @@ def main():
         e1.record(stream)
         e1.synchronize()
         e_ms.append(e0.elapsed_time(e1))
-    e2e_ms = float(np.mean(e_ms))
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=devname)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = D.max_over_ranks(float(np.mean(e_ms)), w, devname)
     h2d = ds.X.nbytes + ds.Y.nbytes
     d2h = sum(v.numel() * v.element_size() for v in outh.values())
 
+    # ---- kernel-only time of one k_train_fused launch (plan cached: one launch per call),
+    #      CUDA events on the launching stream, for the roofline
+    kpool = cwb.Pool(X, gcfg)
+    if args.path:
+        kpool.set_path(args.path)
+    kouts = kpool.train(Y, nu=cfg.nu, M=M)
+    kpool.status()
+    k_ms = []
+    for i in range(max(3, min(args.steps, 10))):
+        flush.fill_(float(i))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = kpool.launches()
+        e0.record(stream)
+        kouts = kpool.train(Y, nu=cfg.nu, M=M, out=kouts)
+        e1.record(stream)
+        e1.synchronize()
+        k_ms.append(e0.elapsed_time(e1))
+        k_launches = kpool.launches() - l0
+    kpool.close()
+    kernel_ms = float(np.mean(k_ms))
     if rank == 0:
         peaks, src = load_peaks()
         ops = alg_ops_per_rep_iter(cfg, n_star, d) * B * M
-        train_s = float(np.mean(train_ms)) * 1e-3
-        achieved = ops / train_s
+        achieved = ops / (kernel_ms * 1e-3)
         peak = fp64_peak_ops(peaks)
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -328,6 +339,10 @@ def main():
                 traffic = json.load(open(tp)).get(cfg.name)
             except Exception:
                 traffic = None
+        rb = 2 if B > 148 else 1  # replications per CTA
+        sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        ctas_per_sm = -(-(-(-B // rb)) // 148)
+        h1_floor_ms = K * n * ctas_per_sm * M / (GATHER_LANE_LOADS_PER_CLK[rb] * sm_hz) * 1e3
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -339,9 +354,15 @@ def main():
             "roofline": {"bound": "alu", "kernel": "k_train_fused" if args.path != 2 else "general path",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "note": ("fp64 add/FMA instructions per launch (DESIGN.md Sec. 5) / mean train-event "
-                                  f"time; peak = 148 SM x 64 fp64 lanes x {peaks.get('sm_max_mhz', 1965)} MHz "
-                                  f"({src} clock)")},
+                         "kernel_ms": kernel_ms, "launches_per_call": int(k_launches),
+                         "note": ("achieved = algorithmic fp64 add/FMA operations of one launch (FMA counted "
+                                  "once; DESIGN.md Sec. 7) / its CUDA-event duration; peak = 148 SM x 64 fp64 "
+                                  f"lanes x {peaks.get('sm_max_mhz', 1965)} MHz ({src} clock)"),
+                         "smem_gather_ceiling": {
+                             "h1_floor_ms": h1_floor_ms,
+                             "note": ("time H1 alone would take at the measured conflict-free shared-memory "
+                                      "gather rate (profiles/ubench_smem_gather.txt); the binding on-chip "
+                                      "ceiling of this kernel")}},
             "e2e": {"value": evals / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                     "api": "cwb_fit_host (pinned host buffers, copies + init + train + sync)"},
