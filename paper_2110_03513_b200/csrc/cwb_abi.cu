@@ -186,7 +186,6 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     c->idx_bytes = ns <= 256 ? 1 : 2;
     c->perm_bytes = n <= 65536 ? 2 : 4;
     c->stream = s;
-    if (const char* e = getenv("CWB_STAGGER")) c->stagger = atoi(e);  // tuning knob (cycles)
     const size_t Ks = K, nn = n, nss = ns, dd = d;
     bool ok = true;
     ok &= cwb_alloc((void**)&c->d_status, sizeof(int), s) == cudaSuccess;

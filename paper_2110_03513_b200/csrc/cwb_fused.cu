@@ -1,36 +1,32 @@
-// cwb_fused.cu -- the whole CWB loop (Alg. 1 supp.) for one or two
-// replications per CTA, all M iterations in one launch.
+// cwb_fused.cu -- the whole CWB loop (Alg. 1 supp.) for RB = 1 or
+// 2 replications per CTA, all M iterations in one launch.
 //
 // Replications are independent boosting runs that share the binned pool, so
-// no CTA ever waits for another: no grid barrier, no atomics, no host round
-// trip between iterations.  A CTA runs PIPES (1 or 2) pipelines; a pipeline is
-// Tp threads working on one replication with its own named barrier, so the
-// latency-bound phases of one overlap the shared-memory gathers of the other.
-// The residuals r (n doubles) and the bin sums u (K x n*) of each pipeline stay
-// in shared memory for all M iterations; when it fits, the read-only pool tables
-// used every iteration (gather schedule, basis windows, cached inverses,
-// selection factors) are staged in shared memory once per CTA, otherwise they
-// are read through L1/L2.  Four pipeline barriers per iteration m:
+// a CTA never waits for another CTA: no grid barrier, no atomics, no host
+// round trip between iterations.  The residuals r (n x RB doubles, the RB
+// replications of a row side by side) and the bin sums u (K x n* x RB) stay
+// in shared memory for all M iterations; when it fits, the read-only pool
+// tables used every iteration (gather schedule, basis windows, cached
+// inverses, selection factors) are staged in shared memory too, otherwise
+// they are read through L1/L2.  Four block barriers per iteration m:
 //
 //   A  H1  u_k(l) = sum_{i in bin l of learner k} r_i      binMatVec loop
 //          The K*n* bins are cut into tasks, sorted by length and dealt to the
-//          Tp threads in snake order by a plan built once per (data set, Tp)
+//          T threads in snake order by a plan built once per (data set, RB, T)
 //          (k_fused_plan).  For each warp the plan holds a gather schedule of
-//          byte offsets ([step/4][lane][4]) in which the 16 lanes of a shared-
-//          memory wavefront always hit distinct bank pairs; one 8-byte load
-//          fetches 4 offsets and each offset addresses a residual directly.
-//          Zero padding rows r[n..n+15] absorb ragged ends; a bin cut into
-//          several tasks is completed by a fixed-order combine.
+//          byte offsets ([step/4][lane][4]) in which the lanes of a shared-
+//          memory wavefront always hit distinct bank groups; one 8- or 16-byte
+//          load fetches 4 offsets and each offset addresses the RB residuals of
+//          a row directly.  Zero padding rows r[n..n+15] absorb ragged ends; a
+//          bin cut into several tasks is completed by a fixed-order combine.
 //   B  H2-H4  one warp per learner, lane j = coefficient j:
 //          s = Zb^T u over the design-point window of basis j,
 //          theta = (G + lambda D)^-1 s with the cached inverse,
 //          delta = |C^T theta|^2 = 2 theta^T s - theta^T G theta with C C^T = G + 2 lambda D
 //          banded, so SSE_k = r^T r - delta_k.
-//   C  H5  per 32-point slice: k* = argmax delta_k, lowest k on ties;
-//          zhat = nu Zb_k* theta_k* at the design points.
-//   D  H6  r_i -= zhat[idx_k*(i)], per-thread r^T r partials.
-//   theta_agg[k*] += nu theta* and the k / SSE / risk traces of iteration m
-//   run in phase A of iteration m+1 on warp 0 of the pipeline (least H1 work).
+//   C  H5  warp q (replication q): k* = argmax delta_k, lowest k on ties;
+//          zhat = nu Zb_k* theta_k* at the design points; theta_agg[k*] += nu theta* (P:L838).
+//   D  H6  r_i -= zhat[idx_k*(i)], r^T r per warp.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -42,12 +38,12 @@ namespace {
 
 constexpr int kDiscard = INT32_MIN;
 constexpr int kPadRows = 16;  // zero rows after the n residual rows, one per bank group
+constexpr int kSlackEntries = 256;  // schedule entries after the last block (2 groups of 4 x 32 lanes)
 
 struct FusedParams {
     int n, K, ns, nsp, d, M, B, n_multi, W;
     int permt_cap;  // entries of permt staged in shared memory (POOL)
     int ztab;       // Zs / zj0 staged in shared memory
-    int stagger;    // start delay (cycles) of pipeline 1
     double nu;
     double inv2n;  // 1 / (2n): risk = r^T r / (2n) without a division on the critical path
     const double* Y;
@@ -65,18 +61,26 @@ struct FusedParams {
     int32_t* k_trace;
     double* sse_trace;
     double* risk_trace;
-    long long* timing;  // optional: cycles per phase (CTA 0, pipeline 0, thread 0), summed over iterations
+    long long* timing;  // optional: cycles per phase (CTA 0, thread 0), summed over iterations
     int* status;
 };
 
 __host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 
-// Shared memory: the pool tables (one copy per CTA, read by every pipeline) followed by
-// one private block per pipeline (one replication each).
-struct PoolLayout {
-    size_t permt, zt, ai, cb, lw, zs, zj, total;
-    __host__ __device__ PoolLayout(int K, int nsp, int d, int W, bool pool, size_t permt_bytes, bool ztab) {
+struct SmemLayout {
+    size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, total;
+    __host__ __device__ SmemLayout(int n, int K, int nsp, int d, int W, int n_multi, int RB, int NW, bool pool,
+                                   size_t permt_bytes, bool ztab) {
         size_t o = 0;
+        r = o; o = align16(o + sizeof(double) * RB * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
+        U = o; o = align16(o + sizeof(double) * RB * ((size_t)K * nsp + W));  // +W: window overrun pad
+        delta = o; o = align16(o + sizeof(double) * RB * K);
+        th = o; o = align16(o + sizeof(double) * RB * (size_t)K * 32);        // theta_k of every learner
+        ss = o; o = align16(o + sizeof(double) * RB * (size_t)NW * 32);       // per-warp s = Zb^T u
+        zhat = o; o = align16(o + sizeof(double) * RB * (size_t)nsp);
+        agg = o; o = align16(o + sizeof(double) * RB * (size_t)K * d);
+        pc = o; o = align16(o + sizeof(double) * RB * (n_multi > 0 ? n_multi : 1));
+        red = o; o = align16(o + sizeof(double) * 2 * RB * (size_t)NW * 32);  // double-buffered per-thread r^T r
         permt = o; if (pool) o = align16(o + permt_bytes);
         zt = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * W * d);
         ai = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * d * d);
@@ -87,29 +91,12 @@ struct PoolLayout {
         total = o;
     }
 };
-struct PipeLayout {
-    size_t r, U, delta, th, ss, zhat, agg, pc, red, misc, total;
-    __host__ __device__ PipeLayout(int n, int K, int nsp, int d, int W, int n_multi, int Tp) {
-        size_t o = 0;
-        r = o; o = align16(o + sizeof(double) * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
-        U = o; o = align16(o + sizeof(double) * ((size_t)K * nsp + W));    // +W: window overrun pad
-        delta = o; o = align16(o + sizeof(double) * K);
-        th = o; o = align16(o + sizeof(double) * (size_t)K * 32);          // theta_k of every learner
-        ss = o; o = align16(o + sizeof(double) * (size_t)(Tp / 32) * 32);  // per-warp s = Zb^T u
-        zhat = o; o = align16(o + sizeof(double) * (size_t)nsp);
-        agg = o; o = align16(o + sizeof(double) * (size_t)K * d);
-        pc = o; o = align16(o + sizeof(double) * (n_multi > 0 ? n_multi : 1));
-        red = o; o = align16(o + sizeof(double) * 2 * (size_t)Tp);          // double-buffered per-thread r^T r
-        misc = o; o = align16(o + 16);                                      // k*, best delta
-        total = o;
-    }
-};
 
 // plan layout (int32), built by k_fused_plan:
 //   [0] n_tasks [1] rounds [2] n_comb [3] n_multi [4] P [5] permt entries [6..7] 0
 //   tt_dest[R*T]   destination of thread t's task in round r (>= 0: u index,
 //                  < 0: piece slot -dest-1, INT32_MIN: no task)
-//   wl[R*NW]       steps of warp w in round r (multiple of 4, 0: none)
+//   wl[R*NW]       steps of warp w in round r (multiple of 8, 0: none)
 //   wb[R*NW]       offset of that block in permt ([step/4][lane][4] byte offsets)
 //   comb_g[KS] comb_first[KS] comb_cnt[KS]   bins cut into several pieces
 __host__ __device__ __forceinline__ int plan_rounds_max(int KS, int T) { return (KS + 2 * T) / T + 1; }
@@ -117,6 +104,25 @@ __host__ __device__ __forceinline__ size_t plan_ints(int KS, int T) {
     const size_t R = plan_rounds_max(KS, T);
     return 8 + R * T + 2 * R * (T / 32) + 3 * (size_t)KS;
 }
+__host__ __device__ __forceinline__ size_t permt_bound(int KS, int T, int P) {
+    return (size_t)plan_rounds_max(KS, T) * T * (size_t)((P + 3) / 4 * 4);
+}
+
+template <int RB> struct RV;  // RB residuals of one row
+template <> struct RV<1> {
+    double x;
+    __device__ __forceinline__ static RV ld(const unsigned char* base, uint32_t off) {
+        RV v; v.x = *reinterpret_cast<const double*>(base + off); return v;
+    }
+    __device__ __forceinline__ double operator[](int) const { return x; }
+};
+template <> struct RV<2> {
+    double x, y;
+    __device__ __forceinline__ static RV ld(const unsigned char* base, uint32_t off) {
+        const double2 t = *reinterpret_cast<const double2*>(base + off); RV v; v.x = t.x; v.y = t.y; return v;
+    }
+    __device__ __forceinline__ double operator[](int q) const { return q ? y : x; }
+};
 
 // 4 byte offsets of consecutive steps of this lane
 template <typename PermT> struct Off4;
@@ -135,9 +141,7 @@ template <> struct Off4<uint32_t> {
     }
 };
 
-__device__ __forceinline__ double lds_at(const unsigned char* base, uint32_t off) {
-    return *reinterpret_cast<const double*>(base + off);
-}
+template <bool SM> __device__ __forceinline__ double2 ld2(const double2* p) { return SM ? *p : __ldg(p); }
 
 __device__ __forceinline__ long long phase_mark(long long* acc, long long t0, bool on) {
     if (!on) return 0;
@@ -146,207 +150,214 @@ __device__ __forceinline__ long long phase_mark(long long* acc, long long t0, bo
     return t;
 }
 
-// barrier of one pipeline (named barrier 1 + pipe over its Tp threads); PIPES == 1: the CTA
-template <int PIPES>
-__device__ __forceinline__ void pipe_sync(int pipe, int Tp) {
-    if (PIPES == 1) __syncthreads();
-    else asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "r"(Tp) : "memory");
-}
-
-// PIPES replications per CTA, each run by its own Tp = T / PIPES threads with their own
-// barriers, so the latency-bound phases of one pipeline overlap the shared-memory gathers
-// of the other; the pool tables are staged once per CTA.
-template <typename IdxT, typename PermT, int PIPES, bool POOL, int MAXT, int MINB>
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int T = blockDim.x, Tp = T / PIPES, NW = Tp >> 5;
-    const int pipe = threadIdx.x / Tp, tid = threadIdx.x - pipe * Tp;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.x * PIPES + pipe;  // this pipeline's replication
-    const bool live = b < p.B;
+    const int T = blockDim.x, NW = T >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b0 = blockIdx.x * RB;
     const int n = p.n;
-    const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns, W = p.W;
-    const PoolLayout PLo(K, nsp, d, W, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab != 0);
-    const PipeLayout L(n, K, nsp, d, W, p.n_multi, Tp);
-    unsigned char* mine = smem + PLo.total + (size_t)pipe * L.total;
-    double* r = (double*)(mine + L.r);
-    const unsigned char* rb = mine + L.r;
-    double* U = (double*)(mine + L.U);  // U[k * nsp + l]
-    double* delta = (double*)(mine + L.delta);
-    double* thall = (double*)(mine + L.th);  // thall[k * 32 + j]
-    double* sS = (double*)(mine + L.ss) + warp * 32;
-    double* zhat = (double*)(mine + L.zhat);
-    double* agg = (double*)(mine + L.agg);
-    double* pc = (double*)(mine + L.pc);
-    double* red = (double*)(mine + L.red);  // red[parity * Tp + tid]: per-thread r^T r partials
-    int* ks_sh = (int*)(mine + L.misc);
-    double* best_sh = (double*)(mine + L.misc + 8);
-    const PermT* permt = POOL ? (const PermT*)(smem + PLo.permt) : (const PermT*)p.permt;
-    const double* ZTc = POOL ? (const double*)(smem + PLo.zt) : p.ZT;
-    const double* Ac = POOL ? (const double*)(smem + PLo.ai) : p.Ainv;
-    const double* Cbc = POOL ? (const double*)(smem + PLo.cb) : p.Cb;
-    const double* Zs_c = p.ztab ? (const double*)(smem + PLo.zs) : p.Zs;
-    const int32_t* zj0_c = p.ztab ? (const int32_t*)(smem + PLo.zj) : p.zj0;
+    const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns;
+    const int W = p.W;
+    const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab != 0);
+    double* r = (double*)(smem + L.r);  // r[i * RB + q]
+    const unsigned char* rb = smem + L.r;
+    double* U = (double*)(smem + L.U);  // U[g * RB + q], g = k * nsp + l
+    double* delta = (double*)(smem + L.delta);
+    double* thall = (double*)(smem + L.th);  // thall[(k * RB + q) * 32 + j]
+    double* zhat = (double*)(smem + L.zhat);  // zhat[q * nsp + l]
+    double* agg = (double*)(smem + L.agg);
+    double* pc = (double*)(smem + L.pc);
+    double* red = (double*)(smem + L.red);  // red[(parity * RB + q) * T + tid]: per-thread r^T r partials
+    const PermT* permt = POOL ? (const PermT*)(smem + L.permt) : (const PermT*)p.permt;
+    const double* ZTc = POOL ? (const double*)(smem + L.zt) : p.ZT;
+    const double* Ac = POOL ? (const double*)(smem + L.ai) : p.Ainv;
+    const double* Cbc = POOL ? (const double*)(smem + L.cb) : p.Cb;
+    double* sS = (double*)(smem + L.ss) + (size_t)warp * RB * 32;
+    const double* Zs_c = p.ztab ? (const double*)(smem + L.zs) : p.Zs;
+    const int32_t* zj0_c = p.ztab ? (const int32_t*)(smem + L.zj) : p.zj0;
     const int zstride = p.ztab ? nsp : ns;  // row stride of Zs / zj0 per learner
     const IdxT* idx = (const IdxT*)p.idx;
-    const bool timed = p.timing && blockIdx.x == 0 && pipe == 0 && tid == 0;
+    const bool timed = p.timing && blockIdx.x == 0 && tid == 0;
     long long tA = 0, tB = 0, tC = 0, tD = 0, tm = 0;
+    __shared__ int ks_sh[2];
+    __shared__ double best_sh[2];
 
-    // ---- prologue (whole CTA): pool staging ------------------------------------------
+    // ---- prologue: pool staging, plan tables, I8 offset f0 = mean(y) --------
     if (POOL) {
         const uint4* src = (const uint4*)p.permt;
-        uint4* dst = (uint4*)(smem + PLo.permt);
+        uint4* dst = (uint4*)(smem + L.permt);
         const int nv = (int)((sizeof(PermT) * (size_t)p.permt_cap) / 16);
-        for (int a = threadIdx.x; a < nv; a += T) dst[a] = __ldg(src + a);
-        for (int a = threadIdx.x; a < K * W * d; a += T) ((double*)(smem + PLo.zt))[a] = __ldg(p.ZT + a);
-        for (int a = threadIdx.x; a < K * d * d; a += T) ((double*)(smem + PLo.ai))[a] = __ldg(p.Ainv + a);
-        for (int a = threadIdx.x; a < K * d * 4; a += T) ((double*)(smem + PLo.cb))[a] = __ldg(p.Cb + a);
-        for (int a = threadIdx.x; a < K * d; a += T) ((int32_t*)(smem + PLo.lw))[a] = __ldg(p.lwin + 2 * a);
+        for (int a = tid; a < nv; a += T) dst[a] = __ldg(src + a);
+        for (int a = tid; a < K * W * d; a += T) ((double*)(smem + L.zt))[a] = __ldg(p.ZT + a);
+        for (int a = tid; a < K * d * d; a += T) ((double*)(smem + L.ai))[a] = __ldg(p.Ainv + a);
+        for (int a = tid; a < K * d * 4; a += T) ((double*)(smem + L.cb))[a] = __ldg(p.Cb + a);
+        for (int a = tid; a < K * d; a += T) ((int32_t*)(smem + L.lw))[a] = __ldg(p.lwin + 2 * a);
     }
     if (p.ztab) {
-        double* zd = (double*)(smem + PLo.zs);
-        int32_t* jd = (int32_t*)(smem + PLo.zj);
-        for (int a = threadIdx.x; a < K * ns; a += T) {
+        double* zd = (double*)(smem + L.zs);
+        int32_t* jd = (int32_t*)(smem + L.zj);
+        for (int a = tid; a < K * ns; a += T) {
             const int k = a / ns, l = a - k * ns;
 #pragma unroll
             for (int q = 0; q < CWB_SPW; q++) zd[((size_t)k * nsp + l) * CWB_SPW + q] = __ldg(p.Zs + (size_t)a * CWB_SPW + q);
             jd[k * nsp + l] = __ldg(p.zj0 + a);
         }
     }
-    __syncthreads();
     const int32_t* pl = p.plan;
     const int rounds = pl[1], n_comb = pl[2];
-    const int RM = plan_rounds_max(KS, Tp);
+    const int RM = plan_rounds_max(KS, T);
     const int32_t* tt_dest = pl + 8;
-    const int32_t* wl = tt_dest + RM * Tp;
+    const int32_t* wl = tt_dest + RM * T;
     const int32_t* wb = wl + RM * NW;
     const int32_t* comb_g = wb + RM * NW;
     const int32_t* comb_first = comb_g + KS;
     const int32_t* comb_cnt = comb_first + KS;
-    const int* lwc = POOL ? (const int32_t*)(smem + PLo.lw) : nullptr;
+    for (int a = tid; a < RB * (K * nsp + W); a += T) U[a] = 0.0;  // empty / padding bins keep u = 0
+    for (int a = tid; a < RB * K * d; a += T) agg[a] = 0.0;
+    for (int a = tid; a < RB * kPadRows; a += T) r[n * RB + a] = 0.0;
 
-    // ---- prologue (per pipeline): I8 offset f0 = mean(y), r = y - f0 ------
-    for (int a = tid; a < K * nsp + W; a += Tp) U[a] = 0.0;  // empty / padding bins keep u = 0
-    for (int a = tid; a < K * d; a += Tp) agg[a] = 0.0;
-    for (int a = tid; a < kPadRows; a += Tp) r[n + a] = 0.0;
-    double f0;
+    double f0[RB];
     {
-        double part = 0.0;
+        double part[RB];
         bool bad = false;
-        for (int i = tid; i < n; i += Tp) {
-            const double v = live ? p.Y[(size_t)b * n + i] : 0.0;
-            bad |= !isfinite(v);
-            r[i] = v;
-            part += v;
+#pragma unroll
+        for (int q = 0; q < RB; q++) part[q] = 0.0;
+        for (int i = tid; i < n; i += T) {
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const double v = (b0 + q < p.B) ? p.Y[(size_t)(b0 + q) * n + i] : 0.0;
+                bad |= !isfinite(v);
+                r[i * RB + q] = v;
+                part[q] += v;
+            }
         }
         if (bad) cwb_dev_fail(p.status, CWB_ENONFINITE);
-        part = warp_sum(part);
-        if (lane == 0) red[warp] = part;
-        pipe_sync<PIPES>(pipe, Tp);
-        double sy = 0.0;
-        for (int w = 0; w < NW; w++) sy += red[w];
-        f0 = sy / (double)n;
-        part = 0.0;
-        for (int i = tid; i < n; i += Tp) {
-            const double v = r[i] - f0;
-            r[i] = v;
-            part += v * v;
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+            part[q] = warp_sum(part[q]);
+            if (lane == 0) red[q * 32 + warp] = part[q];
         }
-        pipe_sync<PIPES>(pipe, Tp);  // everyone has read red[] for f0
-        red[Tp + tid] = part;         // rr_0 -> parity 1
-        pipe_sync<PIPES>(pipe, Tp);
-    }
-    if (PIPES == 2 && pipe == 1 && p.M > 1) {
-        // start the second pipeline about half an iteration later, so that its gathers (phase
-        // A) overlap the latency-bound phases B-D of the first one instead of coinciding
-        const long long t0 = clock64();
-        while (clock64() - t0 < (long long)p.stagger) { }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+            double sy = 0.0;
+            for (int w = 0; w < NW; w++) sy += red[q * 32 + w];
+            f0[q] = sy / (double)n;
+            part[q] = 0.0;
+        }
+        for (int i = tid; i < n; i += T) {
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const double v = r[i * RB + q] - f0[q];
+                r[i * RB + q] = v;
+                part[q] += v * v;
+            }
+        }
+        __syncthreads();  // everyone has read red[] for f0
+#pragma unroll
+        for (int q = 0; q < RB; q++) red[(RB + q) * T + tid] = part[q];  // rr_0 -> parity 1
+        __syncthreads();
     }
     if (timed) tm = clock64();
 
-    // Bookkeeping of iteration mp (one warp): theta_agg[k*] += nu theta* (P:L838), traces k*,
-    // SSE = rr_mp - delta* and risk = rr_(mp+1) / (2n), rr_m = sum of the per-thread partials
-    // of r^T r before the update of iteration m (parity (m+1) & 1).  Runs in phase A of
-    // iteration mp + 1 on warp 0 (least H1 work, lowest issue priority), off the critical path.
-    auto bookkeeping = [&](int mp) {
-        const int kb = ks_sh[0];
-        if (lane < d) agg[kb * d + lane] += p.nu * thall[kb * 32 + lane];
+    // Bookkeeping of iteration mp for replication q (one warp): theta_agg[k*] += nu theta*
+    // (P:L838), traces k*, SSE = rr_mp - delta* and risk = rr_(mp+1) / (2n), with rr_m the
+    // per-thread partials of r^T r before the update of iteration m (parity (m+1) & 1).
+    // Runs in phase A of iteration mp + 1 on the first warps (least H1 work, lowest issue
+    // priority), off the critical path.
+    auto bookkeeping = [&](int mp, int q) {
+        const int b = b0 + q, kb = ks_sh[q];
+        if (lane < d) agg[(q * K + kb) * d + lane] += p.nu * thall[(kb * RB + q) * 32 + lane];
         double s0 = 0.0, s1 = 0.0;
-        for (int t = lane; t < Tp; t += 32) {
-            s0 += red[((mp + 1) & 1) * Tp + t];
-            s1 += red[(mp & 1) * Tp + t];
+        for (int t = lane; t < T; t += 32) {
+            s0 += red[((mp + 1) & 1) * RB * T + q * T + t];
+            s1 += red[(mp & 1) * RB * T + q * T + t];
         }
         const double rr0 = warp_sum(s0), rr1 = warp_sum(s1);
-        if (lane == 0 && live) {
+        if (lane == 0 && b < p.B) {
             if (p.k_trace) p.k_trace[(size_t)mp * p.B + b] = kb;
-            if (p.sse_trace) p.sse_trace[(size_t)mp * p.B + b] = rr0 - best_sh[0];
+            if (p.sse_trace) p.sse_trace[(size_t)mp * p.B + b] = rr0 - best_sh[q];
             if (p.risk_trace) p.risk_trace[(size_t)mp * p.B + b] = rr1 * p.inv2n;
         }
     };
 
     for (int m = 0; m < p.M; m++) {
-        if (m > 0 && warp == 0) bookkeeping(m - 1);
-        // ---- A / H1: u_k(l) = sum of r over bin l, conflict-free gather schedule --
+        if (m > 0 && warp < RB) bookkeeping(m - 1, warp);
+        // ---- A / H1: each lane sums its task, 4 steps per offset load ------------------
         for (int rd = 0; rd < rounds; rd++) {
             const int steps = __ldg(wl + rd * NW + warp);  // warp-uniform
             if (steps == 0) continue;
             const PermT* pt = permt + __ldg(wb + rd * NW + warp) + lane * 4;
-            double a0 = 0.0, a1 = 0.0;
+            double a0[RB], a1[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) { a0[q] = 0.0; a1[q] = 0.0; }
             // software pipeline: the offsets of groups g+2, g+3 load while groups g, g+1 gather
-            const int ng = steps >> 2;  // groups of 4 steps
+            // (steps are a multiple of 8; the schedule buffer has 2 groups of slack at its end)
+            const int ng = steps >> 2;  // groups of 4 steps, even
             Off4<PermT> oa = Off4<PermT>::template ld<POOL>(pt);
-            Off4<PermT> ob = ng > 1 ? Off4<PermT>::template ld<POOL>(pt + 128) : oa;
+            Off4<PermT> ob = Off4<PermT>::template ld<POOL>(pt + 128);
             for (int g = 0; g < ng; g += 2) {
-                Off4<PermT> na = oa, nb = ob;
-                if (g + 2 < ng) na = Off4<PermT>::template ld<POOL>(pt + (g + 2) * 128);
-                if (g + 3 < ng) nb = Off4<PermT>::template ld<POOL>(pt + (g + 3) * 128);
-                const double v0 = lds_at(rb, oa.o0), v1 = lds_at(rb, oa.o1);
-                const double v2 = lds_at(rb, oa.o2), v3 = lds_at(rb, oa.o3);
-                if (g + 1 < ng) {
-                    const double v4 = lds_at(rb, ob.o0), v5 = lds_at(rb, ob.o1);
-                    const double v6 = lds_at(rb, ob.o2), v7 = lds_at(rb, ob.o3);
-                    a0 += v0; a1 += v1; a0 += v2; a1 += v3;
-                    a0 += v4; a1 += v5; a0 += v6; a1 += v7;
-                } else {
-                    a0 += v0; a1 += v1; a0 += v2; a1 += v3;
+                const Off4<PermT> na = Off4<PermT>::template ld<POOL>(pt + (g + 2) * 128);
+                const Off4<PermT> nb = Off4<PermT>::template ld<POOL>(pt + (g + 3) * 128);
+                const RV<RB> v0 = RV<RB>::ld(rb, oa.o0), v1 = RV<RB>::ld(rb, oa.o1);
+                const RV<RB> v2 = RV<RB>::ld(rb, oa.o2), v3 = RV<RB>::ld(rb, oa.o3);
+                const RV<RB> v4 = RV<RB>::ld(rb, ob.o0), v5 = RV<RB>::ld(rb, ob.o1);
+                const RV<RB> v6 = RV<RB>::ld(rb, ob.o2), v7 = RV<RB>::ld(rb, ob.o3);
+#pragma unroll
+                for (int q = 0; q < RB; q++) {
+                    a0[q] += v0[q]; a1[q] += v1[q]; a0[q] += v2[q]; a1[q] += v3[q];
+                    a0[q] += v4[q]; a1[q] += v5[q]; a0[q] += v6[q]; a1[q] += v7[q];
                 }
                 oa = na;
                 ob = nb;
             }
-            const int dest = __ldg(tt_dest + rd * Tp + tid);
-            if (dest >= 0) U[dest] = a0 + a1;
-            else if (dest != kDiscard) pc[-dest - 1] = a0 + a1;
-        }
-        if (n_comb) {  // bins cut into pieces: combine in piece order
-            pipe_sync<PIPES>(pipe, Tp);
-            for (int c = tid; c < n_comb; c += Tp) {
-                const int f = __ldg(comb_first + c), cnt = __ldg(comb_cnt + c), g = __ldg(comb_g + c);
-                double v = pc[f];
-                for (int e = 1; e < cnt; e++) v += pc[f + e];
-                U[g] = v;
+            const int dest = __ldg(tt_dest + rd * T + tid);
+            double* dp = dest >= 0 ? U + (size_t)dest * RB : (dest != kDiscard ? pc + (size_t)(-dest - 1) * RB : nullptr);
+            if (dp) {
+                if (RB == 2) *reinterpret_cast<double2*>(dp) = make_double2(a0[0] + a1[0], a0[RB - 1] + a1[RB - 1]);
+                else dp[0] = a0[0] + a1[0];
             }
         }
-        pipe_sync<PIPES>(pipe, Tp);
+        if (n_comb) {  // bins cut into pieces: combine in piece order
+            __syncthreads();
+            for (int c = tid; c < n_comb; c += T) {
+                const int f = __ldg(comb_first + c), cnt = __ldg(comb_cnt + c), g = __ldg(comb_g + c);
+#pragma unroll
+                for (int q = 0; q < RB; q++) {
+                    double v = pc[f * RB + q];
+                    for (int e = 1; e < cnt; e++) v += pc[(f + e) * RB + q];
+                    U[g * RB + q] = v;
+                }
+            }
+        }
+        __syncthreads();
         if (timed) tm = phase_mark(&tA, tm, true);
         // ---- B / H2-H4, one warp per learner, lane j = coefficient j:
         //      s = Zb^T u (window of basis j), theta = (G + lambda D)^-1 s (cached inverse,
         //      P:L846), c = C^T theta, delta = |c|^2 = 2 theta^T s - theta^T G theta ------
         for (int k = warp; k < K; k += NW) {
-            double sv = 0.0;
+            double sv[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) sv[q] = 0.0;
             __syncwarp();  // sS reuse
             if (lane < d) {
                 const double* zt = ZTc + (size_t)k * W * d + lane;
-                const int lb = POOL ? lwc[k * d + lane] : __ldg(p.lwin + 2 * (k * d + lane));
-                const double* uk = U + (size_t)k * nsp + lb;
+                const int lb = POOL ? ((const int32_t*)(smem + L.lw))[k * d + lane] : __ldg(p.lwin + 2 * (k * d + lane));
+                const double* uk = U + ((size_t)k * nsp + lb) * RB;
 #pragma unroll 4
                 for (int w = 0; w < W; w++) {
                     const double z = POOL ? zt[w * d] : __ldg(zt + w * d);
-                    sv = fma(z, uk[w], sv);
+#pragma unroll
+                    for (int q = 0; q < RB; q++) sv[q] = fma(z, uk[w * RB + q], sv[q]);
                 }
             }
-            sS[lane] = sv;  // lanes >= d store 0
+#pragma unroll
+            for (int q = 0; q < RB; q++) sS[q * 32 + lane] = sv[q];  // lanes >= d store 0
             __syncwarp();
-            double t0 = 0.0, t1 = 0.0;
+            double t0[RB], t1[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) { t0[q] = 0.0; t1[q] = 0.0; }
             if (lane < d) {
                 const double* Ak = Ac + (size_t)k * d * d + lane;  // A^-1 symmetric: column j = row j
                 int jp = 0;
@@ -354,13 +365,17 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 for (; jp + 2 <= d; jp += 2) {
                     const double a0 = POOL ? Ak[jp * d] : __ldg(Ak + jp * d);
                     const double a1 = POOL ? Ak[(jp + 1) * d] : __ldg(Ak + (jp + 1) * d);
-                    const double2 s2 = *reinterpret_cast<const double2*>(sS + jp);
-                    t0 = fma(a0, s2.x, t0);
-                    t1 = fma(a1, s2.y, t1);
+#pragma unroll
+                    for (int q = 0; q < RB; q++) {
+                        const double2 s2 = *reinterpret_cast<const double2*>(sS + q * 32 + jp);
+                        t0[q] = fma(a0, s2.x, t0[q]);
+                        t1[q] = fma(a1, s2.y, t1[q]);
+                    }
                 }
                 if (jp < d) {
                     const double a0 = POOL ? Ak[jp * d] : __ldg(Ak + jp * d);
-                    t0 = fma(a0, sS[jp], t0);
+#pragma unroll
+                    for (int q = 0; q < RB; q++) t0[q] = fma(a0, sS[q * 32 + jp], t0[q]);
                 }
             }
             double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
@@ -368,80 +383,104 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 const double* cbj = Cbc + ((size_t)k * d + lane) * 4;
                 c0 = cbj[0]; c1 = cbj[1]; c2 = cbj[2]; c3 = cbj[3];
             }
-            const double th = t0 + t1;  // 0 on lanes >= d
-            const double h1 = __shfl_down_sync(0xffffffffu, th, 1);
-            const double h2 = __shfl_down_sync(0xffffffffu, th, 2);
-            const double h3 = __shfl_down_sync(0xffffffffu, th, 3);
-            const double c = fma(c3, h3, fma(c2, h2, fma(c1, h1, c0 * th)));
-            const double v = warp_sum(c * c);
-            thall[k * 32 + lane] = th;
-            if (lane == 0) delta[k] = v;
-        }
-        pipe_sync<PIPES>(pipe, Tp);
-        if (timed) tm = phase_mark(&tB, tm, true);
-        // ---- C / H5: per 32-point slice (one warp each): k* = argmax delta (lowest k on
-        //      ties), then zhat = nu Zb_k* theta_k* on its design points ------------
-        for (int sl = warp; sl * 32 < ns; sl += NW) {
-            double best = -INFINITY;
-            int kb = 0;
-            for (int k = lane; k < K; k += 32) {
-                const double v = delta[k];
-                if (v > best) { best = v; kb = k; }
-            }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
-                if (ob > best || (ob == best && ok < kb)) { best = ob; kb = ok; }
+            for (int q = 0; q < RB; q++) {
+                const double th = t0[q] + t1[q];  // 0 on lanes >= d
+                const double h1 = __shfl_down_sync(0xffffffffu, th, 1);
+                const double h2 = __shfl_down_sync(0xffffffffu, th, 2);
+                const double h3 = __shfl_down_sync(0xffffffffu, th, 3);
+                const double c = fma(c3, h3, fma(c2, h2, fma(c1, h1, c0 * th)));
+                const double v = warp_sum(c * c);
+                thall[(k * RB + q) * 32 + lane] = th;
+                if (lane == 0) delta[k * RB + q] = v;
             }
-            const int l = sl * 32 + lane;
-            if (l < ns) {
-                const double* tk = thall + kb * 32;
-                const int a = zj0_c[(size_t)kb * zstride + l];
-                const double2* zs = reinterpret_cast<const double2*>(Zs_c + ((size_t)kb * zstride + l) * CWB_SPW);
-                const double2 za = zs[0], zb = zs[1];
-                double v = za.x * tk[a];
-                if (a + 1 < d) v += za.y * tk[a + 1];
-                if (a + 2 < d) v += zb.x * tk[a + 2];
-                if (a + 3 < d) v += zb.y * tk[a + 3];
-                zhat[l] = p.nu * v;
-            }
-            if (sl == 0 && lane == 0) { ks_sh[0] = kb; best_sh[0] = best; }
         }
-        pipe_sync<PIPES>(pipe, Tp);
+        __syncthreads();
+        if (timed) tm = phase_mark(&tB, tm, true);
+        // ---- C / H5: job (q, slice): k* = argmax delta (lowest k on ties) for
+        //      replication q, then zhat = nu Zb_k* theta_k* on design points slice*32 + lane ------
+        {
+            const int nslice = (ns + 31) >> 5;
+            for (int job = warp; job < RB * nslice; job += NW) {
+                const int q = job % RB, sl = job / RB;
+                double best = -INFINITY;
+                int kb = 0;
+                for (int k = lane; k < K; k += 32) {
+                    const double v = delta[k * RB + q];
+                    if (v > best) { best = v; kb = k; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
+                    if (ob > best || (ob == best && ok < kb)) { best = ob; kb = ok; }
+                }
+                const int l = sl * 32 + lane;
+                if (l < ns) {
+                    const double* tk = thall + (kb * RB + q) * 32;
+                    const int a = zj0_c[(size_t)kb * zstride + l];
+                    const double2* zs = reinterpret_cast<const double2*>(Zs_c + ((size_t)kb * zstride + l) * CWB_SPW);
+                    const double2 za = zs[0], zb = zs[1];
+                    double v = za.x * tk[a];
+                    if (a + 1 < d) v += za.y * tk[a + 1];
+                    if (a + 2 < d) v += zb.x * tk[a + 2];
+                    if (a + 3 < d) v += zb.y * tk[a + 3];
+                    zhat[q * nsp + l] = p.nu * v;
+                }
+                if (sl == 0 && lane == 0) { ks_sh[q] = kb; best_sh[q] = best; }
+            }
+        }
+        __syncthreads();
         if (timed) tm = phase_mark(&tC, tm, true);
         // ---- D / H6: r_i -= zhat[idx_k*(i)], per-thread r^T r partials -------------
         {
-            const IdxT* ik = idx + (size_t)ks_sh[0] * n;
-            double acc = 0.0;
-            for (int i0 = tid; i0 < n; i0 += 4 * Tp) {
-                uint32_t j[4];
+            const int parw = m & 1;
+            const IdxT* ik0 = idx + (size_t)ks_sh[0] * n;
+            const IdxT* ik1 = idx + (size_t)ks_sh[RB - 1] * n;
+            double acc[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) acc[q] = 0.0;
+            for (int i0 = tid; i0 < n; i0 += 4 * T) {
+                uint32_t j0[4], j1[4];
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
-                    const int i = i0 + e * Tp;
-                    j[e] = i < n ? (uint32_t)__ldg(ik + i) : 0u;
+                    const int i = i0 + e * T;
+                    j0[e] = i < n ? (uint32_t)__ldg(ik0 + i) : 0u;
+                    j1[e] = (RB == 2 && i < n) ? (uint32_t)__ldg(ik1 + i) : 0u;
                 }
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
-                    const int i = i0 + e * Tp;
+                    const int i = i0 + e * T;
                     if (i < n) {
-                        const double v = r[i] - zhat[j[e]];
-                        r[i] = v;
-                        acc = fma(v, v, acc);
+                        if (RB == 1) {
+                            const double v = r[i] - zhat[j0[e]];
+                            r[i] = v;
+                            acc[0] = fma(v, v, acc[0]);
+                        } else {
+                            double2 v = *reinterpret_cast<double2*>(r + 2 * i);
+                            v.x -= zhat[j0[e]];
+                            v.y -= zhat[nsp + j1[e]];
+                            *reinterpret_cast<double2*>(r + 2 * i) = v;
+                            acc[0] = fma(v.x, v.x, acc[0]);
+                            acc[RB - 1] = fma(v.y, v.y, acc[RB - 1]);
+                        }
                     }
                 }
             }
-            red[(m & 1) * Tp + tid] = acc;
+#pragma unroll
+            for (int q = 0; q < RB; q++) red[(parw * RB + q) * T + tid] = acc[q];
         }
-        pipe_sync<PIPES>(pipe, Tp);
+        __syncthreads();
         if (timed) tm = phase_mark(&tD, tm, true);
     }
-    if (p.M > 0 && warp == 0) bookkeeping(p.M - 1);
-    pipe_sync<PIPES>(pipe, Tp);  // agg complete
-    if (live) {
-        for (int a = tid; a < K * d; a += Tp) p.agg_out[(size_t)b * K * d + a] = agg[a];
-        if (tid == 0 && p.offset_out) p.offset_out[b] = f0;
-    }
+    if (p.M > 0 && warp < RB) bookkeeping(p.M - 1, warp);
+    __syncthreads();  // agg complete
+#pragma unroll
+    for (int q = 0; q < RB; q++)
+        if (b0 + q < p.B) {
+            for (int a = tid; a < K * d; a += T) p.agg_out[(size_t)(b0 + q) * K * d + a] = agg[q * K * d + a];
+            if (tid == 0 && p.offset_out) p.offset_out[b0 + q] = f0[q];
+        }
     if (timed) {
         p.timing[0] = tA; p.timing[1] = tB; p.timing[2] = tC; p.timing[3] = tD;
     }
@@ -491,7 +530,7 @@ __device__ int block_scan_excl(int* a, int N, int* wsum) {
 // tasks, sorts the tasks by length (descending, ties by bin order; coarse
 // buckets), deals them to the T threads of the fused kernel in snake order and
 // groups the rows of every task by colour (bank group, row mod G) for the
-// scheduler.  Deterministic; runs once per (data set, Tp).
+// scheduler.  Deterministic; runs once per (data set, RB, T).
 template <typename SrcPermT>
 __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __restrict__ perm, int K, int ns,
                              int nsp, int n, int T, int P, int G, int32_t* __restrict__ plan,
@@ -602,8 +641,8 @@ __global__ void k_fused_plan(const int32_t* __restrict__ off, const SrcPermT* __
             const unsigned lt = mask & ((1u << tid) - 1u);
             if (valid) {
                 const int srk = (int)(hist[bk] + run_b[bk] + __popc(lt));
-                // snake order with the longest tasks on the HIGHEST thread ids: the warp
-                // scheduler issues highest-warp-id first, so the critical-path warps get priority
+                // snake order with the longest tasks on the HIGHEST thread ids (the warp
+                // scheduler issues highest-warp-id first: critical-path warps get priority)
                 const int rd = srk / T, i = srk - rd * T;
                 const int th = (rd & 1) ? i : (T - 1 - i);
                 tt_dest[rd * T + th] = s_dest[t];
@@ -727,7 +766,7 @@ __global__ void k_fused_wl(int32_t* __restrict__ plan, const int32_t* __restrict
     for (int e = threadIdx.x; e < RM * NW; e += blockDim.x) {
         int st = 0;
         for (int g = 0; g < gpw; g++) st = max(st, gsteps[e * gpw + g]);
-        wl[e] = (st + 3) / 4 * 4;
+        wl[e] = (st + 7) / 8 * 8;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -769,21 +808,21 @@ __global__ void k_fused_pack(const int32_t* __restrict__ plan, const int32_t* __
     }
 }
 
-template <typename IdxT, typename PermT, int PIPES, bool POOL, int MAXT, int MINB>
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB>
 int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
-    auto kern = k_train_fused<IdxT, PermT, PIPES, POOL, MAXT, MINB>;
+    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -1;
-    const int grid = (fp.B + PIPES - 1) / PIPES;
+    const int grid = (fp.B + RB - 1) / RB;
     kern<<<grid, T, smem, s>>>(fp);
     return 0;
 }
 
 template <typename IdxT, typename PermT>
-int launch_sel(const FusedParams& fp, int T, int pipes, bool pool, size_t smem, cudaStream_t s) {
-    if (pipes == 2) {
-        if (pool) return launch_t<IdxT, PermT, 2, true, 768, 1>(fp, T, smem, s);
-        return launch_t<IdxT, PermT, 2, false, 768, 1>(fp, T, smem, s);
+int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s) {
+    if (RB == 2) {
+        if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1>(fp, T, smem, s);
+        return launch_t<IdxT, PermT, 2, false, 512, 1>(fp, T, smem, s);
     }
     if (T <= 384) {
         if (pool) return launch_t<IdxT, PermT, 1, true, 384, 2>(fp, T, smem, s);
@@ -799,44 +838,42 @@ static const size_t kMaxSmem = 227 * 1024;
 static const size_t kTwoCtaSmem = 113 * 1024;
 
 struct FusedShape {
-    int pipes = 0, Tp = 0, T = 0, P = 0, permt_bytes = 2;
-    bool pool = false, ztab = false;
-    size_t smem = 0, lim = 0;
+    int RB = 0, T = 0, P = 0, permt_bytes = 2;
+    bool pool = false;
+    size_t cap = 0, smem = 0;
 };
 
-static size_t fused_bytes(const cwb_ctx* c, const FusedShape& f, int n_multi, bool pool, size_t pbytes, bool ztab) {
-    return PoolLayout(c->K, c->nsp, c->d, c->W, pool, pbytes, ztab).total +
-           (size_t)f.pipes * PipeLayout((int)c->n, c->K, c->nsp, c->d, c->W, n_multi, f.Tp).total;
-}
-
-// Launch shape for B replications: pipelines per CTA, threads per pipeline, shared-memory
-// limit.  false when the residuals do not fit (the caller then uses the general path).
+// Launch shape for B replications: RB replications per CTA, T threads, pool
+// tables in shared memory or not.  false when the residuals do not fit.
 static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
     if ((int64_t)c->K * c->n + 8 > INT32_MAX) return false;
     if ((int64_t)c->K * c->n_star * 16 > 200 * 1024) return false;  // plan kernel shared memory
-    struct Cand { int pipes, Tp; size_t lim; };
-    Cand cands[3];
+    const int KS = c->K * c->n_star;
+    struct Cand { int RB, T; size_t lim; };
+    Cand cands[4];
     int nc = 0;
     const int nsm = 148;
-    // more than one replication per SM: two pipelines per CTA sharing one copy of the pool
-    if (B > nsm) cands[nc++] = {2, 32 * std::max(8, std::min(12, c->K)), kMaxSmem};
+    if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};                     // ~2 replications per SM: one CTA
     if (B > nsm) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
     cands[nc++] = {1, c->n >= 8192 ? 768 : 512, kMaxSmem};
     for (int i = 0; i < nc; i++) {
         FusedShape f;
-        f.pipes = cands[i].pipes;
-        f.Tp = cands[i].Tp;
-        f.T = f.pipes * f.Tp;
-        f.lim = cands[i].lim;
-        f.permt_bytes = 8 * (c->n + kPadRows) <= 65535 ? 2 : 4;
-        // task size: balance the K*n rows over the Tp threads of a pipeline, but do not cut
-        // bins of up to 1.6x the mean bin size (a cut bin costs a combine pass)
-        f.P = std::max(4, (int)std::max((c->K * c->n + f.Tp - 1) / f.Tp, (int64_t)(1.6 * c->n / c->n_star)));
-        const size_t need = fused_bytes(c, f, 2 * f.Tp, false, 0, false);
-        if (need <= f.lim) {
-            f.smem = need;
-            *out = f;
-            return true;
+        f.RB = cands[i].RB;
+        f.T = cands[i].T;
+        const int64_t stride = 8 * f.RB;
+        f.permt_bytes = stride * (c->n + kPadRows) <= 65535 ? 2 : 4;
+        // task size: balance the K*n rows over T threads, but do not cut bins of up to
+        // 1.6x the mean bin size (a cut bin costs a combine pass)
+        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
+        f.cap = permt_bound(KS, f.T, f.P);
+        for (int pool = 1; pool >= 0; pool--) {
+            SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, false);
+            if (L.total <= cands[i].lim) {
+                f.pool = pool != 0;
+                f.smem = L.total;
+                *out = f;
+                return true;
+            }
         }
     }
     return false;
@@ -849,13 +886,13 @@ size_t cwb_fused_smem_bytes(const cwb_ctx* c) {
 
 // (Re)builds the H1 task plan for the shape of a B-replication launch.
 static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
-    if (c->fused_T == f.Tp && c->fused_P == f.P && c->plan) return CWB_OK;
+    if (c->fused_T == f.T && c->fused_rb == f.RB && c->plan) return CWB_OK;
     cwb_release(c->plan, s);
     cwb_release(c->permt, s);
     c->plan = nullptr;
     c->permt = nullptr;
     c->fused_T = 0;
-    const int KS = c->K * c->n_star, T = f.Tp, G = 16;  // plan per pipeline; 8-byte rows
+    const int KS = c->K * c->n_star, T = f.T, G = 16 / f.RB;
     const int RM = plan_rounds_max(KS, T);
     const int n_groups = RM * T / G;
     const int SB = 2 * ((f.P + 3) / 4 * 4) + G;  // schedule steps bound per group
@@ -867,7 +904,7 @@ static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
     int32_t* sched = scratch + scratch_ints;
     int32_t* gsteps = sched + (size_t)n_groups * SB * G;
     const size_t psmem = sizeof(int) * 4 * (size_t)KS;
-    const int stride = 8;
+    const int stride = 8 * f.RB;
     if (c->perm_bytes == 2) {
         auto kern = k_fused_plan<uint16_t>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
@@ -898,8 +935,10 @@ static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
     CWB_CUDA_TRY(c, cudaMemcpyAsync(&dev_status, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CWB_CUDA_TRY(c, cudaStreamSynchronize(s));
     if (dev_status) return CWB_OK;  // reported by cwb_status
-    if (cwb_alloc(&c->permt, (size_t)f.permt_bytes * hdr[5] + 64, s) != cudaSuccess)
+    const size_t slack = (size_t)f.permt_bytes * kSlackEntries;  // prefetch overrun of the last block
+    if (cwb_alloc(&c->permt, (size_t)f.permt_bytes * hdr[5] + slack, s) != cudaSuccess)
         return cwb_set_error(c, CWB_ENOMEM, "fused plan allocation failed");
+    CWB_CUDA_TRY(c, cudaMemsetAsync((char*)c->permt + (size_t)f.permt_bytes * hdr[5], 0, slack, s));
     const int blocks = std::max(1, std::min(hdr[1] * (T / 32), 1184));
     if (f.permt_bytes == 2)
         k_fused_pack<uint16_t><<<blocks, 256, 0, s>>>(c->plan, scratch, sched, gsteps, KS, T, G, SB, (int)c->n,
@@ -911,7 +950,7 @@ static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
     rc = cwb_check_launch(c, "k_fused_pack");
     if (rc) return rc;
     c->fused_T = T;
-    c->fused_P = f.P;
+    c->fused_rb = f.RB;
     c->permt_bytes = f.permt_bytes;
     c->permt_entries = hdr[5];
     c->plan_multi = hdr[3];
@@ -932,26 +971,27 @@ int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M
     if (!fused_shape(c, B, &f)) return CWB_OK;  // does not fit: caller uses the general path
     int rc = fused_plan(c, f, s);
     if (rc) return rc;
-    if (c->fused_T != f.Tp) return CWB_OK;  // plan failed on the device: cwb_status reports it
+    if (c->fused_T != f.T) return CWB_OK;  // plan failed on the device: cwb_status reports it
     // pool staging levels with the exact schedule size: schedule + B tables, then Zs / zj0
-    const size_t pbytes = ((size_t)c->permt_entries * f.permt_bytes + 15) / 16 * 16;
+    const size_t lim = (f.RB == 1 && f.T <= 384) ? kTwoCtaSmem : kMaxSmem;
+    const size_t pbytes = ((size_t)(c->permt_entries + kSlackEntries) * f.permt_bytes + 15) / 16 * 16;
+    f.pool = false;
     const int nm = c->plan_multi;
-    f.smem = fused_bytes(c, f, nm, false, 0, false);
-    f.pool = f.ztab = false;
+    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, false).total;
+    bool ztab = false;
     for (int lvl = 2; lvl >= 1; lvl--) {
-        const size_t need = fused_bytes(c, f, nm, true, pbytes, lvl == 2);
-        if (need <= f.lim) {
+        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, lvl == 2);
+        if (L1.total <= lim) {
             f.pool = true;
-            f.ztab = lvl == 2;
-            f.smem = need;
+            ztab = lvl == 2;
+            f.smem = L1.total;
             break;
         }
     }
     FusedParams fp;
     fp.n = (int)c->n; fp.K = c->K; fp.ns = c->n_star; fp.nsp = c->nsp; fp.d = c->d; fp.M = M; fp.B = B; fp.nu = nu;
-    fp.n_multi = nm;
-    fp.ztab = f.ztab ? 1 : 0;
-    fp.stagger = c->stagger >= 0 ? c->stagger : 0;
+    fp.n_multi = c->plan_multi;
+    fp.ztab = ztab ? 1 : 0;
     fp.permt_cap = (int)(pbytes / f.permt_bytes);
     fp.Y = Y; fp.idx = c->idx; fp.permt = c->permt; fp.plan = c->plan; fp.zj0 = c->zj0; fp.Zs = c->Zs;
     fp.inv2n = 1.0 / (2.0 * (double)c->n);
@@ -961,10 +1001,10 @@ int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M
     fp.timing = c->timing;
     fp.status = c->d_status;
     const bool i8 = c->idx_bytes == 1, p16 = f.permt_bytes == 2;
-    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.pipes, f.pool, f.smem, s);
-    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.pipes, f.pool, f.smem, s);
-    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.pipes, f.pool, f.smem, s);
-    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.pipes, f.pool, f.smem, s);
+    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s);
     if (rc) return cwb_set_error(c, CWB_ECUDA, "fused kernel: cannot set shared memory size");
     c->launches++;
     c->fused_smem = f.smem;

@@ -75,10 +75,9 @@ struct cwb_ctx {
     int32_t* plan = nullptr;
     void* permt = nullptr;       // step-major task row ids (uint16 / uint32)
     int32_t permt_bytes = 2;
-    int32_t fused_T = 0, fused_P = 0, permt_entries = 0, plan_multi = 0;
+    int32_t fused_T = 0, fused_rb = 0, permt_entries = 0, plan_multi = 0;
     bool fused_pool = false;
     size_t fused_smem = 0;
-    int32_t stagger = 6000;      // fused kernel: start delay of pipeline 1 (cycles), tunable by env
     long long* timing = nullptr;  // optional device buffer: fused-kernel phase cycles (cwb_set_timing)
 
     cwb_train_ws ws;
