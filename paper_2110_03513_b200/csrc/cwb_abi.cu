@@ -158,7 +158,7 @@ void cwb_free(cwb_ctx* c) {
     cudaStream_t s = c->stream;
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
-                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->plan, c->permt,
+                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->plan, c->permt,
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
     delete c;
@@ -193,7 +193,7 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     ok &= cwb_alloc((void**)&c->hi, 8 * Ks, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->z, 8 * Ks * nss, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->bnd, 8 * Ks * (nss - 1), s) == cudaSuccess;
-    ok &= cwb_alloc(&c->idx, (size_t)c->idx_bytes * Ks * nn, s) == cudaSuccess;
+    ok &= cwb_alloc(&c->idx, (size_t)c->idx_bytes * Ks * nn + 16, s) == cudaSuccess;  // +16: bulk-copy slack
     ok &= cwb_alloc((void**)&c->cnt, 4 * Ks * nss, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&c->off, 4 * Ks * (nss + 1), s) == cudaSuccess;
     ok &= cwb_alloc(&c->perm, (size_t)c->perm_bytes * (Ks * nn + 8), s) == cudaSuccess;  // +8: vector-load padding

@@ -32,6 +32,10 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     int32_t* kstar = nullptr;  // Bp
     double* part = nullptr;    // row-block partial sums of squares
     int32_t n_part = 0;
+    double* narrow = nullptr;  // narrow find_best: per-row-range histograms
+    size_t narrow_bytes = 0;
+    double* colpart = nullptr; // column sums: per-row-block partials
+    size_t colpart_bytes = 0;
 };
 
 struct cwb_ctx {

@@ -16,53 +16,57 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "cwb_internal.cuh"
 
 namespace {
 
 constexpr int kRowsH6 = 256;  // rows per block in k_h6
 
-__global__ void k_center(const double* __restrict__ Y, int64_t n, int B, bool center, double* off_ws,
-                         double* offset_out, double* rr, int* status) {
-    const int b = blockIdx.x;
+// Column reductions over the n rows of each vector (I8): blocks of kColRows rows
+// write partial sums, k_center_fin adds them in block order (deterministic).
+constexpr int kColRows = 8192;
+
+__global__ void k_colsum(const double* __restrict__ Y, int64_t n, const double* __restrict__ f0, bool sq,
+                         double* __restrict__ part, int* status) {
+    const int b = blockIdx.y;
     const double* y = Y + (size_t)b * n;
-    __shared__ double red[32];
-    __shared__ double s_f0;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double f0 = 0.0;
-    if (center) {
-        double s = 0.0;
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += y[i];
-        s = warp_sum(s);
-        if (lane == 0) red[w] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int q = 0; q < nw; q++) t += red[q];
-            s_f0 = t / (double)n;
-        }
-        __syncthreads();
-        f0 = s_f0;
-        __syncthreads();
-    }
+    const int64_t r0 = (int64_t)blockIdx.x * kColRows, r1 = min(n, r0 + kColRows);
+    const double c = f0 ? f0[b] : 0.0;
     double s = 0.0;
     bool bad = false;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        double v = y[i] - f0;
-        bad |= !isfinite(y[i]);
-        s += v * v;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const double v = y[i];
+        bad |= !isfinite(v);
+        const double t = v - c;
+        s += sq ? t * t : v;
     }
     if (bad) cwb_dev_fail(status, CWB_ENONFINITE);
+    __shared__ double red[32];
     s = warp_sum(s);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (lane == 0) red[w] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int q = 0; q < nw; q++) t += red[q];
-        rr[b] = t;
-        off_ws[b] = f0;
-        if (offset_out) offset_out[b] = f0;
+        part[(size_t)b * gridDim.x + blockIdx.x] = t;
     }
+}
+
+// mode 0: out[b] = sum / n (mean, also written to offset_out); mode 1: out[b] = sum
+__global__ void k_center_fin(const double* __restrict__ part, int nblk, int B, int64_t n, int mode,
+                             double* __restrict__ out, double* offset_out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double t = 0.0;
+    for (int q = 0; q < nblk; q++) t += part[(size_t)b * nblk + q];
+    if (mode == 0) {
+        t = t / (double)n;
+        if (offset_out) offset_out[b] = t;
+    }
+    out[b] = t;
 }
 
 // Rt[i][b] = w_i (Y[b][i] - off[b]) for b < B, 0 for the padding columns
@@ -258,21 +262,190 @@ __global__ void k_dense_proj(const double* __restrict__ Zb, const double* __rest
     out[(size_t)b * d + j] = s;
 }
 
+// ---------------------------------------------------------------- narrow path
+// binMatVec sums for a few residual vectors (B <= 4), e.g. one
+// findBestBaselearner on a single residual: HBM-bound on the index vector.  A CTA
+// stages a chunk of the residual rows in shared memory; each warp streams one
+// learner's index vector over the chunk (coalesced), groups the lanes holding the
+// same bin (__match_any_sync), and the lowest lane of each group adds the group's
+// values, in lane order, into the warp's private histogram (distinct bins: no
+// conflicting writes, no atomics, deterministic).  Histograms of the row ranges go
+// to P[range][k][l][q] and are combined in range order by k_narrow_combine.
+// TMA bulk copies (cp.async.bulk, global -> shared) completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Staged chunk of residual rows (NB columns) and of the index slices of the CTA's LPC
+// learners.  TMA = true: 16-byte aligned chunks, one elected thread issues the bulk copies
+// of chunk j+1 while chunk j is processed (double buffer); otherwise plain loads.
+template <typename IdxT, int NB, bool TMA>
+__global__ void __launch_bounds__(256) k_h1_narrow(const double* __restrict__ R, int64_t n, int K, int ns,
+                                                    const IdxT* __restrict__ idx, int64_t rows_per_cta, int nc,
+                                                    double* __restrict__ P) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, LPC = T >> 5;
+    const int NBUF = TMA ? 2 : 1;
+    const size_t buf_bytes = sizeof(double) * (size_t)nc * NB + sizeof(IdxT) * (size_t)LPC * nc;  // 16-multiple
+    double* hist = (double*)((unsigned char*)sm + NBUF * buf_bytes) + (size_t)warp * ns * NB;
+    const int k0 = blockIdx.y * LPC, k = k0 + warp;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+    const int nchunks = (int)((r1 - r0 + nc - 1) / nc);
+    for (int a = lane; a < ns * NB; a += 32) hist[a] = 0.0;
+    auto rs_of = [&](int buf) { return (double*)((unsigned char*)sm + buf * buf_bytes); };
+    auto is_of = [&](int buf) { return (IdxT*)(rs_of(buf) + (size_t)nc * NB); };
+    // TMA: rows of the chunk copied in 16-byte units; residual tail rows (len % 2) by plain loads
+    auto issue = [&](int j) {
+        const int buf = j & 1;
+        const int64_t c0 = r0 + (int64_t)j * nc;
+        const int len = (int)min((int64_t)nc, r1 - c0);
+        const uint32_t rbytes = (uint32_t)((len * sizeof(double)) & ~(size_t)15);
+        const uint32_t ibytes = (uint32_t)((len * sizeof(IdxT) + 15) & ~(size_t)15);  // idx buffer has slack
+        int nl = min(LPC, K - k0);
+        mbar_expect_tx(&bars[buf], NB * rbytes + nl * ibytes);
+        for (int q = 0; q < NB; q++)
+            if (rbytes) bulk_g2s(rs_of(buf) + (size_t)q * nc, R + (size_t)q * n + c0, rbytes, &bars[buf]);
+        for (int w = 0; w < nl; w++)
+            bulk_g2s(is_of(buf) + (size_t)w * nc, idx + (size_t)(k0 + w) * n + c0, ibytes, &bars[buf]);
+    };
+    if (TMA) {
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0 && nchunks > 0) issue(0);
+    }
+    for (int j = 0; j < nchunks; j++) {
+        const int buf = TMA ? (j & 1) : 0;
+        const int64_t c0 = r0 + (int64_t)j * nc;
+        const int len = (int)min((int64_t)nc, r1 - c0);
+        double* rs = rs_of(buf);
+        IdxT* is = is_of(buf);
+        if (TMA) {
+            if (tid == 0 && j + 1 < nchunks) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(j + 1);
+            }
+            const int rt = len & 1;  // residual rows not covered by the 16-byte copy
+            if (rt && tid < NB) rs[(size_t)tid * nc + len - 1] = __ldg(R + (size_t)tid * n + c0 + len - 1);
+            mbar_wait(&bars[buf], (uint32_t)((j >> 1) & 1));
+            if (rt) __syncthreads();
+        } else {
+            __syncthreads();  // previous chunk consumed
+            for (int q = 0; q < NB; q++)
+                for (int i = tid; i < len; i += T) rs[(size_t)q * nc + i] = __ldg(R + (size_t)q * n + c0 + i);
+            for (int w = 0; w < LPC; w++) {
+                const IdxT* src = idx + (size_t)min(k0 + w, K - 1) * n + c0;
+#pragma unroll 4
+                for (int i = tid; i < len; i += T) is[w * nc + i] = __ldg(src + i);
+            }
+            __syncthreads();
+        }
+        if (k < K) {
+            const IdxT* iw = is + warp * nc;
+            constexpr int U4 = 4;  // warp-steps in flight: loads and MATCHes of 4 steps overlap
+            for (int i0 = 0; i0 < len; i0 += 32 * U4) {
+                uint32_t bin[U4];
+                unsigned peers[U4];
+                double v[U4][NB], sum[U4][NB];
+#pragma unroll
+                for (int u = 0; u < U4; u++) {
+                    const int i = i0 + u * 32 + lane;
+                    const bool valid = i < len;
+                    bin[u] = valid ? (uint32_t)iw[i] : 0xffffffffu;
+#pragma unroll
+                    for (int q = 0; q < NB; q++) { v[u][q] = valid ? rs[(size_t)q * nc + i] : 0.0; sum[u][q] = v[u][q]; }
+                }
+#pragma unroll
+                for (int u = 0; u < U4; u++) peers[u] = __match_any_sync(0xffffffffu, bin[u]);
+                // group sums in lane order, led by the lowest lane of each group
+                unsigned rem[U4];
+                bool lead[U4];
+#pragma unroll
+                for (int u = 0; u < U4; u++) {
+                    lead[u] = bin[u] != 0xffffffffu && (peers[u] & ((1u << lane) - 1u)) == 0u;
+                    rem[u] = lead[u] ? (peers[u] & (peers[u] - 1u)) : 0u;
+                }
+                while (__any_sync(0xffffffffu, (rem[0] | rem[1] | rem[2] | rem[3]) != 0u)) {
+#pragma unroll
+                    for (int u = 0; u < U4; u++) {
+                        const int src = rem[u] ? __ffs(rem[u]) - 1 : lane;
+#pragma unroll
+                        for (int q = 0; q < NB; q++) {
+                            const double x = __shfl_sync(0xffffffffu, v[u][q], src);
+                            if (rem[u]) sum[u][q] += x;
+                        }
+                        rem[u] &= rem[u] - 1u;
+                    }
+                }
+                // histogram updates in step order (a bin may recur in a later step, led by another lane)
+#pragma unroll
+                for (int u = 0; u < U4; u++) {
+                    if (lead[u])
+#pragma unroll
+                        for (int q = 0; q < NB; q++) hist[bin[u] * NB + q] += sum[u][q];
+                    __syncwarp();
+                }
+            }
+        }
+        if (TMA) __syncthreads();  // buffer j&1 is refilled by the copy issued in iteration j+1
+    }
+    __syncwarp();
+    if (k < K)
+        for (int a = lane; a < ns * NB; a += 32) P[((size_t)blockIdx.x * K + k) * ns * NB + a] = hist[a];
+}
+
+// U[(k*ns + l)*Bp + q] = sum over row ranges (fixed order) of P[range][k][l][q]; columns >= NB are 0
+__global__ void k_narrow_combine(const double* __restrict__ P, int nranges, int K, int ns, int NB, int Bp,
+                                 double* __restrict__ U) {
+    const int64_t tot = (int64_t)K * ns * Bp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(e % Bp);
+        const int64_t g = e / Bp;  // k * ns + l
+        double v = 0.0;
+        if (q < NB)
+            for (int c = 0; c < nranges; c++) v += P[((size_t)c * K * ns + g) * NB + q];
+        U[e] = v;
+    }
+}
+
 }  // namespace
 
 // ===================================================================== host
 
-static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s) {
+static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true) {
     cwb_train_ws& w = c->ws;
     const int Bp = (B + 31) / 32 * 32;
     const int nblk = (int)((c->n + kRowsH6 - 1) / kRowsH6);
-    if (w.Bp >= Bp && w.B >= B && w.Rt) return CWB_OK;
+    if (w.Bp >= Bp && w.B >= B && w.U && (w.Rt || !need_rt)) return CWB_OK;
     cwb_release(w.Rt, s); cwb_release(w.U, s); cwb_release(w.theta, s); cwb_release(w.delta, s);
     cwb_release(w.rr, s); cwb_release(w.zhat, s); cwb_release(w.kstar, s); cwb_release(w.part, s);
+    cwb_release(w.narrow, s);
+    cwb_release(w.colpart, s);
     w = cwb_train_ws();
     const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
     bool ok = true;
-    ok &= cwb_alloc((void**)&w.Rt, sizeof(double) * n * Bp, s) == cudaSuccess;
+    if (need_rt) ok &= cwb_alloc((void**)&w.Rt, sizeof(double) * n * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.U, sizeof(double) * K * ns * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.theta, sizeof(double) * K * d * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.delta, sizeof(double) * K * Bp, s) == cudaSuccess;
@@ -300,6 +473,31 @@ static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_
     c->launches++;
 }
 
+// f0[b] = mean (center) and rr[b] = sum (y - f0)^2 of the B vectors Y[b][n] (I8)
+static int column_stats(cwb_ctx* c, const double* Y, int B, bool center, double* f0, double* rr,
+                        double* offset_out, cudaStream_t s) {
+    cwb_train_ws& w = c->ws;
+    const int nblk = (int)((c->n + kColRows - 1) / kColRows);
+    const size_t need = sizeof(double) * (size_t)nblk * B;
+    if (w.colpart_bytes < need) {
+        cwb_release(w.colpart, s);
+        w.colpart = nullptr;
+        w.colpart_bytes = 0;
+        if (cwb_alloc((void**)&w.colpart, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "column statistics workspace allocation failed");
+        w.colpart_bytes = need;
+    }
+    if (center) {
+        k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, nullptr, false, w.colpart, c->d_status);
+        k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nblk, B, c->n, 0, f0, offset_out);
+        c->launches += 2;
+    }
+    k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, center ? f0 : nullptr, true, w.colpart, c->d_status);
+    k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nblk, B, c->n, 1, rr, nullptr);
+    c->launches += 2;
+    return CWB_OK;
+}
+
 // one findBestBaselearner on the residual columns of ws.Rt
 static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg, int32_t* k_trace,
                            double* sse_trace, int32_t* k_out, double* theta_out, double* sse_out,
@@ -314,15 +512,85 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
     c->launches += 2;
 }
 
+template <typename IdxT, int NB>
+static void launch_narrow(bool tma, const double* R, int64_t n, int K, int ns, const void* idx, int64_t rpc, int nc,
+                          int nranges, int groups, size_t smem, double* P, cudaStream_t s) {
+    if (tma) {
+        auto kern = k_h1_narrow<IdxT, NB, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<dim3(nranges, groups), 256, smem, s>>>(R, n, K, ns, (const IdxT*)idx, rpc, nc, P);
+    } else {
+        auto kern = k_h1_narrow<IdxT, NB, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<dim3(nranges, groups), 256, smem, s>>>(R, n, K, ns, (const IdxT*)idx, rpc, nc, P);
+    }
+}
+
+// findBestBaselearner for B <= 4 residual vectors: narrow H1 + combine, then the general H2-H5
+static int find_best_narrow(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                            double* sse_out, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s, false);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int K = c->K, ns = c->n_star, LPC = 8, groups = (K + LPC - 1) / LPC;
+    const size_t hist = sizeof(double) * (size_t)LPC * ns * B;
+    const size_t per_row = sizeof(double) * B + (size_t)c->idx_bytes * LPC;  // staged bytes per chunk row
+    // TMA bulk copies need 16-byte aligned chunk starts: n a multiple of 16 rows, R 16-byte aligned
+    const bool tma = (c->n % 16) == 0 && ((uintptr_t)R & 15) == 0;
+    const int nbuf = tma ? 2 : 1;
+    if (hist + nbuf * per_row * 512 > 200 * 1024) return CWB_EUNSUPPORTED;
+    int nc = 16384;  // rows staged per chunk, within ~110 KB (two CTAs per SM) if possible
+    while (nc > 512 && hist + nbuf * per_row * nc > 110 * 1024) nc >>= 1;
+    while (nc > 512 && hist + nbuf * per_row * nc > 200 * 1024) nc >>= 1;
+    int nranges = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + groups - 1) / groups, (c->n + nc - 1) / nc));
+    const int64_t rpc = ((c->n + nranges - 1) / nranges + 15) / 16 * 16;  // 16-row aligned range starts
+    nranges = (int)((c->n + rpc - 1) / rpc);
+    const size_t need = sizeof(double) * (size_t)nranges * K * ns * B;
+    if (w.narrow_bytes < need) {
+        cwb_release(w.narrow, s);
+        w.narrow = nullptr;
+        w.narrow_bytes = 0;
+        if (cwb_alloc((void**)&w.narrow, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "narrow find_best workspace allocation failed");
+        w.narrow_bytes = need;
+    }
+    const size_t smem = hist + nbuf * per_row * nc;
+    rc = column_stats(c, R, B, false, nullptr, w.rr, nullptr, s);
+    if (rc) return rc;
+#define NARROW_CASE(IT)                                                                                          \
+    switch (B) {                                                                                                 \
+        case 1: launch_narrow<IT, 1>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
+        case 2: launch_narrow<IT, 2>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
+        case 3: launch_narrow<IT, 3>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
+        default: launch_narrow<IT, 4>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
+    }
+    if (c->idx_bytes == 1) NARROW_CASE(uint8_t) else NARROW_CASE(uint16_t)
+#undef NARROW_CASE
+    const int64_t tot = (int64_t)K * ns * w.Bp;
+    k_narrow_combine<<<(unsigned)std::min<int64_t>(4 * 1184, (tot + 255) / 256), 256, 0, s>>>(w.narrow, nranges, K, ns,
+                                                                                           B, w.Bp, w.U);
+    k_h234<<<dim3(K, w.Bp / 32), 256, 0, s>>>(w.U, w.Bp, ns, c->d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+                                              w.delta);
+    k_h5<<<(w.Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, K, c->d, B, w.Bp, 0.0, 0, w.kstar, nullptr,
+                                            nullptr, nullptr, k_out, theta_out, sse_out);
+    c->launches += 5;
+    return cwb_check_launch(c, "narrow find_best kernels");
+}
+
 int cwb_find_best_general(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
                           double* sse_out, cudaStream_t s) {
+    if (B <= 4 && c->path != 2) {
+        const int rc = find_best_narrow(c, R, B, k_out, theta_out, sse_out, s);
+        if (rc != CWB_EUNSUPPORTED) return rc;
+    }
     int rc = ensure_ws(c, B, s);
     if (rc) return rc;
     cwb_train_ws& w = c->ws;
-    k_center<<<B, 256, 0, s>>>(R, c->n, B, false, w.rr + w.Bp, nullptr, w.rr, c->d_status);
+    rc = column_stats(c, R, B, false, nullptr, w.rr, nullptr, s);
+    if (rc) return rc;
     dim3 gt((unsigned)((c->n + 31) / 32), w.Bp / 32);
     k_tr_in<<<gt, dim3(32, 8), 0, s>>>(R, c->n, B, w.Bp, nullptr, nullptr, w.Rt);
-    c->launches += 2;
+    c->launches += 1;
     find_best_iter(c, B, 0.0, 0, nullptr, nullptr, nullptr, k_out, theta_out, sse_out, s);
     return cwb_check_launch(c, "find_best kernels");
 }
@@ -335,7 +603,8 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
     cwb_train_ws& w = c->ws;
     const int Bp = w.Bp;
     double* off_ws = w.rr + Bp;
-    k_center<<<B, 256, 0, s>>>(Y, c->n, B, true, off_ws, offset_out, w.rr, c->d_status);
+    rc = column_stats(c, Y, B, true, off_ws, w.rr, offset_out, s);
+    if (rc) return rc;
     dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
     k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
     const size_t nagg = (size_t)B * c->K * c->d;

@@ -159,7 +159,8 @@ def test_pool_errors():
 
 # ------------------------------------------------------------ find best
 
-@pytest.mark.parametrize("name,B", [("R0", 8), ("R1", 40), ("R2", 3)])
+@pytest.mark.parametrize("name,B", [("R0", 8), ("R1", 40), ("R2", 3), ("R0", 1), ("R1", 1), ("R1", 2), ("R2", 4),
+                                    ("R1", 5)])
 def test_find_best_matches_oracle(name, B):
     ds = S.make(name, reps=range(B))
     c = ds.cfg
@@ -167,6 +168,27 @@ def test_find_best_matches_oracle(name, B):
     pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
     R = ds.Y - ds.Y.mean(1, keepdims=True)
     R[0] *= 1e-3
+    k, th, sse = [host(t) for t in pg.find_best(dev(R))]
+    for b in range(B):
+        ko, tho, sseo, sall, gap = po.find_best(R[b])
+        if k[b] != ko:
+            assert gap / sseo <= 1e-10
+            continue
+        ok, e = close(th[b], tho, RTOL, scale=np.abs(tho).max())
+        assert ok, e
+        ok, e = close(sse[b], sseo, RTOL)
+        assert ok, e
+    pg.close()
+
+
+@pytest.mark.parametrize("name,B", [("R3", 1), ("R4", 2)])
+def test_find_best_narrow_full_size(name, B):
+    # the narrow (B <= 4) findBestBaselearner at full data size against Algorithm binMatVec
+    ds = S.make(name, reps=range(B))
+    c = ds.cfg
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    R = ds.Y - ds.Y.mean(1, keepdims=True)
     k, th, sse = [host(t) for t in pg.find_best(dev(R))]
     for b in range(B):
         ko, tho, sseo, sall, gap = po.find_best(R[b])

@@ -1,0 +1,31 @@
+"""Time cwb_find_best (one findBestBaselearner) on B residual vectors for a config.
+usage: python tools/findbest_timing.py R3 [B] [reps]"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import cwb_synth as S
+from paper_2110_03513_b200 import cwb
+
+name = sys.argv[1] if len(sys.argv) > 1 else "R3"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+c = S.CONFIGS[name]
+ds = S.make(c, reps=range(B))
+X = torch.as_tensor(ds.X, device="cuda")
+R = torch.as_tensor(ds.Y - ds.Y.mean(1, keepdims=True), device="cuda")
+pool = cwb.Pool(X, cwb.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots))
+for _ in range(3):
+    k, th, sse = pool.find_best(R)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(reps):
+    k, th, sse = pool.find_best(R)
+e1.record()
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / reps
+K, n = c.K, c.n
+idx_bytes = 1 if pool.n_star <= 256 else 2
+alg = K * n * idx_bytes + n * B * 8  # index vector + residuals, read once
+print(f"{name} B={B} find_best {us:.1f} us; K*n*B={K*n*B:.3g} evals -> {K*n*B/us/1e3:.3g} G evals/s; "
+      f"alg bytes {alg/1e6:.1f} MB -> {alg/us/1e3:.0f} GB/s")
