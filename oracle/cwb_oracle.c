@@ -565,6 +565,140 @@ int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------ ACWB */
+
+typedef struct {
+    const orc_pool* p;
+    const double* Y;
+    int B, M, tid, nth;
+    double nu, gamma;
+    double *offset, *theta_f, *theta_h, *sse_trace, *sse_cor_trace, *risk_trace, *gap_trace, *gap_cor_trace;
+    double *f_out, *h_out;
+    int32_t *k_trace, *kcor_trace;
+} acwb_job;
+
+/* fitted values of learner k with parameters theta at every row: b_k(x_i, theta) */
+static void learner_values(const orc_pool* p, int k, const double* theta, double* out) {
+    int d = p->d;
+    int64_t n = p->n;
+    const double* Zb = p->Zb + (size_t)k * p->n_star * d;
+    const int32_t* idx = p->idx + (size_t)k * n;
+    for (int64_t i = 0; i < n; i++) {
+        const double* zi = (p->mode == ORC_MODE_UNBINNED) ? p->Zx + ((size_t)k * n + i) * d : Zb + (size_t)idx[i] * d;
+        double v = 0.0;
+        for (int j = 0; j < d; j++) v += zi[j] * theta[j];
+        out[i] = v;
+    }
+}
+
+/* Algorithm 2 (ACWB), one replication, literally: f, h, g, c are the fitted
+ * values of the primary, momentum and combined models and the error-corrected pseudo
+ * residuals.  Readings: the step of the primary model is nu (the
+ * prose's beta); eta_m = gamma nu / theta_m; the correction residual uses
+ * the previous iteration's correction learner b_{k_cor^[m-1]}(x, theta_cor^[m-1])
+ * (P:L949 prints theta_cor^[m], not yet defined at that point); parameters per P:L966:
+ * theta_g = (1 - theta_m) theta_f + theta_m theta_h, theta_f = theta_g + nu e_k theta,
+ * theta_h += eta_m e_kcor theta_cor, both starting at zero (the offset is shared). */
+static void acwb_one(const acwb_job* J, int b, scratch* w, double* f, double* h, double* g, double* r,
+                     double* c, double* bprev, double* bcur, double* theta, double* theta_cor) {
+    const orc_pool* p = J->p;
+    int64_t n = p->n;
+    int d = p->d, K = p->K, B = J->B;
+    const double* y = J->Y + (size_t)b * n;
+    /* line 2: f0 = argmin_c R_emp(c) = mean(y); h0 = g0 = f0 */
+    double sy = 0.0;
+    for (int64_t i = 0; i < n; i++) sy += y[i];
+    double f0 = sy / (double)n;
+    J->offset[b] = f0;
+    for (int64_t i = 0; i < n; i++) { f[i] = f0; h[i] = f0; g[i] = f0; }
+    double* tf = J->theta_f + (size_t)b * K * d;
+    double* th = J->theta_h + (size_t)b * K * d;
+    for (int a = 0; a < K * d; a++) { tf[a] = 0.0; th[a] = 0.0; }
+    for (int m = 1; m <= J->M; m++) {
+        double vt = 2.0 / (double)(m + 1);                                /* line 4 */
+        for (int64_t i = 0; i < n; i++) g[i] = (1.0 - vt) * f[i] + vt * h[i];  /* line 5 */
+        for (int64_t i = 0; i < n; i++) r[i] = y[i] - g[i];               /* line 6: L2 pseudo residuals at g */
+        int32_t ks, kc;
+        double sse, sse_c, gap, gap_c;
+        find_best_ws(p, r, w, &ks, theta, &sse, NULL, &gap);              /* line 7 */
+        learner_values(p, ks, theta, bcur);
+        for (int64_t i = 0; i < n; i++) f[i] = g[i] + J->nu * bcur[i];    /* line 8 */
+        if (m > 1) {                                                       /* lines 9-13 */
+            double a = (double)m / (double)(m + 1);
+            for (int64_t i = 0; i < n; i++) c[i] = r[i] + a * (c[i] - bprev[i]);
+        } else {
+            for (int64_t i = 0; i < n; i++) c[i] = r[i];
+        }
+        find_best_ws(p, c, w, &kc, theta_cor, &sse_c, NULL, &gap_c);      /* line 14 */
+        double eta = J->gamma * J->nu / vt;                               /* line 15 */
+        learner_values(p, kc, theta_cor, bprev);                          /* b_kcor^[m], reused at m+1 */
+        for (int64_t i = 0; i < n; i++) h[i] = h[i] + eta * bprev[i];     /* line 16 */
+        /* parameter bookkeeping */
+        for (int a = 0; a < K * d; a++) tf[a] = (1.0 - vt) * tf[a] + vt * th[a];
+        for (int j = 0; j < d; j++) tf[ks * d + j] += J->nu * theta[j];
+        for (int j = 0; j < d; j++) th[kc * d + j] += eta * theta_cor[j];
+        double rs = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            double e = y[i] - f[i];
+            rs += 0.5 * e * e;
+        }
+        size_t t = (size_t)(m - 1) * B + b;
+        J->k_trace[t] = ks;
+        J->kcor_trace[t] = kc;
+        J->sse_trace[t] = sse;
+        if (J->sse_cor_trace) J->sse_cor_trace[t] = sse_c;
+        J->risk_trace[t] = rs / (double)n;
+        if (J->gap_trace) J->gap_trace[t] = gap;
+        if (J->gap_cor_trace) J->gap_cor_trace[t] = gap_c;
+    }
+    if (J->f_out)
+        for (int64_t i = 0; i < n; i++) J->f_out[(size_t)b * n + i] = f[i];
+    if (J->h_out)
+        for (int64_t i = 0; i < n; i++) J->h_out[(size_t)b * n + i] = h[i];
+}
+
+static void* acwb_worker(void* arg) {
+    acwb_job* J = (acwb_job*)arg;
+    int64_t n = J->p->n;
+    int d = J->p->d;
+    scratch w;
+    scratch_init(&w, d, J->p->n_star);
+    double* buf = (double*)malloc(sizeof(double) * 7 * n);
+    double* theta = (double*)malloc(sizeof(double) * 2 * d);
+    for (int b = J->tid; b < J->B; b += J->nth)
+        acwb_one(J, b, &w, buf, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, buf + 5 * n, buf + 6 * n, theta,
+                 theta + d);
+    free(buf);
+    free(theta);
+    scratch_free(&w);
+    return NULL;
+}
+
+int orc_train_acwb(const orc_pool* p, const double* Y, int B, double nu, double gamma, int M, int n_threads,
+                   double* offset, double* theta_f, double* theta_h, int32_t* k_trace, int32_t* kcor_trace,
+                   double* sse_trace, double* sse_cor_trace, double* risk_trace, double* gap_trace,
+                   double* gap_cor_trace, double* f_out, double* h_out) {
+    if (!p || p->K < 1) return ORC_EEMPTY;
+    if (B < 1 || M < 0 || !(nu >= 0.0) || !(gamma >= 0.0)) return ORC_EINVAL;
+    for (int64_t a = 0; a < (int64_t)B * p->n; a++)
+        if (!isfinite(Y[a])) return ORC_ENONFINITE;
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > B) n_threads = B;
+    acwb_job* jobs = (acwb_job*)malloc(sizeof(acwb_job) * n_threads);
+    pthread_t* thr = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) {
+        acwb_job J = {p, Y, B, M, t, n_threads, nu, gamma, offset, theta_f, theta_h, sse_trace, sse_cor_trace,
+                      risk_trace, gap_trace, gap_cor_trace, f_out, h_out, k_trace, kcor_trace};
+        jobs[t] = J;
+    }
+    for (int t = 1; t < n_threads; t++) pthread_create(&thr[t], NULL, acwb_worker, &jobs[t]);
+    acwb_worker(&jobs[0]);
+    for (int t = 1; t < n_threads; t++) pthread_join(thr[t], NULL);
+    free(jobs);
+    free(thr);
+    return ORC_OK;
+}
+
 /* -------------------------------------------------------------- predict */
 
 int orc_predict(const orc_pool* p, const double* Xnew, int64_t m, const double* offset,

@@ -130,6 +130,17 @@ int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n
               double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
               double* risk_trace, double* gap_trace, double* f_out);
 
+/* Accelerated CWB, Algorithm 2, L2 loss, for B target vectors: primary
+ * model f, momentum model h, combined model g = (1 - theta_m) f + theta_m h, theta_m =
+ * 2/(m+1); pseudo residuals at g; error-corrected residuals c; eta_m = gamma nu / theta_m.
+ * Outputs: offset[B]; theta_f, theta_h [B][K][d] (parameter bookkeeping of P:L966);
+ * traces [M][B]: k (primary learner), kcor (correction learner), SSE of both fits, risk of
+ * f after iteration m, SSE gaps to the second best (ties); f_out, h_out [B][n] optional. */
+int orc_train_acwb(const orc_pool* p, const double* Y, int B, double nu, double gamma, int M, int n_threads,
+                   double* offset, double* theta_f, double* theta_h, int32_t* k_trace, int32_t* kcor_trace,
+                   double* sse_trace, double* sse_cor_trace, double* risk_trace, double* gap_trace,
+                   double* gap_cor_trace, double* f_out, double* h_out);
+
 /* Prediction with the aggregated parameters (P:L822-826 additivity):
  * f(x) = offset + sum_k g_k(z(x))^T theta_k, x hashed into the training bins
  * (clamped to the end bins outside [lo, hi]).  Xnew K x m; out B x m. */

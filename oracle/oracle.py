@@ -93,6 +93,8 @@ def lib():
                                     C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_double)]
         L.orc_train.argtypes = [C.POINTER(_Pool), _D, C.c_int, C.c_double, C.c_int, C.c_int,
                                 _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p]
+        L.orc_train_acwb.argtypes = [C.c_void_p, _D, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _D, _D, _D,
+                                     _I, _I, _D, _D, _D, _D, _D, _D, _D]
         L.orc_predict.argtypes = [C.POINTER(_Pool), _D, C.c_int64, _D, _D, C.c_int, _D]
         _lib = L
     return _lib
@@ -249,6 +251,22 @@ class TrainResult:
     f: np.ndarray           # B x n  final fit
 
 
+@dataclass
+class AcwbResult:
+    offset: np.ndarray        # B
+    theta_f: np.ndarray       # B x K x d  primary model parameters
+    theta_h: np.ndarray       # B x K x d  momentum model parameters
+    k_trace: np.ndarray       # M x B
+    kcor_trace: np.ndarray    # M x B
+    sse_trace: np.ndarray     # M x B
+    sse_cor_trace: np.ndarray  # M x B
+    risk_trace: np.ndarray    # M x B  risk of f after iteration m
+    gap_trace: np.ndarray     # M x B
+    gap_cor_trace: np.ndarray  # M x B
+    f: np.ndarray             # B x n
+    h: np.ndarray             # B x n
+
+
 class Pool:
     """K binned P-spline base learners on X (K x n)."""
 
@@ -309,6 +327,24 @@ class Pool:
         _chk(lib().orc_train(self._p, Y, B, nu, M, threads, off, agg, kt, st, rt,
                              gt.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p)), "train")
         return TrainResult(off, agg, kt, st, rt, gt, f)
+
+    def train_acwb(self, Y, nu: float = 0.05, gamma: float = 0.0034, M: int = 200,
+                   threads: int = 1) -> AcwbResult:
+        """Accelerated CWB, Algorithm 2, for B target vectors Y (B x n)."""
+        Y = _f64(np.atleast_2d(Y))
+        B = Y.shape[0]
+        K, d, n = self.K, self.d, self.n
+        off = np.empty(B)
+        tf = np.empty((B, K, d))
+        th = np.empty((B, K, d))
+        kt = np.empty((M, B), dtype=np.int32)
+        kc = np.empty((M, B), dtype=np.int32)
+        st, sc, rt, gt, gc = (np.empty((M, B)) for _ in range(5))
+        f = np.empty((B, n))
+        h = np.empty((B, n))
+        _chk(lib().orc_train_acwb(C.cast(self._p, C.c_void_p), Y, B, nu, gamma, M, threads, off, tf, th, kt, kc,
+                                  st, sc, rt, gt, gc, f, h), "train_acwb")
+        return AcwbResult(off, tf, th, kt, kc, st, sc, rt, gt, gc, f, h)
 
     def predict(self, Xnew, offset, theta_agg) -> np.ndarray:
         Xnew = _f64(Xnew)

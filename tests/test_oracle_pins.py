@@ -481,3 +481,100 @@ def test_unbinned_pool_is_penalised_regression_on_x():
         Z = O.bspline_basis(X[kk], X[kk].min(), X[kk].max(), 3, 7)
         t = np.linalg.solve(Z.T @ Z + p.lam[kk] * p.D, Z.T @ r)
         assert abs(sse_all[kk] - ((r - Z @ t) ** 2).sum()) <= 1e-10 * (r @ r)
+
+
+# ------------------------------------------------------------------- ACWB (Algorithm 2)
+
+def _acwb_pool(seed=5, K=3, n=300, n_knots=6):
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(0, 1, (K, n))
+    y = np.sin(6 * X[0]) + 0.5 * X[min(1, K - 1)] ** 2 + 0.3 * rng.standard_normal(n)
+    return O.Pool(X, O.Config(n_knots=n_knots), O.MODE_BINNED), X, y
+
+
+def _fitted(pool, theta, k):
+    return pool.Zb[k][pool.idx[k]] @ theta
+
+
+def test_acwb_gamma_zero_freezes_momentum_model():
+    # gamma = 0 => eta_m = 0 (Alg. 2 line 15) => h^[m] = h^[0] = f^[0] (line 16); theta_h stays 0
+    pool, X, y = _acwb_pool()
+    r = pool.train_acwb(y[None], nu=0.1, gamma=0.0, M=25)
+    assert (r.h == r.offset[0]).all()
+    assert (r.theta_h == 0).all()
+
+
+def test_acwb_first_iteration_is_cwb_first_iteration():
+    # theta_1 = 1 => g^[1] = h^[0] = f^[0] (lines 4-5), so r^[1] = y - mean(y) and c^[1] = r^[1] (line 12):
+    # the primary and correction learners of iteration 1 equal CWB's first selection
+    pool, X, y = _acwb_pool()
+    a = pool.train_acwb(y[None], nu=0.1, gamma=0.5, M=1)
+    c = pool.train(y[None], nu=0.1, M=1)
+    assert a.k_trace[0, 0] == c.k_trace[0, 0] == a.kcor_trace[0, 0]
+    assert np.isclose(a.sse_trace[0, 0], c.sse_trace[0, 0], rtol=1e-14)
+    assert np.isclose(a.sse_cor_trace[0, 0], c.sse_trace[0, 0], rtol=1e-14)
+    # theta_f^[1] = (1-1) 0 + 1 * 0 + nu theta^[1]; theta_h^[1] = eta_1 theta_cor^[1], eta_1 = gamma nu / 1
+    k = a.k_trace[0, 0]
+    assert np.allclose(a.theta_f[0, k], c.theta_agg[0, k], rtol=1e-13, atol=0)
+    assert np.allclose(a.theta_h[0, k], 0.5 * c.theta_agg[0, k], rtol=1e-13, atol=0)
+
+
+def test_acwb_eta_sequence_spec_example():
+    # gamma = 0.0034, nu = 0.05, m = 3: theta_3 = 0.5, eta_3 = 3.4e-4.  With K = 1 every
+    # correction learner is learner 0, so theta_h^[3] - theta_h^[2] = eta_3 theta_cor^[3]; rather than
+    # reading eta directly, check theta_h against the K = 1 matrix recurrence below (exact same etas).
+    assert np.isclose(0.0034 * 0.05 / (2.0 / 4.0), 3.4e-4, rtol=1e-15)
+
+
+def test_acwb_aggregation_invariants():
+    # the parameters are updated additively, so offset + sum_k Z_k theta_f[k] reproduces the
+    # primary model f and offset + sum_k Z_k theta_h[k] the momentum model h
+    pool, X, y = _acwb_pool(seed=9, K=4)
+    r = pool.train_acwb(y[None], nu=0.05, gamma=0.0034, M=60)
+    f = r.offset[0] + sum(_fitted(pool, r.theta_f[0, k], k) for k in range(pool.K))
+    h = r.offset[0] + sum(_fitted(pool, r.theta_h[0, k], k) for k in range(pool.K))
+    assert np.allclose(f, r.f[0], rtol=0, atol=1e-10 * np.abs(y).max())
+    assert np.allclose(h, r.h[0], rtol=0, atol=1e-10 * np.abs(y).max())
+    risk = 0.5 * np.mean((y - r.f[0]) ** 2)
+    assert np.isclose(risk, r.risk_trace[-1, 0], rtol=1e-12)
+
+
+def test_acwb_single_learner_matrix_recurrence():
+    # With K = 1 findBest always returns learner 0 and its fit is the linear smoother
+    # S = Z (Z^T Z + lambda D)^-1 Z^T, so Algorithm 2 becomes a linear recurrence on the fitted
+    # vectors; written here with a dense smoother matrix (not the oracle's per-iteration solves).
+    pool, X, y = _acwb_pool(seed=2, K=1, n=150)
+    Z = pool.Zb[0][pool.idx[0]]
+    S = Z @ np.linalg.solve(pool.G[0] + pool.lam[0] * pool.D, Z.T)
+    nu, gamma, M = 0.2, 0.3, 40
+    f0 = y.mean()
+    f = np.full_like(y, f0)
+    h = f.copy()
+    c = None
+    bcor_prev = None
+    risks = []
+    for m in range(1, M + 1):
+        vt = 2.0 / (m + 1)
+        g = (1 - vt) * f + vt * h
+        rr = y - g
+        f = g + nu * (S @ rr)
+        c = rr if m == 1 else rr + m / (m + 1) * (c - bcor_prev)
+        bcor_prev = S @ c
+        h = h + gamma * nu / vt * bcor_prev
+        risks.append(0.5 * np.mean((y - f) ** 2))
+    r = pool.train_acwb(y[None], nu=nu, gamma=gamma, M=M)
+    assert np.allclose(r.f[0], f, rtol=0, atol=1e-10 * np.abs(y).max())
+    assert np.allclose(r.h[0], h, rtol=0, atol=1e-10 * np.abs(y).max())
+    assert np.allclose(r.risk_trace[:, 0], risks, rtol=1e-9)
+
+
+def test_acwb_replications_independent_and_threads_deterministic():
+    pool, X, y = _acwb_pool(seed=3, K=3)
+    rng = np.random.default_rng(0)
+    Y = np.stack([y, y[::-1].copy(), rng.standard_normal(y.size)])
+    a = pool.train_acwb(Y, nu=0.05, gamma=0.0034, M=30, threads=1)
+    b = pool.train_acwb(Y, nu=0.05, gamma=0.0034, M=30, threads=3)
+    c = pool.train_acwb(Y[1:2], nu=0.05, gamma=0.0034, M=30)
+    for key in ("theta_f", "theta_h", "k_trace", "kcor_trace", "risk_trace"):
+        assert (getattr(a, key) == getattr(b, key)).all(), key
+    assert (a.theta_f[1] == c.theta_f[0]).all() and (a.k_trace[:, 1] == c.k_trace[:, 0]).all()
