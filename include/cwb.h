@@ -158,6 +158,24 @@ int cwb_train(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M, do
               double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
               cudaStream_t stream);
 
+/* Accelerated CWB, Algorithm 2 ("ACWB"), L2 loss, for B target vectors Y[B][n]:
+ * primary model f, momentum model h, combined model g = (1 - t_m) f + t_m h with
+ * t_m = 2/(m+1); pseudo residuals at g; error-corrected residuals
+ * c^[m] = r^[m] + m/(m+1) (c^[m-1] - b_kcor^[m-1]); second findBestBaselearner on c;
+ * h += eta_m b_kcor with eta_m = gamma nu / t_m.  Readings: the primary step
+ * is nu (the prose's beta), the correction recursion uses the previous correction
+ * learner.  Outputs (device):
+ *   offset_out[B]
+ *   theta_f_out[B][K][d], theta_h_out[B][K][d]  parameters of f and h (bookkeeping of
+ *        theta_g = (1-t)theta_f + t theta_h; theta_f = theta_g + nu e_k theta;
+ *        theta_h += eta e_kcor theta_cor), so f = offset + sum_k Z_k theta_f[k]
+ *   k_trace, kcor_trace [M][B]  learners fitted to r and to c
+ *   sse_trace[M][B]             SSE of the fit to r;  risk_trace[M][B]  risk of f
+ * Trace pointers may be NULL.  Paper default gamma = 0.0034. */
+int cwb_train_acwb(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double gamma, int32_t M,
+                   double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
+                   int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t stream);
+
 /* Same as cwb_train but every array is a HOST pointer (X[K][n], Y[B][n] in,
  * the rest out); the host<->device copies are enqueued on `stream` and the
  * call synchronises before returning.  Builds and frees its own context. */

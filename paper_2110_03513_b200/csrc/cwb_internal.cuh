@@ -36,6 +36,8 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     size_t narrow_bytes = 0;
     double* colpart = nullptr; // column sums: per-row-block partials
     size_t colpart_bytes = 0;
+    double* acwb = nullptr;    // ACWB: F, H (n x Bq each), row-block partials, offsets
+    size_t acwb_bytes = 0;
 };
 
 struct cwb_ctx {
@@ -114,6 +116,9 @@ int cwb_fused_plan(cwb_ctx* ctx, cudaStream_t s);
 int cwb_train_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
                       double* offset_out, double* theta_agg_out, int32_t* k_trace,
                       double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_train_acwb_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double gamma, int32_t M,
+                           double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
+                           int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s);
 int cwb_find_best_general(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out,
                           double* theta_out, double* sse_out, cudaStream_t s);
 int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,

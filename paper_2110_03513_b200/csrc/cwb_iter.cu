@@ -190,9 +190,10 @@ __global__ void k_h5(const double* __restrict__ delta, const double* __restrict_
 }
 
 // nu * Zb_{k*} theta* at the design points, per (design point, replication)
+// columns b < B_nu are scaled by nu, columns B_nu <= b < B by nu2
 __global__ void k_zhat(const int32_t* __restrict__ kstar, const double* __restrict__ theta,
                        const int32_t* __restrict__ zj0, const double* __restrict__ Zs, int ns, int d,
-                       int B, int Bp, double nu, double* __restrict__ zhat) {
+                       int B, int Bp, double nu, int B_nu, double nu2, double* __restrict__ zhat) {
     const int b = blockIdx.y * 32 + (threadIdx.x & 31);
     const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (l >= ns) return;
@@ -205,7 +206,7 @@ __global__ void k_zhat(const int32_t* __restrict__ kstar, const double* __restri
         v = zs[0] * th[(size_t)a * Bp];
         for (int q = 1; q < CWB_SPW; q++)
             if (a + q < d) v += zs[q] * th[(size_t)(a + q) * Bp];
-        v *= nu;
+        v *= b < B_nu ? nu : nu2;
     }
     zhat[(size_t)l * Bp + b] = v;
 }
@@ -260,6 +261,118 @@ __global__ void k_dense_proj(const double* __restrict__ Zb, const double* __rest
     double s = 0.0;
     for (int l = 0; l < ns; l++) s += Zb[(size_t)l * d + j] * U[(size_t)l * Bp + b];
     out[(size_t)b * d + j] = s;
+}
+
+// ---------------------------------------------------------------- ACWB path
+// Accelerated CWB, Algorithm 2.  Replication b keeps, row-major with one
+// column per replication, F = y - f (primary model), H = y - h (momentum model); its
+// pseudo residuals r = y - g = (1 - theta_m) F + theta_m H (lines 5-6) and error-corrected
+// residuals c (lines 9-13) are the columns b and B + b of Rt, so binMatVec, fit and SSE
+// (k_h1, k_h234) run once on the 2B columns.
+
+// per replication: k = argmin SSE of column b (line 7), k_cor of column B + b (line 14),
+// traces, parameter bookkeeping of P:L966 (theta_g = (1 - vt) theta_f + vt theta_h,
+// theta_f = theta_g + nu e_k theta, theta_h += eta e_kcor theta_cor)
+__global__ void k_acwb_select(const double* __restrict__ delta, const double* __restrict__ theta,
+                              const double* __restrict__ rr, int K, int d, int B, int Bp, double nu, double vt,
+                              double eta, int m, int32_t* __restrict__ kstar, double* __restrict__ tf,
+                              double* __restrict__ th, int32_t* k_trace, int32_t* kcor_trace, double* sse_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    int ks = 0, kc = 0;
+    double best = delta[b], bestc = delta[B + b];
+    for (int k = 1; k < K; k++) {
+        const double v = delta[(size_t)k * Bp + b], vc = delta[(size_t)k * Bp + B + b];
+        if (v > best) { best = v; ks = k; }
+        if (vc > bestc) { bestc = vc; kc = k; }
+    }
+    kstar[b] = ks;
+    kstar[B + b] = kc;
+    double* f = tf + (size_t)b * K * d;
+    double* h = th + (size_t)b * K * d;
+    for (int a = 0; a < K * d; a++) f[a] = (1.0 - vt) * f[a] + vt * h[a];
+    for (int j = 0; j < d; j++) {
+        f[ks * d + j] += nu * theta[((size_t)ks * d + j) * Bp + b];
+        h[kc * d + j] += eta * theta[((size_t)kc * d + j) * Bp + B + b];
+    }
+    if (k_trace) k_trace[(size_t)m * B + b] = ks;
+    if (kcor_trace) kcor_trace[(size_t)m * B + b] = kc;
+    if (sse_trace) sse_trace[(size_t)m * B + b] = rr[b] - best;
+}
+
+// Rt[i][B + b] = Rt[i][b], F[i][b] = H[i][b] = Rt[i][b] (= y - f0: f = h = g = f0, line 2)
+__global__ void k_acwb_init(double* __restrict__ Rt, double* __restrict__ F, double* __restrict__ H, int64_t n,
+                            int B, int Bp, int Bq) {
+    const int b = blockIdx.y * 32 + (threadIdx.x & 31);
+    if (b >= B) return;
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+         i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const double v = Rt[(size_t)i * Bp + b];
+        Rt[(size_t)i * Bp + B + b] = v;
+        F[(size_t)i * Bq + b] = v;
+        H[(size_t)i * Bq + b] = v;
+    }
+}
+
+// line 8: F = r - nu b_k, line 16: H -= eta b_kcor; then the residuals of iteration m+1:
+// r' = (1 - vt1) F + vt1 H, c' = r' + a1 (c - b_kcor) (lines 4-6, 10); row-block partial
+// sums of F^2 (risk of f), r'^2 and c'^2 (r^T r of the next fits)
+template <typename IdxT>
+__global__ void k_acwb_update(double* __restrict__ Rt, double* __restrict__ F, double* __restrict__ H, int64_t n,
+                              int B, int Bp, int Bq, const int32_t* __restrict__ kstar, const IdxT* __restrict__ idx,
+                              const double* __restrict__ zhat, double eta, double vt1, double a1,
+                              double* __restrict__ part) {
+    __shared__ double red[3][8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const bool live = b < B;
+    const int ks = live ? kstar[b] : 0, kc = live ? kstar[B + b] : 0;
+    const IdxT* ik = idx + (size_t)ks * n;
+    const IdxT* ic = idx + (size_t)kc * n;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6, r1 = min(n, r0 + kRowsH6);
+    double sf = 0.0, sr = 0.0, sc = 0.0;
+    if (live)
+        for (int64_t i = r0 + w; i < r1; i += 8) {
+            const double r = Rt[(size_t)i * Bp + b], c = Rt[(size_t)i * Bp + B + b];
+            const double bk = zhat[(size_t)ik[i] * Bp + b];        // nu b_k (scaled by k_zhat)
+            const double bc = zhat[(size_t)ic[i] * Bp + B + b];    // b_kcor (unscaled)
+            const double Fi = r - bk;
+            const double Hi = H[(size_t)i * Bq + b] - eta * bc;
+            const double rn = (1.0 - vt1) * Fi + vt1 * Hi;
+            const double cn = rn + a1 * (c - bc);
+            F[(size_t)i * Bq + b] = Fi;
+            H[(size_t)i * Bq + b] = Hi;
+            Rt[(size_t)i * Bp + b] = rn;
+            Rt[(size_t)i * Bp + B + b] = cn;
+            sf += Fi * Fi;
+            sr += rn * rn;
+            sc += cn * cn;
+        }
+    red[0][w][lane] = sf;
+    red[1][w][lane] = sr;
+    red[2][w][lane] = sc;
+    __syncthreads();
+    if (w < 3 && live) {
+        double t = 0.0;
+        for (int q = 0; q < 8; q++) t += red[w][q][lane];
+        part[((size_t)w * gridDim.x + blockIdx.x) * Bq + b] = t;
+    }
+}
+
+// rr of the next fits (columns b, B + b) and risk of f after iteration m (R_emp = F^T F / (2n))
+__global__ void k_acwb_rr(const double* __restrict__ part, int nblk, int B, int Bq, int64_t n, int m,
+                          double* __restrict__ rr, double* risk_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double sf = 0.0, sr = 0.0, sc = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        sf += part[((size_t)0 * nblk + q) * Bq + b];
+        sr += part[((size_t)1 * nblk + q) * Bq + b];
+        sc += part[((size_t)2 * nblk + q) * Bq + b];
+    }
+    rr[b] = sr;
+    rr[B + b] = sc;
+    if (risk_trace) risk_trace[(size_t)m * B + b] = sf / (2.0 * (double)n);
 }
 
 // ---------------------------------------------------------------- narrow path
@@ -442,6 +555,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     cwb_release(w.rr, s); cwb_release(w.zhat, s); cwb_release(w.kstar, s); cwb_release(w.part, s);
     cwb_release(w.narrow, s);
     cwb_release(w.colpart, s);
+    cwb_release(w.acwb, s);
     w = cwb_train_ws();
     const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
     bool ok = true;
@@ -614,7 +728,7 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
     for (int m = 0; m < M; m++) {
         find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
-                                                                  c->n_star, c->d, B, Bp, nu, w.zhat);
+                                                                  c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
         dim3 g6(nblk, Bp / 32);
         if (c->idx_bytes == 1)
             k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
@@ -704,4 +818,64 @@ int cwb_bin_mat_mat_impl(const double* Zb, int32_t ns, int32_t d, const void* id
     cwb_release(ones, s);
     cwb_release(U, s);
     return rc;
+}
+
+// ===================================================================== ACWB host
+int cwb_train_acwb_general(cwb_ctx* c, const double* Y, int32_t B, double nu, double gamma, int32_t M,
+                           double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
+                           int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s) {
+    int rc = ensure_ws(c, 2 * B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp, Bq = (B + 31) / 32 * 32;
+    const int nblk = (int)((c->n + kRowsH6 - 1) / kRowsH6);
+    const size_t need = sizeof(double) * (2 * (size_t)c->n * Bq + 3 * (size_t)nblk * Bq + Bq);
+    if (w.acwb_bytes < need) {
+        cwb_release(w.acwb, s);
+        w.acwb = nullptr;
+        w.acwb_bytes = 0;
+        if (cwb_alloc((void**)&w.acwb, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "ACWB workspace allocation failed");
+        w.acwb_bytes = need;
+    }
+    double* F = w.acwb;
+    double* H = F + (size_t)c->n * Bq;
+    double* part = H + (size_t)c->n * Bq;
+    double* off_ws = part + 3 * (size_t)nblk * Bq;
+    // line 2: f0 = mean(y); f = h = g = f0; r^[1] = c^[1] = y - f0
+    rc = column_stats(c, Y, B, true, off_ws, w.rr, offset_out, s);
+    if (rc) return rc;
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
+    k_acwb_init<<<dim3((unsigned)std::min<int64_t>(2048, (c->n + 7) / 8), Bq / 32), 256, 0, s>>>(w.Rt, F, H, c->n, B,
+                                                                                                  Bp, Bq);
+    cudaMemcpyAsync(w.rr + B, w.rr, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
+    const size_t nagg = (size_t)B * c->K * c->d;
+    k_zero<<<(unsigned)std::min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_f_out, nagg);
+    k_zero<<<(unsigned)std::min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_h_out, nagg);
+    c->launches += 5;
+    for (int m = 1; m <= M; m++) {
+        const double vt = 2.0 / (double)(m + 1);              // line 4
+        const double eta = gamma * nu / vt;                   // line 15
+        const double vt1 = 2.0 / (double)(m + 2);             // next iteration's combination
+        const double a1 = (double)(m + 1) / (double)(m + 2);  // next iteration's correction weight
+        h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);  // lines 7 and 14: binMatVec
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G,
+                                                    w.theta, w.delta);
+        k_acwb_select<<<(B + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, vt, eta, m - 1,
+                                                      w.kstar, theta_f_out, theta_h_out, k_trace, kcor_trace,
+                                                      sse_trace);
+        k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, c->n_star, c->d,
+                                                                  2 * B, Bp, nu, B, 1.0, w.zhat);
+        dim3 g6(nblk, Bq / 32);
+        if (c->idx_bytes == 1)
+            k_acwb_update<uint8_t><<<g6, 256, 0, s>>>(w.Rt, F, H, c->n, B, Bp, Bq, w.kstar, (const uint8_t*)c->idx,
+                                                      w.zhat, eta, vt1, a1, part);
+        else
+            k_acwb_update<uint16_t><<<g6, 256, 0, s>>>(w.Rt, F, H, c->n, B, Bp, Bq, w.kstar, (const uint16_t*)c->idx,
+                                                       w.zhat, eta, vt1, a1, part);
+        k_acwb_rr<<<(B + 127) / 128, 128, 0, s>>>(part, nblk, B, Bq, c->n, m - 1, w.rr, risk_trace);
+        c->launches += 6;
+    }
+    return cwb_check_launch(c, "ACWB kernels");
 }

@@ -21,7 +21,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 # the exported symbols declared in include/cwb.h
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
-           "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_fit_host", "cwb_predict",
+           "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_train_acwb", "cwb_fit_host", "cwb_predict",
            "cwb_launch_count", "cwb_set_phase_timing", "cwb_free"]
 
 
@@ -80,6 +80,7 @@ def load() -> C.CDLL:
     L.cwb_set_path.argtypes = [_vp, _i32]
     L.cwb_find_best.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp]
     L.cwb_train.argtypes = [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.cwb_train_acwb.argtypes = [_vp, _vp, _i32, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_fit_host.argtypes = [_vp, _i64, _i32, C.POINTER(cwb_config), _vp, _i32, _f64, _i32,
                                _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_predict.argtypes = [_vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp]
@@ -247,6 +248,24 @@ def cwb_train(ctx, Y, nu: float = 0.05, M: int = 200, traces: bool = True, out=N
     return out
 
 
+def cwb_train_acwb(ctx, Y, nu: float = 0.05, gamma: float = 0.0034, M: int = 200, traces: bool = True):
+    """Accelerated CWB (Alg. 2) for Y[B][n].  Returns a dict of device tensors."""
+    import torch
+    Y = _dev_f64(Y, "Y")
+    ns, d, K, n = cwb_get_dims(ctx)
+    B = Y.shape[0]
+    f = dict(dtype=torch.float64, device=Y.device)
+    out = dict(offset=torch.empty(B, **f), theta_f=torch.empty((B, K, d), **f), theta_h=torch.empty((B, K, d), **f))
+    if traces:
+        out.update(k_trace=torch.empty((M, B), dtype=torch.int32, device=Y.device),
+                   kcor_trace=torch.empty((M, B), dtype=torch.int32, device=Y.device),
+                   sse_trace=torch.empty((M, B), **f), risk_trace=torch.empty((M, B), **f))
+    _chk(load().cwb_train_acwb(ctx, _ptr(Y), B, float(nu), float(gamma), M, _ptr(out["offset"]), _ptr(out["theta_f"]),
+                               _ptr(out["theta_h"]), _ptr(out.get("k_trace")), _ptr(out.get("kcor_trace")),
+                               _ptr(out.get("sse_trace")), _ptr(out.get("risk_trace")), _stream(Y)), ctx)
+    return out
+
+
 def cwb_fit_host(X, Y, cfg: Config | None = None, nu: float = 0.05, M: int = 200, stream=None):
     """Whole fit from HOST numpy arrays (copies inside the call)."""
     import numpy as np
@@ -309,6 +328,9 @@ class Pool:
 
     def find_best(self, R):
         return cwb_find_best(self.ctx, R)
+
+    def train_acwb(self, Y, nu=0.05, gamma=0.0034, M=200, traces=True):
+        return cwb_train_acwb(self.ctx, Y, nu, gamma, M, traces)
 
     def predict(self, Xnew, offset, theta_agg):
         return cwb_predict(self.ctx, Xnew, offset, theta_agg)
