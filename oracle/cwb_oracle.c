@@ -699,6 +699,216 @@ int orc_train_acwb(const orc_pool* p, const double* Y, int B, double nu, double 
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------ HCWB */
+
+/* weighted fit of learner k (w = 0/1 row mask, P:L870 observation weights):
+ * theta = (Z^T W Z + lambda D)^-1 Z^T W r, SSE = sum_i w_i (r_i - Z(i) theta)^2 */
+static double fit_one_w(const orc_pool* p, int k, const double* r, const double* w, const double* Lw, scratch* ws,
+                        double* theta) {
+    int d = p->d, n_star = p->n_star;
+    int64_t n = p->n;
+    const int32_t* idx = p->idx + (size_t)k * n;
+    const double* Zb = p->Zb + (size_t)k * n_star * d;
+    if (p->mode == ORC_MODE_BINNED) {
+        orc_bin_mat_vec(Zb, n_star, d, idx, w, r, n, ws->s);   /* P:L898-904 with weights */
+    } else {
+        const double* rows = (p->mode == ORC_MODE_DENSE) ? Zb : p->Zx + (size_t)k * n * d;
+        dense_ztwr_rows(rows, (p->mode == ORC_MODE_DENSE) ? idx : NULL, d, w, r, n, ws->s);
+    }
+    chol_fb(Lw + (size_t)k * d * d, d, ws->s, theta);
+    double sse = 0.0;
+    for (int64_t i = 0; i < n; i++) {
+        if (w[i] == 0.0) continue;
+        const double* zi = (p->mode == ORC_MODE_UNBINNED) ? p->Zx + ((size_t)k * n + i) * d : Zb + (size_t)idx[i] * d;
+        double v = 0.0;
+        for (int j = 0; j < d; j++) v += zi[j] * theta[j];
+        double e = r[i] - v;
+        sse += e * e;
+    }
+    return sse;
+}
+
+static void find_best_w(const orc_pool* p, const double* r, const double* w, const double* Lw, scratch* ws,
+                        int32_t* k_out, double* theta_out, double* sse_out, double* gap_out) {
+    int d = p->d, best = -1;
+    double best_sse = 0.0, second = INFINITY;
+    for (int k = 0; k < p->K; k++) {
+        double sse = fit_one_w(p, k, r, w, Lw, ws, ws->theta);
+        if (best < 0 || sse < best_sse) {
+            if (best >= 0) second = best_sse;
+            best = k;
+            best_sse = sse;
+            for (int j = 0; j < d; j++) theta_out[j] = ws->theta[j];
+        } else if (sse < second) {
+            second = sse;
+        }
+    }
+    *k_out = best;
+    *sse_out = best_sse;
+    if (gap_out) *gap_out = second - best_sse;
+}
+
+typedef struct {
+    const orc_pool* p;
+    const double* Y;
+    const double* wtr;   /* n: 1 = training row, 0 = validation row */
+    const double* Ltr;   /* K x d x d: Cholesky of Z^T W Z + lambda D (training rows) */
+    int B, M, pat0, tid, nth;
+    double nu, gamma;
+    double *offset, *theta_f, *sse_trace, *risk_trace, *val_risk_trace, *gap_trace, *gap_cor_trace, *f_out;
+    int32_t *k_trace, *kcor_trace, *switch_iter;
+} hcwb_job;
+
+/* Algorithm 3 (HCWB): updateACWB (Alg. 2 lines 4-16) on D_train while the
+ * validation-risk patience counter is below pat0, then updateCWB (Alg. 1 lines 4-10) on D.
+ * Readings: "if pat0 < pat" is read as "while the counter < pat0"; the
+ * counter increments when R_emp(f^[m] | D_val) > R_emp(f^[m-1] | D_val), else resets; one
+ * pool on D (bins, basis, lambda) with the training fits weighted by the training mask;
+ * f^[0] = mean of the training targets; after the switch CWB continues from f. */
+static void hcwb_one(const hcwb_job* J, int b, scratch* w, double* f, double* h, double* g, double* r, double* c,
+                     double* bprev, double* bcur, double* theta, double* theta_cor, double* th) {
+    const orc_pool* p = J->p;
+    int64_t n = p->n;
+    int d = p->d, K = p->K, B = J->B;
+    const double* y = J->Y + (size_t)b * n;
+    const double* wt = J->wtr;
+    double sy = 0.0, ntr = 0.0, nval = 0.0;
+    for (int64_t i = 0; i < n; i++) { sy += wt[i] * y[i]; ntr += wt[i]; nval += 1.0 - wt[i]; }
+    double f0 = sy / ntr;
+    J->offset[b] = f0;
+    for (int64_t i = 0; i < n; i++) { f[i] = f0; h[i] = f0; g[i] = f0; }
+    double* tf = J->theta_f + (size_t)b * K * d;
+    for (int a = 0; a < K * d; a++) { tf[a] = 0.0; th[a] = 0.0; }
+    double vrisk_prev = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        if (wt[i] == 0.0) { double e = y[i] - f[i]; vrisk_prev += 0.5 * e * e; }
+    vrisk_prev /= nval;
+    int pat = 0, accel = 1, ma = 0;  /* ma: ACWB iteration counter */
+    J->switch_iter[b] = J->M;
+    for (int m = 0; m < J->M; m++) {
+        int32_t ks, kc = -1;
+        double sse, gap, gap_c = 0.0;
+        size_t t = (size_t)m * B + b;
+        if (accel) {
+            ma++;
+            double vt = 2.0 / (double)(ma + 1);
+            for (int64_t i = 0; i < n; i++) g[i] = (1.0 - vt) * f[i] + vt * h[i];
+            for (int64_t i = 0; i < n; i++) r[i] = y[i] - g[i];
+            find_best_w(p, r, wt, J->Ltr, w, &ks, theta, &sse, &gap);
+            learner_values(p, ks, theta, bcur);
+            for (int64_t i = 0; i < n; i++) f[i] = g[i] + J->nu * bcur[i];
+            if (ma > 1) {
+                double a = (double)ma / (double)(ma + 1);
+                for (int64_t i = 0; i < n; i++) c[i] = r[i] + a * (c[i] - bprev[i]);
+            } else {
+                for (int64_t i = 0; i < n; i++) c[i] = r[i];
+            }
+            double sse_c;
+            find_best_w(p, c, wt, J->Ltr, w, &kc, theta_cor, &sse_c, &gap_c);
+            double eta = J->gamma * J->nu / vt;
+            learner_values(p, kc, theta_cor, bprev);
+            for (int64_t i = 0; i < n; i++) h[i] = h[i] + eta * bprev[i];
+            for (int a = 0; a < K * d; a++) tf[a] = (1.0 - vt) * tf[a] + vt * th[a];
+            for (int j = 0; j < d; j++) tf[ks * d + j] += J->nu * theta[j];
+            for (int j = 0; j < d; j++) th[kc * d + j] += eta * theta_cor[j];
+        } else {
+            for (int64_t i = 0; i < n; i++) r[i] = y[i] - f[i];
+            find_best_ws(p, r, w, &ks, theta, &sse, NULL, &gap);
+            learner_values(p, ks, theta, bcur);
+            for (int64_t i = 0; i < n; i++) f[i] = f[i] + J->nu * bcur[i];
+            for (int j = 0; j < d; j++) tf[ks * d + j] += J->nu * theta[j];
+        }
+        double rs = 0.0, vr = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            double e = y[i] - f[i];
+            rs += 0.5 * e * e;
+            if (wt[i] == 0.0) vr += 0.5 * e * e;
+        }
+        vr /= nval;
+        if (accel) {  /* Alg. 3 line 6 */
+            if (vr > vrisk_prev) pat++;
+            else pat = 0;
+            if (pat >= J->pat0) { accel = 0; J->switch_iter[b] = m + 1; }
+        }
+        vrisk_prev = vr;
+        J->k_trace[t] = ks;
+        J->kcor_trace[t] = kc;
+        J->sse_trace[t] = sse;
+        J->risk_trace[t] = rs / (double)n;
+        J->val_risk_trace[t] = vr;
+        if (J->gap_trace) J->gap_trace[t] = gap;
+        if (J->gap_cor_trace) J->gap_cor_trace[t] = gap_c;
+    }
+    if (J->f_out)
+        for (int64_t i = 0; i < n; i++) J->f_out[(size_t)b * n + i] = f[i];
+}
+
+static void* hcwb_worker(void* arg) {
+    hcwb_job* J = (hcwb_job*)arg;
+    int64_t n = J->p->n;
+    int d = J->p->d, K = J->p->K;
+    scratch w;
+    scratch_init(&w, d, J->p->n_star);
+    double* buf = (double*)malloc(sizeof(double) * 7 * n);
+    double* theta = (double*)malloc(sizeof(double) * (2 * d + (size_t)K * d));
+    for (int b = J->tid; b < J->B; b += J->nth)
+        hcwb_one(J, b, &w, buf, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, buf + 5 * n, buf + 6 * n, theta,
+                 theta + d, theta + 2 * d);
+    free(buf);
+    free(theta);
+    scratch_free(&w);
+    return NULL;
+}
+
+int orc_train_hcwb(const orc_pool* p, const double* Y, int B, const uint8_t* val_mask, double nu, double gamma,
+                   int pat0, int M, int n_threads, double* offset, double* theta_f, int32_t* k_trace,
+                   int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                   int32_t* switch_iter, double* gap_trace, double* gap_cor_trace, double* f_out) {
+    if (!p || p->K < 1) return ORC_EEMPTY;
+    if (B < 1 || M < 0 || pat0 < 1 || !(nu >= 0.0) || !(gamma >= 0.0)) return ORC_EINVAL;
+    int64_t n = p->n, ntr = 0;
+    int d = p->d, K = p->K;
+    for (int64_t a = 0; a < (int64_t)B * n; a++)
+        if (!isfinite(Y[a])) return ORC_ENONFINITE;
+    double* wtr = (double*)malloc(sizeof(double) * n);
+    for (int64_t i = 0; i < n; i++) { wtr[i] = val_mask[i] ? 0.0 : 1.0; ntr += val_mask[i] ? 0 : 1; }
+    if (ntr == 0 || ntr == n) { free(wtr); return ORC_EINVAL; }
+    /* training-row penalised normal matrices Z^T W Z + lambda D (binMatMat with weights) */
+    double* Ltr = (double*)malloc(sizeof(double) * (size_t)K * d * d);
+    double* A = (double*)malloc(sizeof(double) * d * d);
+    int st = ORC_OK;
+    for (int k = 0; k < K && st == ORC_OK; k++) {
+        const double* Zb = p->Zb + (size_t)k * p->n_star * d;
+        const int32_t* idx = p->idx + (size_t)k * n;
+        if (p->mode == ORC_MODE_BINNED) orc_bin_mat_mat(Zb, p->n_star, d, idx, wtr, n, A);
+        else {
+            const double* rows = (p->mode == ORC_MODE_DENSE) ? Zb : p->Zx + (size_t)k * n * d;
+            orc_dense_ztwz(rows, d, (p->mode == ORC_MODE_DENSE) ? idx : NULL, wtr, n, A);
+        }
+        for (int a = 0; a < d * d; a++) A[a] += p->lambda[k] * p->D[a];
+        st = orc_cholesky(A, d, Ltr + (size_t)k * d * d);
+    }
+    free(A);
+    if (st != ORC_OK) { free(wtr); free(Ltr); return ORC_ECALIB; }
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > B) n_threads = B;
+    hcwb_job* jobs = (hcwb_job*)malloc(sizeof(hcwb_job) * n_threads);
+    pthread_t* thr = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) {
+        hcwb_job J = {p, Y, wtr, Ltr, B, M, pat0, t, n_threads, nu, gamma, offset, theta_f, sse_trace, risk_trace,
+                      val_risk_trace, gap_trace, gap_cor_trace, f_out, k_trace, kcor_trace, switch_iter};
+        jobs[t] = J;
+    }
+    for (int t = 1; t < n_threads; t++) pthread_create(&thr[t], NULL, hcwb_worker, &jobs[t]);
+    hcwb_worker(&jobs[0]);
+    for (int t = 1; t < n_threads; t++) pthread_join(thr[t], NULL);
+    free(jobs);
+    free(thr);
+    free(wtr);
+    free(Ltr);
+    return ORC_OK;
+}
+
 /* -------------------------------------------------------------- predict */
 
 int orc_predict(const orc_pool* p, const double* Xnew, int64_t m, const double* offset,

@@ -141,6 +141,17 @@ int orc_train_acwb(const orc_pool* p, const double* Y, int B, double nu, double 
                    double* sse_trace, double* sse_cor_trace, double* risk_trace, double* gap_trace,
                    double* gap_cor_trace, double* f_out, double* h_out);
 
+/* Hybrid CWB, Algorithm 3: ACWB on the training rows (val_mask[i] == 0) while
+ * the validation-risk patience counter is below pat0, then CWB on all rows.  Outputs:
+ * offset[B] (mean of the training targets), theta_f[B][K][d] (final primary model);
+ * traces [M][B]: k (primary / CWB learner), kcor (-1 after the switch), SSE of the primary fit
+ * (training rows before the switch), risk of f on all rows, validation risk of f, SSE gaps;
+ * switch_iter[B] = first CWB iteration (0-based; M if none); f_out[B][n] optional. */
+int orc_train_hcwb(const orc_pool* p, const double* Y, int B, const uint8_t* val_mask, double nu, double gamma,
+                   int pat0, int M, int n_threads, double* offset, double* theta_f, int32_t* k_trace,
+                   int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                   int32_t* switch_iter, double* gap_trace, double* gap_cor_trace, double* f_out);
+
 /* Prediction with the aggregated parameters (P:L822-826 additivity):
  * f(x) = offset + sum_k g_k(z(x))^T theta_k, x hashed into the training bins
  * (clamped to the end bins outside [lo, hi]).  Xnew K x m; out B x m. */

@@ -95,6 +95,8 @@ def lib():
                                 _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p]
         L.orc_train_acwb.argtypes = [C.c_void_p, _D, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _D, _D, _D,
                                      _I, _I, _D, _D, _D, _D, _D, _D, _D]
+        L.orc_train_hcwb.argtypes = [C.c_void_p, _D, C.c_int, _P(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_double,
+                                     C.c_double, C.c_int, C.c_int, C.c_int, _D, _D, _I, _I, _D, _D, _D, _I, _D, _D, _D]
         L.orc_predict.argtypes = [C.POINTER(_Pool), _D, C.c_int64, _D, _D, C.c_int, _D]
         _lib = L
     return _lib
@@ -267,6 +269,21 @@ class AcwbResult:
     h: np.ndarray             # B x n
 
 
+@dataclass
+class HcwbResult:
+    offset: np.ndarray          # B
+    theta_f: np.ndarray         # B x K x d
+    k_trace: np.ndarray         # M x B
+    kcor_trace: np.ndarray      # M x B (-1 after the switch)
+    sse_trace: np.ndarray       # M x B
+    risk_trace: np.ndarray      # M x B  risk of f on all rows
+    val_risk_trace: np.ndarray  # M x B  risk of f on the validation rows
+    switch_iter: np.ndarray     # B
+    gap_trace: np.ndarray       # M x B
+    gap_cor_trace: np.ndarray   # M x B
+    f: np.ndarray               # B x n
+
+
 class Pool:
     """K binned P-spline base learners on X (K x n)."""
 
@@ -345,6 +362,24 @@ class Pool:
         _chk(lib().orc_train_acwb(C.cast(self._p, C.c_void_p), Y, B, nu, gamma, M, threads, off, tf, th, kt, kc,
                                   st, sc, rt, gt, gc, f, h), "train_acwb")
         return AcwbResult(off, tf, th, kt, kc, st, sc, rt, gt, gc, f, h)
+
+    def train_hcwb(self, Y, val_mask, nu: float = 0.05, gamma: float = 0.037, pat0: int = 5, M: int = 200,
+                   threads: int = 1) -> HcwbResult:
+        """Hybrid CWB, Algorithm 3; val_mask[n] = 1 for validation rows."""
+        Y = _f64(np.atleast_2d(Y))
+        B = Y.shape[0]
+        K, d, n = self.K, self.d, self.n
+        vm = np.ascontiguousarray(val_mask, dtype=np.uint8)
+        off = np.empty(B)
+        tf = np.empty((B, K, d))
+        kt = np.empty((M, B), dtype=np.int32)
+        kc = np.empty((M, B), dtype=np.int32)
+        st, rt, vt, gt, gc = (np.empty((M, B)) for _ in range(5))
+        sw = np.empty(B, dtype=np.int32)
+        f = np.empty((B, n))
+        _chk(lib().orc_train_hcwb(C.cast(self._p, C.c_void_p), Y, B, vm, nu, gamma, pat0, M, threads, off, tf, kt, kc,
+                                  st, rt, vt, sw, gt, gc, f), "train_hcwb")
+        return HcwbResult(off, tf, kt, kc, st, rt, vt, sw, gt, gc, f)
 
     def predict(self, Xnew, offset, theta_agg) -> np.ndarray:
         Xnew = _f64(Xnew)

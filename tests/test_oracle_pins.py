@@ -578,3 +578,79 @@ def test_acwb_replications_independent_and_threads_deterministic():
     for key in ("theta_f", "theta_h", "k_trace", "kcor_trace", "risk_trace"):
         assert (getattr(a, key) == getattr(b, key)).all(), key
     assert (a.theta_f[1] == c.theta_f[0]).all() and (a.k_trace[:, 1] == c.k_trace[:, 0]).all()
+
+
+# ------------------------------------------------------------------- HCWB (Algorithm 3)
+
+def _hcwb_reference_k1(pool, y, vm, nu, gamma, pat0, M):
+    """K = 1: the fits are linear smoothers, S_w = Z (Z^T W Z + lambda D)^-1 Z^T W on the training
+    rows before the switch, S = Z (Z^T Z + lambda D)^-1 Z^T on all rows after it."""
+    Z = pool.Zb[0][pool.idx[0]]
+    w = (vm == 0).astype(float)
+    lam, D = pool.lam[0], pool.D
+    Sw = Z @ np.linalg.solve(Z.T @ (w[:, None] * Z) + lam * D, (Z * w[:, None]).T)
+    S = Z @ np.linalg.solve(Z.T @ Z + lam * D, Z.T)
+    f0 = (w * y).sum() / w.sum()
+    f = np.full_like(y, f0)
+    h = f.copy()
+    c = bprev = None
+    val = vm == 1
+    vprev = 0.5 * np.mean((y[val] - f[val]) ** 2)
+    pat, accel, ma, switch = 0, True, 0, M
+    vr_trace = []
+    for m in range(M):
+        if accel:
+            ma += 1
+            vt = 2.0 / (ma + 1)
+            g = (1 - vt) * f + vt * h
+            r = y - g
+            f = g + nu * (Sw @ r)
+            c = r if ma == 1 else r + ma / (ma + 1) * (c - bprev)
+            bprev = Sw @ c
+            h = h + gamma * nu / vt * bprev
+        else:
+            f = f + nu * (S @ (y - f))
+        vr = 0.5 * np.mean((y[val] - f[val]) ** 2)
+        if accel:
+            pat = pat + 1 if vr > vprev else 0
+            if pat >= pat0:
+                accel, switch = False, m + 1
+        vprev = vr
+        vr_trace.append(vr)
+    return f, switch, np.array(vr_trace)
+
+
+def test_hcwb_single_learner_matches_smoother_formulation():
+    pool, X, y = _acwb_pool(seed=4, K=1, n=200)
+    rng = np.random.default_rng(7)
+    vm = (rng.uniform(size=y.size) < 0.3).astype(np.uint8)
+    for nu, gamma, pat0, M in [(0.3, 0.4, 2, 80), (0.1, 0.037, 5, 120), (0.5, 2.0, 1, 40)]:
+        f, switch, vr = _hcwb_reference_k1(pool, y, vm, nu, gamma, pat0, M)
+        r = pool.train_hcwb(y[None], vm, nu=nu, gamma=gamma, pat0=pat0, M=M)
+        assert r.switch_iter[0] == switch
+        assert np.allclose(r.f[0], f, rtol=0, atol=1e-9 * np.abs(y).max())
+        assert np.allclose(r.val_risk_trace[:, 0], vr, rtol=1e-8)
+
+
+def test_hcwb_switch_is_one_way_and_aggregation_holds():
+    pool, X, y = _acwb_pool(seed=11, K=4, n=400)
+    rng = np.random.default_rng(3)
+    vm = (rng.uniform(size=y.size) < 0.3).astype(np.uint8)
+    r = pool.train_hcwb(y[None], vm, nu=0.3, gamma=1.0, pat0=2, M=150)
+    s = r.switch_iter[0]
+    assert 0 < s < 150, "expected a switch with strong momentum"
+    assert (r.kcor_trace[:s, 0] >= 0).all() and (r.kcor_trace[s:, 0] == -1).all()
+    f = r.offset[0] + sum(_fitted(pool, r.theta_f[0, k], k) for k in range(pool.K))
+    assert np.allclose(f, r.f[0], rtol=0, atol=1e-10 * np.abs(y).max())
+    assert np.isclose(r.offset[0], y[vm == 0].mean(), rtol=1e-14)
+    # no switch if the patience is never exhausted
+    r2 = pool.train_hcwb(y[None], vm, nu=0.3, gamma=1.0, pat0=10 ** 6, M=40)
+    assert r2.switch_iter[0] == 40 and (r2.kcor_trace >= 0).all()
+
+
+def test_hcwb_errors():
+    pool, X, y = _acwb_pool(seed=1, K=2, n=100)
+    with pytest.raises(O.OracleError):
+        pool.train_hcwb(y[None], np.zeros(y.size, np.uint8))      # no validation rows
+    with pytest.raises(O.OracleError):
+        pool.train_hcwb(y[None], np.ones(y.size, np.uint8))       # no training rows
