@@ -130,3 +130,12 @@ def make(cfg: SynthConfig | str, reps=None) -> Dataset:
         sd = float(np.std(e, ddof=1))
         Y[c] = e + eps[c] * (sd / cfg.snr)
     return Dataset(cfg, X, Y, reps)
+
+
+def validation_mask(n: int, frac: float = 0.3, seed: int = 0) -> np.ndarray:
+    """Seeded train/validation split for HCWB (30 % validation): uint8[n], 1 = validation row.
+    Exactly round(frac * n) validation rows, drawn without replacement."""
+    rng = np.random.default_rng(np.random.SeedSequence([SEED, 7, seed]))
+    m = np.zeros(n, dtype=np.uint8)
+    m[rng.choice(n, size=int(round(frac * n)), replace=False)] = 1
+    return m

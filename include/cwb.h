@@ -176,6 +176,24 @@ int cwb_train_acwb(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double g
                    double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
                    int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t stream);
 
+/* Hybrid CWB, Algorithm 3 ("HCWB"), L2 loss.  val_mask[n] (device, uint8):
+ * 1 = validation row (D_val), 0 = training row (D_train); the split is the caller's
+ * (seeded) draw.  Per replication: ACWB (as cwb_train_acwb, momentum gamma) fitted on the
+ * training rows while the validation-risk patience counter is below pat0 (the counter
+ * increments when R_emp(f^[m] | D_val) > R_emp(f^[m-1] | D_val), resets otherwise;
+ * P:L986's "if pat0 < pat" read this way), then CWB on all rows continuing from
+ * the primary model f.  One pool (bins, basis, lambda) on all rows; training fits use the
+ * training-row G.  Outputs (device): offset_out[B] (mean of the training targets),
+ * theta_f_out[B][K][d] (f = offset + sum_k Z_k theta_f[k]); traces [M][B]: k_trace,
+ * kcor_trace (-1 after the switch), sse_trace (SSE of the primary fit on its rows),
+ * risk_trace (risk of f on all rows), val_risk_trace; switch_iter[B] = first CWB
+ * iteration (M if none).  Trace pointers may be NULL.  Paper defaults gamma = 0.037,
+ * pat0 = 5.  Errors: CWB_EINVAL (pat0 < 1, ...), CWB_ECALIB. */
+int cwb_train_hcwb(cwb_ctx* ctx, const double* Y, int32_t B, const uint8_t* val_mask, double nu, double gamma,
+                   int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
+                   int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                   int32_t* switch_iter, cudaStream_t stream);
+
 /* Same as cwb_train but every array is a HOST pointer (X[K][n], Y[B][n] in,
  * the rest out); the host<->device copies are enqueued on `stream` and the
  * call synchronises before returning.  Builds and frees its own context. */

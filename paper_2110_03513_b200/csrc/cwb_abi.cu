@@ -324,6 +324,19 @@ int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gam
                                   sse_trace, risk_trace, s);
 }
 
+int cwb_train_hcwb(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_mask, double nu, double gamma,
+                   int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
+                   int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                   int32_t* switch_iter, cudaStream_t s) {
+    if (!c || !Y || !val_mask || !theta_f_out || B < 1 || M < 0 || pat0 < 1 || !(nu >= 0.0) || !isfinite(nu) ||
+        !(gamma >= 0.0) || !isfinite(gamma))
+        return cwb_set_error(c, CWB_EINVAL, "cwb_train_hcwb: invalid argument");
+    if (c->status) return c->status;
+    c->stream = s;
+    return cwb_train_hcwb_general(c, Y, B, val_mask, nu, gamma, pat0, M, offset_out, theta_f_out, k_trace, kcor_trace,
+                                  sse_trace, risk_trace, val_risk_trace, switch_iter, s);
+}
+
 int cwb_fit_host(const double* X, int64_t n, int32_t K, const cwb_config* cfg, const double* Y, int32_t B,
                  double nu, int32_t M, double* offset_out, double* theta_agg_out, int32_t* k_trace,
                  double* sse_trace, double* risk_trace, cudaStream_t s) {

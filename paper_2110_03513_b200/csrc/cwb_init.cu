@@ -16,6 +16,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "cwb_internal.cuh"
 
 namespace {
@@ -500,6 +502,51 @@ __global__ void k_zt(const double* __restrict__ Zb, const int32_t* __restrict__ 
     }
 }
 
+// Training-row statistics for HCWB (Alg. 3): counts of the rows with mask == 0 per bin
+// (binMatMat with 0/1 observation weights).  Integer atomics: exact.
+template <typename IdxT>
+__global__ void k_count_masked(const IdxT* __restrict__ idx, const uint8_t* __restrict__ mask, int64_t n, int ns,
+                               uint32_t* __restrict__ cnt, const int* status) {
+    extern __shared__ uint32_t hc[];
+    if (status && *status) return;
+    const int k = blockIdx.y;
+    for (int l = threadIdx.x; l < ns; l += blockDim.x) hc[l] = 0u;
+    __syncthreads();
+    const IdxT* ik = idx + (size_t)k * n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (!mask[i]) atomicAdd(&hc[ik[i]], 1u);
+    __syncthreads();
+    for (int l = threadIdx.x; l < ns; l += blockDim.x)
+        if (hc[l]) atomicAdd(&cnt[(size_t)k * ns + l], hc[l]);
+}
+
+// (G + lambda D)^-1 for a given lambda (one warp per learner): the cached inverse of the
+// training-row learners, with the lambda calibrated on all rows (HCWB readings)
+__global__ void k_inverse_fixed(const double* __restrict__ Gall, const double* __restrict__ lambda, int d,
+                                double* __restrict__ Ainv_out, int* status) {
+    __shared__ double Gs[CWB_MAX_D][DS], Dm[CWB_MAX_D][DS], Xs[CWB_MAX_D][DS];
+    __shared__ double Lb[(CWB_MAX_D + 4) * 4], inv[CWB_MAX_D];
+    __shared__ bool s_ok;
+    if (status && *status) return;
+    const int k = blockIdx.x, i = threadIdx.x;
+    for (int e = i; e < (CWB_MAX_D + 4) * 4; e += 32) Lb[e] = 0.0;
+    if (i < d)
+        for (int c = 0; c < d; c++) {
+            Gs[i][c] = Gall[((size_t)k * d + i) * d + c];
+            Dm[i][c] = dpen(i, c, d);
+        }
+    __syncwarp();
+    band_factor(lambda[k], d, Gs, Dm, Lb, inv, &s_ok);
+    if (!s_ok) {
+        if (i == 0) cwb_dev_fail(status, CWB_ECALIB);
+        return;
+    }
+    if (i < d) band_solve(d, Lb, inv, [&](int j) { return j == i ? 1.0 : 0.0; }, Xs, i);
+    __syncwarp();
+    if (i < d)
+        for (int c = 0; c < d; c++) Ainv_out[((size_t)k * d + i) * d + c] = 0.5 * (Xs[i][c] + Xs[c][i]);
+}
+
 }  // namespace
 
 // ===================================================================== host
@@ -575,4 +622,23 @@ int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
     k_zt<<<K, 256, 0, s>>>(c->Zb, c->lwin, ns, d, c->W, c->ZT, c->d_status);
     c->launches += 4;
     return cwb_check_launch(c, "pool kernels");
+}
+
+// HCWB training-row tables: G_tr = Zb^T diag(cnt_tr) Zb and (G_tr + lambda D)^-1
+int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, double* G_tr, double* Ainv_tr,
+                           cudaStream_t s) {
+    const int K = c->K, ns = c->n_star, d = c->d;
+    cudaMemsetAsync(cnt_tr, 0, sizeof(uint32_t) * (size_t)K * ns, s);
+    const int gx = (int)std::min<int64_t>(64, (c->n + 1023) / 1024);
+    const size_t smem = sizeof(uint32_t) * ns;
+    if (c->idx_bytes == 1)
+        k_count_masked<uint8_t><<<dim3(gx, K), 1024, smem, s>>>((const uint8_t*)c->idx, mask, c->n, ns, cnt_tr,
+                                                                c->d_status);
+    else
+        k_count_masked<uint16_t><<<dim3(gx, K), 1024, smem, s>>>((const uint16_t*)c->idx, mask, c->n, ns, cnt_tr,
+                                                                 c->d_status);
+    k_gram<<<K, 256, 0, s>>>(c->Zb, cnt_tr, ns, d, c->lwin, G_tr, c->d_status);
+    k_inverse_fixed<<<K, 32, 0, s>>>(G_tr, c->lambda, d, Ainv_tr, c->d_status);
+    c->launches += 3;
+    return cwb_check_launch(c, "masked pool kernels");
 }

@@ -29,7 +29,7 @@ constexpr int kRowsH6 = 256;  // rows per block in k_h6
 constexpr int kColRows = 8192;
 
 __global__ void k_colsum(const double* __restrict__ Y, int64_t n, const double* __restrict__ f0, bool sq,
-                         double* __restrict__ part, int* status) {
+                         double* __restrict__ part, int* status, const uint8_t* mask = nullptr, int keep = 0) {
     const int b = blockIdx.y;
     const double* y = Y + (size_t)b * n;
     const int64_t r0 = (int64_t)blockIdx.x * kColRows, r1 = min(n, r0 + kColRows);
@@ -39,6 +39,7 @@ __global__ void k_colsum(const double* __restrict__ Y, int64_t n, const double* 
     for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
         const double v = y[i];
         bad |= !isfinite(v);
+        if (mask && mask[i] != keep) continue;
         const double t = v - c;
         s += sq ? t * t : v;
     }
@@ -57,13 +58,13 @@ __global__ void k_colsum(const double* __restrict__ Y, int64_t n, const double* 
 
 // mode 0: out[b] = sum / n (mean, also written to offset_out); mode 1: out[b] = sum
 __global__ void k_center_fin(const double* __restrict__ part, int nblk, int B, int64_t n, int mode,
-                             double* __restrict__ out, double* offset_out) {
+                             double* __restrict__ out, double* offset_out, const double* ncount = nullptr) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     double t = 0.0;
     for (int q = 0; q < nblk; q++) t += part[(size_t)b * nblk + q];
     if (mode == 0) {
-        t = t / (double)n;
+        t = t / (ncount ? *ncount : (double)n);
         if (offset_out) offset_out[b] = t;
     }
     out[b] = t;
@@ -120,11 +121,14 @@ __global__ void k_h1(const double* __restrict__ Rt, int64_t n, int Bp, int K, in
 }
 
 // H2-H4 for one learner (blockIdx.x) and 32 replications (blockIdx.y)
+// (HCWB: column b uses Ainv2 / G2 when phase[b mod Bph] != 0)
 __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
                        const int32_t* __restrict__ zj0, const double* __restrict__ Zs,
                        const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
                        const double* __restrict__ G, double* __restrict__ theta,
-                       double* __restrict__ delta) {
+                       double* __restrict__ delta, const double* __restrict__ Ainv2 = nullptr,
+                       const double* __restrict__ G2 = nullptr, const int32_t* __restrict__ phase = nullptr,
+                       int Bph = 0) {
     __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
     const int k = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -139,7 +143,8 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
         S[j][lane] = s;
     }
     __syncthreads();
-    const double* Ai = Ainv + (size_t)k * d * d;
+    const bool set2 = phase && b < 2 * Bph && phase[b >= Bph ? b - Bph : b] != 0;
+    const double* Ai = (set2 ? Ainv2 : Ainv) + (size_t)k * d * d;
     for (int j = w; j < d; j += nw) {
         double t = 0.0;
         for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][lane];
@@ -147,7 +152,7 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
         theta[((size_t)k * d + j) * Bp + b] = t;
     }
     __syncthreads();
-    const double* Gk = G + (size_t)k * d * d;
+    const double* Gk = (set2 ? G2 : G) + (size_t)k * d * d;
     for (int j = w; j < d; j += nw) {
         double gt = 0.0;
         for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++)
@@ -375,6 +380,212 @@ __global__ void k_acwb_rr(const double* __restrict__ part, int nblk, int B, int 
     if (risk_trace) risk_trace[(size_t)m * B + b] = sf / (2.0 * (double)n);
 }
 
+// ---------------------------------------------------------------- HCWB path
+// Hybrid CWB, Algorithm 3: per replication, ACWB fitted on the training rows
+// (val_mask == 0; their residual columns are zero on validation rows, and they use the
+// training-row G_tr, (G_tr + lambda D)^-1) while the validation-risk patience counter is
+// below pat0, then CWB on all rows (G, A^-1 of the pool).  phase[b]: 0 ACWB, 1 CWB.
+
+__global__ void k_hcwb_scale_vprev(double* __restrict__ v, const double* __restrict__ cnt, int B) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) v[b] = v[b] / (2.0 * cnt[1]);
+}
+
+__global__ void k_fill_int(int32_t* __restrict__ p, int cnt, int v) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < cnt) p[b] = v;
+}
+
+__global__ void k_mask_count(const uint8_t* __restrict__ mask, int64_t n, double* __restrict__ cnt) {
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v += mask[i] ? 1.0 : 0.0;
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); q++) t += red[q];
+        cnt[0] = (double)n - t;  // training rows
+        cnt[1] = t;              // validation rows
+    }
+}
+
+// F = H = Rt[i][b] (= y - f0, all rows); fitting columns b, B+b masked to the training rows
+__global__ void k_hcwb_init(double* __restrict__ Rt, double* __restrict__ F, double* __restrict__ H,
+                            const uint8_t* __restrict__ mask, int64_t n, int B, int Bp, int Bq) {
+    const int b = blockIdx.y * 32 + (threadIdx.x & 31);
+    if (b >= B) return;
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+         i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const double v = Rt[(size_t)i * Bp + b];
+        F[(size_t)i * Bq + b] = v;
+        H[(size_t)i * Bq + b] = v;
+        const double vm = mask[i] ? 0.0 : v;
+        Rt[(size_t)i * Bp + b] = vm;
+        Rt[(size_t)i * Bp + B + b] = vm;
+    }
+}
+
+__global__ void k_hcwb_select(const double* __restrict__ delta, const double* __restrict__ theta,
+                              const double* __restrict__ rr, const int32_t* __restrict__ phase, int K, int d, int B,
+                              int Bp, double nu, double vt, double eta, int m, int32_t* __restrict__ kstar,
+                              double* __restrict__ tf, double* __restrict__ th, int32_t* k_trace, int32_t* kcor_trace,
+                              double* sse_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const bool acc = phase[b] == 0;
+    int ks = 0, kc = 0;
+    double best = delta[b], bestc = delta[B + b];
+    for (int k = 1; k < K; k++) {
+        const double v = delta[(size_t)k * Bp + b], vc = delta[(size_t)k * Bp + B + b];
+        if (v > best) { best = v; ks = k; }
+        if (vc > bestc) { bestc = vc; kc = k; }
+    }
+    kstar[b] = ks;
+    kstar[B + b] = kc;
+    double* f = tf + (size_t)b * K * d;
+    double* h = th + (size_t)b * K * d;
+    if (acc) {  // ACWB bookkeeping
+        for (int a = 0; a < K * d; a++) f[a] = (1.0 - vt) * f[a] + vt * h[a];
+        for (int j = 0; j < d; j++) {
+            f[ks * d + j] += nu * theta[((size_t)ks * d + j) * Bp + b];
+            h[kc * d + j] += eta * theta[((size_t)kc * d + j) * Bp + B + b];
+        }
+    } else {    // CWB aggregation
+        for (int j = 0; j < d; j++) f[ks * d + j] += nu * theta[((size_t)ks * d + j) * Bp + b];
+    }
+    if (k_trace) k_trace[(size_t)m * B + b] = ks;
+    if (kcor_trace) kcor_trace[(size_t)m * B + b] = acc ? kc : -1;
+    if (sse_trace) sse_trace[(size_t)m * B + b] = rr[b] - best;
+}
+
+// pass 1: models after iteration m.  ACWB: F = (1-vt)F + vt H - nu b_k (= y - (g + nu b_k)),
+// H -= eta b_kcor; CWB: F -= nu b_k.  Partial sums of F^2 on all rows and on validation rows.
+template <typename IdxT>
+__global__ void k_hcwb_update(double* __restrict__ F, double* __restrict__ H, const uint8_t* __restrict__ mask,
+                              int64_t n, int B, int Bp, int Bq, const int32_t* __restrict__ phase,
+                              const int32_t* __restrict__ kstar, const IdxT* __restrict__ idx,
+                              const double* __restrict__ zhat, double vt, double eta, double* __restrict__ part) {
+    __shared__ double red[2][8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const bool live = b < B;
+    const bool acc = live && phase[b] == 0;
+    const int ks = live ? kstar[b] : 0, kc = live ? kstar[B + b] : 0;
+    const IdxT* ik = idx + (size_t)ks * n;
+    const IdxT* ic = idx + (size_t)kc * n;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6, r1 = min(n, r0 + kRowsH6);
+    double sa = 0.0, sv = 0.0;
+    if (live)
+        for (int64_t i = r0 + w; i < r1; i += 8) {
+            const double Fo = F[(size_t)i * Bq + b];
+            const double bk = zhat[(size_t)ik[i] * Bp + b];
+            double Fn;
+            if (acc) {
+                const double Ho = H[(size_t)i * Bq + b];
+                const double bc = zhat[(size_t)ic[i] * Bp + B + b];
+                Fn = (1.0 - vt) * Fo + vt * Ho - bk;
+                H[(size_t)i * Bq + b] = Ho - eta * bc;
+            } else {
+                Fn = Fo - bk;
+            }
+            F[(size_t)i * Bq + b] = Fn;
+            sa += Fn * Fn;
+            if (mask[i]) sv += Fn * Fn;
+        }
+    red[0][w][lane] = sa;
+    red[1][w][lane] = sv;
+    __syncthreads();
+    if (w < 2 && live) {
+        double t = 0.0;
+        for (int q = 0; q < 8; q++) t += red[w][q][lane];
+        part[((size_t)w * gridDim.x + blockIdx.x) * Bq + b] = t;
+    }
+}
+
+// risk traces and the patience counter (Alg. 3 line 6): phase 0 -> 1 after pat0 consecutive
+// increases of the validation risk
+__global__ void k_hcwb_decide(const double* __restrict__ part, int nblk, int B, int Bq, int64_t n,
+                              const double* __restrict__ cnt, int m, int pat0, int32_t* __restrict__ phase,
+                              int32_t* __restrict__ pat, double* __restrict__ vprev, int32_t* switch_iter,
+                              double* risk_trace, double* val_risk_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double sa = 0.0, sv = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        sa += part[((size_t)0 * nblk + q) * Bq + b];
+        sv += part[((size_t)1 * nblk + q) * Bq + b];
+    }
+    const double vr = sv / (2.0 * cnt[1]);
+    if (risk_trace) risk_trace[(size_t)m * B + b] = sa / (2.0 * (double)n);
+    if (val_risk_trace) val_risk_trace[(size_t)m * B + b] = vr;
+    if (phase[b] == 0) {
+        pat[b] = vr > vprev[b] ? pat[b] + 1 : 0;
+        if (pat[b] >= pat0) {
+            phase[b] = 1;
+            if (switch_iter) switch_iter[b] = m + 1;
+        }
+    }
+    vprev[b] = vr;
+}
+
+// pass 2: fitting columns of iteration m+1.  ACWB: r' = (1-vt1) F + vt1 H, c' = r' + a1 (c - b_kcor),
+// zero on validation rows; CWB: r' = F on all rows, c' = 0.  Partial sums of r'^2, c'^2.
+template <typename IdxT>
+__global__ void k_hcwb_prepare(double* __restrict__ Rt, const double* __restrict__ F, const double* __restrict__ H,
+                               const uint8_t* __restrict__ mask, int64_t n, int B, int Bp, int Bq,
+                               const int32_t* __restrict__ phase, const int32_t* __restrict__ kstar,
+                               const IdxT* __restrict__ idx, const double* __restrict__ zhat, double vt1, double a1,
+                               double* __restrict__ part) {
+    __shared__ double red[2][8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const bool live = b < B;
+    const bool acc = live && phase[b] == 0;
+    const int kc = live ? kstar[B + b] : 0;
+    const IdxT* ic = idx + (size_t)kc * n;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6, r1 = min(n, r0 + kRowsH6);
+    double sr = 0.0, sc = 0.0;
+    if (live)
+        for (int64_t i = r0 + w; i < r1; i += 8) {
+            const double Fi = F[(size_t)i * Bq + b];
+            double rn, cn;
+            if (acc) {
+                rn = (1.0 - vt1) * Fi + vt1 * H[(size_t)i * Bq + b];
+                cn = rn + a1 * (Rt[(size_t)i * Bp + B + b] - zhat[(size_t)ic[i] * Bp + B + b]);
+                if (mask[i]) { rn = 0.0; cn = 0.0; }
+            } else {
+                rn = Fi;
+                cn = 0.0;
+            }
+            Rt[(size_t)i * Bp + b] = rn;
+            Rt[(size_t)i * Bp + B + b] = cn;
+            sr += rn * rn;
+            sc += cn * cn;
+        }
+    red[0][w][lane] = sr;
+    red[1][w][lane] = sc;
+    __syncthreads();
+    if (w < 2 && live) {
+        double t = 0.0;
+        for (int q = 0; q < 8; q++) t += red[w][q][lane];
+        part[((size_t)(2 + w) * gridDim.x + blockIdx.x) * Bq + b] = t;
+    }
+}
+
+__global__ void k_hcwb_rr(const double* __restrict__ part, int nblk, int B, int Bq, double* __restrict__ rr) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double sr = 0.0, sc = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        sr += part[((size_t)2 * nblk + q) * Bq + b];
+        sc += part[((size_t)3 * nblk + q) * Bq + b];
+    }
+    rr[b] = sr;
+    rr[B + b] = sc;
+}
+
 // ---------------------------------------------------------------- narrow path
 // binMatVec sums for a few residual vectors (B <= 4), e.g. one
 // findBestBaselearner on a single residual: HBM-bound on the index vector.  A CTA
@@ -589,7 +800,8 @@ static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_
 
 // f0[b] = mean (center) and rr[b] = sum (y - f0)^2 of the B vectors Y[b][n] (I8)
 static int column_stats(cwb_ctx* c, const double* Y, int B, bool center, double* f0, double* rr,
-                        double* offset_out, cudaStream_t s) {
+                        double* offset_out, cudaStream_t s, const uint8_t* mask = nullptr, int keep = 0,
+                        const double* ncount = nullptr) {
     cwb_train_ws& w = c->ws;
     const int nblk = (int)((c->n + kColRows - 1) / kColRows);
     const size_t need = sizeof(double) * (size_t)nblk * B;
@@ -602,11 +814,11 @@ static int column_stats(cwb_ctx* c, const double* Y, int B, bool center, double*
         w.colpart_bytes = need;
     }
     if (center) {
-        k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, nullptr, false, w.colpart, c->d_status);
-        k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nblk, B, c->n, 0, f0, offset_out);
+        k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, nullptr, false, w.colpart, c->d_status, mask, keep);
+        k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nblk, B, c->n, 0, f0, offset_out, ncount);
         c->launches += 2;
     }
-    k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, center ? f0 : nullptr, true, w.colpart, c->d_status);
+    k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, f0, true, w.colpart, c->d_status, mask, keep);
     k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nblk, B, c->n, 1, rr, nullptr);
     c->launches += 2;
     return CWB_OK;
@@ -878,4 +1090,100 @@ int cwb_train_acwb_general(cwb_ctx* c, const double* Y, int32_t B, double nu, do
         c->launches += 6;
     }
     return cwb_check_launch(c, "ACWB kernels");
+}
+
+// ===================================================================== HCWB host
+int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_mask, double nu, double gamma,
+                           int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
+                           int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                           int32_t* switch_iter, cudaStream_t s) {
+    int rc = ensure_ws(c, 2 * B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp, Bq = (B + 31) / 32 * 32;
+    const int K = c->K, ns = c->n_star, d = c->d;
+    const int nblk = (int)((c->n + kRowsH6 - 1) / kRowsH6);
+    // F, H (n x Bq), partials (4 x nblk x Bq), offsets, theta_h (B x K x d), vprev, counts,
+    // G_tr, Ainv_tr (K x d x d), cnt_tr (K x n*), phase, pat (ints)
+    const size_t dbl = 2 * (size_t)c->n * Bq + 4 * (size_t)nblk * Bq + Bq + (size_t)B * K * d + Bq + 2 +
+                       2 * (size_t)K * d * d;
+    const size_t need = sizeof(double) * dbl + sizeof(uint32_t) * (size_t)K * ns + 2 * sizeof(int32_t) * Bq;
+    if (w.acwb_bytes < need) {
+        cwb_release(w.acwb, s);
+        w.acwb = nullptr;
+        w.acwb_bytes = 0;
+        if (cwb_alloc((void**)&w.acwb, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "HCWB workspace allocation failed");
+        w.acwb_bytes = need;
+    }
+    double* F = w.acwb;
+    double* H = F + (size_t)c->n * Bq;
+    double* part = H + (size_t)c->n * Bq;
+    double* off_ws = part + 4 * (size_t)nblk * Bq;
+    double* th = off_ws + Bq;
+    double* vprev = th + (size_t)B * K * d;
+    double* cnt = vprev + Bq;
+    double* G_tr = cnt + 2;
+    double* Ainv_tr = G_tr + (size_t)K * d * d;
+    uint32_t* cnt_tr = (uint32_t*)(Ainv_tr + (size_t)K * d * d);
+    int32_t* phase = (int32_t*)(cnt_tr + (size_t)K * ns);
+    int32_t* pat = phase + Bq;
+    rc = cwb_launch_masked_pool(c, val_mask, cnt_tr, G_tr, Ainv_tr, s);
+    if (rc) return rc;
+    k_mask_count<<<1, 1024, 0, s>>>(val_mask, c->n, cnt);
+    cudaMemsetAsync(phase, 0, sizeof(int32_t) * 2 * Bq, s);
+    // f0 = mean of the training targets (Alg. 2 line 2 on D_train); rr = sum over training rows
+    rc = column_stats(c, Y, B, true, off_ws, w.rr, offset_out, s, val_mask, 0, cnt);
+    if (rc) return rc;
+    {   // validation risk of f0: sum over validation rows of (y - f0)^2 / (2 n_val)
+        const int nb = (int)((c->n + kColRows - 1) / kColRows);
+        k_colsum<<<dim3(nb, B), 256, 0, s>>>(Y, c->n, off_ws, true, w.colpart, c->d_status, val_mask, 1);
+        k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nb, B, c->n, 1, vprev, nullptr);
+        c->launches += 2;
+    }
+    cudaMemcpyAsync(w.rr + B, w.rr, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
+    k_hcwb_init<<<dim3((unsigned)std::min<int64_t>(2048, (c->n + 7) / 8), Bq / 32), 256, 0, s>>>(w.Rt, F, H, val_mask,
+                                                                                                  c->n, B, Bp, Bq);
+    const size_t nagg = (size_t)B * K * d;
+    k_zero<<<(unsigned)std::min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_f_out, nagg);
+    k_zero<<<(unsigned)std::min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(th, nagg);
+    c->launches += 5;
+    // vprev holds sum (y - f0)^2 over validation rows: scale by 1 / (2 n_val) once
+    k_hcwb_scale_vprev<<<(B + 127) / 128, 128, 0, s>>>(vprev, cnt, B);
+    if (switch_iter) k_fill_int<<<(B + 127) / 128, 128, 0, s>>>(switch_iter, B, M);
+    c->launches += 2;
+    for (int m = 0; m < M; m++) {
+        // ACWB iteration index ma = m + 1 while a replication is in phase 0
+        const double vt = 2.0 / (double)(m + 2);
+        const double eta = gamma * nu / vt;
+        const double vt1 = 2.0 / (double)(m + 3);
+        const double a1 = (double)(m + 2) / (double)(m + 3);
+        h1(c, w.Rt, Bp, K, ns, c->off, c->perm, c->perm_bytes, w.U, s);
+        k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->zj0, c->Zs, c->lwin, Ainv_tr, G_tr, w.theta, w.delta,
+                                                c->Ainv, c->G, phase, B);
+        k_hcwb_select<<<(B + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, phase, K, d, B, Bp, nu, vt, eta, m,
+                                                      w.kstar, theta_f_out, th, k_trace, kcor_trace, sse_trace);
+        k_zhat<<<dim3((ns + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, ns, d, 2 * B, Bp, nu, B,
+                                                           1.0, w.zhat);
+        dim3 g6(nblk, Bq / 32);
+        if (c->idx_bytes == 1)
+            k_hcwb_update<uint8_t><<<g6, 256, 0, s>>>(F, H, val_mask, c->n, B, Bp, Bq, phase, w.kstar,
+                                                      (const uint8_t*)c->idx, w.zhat, vt, eta, part);
+        else
+            k_hcwb_update<uint16_t><<<g6, 256, 0, s>>>(F, H, val_mask, c->n, B, Bp, Bq, phase, w.kstar,
+                                                       (const uint16_t*)c->idx, w.zhat, vt, eta, part);
+        k_hcwb_decide<<<(B + 127) / 128, 128, 0, s>>>(part, nblk, B, Bq, c->n, cnt, m, pat0, phase, pat, vprev,
+                                                      switch_iter, risk_trace, val_risk_trace);
+        if (c->idx_bytes == 1)
+            k_hcwb_prepare<uint8_t><<<g6, 256, 0, s>>>(w.Rt, F, H, val_mask, c->n, B, Bp, Bq, phase, w.kstar,
+                                                       (const uint8_t*)c->idx, w.zhat, vt1, a1, part);
+        else
+            k_hcwb_prepare<uint16_t><<<g6, 256, 0, s>>>(w.Rt, F, H, val_mask, c->n, B, Bp, Bq, phase, w.kstar,
+                                                        (const uint16_t*)c->idx, w.zhat, vt1, a1, part);
+        k_hcwb_rr<<<(B + 127) / 128, 128, 0, s>>>(part, nblk, B, Bq, w.rr);
+        c->launches += 8;
+    }
+    return cwb_check_launch(c, "HCWB kernels");
 }

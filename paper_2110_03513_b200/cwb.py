@@ -21,7 +21,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 # the exported symbols declared in include/cwb.h
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
-           "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_train_acwb", "cwb_fit_host", "cwb_predict",
+           "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
            "cwb_launch_count", "cwb_set_phase_timing", "cwb_free"]
 
 
@@ -81,6 +81,8 @@ def load() -> C.CDLL:
     L.cwb_find_best.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp]
     L.cwb_train.argtypes = [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_train_acwb.argtypes = [_vp, _vp, _i32, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.cwb_train_hcwb.argtypes = [_vp, _vp, _i32, _vp, _f64, _f64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp, _vp]
     L.cwb_fit_host.argtypes = [_vp, _i64, _i32, C.POINTER(cwb_config), _vp, _i32, _f64, _i32,
                                _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_predict.argtypes = [_vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp]
@@ -266,6 +268,28 @@ def cwb_train_acwb(ctx, Y, nu: float = 0.05, gamma: float = 0.0034, M: int = 200
     return out
 
 
+def cwb_train_hcwb(ctx, Y, val_mask, nu: float = 0.05, gamma: float = 0.037, pat0: int = 5, M: int = 200):
+    """Hybrid CWB (Alg. 3) for Y[B][n]; val_mask[n] uint8 (1 = validation row).  Dict of device tensors."""
+    import torch
+    Y = _dev_f64(Y, "Y")
+    if not isinstance(val_mask, torch.Tensor) or val_mask.dtype != torch.uint8 or not val_mask.is_cuda:
+        raise TypeError("val_mask must be a uint8 CUDA tensor")
+    val_mask = val_mask.contiguous()
+    ns, d, K, n = cwb_get_dims(ctx)
+    B = Y.shape[0]
+    f = dict(dtype=torch.float64, device=Y.device)
+    i32 = dict(dtype=torch.int32, device=Y.device)
+    out = dict(offset=torch.empty(B, **f), theta_f=torch.empty((B, K, d), **f),
+               k_trace=torch.empty((M, B), **i32), kcor_trace=torch.empty((M, B), **i32),
+               sse_trace=torch.empty((M, B), **f), risk_trace=torch.empty((M, B), **f),
+               val_risk_trace=torch.empty((M, B), **f), switch_iter=torch.empty(B, **i32))
+    _chk(load().cwb_train_hcwb(ctx, _ptr(Y), B, _ptr(val_mask), float(nu), float(gamma), int(pat0), M,
+                               _ptr(out["offset"]), _ptr(out["theta_f"]), _ptr(out["k_trace"]),
+                               _ptr(out["kcor_trace"]), _ptr(out["sse_trace"]), _ptr(out["risk_trace"]),
+                               _ptr(out["val_risk_trace"]), _ptr(out["switch_iter"]), _stream(Y)), ctx)
+    return out
+
+
 def cwb_fit_host(X, Y, cfg: Config | None = None, nu: float = 0.05, M: int = 200, stream=None):
     """Whole fit from HOST numpy arrays (copies inside the call)."""
     import numpy as np
@@ -331,6 +355,9 @@ class Pool:
 
     def train_acwb(self, Y, nu=0.05, gamma=0.0034, M=200, traces=True):
         return cwb_train_acwb(self.ctx, Y, nu, gamma, M, traces)
+
+    def train_hcwb(self, Y, val_mask, nu=0.05, gamma=0.037, pat0=5, M=200):
+        return cwb_train_hcwb(self.ctx, Y, val_mask, nu, gamma, pat0, M)
 
     def predict(self, Xnew, offset, theta_agg):
         return cwb_predict(self.ctx, Xnew, offset, theta_agg)
