@@ -221,7 +221,7 @@ def main():
     X = torch.as_tensor(ds.X, device=devname)
     Y = torch.as_tensor(ds.Y, device=devname)
     gcfg = cwb.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots,
-                      degree=cfg.degree, df=cfg.df)
+                      degree=cfg.degree, df=cfg.df, batch_hint=cfg.B)
     B, K, n, M = cfg.B, cfg.K, cfg.n, cfg.M
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=devname)

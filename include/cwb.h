@@ -57,9 +57,12 @@ typedef struct {
     int32_t n_knots;      /* inner knots (default 20); d = n_knots + degree + 1 <= 32             */
     double df;            /* target degrees of freedom per learner (default 5)                   */
     int32_t df_kind;      /* 1: df1 = tr H, 2: df2 = tr(2H - H^2) (supp. P:L314-318)              */
+    int32_t batch_hint;   /* expected B of the cwb_train calls (0: unknown).  When > 0, cwb_init
+                             builds the fused kernel's gather plan for that B on a side stream,
+                             overlapped with the rest of the pool construction.                   */
 } cwb_config;
 
-/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5. */
+/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5, no batch hint. */
 void cwb_default_config(cwb_config* cfg);
 
 /* Library ABI version (major*100 + minor). */

@@ -100,6 +100,7 @@ void cwb_default_config(cwb_config* cfg) {
     cfg->n_knots = 20;
     cfg->df = 5.0;
     cfg->df_kind = 1;
+    cfg->batch_hint = 0;
 }
 
 int cwb_version(void) { return 100; }
@@ -156,11 +157,15 @@ int cwb_bin_mat_vec(const double* Zb, int32_t n_star, int32_t d, const void* idx
 void cwb_free(cwb_ctx* c) {
     if (!c) return;
     cudaStream_t s = c->stream;
+    if (c->ev_plan) cudaStreamWaitEvent(s, c->ev_plan, 0);  // a plan still building on the side stream
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
                     c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->plan, c->permt,
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
+    if (c->ev_plan) cudaEventDestroy(c->ev_plan);
+    if (c->ev_csr) cudaEventDestroy(c->ev_csr);
+    if (c->s2) cudaStreamDestroy(c->s2);
     delete c;
 }
 
@@ -183,6 +188,7 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     cwb_ctx* c = new cwb_ctx();
     c->n = n; c->K = K; c->n_star = (int32_t)ns; c->d = d; c->degree = cfg.degree; c->n_knots = cfg.n_knots;
     c->df = cfg.df; c->df_kind = cfg.df_kind;
+    c->batch_hint = cfg.batch_hint > 0 ? cfg.batch_hint : 0;
     c->idx_bytes = ns <= 256 ? 1 : 2;
     c->perm_bytes = n <= 65536 ? 2 : 4;
     c->stream = s;
@@ -228,6 +234,7 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
 int cwb_status(cwb_ctx* c) {
     if (!c) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_status: NULL context");
     if (c->status) return c->status;
+    if (c->ev_plan) cudaEventSynchronize(c->ev_plan);
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return cwb_set_error(c, CWB_ECUDA, cudaGetErrorString(e));
     int dev = 0;

@@ -31,6 +31,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <atomic>
+#include <mutex>
 
 #include "cwb_internal.cuh"
 
@@ -43,7 +46,7 @@ constexpr int kSlackEntries = 256;  // schedule entries after the last block (2 
 struct FusedParams {
     int n, K, ns, nsp, d, M, B, n_multi, W;
     int permt_cap;  // entries of permt staged in shared memory (POOL)
-    int ztab;       // Zs / zj0 staged in shared memory
+    int ztab;       // bit 0: Zs / zj0 staged in shared memory, bit 1: the index vectors too
     double nu;
     double inv2n;  // 1 / (2n): risk = r^T r / (2n) without a division on the critical path
     const double* Y;
@@ -68,9 +71,9 @@ struct FusedParams {
 __host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 
 struct SmemLayout {
-    size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, total;
+    size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, ix, total;
     __host__ __device__ SmemLayout(int n, int K, int nsp, int d, int W, int n_multi, int RB, int NW, bool pool,
-                                   size_t permt_bytes, bool ztab) {
+                                   size_t permt_bytes, int ztab, int idx_bytes = 1) {
         size_t o = 0;
         r = o; o = align16(o + sizeof(double) * RB * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
         U = o; o = align16(o + sizeof(double) * RB * ((size_t)K * nsp + W));  // +W: window overrun pad
@@ -88,6 +91,7 @@ struct SmemLayout {
         lw = o; if (pool) o = align16(o + sizeof(int32_t) * (size_t)K * d);
         zs = o; if (ztab) o = align16(o + sizeof(double) * (size_t)K * nsp * CWB_SPW);
         zj = o; if (ztab) o = align16(o + sizeof(int32_t) * (size_t)K * nsp);
+        ix = o; if (ztab & 2) o = align16(o + (size_t)idx_bytes * K * n);
         total = o;
     }
 };
@@ -159,7 +163,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     const int n = p.n;
     const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns;
     const int W = p.W;
-    const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab != 0);
+    const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab,
+                       (int)sizeof(IdxT));
     double* r = (double*)(smem + L.r);  // r[i * RB + q]
     const unsigned char* rb = smem + L.r;
     double* U = (double*)(smem + L.U);  // U[g * RB + q], g = k * nsp + l
@@ -174,10 +179,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     const double* Ac = POOL ? (const double*)(smem + L.ai) : p.Ainv;
     const double* Cbc = POOL ? (const double*)(smem + L.cb) : p.Cb;
     double* sS = (double*)(smem + L.ss) + (size_t)warp * RB * 32;
-    const double* Zs_c = p.ztab ? (const double*)(smem + L.zs) : p.Zs;
-    const int32_t* zj0_c = p.ztab ? (const int32_t*)(smem + L.zj) : p.zj0;
-    const int zstride = p.ztab ? nsp : ns;  // row stride of Zs / zj0 per learner
-    const IdxT* idx = (const IdxT*)p.idx;
+    // POOL: every per-iteration table is in shared memory (compile-time known: LDS, not generic loads)
+    const double* Zs_c = POOL ? (const double*)(smem + L.zs) : p.Zs;
+    const int32_t* zj0_c = POOL ? (const int32_t*)(smem + L.zj) : p.zj0;
+    const int zstride = POOL ? nsp : ns;  // row stride of Zs / zj0 per learner
+    const IdxT* idx = POOL ? (const IdxT*)(smem + L.ix) : (const IdxT*)p.idx;
     const bool timed = p.timing && blockIdx.x == 0 && tid == 0;
     long long tA = 0, tB = 0, tC = 0, tD = 0, tm = 0;
     __shared__ int ks_sh[2];
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         for (int a = tid; a < K * d * 4; a += T) ((double*)(smem + L.cb))[a] = __ldg(p.Cb + a);
         for (int a = tid; a < K * d; a += T) ((int32_t*)(smem + L.lw))[a] = __ldg(p.lwin + 2 * a);
     }
-    if (p.ztab) {
+    if (POOL) {
         double* zd = (double*)(smem + L.zs);
         int32_t* jd = (int32_t*)(smem + L.zj);
         for (int a = tid; a < K * ns; a += T) {
@@ -203,6 +209,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             for (int q = 0; q < CWB_SPW; q++) zd[((size_t)k * nsp + l) * CWB_SPW + q] = __ldg(p.Zs + (size_t)a * CWB_SPW + q);
             jd[k * nsp + l] = __ldg(p.zj0 + a);
         }
+    }
+    if (POOL) {  // index vectors (K x n), 16-byte copies + tail
+        const size_t nb = sizeof(IdxT) * (size_t)K * n, nv = nb / 16;
+        const uint4* src = (const uint4*)p.idx;
+        uint4* dst = (uint4*)(smem + L.ix);
+        for (size_t a = tid; a < nv; a += T) dst[a] = __ldg(src + a);
+        for (size_t a = nv * 16 + tid; a < nb; a += T) (smem + L.ix)[a] = ((const unsigned char*)p.idx)[a];
     }
     const int32_t* pl = p.plan;
     const int rounds = pl[1], n_comb = pl[2];
@@ -348,8 +361,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
 #pragma unroll 4
                 for (int w = 0; w < W; w++) {
                     const double z = POOL ? zt[w * d] : __ldg(zt + w * d);
-#pragma unroll
-                    for (int q = 0; q < RB; q++) sv[q] = fma(z, uk[w * RB + q], sv[q]);
+                    if (RB == 2) {
+                        const double2 u2 = *reinterpret_cast<const double2*>(uk + 2 * w);
+                        sv[0] = fma(z, u2.x, sv[0]);
+                        sv[RB - 1] = fma(z, u2.y, sv[RB - 1]);
+                    } else {
+                        sv[0] = fma(z, uk[w], sv[0]);
+                    }
                 }
             }
 #pragma unroll
@@ -445,8 +463,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const int i = i0 + e * T;
-                    j0[e] = i < n ? (uint32_t)__ldg(ik0 + i) : 0u;
-                    j1[e] = (RB == 2 && i < n) ? (uint32_t)__ldg(ik1 + i) : 0u;
+                    j0[e] = i < n ? (uint32_t)ik0[i] : 0u;
+                    j1[e] = (RB == 2 && i < n) ? (uint32_t)ik1[i] : 0u;
                 }
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
@@ -821,6 +839,10 @@ int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
 template <typename IdxT, typename PermT>
 int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s) {
     if (RB == 2) {
+        if (T > 512) {
+            if (pool) return launch_t<IdxT, PermT, 2, true, 768, 1>(fp, T, smem, s);
+            return launch_t<IdxT, PermT, 2, false, 768, 1>(fp, T, smem, s);
+        }
         if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1>(fp, T, smem, s);
         return launch_t<IdxT, PermT, 2, false, 512, 1>(fp, T, smem, s);
     }
@@ -853,7 +875,7 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
     Cand cands[4];
     int nc = 0;
     const int nsm = 148;
-    if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};                     // ~2 replications per SM: one CTA
+    if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};  // ~2 replications per SM: one CTA (512 best of 256..768)
     if (B > nsm) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
     cands[nc++] = {1, c->n >= 8192 ? 768 : 512, kMaxSmem};
     for (int i = 0; i < nc; i++) {
@@ -867,7 +889,7 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
         f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
         f.cap = permt_bound(KS, f.T, f.P);
         for (int pool = 1; pool >= 0; pool--) {
-            SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, false);
+            SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, 0);
             if (L.total <= cands[i].lim) {
                 f.pool = pool != 0;
                 f.smem = L.total;
@@ -885,20 +907,44 @@ size_t cwb_fused_smem_bytes(const cwb_ctx* c) {
 }
 
 // (Re)builds the H1 task plan for the shape of a B-replication launch.
-static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
-    if (c->fused_T == f.T && c->fused_rb == f.RB && c->plan) return CWB_OK;
+// Pinned host slots for the plan headers (read back without a synchronous copy).
+static int32_t* pinned_header_slot() {
+    static std::once_flag once;
+    static int32_t* pool = nullptr;
+    static std::atomic<unsigned> next{0};
+    std::call_once(once, [] {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(int32_t) * 16 * 256, cudaHostAllocDefault) == cudaSuccess) pool = (int32_t*)p;
+    });
+    if (!pool) return nullptr;
+    return pool + 16 * (next.fetch_add(1) % 256);
+}
+
+// Launches the H1 plan for launch shape f on stream s (allocations stream-ordered on s):
+// k_fused_plan -> k_fused_sched -> k_fused_wl -> k_fused_pack into a schedule buffer of bound
+// size, then an asynchronous copy of the header and the device status to a pinned slot and
+// an event.  No host synchronisation: fused_plan_finish reads the header when it is needed.
+static int fused_plan_launch(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
+    if (c->ev_plan) CWB_CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_plan, 0));  // previous plan may still build
     cwb_release(c->plan, s);
     cwb_release(c->permt, s);
     c->plan = nullptr;
     c->permt = nullptr;
     c->fused_T = 0;
+    c->plan_pending = false;
     const int KS = c->K * c->n_star, T = f.T, G = 16 / f.RB;
-    const int RM = plan_rounds_max(KS, T);
+    const int RM = plan_rounds_max(KS, T), NW = T / 32;
     const int n_groups = RM * T / G;
     const int SB = 2 * ((f.P + 3) / 4 * 4) + G;  // schedule steps bound per group
     const size_t scratch_ints = 22 * (size_t)(KS + 2 * T) + (size_t)RM * T + (size_t)c->K * c->n;
     const size_t sched_ints = (size_t)n_groups * SB * G + n_groups;
-    if (cwb_alloc((void**)&c->plan, sizeof(int32_t) * (plan_ints(KS, T) + scratch_ints + sched_ints), s) != cudaSuccess)
+    const size_t permt_cap = (size_t)RM * T * ((SB + 7) / 8 * 8) + kSlackEntries;
+    if (!c->h_hdr) c->h_hdr = pinned_header_slot();
+    if (!c->h_hdr) return cwb_set_error(c, CWB_ENOMEM, "pinned header allocation failed");
+    if (!c->ev_plan && cudaEventCreateWithFlags(&c->ev_plan, cudaEventDisableTiming) != cudaSuccess)
+        return cwb_set_error(c, CWB_ECUDA, "event creation failed");
+    if (cwb_alloc((void**)&c->plan, sizeof(int32_t) * (plan_ints(KS, T) + scratch_ints + sched_ints), s) != cudaSuccess ||
+        cwb_alloc(&c->permt, (size_t)f.permt_bytes * permt_cap, s) != cudaSuccess)
         return cwb_set_error(c, CWB_ENOMEM, "fused plan allocation failed");
     int32_t* scratch = c->plan + plan_ints(KS, T);
     int32_t* sched = scratch + scratch_ints;
@@ -924,43 +970,55 @@ static int fused_plan(cwb_ctx* c, const FusedShape& f, cudaStream_t s) {
         k_fused_sched<16><<<(sthreads + 31) / 32, 32, 0, s>>>(c->plan, scratch, T, KS, SB, n_groups, sched, gsteps,
                                                               c->d_status);
     k_fused_wl<<<1, 256, 0, s>>>(c->plan, gsteps, KS, T, G, c->d_status);
-    c->launches += 3;
-    int rc = cwb_check_launch(c, "fused plan kernels");
-    if (rc) return rc;
-    // exact schedule size (one host sync per plan build): sizes the schedule buffer and
-    // its shared-memory copy
-    int32_t hdr[8] = {0};
-    int dev_status = 0;
-    CWB_CUDA_TRY(c, cudaMemcpyAsync(hdr, c->plan, sizeof(hdr), cudaMemcpyDeviceToHost, s));
-    CWB_CUDA_TRY(c, cudaMemcpyAsync(&dev_status, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CWB_CUDA_TRY(c, cudaStreamSynchronize(s));
-    if (dev_status) return CWB_OK;  // reported by cwb_status
-    const size_t slack = (size_t)f.permt_bytes * kSlackEntries;  // prefetch overrun of the last block
-    if (cwb_alloc(&c->permt, (size_t)f.permt_bytes * hdr[5] + slack, s) != cudaSuccess)
-        return cwb_set_error(c, CWB_ENOMEM, "fused plan allocation failed");
-    CWB_CUDA_TRY(c, cudaMemsetAsync((char*)c->permt + (size_t)f.permt_bytes * hdr[5], 0, slack, s));
-    const int blocks = std::max(1, std::min(hdr[1] * (T / 32), 1184));
+    const int blocks = std::max(1, std::min(RM * NW, 1184));
     if (f.permt_bytes == 2)
         k_fused_pack<uint16_t><<<blocks, 256, 0, s>>>(c->plan, scratch, sched, gsteps, KS, T, G, SB, (int)c->n,
                                                       stride, (uint16_t*)c->permt, c->d_status);
     else
         k_fused_pack<uint32_t><<<blocks, 256, 0, s>>>(c->plan, scratch, sched, gsteps, KS, T, G, SB, (int)c->n,
                                                       stride, (uint32_t*)c->permt, c->d_status);
-    c->launches++;
-    rc = cwb_check_launch(c, "k_fused_pack");
+    c->launches += 4;
+    CWB_CUDA_TRY(c, cudaMemcpyAsync(c->h_hdr, c->plan, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, s));
+    CWB_CUDA_TRY(c, cudaMemcpyAsync(c->h_hdr + 8, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CWB_CUDA_TRY(c, cudaEventRecord(c->ev_plan, s));
+    int rc = cwb_check_launch(c, "fused plan kernels");
     if (rc) return rc;
-    c->fused_T = T;
-    c->fused_rb = f.RB;
-    c->permt_bytes = f.permt_bytes;
+    c->plan_pending = true;
+    c->plan_T = T;
+    c->plan_rb = f.RB;
+    c->plan_permt_bytes = f.permt_bytes;
+    c->plan_cap = permt_cap;
+    return CWB_OK;
+}
+
+// Waits for the plan (host), takes over its header.
+static int fused_plan_finish(cwb_ctx* c) {
+    if (!c->plan_pending) return CWB_OK;
+    CWB_CUDA_TRY(c, cudaEventSynchronize(c->ev_plan));
+    c->plan_pending = false;
+    const int32_t* hdr = c->h_hdr;
+    if (hdr[8]) return CWB_OK;  // device error: reported by cwb_status
+    if ((size_t)hdr[5] + kSlackEntries > c->plan_cap) return cwb_set_error(c, CWB_ECUDA, "fused plan exceeds its bound");
+    c->fused_T = c->plan_T;
+    c->fused_rb = c->plan_rb;
+    c->permt_bytes = c->plan_permt_bytes;
     c->permt_entries = hdr[5];
     c->plan_multi = hdr[3];
     return CWB_OK;
 }
 
+// Pre-builds the plan for the expected batch (cwb_config.batch_hint) on a side stream that
+// starts right after the bin inversion, so it overlaps the basis / binMatMat / df->lambda
+// kernels of cwb_init.  Called by cwb_launch_init after k_csr.
 int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
-    // built lazily by the first cwb_train (the shape depends on B)
-    (void)c; (void)s;
-    return CWB_OK;
+    if (c->batch_hint <= 0) return CWB_OK;
+    FusedShape f;
+    if (!fused_shape(c, c->batch_hint, &f)) return CWB_OK;
+    if (!c->s2 && cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess) return CWB_OK;
+    if (!c->ev_csr && cudaEventCreateWithFlags(&c->ev_csr, cudaEventDisableTiming) != cudaSuccess) return CWB_OK;
+    CWB_CUDA_TRY(c, cudaEventRecord(c->ev_csr, s));
+    CWB_CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_csr, 0));
+    return fused_plan_launch(c, f, c->s2);
 }
 
 int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
@@ -969,29 +1027,34 @@ int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M
     *launched = false;
     FusedShape f;
     if (!fused_shape(c, B, &f)) return CWB_OK;  // does not fit: caller uses the general path
-    int rc = fused_plan(c, f, s);
+    int rc = CWB_OK;
+    const bool have = (c->plan_pending && c->plan_T == f.T && c->plan_rb == f.RB) ||
+                      (!c->plan_pending && c->fused_T == f.T && c->fused_rb == f.RB && c->plan);
+    if (!have) rc = fused_plan_launch(c, f, s);
+    if (rc) return rc;
+    rc = fused_plan_finish(c);
     if (rc) return rc;
     if (c->fused_T != f.T) return CWB_OK;  // plan failed on the device: cwb_status reports it
+    CWB_CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_plan, 0));  // the plan may come from the side stream
     // pool staging levels with the exact schedule size: schedule + B tables, then Zs / zj0
     const size_t lim = (f.RB == 1 && f.T <= 384) ? kTwoCtaSmem : kMaxSmem;
-    const size_t pbytes = ((size_t)(c->permt_entries + kSlackEntries) * f.permt_bytes + 15) / 16 * 16;
+    const size_t pbytes = ((size_t)(c->permt_entries + kSlackEntries) * f.permt_bytes + 15) / 16 * 16;  // < plan_cap
     f.pool = false;
     const int nm = c->plan_multi;
-    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, false).total;
-    bool ztab = false;
-    for (int lvl = 2; lvl >= 1; lvl--) {
-        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, lvl == 2);
+    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, 0).total;
+    int ztab = 0;
+    {   // POOL: schedule, B tables, Zs / zj0 and the index vectors all in shared memory, or none
+        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, 3, c->idx_bytes);
         if (L1.total <= lim) {
             f.pool = true;
-            ztab = lvl == 2;
+            ztab = 3;
             f.smem = L1.total;
-            break;
         }
     }
     FusedParams fp;
     fp.n = (int)c->n; fp.K = c->K; fp.ns = c->n_star; fp.nsp = c->nsp; fp.d = c->d; fp.M = M; fp.B = B; fp.nu = nu;
     fp.n_multi = c->plan_multi;
-    fp.ztab = ztab ? 1 : 0;
+    fp.ztab = ztab;
     fp.permt_cap = (int)(pbytes / f.permt_bytes);
     fp.Y = Y; fp.idx = c->idx; fp.permt = c->permt; fp.plan = c->plan; fp.zj0 = c->zj0; fp.Zs = c->Zs;
     fp.inv2n = 1.0 / (2.0 * (double)c->n);

@@ -85,6 +85,14 @@ struct cwb_ctx {
     bool fused_pool = false;
     size_t fused_smem = 0;
     long long* timing = nullptr;  // optional device buffer: fused-kernel phase cycles (cwb_set_timing)
+    // plan pre-built during cwb_init on a side stream (cwb_config.batch_hint)
+    int32_t batch_hint = 0;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_csr = nullptr, ev_plan = nullptr;
+    int32_t* h_hdr = nullptr;  // pinned: plan header [0..7], device status [8]
+    bool plan_pending = false;
+    int32_t plan_T = 0, plan_rb = 0, plan_permt_bytes = 2;
+    size_t plan_cap = 0;
 
     cwb_train_ws ws;
 };

@@ -279,6 +279,24 @@ def test_paths_agree_and_deterministic():
     assert ok, e
 
 
+@pytest.mark.parametrize("name,B", [("R1", 256), ("R1", 100), ("R0", 8)])
+def test_batch_hint_prebuilt_plan_identical(name, B):
+    # cwb_init with batch_hint pre-builds the gather plan on a side stream; results are bitwise
+    # those of the lazily built plan (and of a hint that does not match B)
+    ds = S.make(name, reps=range(B))
+    c = ds.cfg
+    outs = []
+    for hint in (0, B, 7):
+        gc = gpu_cfg_of(c)
+        gc.batch_hint = hint
+        pg = cwb.Pool(dev(ds.X), gc)
+        outs.append(_gpu_train(pg, ds.Y, c, 0))
+        pg.close()
+    for o in outs[1:]:
+        for k in o:
+            assert (o[k] == outs[0][k]).all(), k
+
+
 def test_train_r2_full_launch_sampled():
     # full R2 launch (B = 1024, the bench configuration of that rung); replications sampled
     ds = S.make("R2")
