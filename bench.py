@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--config", default="R1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 fused, 2 general")
+    ap.add_argument("--algo", default="cwb", choices=["cwb", "acwb", "hcwb"],
+                    help="cwb: Alg. 1 supp. (default, the headline); acwb: Alg. 2; hcwb: Alg. 3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     args = ap.parse_args()
@@ -229,6 +231,14 @@ def main():
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps + args.warmup)]
     outs = None
     launches = []
+    vm = torch.as_tensor(S.validation_mask(n), device=devname) if args.algo == "hcwb" else None
+
+    def train(pool, out=None):
+        if args.algo == "acwb":   # Alg. 2, gamma = 0.0034
+            return pool.train_acwb(Y, nu=cfg.nu, gamma=0.0034, M=M)
+        if args.algo == "hcwb":   # Alg. 3, gamma = 0.037, pat0 = 5, 30 % validation
+            return pool.train_hcwb(Y, vm, nu=cfg.nu, gamma=0.037, pat0=5, M=M)
+        return pool.train(Y, nu=cfg.nu, M=M, out=out)
 
     def step(i):
         nonlocal outs
@@ -238,7 +248,7 @@ def main():
         if args.path:
             pool.set_path(args.path)
         b.record(stream)
-        outs = pool.train(Y, nu=cfg.nu, M=M, out=outs)
+        outs = train(pool, outs)
         c_.record(stream)
         launches.append(pool.launches())
         pool.close()
@@ -269,7 +279,16 @@ def main():
     init_ms = step_ms - train_ms
     total_ms = D.max_over_ranks(float(step_ms.sum()), w, devname)
     ms_per_step = total_ms / args.steps
-    evals = K * n * B * M * ws
+    # learner-row evaluations per step: K*n*B per findBest; ACWB fits twice per
+    # iteration; HCWB twice while accelerated (its switch iterations from the last step), then once
+    if args.algo == "acwb":
+        evals_rank = 2 * K * n * B * M
+    elif args.algo == "hcwb":
+        sw = outs["switch_iter"].cpu().numpy().astype(np.int64)
+        evals_rank = int(K * n * (2 * sw + (M - sw)).sum())
+    else:
+        evals_rank = K * n * B * M
+    evals = evals_rank * ws
     value = evals / (ms_per_step * 1e-3)
 
     # ---- end-to-end through the host-pointer C-ABI call (pinned host buffers)
@@ -292,6 +311,25 @@ def main():
         if rc:
             raise cwb.CwbError(rc, lib.cwb_last_error(None).decode())
 
+    if args.algo != "cwb":
+        Xd = torch.empty_like(X)
+        Yd = torch.empty_like(Y)
+        host_out = {}
+
+        def e2e_step():  # noqa: F811 - pinned H2D of X, Y; pool + train; D2H of every output
+            Xd.copy_(Xh, non_blocking=True)
+            Yd.copy_(Yh, non_blocking=True)
+            pool = cwb.Pool(Xd, gcfg)
+            if args.algo == "acwb":
+                o = pool.train_acwb(Yd, nu=cfg.nu, gamma=0.0034, M=M)
+            else:
+                o = pool.train_hcwb(Yd, vm, nu=cfg.nu, gamma=0.037, pat0=5, M=M)
+            for k_, v_ in o.items():
+                if k_ not in host_out:
+                    host_out[k_] = torch.empty(v_.shape, dtype=v_.dtype).pin_memory()
+                host_out[k_].copy_(v_, non_blocking=True)
+            pool.close()
+            stream.synchronize()
     for i in range(3):
         e2e_step()
     e_ms = []
@@ -305,14 +343,14 @@ def main():
         e_ms.append(e0.elapsed_time(e1))
     e2e_ms = D.max_over_ranks(float(np.mean(e_ms)), w, devname)
     h2d = ds.X.nbytes + ds.Y.nbytes
-    d2h = sum(v.numel() * v.element_size() for v in outh.values())
+    d2h = sum(v.numel() * v.element_size() for v in (outh if args.algo == "cwb" else host_out).values())
 
     # ---- kernel-only time of one k_train_fused launch (plan cached: one launch per call),
     #      CUDA events on the launching stream, for the roofline
     kpool = cwb.Pool(X, gcfg)
     if args.path:
         kpool.set_path(args.path)
-    kouts = kpool.train(Y, nu=cfg.nu, M=M)
+    kouts = train(kpool)
     kpool.status()
     k_ms = []
     for i in range(max(3, min(args.steps, 10))):
@@ -320,7 +358,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = kpool.launches()
         e0.record(stream)
-        kouts = kpool.train(Y, nu=cfg.nu, M=M, out=kouts)
+        kouts = train(kpool, kouts)
         e1.record(stream)
         e1.synchronize()
         k_ms.append(e0.elapsed_time(e1))
@@ -329,7 +367,7 @@ def main():
     kernel_ms = float(np.mean(k_ms))
     if rank == 0:
         peaks, src = load_peaks()
-        ops = alg_ops_per_rep_iter(cfg, n_star, d) * B * M
+        ops = alg_ops_per_rep_iter(cfg, n_star, d) * B * M * (1 if args.algo == "cwb" else 2)
         achieved = ops / (kernel_ms * 1e-3)
         peak = fp64_peak_ops(peaks)
         traffic = None
@@ -348,10 +386,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper Sec. 4.1.1 generator, seeded; OpenML sets not available)",
-            "config": workload_config(cfg, n_star, d),
+            "config": dict(workload_config(cfg, n_star, d), algo=args.algo),
             "iters_per_s": M / (ms_per_step * 1e-3),
             "phase_ms": {"init": float(np.mean(init_ms)), "train": float(np.mean(train_ms))},
-            "roofline": {"bound": "alu", "kernel": "k_train_fused" if args.path != 2 else "general path",
+            "roofline": {"bound": "alu",
+                         "kernel": ("k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
+                         else f"{args.algo} per-iteration kernels (general path)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel_ms": kernel_ms, "launches_per_call": int(k_launches),
@@ -365,7 +405,8 @@ def main():
                                       "ceiling of this kernel")}},
             "e2e": {"value": evals / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-                    "api": "cwb_fit_host (pinned host buffers, copies + init + train + sync)"},
+                    "api": ("cwb_fit_host (pinned host buffers, copies + init + train + sync)" if args.algo == "cwb"
+                            else f"pinned H2D of X, Y + cwb_init + cwb_train_{args.algo} + D2H of all outputs")},
             "clocks": clk.summary(),
             "gpu_launches": int(sum(launches)),
         }
