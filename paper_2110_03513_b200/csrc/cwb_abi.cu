@@ -327,6 +327,14 @@ int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gam
         return cwb_set_error(c, CWB_EINVAL, "cwb_train_acwb: invalid argument");
     if (c->status) return c->status;
     c->stream = s;
+    if (c->path != 2) {
+        bool launched = false;
+        int rc = cwb_train_acwb_fused(c, Y, B, nu, gamma, M, offset_out, theta_f_out, theta_h_out, k_trace,
+                                      kcor_trace, sse_trace, risk_trace, s, &launched);
+        if (rc || launched) return rc;
+        if (c->path == 1)
+            return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: fused path needs more shared memory than a CTA has");
+    }
     return cwb_train_acwb_general(c, Y, B, nu, gamma, M, offset_out, theta_f_out, theta_h_out, k_trace, kcor_trace,
                                   sse_trace, risk_trace, s);
 }

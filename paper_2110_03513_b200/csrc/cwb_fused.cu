@@ -48,6 +48,7 @@ struct FusedParams {
     int permt_cap;  // entries of permt staged in shared memory (POOL)
     int ztab;       // bit 0: Zs / zj0 staged in shared memory, bit 1: the index vectors too
     double nu;
+    double gamma;  // ACC: momentum parameter (Alg. 2)
     double inv2n;  // 1 / (2n): risk = r^T r / (2n) without a division on the critical path
     const double* Y;
     const void* idx;
@@ -61,6 +62,8 @@ struct FusedParams {
     const double* Cb;     // K x d x 4
     double* offset_out;
     double* agg_out;
+    double* agg2_out;    // ACC: theta_h
+    int32_t* kcor_trace; // ACC
     int32_t* k_trace;
     double* sse_trace;
     double* risk_trace;
@@ -72,8 +75,9 @@ __host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) &
 
 struct SmemLayout {
     size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, ix, total;
+    size_t hh;  // ACC: H = y - h (momentum model), n doubles
     __host__ __device__ SmemLayout(int n, int K, int nsp, int d, int W, int n_multi, int RB, int NW, bool pool,
-                                   size_t permt_bytes, int ztab, int idx_bytes = 1) {
+                                   size_t permt_bytes, int ztab, int idx_bytes = 1, bool acc = false) {
         size_t o = 0;
         r = o; o = align16(o + sizeof(double) * RB * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
         U = o; o = align16(o + sizeof(double) * RB * ((size_t)K * nsp + W));  // +W: window overrun pad
@@ -83,7 +87,8 @@ struct SmemLayout {
         zhat = o; o = align16(o + sizeof(double) * RB * (size_t)nsp);
         agg = o; o = align16(o + sizeof(double) * RB * (size_t)K * d);
         pc = o; o = align16(o + sizeof(double) * RB * (n_multi > 0 ? n_multi : 1));
-        red = o; o = align16(o + sizeof(double) * 2 * RB * (size_t)NW * 32);  // double-buffered per-thread r^T r
+        red = o; o = align16(o + sizeof(double) * 2 * (RB + (acc ? 1 : 0)) * (size_t)NW * 32);  // per-thread r^T r
+        hh = o; if (acc) o = align16(o + sizeof(double) * (size_t)n);
         permt = o; if (pool) o = align16(o + permt_bytes);
         zt = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * W * d);
         ai = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * d * d);
@@ -154,17 +159,21 @@ __device__ __forceinline__ long long phase_mark(long long* acc, long long t0, bo
     return t;
 }
 
-template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB>
+// ACC (accelerated CWB, Alg. 2): RB = 2 columns of ONE replication per CTA, column 0 the pseudo
+// residuals r = y - g, column 1 the error-corrected residuals c; H = y - h in shared memory.
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false>
 __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int T = blockDim.x, NW = T >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b0 = blockIdx.x * RB;
+    static_assert(!ACC || RB == 2, "ACWB runs its two columns as RB = 2");
+    const int b0 = ACC ? blockIdx.x : blockIdx.x * RB;  // ACC: the replication; else the first of RB
     const int n = p.n;
     const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns;
     const int W = p.W;
     const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab,
-                       (int)sizeof(IdxT));
+                       (int)sizeof(IdxT), ACC);
+    double* Hm = (double*)(smem + L.hh);  // ACC only
     double* r = (double*)(smem + L.r);  // r[i * RB + q]
     const unsigned char* rb = smem + L.r;
     double* U = (double*)(smem + L.U);  // U[g * RB + q], g = k * nsp + l
@@ -239,7 +248,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         for (int i = tid; i < n; i += T) {
 #pragma unroll
             for (int q = 0; q < RB; q++) {
-                const double v = (b0 + q < p.B) ? p.Y[(size_t)(b0 + q) * n + i] : 0.0;
+                const int bq = ACC ? b0 : b0 + q;
+                const double v = (bq < p.B) ? p.Y[(size_t)bq * n + i] : 0.0;
                 bad |= !isfinite(v);
                 r[i * RB + q] = v;
                 part[q] += v;
@@ -269,7 +279,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
         __syncthreads();  // everyone has read red[] for f0
 #pragma unroll
-        for (int q = 0; q < RB; q++) red[(RB + q) * T + tid] = part[q];  // rr_0 -> parity 1
+        for (int q = 0; q < RB; q++) red[((ACC ? RB + 1 : RB) + q) * T + tid] = part[q];  // rr_0 -> parity 1
+        if (ACC)  // f = h = g = f0 (Alg. 2 line 2): H = y - f0; r = c = y - f0 already
+            for (int i = tid; i < n; i += T) Hm[i] = r[i * RB];
         __syncthreads();
     }
     if (timed) tm = clock64();
@@ -279,13 +291,40 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     // per-thread partials of r^T r before the update of iteration m (parity (m+1) & 1).
     // Runs in phase A of iteration mp + 1 on the first warps (least H1 work, lowest issue
     // priority), off the critical path.
+    const int NRB = RB + (ACC ? 1 : 0);  // per-thread partial slots: RB columns (+ F^2 for ACC)
+    auto bookkeeping_acc = [&](int mp) {
+        // Alg. 2 parameters: theta_g = (1-vt) theta_f + vt theta_h; theta_f = theta_g + nu e_k theta;
+        // theta_h += eta e_kcor theta_cor; traces; risk of f = F^T F / (2n) (slot RB, parity mp)
+        const double vt = 2.0 / (double)(mp + 2), eta = p.gamma * p.nu / vt;
+        const int k0 = ks_sh[0], k1 = ks_sh[1];
+        double* tf = agg;
+        double* th = agg + K * d;
+        for (int a = lane; a < K * d; a += 32) tf[a] = (1.0 - vt) * tf[a] + vt * th[a];
+        __syncwarp();
+        if (lane < d) {
+            tf[k0 * d + lane] += p.nu * thall[(k0 * RB + 0) * 32 + lane];
+            th[k1 * d + lane] += eta * thall[(k1 * RB + 1) * 32 + lane];
+        }
+        double s0 = 0.0, sf = 0.0;
+        for (int t = lane; t < T; t += 32) {
+            s0 += red[((mp + 1) & 1) * NRB * T + t];
+            sf += red[(mp & 1) * NRB * T + RB * T + t];
+        }
+        const double rr0 = warp_sum(s0), rf = warp_sum(sf);
+        if (lane == 0 && b0 < p.B) {
+            if (p.k_trace) p.k_trace[(size_t)mp * p.B + b0] = k0;
+            if (p.kcor_trace) p.kcor_trace[(size_t)mp * p.B + b0] = k1;
+            if (p.sse_trace) p.sse_trace[(size_t)mp * p.B + b0] = rr0 - best_sh[0];
+            if (p.risk_trace) p.risk_trace[(size_t)mp * p.B + b0] = rf * p.inv2n;
+        }
+    };
     auto bookkeeping = [&](int mp, int q) {
         const int b = b0 + q, kb = ks_sh[q];
         if (lane < d) agg[(q * K + kb) * d + lane] += p.nu * thall[(kb * RB + q) * 32 + lane];
         double s0 = 0.0, s1 = 0.0;
         for (int t = lane; t < T; t += 32) {
-            s0 += red[((mp + 1) & 1) * RB * T + q * T + t];
-            s1 += red[(mp & 1) * RB * T + q * T + t];
+            s0 += red[((mp + 1) & 1) * NRB * T + q * T + t];
+            s1 += red[(mp & 1) * NRB * T + q * T + t];
         }
         const double rr0 = warp_sum(s0), rr1 = warp_sum(s1);
         if (lane == 0 && b < p.B) {
@@ -296,7 +335,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     };
 
     for (int m = 0; m < p.M; m++) {
-        if (m > 0 && warp < RB) bookkeeping(m - 1, warp);
+        if (ACC) {
+            if (m > 0 && warp == 0) bookkeeping_acc(m - 1);
+        } else if (m > 0 && warp < RB) {
+            bookkeeping(m - 1, warp);
+        }
         // ---- A / H1: each lane sums its task, 4 steps per offset load ------------------
         for (int rd = 0; rd < rounds; rd++) {
             const int steps = __ldg(wl + rd * NW + warp);  // warp-uniform
@@ -443,7 +486,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                     if (a + 1 < d) v += za.y * tk[a + 1];
                     if (a + 2 < d) v += zb.x * tk[a + 2];
                     if (a + 3 < d) v += zb.y * tk[a + 3];
-                    zhat[q * nsp + l] = p.nu * v;
+                    zhat[q * nsp + l] = (ACC && q == 1) ? v : p.nu * v;  // ACC: b_kcor unscaled
                 }
                 if (sl == 0 && lane == 0) { ks_sh[q] = kb; best_sh[q] = best; }
             }
@@ -455,9 +498,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             const int parw = m & 1;
             const IdxT* ik0 = idx + (size_t)ks_sh[0] * n;
             const IdxT* ik1 = idx + (size_t)ks_sh[RB - 1] * n;
-            double acc[RB];
+            double acc[RB], accF = 0.0;
 #pragma unroll
             for (int q = 0; q < RB; q++) acc[q] = 0.0;
+            // ACC (Alg. 2, ACWB iteration ma = m + 1): F = r - nu b_k (line 8), H -= eta b_kcor (line 16),
+            // next columns r' = (1 - vt1) F + vt1 H (lines 4-6), c' = r' + a1 (c - b_kcor) (line 10)
+            const double vt = 2.0 / (double)(m + 2), eta = p.gamma * p.nu / vt;
+            const double vt1 = 2.0 / (double)(m + 3), a1 = (double)(m + 2) / (double)(m + 3);
             for (int i0 = tid; i0 < n; i0 += 4 * T) {
                 uint32_t j0[4], j1[4];
 #pragma unroll
@@ -474,6 +521,18 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                             const double v = r[i] - zhat[j0[e]];
                             r[i] = v;
                             acc[0] = fma(v, v, acc[0]);
+                        } else if (ACC) {
+                            const double2 v = *reinterpret_cast<double2*>(r + 2 * i);
+                            const double bc = zhat[nsp + j1[e]];
+                            const double F = v.x - zhat[j0[e]];
+                            const double H = Hm[i] - eta * bc;
+                            const double rn = (1.0 - vt1) * F + vt1 * H;
+                            const double cn = rn + a1 * (v.y - bc);
+                            Hm[i] = H;
+                            *reinterpret_cast<double2*>(r + 2 * i) = make_double2(rn, cn);
+                            accF = fma(F, F, accF);
+                            acc[0] = fma(rn, rn, acc[0]);
+                            acc[RB - 1] = fma(cn, cn, acc[RB - 1]);
                         } else {
                             double2 v = *reinterpret_cast<double2*>(r + 2 * i);
                             v.x -= zhat[j0[e]];
@@ -486,19 +545,34 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 }
             }
 #pragma unroll
-            for (int q = 0; q < RB; q++) red[(parw * RB + q) * T + tid] = acc[q];
+            for (int q = 0; q < RB; q++) red[(parw * NRB + q) * T + tid] = acc[q];
+            if (ACC) red[(parw * NRB + RB) * T + tid] = accF;
         }
         __syncthreads();
         if (timed) tm = phase_mark(&tD, tm, true);
     }
-    if (p.M > 0 && warp < RB) bookkeeping(p.M - 1, warp);
+    if (ACC) {
+        if (p.M > 0 && warp == 0) bookkeeping_acc(p.M - 1);
+    } else if (p.M > 0 && warp < RB) {
+        bookkeeping(p.M - 1, warp);
+    }
     __syncthreads();  // agg complete
-#pragma unroll
-    for (int q = 0; q < RB; q++)
-        if (b0 + q < p.B) {
-            for (int a = tid; a < K * d; a += T) p.agg_out[(size_t)(b0 + q) * K * d + a] = agg[q * K * d + a];
-            if (tid == 0 && p.offset_out) p.offset_out[b0 + q] = f0[q];
+    if (ACC) {
+        if (b0 < p.B) {
+            for (int a = tid; a < K * d; a += T) {
+                p.agg_out[(size_t)b0 * K * d + a] = agg[a];
+                p.agg2_out[(size_t)b0 * K * d + a] = agg[K * d + a];
+            }
+            if (tid == 0 && p.offset_out) p.offset_out[b0] = f0[0];
         }
+    } else {
+#pragma unroll
+        for (int q = 0; q < RB; q++)
+            if (b0 + q < p.B) {
+                for (int a = tid; a < K * d; a += T) p.agg_out[(size_t)(b0 + q) * K * d + a] = agg[q * K * d + a];
+                if (tid == 0 && p.offset_out) p.offset_out[b0 + q] = f0[q];
+            }
+    }
     if (timed) {
         p.timing[0] = tA; p.timing[1] = tB; p.timing[2] = tC; p.timing[3] = tD;
     }
@@ -826,18 +900,22 @@ __global__ void k_fused_pack(const int32_t* __restrict__ plan, const int32_t* __
     }
 }
 
-template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB>
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false>
 int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
-    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB>;
+    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB, ACC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -1;
-    const int grid = (fp.B + RB - 1) / RB;
+    const int grid = ACC ? fp.B : (fp.B + RB - 1) / RB;
     kern<<<grid, T, smem, s>>>(fp);
     return 0;
 }
 
 template <typename IdxT, typename PermT>
-int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s) {
+int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s, bool acc = false) {
+    if (acc) {  // ACWB: two columns of one replication, 512 threads
+        if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, true>(fp, T, smem, s);
+        return launch_t<IdxT, PermT, 2, false, 512, 1, true>(fp, T, smem, s);
+    }
     if (RB == 2) {
         if (T > 512) {
             if (pool) return launch_t<IdxT, PermT, 2, true, 768, 1>(fp, T, smem, s);
@@ -1021,12 +1099,25 @@ int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
     return fused_plan_launch(c, f, c->s2);
 }
 
-int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
-                    double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
-                    cudaStream_t s, bool* launched) {
+// Shared host path of the fused CWB (acc = false) and ACWB (acc = true) launches.
+static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, double nu, double gamma, int32_t M,
+                              double* offset_out, double* theta_out, double* theta_h_out, int32_t* k_trace,
+                              int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s,
+                              bool* launched) {
     *launched = false;
     FusedShape f;
-    if (!fused_shape(c, B, &f)) return CWB_OK;  // does not fit: caller uses the general path
+    if (acc) {  // the two columns (r, c) of a replication run as RB = 2 in a 512-thread CTA
+        if ((int64_t)c->K * c->n + 8 > INT32_MAX || (int64_t)c->K * c->n_star * 16 > 200 * 1024) return CWB_OK;
+        f.RB = 2;
+        f.T = 512;
+        f.permt_bytes = 16 * (c->n + kPadRows) <= 65535 ? 2 : 4;
+        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
+        if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, 2, f.T / 32, false, 0, 0, c->idx_bytes, true)
+                .total > kMaxSmem)
+            return CWB_OK;
+    } else if (!fused_shape(c, B, &f)) {
+        return CWB_OK;  // does not fit: caller uses the general path
+    }
     int rc = CWB_OK;
     const bool have = (c->plan_pending && c->plan_T == f.T && c->plan_rb == f.RB) ||
                       (!c->plan_pending && c->fused_T == f.T && c->fused_rb == f.RB && c->plan);
@@ -1036,15 +1127,15 @@ int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M
     if (rc) return rc;
     if (c->fused_T != f.T) return CWB_OK;  // plan failed on the device: cwb_status reports it
     CWB_CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_plan, 0));  // the plan may come from the side stream
-    // pool staging levels with the exact schedule size: schedule + B tables, then Zs / zj0
     const size_t lim = (f.RB == 1 && f.T <= 384) ? kTwoCtaSmem : kMaxSmem;
     const size_t pbytes = ((size_t)(c->permt_entries + kSlackEntries) * f.permt_bytes + 15) / 16 * 16;  // < plan_cap
     f.pool = false;
     const int nm = c->plan_multi;
-    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, 0).total;
+    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, 0, c->idx_bytes, acc).total;
+    if (f.smem > lim) return CWB_OK;
     int ztab = 0;
     {   // POOL: schedule, B tables, Zs / zj0 and the index vectors all in shared memory, or none
-        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, 3, c->idx_bytes);
+        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, 3, c->idx_bytes, acc);
         if (L1.total <= lim) {
             f.pool = true;
             ztab = 3;
@@ -1053,25 +1144,41 @@ int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M
     }
     FusedParams fp;
     fp.n = (int)c->n; fp.K = c->K; fp.ns = c->n_star; fp.nsp = c->nsp; fp.d = c->d; fp.M = M; fp.B = B; fp.nu = nu;
+    fp.gamma = gamma;
     fp.n_multi = c->plan_multi;
     fp.ztab = ztab;
     fp.permt_cap = (int)(pbytes / f.permt_bytes);
     fp.Y = Y; fp.idx = c->idx; fp.permt = c->permt; fp.plan = c->plan; fp.zj0 = c->zj0; fp.Zs = c->Zs;
     fp.inv2n = 1.0 / (2.0 * (double)c->n);
     fp.ZT = c->ZT; fp.lwin = c->lwin; fp.Ainv = c->Ainv; fp.Cb = c->Cb; fp.W = c->W;
-    fp.offset_out = offset_out; fp.agg_out = theta_agg_out;
-    fp.k_trace = k_trace; fp.sse_trace = sse_trace; fp.risk_trace = risk_trace;
+    fp.offset_out = offset_out; fp.agg_out = theta_out; fp.agg2_out = theta_h_out;
+    fp.k_trace = k_trace; fp.kcor_trace = kcor_trace; fp.sse_trace = sse_trace; fp.risk_trace = risk_trace;
     fp.timing = c->timing;
     fp.status = c->d_status;
     const bool i8 = c->idx_bytes == 1, p16 = f.permt_bytes == 2;
-    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s);
-    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s);
-    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s);
-    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s);
+    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
+    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
+    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
+    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
     if (rc) return cwb_set_error(c, CWB_ECUDA, "fused kernel: cannot set shared memory size");
     c->launches++;
     c->fused_smem = f.smem;
     c->fused_pool = f.pool;
     *launched = true;
     return cwb_check_launch(c, "k_train_fused");
+}
+
+int cwb_train_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                    double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+                    cudaStream_t s, bool* launched) {
+    return train_fused_common(c, false, Y, B, nu, 0.0, M, offset_out, theta_agg_out, nullptr, k_trace, nullptr,
+                              sse_trace, risk_trace, s, launched);
+}
+
+int cwb_train_acwb_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, double gamma, int32_t M,
+                         double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
+                         int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s,
+                         bool* launched) {
+    return train_fused_common(c, true, Y, B, nu, gamma, M, offset_out, theta_f_out, theta_h_out, k_trace,
+                              kcor_trace, sse_trace, risk_trace, s, launched);
 }

@@ -124,6 +124,10 @@ int cwb_fused_plan(cwb_ctx* ctx, cudaStream_t s);
 int cwb_train_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
                       double* offset_out, double* theta_agg_out, int32_t* k_trace,
                       double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_train_acwb_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, double gamma, int32_t M,
+                         double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
+                         int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s,
+                         bool* launched);
 int cwb_train_acwb_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double gamma, int32_t M,
                            double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
                            int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s);
