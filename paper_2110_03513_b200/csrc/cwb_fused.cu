@@ -807,13 +807,16 @@ __global__ void k_fused_sched(const int32_t* __restrict__ plan, const int32_t* _
 #pragma unroll 1
         for (int e = 0; e < G; e++) {
             const int cur = (first + e) % G;
-            int pick = -1;
-            if (L == cur && tot > 0) {
-                int bv = 0;
+            // most rows among the free colours, ties lowest colour: max of packed keys
+            // (rem << 4 | 15 - c), reduced as a tree to keep the dependent chain short
+            int kv[G];
 #pragma unroll
-                for (int c = 0; c < G; c++)
-                    if (!((taken >> c) & 1u) && rem[c] > bv) { bv = rem[c]; pick = c; }
-            }
+            for (int c = 0; c < G; c++) kv[c] = ((taken >> c) & 1u) ? 0 : (rem[c] << 4) | (15 - c);
+#pragma unroll
+            for (int w = G / 2; w > 0; w >>= 1)
+#pragma unroll
+                for (int c = 0; c < w; c++) kv[c] = max(kv[c], kv[c + w]);
+            int pick = (L == cur && tot > 0 && (kv[0] >> 4) > 0) ? 15 - (kv[0] & 15) : -1;
             pick = __shfl_sync(0xffffffffu, pick, cur, G);
             if (pick >= 0) {
                 taken |= 1u << pick;
