@@ -14,7 +14,10 @@ Timing: W warm-up steps, then K steps, each bracketed by CUDA events on the
 launching stream; L2 is flushed (256 MiB write) between steps outside the
 events; barrier + synchronize around the timed region; max over ranks.
 N > 1 (torchrun): replications are sharded (weak scaling, every rank its own
-B replications, no collective on the data path).
+B replications, no collective on the data path); with --shard rows the rows
+are (strong scaling: the B replications of the workload on n rows split over
+the ranks, one NCCL all-reduce of (K d + 1) x B doubles per iteration issued
+by libcwb).
 
 --impl reference times the CPU oracle (oracle/, plain fp64 C) on a bounded
 sample of the same workload on the host cores (rank 0 only).
@@ -197,6 +200,8 @@ def main():
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 fused, 2 general")
     ap.add_argument("--algo", default="cwb", choices=["cwb", "acwb", "hcwb"],
                     help="cwb: Alg. 1 supp. (default, the headline); acwb: Alg. 2; hcwb: Alg. 3")
+    ap.add_argument("--shard", default="replications", choices=["replications", "rows"],
+                    help="multi-GPU sharding: replications (weak, default) or rows (strong, NCCL per iteration)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     args = ap.parse_args()
@@ -217,13 +222,29 @@ def main():
     D.init_process_group(w, "nccl", torch.device(devname))
     from paper_2110_03513_b200 import cwb
 
-    # this rank's replications (weak scaling): rank r owns [r*B, (r+1)*B)
-    reps = D.replication_block(cfg.B, rank)
+    rows = args.shard == "rows"
+    if rows and args.algo != "cwb":
+        raise SystemExit("--shard rows supports --algo cwb only")
+    # replications: this rank's block (weak scaling), rank r owns [r*B, (r+1)*B);
+    # rows: the workload's B replications on every rank, this rank's row block of them
+    reps = range(cfg.B) if rows else D.replication_block(cfg.B, rank)
     ds = S.make(cfg, reps=reps)
+    blk = D.row_block(cfg.n, rank, ws) if rows else range(cfg.n)
     X = torch.as_tensor(ds.X, device=devname)
-    Y = torch.as_tensor(ds.Y, device=devname)
+    Y_host = np.ascontiguousarray(ds.Y[:, blk.start:blk.stop])
+    Y = torch.as_tensor(Y_host, device=devname)
     gcfg = cwb.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots,
-                      degree=cfg.degree, df=cfg.df, batch_hint=cfg.B)
+                      degree=cfg.degree, df=cfg.df, batch_hint=0 if rows else cfg.B)
+    comm = None
+    if rows:  # libcwb's own NCCL communicator, id from rank 0 over the torch process group
+        uid = D.nccl_unique_id(w, torch.device(devname)) if ws > 1 else cwb.cwb_comm_unique_id()
+        comm = cwb.Comm(rank, ws, unique_id=uid)
+
+    def new_pool(Xsrc):
+        p_ = cwb.Pool(Xsrc, gcfg)
+        if comm is not None:
+            p_.attach(comm)
+        return p_
     B, K, n, M = cfg.B, cfg.K, cfg.n, cfg.M
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=devname)
@@ -244,7 +265,7 @@ def main():
         nonlocal outs
         a, b, c_ = ev[i]
         a.record(stream)
-        pool = cwb.Pool(X, gcfg)
+        pool = new_pool(X)
         if args.path:
             pool.set_path(args.path)
         b.record(stream)
@@ -288,12 +309,12 @@ def main():
         evals_rank = int(K * n * (2 * sw + (M - sw)).sum())
     else:
         evals_rank = K * n * B * M
-    evals = evals_rank * ws
+    evals = evals_rank if rows else evals_rank * ws
     value = evals / (ms_per_step * 1e-3)
 
     # ---- end-to-end through the host-pointer C-ABI call (pinned host buffers)
     Xh = torch.as_tensor(ds.X).pin_memory()
-    Yh = torch.as_tensor(ds.Y).pin_memory()
+    Yh = torch.as_tensor(Y_host).pin_memory()
     outh = {"offset": torch.empty(B, dtype=torch.float64).pin_memory(),
             "theta_agg": torch.empty((B, K, d), dtype=torch.float64).pin_memory(),
             "k_trace": torch.empty((M, B), dtype=torch.int32).pin_memory(),
@@ -311,7 +332,7 @@ def main():
         if rc:
             raise cwb.CwbError(rc, lib.cwb_last_error(None).decode())
 
-    if args.algo != "cwb":
+    if args.algo != "cwb" or rows:
         Xd = torch.empty_like(X)
         Yd = torch.empty_like(Y)
         host_out = {}
@@ -319,8 +340,10 @@ def main():
         def e2e_step():  # noqa: F811 - pinned H2D of X, Y; pool + train; D2H of every output
             Xd.copy_(Xh, non_blocking=True)
             Yd.copy_(Yh, non_blocking=True)
-            pool = cwb.Pool(Xd, gcfg)
-            if args.algo == "acwb":
+            pool = new_pool(Xd)
+            if args.algo == "cwb":
+                o = pool.train(Yd, nu=cfg.nu, M=M)
+            elif args.algo == "acwb":
                 o = pool.train_acwb(Yd, nu=cfg.nu, gamma=0.0034, M=M)
             else:
                 o = pool.train_hcwb(Yd, vm, nu=cfg.nu, gamma=0.037, pat0=5, M=M)
@@ -342,12 +365,12 @@ def main():
         e1.synchronize()
         e_ms.append(e0.elapsed_time(e1))
     e2e_ms = D.max_over_ranks(float(np.mean(e_ms)), w, devname)
-    h2d = ds.X.nbytes + ds.Y.nbytes
-    d2h = sum(v.numel() * v.element_size() for v in (outh if args.algo == "cwb" else host_out).values())
+    h2d = ds.X.nbytes + Y_host.nbytes
+    d2h = sum(v.numel() * v.element_size() for v in (outh if args.algo == "cwb" and not rows else host_out).values())
 
     # ---- kernel-only time of one k_train_fused launch (plan cached: one launch per call),
     #      CUDA events on the launching stream, for the roofline
-    kpool = cwb.Pool(X, gcfg)
+    kpool = new_pool(X)
     if args.path:
         kpool.set_path(args.path)
     kouts = train(kpool)
@@ -367,7 +390,9 @@ def main():
     kernel_ms = float(np.mean(k_ms))
     if rank == 0:
         peaks, src = load_peaks()
-        ops = alg_ops_per_rep_iter(cfg, n_star, d) * B * M * (1 if args.algo == "cwb" else 2)
+        import dataclasses
+        ops = alg_ops_per_rep_iter(dataclasses.replace(cfg, n=len(blk)), n_star, d) * B * M * (
+            1 if args.algo == "cwb" else 2)  # this rank's rows
         achieved = ops / (kernel_ms * 1e-3)
         peak = fp64_peak_ops(peaks)
         traffic = None
@@ -384,13 +409,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if rows else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper Sec. 4.1.1 generator, seeded; OpenML sets not available)",
-            "config": dict(workload_config(cfg, n_star, d), algo=args.algo),
+            "config": dict(workload_config(cfg, n_star, d), algo=args.algo, shard=args.shard,
+                           parallelism=(f"rows{ws}" if rows else f"replications{ws}")),
             "iters_per_s": M / (ms_per_step * 1e-3),
             "phase_ms": {"init": float(np.mean(init_ms)), "train": float(np.mean(train_ms))},
             "roofline": {"bound": "alu",
-                         "kernel": ("k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
+                         "kernel": ("general path, row-sharded" if rows else
+                                    "k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
                          else f"{args.algo} per-iteration kernels (general path)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -405,7 +432,8 @@ def main():
                                       "ceiling of this kernel")}},
             "e2e": {"value": evals / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-                    "api": ("cwb_fit_host (pinned host buffers, copies + init + train + sync)" if args.algo == "cwb"
+                    "api": ("cwb_fit_host (pinned host buffers, copies + init + train + sync)"
+                            if args.algo == "cwb" and not rows
                             else f"pinned H2D of X, Y + cwb_init + cwb_train_{args.algo} + D2H of all outputs")},
             "clocks": clk.summary(),
             "gpu_launches": int(sum(launches)),
@@ -417,6 +445,9 @@ def main():
             except Exception as e:  # keep the GPU line even if the host leg fails
                 line["cpu_baseline"] = {"error": str(e)}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

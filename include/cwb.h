@@ -218,6 +218,62 @@ int cwb_predict(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offse
  * the M iterations.  NULL switches it off (default). */
 int cwb_set_phase_timing(cwb_ctx* ctx, int64_t* cycles4);
 
+/* ------------------------------------------------------------- row sharding
+ * The rows of the data are partitioned over `world` ranks (one process and GPU
+ * each).  binMatVec is linear in the rows -- u(l) is a sum over the rows i of bin l
+ * and s = Zb^T u -- and so is r^T r, so each iteration needs
+ * the sum over ranks of the per-rank s (K x d per replication) and r^T r: one
+ * all-reduce of (K d + 1) x Bp doubles (Bp = B rounded up to 32).  The selection
+ * (P:L292), theta, theta_agg and the traces are then the same bytes on every rank,
+ * and the residual update touches the local rows only.
+ *
+ * Every rank calls cwb_init on the FULL X (the pool -- bins, basis, G, lambda,
+ * A^-1 -- is a function of all rows; identical on every rank) and then
+ * attaches exactly once, before its first cwb_train / cwb_find_best.  From then
+ * on the context holds only rows [row_begin, row_end) = [floor(n r / W),
+ * floor(n (r + 1) / W)) of the index vectors, cwb_train / cwb_find_best take the
+ * LOCAL block Y[B][row_end - row_begin] (R for find_best) and every rank must make
+ * the same sequence of calls with the same B, nu and M.  offset = mean over all n
+ * rows, risk = r^T r / (2 n) with the global n.  Sums of different rank counts
+ * differ in rounding order from the unsharded run (within the parity tolerance).
+ * cwb_get_dims then reports the local row count.  cwb_train_acwb / cwb_train_hcwb
+ * and the fused path are not available on a row-sharded context
+ * (CWB_EUNSUPPORTED).  Errors: CWB_EINVAL (rank outside [0, world), world > n,
+ * already attached), CWB_ENCCL (library or communicator failure). */
+
+/* Writes a fresh NCCL unique id (128 bytes, HOST buffer) for cwb_comm_init:
+ * call on one rank and send the bytes to the others.  The NCCL library
+ * (libnccl.so.2) is loaded on first use; CWB_ENCCL if it cannot be. */
+int cwb_comm_unique_id(void* id_out128);
+
+/* A communicator of `world` ranks, this process being `rank`; it may serve any
+ * number of contexts (one at a time per stream) and must outlive them.
+ * cwb_comm_init: an NCCL communicator, ncclCommInitRank(world, id, rank) on the
+ * current device (all ranks call it collectively); the all-reduces are issued
+ * on the stream of each cwb_train / cwb_find_best call.
+ * cwb_comm_init_fn: the caller's collective.  fn(buf, count, stream, user) must
+ * replace the DEVICE array buf[count] (fp64) by its elementwise sum over the
+ * world ranks -- the same bytes on every rank -- ordered after the work already
+ * on `stream` and before the work enqueued after it returns (it may synchronise
+ * the stream), and return 0 (anything else fails the call with CWB_ENCCL).
+ * Errors: CWB_EINVAL (rank outside [0, world), NULL arguments), CWB_ENCCL. */
+typedef struct cwb_comm cwb_comm;
+typedef int (*cwb_allreduce_fn)(double* buf, int64_t count, cudaStream_t stream, void* user);
+int cwb_comm_init(cwb_comm** comm, const void* id128, int32_t rank, int32_t world);
+int cwb_comm_init_fn(cwb_comm** comm, cwb_allreduce_fn fn, void* user, int32_t rank, int32_t world);
+
+/* Destroys the communicator (NCCL: ncclCommDestroy).  No context attached to it may
+ * be used afterwards; work they enqueued must have completed.  comm may be NULL. */
+void cwb_comm_free(cwb_comm* comm);
+
+/* Row-shard ctx over comm (borrowed): keeps this rank's row block, as described
+ * above.  Once per context, before its first cwb_train / cwb_find_best. */
+int cwb_attach_comm(cwb_ctx* ctx, cwb_comm* comm);
+
+/* Host outputs: first row of this context's block and its row count
+ * (0 and n when not sharded), rank and world (0 and 1 when not sharded). */
+int cwb_get_rows(const cwb_ctx* ctx, int64_t* row_begin, int64_t* n_rows, int32_t* rank, int32_t* world);
+
 /* Number of kernels this context has launched so far (bench evidence). */
 int64_t cwb_launch_count(const cwb_ctx* ctx);
 

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcwb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
+FLAGS = ["-shared", "-Xcompiler", "-fPIC", "-ldl", "-gencode", "arch=compute_100a,code=sm_100a",
          "-lineinfo", "-O3", "-std=c++17", "--expt-relaxed-constexpr"]
 
 

@@ -160,7 +160,7 @@ void cwb_free(cwb_ctx* c) {
     if (c->ev_plan) cudaStreamWaitEvent(s, c->ev_plan, 0);  // a plan still building on the side stream
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
-                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->plan, c->permt,
+                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->plan, c->permt,
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
     if (c->ev_plan) cudaEventDestroy(c->ev_plan);
@@ -289,6 +289,7 @@ int cwb_get_pool(cwb_ctx* c, double* z, uint16_t* idx, double* Zb, double* G, do
 
 int cwb_set_path(cwb_ctx* c, int32_t path) {
     if (!c || path < 0 || path > 2) return cwb_set_error(c, CWB_EINVAL, "cwb_set_path: invalid argument");
+    if (c->rows && path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_set_path: row-sharded context");
     c->path = path;
     return CWB_OK;
 }
@@ -298,6 +299,7 @@ int cwb_find_best(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double
     if (!c || !R || B < 1) return cwb_set_error(c, CWB_EINVAL, "cwb_find_best: invalid argument");
     if (c->status) return c->status;
     c->stream = s;
+    if (c->rows) return cwb_find_best_rows(c, R, B, k_out, theta_out, sse_out, s);
     return cwb_find_best_general(c, R, B, k_out, theta_out, sse_out, s);
 }
 
@@ -308,6 +310,8 @@ int cwb_train(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, doub
         return cwb_set_error(c, CWB_EINVAL, "cwb_train: invalid argument");
     if (c->status) return c->status;
     c->stream = s;
+    if (c->rows)
+        return cwb_train_rows(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace, s);
     if (c->path != 2) {
         bool launched = false;
         int rc = cwb_train_fused(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace,
@@ -327,6 +331,7 @@ int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gam
         return cwb_set_error(c, CWB_EINVAL, "cwb_train_acwb: invalid argument");
     if (c->status) return c->status;
     c->stream = s;
+    if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: row-sharded context");
     if (c->path != 2) {
         bool launched = false;
         int rc = cwb_train_acwb_fused(c, Y, B, nu, gamma, M, offset_out, theta_f_out, theta_h_out, k_trace,
@@ -348,6 +353,7 @@ int cwb_train_hcwb(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_ma
         return cwb_set_error(c, CWB_EINVAL, "cwb_train_hcwb: invalid argument");
     if (c->status) return c->status;
     c->stream = s;
+    if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: row-sharded context");
     return cwb_train_hcwb_general(c, Y, B, val_mask, nu, gamma, pat0, M, offset_out, theta_f_out, k_trace, kcor_trace,
                                   sse_trace, risk_trace, val_risk_trace, switch_iter, s);
 }

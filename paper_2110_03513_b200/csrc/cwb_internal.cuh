@@ -38,6 +38,7 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     size_t colpart_bytes = 0;
     double* acwb = nullptr;    // ACWB: F, H (n x Bq each), row-block partials, offsets
     size_t acwb_bytes = 0;
+    double* pack = nullptr;    // row sharding: [K][d][Bp] partial s, then [Bp] partial r^T r
 };
 
 struct cwb_ctx {
@@ -94,6 +95,12 @@ struct cwb_ctx {
     int32_t plan_T = 0, plan_rb = 0, plan_permt_bytes = 2;
     size_t plan_cap = 0;
 
+    // row sharding (cwb_attach_comm): n is then the local row count
+    bool rows = false;
+    int32_t rank = 0, world = 1;
+    int64_t n_glob = 0, row0 = 0;
+    cwb_comm* comm = nullptr;  // borrowed
+
     cwb_train_ws ws;
 };
 
@@ -139,6 +146,11 @@ int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, do
                            cudaStream_t s);
 int cwb_find_best_general(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out,
                           double* theta_out, double* sse_out, cudaStream_t s);
+int cwb_train_rows(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                   double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_find_best_rows(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                       double* sse_out, cudaStream_t s);
+int cwb_rows_allreduce(cwb_ctx* ctx, double* buf, int64_t count, cudaStream_t s);
 int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
                      const double* theta_agg, int32_t B, double* out, cudaStream_t s);
 

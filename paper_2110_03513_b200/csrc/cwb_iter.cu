@@ -122,13 +122,14 @@ __global__ void k_h1(const double* __restrict__ Rt, int64_t n, int Bp, int K, in
 
 // H2-H4 for one learner (blockIdx.x) and 32 replications (blockIdx.y)
 // (HCWB: column b uses Ainv2 / G2 when phase[b mod Bph] != 0)
+// (row sharding: smode 1 writes s to Sg[k][d][Bp] and stops, smode 2 reads the summed s from Sg)
 __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
                        const int32_t* __restrict__ zj0, const double* __restrict__ Zs,
                        const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
                        const double* __restrict__ G, double* __restrict__ theta,
                        double* __restrict__ delta, const double* __restrict__ Ainv2 = nullptr,
                        const double* __restrict__ G2 = nullptr, const int32_t* __restrict__ phase = nullptr,
-                       int Bph = 0) {
+                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0) {
     __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
     const int k = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -137,11 +138,18 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
     const double* zs = Zs + (size_t)k * ns * CWB_SPW;
     const double* u = U + (size_t)k * ns * Bp + b;
     for (int j = w; j < d; j += nw) {
-        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
-        double s = 0.0;
-        for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * Bp];
+        double s;
+        if (smode == 2) {
+            s = Sg[((size_t)k * d + j) * Bp + b];
+        } else {
+            const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+            s = 0.0;
+            for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * Bp];
+            if (smode == 1) Sg[((size_t)k * d + j) * Bp + b] = s;
+        }
         S[j][lane] = s;
     }
+    if (smode == 1) return;  // block-uniform
     __syncthreads();
     const bool set2 = phase && b < 2 * Bph && phase[b >= Bph ? b - Bph : b] != 0;
     const double* Ai = (set2 ? Ainv2 : Ainv) + (size_t)k * d * d;
@@ -250,6 +258,22 @@ __global__ void k_rr(const double* __restrict__ part, int nblk, int B, int Bp, i
     for (int q = 0; q < nblk; q++) s += part[(size_t)q * Bp + b];
     rr[b] = s;
     if (risk_trace) risk_trace[(size_t)m * B + b] = s / (2.0 * (double)n);
+}
+
+// row sharding: f0[b] = (sum over all ranks' rows) / n, as k_center_fin mode 0
+__global__ void k_mean_glob(const double* __restrict__ sum, int B, int64_t n, double* __restrict__ f0,
+                            double* offset_out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double t = sum[b] / (double)n;
+    f0[b] = t;
+    if (offset_out) offset_out[b] = t;
+}
+
+// row sharding: risk of one iteration from the summed r^T r, as k_rr
+__global__ void k_risk(const double* __restrict__ rr, int B, int64_t n, double* __restrict__ risk_row) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) risk_row[b] = rr[b] / (2.0 * (double)n);
 }
 
 __global__ void k_zero(double* p, size_t cnt) {
@@ -767,6 +791,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     cwb_release(w.narrow, s);
     cwb_release(w.colpart, s);
     cwb_release(w.acwb, s);
+    cwb_release(w.pack, s);
     w = cwb_train_ws();
     const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
     bool ok = true;
@@ -778,6 +803,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     ok &= cwb_alloc((void**)&w.zhat, sizeof(double) * ns * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.kstar, sizeof(int32_t) * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.part, sizeof(double) * (size_t)nblk * Bp, s) == cudaSuccess;
+    if (c->rows) ok &= cwb_alloc((void**)&w.pack, sizeof(double) * (K * d + 1) * Bp, s) == cudaSuccess;
     if (!ok) return cwb_set_error(c, CWB_ENOMEM, "general-path workspace allocation failed");
     w.B = B; w.Bp = Bp; w.n_part = nblk;
     return CWB_OK;
@@ -950,6 +976,124 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
         c->launches += 3;
     }
     return cwb_check_launch(c, "general train kernels");
+}
+
+// ------------------------------------------------------------ row sharding
+// include/cwb.h "row sharding": the context holds rows [row0, row0 + n) of n_glob.
+// Per iteration: local H1 and s = Zb^T u (k_h234 smode 1) into pack[K][d][Bp], the local
+// r^T r in pack[K d Bp ..]; one all-reduce of the pack; then H3-H5 from the summed s and
+// r^T r on every rank (identical bytes in -> identical k*, theta), H6 on the local rows.
+
+// column sums of Y[B][n] (local rows) into out[B]: sum y (f0 == nullptr, sq false) or sum (y - f0)^2
+static int col_sums(cwb_ctx* c, const double* Y, int B, const double* f0, bool sq, double* out, cudaStream_t s) {
+    cwb_train_ws& w = c->ws;
+    const int nblk = (int)((c->n + kColRows - 1) / kColRows);
+    const size_t need = sizeof(double) * (size_t)nblk * B;
+    if (w.colpart_bytes < need) {
+        cwb_release(w.colpart, s);
+        w.colpart = nullptr;
+        w.colpart_bytes = 0;
+        if (cwb_alloc((void**)&w.colpart, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "column statistics workspace allocation failed");
+        w.colpart_bytes = need;
+    }
+    k_colsum<<<dim3(nblk, B), 256, 0, s>>>(Y, c->n, f0, sq, w.colpart, c->d_status);
+    k_center_fin<<<(B + 127) / 128, 128, 0, s>>>(w.colpart, nblk, B, c->n, 1, out, nullptr);
+    c->launches += 2;
+    return CWB_OK;
+}
+
+// H1 + s on the local rows, all-reduce of (s, r^T r), H3-H5 (k_h5 reads the summed r^T r)
+static int find_best_rows_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg, int32_t* k_trace,
+                               double* sse_trace, int32_t* k_out, double* theta_out, double* sse_out,
+                               double* risk_prev, cudaStream_t s) {
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp, K = c->K, d = c->d;
+    double* rr_g = w.pack + (size_t)K * d * Bp;
+    h1(c, w.Rt, Bp, K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+                                            w.delta, nullptr, nullptr, nullptr, 0, w.pack, 1);
+    c->launches += 1;
+    int rc = cwb_check_launch(c, "row-sharded s kernels");
+    if (rc) return rc;
+    rc = cwb_rows_allreduce(c, w.pack, (int64_t)(K * d + 1) * Bp, s);
+    if (rc) return rc;
+    if (risk_prev) {
+        k_risk<<<(B + 127) / 128, 128, 0, s>>>(rr_g, B, c->n_glob, risk_prev);
+        c->launches += 1;
+    }
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+                                            w.delta, nullptr, nullptr, nullptr, 0, w.pack, 2);
+    k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, rr_g, K, d, B, Bp, nu, m, w.kstar, agg, k_trace,
+                                          sse_trace, k_out, theta_out, sse_out);
+    c->launches += 2;
+    return CWB_OK;
+}
+
+int cwb_find_best_rows(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                       double* sse_out, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp;
+    double* rr_g = w.pack + (size_t)c->K * c->d * Bp;
+    CWB_CUDA_TRY(c, cudaMemsetAsync(rr_g, 0, sizeof(double) * Bp, s));
+    rc = col_sums(c, R, B, nullptr, true, rr_g, s);  // local r^T r (f0 = 0)
+    if (rc) return rc;
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(R, c->n, B, Bp, nullptr, nullptr, w.Rt);
+    c->launches += 1;
+    rc = find_best_rows_iter(c, B, 0.0, 0, nullptr, nullptr, nullptr, k_out, theta_out, sse_out, nullptr, s);
+    if (rc) return rc;
+    return cwb_check_launch(c, "row-sharded find_best kernels");
+}
+
+int cwb_train_rows(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                   double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp;
+    double* rr_g = w.pack + (size_t)c->K * c->d * Bp;
+    double* f0 = w.rr + Bp;
+    CWB_CUDA_TRY(c, cudaMemsetAsync(rr_g, 0, sizeof(double) * Bp, s));
+    // f0 = mean over all rows: local sums, all-reduce, / n_glob
+    rc = col_sums(c, Y, B, nullptr, false, rr_g, s);
+    if (rc) return rc;
+    rc = cwb_rows_allreduce(c, rr_g, Bp, s);
+    if (rc) return rc;
+    k_mean_glob<<<(B + 127) / 128, 128, 0, s>>>(rr_g, B, c->n_glob, f0, offset_out);
+    c->launches += 1;
+    rc = col_sums(c, Y, B, f0, true, rr_g, s);  // local r^T r, summed by the first iteration's all-reduce
+    if (rc) return rc;
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, f0, nullptr, w.Rt);
+    const size_t nagg = (size_t)B * c->K * c->d;
+    k_zero<<<(unsigned)min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_agg_out, nagg);
+    c->launches += 2;
+    const int nblk = w.n_part;
+    for (int m = 0; m < M; m++) {
+        double* risk_prev = (risk_trace && m > 0) ? risk_trace + (size_t)(m - 1) * B : nullptr;
+        rc = find_best_rows_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr,
+                                 risk_prev, s);
+        if (rc) return rc;
+        k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, c->n_star,
+                                                                  c->d, B, Bp, nu, B, nu, w.zhat);
+        dim3 g6(nblk, Bp / 32);
+        if (c->idx_bytes == 1)
+            k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
+        else
+            k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
+        k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, rr_g, nullptr);  // local r^T r
+        c->launches += 3;
+    }
+    if (M > 0 && risk_trace) {  // the last iteration's risk needs one more sum
+        rc = cwb_rows_allreduce(c, rr_g, Bp, s);
+        if (rc) return rc;
+        k_risk<<<(B + 127) / 128, 128, 0, s>>>(rr_g, B, c->n_glob, risk_trace + (size_t)(M - 1) * B);
+        c->launches += 1;
+    }
+    return cwb_check_launch(c, "row-sharded train kernels");
 }
 
 // ------------------------------------------------ stand-alone primitives

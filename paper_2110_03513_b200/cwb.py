@@ -22,7 +22,8 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
            "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
-           "cwb_launch_count", "cwb_set_phase_timing", "cwb_free"]
+           "cwb_launch_count", "cwb_set_phase_timing", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
+           "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_get_rows"]
 
 
 class CwbError(RuntimeError):
@@ -54,6 +55,8 @@ class Config:
 
 _lib = None
 _vp, _i32, _i64, _f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+# int (*cwb_allreduce_fn)(double* buf, int64_t count, cudaStream_t stream, void* user)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 
 
 def load() -> C.CDLL:
@@ -92,6 +95,13 @@ def load() -> C.CDLL:
     L.cwb_launch_count.restype = C.c_int64
     L.cwb_free.argtypes = [_vp]
     L.cwb_free.restype = None
+    L.cwb_comm_unique_id.argtypes = [_vp]
+    L.cwb_comm_init.argtypes = [C.POINTER(_vp), _vp, _i32, _i32]
+    L.cwb_comm_init_fn.argtypes = [C.POINTER(_vp), ALLREDUCE_FN, _vp, _i32, _i32]
+    L.cwb_comm_free.argtypes = [_vp]
+    L.cwb_comm_free.restype = None
+    L.cwb_attach_comm.argtypes = [_vp, _vp]
+    L.cwb_get_rows.argtypes = [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)]
     _lib = L
     return L
 
@@ -338,6 +348,65 @@ def cwb_free(ctx) -> None:
         load().cwb_free(ctx)
 
 
+# ------------------------------------------------------------- row sharding
+
+def cwb_comm_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (call on one rank, send the bytes to the others)."""
+    buf = C.create_string_buffer(128)
+    _chk(load().cwb_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+class Comm:
+    """RAII wrapper of a cwb_comm: an NCCL communicator built by libcwb (unique_id given), or
+    the caller's collective fn(buf_ptr, count, stream_ptr) -> None, which must replace the
+    device fp64 array buf[count] by its sum over the ranks (include/cwb.h)."""
+
+    def __init__(self, rank: int, world: int, unique_id: bytes | None = None, fn=None):
+        self.rank, self.world, self.h, self._cb = rank, world, C.c_void_p(), None
+        if unique_id is not None:
+            if len(unique_id) != 128:
+                raise ValueError("unique_id must be 128 bytes")
+            buf = C.create_string_buffer(bytes(unique_id), 128)
+            _chk(load().cwb_comm_init(C.byref(self.h), C.cast(buf, C.c_void_p), rank, world))
+        elif fn is not None:
+            def tramp(buf, count, stream, user):
+                try:
+                    fn(buf, count, stream)
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported to C as a failed collective
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            self._cb = ALLREDUCE_FN(tramp)
+            _chk(load().cwb_comm_init_fn(C.byref(self.h), self._cb, None, rank, world))
+        else:
+            raise ValueError("need unique_id or fn")
+
+    def close(self):
+        if self.h:
+            load().cwb_comm_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cwb_attach_comm(ctx, comm: Comm) -> None:
+    """Row-shard ctx over comm (include/cwb.h "row sharding")."""
+    _chk(load().cwb_attach_comm(ctx, comm.h), ctx)
+
+
+def cwb_get_rows(ctx):
+    """(row_begin, n_rows, rank, world) of the context."""
+    r0, nl, rk, ws = _i64(), _i64(), _i32(), _i32()
+    _chk(load().cwb_get_rows(ctx, C.byref(r0), C.byref(nl), C.byref(rk), C.byref(ws)), ctx)
+    return r0.value, nl.value, rk.value, ws.value
+
+
 class Pool:
     """RAII wrapper of a cwb_ctx."""
 
@@ -377,6 +446,14 @@ class Pool:
 
     def launches(self):
         return cwb_launch_count(self.ctx)
+
+    def attach(self, comm: Comm):
+        cwb_attach_comm(self.ctx, comm)
+        self._comm = comm  # the communicator must outlive the context
+        self.n_star, self.d, self.K, self.n = cwb_get_dims(self.ctx)
+
+    def rows(self):
+        return cwb_get_rows(self.ctx)
 
     def close(self):
         if self.ctx:

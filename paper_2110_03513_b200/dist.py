@@ -1,8 +1,15 @@
 """Multi-GPU plumbing (host side only): one process per GPU, torch.distributed for the
-process group.  The hot path shards over REPLICATIONS (independent boosting runs that
-share X): every rank builds the pool from the same X and trains its
-own contiguous block of replications -- no collective on the data path.  Collectives
-are used only for timing (max over ranks) and, optionally, to gather results.
+process group.  Two shardings:
+
+* REPLICATIONS (independent boosting runs that share X): every rank builds the pool
+  from the same X and trains its own contiguous block of replications -- no
+  collective on the data path.  Collectives are used only for timing (max over
+  ranks) and, optionally, to gather results.
+* ROWS (include/cwb.h "row sharding"): every rank builds the pool from the full X,
+  keeps the row block `row_block(n, rank, world)` and sums s = Zb^T u and r^T r with
+  one all-reduce per iteration -- issued by libcwb itself over its own NCCL
+  communicator (cwb.Comm(rank, world, unique_id=nccl_unique_id(w))), or through
+  torch.distributed (cwb.Comm(rank, world, fn=torch_allreduce_fn())).
 """
 from __future__ import annotations
 
@@ -79,3 +86,61 @@ def gather_rows(t, w: World):
     parts = [torch.empty_like(t) for _ in range(w.size)]
     dist.all_gather(parts, t.contiguous())
     return torch.cat(parts, 0)
+
+
+def row_block(n: int, rank: int, world: int) -> range:
+    """Rows [floor(n r / W), floor(n (r+1) / W)) of rank r: the block libcwb keeps after an
+    attach (cwb_rows.cu restrict_rows uses the same formula)."""
+    if world < 1 or not 0 <= rank < world or n < world:
+        raise ValueError("need 0 <= rank < world <= n")
+    return range(n * rank // world, n * (rank + 1) // world)
+
+
+def broadcast_bytes(data: bytes | None, w: World, src: int = 0, device="cpu") -> bytes:
+    """Rank src's bytes on every rank (e.g. the 128-byte NCCL unique id)."""
+    if w.size <= 1:
+        return bytes(data)
+    import torch
+    import torch.distributed as dist
+    n = torch.tensor([len(data) if w.rank == src else 0], dtype=torch.int64, device=device)
+    dist.broadcast(n, src)
+    buf = torch.zeros(int(n.item()), dtype=torch.uint8, device=device)
+    if w.rank == src:
+        buf.copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+    dist.broadcast(buf, src)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+def nccl_unique_id(w: World, device="cpu") -> bytes:
+    """A libcwb NCCL unique id made on rank 0 and broadcast to all ranks."""
+    from . import cwb
+    uid = cwb.cwb_comm_unique_id() if w.rank == 0 else None
+    return broadcast_bytes(uid, w, 0, device)
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of a raw device fp64 array (no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+def device_view(ptr: int, count: int, device="cuda"):
+    import torch
+    return torch.as_tensor(_DevArray(ptr, count), device=device)
+
+
+def torch_allreduce_fn(device="cuda"):
+    """A cwb_comm_init_fn collective over the default torch.distributed group: sums the
+    library's device buffer in place.  The library's stream is synchronised first and the
+    sum is complete when the callback returns (the stream contract of cwb_allreduce_fn)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(ptr, count, stream):
+        torch.cuda.synchronize(device)
+        t = device_view(ptr, count, device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        torch.cuda.synchronize(device)
+    return fn

@@ -86,3 +86,97 @@ def test_split_and_block_host_logic():
         D.split_replications(4, 2, 2)
     w = D.World()
     assert D.max_over_ranks(3.5, w) == 3.5
+
+
+# ----------------------------------------------------------------- row sharding
+# The decomposition the GPU row-sharded path (include/cwb.h "row sharding") relies on,
+# run with the oracle's binMatVec / Cholesky solve as its steps over a world-2 gloo
+# group: every rank holds the full pool and a row block; per iteration the per-rank
+# s = Zb^T u (binMatVec is a sum over rows) and r^T r are all-reduced, the
+# selection runs redundantly, the update touches local rows.  It must reproduce the
+# single-process oracle run.
+
+def _rows_worker(rank, size, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(size),
+                      LOCAL_RANK=str(rank))
+    try:
+        import torch.distributed as dist
+        import cwb_synth as S
+        from oracle import oracle as O
+        w = D.world_from_env()
+        D.init_process_group(w, "gloo")
+        uid = D.broadcast_bytes(bytes(range(128)) if w.rank == 0 else None, w)
+        cfg = S.CONFIGS["R0"]
+        ds = S.make(cfg, reps=range(3))
+        pool = O.Pool(ds.X, O.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed,
+                                     n_knots=cfg.n_knots), O.MODE_BINNED)
+        K, n, d, B, M, nu = pool.K, pool.n, pool.d, ds.Y.shape[0], cfg.M, cfg.nu
+        blk = D.row_block(n, w.rank, w.size)
+        idx = pool.idx[:, blk.start:blk.stop]
+        Y = ds.Y[:, blk.start:blk.stop]
+        t = torch.as_tensor(Y.sum(axis=1))
+        dist.all_reduce(t)
+        f0 = t.numpy() / n
+        R = Y - f0[:, None]
+        rr_loc = (R * R).sum(axis=1)
+        A = [pool.G[k] + pool.lam[k] * pool.D for k in range(K)]
+        ks = np.zeros((M, B), dtype=np.int64)
+        agg = np.zeros((B, K, d))
+        for m in range(M):
+            s_loc = np.array([[O.bin_mat_vec(pool.Zb[k], idx[k], R[b]) for k in range(K)] for b in range(B)])
+            pack = torch.as_tensor(np.concatenate([s_loc.ravel(), rr_loc]))
+            dist.all_reduce(pack)
+            s = pack[: B * K * d].numpy().reshape(B, K, d)
+            rr = pack[B * K * d:].numpy()
+            for b in range(B):
+                th = [O.chol_solve(A[k], s[b, k]) for k in range(K)]
+                sse = [rr[b] - 2 * th[k] @ s[b, k] + th[k] @ pool.G[k] @ th[k] for k in range(K)]
+                k = int(np.argmin(sse))
+                ks[m, b] = k
+                agg[b, k] += nu * th[k]
+                R[b] -= nu * (pool.Zb[k][idx[k]] @ th[k])
+            rr_loc = (R * R).sum(axis=1)
+        if w.rank == 0:
+            q.put(("ok", ks, agg, f0, uid))
+        dist.destroy_process_group()
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+        q.put(("err", traceback.format_exc()))
+
+
+def test_row_sharding_decomposition_matches_single_process():
+    size = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, size, port, q)) for r in range(size)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert out[0] == "ok", out
+    _, ks, agg, f0, uid = out
+    import cwb_synth as S
+    from oracle import oracle as O
+    cfg = S.CONFIGS["R0"]
+    ds = S.make(cfg, reps=range(3))
+    pool = O.Pool(ds.X, O.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots),
+                  O.MODE_BINNED)
+    ref = pool.train(ds.Y, nu=cfg.nu, M=cfg.M)
+    assert uid == bytes(range(128))
+    assert (ks == ref.k_trace).all()
+    np.testing.assert_allclose(f0, ref.offset, rtol=1e-13)
+    np.testing.assert_allclose(agg, ref.theta_agg, rtol=1e-9, atol=1e-12 * np.abs(ref.theta_agg).max())
+
+
+def test_row_block_partition():
+    for n in range(1, 60):
+        for world in range(1, min(n, 9) + 1):
+            rows = [i for r in range(world) for i in D.row_block(n, r, world)]
+            assert rows == list(range(n))
+            sizes = [len(D.row_block(n, r, world)) for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        D.row_block(3, 0, 4)
+    assert D.broadcast_bytes(b"abc", D.World()) == b"abc"
