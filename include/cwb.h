@@ -140,6 +140,14 @@ int cwb_get_pool(cwb_ctx* ctx, double* z, uint16_t* idx, double* Zb, double* G, 
  * general per-iteration kernels. */
 int cwb_set_path(cwb_ctx* ctx, int32_t path);
 
+/* H1 implementation of cwb_find_best for B <= 4 columns (tests and benchmarks
+ * compare them): 0 = streaming gather plan (built on the first call, which
+ * synchronises the stream; per chunk of 8192 rows the bins of every learner
+ * inverted into a gather schedule, binMatVec P:L898-902), falling back to 1
+ * when n* > 12288; 1 = per-warp histograms with __match_any_sync grouping.
+ * Errors: CWB_EINVAL (mode not 0 or 1). */
+int cwb_set_narrow(cwb_ctx* ctx, int32_t mode);
+
 /* findBestBaselearner (Alg. 1 supp. lines 5-9) for B
  * residual vectors R[B][n]:
  *   k_out[B]        argmin_k SSE_k (lowest k on ties)

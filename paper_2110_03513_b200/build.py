@@ -31,11 +31,31 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles every csrc/*.cu to an object in parallel (objects of unchanged sources are
+    reused), then links libcwb.so."""
     if force or not up_to_date():
-        cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *sources()]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-            print(" ".join(cmd), file=sys.stderr)
+        from concurrent.futures import ThreadPoolExecutor
+        odir = os.path.join(HERE, "build")
+        os.makedirs(odir, exist_ok=True)
+        hdrs = [p for p in deps() if not p.endswith(".cu")]
+        newest_hdr = max(os.path.getmtime(p) for p in hdrs)
+        comp = [f for f in FLAGS if f not in ("-shared", "-ldl")]
+
+        def obj(src):
+            o = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
+            if not force and os.path.exists(o) and os.path.getmtime(o) >= max(os.path.getmtime(src), newest_hdr):
+                return o
+            cmd = [NVCC, *comp, "-c", "-o", o + ".tmp", src]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.run(cmd, check=True)
+            os.replace(o + ".tmp", o)
+            return o
+
+        with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+            objs = list(ex.map(obj, sources()))
+        cmd = [NVCC, "-shared", "-ldl", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp", *objs]
         subprocess.run(cmd, check=True)
         os.replace(LIB + ".tmp", LIB)
     return LIB

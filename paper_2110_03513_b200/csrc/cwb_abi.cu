@@ -163,6 +163,7 @@ void cwb_free(cwb_ctx* c) {
                     c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->plan, c->permt,
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
+    cwb_stream_release(c, s);
     if (c->ev_plan) cudaEventDestroy(c->ev_plan);
     if (c->ev_csr) cudaEventDestroy(c->ev_csr);
     if (c->s2) cudaStreamDestroy(c->s2);
@@ -284,6 +285,12 @@ int cwb_get_pool(cwb_ctx* c, double* z, uint16_t* idx, double* Zb, double* G, do
             CWB_CUDA_TRY(c, cudaDeviceSynchronize());
         }
     }
+    return CWB_OK;
+}
+
+int cwb_set_narrow(cwb_ctx* c, int32_t mode) {
+    if (!c || mode < 0 || mode > 1) return cwb_set_error(c, CWB_EINVAL, "cwb_set_narrow: invalid argument");
+    c->narrow_mode = mode;
     return CWB_OK;
 }
 

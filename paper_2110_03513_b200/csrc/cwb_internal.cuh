@@ -41,6 +41,19 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     double* pack = nullptr;    // row sharding: [K][d][Bp] partial s, then [Bp] partial r^T r
 };
 
+struct cwb_stream_plan {  // streaming binMatVec gather plan (cwb_stream.cu), built on first use
+    bool ready = false;
+    int32_t Ks = 0, nch = 0, nlg = 0, nitems = 0;
+    long long ngroups = 0, nblocks = 0;
+    void* ent = nullptr;        // u16 chunk-local row ids, [block][lane][4]
+    uint2* gtab = nullptr;      // per 32-task group: {first block, blocks}
+    uint16_t* dest = nullptr;   // per group and lane: kl * n* + l, 0xffff none
+    int2* isize = nullptr;      // per item (learner group, chunk): {groups, blocks}
+    int2* ibase = nullptr;      // per item: first group, first block
+    double* part = nullptr;     // per-CTA bin sums
+    size_t part_bytes = 0;
+};
+
 struct cwb_ctx {
     // dimensions / configuration
     int64_t n = 0;
@@ -49,6 +62,7 @@ struct cwb_ctx {
     int32_t idx_bytes = 1;   // 1: uint8 index vector, 2: uint16
     int32_t perm_bytes = 2;  // 2: uint16 row ids, 4: uint32
     int32_t path = 0;        // 0 auto, 1 fused, 2 general
+    int32_t narrow_mode = 0; // narrow findBest H1: 0 stream plan (fallback histograms), 1 histograms
     cudaStream_t stream = 0;
     int status = CWB_OK;
     std::string err;
@@ -102,6 +116,7 @@ struct cwb_ctx {
     cwb_comm* comm = nullptr;  // borrowed
 
     cwb_train_ws ws;
+    cwb_stream_plan sp;
 };
 
 // ----------------------------------------------------------------- helpers
@@ -151,6 +166,9 @@ int cwb_train_rows(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t 
 int cwb_find_best_rows(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out, double* theta_out,
                        double* sse_out, cudaStream_t s);
 int cwb_rows_allreduce(cwb_ctx* ctx, double* buf, int64_t count, cudaStream_t s);
+int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                         double* sse_out, cudaStream_t s);
+void cwb_stream_release(cwb_ctx* c, cudaStream_t s);
 int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
                      const double* theta_agg, int32_t B, double* out, cudaStream_t s);
 

@@ -129,14 +129,17 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
                        const double* __restrict__ G, double* __restrict__ theta,
                        double* __restrict__ delta, const double* __restrict__ Ainv2 = nullptr,
                        const double* __restrict__ G2 = nullptr, const int32_t* __restrict__ phase = nullptr,
-                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0) {
+                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0, int Bu = 0) {
     __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
     const int k = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int b = blockIdx.y * 32 + lane;
     const int32_t* j0 = zj0 + (size_t)k * ns;
     const double* zs = Zs + (size_t)k * ns * CWB_SPW;
-    const double* u = U + (size_t)k * ns * Bp + b;
+    // U columns: stride Bu (narrow findBest: only the B real columns are stored), else Bp
+    const int bu = Bu ? Bu : Bp;
+    const bool uval = b < bu;
+    const double* u = U + (size_t)k * ns * bu + (uval ? b : 0);
     for (int j = w; j < d; j += nw) {
         double s;
         if (smode == 2) {
@@ -144,7 +147,8 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
         } else {
             const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
             s = 0.0;
-            for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * Bp];
+            if (uval)
+                for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * bu];
             if (smode == 1) Sg[((size_t)k * d + j) * Bp + b] = s;
         }
         S[j][lane] = s;
@@ -909,6 +913,7 @@ static int find_best_narrow(cwb_ctx* c, const double* R, int32_t B, int32_t* k_o
     const size_t smem = hist + nbuf * per_row * nc;
     rc = column_stats(c, R, B, false, nullptr, w.rr, nullptr, s);
     if (rc) return rc;
+    // streaming gather plan (cwb_stream.cu) when it applies, else the MATCH.ANY histograms
 #define NARROW_CASE(IT)                                                                                          \
     switch (B) {                                                                                                 \
         case 1: launch_narrow<IT, 1>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
@@ -916,21 +921,28 @@ static int find_best_narrow(cwb_ctx* c, const double* R, int32_t B, int32_t* k_o
         case 3: launch_narrow<IT, 3>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
         default: launch_narrow<IT, 4>(tma, R, c->n, K, ns, c->idx, rpc, nc, nranges, groups, smem, w.narrow, s); break; \
     }
-    if (c->idx_bytes == 1) NARROW_CASE(uint8_t) else NARROW_CASE(uint16_t)
+    {
+        if (c->idx_bytes == 1) NARROW_CASE(uint8_t) else NARROW_CASE(uint16_t)
 #undef NARROW_CASE
-    const int64_t tot = (int64_t)K * ns * w.Bp;
-    k_narrow_combine<<<(unsigned)std::min<int64_t>(4 * 1184, (tot + 255) / 256), 256, 0, s>>>(w.narrow, nranges, K, ns,
-                                                                                           B, w.Bp, w.U);
+        const int64_t tot = (int64_t)K * ns * w.Bp;
+        k_narrow_combine<<<(unsigned)std::min<int64_t>(4 * 1184, (tot + 255) / 256), 256, 0, s>>>(
+            w.narrow, nranges, K, ns, B, w.Bp, w.U);
+        c->launches += 2;
+    }
     k_h234<<<dim3(K, w.Bp / 32), 256, 0, s>>>(w.U, w.Bp, ns, c->d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
                                               w.delta);
     k_h5<<<(w.Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, K, c->d, B, w.Bp, 0.0, 0, w.kstar, nullptr,
                                             nullptr, nullptr, k_out, theta_out, sse_out);
-    c->launches += 5;
+    c->launches += 2;
     return cwb_check_launch(c, "narrow find_best kernels");
 }
 
 int cwb_find_best_general(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
                           double* sse_out, cudaStream_t s) {
+    if (B <= 4 && c->path != 2 && c->narrow_mode == 0) {
+        const int rc = cwb_find_best_stream(c, R, B, k_out, theta_out, sse_out, s);
+        if (rc != CWB_EUNSUPPORTED) return rc;
+    }
     if (B <= 4 && c->path != 2) {
         const int rc = find_best_narrow(c, R, B, k_out, theta_out, sse_out, s);
         if (rc != CWB_EUNSUPPORTED) return rc;

@@ -1,0 +1,623 @@
+// cwb_stream.cu -- streaming binMatVec (H1) for a few residual vectors
+// over large n: the index-streaming path of findBestBaselearner (SURVEY Sec. 8(d)
+// target: one residual column at R3/R4 sizes, bound by HBM on the index stream).
+//
+// binMatVec for learner k is u_k(l) = sum_{i : idx_k(i) = l} r_i.  On
+// B200 the scatter-add of the paper's loop would be an fp64 shared-memory atomic (a
+// CAS loop on sm_100a); instead the bins are inverted per chunk of rows once per pool
+// (the "hash map" of P:L861, stored as a gather plan) and every lane *gathers* the
+// rows of one bin into a register:
+//
+//   plan (built once, lazily, on the first narrow findBest):
+//     rows are cut into chunks of C = 8192 (a chunk of r is 64 KB of shared memory);
+//     learners into groups of Ks (the group's bin sums, Ks * n* doubles, stay in
+//     shared memory across chunks).  For every item (learner group, chunk) the
+//     non-empty bins of the group's learners are tasks; tasks are sorted by row count
+//     (descending) and dealt to lanes 32 at a time, so the 32 lanes of a warp-group
+//     sum bins of (nearly) equal length.  Entries are chunk-local row ids (u16) laid
+//     out [step/4][lane][4]: one coalesced 8-byte load per lane per 4 steps.  Lanes
+//     past their bin's end read padding rows C + (lane mod 16) (zeros, distinct banks).
+//   kernel k_h1_stream: CTA = (learner group, contiguous chunk range, column q).  Per
+//     chunk: the residual chunk is loaded into shared memory, every warp takes groups
+//     of the item round-robin, gathers r[row] from shared memory and adds, and the
+//     lane adds its bin total into the CTA's bin sums (each (learner, bin) is one task
+//     per item: no conflicting writes).  At the end the CTA writes its bin sums; a
+//     combine kernel adds the CTA partials of a learner group in CTA order.
+//
+// Deterministic: every sum has a fixed order (plan order within a bin and chunk,
+// chunks ascending within a CTA, CTAs ascending in the combine).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "cwb_internal.cuh"
+
+namespace {
+
+constexpr int kC = 8192;        // rows per chunk (chunk-local ids fit u16, pad ids C..C+15)
+constexpr int kPad = 16;        // zero padding rows after the chunk
+constexpr int kUBudget = 4096;  // doubles of bin sums per CTA (32 KB): Ks * n* <= kUBudget
+constexpr int kStreamT = 512;   // threads of the stream kernel
+
+// ---------------------------------------------------------------- plan kernels
+// bin counts of every (learner, chunk): cnt[(k * nch + c) * ns + l]
+template <typename IdxT>
+__global__ void k_sp_count(const IdxT* __restrict__ idx, int64_t n, int ns, int nch, uint32_t* __restrict__ cnt) {
+    extern __shared__ uint32_t h[];
+    const int c = blockIdx.x, k = blockIdx.y;
+    for (int l = threadIdx.x; l < ns; l += blockDim.x) h[l] = 0;
+    __syncthreads();
+    const int64_t r0 = (int64_t)c * kC, r1 = min(n, r0 + kC);
+    const IdxT* ik = idx + (size_t)k * n;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&h[ik[i]], 1u);
+    __syncthreads();
+    uint32_t* o = cnt + ((size_t)k * nch + c) * ns;
+    for (int l = threadIdx.x; l < ns; l += blockDim.x) o[l] = h[l];
+}
+
+// start of chunk c's rows inside bin l of the bin inversion (perm is ascending within a bin)
+__global__ void k_sp_start(const uint32_t* __restrict__ cnt, const int32_t* __restrict__ off, int K, int ns,
+                           int nch, uint32_t* __restrict__ cst) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)K * ns) return;
+    const int k = (int)(g / ns), l = (int)(g - (int64_t)k * ns);
+    uint32_t run = (uint32_t)off[(size_t)k * (ns + 1) + l];
+    for (int c = 0; c < nch; c++) {
+        const size_t e = ((size_t)k * nch + c) * ns + l;
+        cst[e] = run;
+        run += cnt[e];
+    }
+}
+
+// One block per item (learner group lg, chunk c): sort the group's non-empty bins by
+// count (descending, ties by task id) with a bitonic sort of packed keys in shared
+// memory; write the sorted task ids (kl * ns + l) and the item's group / block counts.
+__global__ void k_sp_sort(const uint32_t* __restrict__ cnt, int K, int ns, int nch, int Ks, int NTP,
+                          uint32_t* __restrict__ tasks, int2* __restrict__ isize) {
+    extern __shared__ unsigned long long key[];
+    const int item = blockIdx.x, lg = item / nch, c = item - lg * nch;
+    const int k0 = lg * Ks, ke = min(K, k0 + Ks), NT = (ke - k0) * ns;
+    for (int t = threadIdx.x; t < NTP; t += blockDim.x) {
+        unsigned long long v = ~0ull;
+        if (t < NT) {
+            const int kl = t / ns, l = t - kl * ns;
+            const uint32_t q = cnt[((size_t)(k0 + kl) * nch + c) * ns + l];
+            if (q) v = ((unsigned long long)(0xffffffffu - q) << 32) | (uint32_t)t;
+        }
+        key[t] = v;
+    }
+    __syncthreads();
+    for (int size = 2; size <= NTP; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < NTP / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = key[lo], b = key[hi];
+                if ((a > b) == up) { key[lo] = b; key[hi] = a; }
+            }
+            __syncthreads();
+        }
+    __shared__ int s_nt;
+    if (threadIdx.x == 0) s_nt = 0;
+    __syncthreads();
+    uint32_t* tk = tasks + (size_t)item * NTP;
+    for (int t = threadIdx.x; t < NTP; t += blockDim.x) {
+        const unsigned long long v = key[t];
+        tk[t] = v == ~0ull ? 0xffffffffu : (uint32_t)v;
+        if (v != ~0ull && (t + 1 == NTP || key[t + 1] == ~0ull)) s_nt = t + 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) isize[item] = make_int2((s_nt + 31) / 32, 0);  // blocks: k_sp_sched<false>
+}
+
+// exclusive scan of the (groups, blocks) counts of the items (one thread: items <= a few thousand)
+__global__ void k_sp_scan(const int2* __restrict__ isize, int nitems, int2* __restrict__ ibase,
+                          long long* __restrict__ tot) {
+    long long g = 0, b = 0;
+    for (int i = 0; i < nitems; i++) {
+        ibase[i] = make_int2((int)g, (int)b);
+        g += isize[i].x;
+        b += isize[i].y;
+    }
+    tot[0] = g;
+    tot[1] = b;
+}
+
+// Gather schedule of one item: one block per item, one warp per 32-task group.  The 16
+// lanes of a half-warp read 8-byte rows in one shared-memory wavefront when the rows
+// have distinct colours (row mod 16 = bank pair).  Every step each half-warp assigns
+// colours greedily: the lane with the most rows left picks first (ties: lowest lane),
+// taking the free colour it holds most rows of; lanes without a pick read padding
+// rows C + (a free colour), so every step is conflict-free.  Steps run until the
+// warp's 32 bins are exhausted, rounded up to a multiple of 4 with padding steps.
+// EMIT = false: count the steps (isize[item].y += blocks); EMIT = true: write entries,
+// group table and destinations at the scanned offsets.
+template <typename PermT, bool EMIT>
+__global__ void __launch_bounds__(512) k_sp_sched(
+    const uint32_t* __restrict__ tasks, const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ cst,
+    const PermT* __restrict__ perm, int64_t n, int ns, int nch, int Ks, int NTP, int2* __restrict__ isize,
+    const int2* __restrict__ ibase, uint32_t* __restrict__ gsteps, uint16_t* __restrict__ ent,
+    uint2* __restrict__ gtab, uint16_t* __restrict__ dest) {
+    const int item = blockIdx.x, lg = item / nch, c = item - lg * nch;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int hl = lane & 15, hb = lane & 16;
+    const unsigned hmask = 0xffffu << hb;
+    const int ng = isize[item].x;
+    const uint32_t* tk = tasks + (size_t)item * NTP;
+    uint32_t* gs = gsteps + (size_t)item * (NTP / 32);
+    const uint32_t base = (uint32_t)c * kC;
+    for (int g = w; g < ng; g += nw) {
+        const uint32_t t = tk[32 * g + lane];
+        int rem = 0;
+        uint32_t st = 0;
+        int k = lg * Ks;
+        if (t != 0xffffffffu) {
+            const uint32_t kl = t / ns, l = t - kl * ns;
+            k += (int)kl;
+            const size_t e = ((size_t)k * nch + c) * ns + l;
+            rem = (int)cnt[e];
+            st = cst[e];
+        }
+        const PermT* rows = perm + (size_t)k * n + st;
+        int cc[16], pos[16];
+#pragma unroll
+        for (int x = 0; x < 16; x++) { cc[x] = 0; pos[x] = 0; }
+        for (int s = 0; s < rem; s++) cc[((uint32_t)rows[s] - base) & 15]++;
+        uint16_t* eg = nullptr;
+        if (EMIT) {
+            uint32_t part = 0;
+            for (int h = lane; h < g; h += 32) part += gs[h] / 4;
+            for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            const uint32_t bb = (uint32_t)ibase[item].y + part;
+            const int gg = ibase[item].x + g;
+            if (lane == 0) gtab[gg] = make_uint2(bb, gs[g] / 4);
+            dest[(size_t)gg * 32 + lane] = t != 0xffffffffu ? (uint16_t)t : (uint16_t)0xffff;
+            eg = ent + (size_t)bb * 128 + lane * 4;
+        }
+        uint32_t steps = 0;
+        while (__any_sync(0xffffffffu, rem > 0) || (steps & 3)) {
+            unsigned fr = 0xffffu;
+            int pick = -1;
+            bool assigned = false;
+            for (int r = 0; r < 16; r++) {
+                int key = assigned ? -1 : ((rem << 4) | (15 - hl));
+#pragma unroll
+                for (int o = 8; o; o >>= 1) key = max(key, __shfl_xor_sync(hmask, key, o));
+                if (key < 16) break;  // the best unassigned lane has no rows left: the rest pad
+                const int win = 15 - (key & 15);
+                int x = -1;
+                if (hl == win) {
+                    int best = 0;
+#pragma unroll
+                    for (int y = 0; y < 16; y++)
+                        if (((fr >> y) & 1u) && cc[y] > best) { best = cc[y]; x = y; }
+                    assigned = true;
+                    pick = x;
+                }
+                x = __shfl_sync(hmask, x, hb | win);
+                if (x >= 0) fr &= ~(1u << x);
+            }
+            const unsigned np = (~__ballot_sync(0xffffffffu, pick >= 0) >> hb) & 0xffffu;  // lanes padding
+            uint16_t v;
+            if (pick >= 0) {
+                int p = pos[pick];
+                while ((((uint32_t)rows[p] - base) & 15) != (uint32_t)pick) p++;
+                v = (uint16_t)((uint32_t)rows[p] - base);
+                pos[pick] = p + 1;
+                cc[pick]--;
+                rem--;
+            } else {
+                int rank = __popc(np & ((1u << hl) - 1u));
+                unsigned f = fr;
+                while (rank--) f &= f - 1u;
+                v = (uint16_t)(kC + (__ffs(f) - 1));
+            }
+            if (EMIT) eg[(size_t)(steps >> 2) * 128 + (steps & 3)] = v;
+            steps++;
+        }
+        if (!EMIT && lane == 0) {
+            gs[g] = steps;
+            atomicAdd(&isize[item].y, (int)(steps / 4));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- stream kernel
+// grid (N, B): CTA j takes the items [j I / N, (j+1) I / N) of the (learner group major,
+// chunk minor) item order, column q = blockIdx.y.  When the learner group changes, the
+// bin sums go to the CTA's next partial slot P[q][j][slot] (slot = lg - first lg of j).
+constexpr int kBatch = 8;  // entry blocks of a group loaded at once (one memory latency per 8 blocks)
+
+__device__ __forceinline__ double gather4(const double* __restrict__ rs, uint2 v) {
+    // fixed order: entries 0, 1, 2, 3 of the block
+    double a = rs[v.x & 0xffff];
+    a += rs[v.x >> 16];
+    a += rs[v.y & 0xffff];
+    a += rs[v.y >> 16];
+    return a;
+}
+
+__global__ void __launch_bounds__(kStreamT, 2)
+    k_h1_stream(const double* __restrict__ R, int64_t n, int nch, int Ks, int ns, int nitems, int nslot,
+                const uint2* __restrict__ ent, const uint2* __restrict__ gtab, const uint16_t* __restrict__ dest,
+                const int2* __restrict__ isize, const int2* __restrict__ ibase, double* __restrict__ P,
+                double* __restrict__ rrp, int* status) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[kStreamT / 32];
+    double* rs = sm;                // kC + kPad residuals of the chunk
+    double* U = sm + kC + kPad;     // Ks * ns bin sums
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const int N = gridDim.x, j = blockIdx.x, q = blockIdx.y;
+    const int i0 = (int)((int64_t)nitems * j / N), i1 = (int)((int64_t)nitems * (j + 1) / N);
+    const int NU = Ks * ns;
+    double* Pj = P + ((size_t)q * N + j) * nslot * NU;
+    for (int a = tid; a < NU; a += blockDim.x) U[a] = 0.0;
+    if (tid < kPad) rs[kC + tid] = 0.0;
+    const double* col = R + (size_t)q * n;
+    int cur_lg = i0 / nch, slot = 0, cur_c = -1;
+    for (int item = i0; item < i1; item++) {
+        const int lg = item / nch, c = item - lg * nch;
+        if (lg != cur_lg) {  // flush the bin sums of the previous learner group
+            __syncthreads();
+            for (int a = tid; a < NU; a += blockDim.x) {
+                Pj[(size_t)slot * NU + a] = U[a];
+                U[a] = 0.0;
+            }
+            slot++;
+            cur_lg = lg;
+        }
+        if (c != cur_c) {
+            const int64_t r0 = (int64_t)c * kC;
+            const int len = (int)min((int64_t)kC, n - r0);
+            __syncthreads();  // previous chunk consumed
+            double sq = 0.0;  // r^T r of the chunk (I8 / the SSE identity), by the items of learner group 0
+            if ((((uintptr_t)(col + r0)) & 15) == 0) {
+                const int h = len >> 1;
+                const double2* src = (const double2*)(col + r0);
+                for (int i = tid; i < h; i += blockDim.x) {
+                    const double2 v = __ldg(src + i);
+                    ((double2*)rs)[i] = v;
+                    sq += v.x * v.x;
+                    sq += v.y * v.y;
+                }
+                if ((len & 1) && tid == 0) {
+                    const double v = __ldg(col + r0 + len - 1);
+                    rs[len - 1] = v;
+                    sq += v * v;
+                }
+            } else {
+                for (int i = tid; i < len; i += blockDim.x) {
+                    const double v = __ldg(col + r0 + i);
+                    rs[i] = v;
+                    sq += v * v;
+                }
+            }
+            if (lg == 0) {  // block-uniform: one writer per chunk, fixed order
+                if (!isfinite(sq)) cwb_dev_fail(status, CWB_ENONFINITE);
+                sq = warp_sum(sq);
+                if (lane == 0) red[w] = sq;
+                __syncthreads();
+                if (tid == 0) {
+                    double t = 0.0;
+                    for (int u = 0; u < nw; u++) t += red[u];
+                    rrp[(size_t)q * nch + c] = t;
+                }
+            }
+            cur_c = c;
+        }
+        __syncthreads();
+        const int2 isz = isize[item], ib = ibase[item];
+        const int ng = isz.x, gb = ib.x;
+        int g = w;
+        uint2 gt = make_uint2(0, 0);
+        uint16_t dst = 0xffff;
+        if (g < ng) {
+            gt = __ldg(gtab + gb + g);
+            dst = __ldg(dest + (size_t)(gb + g) * 32 + lane);
+        }
+        while (g < ng) {
+            const uint2* e = ent + (size_t)gt.x * 32 + lane;
+            uint2 v[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; u++)
+                if (u < (int)gt.y) v[u] = __ldg(e + (size_t)u * 32);
+            // next group's header while the blocks are in flight
+            const int gn = g + nw;
+            uint2 gtn = make_uint2(0, 0);
+            uint16_t dstn = 0xffff;
+            if (gn < ng) {
+                gtn = __ldg(gtab + gb + gn);
+                dstn = __ldg(dest + (size_t)(gb + gn) * 32 + lane);
+            }
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int u = 0; u < kBatch; u += 2) {
+                if (u < (int)gt.y) a0 += gather4(rs, v[u]);
+                if (u + 1 < (int)gt.y) a1 += gather4(rs, v[u + 1]);
+            }
+            for (uint32_t s0 = kBatch; s0 < gt.y; s0 += kBatch) {  // long bins (rare): further batches
+#pragma unroll
+                for (int u = 0; u < kBatch; u++)
+                    if (s0 + u < gt.y) v[u] = __ldg(e + (size_t)(s0 + u) * 32);
+#pragma unroll
+                for (int u = 0; u < kBatch; u += 2) {
+                    if (s0 + u < gt.y) a0 += gather4(rs, v[u]);
+                    if (s0 + u + 1 < gt.y) a1 += gather4(rs, v[u + 1]);
+                }
+            }
+            if (dst != 0xffff) U[dst] += a0 + a1;
+            g = gn;
+            gt = gtn;
+            dst = dstn;
+        }
+    }
+    __syncthreads();
+    if (i0 < i1)
+        for (int a = tid; a < NU; a += blockDim.x) Pj[(size_t)slot * NU + a] = U[a];
+}
+
+// findBestBaselearner tail for B <= 4 columns, one block per learner k, fused with the
+// combine of the stream kernel's partials:
+//   u_k(l) = sum over CTAs of the partial bin sums            (binMatVec)
+//   s = Zb^T u over the design-point window of basis j
+//   theta = (G + lambda D)^-1 s with the cached inverse
+//   delta = 2 theta^T s - theta^T G theta, SSE = r^T r - delta
+// and the last block to finish (atomic ticket) takes argmin SSE over k, lowest k on ties
+// (P:L292), for every column.
+__global__ void __launch_bounds__(256) k_fit_narrow(
+    const double* __restrict__ P, int K, int ns, int Ks, int nch, int nitems, int N, int nslot, int B, int d,
+    const int32_t* __restrict__ zj0, const double* __restrict__ Zs, const int32_t* __restrict__ lwin,
+    const double* __restrict__ Ainv, const double* __restrict__ G, const double* __restrict__ rrp,
+    double* __restrict__ theta, double* __restrict__ delta, unsigned* __restrict__ ticket, int32_t* __restrict__ k_out,
+    double* __restrict__ theta_out, double* __restrict__ sse_out) {
+    extern __shared__ double u[];  // [ns][B]
+    __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4];
+    __shared__ bool last;
+    const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const int lg = k / Ks, NU = Ks * ns, a0 = (k - lg * Ks) * ns;
+    // the CTAs whose item range meets [lg nch, (lg+1) nch), and their slot for lg
+    __shared__ int s_j[2 * 148 + 1], s_slot[2 * 148 + 1], s_nj;
+    if (tid == 0) {
+        const int64_t it0 = (int64_t)lg * nch, it1 = it0 + nch;
+        int jlo = (int)(it0 * N / nitems), m = 0;
+        while (jlo > 0 && (int64_t)nitems * jlo / N > it0) jlo--;
+        for (int jj = jlo; jj < N && m < 2 * 148 + 1; jj++) {
+            const int64_t b0 = (int64_t)nitems * jj / N, b1 = (int64_t)nitems * (jj + 1) / N;
+            if (b0 >= it1) break;
+            if (b1 <= it0 || b0 == b1) continue;
+            s_j[m] = jj;
+            s_slot[m] = lg - (int)(b0 / nch);
+            m++;
+        }
+        s_nj = m;
+    }
+    __syncthreads();
+    const int nj = s_nj;
+    for (int l = tid; l < ns; l += blockDim.x)
+        for (int q = 0; q < B; q++) {
+            double v = 0.0;
+            int m = 0;
+            for (; m + 4 <= nj; m += 4) {  // loads of 4 partials in flight, added in CTA order
+                const double p0 = P[(((size_t)q * N + s_j[m]) * nslot + s_slot[m]) * NU + a0 + l];
+                const double p1 = P[(((size_t)q * N + s_j[m + 1]) * nslot + s_slot[m + 1]) * NU + a0 + l];
+                const double p2 = P[(((size_t)q * N + s_j[m + 2]) * nslot + s_slot[m + 2]) * NU + a0 + l];
+                const double p3 = P[(((size_t)q * N + s_j[m + 3]) * nslot + s_slot[m + 3]) * NU + a0 + l];
+                v += p0; v += p1; v += p2; v += p3;
+            }
+            for (; m < nj; m++) v += P[(((size_t)q * N + s_j[m]) * nslot + s_slot[m]) * NU + a0 + l];
+            u[l * B + q] = v;
+        }
+    __syncthreads();
+    const int32_t* j0 = zj0 + (size_t)k * ns;
+    const double* zs = Zs + (size_t)k * ns * CWB_SPW;
+    for (int j = w; j < d; j += nw) {
+        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int l = lb + lane; l < le; l += 32) {
+            const double z = zs[l * CWB_SPW + (j - j0[l])];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (q < B) acc[q] += z * u[l * B + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const double t = warp_sum(acc[q]);
+            if (lane == 0 && q < B) S[j][q] = t;
+        }
+    }
+    __syncthreads();
+    const double* Ai = Ainv + (size_t)k * d * d;
+    if (tid < d * B) {
+        const int j = tid / B, q = tid - j * B;
+        double t = 0.0;
+        for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][q];
+        Th[j][q] = t;
+        theta[((size_t)k * d + j) * 4 + q] = t;
+    }
+    __syncthreads();
+    if (tid < B) {
+        const int q = tid;
+        const double* Gk = G + (size_t)k * d * d;
+        double v = 0.0;
+        for (int j = 0; j < d; j++) {
+            double gt = 0.0;
+            for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++) gt += Gk[j * d + jp] * Th[jp][q];
+            v += Th[j][q] * (2.0 * S[j][q] - gt);
+        }
+        delta[(size_t)k * 4 + q] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(ticket, 1u) == (unsigned)(K - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (w < B) {  // warp q: argmax delta over k (lowest k on ties), r^T r from the chunk partials
+        const int q = w;
+        int ks = K;
+        double best = 0.0;
+        for (int kk = lane; kk < K; kk += 32) {
+            const double v = __ldcg(delta + (size_t)kk * 4 + q);
+            if (ks == K || v > best) { best = v; ks = kk; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, ks, o);
+            if (ok < K && (ks == K || ob > best || (ob == best && ok < ks))) { best = ob; ks = ok; }
+        }
+        double rr = 0.0;
+        for (int c = lane; c < nch; c += 32) rr += __ldcg(rrp + (size_t)q * nch + c);
+        rr = warp_sum(rr);
+        if (lane == 0) {
+            if (k_out) k_out[q] = ks;
+            if (sse_out) sse_out[q] = rr - best;
+        }
+        if (theta_out && lane < d) theta_out[(size_t)q * d + lane] = __ldcg(theta + ((size_t)ks * d + lane) * 4 + q);
+    }
+    if (tid == 0) *ticket = 0u;  // ready for the next call
+}
+
+}  // namespace
+
+// ===================================================================== host
+
+void cwb_stream_release(cwb_ctx* c, cudaStream_t s) {
+    cwb_stream_plan& p = c->sp;
+    cwb_release(p.ent, s); cwb_release(p.gtab, s); cwb_release(p.dest, s); cwb_release(p.isize, s);
+    cwb_release(p.ibase, s); cwb_release(p.part, s);
+    p = cwb_stream_plan();
+}
+
+// Builds the gather plan (once per pool).  Synchronises the stream once (sizes).
+static int stream_plan(cwb_ctx* c, cudaStream_t s) {
+    cwb_stream_plan& p = c->sp;
+    if (p.ready) return CWB_OK;
+    const int K = c->K, ns = c->n_star;
+    const int64_t n = c->n;
+    if (ns > 12288) return CWB_EUNSUPPORTED;
+    // learner group size: bin sums within the shared-memory budget, and at least 2 x 148 items
+    const int nch0 = (int)((n + kC - 1) / kC);
+    const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / (2 * 148))));
+    if ((int64_t)Ks * ns > 0xfffe) return CWB_EUNSUPPORTED;
+    const int nch = (int)((n + kC - 1) / kC), nlg = (K + Ks - 1) / Ks, nitems = nlg * nch;
+    int NTP = 32;
+    while (NTP < Ks * ns) NTP <<= 1;
+    if ((size_t)NTP * 8 > 200 * 1024) return CWB_EUNSUPPORTED;
+    uint32_t *cnt = nullptr, *cst = nullptr, *tasks = nullptr, *gsteps = nullptr;
+    int2 *isize = nullptr, *ibase = nullptr;
+    long long* tot = nullptr;
+    bool ok = true;
+    const size_t nc = (size_t)K * nch * ns;
+    ok &= cwb_alloc((void**)&cnt, sizeof(uint32_t) * nc, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&cst, sizeof(uint32_t) * nc, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&tasks, sizeof(uint32_t) * (size_t)nitems * NTP, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&gsteps, sizeof(uint32_t) * (size_t)nitems * (NTP / 32 + 1), s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&isize, sizeof(int2) * nitems, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&ibase, sizeof(int2) * nitems, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&tot, sizeof(long long) * 2, s) == cudaSuccess;
+    auto cleanup = [&]() {
+        cwb_release(cnt, s); cwb_release(cst, s); cwb_release(tasks, s); cwb_release(tot, s); cwb_release(gsteps, s);
+    };
+    if (!ok) {
+        cleanup(); cwb_release(isize, s); cwb_release(ibase, s);
+        return cwb_set_error(c, CWB_ENOMEM, "stream plan allocation failed");
+    }
+    const size_t hsm = sizeof(uint32_t) * ns;
+    if (c->idx_bytes == 1)
+        k_sp_count<uint8_t><<<dim3(nch, K), 256, hsm, s>>>((const uint8_t*)c->idx, n, ns, nch, cnt);
+    else
+        k_sp_count<uint16_t><<<dim3(nch, K), 256, hsm, s>>>((const uint16_t*)c->idx, n, ns, nch, cnt);
+    k_sp_start<<<(unsigned)(((int64_t)K * ns + 255) / 256), 256, 0, s>>>(cnt, c->off, K, ns, nch, cst);
+    const size_t ssm = sizeof(unsigned long long) * NTP;
+    cudaFuncSetAttribute(k_sp_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    k_sp_sort<<<nitems, 512, ssm, s>>>(cnt, K, ns, nch, Ks, NTP, tasks, isize);
+    if (c->perm_bytes == 2)
+        k_sp_sched<uint16_t, false><<<nitems, 512, 0, s>>>(tasks, cnt, cst, (const uint16_t*)c->perm, n, ns, nch, Ks,
+                                                           NTP, isize, ibase, gsteps, nullptr, nullptr, nullptr);
+    else
+        k_sp_sched<uint32_t, false><<<nitems, 512, 0, s>>>(tasks, cnt, cst, (const uint32_t*)c->perm, n, ns, nch, Ks,
+                                                           NTP, isize, ibase, gsteps, nullptr, nullptr, nullptr);
+    k_sp_scan<<<1, 1, 0, s>>>(isize, nitems, ibase, tot);
+    c->launches += 5;
+    long long h_tot[2] = {0, 0};
+    cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cleanup(); cwb_release(isize, s); cwb_release(ibase, s);
+        return cwb_set_error(c, CWB_ECUDA, std::string("stream plan: ") + cudaGetErrorString(e));
+    }
+    const long long ngt = h_tot[0], nbt = h_tot[1];
+    if (nbt >= (1ll << 31) / 32 || ngt >= (1ll << 31) / 32) {
+        cleanup(); cwb_release(isize, s); cwb_release(ibase, s);
+        return CWB_EUNSUPPORTED;
+    }
+    ok = cwb_alloc((void**)&p.ent, (size_t)std::max(1ll, nbt) * 256, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&p.gtab, sizeof(uint2) * (size_t)std::max(1ll, ngt), s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&p.dest, sizeof(uint16_t) * 32 * (size_t)std::max(1ll, ngt), s) == cudaSuccess;
+    if (!ok) {
+        cleanup(); cwb_release(isize, s); cwb_release(ibase, s);
+        cwb_stream_release(c, s);
+        return cwb_set_error(c, CWB_ENOMEM, "stream plan allocation failed");
+    }
+    if (c->perm_bytes == 2)
+        k_sp_sched<uint16_t, true><<<nitems, 512, 0, s>>>(tasks, cnt, cst, (const uint16_t*)c->perm, n, ns, nch, Ks,
+                                                          NTP, isize, ibase, gsteps, (uint16_t*)p.ent, p.gtab, p.dest);
+    else
+        k_sp_sched<uint32_t, true><<<nitems, 512, 0, s>>>(tasks, cnt, cst, (const uint32_t*)c->perm, n, ns, nch, Ks,
+                                                          NTP, isize, ibase, gsteps, (uint16_t*)p.ent, p.gtab, p.dest);
+    c->launches += 1;
+    cleanup();
+    p.isize = isize;
+    p.ibase = ibase;
+    p.Ks = Ks;
+    p.nch = nch;
+    p.nlg = nlg;
+    p.nitems = nitems;
+    p.ngroups = ngt;
+    p.nblocks = nbt;
+    p.ready = true;
+    return cwb_check_launch(c, "stream plan kernels");
+}
+
+// findBestBaselearner for B <= 4 residual columns R[B][n] (k_out[B], theta_out[B][d], sse_out[B]):
+// k_h1_stream + k_fit_narrow.  CWB_EUNSUPPORTED when the plan does not apply (caller falls back).
+int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
+                         double* sse_out, cudaStream_t s) {
+    if (c->rows || B < 1 || B > 4 || (size_t)c->n_star * B * sizeof(double) > 96 * 1024) return CWB_EUNSUPPORTED;
+    int rc = stream_plan(c, s);
+    if (rc) return rc;
+    cwb_stream_plan& p = c->sp;
+    const int K = c->K, ns = c->n_star, d = c->d;
+    const int N = std::max(1, std::min(p.nitems, 2 * 148));
+    // learner groups met by one CTA's item range
+    const int per = (p.nitems + N - 1) / N;
+    const int nslot = std::min(p.nlg, (per + p.nch - 1) / p.nch + 1);
+    const size_t part = (size_t)B * N * nslot * p.Ks * ns, extra = (size_t)4 * p.nch + (size_t)K * (d + 1) * 4 + 1;
+    const size_t need = sizeof(double) * (part + extra);
+    if (p.part_bytes < need) {
+        cwb_release(p.part, s);
+        p.part = nullptr;
+        p.part_bytes = 0;
+        if (cwb_alloc((void**)&p.part, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "stream find_best workspace allocation failed");
+        p.part_bytes = need;
+        cudaMemsetAsync(p.part + part + extra - 1, 0, sizeof(double), s);  // ticket
+    }
+    double* rrp = p.part + part;
+    double* th = rrp + 4 * p.nch;
+    double* de = th + (size_t)K * d * 4;
+    unsigned* ticket = (unsigned*)(p.part + part + extra - 1);
+    const size_t smem = sizeof(double) * ((size_t)kC + kPad + (size_t)p.Ks * ns);
+    cudaFuncSetAttribute(k_h1_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_h1_stream<<<dim3(N, B), kStreamT, smem, s>>>(R, c->n, p.nch, p.Ks, ns, p.nitems, nslot, (const uint2*)p.ent,
+                                                    p.gtab, p.dest, p.isize, p.ibase, p.part, rrp, c->d_status);
+    const size_t fsm = sizeof(double) * (size_t)ns * B;
+    cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    k_fit_narrow<<<K, 256, fsm, s>>>(p.part, K, ns, p.Ks, p.nch, p.nitems, N, nslot, B, d, c->zj0, c->Zs, c->lwin,
+                                     c->Ainv, c->G, rrp, th, de, ticket, k_out, theta_out, sse_out);
+    c->launches += 2;
+    return cwb_check_launch(c, "stream find_best kernels");
+}

@@ -21,7 +21,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 # the exported symbols declared in include/cwb.h
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
-           "cwb_set_path", "cwb_find_best", "cwb_train", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
+           "cwb_set_path", "cwb_set_narrow", "cwb_find_best", "cwb_train", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
            "cwb_launch_count", "cwb_set_phase_timing", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
            "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_get_rows"]
 
@@ -82,6 +82,7 @@ def load() -> C.CDLL:
     L.cwb_get_lambda.argtypes = [_vp, _vp]
     L.cwb_get_pool.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_set_path.argtypes = [_vp, _i32]
+    L.cwb_set_narrow.argtypes = [_vp, _i32]
     L.cwb_find_best.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp]
     L.cwb_train.argtypes = [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_train_acwb.argtypes = [_vp, _vp, _i32, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
@@ -226,6 +227,10 @@ def cwb_get_pool(ctx, device="cuda"):
 
 def cwb_set_path(ctx, path: int) -> None:
     _chk(load().cwb_set_path(ctx, path), ctx)
+
+
+def cwb_set_narrow(ctx, mode: int) -> None:
+    _chk(load().cwb_set_narrow(ctx, mode), ctx)
 
 
 def cwb_find_best(ctx, R):
@@ -434,6 +439,9 @@ class Pool:
 
     def set_path(self, p):
         cwb_set_path(self.ctx, p)
+
+    def set_narrow(self, mode):
+        cwb_set_narrow(self.ctx, mode)
 
     def lam(self):
         return cwb_get_lambda(self.ctx)

@@ -1,5 +1,6 @@
 """Time cwb_find_best (one findBestBaselearner) on B residual vectors for a config.
-usage: python tools/findbest_timing.py R3 [B] [reps]"""
+The calls are captured in a CUDA graph (no host launch overhead in the measurement).
+usage: python tools/findbest_timing.py R3 [B] [reps] [narrow_mode]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,23 +10,33 @@ from paper_2110_03513_b200 import cwb
 name = sys.argv[1] if len(sys.argv) > 1 else "R3"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+mode = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 c = S.CONFIGS[name]
 ds = S.make(c, reps=range(B))
 X = torch.as_tensor(ds.X, device="cuda")
 R = torch.as_tensor(ds.Y - ds.Y.mean(1, keepdims=True), device="cuda")
 pool = cwb.Pool(X, cwb.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots))
-for _ in range(3):
-    k, th, sse = pool.find_best(R)
+pool.set_narrow(mode)
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    for _ in range(3):
+        k, th, sse = pool.find_best(R)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            k, th, sse = pool.find_best(R)
+torch.cuda.synchronize()
+g.replay()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(reps):
-    k, th, sse = pool.find_best(R)
+g.replay()
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / reps
 K, n = c.K, c.n
 idx_bytes = 1 if pool.n_star <= 256 else 2
 alg = K * n * idx_bytes + n * B * 8  # index vector + residuals, read once
-print(f"{name} B={B} find_best {us:.1f} us; K*n*B={K*n*B:.3g} evals -> {K*n*B/us/1e3:.3g} G evals/s; "
+print(f"{name} B={B} mode={mode} find_best {us:.1f} us; K*n*B={K*n*B:.3g} evals -> {K*n*B/us/1e3:.3g} G evals/s; "
       f"alg bytes {alg/1e6:.1f} MB -> {alg/us/1e3:.0f} GB/s")
