@@ -36,10 +36,10 @@
 
 namespace {
 
-constexpr int kC = 8192;        // rows per chunk (chunk-local ids fit u16, pad ids C..C+15)
+constexpr int kC = 8176;        // rows per chunk: byte offsets of rows and pad rows (C..C+15) fit u16
 constexpr int kPad = 16;        // zero padding rows after the chunk
 constexpr int kUBudget = 4096;  // doubles of bin sums per CTA (32 KB): Ks * n* <= kUBudget
-constexpr int kStreamT = 512;   // threads of the stream kernel
+constexpr int kStreamT = 512;   // threads of the stream kernel (two CTAs per SM)
 
 // ---------------------------------------------------------------- plan kernels
 // bin counts of every (learner, chunk): cnt[(k * nch + c) * ns + l]
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(512) k_sp_sched(
             if (pick >= 0) {
                 int p = pos[pick];
                 while ((((uint32_t)rows[p] - base) & 15) != (uint32_t)pick) p++;
-                v = (uint16_t)((uint32_t)rows[p] - base);
+                v = (uint16_t)(((uint32_t)rows[p] - base) * 8u);  // byte offset in the staged chunk
                 pos[pick] = p + 1;
                 cc[pick]--;
                 rem--;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(512) k_sp_sched(
                 int rank = __popc(np & ((1u << hl) - 1u));
                 unsigned f = fr;
                 while (rank--) f &= f - 1u;
-                v = (uint16_t)(kC + (__ffs(f) - 1));
+                v = (uint16_t)((kC + (__ffs(f) - 1)) * 8);
             }
             if (EMIT) eg[(size_t)(steps >> 2) * 128 + (steps & 3)] = v;
             steps++;
@@ -225,19 +225,31 @@ __global__ void __launch_bounds__(512) k_sp_sched(
 }
 
 // ---------------------------------------------------------------- stream kernel
-// grid (N, B): CTA j takes the items [j I / N, (j+1) I / N) of the (learner group major,
-// chunk minor) item order, column q = blockIdx.y.  When the learner group changes, the
-// bin sums go to the CTA's next partial slot P[q][j][slot] (slot = lg - first lg of j).
-constexpr int kBatch = 8;  // entry blocks of a group loaded at once (one memory latency per 8 blocks)
+// grid (N, B), two CTAs per SM: CTA j takes the items [j I / N, (j+1) I / N) of the (learner
+// group major, chunk minor) item order, column q = blockIdx.y.  When the learner group
+// changes, the bin sums go to the CTA's next partial slot P[q][j][slot] (slot = lg - first
+// lg of j).  Per item the residual chunk, the group table and the destinations are staged in
+// shared memory.  Each warp streams the entry blocks of its groups (groups w, w + nw, ...)
+// as pieces of kPiece blocks through registers, two pieces ahead of the gathers.  Entries
+// are byte offsets of rows in the staged chunk (LDS [R + UR]).
+constexpr int kPiece = 4;      // entry blocks (256 B) per piece
+constexpr int kMaxG = 128;     // groups per item staged in shared memory (Ks * n* <= 4096)
 
-__device__ __forceinline__ double gather4(const double* __restrict__ rs, uint2 v) {
+__device__ __forceinline__ double gat(const unsigned char* __restrict__ rb, uint32_t off) {
+    return *(const double*)(rb + off);
+}
+__device__ __forceinline__ double gather4(const unsigned char* __restrict__ rb, uint2 v) {
     // fixed order: entries 0, 1, 2, 3 of the block
-    double a = rs[v.x & 0xffff];
-    a += rs[v.x >> 16];
-    a += rs[v.y & 0xffff];
-    a += rs[v.y >> 16];
+    double a = gat(rb, v.x & 0xffff);
+    a += gat(rb, v.x >> 16);
+    a += gat(rb, v.y & 0xffff);
+    a += gat(rb, v.y >> 16);
     return a;
 }
+
+struct Piece {
+    uint2 v[kPiece];
+};
 
 __global__ void __launch_bounds__(kStreamT, 2)
     k_h1_stream(const double* __restrict__ R, int64_t n, int nch, int Ks, int ns, int nitems, int nslot,
@@ -246,12 +258,15 @@ __global__ void __launch_bounds__(kStreamT, 2)
                 double* __restrict__ rrp, int* status) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[kStreamT / 32];
-    double* rs = sm;                // kC + kPad residuals of the chunk
-    double* U = sm + kC + kPad;     // Ks * ns bin sums
+    __shared__ uint2 s_gt[kMaxG];
+    __shared__ __align__(16) uint16_t s_dst[kMaxG * 32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const int NU = Ks * ns;
+    double* rs = sm;                      // kC residuals of the chunk, then kPad zero rows
+    const unsigned char* rb = (const unsigned char*)rs;
+    double* U = sm + kC + kPad;           // Ks * ns bin sums
     const int N = gridDim.x, j = blockIdx.x, q = blockIdx.y;
     const int i0 = (int)((int64_t)nitems * j / N), i1 = (int)((int64_t)nitems * (j + 1) / N);
-    const int NU = Ks * ns;
     double* Pj = P + ((size_t)q * N + j) * nslot * NU;
     for (int a = tid; a < NU; a += blockDim.x) U[a] = 0.0;
     if (tid < kPad) rs[kC + tid] = 0.0;
@@ -259,8 +274,8 @@ __global__ void __launch_bounds__(kStreamT, 2)
     int cur_lg = i0 / nch, slot = 0, cur_c = -1;
     for (int item = i0; item < i1; item++) {
         const int lg = item / nch, c = item - lg * nch;
+        __syncthreads();  // previous item consumed (chunk, group table, bin sums)
         if (lg != cur_lg) {  // flush the bin sums of the previous learner group
-            __syncthreads();
             for (int a = tid; a < NU; a += blockDim.x) {
                 Pj[(size_t)slot * NU + a] = U[a];
                 U[a] = 0.0;
@@ -268,10 +283,13 @@ __global__ void __launch_bounds__(kStreamT, 2)
             slot++;
             cur_lg = lg;
         }
+        const int2 isz = isize[item], ib = ibase[item];
+        const int ng = isz.x, gb = ib.x;
+        for (int g = tid; g < ng; g += blockDim.x) s_gt[g] = gtab[gb + g];
+        for (int a = tid; a < ng * 16; a += blockDim.x) ((uint32_t*)s_dst)[a] = ((const uint32_t*)dest)[(size_t)gb * 16 + a];
         if (c != cur_c) {
             const int64_t r0 = (int64_t)c * kC;
             const int len = (int)min((int64_t)kC, n - r0);
-            __syncthreads();  // previous chunk consumed
             double sq = 0.0;  // r^T r of the chunk (I8 / the SSE identity), by the items of learner group 0
             if ((((uintptr_t)(col + r0)) & 15) == 0) {
                 const int h = len >> 1;
@@ -308,49 +326,44 @@ __global__ void __launch_bounds__(kStreamT, 2)
             cur_c = c;
         }
         __syncthreads();
-        const int2 isz = isize[item], ib = ibase[item];
-        const int ng = isz.x, gb = ib.x;
-        int g = w;
-        uint2 gt = make_uint2(0, 0);
-        uint16_t dst = 0xffff;
-        if (g < ng) {
-            gt = __ldg(gtab + gb + g);
-            dst = __ldg(dest + (size_t)(gb + g) * 32 + lane);
-        }
-        while (g < ng) {
-            const uint2* e = ent + (size_t)gt.x * 32 + lane;
-            uint2 v[kBatch];
+        // this warp's pieces (group g, first block b0), groups w, w + nw, ...; loads two pieces ahead
+        int lg_ = w, lb_ = 0;  // next piece to load
+        auto load = [&](Piece& pc) {
+            if (lg_ < ng) {
+                const uint2 gt = s_gt[lg_];
+                const uint2* e = ent + ((size_t)gt.x + lb_) * 32 + lane;
+                const int nb = (int)gt.y - lb_;
 #pragma unroll
-            for (int u = 0; u < kBatch; u++)
-                if (u < (int)gt.y) v[u] = __ldg(e + (size_t)u * 32);
-            // next group's header while the blocks are in flight
-            const int gn = g + nw;
-            uint2 gtn = make_uint2(0, 0);
-            uint16_t dstn = 0xffff;
-            if (gn < ng) {
-                gtn = __ldg(gtab + gb + gn);
-                dstn = __ldg(dest + (size_t)(gb + gn) * 32 + lane);
+                for (int u = 0; u < kPiece; u++)
+                    if (u < nb) pc.v[u] = __ldg(e + u * 32);
+                lb_ += kPiece;
+                if (lb_ >= (int)gt.y) { lg_ += nw; lb_ = 0; }
             }
-            double a0 = 0.0, a1 = 0.0;
+        };
+        Piece p0, p1, p2;
+        load(p0);
+        load(p1);
+        int cg = w, cb = 0;
+        double a0 = 0.0, a1 = 0.0;
+        while (cg < ng) {
+            load(p2);
+            const uint2 gt = s_gt[cg];
+            const int nb = (int)gt.y - cb;
 #pragma unroll
-            for (int u = 0; u < kBatch; u += 2) {
-                if (u < (int)gt.y) a0 += gather4(rs, v[u]);
-                if (u + 1 < (int)gt.y) a1 += gather4(rs, v[u + 1]);
+            for (int u = 0; u < kPiece; u += 2) {
+                if (u < nb) a0 += gather4(rb, p0.v[u]);
+                if (u + 1 < nb) a1 += gather4(rb, p0.v[u + 1]);
             }
-            for (uint32_t s0 = kBatch; s0 < gt.y; s0 += kBatch) {  // long bins (rare): further batches
-#pragma unroll
-                for (int u = 0; u < kBatch; u++)
-                    if (s0 + u < gt.y) v[u] = __ldg(e + (size_t)(s0 + u) * 32);
-#pragma unroll
-                for (int u = 0; u < kBatch; u += 2) {
-                    if (s0 + u < gt.y) a0 += gather4(rs, v[u]);
-                    if (s0 + u + 1 < gt.y) a1 += gather4(rs, v[u + 1]);
-                }
+            cb += kPiece;
+            if (cb >= (int)gt.y) {  // group complete: lane's bin total
+                const uint16_t dst = s_dst[cg * 32 + lane];
+                if (dst != 0xffff) U[dst] += a0 + a1;
+                a0 = a1 = 0.0;
+                cg += nw;
+                cb = 0;
             }
-            if (dst != 0xffff) U[dst] += a0 + a1;
-            g = gn;
-            gt = gtn;
-            dst = dstn;
+            p0 = p1;
+            p1 = p2;
         }
     }
     __syncthreads();
@@ -366,19 +379,19 @@ __global__ void __launch_bounds__(kStreamT, 2)
 //   delta = 2 theta^T s - theta^T G theta, SSE = r^T r - delta
 // and the last block to finish (atomic ticket) takes argmin SSE over k, lowest k on ties
 // (P:L292), for every column.
-__global__ void __launch_bounds__(256) k_fit_narrow(
-    const double* __restrict__ P, int K, int ns, int Ks, int nch, int nitems, int N, int nslot, int B, int d,
-    const int32_t* __restrict__ zj0, const double* __restrict__ Zs, const int32_t* __restrict__ lwin,
-    const double* __restrict__ Ainv, const double* __restrict__ G, const double* __restrict__ rrp,
-    double* __restrict__ theta, double* __restrict__ delta, unsigned* __restrict__ ticket, int32_t* __restrict__ k_out,
-    double* __restrict__ theta_out, double* __restrict__ sse_out) {
+__global__ void __launch_bounds__(1024) k_fit_narrow(
+    const double* __restrict__ P, int K, int ns, int Ks, int nch, int nitems, int N, int nslot, int B, int d, int W,
+    const double* __restrict__ ZT, const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
+    const double* __restrict__ G, const double* __restrict__ rrp, double* __restrict__ theta, double* __restrict__ delta,
+    unsigned* __restrict__ ticket, int32_t* __restrict__ k_out, double* __restrict__ theta_out,
+    double* __restrict__ sse_out) {
     extern __shared__ double u[];  // [ns][B]
-    __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4];
+    __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4], V[CWB_MAX_D][4];
+    __shared__ int s_j[2 * 148 + 1], s_slot[2 * 148 + 1], s_nj;
     __shared__ bool last;
     const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
     const int lg = k / Ks, NU = Ks * ns, a0 = (k - lg * Ks) * ns;
     // the CTAs whose item range meets [lg nch, (lg+1) nch), and their slot for lg
-    __shared__ int s_j[2 * 148 + 1], s_slot[2 * 148 + 1], s_nj;
     if (tid == 0) {
         const int64_t it0 = (int64_t)lg * nch, it1 = it0 + nch;
         int jlo = (int)(it0 * N / nitems), m = 0;
@@ -395,31 +408,31 @@ __global__ void __launch_bounds__(256) k_fit_narrow(
     }
     __syncthreads();
     const int nj = s_nj;
-    for (int l = tid; l < ns; l += blockDim.x)
-        for (int q = 0; q < B; q++) {
-            double v = 0.0;
-            int m = 0;
-            for (; m + 4 <= nj; m += 4) {  // loads of 4 partials in flight, added in CTA order
-                const double p0 = P[(((size_t)q * N + s_j[m]) * nslot + s_slot[m]) * NU + a0 + l];
-                const double p1 = P[(((size_t)q * N + s_j[m + 1]) * nslot + s_slot[m + 1]) * NU + a0 + l];
-                const double p2 = P[(((size_t)q * N + s_j[m + 2]) * nslot + s_slot[m + 2]) * NU + a0 + l];
-                const double p3 = P[(((size_t)q * N + s_j[m + 3]) * nslot + s_slot[m + 3]) * NU + a0 + l];
-                v += p0; v += p1; v += p2; v += p3;
-            }
-            for (; m < nj; m++) v += P[(((size_t)q * N + s_j[m]) * nslot + s_slot[m]) * NU + a0 + l];
-            u[l * B + q] = v;
+    for (int e = tid; e < ns * B; e += blockDim.x) {  // u_k(l) for column q, partials added in CTA order
+        const int l = e / B, q = e - l * B;
+        const double* pq = P + (size_t)q * N * nslot * NU + a0 + l;
+        double v = 0.0;
+        int m = 0;
+        for (; m + 8 <= nj; m += 8) {
+            double t[8];
+#pragma unroll
+            for (int x = 0; x < 8; x++) t[x] = pq[((size_t)s_j[m + x] * nslot + s_slot[m + x]) * NU];
+#pragma unroll
+            for (int x = 0; x < 8; x++) v += t[x];
         }
+        for (; m < nj; m++) v += pq[((size_t)s_j[m] * nslot + s_slot[m]) * NU];
+        u[e] = v;
+    }
     __syncthreads();
-    const int32_t* j0 = zj0 + (size_t)k * ns;
-    const double* zs = Zs + (size_t)k * ns * CWB_SPW;
+    // s_j = sum over the design-point window of basis j of Zb[l][j] u(l)   (ZT: window-major basis)
     for (int j = w; j < d; j += nw) {
         const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int l = lb + lane; l < le; l += 32) {
-            const double z = zs[l * CWB_SPW + (j - j0[l])];
+        for (int x = lane; x < le - lb; x += 32) {
+            const double z = ZT[((size_t)k * W + x) * d + j];
 #pragma unroll
             for (int q = 0; q < 4; q++)
-                if (q < B) acc[q] += z * u[l * B + q];
+                if (q < B) acc[q] += z * u[(lb + x) * B + q];
         }
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -428,25 +441,26 @@ __global__ void __launch_bounds__(256) k_fit_narrow(
         }
     }
     __syncthreads();
-    const double* Ai = Ainv + (size_t)k * d * d;
-    if (tid < d * B) {
-        const int j = tid / B, q = tid - j * B;
+    const int jq = tid / B, qq = tid - jq * B;
+    if (tid < d * B) {  // theta = A^-1 s (cached inverse)
+        const double* Ai = Ainv + ((size_t)k * d + jq) * d;
         double t = 0.0;
-        for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][q];
-        Th[j][q] = t;
-        theta[((size_t)k * d + j) * 4 + q] = t;
+        for (int jp = 0; jp < d; jp++) t += Ai[jp] * S[jp][qq];
+        Th[jq][qq] = t;
+        theta[((size_t)k * d + jq) * 4 + qq] = t;
+    }
+    __syncthreads();
+    if (tid < d * B) {  // theta_j (2 s_j - (G theta)_j), G banded (|j - j'| <= 3)
+        const double* Gk = G + ((size_t)k * d + jq) * d;
+        double gt = 0.0;
+        for (int jp = max(0, jq - (CWB_SPW - 1)); jp <= min(d - 1, jq + CWB_SPW - 1); jp++) gt += Gk[jp] * Th[jp][qq];
+        V[jq][qq] = Th[jq][qq] * (2.0 * S[jq][qq] - gt);
     }
     __syncthreads();
     if (tid < B) {
-        const int q = tid;
-        const double* Gk = G + (size_t)k * d * d;
         double v = 0.0;
-        for (int j = 0; j < d; j++) {
-            double gt = 0.0;
-            for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++) gt += Gk[j * d + jp] * Th[jp][q];
-            v += Th[j][q] * (2.0 * S[j][q] - gt);
-        }
-        delta[(size_t)k * 4 + q] = v;
+        for (int j = 0; j < d; j++) v += V[j][tid];
+        delta[(size_t)k * 4 + tid] = v;
     }
     __threadfence();
     __syncthreads();
@@ -497,7 +511,7 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
     if (p.ready) return CWB_OK;
     const int K = c->K, ns = c->n_star;
     const int64_t n = c->n;
-    if (ns > 12288) return CWB_EUNSUPPORTED;
+    if (ns > kUBudget) return CWB_EUNSUPPORTED;  // <= kMaxG groups of 32 tasks per item
     // learner group size: bin sums within the shared-memory budget, and at least 2 x 148 items
     const int nch0 = (int)((n + kC - 1) / kC);
     const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / (2 * 148))));
@@ -586,7 +600,8 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
 // k_h1_stream + k_fit_narrow.  CWB_EUNSUPPORTED when the plan does not apply (caller falls back).
 int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
                          double* sse_out, cudaStream_t s) {
-    if (c->rows || B < 1 || B > 4 || (size_t)c->n_star * B * sizeof(double) > 96 * 1024) return CWB_EUNSUPPORTED;
+    if (c->rows || B < 1 || B > 4 || (size_t)c->n_star * B * sizeof(double) > 96 * 1024 ||
+        c->n_star > kUBudget) return CWB_EUNSUPPORTED;
     int rc = stream_plan(c, s);
     if (rc) return rc;
     cwb_stream_plan& p = c->sp;
@@ -616,8 +631,8 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
                                                     p.gtab, p.dest, p.isize, p.ibase, p.part, rrp, c->d_status);
     const size_t fsm = sizeof(double) * (size_t)ns * B;
     cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    k_fit_narrow<<<K, 256, fsm, s>>>(p.part, K, ns, p.Ks, p.nch, p.nitems, N, nslot, B, d, c->zj0, c->Zs, c->lwin,
-                                     c->Ainv, c->G, rrp, th, de, ticket, k_out, theta_out, sse_out);
+    k_fit_narrow<<<K, 1024, fsm, s>>>(p.part, K, ns, p.Ks, p.nch, p.nitems, N, nslot, B, d, c->W, c->ZT, c->lwin,
+                                      c->Ainv, c->G, rrp, th, de, ticket, k_out, theta_out, sse_out);
     c->launches += 2;
     return cwb_check_launch(c, "stream find_best kernels");
 }
