@@ -478,7 +478,17 @@ typedef struct {
     double nu;
     double *offset, *theta_agg, *sse_trace, *risk_trace, *gap_trace, *f_out;
     int32_t* k_trace;
+    int loss; /* ORC_LOSS_L2 or ORC_LOSS_BERNOULLI */
 } train_job;
+
+/* Bernoulli loss of the logistic model, y in {0, 1}:
+ * L(y, f) = log(1 + exp(f)) - y f, written so that exp never overflows. */
+static double bern_loss(double y, double f) {
+    double sp = f > 0.0 ? f + log1p(exp(-f)) : log1p(exp(f));
+    return sp - y * f;
+}
+/* pseudo residual -dL/df = y - 1 / (1 + exp(-f)) */
+static double bern_resid(double y, double f) { return y - 1.0 / (1.0 + exp(-f)); }
 
 /* Alg. 1 supp., one replication at a time. */
 static void train_one(const train_job* J, int b, scratch* w, double* f, double* r, double* theta) {
@@ -486,17 +496,20 @@ static void train_one(const train_job* J, int b, scratch* w, double* f, double* 
     int64_t n = p->n;
     int d = p->d, K = p->K, B = J->B;
     const double* y = J->Y + (size_t)b * n;
-    /* line 2: f0 = argmin_c R_emp(c) = mean(y) for L2 (S:L319 reading) */
+    /* line 2: f0 = argmin_c R_emp(c): mean(y) for L2, log(p / (1 - p)) with p = mean(y) for
+     * the Bernoulli loss (S:L319 reading; the caller checked 0 < p < 1) */
     double sy = 0.0;
     for (int64_t i = 0; i < n; i++) sy += y[i];
     double f0 = sy / (double)n;
+    if (J->loss == ORC_LOSS_BERNOULLI) f0 = log(f0 / (1.0 - f0));
     J->offset[b] = f0;
     for (int64_t i = 0; i < n; i++) f[i] = f0;
     double* agg = J->theta_agg + (size_t)b * K * d;
     for (int a = 0; a < K * d; a++) agg[a] = 0.0;
     for (int m = 0; m < J->M; m++) {
-        /* line 4: pseudo residuals r = -dL/df = y - f for L = 1/2 (y - f)^2 (G9) */
-        for (int64_t i = 0; i < n; i++) r[i] = y[i] - f[i];
+        /* line 4: pseudo residuals r = -dL/df: y - f for L = 1/2 (y - f)^2 (G9),
+         * y - 1 / (1 + exp(-f)) for the Bernoulli loss */
+        for (int64_t i = 0; i < n; i++) r[i] = J->loss == ORC_LOSS_BERNOULLI ? bern_resid(y[i], f[i]) : y[i] - f[i];
         /* lines 5-9: fit every learner, SSE, argmin */
         int32_t ks;
         double sse, gap;
@@ -515,8 +528,12 @@ static void train_one(const train_job* J, int b, scratch* w, double* f, double* 
         for (int j = 0; j < d; j++) agg[ks * d + j] += J->nu * theta[j];
         double rs = 0.0;
         for (int64_t i = 0; i < n; i++) {
-            double e = y[i] - f[i];
-            rs += 0.5 * e * e;
+            if (J->loss == ORC_LOSS_BERNOULLI) {
+                rs += bern_loss(y[i], f[i]);
+            } else {
+                double e = y[i] - f[i];
+                rs += 0.5 * e * e;
+            }
         }
         J->k_trace[(size_t)m * B + b] = ks;
         J->sse_trace[(size_t)m * B + b] = sse;
@@ -541,20 +558,47 @@ static void* train_worker(void* arg) {
     return NULL;
 }
 
+static int train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
+                      double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
+                      double* risk_trace, double* gap_trace, double* f_out);
+
 int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n_threads,
               double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
               double* risk_trace, double* gap_trace, double* f_out) {
+    return train_loss(p, Y, B, ORC_LOSS_L2, nu, M, n_threads, offset, theta_agg, k_trace, sse_trace, risk_trace,
+                      gap_trace, f_out);
+}
+
+int orc_train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
+                   double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
+                   double* risk_trace, double* gap_trace, double* f_out) {
+    return train_loss(p, Y, B, loss, nu, M, n_threads, offset, theta_agg, k_trace, sse_trace, risk_trace,
+                      gap_trace, f_out);
+}
+
+static int train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
+                      double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
+                      double* risk_trace, double* gap_trace, double* f_out) {
     if (!p || p->K < 1) return ORC_EEMPTY;
-    if (B < 1 || M < 0 || !(nu >= 0.0)) return ORC_EINVAL;
+    if (B < 1 || M < 0 || !(nu >= 0.0) || (loss != ORC_LOSS_L2 && loss != ORC_LOSS_BERNOULLI)) return ORC_EINVAL;
     for (int64_t a = 0; a < (int64_t)B * p->n; a++)
         if (!isfinite(Y[a])) return ORC_ENONFINITE;
+    if (loss == ORC_LOSS_BERNOULLI) {  /* y in {0, 1}; mean(y) in (0, 1) */
+        for (int64_t a = 0; a < (int64_t)B * p->n; a++)
+            if (Y[a] != 0.0 && Y[a] != 1.0) return ORC_EINVAL;
+        for (int b = 0; b < B; b++) {
+            double sy = 0.0;
+            for (int64_t i = 0; i < p->n; i++) sy += Y[(size_t)b * p->n + i];
+            if (sy == 0.0 || sy == (double)p->n) return ORC_EDEGENERATE;
+        }
+    }
     if (n_threads < 1) n_threads = 1;
     if (n_threads > B) n_threads = B;
     train_job* jobs = (train_job*)malloc(sizeof(train_job) * n_threads);
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
     for (int t = 0; t < n_threads; t++) {
         train_job J = {p, Y, B, M, t, n_threads, nu, offset, theta_agg, sse_trace,
-                       risk_trace, gap_trace, f_out, k_trace};
+                       risk_trace, gap_trace, f_out, k_trace, loss};
         jobs[t] = J;
     }
     for (int t = 1; t < n_threads; t++) pthread_create(&th[t], NULL, train_worker, &jobs[t]);

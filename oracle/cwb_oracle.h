@@ -130,6 +130,17 @@ int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n
               double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
               double* risk_trace, double* gap_trace, double* f_out);
 
+/* orc_train with a loss: ORC_LOSS_L2 (as orc_train) or ORC_LOSS_BERNOULLI, y in {0, 1}:
+ * L(y, f) = log(1 + exp(f)) - y f, pseudo residuals r = y - 1/(1 + exp(-f))
+ * (P:L833), offset log(p/(1-p)) with p = mean(y) (Alg. 1 line 2),
+ * risk_trace = mean L after the update of iteration m.  ORC_EINVAL if some y is not 0
+ * or 1, ORC_EDEGENERATE if mean(y) is 0 or 1. */
+#define ORC_LOSS_L2 0
+#define ORC_LOSS_BERNOULLI 1
+int orc_train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
+                   double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
+                   double* risk_trace, double* gap_trace, double* f_out);
+
 /* Accelerated CWB, Algorithm 2, L2 loss, for B target vectors: primary
  * model f, momentum model h, combined model g = (1 - theta_m) f + theta_m h, theta_m =
  * 2/(m+1); pseudo residuals at g; error-corrected residuals c; eta_m = gamma nu / theta_m.

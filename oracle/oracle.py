@@ -93,6 +93,8 @@ def lib():
                                     C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_double)]
         L.orc_train.argtypes = [C.POINTER(_Pool), _D, C.c_int, C.c_double, C.c_int, C.c_int,
                                 _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p]
+        L.orc_train_loss.argtypes = [C.POINTER(_Pool), _D, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                     _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p]
         L.orc_train_acwb.argtypes = [C.c_void_p, _D, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _D, _D, _D,
                                      _I, _I, _D, _D, _D, _D, _D, _D, _D]
         L.orc_train_hcwb.argtypes = [C.c_void_p, _D, C.c_int, _P(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_double,
@@ -343,6 +345,23 @@ class Pool:
         f = np.empty((B, self.n))
         _chk(lib().orc_train(self._p, Y, B, nu, M, threads, off, agg, kt, st, rt,
                              gt.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p)), "train")
+        return TrainResult(off, agg, kt, st, rt, gt, f)
+
+    def train_bernoulli(self, Y, nu: float = 0.05, M: int = 200, threads: int = 1) -> TrainResult:
+        """Alg. 1 supp. with the Bernoulli loss, y in {0, 1}, for B
+        target vectors Y (B x n); risk_trace = mean log-loss after iteration m."""
+        Y = _f64(np.atleast_2d(Y))
+        B = Y.shape[0]
+        K, d = self.K, self.d
+        off = np.empty(B)
+        agg = np.empty((B, K, d))
+        kt = np.empty((M, B), dtype=np.int32)
+        st = np.empty((M, B))
+        rt = np.empty((M, B))
+        gt = np.empty((M, B))
+        f = np.empty((B, self.n))
+        _chk(lib().orc_train_loss(self._p, Y, B, 1, nu, M, threads, off, agg, kt, st, rt,
+                                  gt.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p)), "train_bernoulli")
         return TrainResult(off, agg, kt, st, rt, gt, f)
 
     def train_acwb(self, Y, nu: float = 0.05, gamma: float = 0.0034, M: int = 200,

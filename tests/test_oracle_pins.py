@@ -654,3 +654,91 @@ def test_hcwb_errors():
         pool.train_hcwb(y[None], np.zeros(y.size, np.uint8))      # no validation rows
     with pytest.raises(O.OracleError):
         pool.train_hcwb(y[None], np.ones(y.size, np.uint8))       # no training rows
+
+
+# --------------------------------------------------- Bernoulli loss
+# Alg. 1 supp. with the Bernoulli loss L(y, f) = log(1 + exp(f)) - y f, y in {0, 1}
+# (S:L298-334): pseudo residuals y - sigma(f), offset logit(mean y) (line 2).
+
+def _bern_data(seed=11, K=3, n=400, n_knots=6, df=5.0):
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(0, 1, (K, n))
+    eta = 2.0 * np.sin(5 * X[0]) + 1.5 * (X[min(1, K - 1)] - 0.5)
+    y = (rng.uniform(size=n) < 1.0 / (1.0 + np.exp(-eta))).astype(float)
+    return O.Pool(X, O.Config(n_knots=n_knots, df=df), O.MODE_BINNED), X, y
+
+
+def test_bernoulli_offset_and_first_iteration():
+    p, X, y = _bern_data()
+    res = p.train_bernoulli(y, nu=0.1, M=3)
+    pb = y.mean()
+    assert abs(res.offset[0] - math.log(pb / (1 - pb))) <= 1e-15 * 4     # argmin_c R_emp(c), closed form
+    # at f = logit(p) every pseudo residual is y - p: iteration 1 fits the L2 residual y - mean(y)
+    k, th, sse, _, _ = p.find_best(y - pb)
+    assert res.k_trace[0, 0] == k
+    assert abs(res.sse_trace[0, 0] - sse) <= 1e-12 * sse
+
+
+@pytest.mark.parametrize("frac", [0.5, 0.3])
+def test_bernoulli_nu_zero_risk_is_entropy(frac):
+    p, X, y = _bern_data()
+    n = y.size
+    y = np.zeros(n)
+    y[: int(frac * n)] = 1.0
+    res = p.train_bernoulli(y, nu=0.0, M=4)
+    q = y.mean()
+    ent = -(q * math.log(q) + (1 - q) * math.log(1 - q))   # log-loss of the constant model; log 2 at q = 1/2
+    assert np.abs(res.risk_trace[:, 0] - ent).max() <= 1e-13
+    if frac == 0.5:
+        assert abs(res.risk_trace[0, 0] - math.log(2.0)) <= 1e-14
+
+
+def test_bernoulli_single_learner_converges_to_logistic_mle():
+    # K = 1: the boosting step theta += nu (G + lambda D)^-1 Z^T (y - sigma(f)) is preconditioned
+    # gradient descent on the log-likelihood over span(Z) (which contains the constants:
+    # B-splines sum to 1), so its fixed point is the logistic-regression MLE on Z, found here
+    # independently by Newton's method (IRLS).
+    p, X, y = _bern_data(seed=3, K=1, n=600, n_knots=4, df=7.5)
+    res = p.train_bernoulli(y, nu=1.0, M=1500)
+    Z = p.Zb[0][p.idx[0]]
+    beta = np.zeros(Z.shape[1])
+    for _ in range(60):
+        eta = Z @ beta
+        mu = 1.0 / (1.0 + np.exp(-eta))
+        W = mu * (1 - mu)
+        beta = beta + np.linalg.solve(Z.T @ (W[:, None] * Z), Z.T @ (y - mu))
+    f_mle = Z @ beta
+    assert np.abs(res.f[0] - f_mle).max() <= 1e-8 * (1 + np.abs(f_mle).max())
+    mu = 1.0 / (1.0 + np.exp(-res.f[0]))
+    assert np.abs(Z.T @ (y - mu)).max() <= 1e-9 * y.size             # score equations
+
+
+def test_bernoulli_risk_decreases_and_aggregation():
+    p, X, y = _bern_data(seed=5)
+    Y = np.stack([y, 1.0 - y])
+    res = p.train_bernoulli(Y, nu=0.05, M=60, threads=2)
+    assert (np.diff(res.risk_trace, axis=0) <= 1e-14).all()   # small steps along -gradient
+    pred = p.predict(X, res.offset, res.theta_agg)
+    assert np.abs(pred - res.f).max() <= 1e-12 * (1 + np.abs(res.f).max())
+    # 1 - y is the label swap: f -> -f, same selections
+    assert (res.k_trace[:, 0] == res.k_trace[:, 1]).all()
+    assert np.abs(res.f[0] + res.f[1]).max() <= 1e-12 * np.abs(res.f).max()
+    res1 = p.train_bernoulli(Y, nu=0.05, M=60, threads=1)
+    assert (res1.theta_agg == res.theta_agg).all()
+
+
+def test_bernoulli_binned_mode_equals_dense_mode():
+    pb, X, y = _bern_data(seed=8)
+    pd = O.Pool(X, O.Config(n_knots=6), O.MODE_DENSE)
+    a = pb.train_bernoulli(y, nu=0.1, M=40)
+    b = pd.train_bernoulli(y, nu=0.1, M=40)
+    assert (a.k_trace == b.k_trace).all()
+    assert np.abs(a.theta_agg - b.theta_agg).max() <= 1e-10 * np.abs(b.theta_agg).max()
+
+
+def test_bernoulli_errors():
+    p, X, y = _bern_data()
+    with pytest.raises(O.OracleError):
+        p.train_bernoulli(np.where(y > 0, 2.0, 0.0), M=2)        # y not in {0, 1}
+    with pytest.raises(O.OracleError):
+        p.train_bernoulli(np.ones_like(y), M=2)                   # mean(y) = 1
