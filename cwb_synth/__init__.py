@@ -139,3 +139,17 @@ def validation_mask(n: int, frac: float = 0.3, seed: int = 0) -> np.ndarray:
     m = np.zeros(n, dtype=np.uint8)
     m[rng.choice(n, size=int(round(frac * n)), replace=False)] = 1
     return m
+
+
+def binary_targets(ds: Dataset, scale: float = 2.0) -> np.ndarray:
+    """Seeded 0/1 targets for the Bernoulli-loss workload (binary classification, the paper's
+    real-data setting P:L411): replication c's latent Y[c] standardised to SD `scale` on the
+    logit scale, y ~ Bernoulli(1 / (1 + exp(-z))) with uniforms from the replication's own
+    seed stream (SeedSequence([SEED, 9, cfg_id, rep]))."""
+    out = np.empty_like(ds.Y)
+    for c, b in enumerate(ds.reps):
+        z = ds.Y[c] - ds.Y[c].mean()
+        z = scale * z / z.std(ddof=1)
+        u = np.random.default_rng(np.random.SeedSequence([SEED, 9, ds.cfg.cfg_id, int(b)])).uniform(size=z.size)
+        out[c] = (u < 1.0 / (1.0 + np.exp(-z))).astype(np.float64)
+    return out

@@ -187,6 +187,20 @@ int cwb_train_acwb(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double g
                    double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
                    int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t stream);
 
+/* CWB (Alg. 1 supp.) with the Bernoulli loss of the logistic model,
+ * L(y, f) = log(1 + exp(f)) - y f for y in {0, 1} (binary classification, the paper's
+ * real-data setting P:L411).  Arguments and outputs as
+ * cwb_train, except: offset_out[b] = log(p / (1 - p)) with p = mean(y_b) (Alg. 1 line 2,
+ * argmin_c R_emp(c)); the pseudo residuals are r = y - 1 / (1 + exp(-f)), fitted
+ * by the base learners with the L2 criterion as for the L2 loss (sse_trace = SSE of that
+ * fit); risk_trace[m][b] = mean L(y, f) after the update of iteration m.  General path
+ * (per-iteration kernels).  Errors: CWB_EINVAL (arguments; a target value that is not 0
+ * or 1, reported by cwb_status), CWB_EDEGENERATE (mean(y_b) is 0 or 1, cwb_status),
+ * CWB_ENONFINITE, CWB_EUNSUPPORTED (row-sharded context, cwb_set_path(1)). */
+int cwb_train_bernoulli(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                        double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+                        cudaStream_t stream);
+
 /* Hybrid CWB, Algorithm 3 ("HCWB"), L2 loss.  val_mask[n] (device, uint8):
  * 1 = validation row (D_val), 0 = training row (D_train); the split is the caller's
  * (seeded) draw.  Per replication: ACWB (as cwb_train_acwb, momentum gamma) fitted on the

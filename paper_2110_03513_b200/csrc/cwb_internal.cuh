@@ -39,6 +39,8 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     double* acwb = nullptr;    // ACWB: F, H (n x Bq each), row-block partials, offsets
     size_t acwb_bytes = 0;
     double* pack = nullptr;    // row sharding: [K][d][Bp] partial s, then [Bp] partial r^T r
+    double* bern = nullptr;    // Bernoulli loss: F, Yt (n x Bp each), row-block partials
+    size_t bern_bytes = 0;
 };
 
 struct cwb_stream_plan {  // streaming binMatVec gather plan (cwb_stream.cu), built on first use
@@ -157,6 +159,9 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
                            int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
                            int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
                            int32_t* switch_iter, cudaStream_t s);
+int cwb_train_bernoulli_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
+                                double* offset_out, double* theta_agg_out, int32_t* k_trace,
+                                double* sse_trace, double* risk_trace, cudaStream_t s);
 int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, double* G_tr, double* Ainv_tr,
                            cudaStream_t s);
 int cwb_find_best_general(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out,

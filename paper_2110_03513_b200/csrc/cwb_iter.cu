@@ -614,6 +614,106 @@ __global__ void k_hcwb_rr(const double* __restrict__ part, int nblk, int B, int 
     rr[B + b] = sc;
 }
 
+// ---------------------------------------------------------------- Bernoulli loss
+// CWB (Alg. 1 supp.) with the Bernoulli loss L(y, f) = log(1 + exp(f)) - y f,
+// y in {0, 1}: offset logit(mean y) (line 2), pseudo residuals
+// r = y - 1 / (1 + exp(-f)) (line 4); the base-learner fits and the selection are
+// the L2 fits of r as for the L2 loss.  Per replication the fit F[i][b] = f(x_i) and the
+// targets Yt[i][b] are kept row-major next to the residuals Rt[i][b].
+
+// f0[b] = log(p / (1 - p)), p = mean(y_b) (in f0 on entry); CWB_EDEGENERATE for p in {0, 1}
+__global__ void k_bern_offset(double* __restrict__ f0, int B, double* offset_out, int* status) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double p = f0[b];
+    if (!(p > 0.0 && p < 1.0)) cwb_dev_fail(status, CWB_EDEGENERATE);
+    const double t = log(p / (1.0 - p));
+    f0[b] = t;
+    if (offset_out) offset_out[b] = t;
+}
+
+// Yt = Y^T (0/1 check, CWB_EINVAL otherwise); padding columns 0
+__global__ void k_bern_init(const double* __restrict__ Y, int64_t n, int B, int Bp, double* __restrict__ Yt,
+                            int* status) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int b0 = blockIdx.y * 32;
+    for (int q = threadIdx.y; q < 32; q += blockDim.y) {
+        const int b = b0 + q;
+        const int64_t i = i0 + threadIdx.x;
+        double v = 0.0;
+        if (b < B && i < n) {
+            v = Y[(size_t)b * n + i];
+            if (v != 0.0 && v != 1.0) cwb_dev_fail(status, CWB_EINVAL);
+        }
+        tile[q][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int q = threadIdx.y; q < 32; q += blockDim.y) {
+        const int64_t i = i0 + q;
+        const int b = b0 + threadIdx.x;
+        if (i < n) Yt[(size_t)i * Bp + b] = tile[threadIdx.x][q];
+    }
+}
+
+// (f0 != NULL) f = f0 (line 2); (zhat != NULL) f += nu b_{k*}(x) at the design points (line 10);
+// then r = y - sigma(f) (line 4 of the next iteration) and row-block partial sums of r^2, L(y, f)
+template <typename IdxT>
+__global__ void k_bern_update(double* __restrict__ Rt, double* __restrict__ F, const double* __restrict__ Yt,
+                              int64_t n, int Bp, int B, const double* __restrict__ f0, const int32_t* __restrict__ kstar,
+                              const IdxT* __restrict__ idx, const double* __restrict__ zhat, double* __restrict__ part,
+                              int nblk) {
+    __shared__ double red[2][8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const IdxT* ik = zhat ? idx + (size_t)kstar[b] * n : nullptr;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6;
+    const int64_t r1 = min(n, r0 + kRowsH6);
+    double a2 = 0.0, al = 0.0;
+    for (int64_t i = r0 + w; i < r1; i += 8) {
+        const size_t e = (size_t)i * Bp + b;
+        double f;
+        if (f0) {
+            f = b < B ? f0[b] : 0.0;
+            F[e] = f;
+        } else {
+            f = F[e];
+        }
+        if (zhat) {
+            f = f + zhat[(size_t)ik[i] * Bp + b];
+            F[e] = f;
+        }
+        const double y = Yt[e];
+        const double r = y - 1.0 / (1.0 + exp(-f));
+        Rt[e] = r;
+        a2 += r * r;
+        al += (f > 0.0 ? f + log1p(exp(-f)) : log1p(exp(f))) - y * f;
+    }
+    red[0][w][lane] = a2;
+    red[1][w][lane] = al;
+    __syncthreads();
+    if (w == 0) {
+        double s2 = 0.0, sl = 0.0;
+        for (int q = 0; q < 8; q++) { s2 += red[0][q][lane]; sl += red[1][q][lane]; }
+        part[(size_t)blockIdx.x * Bp + b] = s2;
+        part[((size_t)nblk + blockIdx.x) * Bp + b] = sl;
+    }
+}
+
+// rr[b] = r^T r; risk_trace[m][b] = mean L(y, f) (m >= 0)
+__global__ void k_bern_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n, int m,
+                          double* __restrict__ rr, double* risk_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double s = 0.0, l = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        s += part[(size_t)q * Bp + b];
+        l += part[((size_t)nblk + q) * Bp + b];
+    }
+    rr[b] = s;
+    if (risk_trace && m >= 0) risk_trace[(size_t)m * B + b] = l / (double)n;
+}
+
 // ---------------------------------------------------------------- narrow path
 // binMatVec sums for a few residual vectors (B <= 4), e.g. one
 // findBestBaselearner on a single residual: HBM-bound on the index vector.  A CTA
@@ -796,6 +896,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     cwb_release(w.colpart, s);
     cwb_release(w.acwb, s);
     cwb_release(w.pack, s);
+    cwb_release(w.bern, s);
     w = cwb_train_ws();
     const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
     bool ok = true;
@@ -988,6 +1089,58 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
         c->launches += 3;
     }
     return cwb_check_launch(c, "general train kernels");
+}
+
+// CWB with the Bernoulli loss on the general path (kernels above).
+int cwb_train_bernoulli_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
+                                double* offset_out, double* theta_agg_out, int32_t* k_trace,
+                                double* sse_trace, double* risk_trace, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp;
+    const int nblk = w.n_part;
+    const size_t need = sizeof(double) * ((size_t)2 * c->n * Bp + (size_t)2 * nblk * Bp);
+    if (w.bern_bytes < need) {
+        cwb_release(w.bern, s);
+        w.bern = nullptr;
+        w.bern_bytes = 0;
+        if (cwb_alloc((void**)&w.bern, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "Bernoulli workspace allocation failed");
+        w.bern_bytes = need;
+    }
+    double* F = w.bern;
+    double* Yt = F + (size_t)c->n * Bp;
+    double* part = Yt + (size_t)c->n * Bp;
+    double* f0 = w.rr + Bp;
+    rc = column_stats(c, Y, B, true, f0, w.rr, nullptr, s);  // f0 = mean(y), finiteness
+    if (rc) return rc;
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_bern_init<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, Yt, c->d_status);
+    k_bern_offset<<<(B + 127) / 128, 128, 0, s>>>(f0, B, offset_out, c->d_status);
+    const size_t nagg = (size_t)B * c->K * c->d;
+    k_zero<<<(unsigned)min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_agg_out, nagg);
+    dim3 g6(nblk, Bp / 32);
+    auto update = [&](bool first) {
+        if (c->idx_bytes == 1)
+            k_bern_update<uint8_t><<<g6, 256, 0, s>>>(w.Rt, F, Yt, c->n, Bp, B, first ? f0 : nullptr, w.kstar,
+                                                      (const uint8_t*)c->idx, first ? nullptr : w.zhat, part, nblk);
+        else
+            k_bern_update<uint16_t><<<g6, 256, 0, s>>>(w.Rt, F, Yt, c->n, Bp, B, first ? f0 : nullptr, w.kstar,
+                                                       (const uint16_t*)c->idx, first ? nullptr : w.zhat, part, nblk);
+    };
+    update(true);  // f = f0, r = y - sigma(f0), r^T r
+    k_bern_rr<<<(B + 127) / 128, 128, 0, s>>>(part, nblk, B, Bp, c->n, -1, w.rr, nullptr);
+    c->launches += 5;
+    for (int m = 0; m < M; m++) {
+        find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
+        k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
+                                                                  c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
+        update(false);
+        k_bern_rr<<<(B + 127) / 128, 128, 0, s>>>(part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+        c->launches += 3;
+    }
+    return cwb_check_launch(c, "Bernoulli train kernels");
 }
 
 // ------------------------------------------------------------ row sharding

@@ -1,5 +1,2 @@
-python __graft_entry__.py build > gpurun_out/s7_build.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_stream.py -x -q > gpurun_out/s7_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/s7_pytest.log
-for cfg in R2 R3 R4; do timeout 120 python tools/findbest_timing.py $cfg 1 20 0 >> gpurun_out/s7_fb.log 2>&1; done
-timeout 120 python tools/findbest_timing.py R4 1 3 0 > gpurun_out/s7_plain.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_h1_stream|k_fit_narrow" -s 2 -c 2 -o gpurun_out/s7_stream python tools/findbest_timing.py R4 1 3 0 > gpurun_out/s7_ncu.log 2>&1
+python __graft_entry__.py build > gpurun_out/s8_build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s8_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/s8_pytest.log
