@@ -46,6 +46,9 @@ typedef enum {
     CWB_ENOMEM = -8,        /* device allocation failed                                       */
     CWB_EUNSUPPORTED = -9   /* configuration outside what the kernels implement               */
 } cwb_code;
+/* Error state of a context: a call rejected before any work is enqueued (CWB_EINVAL for
+ * its arguments, CWB_EUNSUPPORTED) leaves the context usable; any other error (a device-
+ * side status, CUDA, NCCL, allocation) is kept and returned by every later call on it. */
 
 typedef struct cwb_ctx cwb_ctx;
 
@@ -60,9 +63,16 @@ typedef struct {
     int32_t batch_hint;   /* expected B of the cwb_train calls (0: unknown).  When > 0, cwb_init
                              builds the fused kernel's gather plan for that B on a side stream,
                              overlapped with the rest of the pool construction.                   */
+    int32_t unbinned;     /* 0: binned learners (the paper's method, default).  1: unbinned ("nb")
+                             learners on the raw feature values, the
+                             baseline binning is compared against: per row 4 non-zero
+                             cubic B-spline values at the knot span of x.  Degree 3 only;
+                             cwb_train (L2) and cwb_find_best on the per-iteration kernels;
+                             the other training calls and cwb_predict return CWB_EUNSUPPORTED. */
 } cwb_config;
 
-/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5, no batch hint. */
+/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5, no batch hint,
+ * binned learners. */
 void cwb_default_config(cwb_config* cfg);
 
 /* Library ABI version (major*100 + minor). */

@@ -26,7 +26,8 @@ int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32
 
 int cwb_set_error(cwb_ctx* ctx, int code, const std::string& msg) {
     if (ctx) {
-        if (ctx->status == CWB_OK) ctx->status = code;
+        // argument / unsupported-configuration rejections leave the context usable (include/cwb.h)
+        if (ctx->status == CWB_OK && code != CWB_EINVAL && code != CWB_EUNSUPPORTED) ctx->status = code;
         ctx->err = msg;
     } else {
         g_err = msg;
@@ -101,6 +102,7 @@ void cwb_default_config(cwb_config* cfg) {
     cfg->df = 5.0;
     cfg->df_kind = 1;
     cfg->batch_hint = 0;
+    cfg->unbinned = 0;
 }
 
 int cwb_version(void) { return 100; }
@@ -164,6 +166,7 @@ void cwb_free(cwb_ctx* c) {
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
     cwb_stream_release(c, s);
+    cwb_nb_release(c, s);
     if (c->ev_plan) cudaEventDestroy(c->ev_plan);
     if (c->ev_csr) cudaEventDestroy(c->ev_csr);
     if (c->s2) cudaStreamDestroy(c->s2);
@@ -186,10 +189,15 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
         return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: need degree 1..3 and d <= 32");
     if (cfg.df_kind != 1 && cfg.df_kind != 2) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: df_kind");
     if (n > INT32_MAX) return cwb_set_error(nullptr, CWB_EUNSUPPORTED, "cwb_init: n >= 2^31");
+    if (cfg.unbinned != 0 && cfg.unbinned != 1) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: unbinned");
+    if (cfg.unbinned && (cfg.degree != 3 || cfg.n_knots + 1 > 255))
+        return cwb_set_error(nullptr, CWB_EUNSUPPORTED, "cwb_init: unbinned learners need degree 3");
     cwb_ctx* c = new cwb_ctx();
     c->n = n; c->K = K; c->n_star = (int32_t)ns; c->d = d; c->degree = cfg.degree; c->n_knots = cfg.n_knots;
     c->df = cfg.df; c->df_kind = cfg.df_kind;
-    c->batch_hint = cfg.batch_hint > 0 ? cfg.batch_hint : 0;
+    c->batch_hint = cfg.batch_hint > 0 && !cfg.unbinned ? cfg.batch_hint : 0;
+    c->nb = cfg.unbinned != 0;
+    if (c->nb) c->path = 2;  // per-iteration kernels only
     c->idx_bytes = ns <= 256 ? 1 : 2;
     c->perm_bytes = n <= 65536 ? 2 : 4;
     c->stream = s;
@@ -241,7 +249,11 @@ int cwb_status(cwb_ctx* c) {
     int dev = 0;
     e = cudaMemcpy(&dev, c->d_status, sizeof(int), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cwb_set_error(c, CWB_ECUDA, cudaGetErrorString(e));
-    if (dev) return cwb_set_error(c, dev, std::string("device: ") + status_name(dev));
+    if (dev) {  // device-side errors are kept whatever their code
+        cwb_set_error(c, dev, std::string("device: ") + status_name(dev));
+        if (c->status == CWB_OK) c->status = dev;
+        return dev;
+    }
     return CWB_OK;
 }
 
@@ -338,6 +350,7 @@ int cwb_train_bernoulli(cwb_ctx* c, const double* Y, int32_t B, double nu, int32
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: row-sharded context");
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: unbinned pool (cwb_train only)");
     if (c->path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: general path only");
     return cwb_train_bernoulli_general(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace, s);
 }
@@ -351,6 +364,7 @@ int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gam
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: row-sharded context");
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: unbinned pool (cwb_train only)");
     if (c->path != 2) {
         bool launched = false;
         int rc = cwb_train_acwb_fused(c, Y, B, nu, gamma, M, offset_out, theta_f_out, theta_h_out, k_trace,
@@ -373,6 +387,7 @@ int cwb_train_hcwb(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_ma
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: row-sharded context");
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: unbinned pool (cwb_train only)");
     return cwb_train_hcwb_general(c, Y, B, val_mask, nu, gamma, pat0, M, offset_out, theta_f_out, k_trace, kcor_trace,
                                   sse_trace, risk_trace, val_risk_trace, switch_iter, s);
 }
@@ -423,6 +438,7 @@ int cwb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offset,
     if (!c || !Xnew || !offset || !theta_agg || !out || m < 1 || B < 1)
         return cwb_set_error(c, CWB_EINVAL, "cwb_predict: invalid argument");
     if (c->status) return c->status;
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_predict: unbinned pool");
     c->stream = s;
     return cwb_predict_impl(c, Xnew, m, offset, theta_agg, B, out, s);
 }

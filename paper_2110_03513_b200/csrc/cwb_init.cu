@@ -613,11 +613,18 @@ int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
     rc = cwb_launch_csr(c, c->idx, c->idx_bytes, c->n, K, ns, c->cnt, c->off, c->perm,
                         c->perm_bytes, s);
     if (rc) return rc;
-    rc = cwb_fused_plan(c, s);
-    if (rc) return rc;
+    if (!c->nb) {
+        rc = cwb_fused_plan(c, s);
+        if (rc) return rc;
+    }
     k_basis<<<K, 128, sizeof(int32_t) * ns, s>>>(c->z, c->lo, c->hi, ns, c->degree, c->n_knots, d,
                                                  c->Zb, c->zj0, c->Zs, c->lwin, c->d_status);
-    k_gram<<<K, 256, 0, s>>>(c->Zb, c->cnt, ns, d, c->lwin, c->G, c->d_status);
+    if (c->nb) {  // unbinned learners: G = Z^T Z on the raw x (cwb_nb.cu)
+        rc = cwb_nb_init(c, X, s);
+        if (rc) return rc;
+    } else {
+        k_gram<<<K, 256, 0, s>>>(c->Zb, c->cnt, ns, d, c->lwin, c->G, c->d_status);
+    }
     k_lambda<<<K, 32, 0, s>>>(c->G, d, c->df, c->df_kind, c->lambda, c->Ainv, c->Cb, c->d_status);
     k_zt<<<K, 256, 0, s>>>(c->Zb, c->lwin, ns, d, c->W, c->ZT, c->d_status);
     c->launches += 4;

@@ -119,6 +119,19 @@ struct cwb_ctx {
 
     cwb_train_ws ws;
     cwb_stream_plan sp;
+
+    // unbinned learners (cwb_nb.cu, cwb_config.unbinned)
+    bool nb = false;
+    int32_t nb_spans = 0, nb_Q = 0;  // knot spans S = n_knots + 1; H12 work items per learner
+    uint8_t* nb_sp = nullptr;        // K x n   knot span of x_ki
+    double* nb_t = nullptr;          // K x n   (x - knot) / h
+    double* nb_ts = nullptr;         // K x n   the same in span-sorted order
+    uint32_t* nb_cnt = nullptr;      // K x S   rows per span
+    int32_t* nb_off = nullptr;       // K x (S+1)
+    void* nb_perm = nullptr;         // K x n   rows sorted by span
+    double* nb_P = nullptr;          // H12 partials
+    size_t nb_Pbytes = 0;
+    double* nb_S = nullptr;          // K x d x Bp projections s
 };
 
 // ----------------------------------------------------------------- helpers
@@ -174,6 +187,11 @@ int cwb_rows_allreduce(cwb_ctx* ctx, double* buf, int64_t count, cudaStream_t s)
 int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out, double* theta_out,
                          double* sse_out, cudaStream_t s);
 void cwb_stream_release(cwb_ctx* c, cudaStream_t s);
+int cwb_nb_init(cwb_ctx* c, const double* X, cudaStream_t s);
+int cwb_nb_h12(cwb_ctx* c, const double* Rt, int Bp, double* Sg, cudaStream_t s);
+void cwb_nb_h6(cwb_ctx* c, double* Rt, int Bp, const int32_t* kstar, const double* theta, double nu,
+               int rows_per_blk, int nblk, double* part, cudaStream_t s);
+void cwb_nb_release(cwb_ctx* c, cudaStream_t s);
 int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
                      const double* theta_agg, int32_t B, double* out, cudaStream_t s);
 

@@ -908,7 +908,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     ok &= cwb_alloc((void**)&w.zhat, sizeof(double) * ns * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.kstar, sizeof(int32_t) * Bp, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&w.part, sizeof(double) * (size_t)nblk * Bp, s) == cudaSuccess;
-    if (c->rows) ok &= cwb_alloc((void**)&w.pack, sizeof(double) * (K * d + 1) * Bp, s) == cudaSuccess;
+    if (c->rows || c->nb) ok &= cwb_alloc((void**)&w.pack, sizeof(double) * (K * d + 1) * Bp, s) == cudaSuccess;
     if (!ok) return cwb_set_error(c, CWB_ENOMEM, "general-path workspace allocation failed");
     w.B = B; w.Bp = Bp; w.n_part = nblk;
     return CWB_OK;
@@ -961,9 +961,15 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
                            cudaStream_t s) {
     cwb_train_ws& w = c->ws;
     const int Bp = w.Bp;
-    h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
-    k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
-                                                c->Ainv, c->G, w.theta, w.delta);
+    if (c->nb) {  // unbinned learners: s = Z^T r by the 4-tap scatter (cwb_nb.cu), then H3-H4 from s
+        cwb_nb_h12(c, w.Rt, Bp, w.pack, s);
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin, c->Ainv,
+                                                    c->G, w.theta, w.delta, nullptr, nullptr, nullptr, 0, w.pack, 2);
+    } else {
+        h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
+                                                    c->Ainv, c->G, w.theta, w.delta);
+    }
     k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
                                           agg, k_trace, sse_trace, k_out, theta_out, sse_out);
     c->launches += 2;
@@ -1078,9 +1084,15 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
     const int nblk = w.n_part;
     for (int m = 0; m < M; m++) {
         find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
+        dim3 g6(nblk, Bp / 32);
+        if (c->nb) {
+            cwb_nb_h6(c, w.Rt, Bp, w.kstar, w.theta, nu, kRowsH6, nblk, w.part, s);
+            k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+            c->launches += 1;
+            continue;
+        }
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
                                                                   c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
-        dim3 g6(nblk, Bp / 32);
         if (c->idx_bytes == 1)
             k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
         else

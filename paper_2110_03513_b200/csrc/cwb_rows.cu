@@ -185,6 +185,7 @@ int cwb_attach_comm(cwb_ctx* c, cwb_comm* m) {
     if (c->status) return c->status;
     if (!m) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: NULL communicator");
     if (c->rows) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: context already attached");
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_attach_comm: unbinned pool");
     if (m->world > c->n) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: world > n");
     const int rc = restrict_rows(c, m->rank, m->world);
     if (rc) return rc;

@@ -35,7 +35,8 @@ class CwbError(RuntimeError):
 
 class cwb_config(C.Structure):
     _fields_ = [("n_star_rule", C.c_int32), ("n_star_fixed", C.c_int32), ("degree", C.c_int32),
-                ("n_knots", C.c_int32), ("df", C.c_double), ("df_kind", C.c_int32), ("batch_hint", C.c_int32)]
+                ("n_knots", C.c_int32), ("df", C.c_double), ("df_kind", C.c_int32), ("batch_hint", C.c_int32),
+                ("unbinned", C.c_int32)]
 
 
 @dataclass
@@ -47,10 +48,11 @@ class Config:
     df: float = 5.0
     df_kind: int = 1
     batch_hint: int = 0  # expected B of the train calls: lets cwb_init pre-build the fused plan
+    unbinned: int = 0    # 1: learners on the raw x (no binning), SURVEY NEXT-3
 
     def c(self) -> cwb_config:
         return cwb_config(self.n_star_rule, self.n_star_fixed, self.degree, self.n_knots, self.df,
-                          self.df_kind, self.batch_hint)
+                          self.df_kind, self.batch_hint, self.unbinned)
 
 
 _lib = None

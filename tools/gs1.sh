@@ -1,2 +1,2 @@
-python __graft_entry__.py build > gpurun_out/s8_build.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s8_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/s8_pytest.log
+python __graft_entry__.py build > gpurun_out/s10_build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s10_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/s10_pytest.log
