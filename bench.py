@@ -42,9 +42,11 @@ METRIC = "learner-row evaluations/s (K*n*B per boosting iteration) and boosting 
 UNIT = "evals/s"
 
 
-def alg_ops_per_rep_iter(c, n_star, d):
+def alg_ops_per_rep_iter(c, n_star, d, unbinned=False):
     """Algorithmic fp64 add/FMA operations per replication-iteration of the fused kernel."""
     K, n = c.K, c.n
+    if unbinned:  # 4-tap scatter per (learner, row), fit/SSE as binned, r -= nu Z theta with 4 taps
+        return 4 * K * n + K * d * d + 5 * K * d + 4 * n + 2 * n + d
     h1 = K * n                      # binMatVec sums: one add per (learner, row)
     h2 = 4 * K * n_star             # s = Zb^T u, 4 non-zeros per design point
     h3 = K * d * d                  # theta = A^-1 s
@@ -198,10 +200,13 @@ def main():
     ap.add_argument("--config", default="R1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 fused, 2 general")
-    ap.add_argument("--algo", default="cwb", choices=["cwb", "acwb", "hcwb"],
-                    help="cwb: Alg. 1 supp. (default, the headline); acwb: Alg. 2; hcwb: Alg. 3")
+    ap.add_argument("--algo", default="cwb", choices=["cwb", "acwb", "hcwb", "bernoulli"],
+                    help="cwb: Alg. 1 supp. (default, the headline); acwb: Alg. 2; hcwb: Alg. 3; "
+                         "bernoulli: Alg. 1 with the Bernoulli loss on seeded 0/1 targets")
     ap.add_argument("--shard", default="replications", choices=["replications", "rows"],
                     help="multi-GPU sharding: replications (weak, default) or rows (strong, NCCL per iteration)")
+    ap.add_argument("--unbinned", action="store_true",
+                    help="unbinned learners on the raw x (SURVEY NEXT-3): the baseline binning is compared to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     args = ap.parse_args()
@@ -231,10 +236,12 @@ def main():
     ds = S.make(cfg, reps=reps)
     blk = D.row_block(cfg.n, rank, ws) if rows else range(cfg.n)
     X = torch.as_tensor(ds.X, device=devname)
-    Y_host = np.ascontiguousarray(ds.Y[:, blk.start:blk.stop])
+    Ysrc = S.binary_targets(ds) if args.algo == "bernoulli" else ds.Y
+    Y_host = np.ascontiguousarray(Ysrc[:, blk.start:blk.stop])
     Y = torch.as_tensor(Y_host, device=devname)
     gcfg = cwb.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots,
-                      degree=cfg.degree, df=cfg.df, batch_hint=0 if rows else cfg.B)
+                      degree=cfg.degree, df=cfg.df, batch_hint=0 if rows or args.unbinned else cfg.B,
+                      unbinned=int(args.unbinned))
     comm = None
     if rows:  # libcwb's own NCCL communicator, id from rank 0 over the torch process group
         uid = D.nccl_unique_id(w, torch.device(devname)) if ws > 1 else cwb.cwb_comm_unique_id()
@@ -259,6 +266,8 @@ def main():
             return pool.train_acwb(Y, nu=cfg.nu, gamma=0.0034, M=M)
         if args.algo == "hcwb":   # Alg. 3, gamma = 0.037, pat0 = 5, 30 % validation
             return pool.train_hcwb(Y, vm, nu=cfg.nu, gamma=0.037, pat0=5, M=M)
+        if args.algo == "bernoulli":  # Alg. 1, Bernoulli loss
+            return pool.train_bernoulli(Y, nu=cfg.nu, M=M)
         return pool.train(Y, nu=cfg.nu, M=M, out=out)
 
     def step(i):
@@ -345,6 +354,8 @@ def main():
                 o = pool.train(Yd, nu=cfg.nu, M=M)
             elif args.algo == "acwb":
                 o = pool.train_acwb(Yd, nu=cfg.nu, gamma=0.0034, M=M)
+            elif args.algo == "bernoulli":
+                o = pool.train_bernoulli(Yd, nu=cfg.nu, M=M)
             else:
                 o = pool.train_hcwb(Yd, vm, nu=cfg.nu, gamma=0.037, pat0=5, M=M)
             for k_, v_ in o.items():
@@ -391,8 +402,8 @@ def main():
     if rank == 0:
         peaks, src = load_peaks()
         import dataclasses
-        ops = alg_ops_per_rep_iter(dataclasses.replace(cfg, n=len(blk)), n_star, d) * B * M * (
-            1 if args.algo == "cwb" else 2)  # this rank's rows
+        ops = alg_ops_per_rep_iter(dataclasses.replace(cfg, n=len(blk)), n_star, d, args.unbinned) * B * M * (
+            1 if args.algo in ("cwb", "bernoulli") else 2)  # this rank's rows
         achieved = ops / (kernel_ms * 1e-3)
         peak = fp64_peak_ops(peaks)
         traffic = None
@@ -412,11 +423,13 @@ def main():
             "scaling": "strong" if rows else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper Sec. 4.1.1 generator, seeded; OpenML sets not available)",
             "config": dict(workload_config(cfg, n_star, d), algo=args.algo, shard=args.shard,
+                           learners="unbinned" if args.unbinned else "binned",
                            parallelism=(f"rows{ws}" if rows else f"replications{ws}")),
             "iters_per_s": M / (ms_per_step * 1e-3),
             "phase_ms": {"init": float(np.mean(init_ms)), "train": float(np.mean(train_ms))},
             "roofline": {"bound": "alu",
-                         "kernel": ("general path, row-sharded" if rows else
+                         "kernel": ("general path, unbinned learners" if args.unbinned else
+                                    "general path, row-sharded" if rows else
                                     "k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
                          else f"{args.algo} per-iteration kernels (general path)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",

@@ -69,6 +69,13 @@ struct FusedParams {
     double* risk_trace;
     long long* timing;  // optional: cycles per phase (CTA 0, thread 0), summed over iterations
     int* status;
+    // HC (hybrid CWB, Alg. 3): validation mask, training-row tables, patience, extra outputs
+    const uint8_t* vmask;  // n, 1 = validation row
+    const double* Ainv_tr;  // K x d x d  (G_tr + lambda D)^-1
+    const double* Cb_tr;    // K x d x 4  band of C_tr, C_tr C_tr^T = G_tr + 2 lambda D
+    int pat0;
+    double* val_risk_trace;
+    int32_t* switch_iter;
 };
 
 __host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -76,8 +83,10 @@ __host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) &
 struct SmemLayout {
     size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, ix, total;
     size_t hh;  // ACC: H = y - h (momentum model), n doubles
+    size_t ff, mk;  // HC: F = y - f (primary model, all rows), n doubles; validation mask, n bytes
     __host__ __device__ SmemLayout(int n, int K, int nsp, int d, int W, int n_multi, int RB, int NW, bool pool,
-                                   size_t permt_bytes, int ztab, int idx_bytes = 1, bool acc = false) {
+                                   size_t permt_bytes, int ztab, int idx_bytes = 1, bool acc = false,
+                                   bool hc = false) {
         size_t o = 0;
         r = o; o = align16(o + sizeof(double) * RB * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
         U = o; o = align16(o + sizeof(double) * RB * ((size_t)K * nsp + W));  // +W: window overrun pad
@@ -87,8 +96,10 @@ struct SmemLayout {
         zhat = o; o = align16(o + sizeof(double) * RB * (size_t)nsp);
         agg = o; o = align16(o + sizeof(double) * RB * (size_t)K * d);
         pc = o; o = align16(o + sizeof(double) * RB * (n_multi > 0 ? n_multi : 1));
-        red = o; o = align16(o + sizeof(double) * 2 * (RB + (acc ? 1 : 0)) * (size_t)NW * 32);  // per-thread r^T r
+        red = o; o = align16(o + sizeof(double) * 2 * (RB + (acc ? 1 : 0) + (hc ? 1 : 0)) * (size_t)NW * 32);
         hh = o; if (acc) o = align16(o + sizeof(double) * (size_t)n);
+        ff = o; if (hc) o = align16(o + sizeof(double) * (size_t)n);
+        mk = o; if (hc) o = align16(o + (size_t)n);
         permt = o; if (pool) o = align16(o + permt_bytes);
         zt = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * W * d);
         ai = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * d * d);
@@ -161,19 +172,26 @@ __device__ __forceinline__ long long phase_mark(long long* acc, long long t0, bo
 
 // ACC (accelerated CWB, Alg. 2): RB = 2 columns of ONE replication per CTA, column 0 the pseudo
 // residuals r = y - g, column 1 the error-corrected residuals c; H = y - h in shared memory.
-template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false>
+// HC (hybrid CWB, Alg. 3, with ACC): per replication (CTA) ACWB on the training rows while the
+// validation-risk patience counter is below pat0, then CWB on all rows from the primary model;
+// F = y - f in shared memory, fitting columns zero on validation rows while accelerated, the
+// training-row tables (A_tr^-1, C_tr) until the switch, the pool's afterwards.
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false, bool HC = false>
 __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int T = blockDim.x, NW = T >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     static_assert(!ACC || RB == 2, "ACWB runs its two columns as RB = 2");
+    static_assert(!HC || ACC, "HCWB builds on the ACWB layout");
     const int b0 = ACC ? blockIdx.x : blockIdx.x * RB;  // ACC: the replication; else the first of RB
     const int n = p.n;
     const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns;
     const int W = p.W;
     const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab,
-                       (int)sizeof(IdxT), ACC);
+                       (int)sizeof(IdxT), ACC, HC);
     double* Hm = (double*)(smem + L.hh);  // ACC only
+    double* Fm = (double*)(smem + L.ff);  // HC only
+    uint8_t* mk = (uint8_t*)(smem + L.mk);  // HC only
     double* r = (double*)(smem + L.r);  // r[i * RB + q]
     const unsigned char* rb = smem + L.r;
     double* U = (double*)(smem + L.U);  // U[g * RB + q], g = k * nsp + l
@@ -185,8 +203,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     double* red = (double*)(smem + L.red);  // red[(parity * RB + q) * T + tid]: per-thread r^T r partials
     const PermT* permt = POOL ? (const PermT*)(smem + L.permt) : (const PermT*)p.permt;
     const double* ZTc = POOL ? (const double*)(smem + L.zt) : p.ZT;
-    const double* Ac = POOL ? (const double*)(smem + L.ai) : p.Ainv;
-    const double* Cbc = POOL ? (const double*)(smem + L.cb) : p.Cb;
+    // HC: training-row tables until the switch (POOL: the shared-memory copy is restaged then)
+    const double* Ac = POOL ? (const double*)(smem + L.ai) : (HC ? p.Ainv_tr : p.Ainv);
+    const double* Cbc = POOL ? (const double*)(smem + L.cb) : (HC ? p.Cb_tr : p.Cb);
     double* sS = (double*)(smem + L.ss) + (size_t)warp * RB * 32;
     // POOL: every per-iteration table is in shared memory (compile-time known: LDS, not generic loads)
     const double* Zs_c = POOL ? (const double*)(smem + L.zs) : p.Zs;
@@ -197,6 +216,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     long long tA = 0, tB = 0, tC = 0, tD = 0, tm = 0;
     __shared__ int ks_sh[2];
     __shared__ double best_sh[2];
+    __shared__ int hc_ph, hc_pu, hc_pat, hc_sw;  // HC: phase (0 ACWB, 1 CWB), phase of the last fit, counter, switch
+    __shared__ double hc_vprev, hc_ntr, hc_nval;
 
     // ---- prologue: pool staging, plan tables, I8 offset f0 = mean(y) --------
     if (POOL) {
@@ -205,8 +226,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         const int nv = (int)((sizeof(PermT) * (size_t)p.permt_cap) / 16);
         for (int a = tid; a < nv; a += T) dst[a] = __ldg(src + a);
         for (int a = tid; a < K * W * d; a += T) ((double*)(smem + L.zt))[a] = __ldg(p.ZT + a);
-        for (int a = tid; a < K * d * d; a += T) ((double*)(smem + L.ai))[a] = __ldg(p.Ainv + a);
-        for (int a = tid; a < K * d * 4; a += T) ((double*)(smem + L.cb))[a] = __ldg(p.Cb + a);
+        const double* ai_src = HC ? p.Ainv_tr : p.Ainv;
+        const double* cb_src = HC ? p.Cb_tr : p.Cb;
+        for (int a = tid; a < K * d * d; a += T) ((double*)(smem + L.ai))[a] = __ldg(ai_src + a);
+        for (int a = tid; a < K * d * 4; a += T) ((double*)(smem + L.cb))[a] = __ldg(cb_src + a);
         for (int a = tid; a < K * d; a += T) ((int32_t*)(smem + L.lw))[a] = __ldg(p.lwin + 2 * a);
     }
     if (POOL) {
@@ -239,8 +262,61 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     for (int a = tid; a < RB * K * d; a += T) agg[a] = 0.0;
     for (int a = tid; a < RB * kPadRows; a += T) r[n * RB + a] = 0.0;
 
+    const int NRB = RB + (ACC ? 1 : 0) + (HC ? 1 : 0);  // per-thread partial slots (+ F^2, + F^2 on D_val)
     double f0[RB];
-    {
+    if (HC) {
+        // f0 = mean of the training targets (Alg. 3 / Alg. 2 line 2 on D_train); F = H = y - f0 on all
+        // rows; fitting columns r = c = y - f0 on the training rows, 0 on the validation rows;
+        // r^T r over the training rows; validation risk of f0 = sum_val (y - f0)^2 / (2 n_val)
+        double sy = 0.0, ntr = 0.0;
+        bool bad = false;
+        for (int i = tid; i < n; i += T) {
+            const uint8_t v_ = p.vmask[i];
+            mk[i] = v_;
+            const double y = p.Y[(size_t)b0 * n + i];
+            bad |= !isfinite(y);
+            Fm[i] = y;
+            if (!v_) { sy += y; ntr += 1.0; }
+        }
+        if (bad) cwb_dev_fail(p.status, CWB_ENONFINITE);
+        sy = warp_sum(sy);
+        ntr = warp_sum(ntr);
+        if (lane == 0) { red[warp] = sy; red[32 + warp] = ntr; }
+        __syncthreads();
+        double st = 0.0, nt = 0.0;
+        for (int w = 0; w < NW; w++) { st += red[w]; nt += red[32 + w]; }
+        f0[0] = f0[RB - 1] = st / nt;
+        double ptr = 0.0, pv = 0.0;
+        for (int i = tid; i < n; i += T) {
+            const double v = Fm[i] - f0[0];
+            Fm[i] = v;
+            Hm[i] = v;
+            const double vm = mk[i] ? 0.0 : v;
+            r[2 * i] = vm;
+            r[2 * i + 1] = vm;
+            ptr += vm * vm;
+            if (mk[i]) pv += v * v;
+        }
+        __syncthreads();  // everyone has read red[] for f0
+        red[(NRB + 0) * T + tid] = ptr;  // rr_0 of both columns -> parity 1
+        red[(NRB + 1) * T + tid] = ptr;
+        pv = warp_sum(pv);
+        __shared__ double s_pv[32];
+        if (lane == 0) s_pv[warp] = pv;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < NW; w++) t += s_pv[w];
+            hc_ntr = nt;
+            hc_nval = (double)n - nt;
+            hc_vprev = t / (2.0 * hc_nval);
+            hc_ph = 0;
+            hc_pu = 0;
+            hc_pat = 0;
+            hc_sw = p.M;
+        }
+        __syncthreads();
+    } else {
         double part[RB];
         bool bad = false;
 #pragma unroll
@@ -279,7 +355,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
         __syncthreads();  // everyone has read red[] for f0
 #pragma unroll
-        for (int q = 0; q < RB; q++) red[((ACC ? RB + 1 : RB) + q) * T + tid] = part[q];  // rr_0 -> parity 1
+        for (int q = 0; q < RB; q++) red[(NRB + q) * T + tid] = part[q];  // rr_0 -> parity 1
         if (ACC)  // f = h = g = f0 (Alg. 2 line 2): H = y - f0; r = c = y - f0 already
             for (int i = tid; i < n; i += T) Hm[i] = r[i * RB];
         __syncthreads();
@@ -291,7 +367,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     // per-thread partials of r^T r before the update of iteration m (parity (m+1) & 1).
     // Runs in phase A of iteration mp + 1 on the first warps (least H1 work, lowest issue
     // priority), off the critical path.
-    const int NRB = RB + (ACC ? 1 : 0);  // per-thread partial slots: RB columns (+ F^2 for ACC)
     auto bookkeeping_acc = [&](int mp) {
         // Alg. 2 parameters: theta_g = (1-vt) theta_f + vt theta_h; theta_f = theta_g + nu e_k theta;
         // theta_h += eta e_kcor theta_cor; traces; risk of f = F^T F / (2n) (slot RB, parity mp)
@@ -318,6 +393,32 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             if (p.risk_trace) p.risk_trace[(size_t)mp * p.B + b0] = rf * p.inv2n;
         }
     };
+    auto bookkeeping_hc = [&](int mp) {
+        // Alg. 3: the fit of iteration mp ran in phase hc_pu: 0 -> ACWB bookkeeping of theta_f,
+        // theta_h; 1 -> CWB aggregation theta_f[k] += nu theta.  Traces k, kcor (-1 after the
+        // switch), SSE = rr_mp - delta*; the risk traces are written by the decide step.
+        const double vt = 2.0 / (double)(mp + 2), eta = p.gamma * p.nu / vt;
+        const int k0 = ks_sh[0], k1 = ks_sh[1];
+        const bool accel = hc_pu == 0;
+        double* tf = agg;
+        double* th = agg + K * d;
+        if (accel) {
+            for (int a = lane; a < K * d; a += 32) tf[a] = (1.0 - vt) * tf[a] + vt * th[a];
+            __syncwarp();
+        }
+        if (lane < d) {
+            tf[k0 * d + lane] += p.nu * thall[(k0 * RB + 0) * 32 + lane];
+            if (accel) th[k1 * d + lane] += eta * thall[(k1 * RB + 1) * 32 + lane];
+        }
+        double s0 = 0.0;
+        for (int t = lane; t < T; t += 32) s0 += red[((mp + 1) & 1) * NRB * T + t];
+        const double rr0 = warp_sum(s0);
+        if (lane == 0 && b0 < p.B) {
+            if (p.k_trace) p.k_trace[(size_t)mp * p.B + b0] = k0;
+            if (p.kcor_trace) p.kcor_trace[(size_t)mp * p.B + b0] = accel ? k1 : -1;
+            if (p.sse_trace) p.sse_trace[(size_t)mp * p.B + b0] = rr0 - best_sh[0];
+        }
+    };
     auto bookkeeping = [&](int mp, int q) {
         const int b = b0 + q, kb = ks_sh[q];
         if (lane < d) agg[(q * K + kb) * d + lane] += p.nu * thall[(kb * RB + q) * 32 + lane];
@@ -335,7 +436,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     };
 
     for (int m = 0; m < p.M; m++) {
-        if (ACC) {
+        if (HC) {
+            if (m > 0 && warp == 0) bookkeeping_hc(m - 1);
+        } else if (ACC) {
             if (m > 0 && warp == 0) bookkeeping_acc(m - 1);
         } else if (m > 0 && warp < RB) {
             bookkeeping(m - 1, warp);
@@ -494,7 +597,91 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         __syncthreads();
         if (timed) tm = phase_mark(&tC, tm, true);
         // ---- D / H6: r_i -= zhat[idx_k*(i)], per-thread r^T r partials -------------
-        {
+        if (HC) {
+            // D1: models after iteration m (phase hc_ph): ACWB F = (1-vt) F + vt H - nu b_k (= y - (g + nu b_k)),
+            //     H -= eta b_kcor; CWB F -= nu b_k.  Partials of F^2 on all rows and on D_val.
+            const int parw = m & 1;
+            const bool accel = hc_ph == 0;
+            const IdxT* ik0 = idx + (size_t)ks_sh[0] * n;
+            const IdxT* ik1 = idx + (size_t)ks_sh[1] * n;
+            const double vt = 2.0 / (double)(m + 2), eta = p.gamma * p.nu / vt;
+            const double vt1 = 2.0 / (double)(m + 3), a1 = (double)(m + 2) / (double)(m + 3);
+            double accA = 0.0, accV = 0.0;
+            for (int i = tid; i < n; i += T) {
+                const double bk = zhat[ik0[i]];
+                const double F = Fm[i];
+                double Fn;
+                if (accel) {
+                    const double Hh = Hm[i];
+                    Fn = (1.0 - vt) * F + vt * Hh - bk;
+                    Hm[i] = Hh - eta * zhat[nsp + ik1[i]];
+                } else {
+                    Fn = F - bk;
+                }
+                Fm[i] = Fn;
+                accA = fma(Fn, Fn, accA);
+                if (mk[i]) accV = fma(Fn, Fn, accV);
+            }
+            red[(parw * NRB + RB) * T + tid] = accA;
+            red[(parw * NRB + RB + 1) * T + tid] = accV;
+            __syncthreads();
+            // decide (Alg. 3 line 6): risk traces, patience counter, one-way switch to CWB
+            if (warp == 0) {
+                double sa = 0.0, sv = 0.0;
+                for (int t = lane; t < T; t += 32) {
+                    sa += red[(parw * NRB + RB) * T + t];
+                    sv += red[(parw * NRB + RB + 1) * T + t];
+                }
+                sa = warp_sum(sa);
+                sv = warp_sum(sv);
+                if (lane == 0) {
+                    const double vr = sv / (2.0 * hc_nval);
+                    if (b0 < p.B) {
+                        if (p.risk_trace) p.risk_trace[(size_t)m * p.B + b0] = sa * p.inv2n;
+                        if (p.val_risk_trace) p.val_risk_trace[(size_t)m * p.B + b0] = vr;
+                    }
+                    hc_pu = hc_ph;
+                    if (hc_ph == 0) {
+                        hc_pat = vr > hc_vprev ? hc_pat + 1 : 0;
+                        if (hc_pat >= p.pat0) {
+                            hc_ph = 1;
+                            hc_sw = m + 1;
+                        }
+                    }
+                    hc_vprev = vr;
+                }
+            }
+            __syncthreads();
+            const bool accel1 = hc_ph == 0;
+            if (accel && !accel1) {  // switched: the pool's tables from now on
+                if (POOL) {
+                    for (int a = tid; a < K * d * d; a += T) ((double*)(smem + L.ai))[a] = __ldg(p.Ainv + a);
+                    for (int a = tid; a < K * d * 4; a += T) ((double*)(smem + L.cb))[a] = __ldg(p.Cb + a);
+                } else {
+                    Ac = p.Ainv;
+                    Cbc = p.Cb;
+                }
+            }
+            // D2: fitting columns of iteration m+1.  ACWB: r' = (1-vt1) F + vt1 H, c' = r' + a1 (c - b_kcor),
+            //     zero on D_val; CWB: r' = F on all rows, c' = 0.  Partials of r'^2, c'^2.
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int i = tid; i < n; i += T) {
+                double rn, cn;
+                if (accel1) {
+                    rn = (1.0 - vt1) * Fm[i] + vt1 * Hm[i];
+                    cn = rn + a1 * (r[2 * i + 1] - zhat[nsp + ik1[i]]);
+                    if (mk[i]) { rn = 0.0; cn = 0.0; }
+                } else {
+                    rn = Fm[i];
+                    cn = 0.0;
+                }
+                *reinterpret_cast<double2*>(r + 2 * i) = make_double2(rn, cn);
+                acc0 = fma(rn, rn, acc0);
+                acc1 = fma(cn, cn, acc1);
+            }
+            red[(parw * NRB + 0) * T + tid] = acc0;
+            red[(parw * NRB + 1) * T + tid] = acc1;
+        } else {
             const int parw = m & 1;
             const IdxT* ik0 = idx + (size_t)ks_sh[0] * n;
             const IdxT* ik1 = idx + (size_t)ks_sh[RB - 1] * n;
@@ -551,7 +738,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         __syncthreads();
         if (timed) tm = phase_mark(&tD, tm, true);
     }
-    if (ACC) {
+    if (HC) {
+        if (p.M > 0 && warp == 0) bookkeeping_hc(p.M - 1);
+    } else if (ACC) {
         if (p.M > 0 && warp == 0) bookkeeping_acc(p.M - 1);
     } else if (p.M > 0 && warp < RB) {
         bookkeeping(p.M - 1, warp);
@@ -561,9 +750,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         if (b0 < p.B) {
             for (int a = tid; a < K * d; a += T) {
                 p.agg_out[(size_t)b0 * K * d + a] = agg[a];
-                p.agg2_out[(size_t)b0 * K * d + a] = agg[K * d + a];
+                if (p.agg2_out) p.agg2_out[(size_t)b0 * K * d + a] = agg[K * d + a];
             }
             if (tid == 0 && p.offset_out) p.offset_out[b0] = f0[0];
+            if (HC && tid == 0 && p.switch_iter) p.switch_iter[b0] = hc_sw;
         }
     } else {
 #pragma unroll
@@ -903,9 +1093,9 @@ __global__ void k_fused_pack(const int32_t* __restrict__ plan, const int32_t* __
     }
 }
 
-template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false>
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false, bool HC = false>
 int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
-    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB, ACC>;
+    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB, ACC, HC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -1;
     const int grid = ACC ? fp.B : (fp.B + RB - 1) / RB;
@@ -914,7 +1104,12 @@ int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
 }
 
 template <typename IdxT, typename PermT>
-int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s, bool acc = false) {
+int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s, bool acc = false,
+               bool hc = false) {
+    if (hc) {  // HCWB: the ACWB layout plus F, the validation mask and the phase state
+        if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, true, true>(fp, T, smem, s);
+        return launch_t<IdxT, PermT, 2, false, 512, 1, true, true>(fp, T, smem, s);
+    }
     if (acc) {  // ACWB: two columns of one replication, 512 threads
         if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, true>(fp, T, smem, s);
         return launch_t<IdxT, PermT, 2, false, 512, 1, true>(fp, T, smem, s);
@@ -1103,10 +1298,19 @@ int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
 }
 
 // Shared host path of the fused CWB (acc = false) and ACWB (acc = true) launches.
+struct HcArgs {  // HCWB extras of a fused launch
+    const uint8_t* vmask = nullptr;
+    const double* Ainv_tr = nullptr;
+    const double* Cb_tr = nullptr;
+    int pat0 = 0;
+    double* val_risk_trace = nullptr;
+    int32_t* switch_iter = nullptr;
+};
+
 static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, double nu, double gamma, int32_t M,
                               double* offset_out, double* theta_out, double* theta_h_out, int32_t* k_trace,
                               int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s,
-                              bool* launched) {
+                              bool* launched, const HcArgs* hc = nullptr) {
     *launched = false;
     FusedShape f;
     if (acc) {  // the two columns (r, c) of a replication run as RB = 2 in a 512-thread CTA
@@ -1115,7 +1319,8 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
         f.T = 512;
         f.permt_bytes = 16 * (c->n + kPadRows) <= 65535 ? 2 : 4;
         f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
-        if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, 2, f.T / 32, false, 0, 0, c->idx_bytes, true)
+        if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, 2, f.T / 32, false, 0, 0, c->idx_bytes, true,
+                       hc != nullptr)
                 .total > kMaxSmem)
             return CWB_OK;
     } else if (!fused_shape(c, B, &f)) {
@@ -1134,11 +1339,14 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
     const size_t pbytes = ((size_t)(c->permt_entries + kSlackEntries) * f.permt_bytes + 15) / 16 * 16;  // < plan_cap
     f.pool = false;
     const int nm = c->plan_multi;
-    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, 0, c->idx_bytes, acc).total;
+    const bool hcm = hc != nullptr;
+    f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, 0, c->idx_bytes, acc,
+                        hcm).total;
     if (f.smem > lim) return CWB_OK;
     int ztab = 0;
     {   // POOL: schedule, B tables, Zs / zj0 and the index vectors all in shared memory, or none
-        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, 3, c->idx_bytes, acc);
+        SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, 3, c->idx_bytes, acc,
+                      hcm);
         if (L1.total <= lim) {
             f.pool = true;
             ztab = 3;
@@ -1158,11 +1366,17 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
     fp.k_trace = k_trace; fp.kcor_trace = kcor_trace; fp.sse_trace = sse_trace; fp.risk_trace = risk_trace;
     fp.timing = c->timing;
     fp.status = c->d_status;
+    fp.vmask = nullptr; fp.Ainv_tr = nullptr; fp.Cb_tr = nullptr; fp.pat0 = 0;
+    fp.val_risk_trace = nullptr; fp.switch_iter = nullptr;
+    if (hcm) {
+        fp.vmask = hc->vmask; fp.Ainv_tr = hc->Ainv_tr; fp.Cb_tr = hc->Cb_tr; fp.pat0 = hc->pat0;
+        fp.val_risk_trace = hc->val_risk_trace; fp.switch_iter = hc->switch_iter;
+    }
     const bool i8 = c->idx_bytes == 1, p16 = f.permt_bytes == 2;
-    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
-    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
-    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
-    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc);
+    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
+    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
+    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
+    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
     if (rc) return cwb_set_error(c, CWB_ECUDA, "fused kernel: cannot set shared memory size");
     c->launches++;
     c->fused_smem = f.smem;
@@ -1184,4 +1398,16 @@ int cwb_train_acwb_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, doub
                          bool* launched) {
     return train_fused_common(c, true, Y, B, nu, gamma, M, offset_out, theta_f_out, theta_h_out, k_trace,
                               kcor_trace, sse_trace, risk_trace, s, launched);
+}
+
+int cwb_train_hcwb_fused(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_mask, const double* Ainv_tr,
+                         const double* Cb_tr, double nu, double gamma, int32_t pat0, int32_t M, double* offset_out,
+                         double* theta_f_out, int32_t* k_trace, int32_t* kcor_trace, double* sse_trace,
+                         double* risk_trace, double* val_risk_trace, int32_t* switch_iter, cudaStream_t s,
+                         bool* launched) {
+    HcArgs h;
+    h.vmask = val_mask; h.Ainv_tr = Ainv_tr; h.Cb_tr = Cb_tr; h.pat0 = pat0;
+    h.val_risk_trace = val_risk_trace; h.switch_iter = switch_iter;
+    return train_fused_common(c, true, Y, B, nu, gamma, M, offset_out, theta_f_out, nullptr, k_trace, kcor_trace,
+                              sse_trace, risk_trace, s, launched, &h);
 }

@@ -522,8 +522,9 @@ __global__ void k_count_masked(const IdxT* __restrict__ idx, const uint8_t* __re
 
 // (G + lambda D)^-1 for a given lambda (one warp per learner): the cached inverse of the
 // training-row learners, with the lambda calibrated on all rows (HCWB readings)
+// (Cb_out != NULL: also the band of C, C C^T = G + 2 lambda D, as k_lambda's selection factor)
 __global__ void k_inverse_fixed(const double* __restrict__ Gall, const double* __restrict__ lambda, int d,
-                                double* __restrict__ Ainv_out, int* status) {
+                                double* __restrict__ Ainv_out, int* status, double* __restrict__ Cb_out = nullptr) {
     __shared__ double Gs[CWB_MAX_D][DS], Dm[CWB_MAX_D][DS], Xs[CWB_MAX_D][DS];
     __shared__ double Lb[(CWB_MAX_D + 4) * 4], inv[CWB_MAX_D];
     __shared__ bool s_ok;
@@ -545,6 +546,17 @@ __global__ void k_inverse_fixed(const double* __restrict__ Gall, const double* _
     __syncwarp();
     if (i < d)
         for (int c = 0; c < d; c++) Ainv_out[((size_t)k * d + i) * d + c] = 0.5 * (Xs[i][c] + Xs[c][i]);
+    if (!Cb_out) return;
+    __syncwarp();
+    __shared__ bool s_ok2;
+    band_factor(2.0 * lambda[k], d, Gs, Dm, Lb, inv, &s_ok2);
+    if (!s_ok2) {
+        if (i == 0) cwb_dev_fail(status, CWB_ECALIB);
+        return;
+    }
+    if (i < d)
+        for (int q = 0; q < 4; q++)  // Cb[j][q] = C[j+q][j]
+            Cb_out[((size_t)k * d + i) * 4 + q] = (q <= BW && i + q < d) ? Lb[(i + q) * 4 + q] : 0.0;
 }
 
 }  // namespace
@@ -633,7 +645,7 @@ int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
 
 // HCWB training-row tables: G_tr = Zb^T diag(cnt_tr) Zb and (G_tr + lambda D)^-1
 int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, double* G_tr, double* Ainv_tr,
-                           cudaStream_t s) {
+                           cudaStream_t s, double* Cb_tr) {
     const int K = c->K, ns = c->n_star, d = c->d;
     cudaMemsetAsync(cnt_tr, 0, sizeof(uint32_t) * (size_t)K * ns, s);
     const int gx = (int)std::min<int64_t>(64, (c->n + 1023) / 1024);
@@ -645,7 +657,7 @@ int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, do
         k_count_masked<uint16_t><<<dim3(gx, K), 1024, smem, s>>>((const uint16_t*)c->idx, mask, c->n, ns, cnt_tr,
                                                                  c->d_status);
     k_gram<<<K, 256, 0, s>>>(c->Zb, cnt_tr, ns, d, c->lwin, G_tr, c->d_status);
-    k_inverse_fixed<<<K, 32, 0, s>>>(G_tr, c->lambda, d, Ainv_tr, c->d_status);
+    k_inverse_fixed<<<K, 32, 0, s>>>(G_tr, c->lambda, d, Ainv_tr, c->d_status, Cb_tr);
     c->launches += 3;
     return cwb_check_launch(c, "masked pool kernels");
 }

@@ -168,6 +168,11 @@ int cwb_train_acwb_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, doub
 int cwb_train_acwb_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double gamma, int32_t M,
                            double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
                            int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_train_hcwb_fused(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_mask, const double* Ainv_tr,
+                         const double* Cb_tr, double nu, double gamma, int32_t pat0, int32_t M, double* offset_out,
+                         double* theta_f_out, int32_t* k_trace, int32_t* kcor_trace, double* sse_trace,
+                         double* risk_trace, double* val_risk_trace, int32_t* switch_iter, cudaStream_t s,
+                         bool* launched);
 int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_mask, double nu, double gamma,
                            int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
                            int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
@@ -176,7 +181,7 @@ int cwb_train_bernoulli_general(cwb_ctx* c, const double* Y, int32_t B, double n
                                 double* offset_out, double* theta_agg_out, int32_t* k_trace,
                                 double* sse_trace, double* risk_trace, cudaStream_t s);
 int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, double* G_tr, double* Ainv_tr,
-                           cudaStream_t s);
+                           cudaStream_t s, double* Cb_tr = nullptr);
 int cwb_find_best_general(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out,
                           double* theta_out, double* sse_out, cudaStream_t s);
 int cwb_train_rows(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,

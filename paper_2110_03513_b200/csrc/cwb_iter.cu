@@ -1427,7 +1427,7 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
     // F, H (n x Bq), partials (4 x nblk x Bq), offsets, theta_h (B x K x d), vprev, counts,
     // G_tr, Ainv_tr (K x d x d), cnt_tr (K x n*), phase, pat (ints)
     const size_t dbl = 2 * (size_t)c->n * Bq + 4 * (size_t)nblk * Bq + Bq + (size_t)B * K * d + Bq + 2 +
-                       2 * (size_t)K * d * d;
+                       2 * (size_t)K * d * d + 4 * (size_t)K * d;
     const size_t need = sizeof(double) * dbl + sizeof(uint32_t) * (size_t)K * ns + 2 * sizeof(int32_t) * Bq;
     if (w.acwb_bytes < need) {
         cwb_release(w.acwb, s);
@@ -1446,11 +1446,20 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
     double* cnt = vprev + Bq;
     double* G_tr = cnt + 2;
     double* Ainv_tr = G_tr + (size_t)K * d * d;
-    uint32_t* cnt_tr = (uint32_t*)(Ainv_tr + (size_t)K * d * d);
+    double* Cb_tr = Ainv_tr + (size_t)K * d * d;
+    uint32_t* cnt_tr = (uint32_t*)(Cb_tr + (size_t)K * d * 4);
     int32_t* phase = (int32_t*)(cnt_tr + (size_t)K * ns);
     int32_t* pat = phase + Bq;
-    rc = cwb_launch_masked_pool(c, val_mask, cnt_tr, G_tr, Ainv_tr, s);
+    rc = cwb_launch_masked_pool(c, val_mask, cnt_tr, G_tr, Ainv_tr, s, Cb_tr);
     if (rc) return rc;
+    if (c->path != 2) {  // the whole run in one persistent kernel when it fits (cwb_fused.cu, HC mode)
+        bool launched = false;
+        rc = cwb_train_hcwb_fused(c, Y, B, val_mask, Ainv_tr, Cb_tr, nu, gamma, pat0, M, offset_out, theta_f_out,
+                                  k_trace, kcor_trace, sse_trace, risk_trace, val_risk_trace, switch_iter, s,
+                                  &launched);
+        if (rc || launched) return rc;
+        if (c->path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: fused path does not fit");
+    }
     k_mask_count<<<1, 1024, 0, s>>>(val_mask, c->n, cnt);
     cudaMemsetAsync(phase, 0, sizeof(int32_t) * 2 * Bq, s);
     // f0 = mean of the training targets (Alg. 2 line 2 on D_train); rr = sum over training rows

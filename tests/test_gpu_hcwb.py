@@ -38,7 +38,7 @@ def first_divergence(g, o, gap, sse):
     return first
 
 
-def check(name, reps, nu=None, gamma=0.037, pat0=5, M=None, frac=0.3):
+def check(name, reps, nu=None, gamma=0.037, pat0=5, M=None, frac=0.3, path=0):
     ds = S.make(name, reps=reps)
     c = ds.cfg
     nu = c.nu if nu is None else nu
@@ -47,6 +47,7 @@ def check(name, reps, nu=None, gamma=0.037, pat0=5, M=None, frac=0.3):
     po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
     ro = po.train_hcwb(ds.Y, vm, nu=nu, gamma=gamma, pat0=pat0, M=M, threads=8)
     pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    pg.set_path(path)
     out = pg.train_hcwb(dev(ds.Y), dev(vm, torch.uint8), nu=nu, gamma=gamma, pat0=pat0, M=M)
     pg.status()
     g = {k: host(v) for k, v in out.items()}
@@ -74,15 +75,39 @@ def check(name, reps, nu=None, gamma=0.037, pat0=5, M=None, frac=0.3):
     return g, ro
 
 
-def test_hcwb_parity_r1_switches():
+@pytest.mark.parametrize("path", [1, 2])  # 1: fused persistent kernel (HC mode), 2: per-iteration kernels
+def test_hcwb_parity_r1_switches(path):
     # strong momentum so that replications switch at different iterations inside one launch
-    g, ro = check("R1", list(range(24)), nu=0.1, gamma=0.5, pat0=3, M=200)
+    g, ro = check("R1", list(range(24)), nu=0.1, gamma=0.5, pat0=3, M=200, path=path)
     assert (ro.switch_iter < 200).sum() >= 12 and len(set(ro.switch_iter.tolist())) > 3
 
 
-@pytest.mark.parametrize("name,reps", [("R0", range(8)), ("R1", range(16)), ("R2", [0, 5, 1000])])
-def test_hcwb_parity_paper_defaults(name, reps):
-    check(name, list(reps))
+@pytest.mark.parametrize("name,reps,path", [("R0", range(8), 1), ("R0", range(8), 2), ("R1", range(16), 1),
+                                            ("R1", range(16), 2), ("R2", [0, 5, 1000], 0)])
+def test_hcwb_parity_paper_defaults(name, reps, path):
+    check(name, list(reps), path=path)
+
+
+def test_hcwb_fused_equals_general_all_replications():
+    # R1 at its full B = 256: the fused HC kernel and the per-iteration kernels agree
+    ds = S.make("R1")
+    c = ds.cfg
+    vm = dev(S.validation_mask(c.n), torch.uint8)
+    res = []
+    for path in (1, 2):
+        pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+        pg.set_path(path)
+        out = pg.train_hcwb(dev(ds.Y), vm, M=c.M)
+        pg.status()
+        res.append({k: host(v) for k, v in out.items()})
+        pg.close()
+    a, b = res
+    same = (a["k_trace"] == b["k_trace"]).all(0) & (a["switch_iter"] == b["switch_iter"])
+    assert same.mean() >= 0.95
+    ok, e = close(a["theta_f"][same], b["theta_f"][same], RTOL, scale=np.abs(b["theta_f"]).max())
+    assert ok, e
+    ok, e = close(a["val_risk_trace"][:, same], b["val_risk_trace"][:, same], RTOL)
+    assert ok, e
 
 
 def test_hcwb_errors():
