@@ -52,6 +52,7 @@ struct cwb_stream_plan {  // streaming binMatVec gather plan (cwb_stream.cu), bu
     uint16_t* dest = nullptr;   // per group and lane: kl * n* + l, 0xffff none
     int2* isize = nullptr;      // per item (learner group, chunk): {groups, blocks}
     int2* ibase = nullptr;      // per item: first group, first block
+    uint32_t* wst = nullptr;    // per item: first block of each of the 32 kernel warps, + end
     double* part = nullptr;     // per-CTA bin sums
     size_t part_bytes = 0;
 };

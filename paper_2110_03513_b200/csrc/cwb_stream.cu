@@ -38,8 +38,10 @@ namespace {
 
 constexpr int kC = 8176;        // rows per chunk: byte offsets of rows and pad rows (C..C+15) fit u16
 constexpr int kPad = 16;        // zero padding rows after the chunk
-constexpr int kUBudget = 4096;  // doubles of bin sums per CTA (32 KB): Ks * n* <= kUBudget
-constexpr int kStreamT = 512;   // threads of the stream kernel (two CTAs per SM)
+constexpr int kUBudget = 6144;  // doubles of bin sums per CTA (48 KB): Ks * n* <= kUBudget
+constexpr int kStreamT = 1024;  // threads of the stream kernel (one CTA per SM)
+constexpr int kNWK = kStreamT / 32;  // kernel warps: the plan deals groups to them
+constexpr int kStage = 4;        // entry blocks per register stage (two stages in flight per warp)
 
 // ---------------------------------------------------------------- plan kernels
 // bin counts of every (learner, chunk): cnt[(k * nch + c) * ns + l]
@@ -134,6 +136,28 @@ __global__ void k_sp_scan(const int2* __restrict__ isize, int nitems, int2* __re
 // warp's 32 bins are exhausted, rounded up to a multiple of 4 with padding steps.
 // EMIT = false: count the steps (isize[item].y += blocks); EMIT = true: write entries,
 // group table and destinations at the scanned offsets.
+// kernel warp of group g (the stream kernel deals the groups of an item to its kNWK warps in snake
+// order: round g / kNWK left to right when even, right to left when odd) and the warp-major order key
+__device__ __forceinline__ int gwarp(int g) {
+    const int r = g / kNWK, x = g - r * kNWK;
+    return (r & 1) ? kNWK - 1 - x : x;
+}
+__device__ __forceinline__ uint32_t gorder(int g) { return ((uint32_t)gwarp(g) << 16) | (uint32_t)(g / kNWK); }
+
+// first entry block of every kernel warp's stream in item `item` (+ the item's end)
+__global__ void k_sp_wstart(const int2* __restrict__ isize, const int2* __restrict__ ibase,
+                            const uint32_t* __restrict__ gsteps, int NTP, uint32_t* __restrict__ wst) {
+    const int item = blockIdx.x, lane = threadIdx.x;  // lane = kernel warp
+    const int ng = isize[item].x;
+    const uint32_t* gs = gsteps + (size_t)item * (NTP / 32);
+    if (lane < kNWK) {
+        uint32_t part = 0;
+        for (int h = 0; h < ng; h++) part += gwarp(h) < lane ? gs[h] / 4 : 0u;
+        wst[(size_t)item * (kNWK + 1) + lane] = (uint32_t)ibase[item].y + part;
+    }
+    if (lane == 0) wst[(size_t)item * (kNWK + 1) + kNWK] = (uint32_t)(ibase[item].y + isize[item].y);
+}
+
 template <typename PermT, bool EMIT>
 __global__ void __launch_bounds__(512) k_sp_sched(
     const uint32_t* __restrict__ tasks, const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ cst,
@@ -166,11 +190,16 @@ __global__ void __launch_bounds__(512) k_sp_sched(
         for (int x = 0; x < 16; x++) { cc[x] = 0; pos[x] = 0; }
         for (int s = 0; s < rem; s++) cc[((uint32_t)rows[s] - base) & 15]++;
         uint16_t* eg = nullptr;
+        uint32_t nblk_g = 0;
         if (EMIT) {
+            // blocks in warp-major order: the groups of kernel warp 0 (snake-dealt, see gwarp), then of
+            // warp 1, ...; within a warp in dealing order
+            const uint32_t og = gorder(g);
             uint32_t part = 0;
-            for (int h = lane; h < g; h += 32) part += gs[h] / 4;
+            for (int h = lane; h < ng; h += 32) part += gorder(h) < og ? gs[h] / 4 : 0u;
             for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
             const uint32_t bb = (uint32_t)ibase[item].y + part;
+            nblk_g = gs[g] / 4;
             const int gg = ibase[item].x + g;
             if (lane == 0) gtab[gg] = make_uint2(bb, gs[g] / 4);
             dest[(size_t)gg * 32 + lane] = t != 0xffffffffu ? (uint16_t)t : (uint16_t)0xffff;
@@ -178,7 +207,10 @@ __global__ void __launch_bounds__(512) k_sp_sched(
         }
         uint32_t steps = 0;
         while (__any_sync(0xffffffffu, rem > 0) || (steps & 3)) {
-            unsigned fr = 0xffffu;
+            // colours used once (fr2) may take a second lane (a 2-way conflict: one extra wavefront)
+            // rather than leave the lane a padding entry: the entry stream, not the shared-memory pipe,
+            // is the bound of the stream kernel
+            unsigned fr = 0xffffu, fr2 = 0u;
             int pick = -1;
             bool assigned = false;
             for (int r = 0; r < 16; r++) {
@@ -193,11 +225,20 @@ __global__ void __launch_bounds__(512) k_sp_sched(
 #pragma unroll
                     for (int y = 0; y < 16; y++)
                         if (((fr >> y) & 1u) && cc[y] > best) { best = cc[y]; x = y; }
+                    if (x < 0) {
+                        best = 0;
+#pragma unroll
+                        for (int y = 0; y < 16; y++)
+                            if (((fr2 >> y) & 1u) && cc[y] > best) { best = cc[y]; x = y; }
+                    }
                     assigned = true;
                     pick = x;
                 }
                 x = __shfl_sync(hmask, x, hb | win);
-                if (x >= 0) fr &= ~(1u << x);
+                if (x >= 0) {
+                    if ((fr >> x) & 1u) { fr &= ~(1u << x); fr2 |= 1u << x; }
+                    else fr2 &= ~(1u << x);
+                }
             }
             const unsigned np = (~__ballot_sync(0xffffffffu, pick >= 0) >> hb) & 0xffffu;  // lanes padding
             uint16_t v;
@@ -208,12 +249,17 @@ __global__ void __launch_bounds__(512) k_sp_sched(
                 pos[pick] = p + 1;
                 cc[pick]--;
                 rem--;
-            } else {
+            } else {  // padding row of a free colour, else of a colour used once, else any
                 int rank = __popc(np & ((1u << hl) - 1u));
-                unsigned f = fr;
+                const int n1 = __popc(fr), n2 = __popc(fr2);
+                unsigned f = rank < n1 ? fr : (rank < n1 + n2 ? fr2 : 0xffffu);
+                rank = rank < n1 ? rank : (rank < n1 + n2 ? rank - n1 : (rank - n1 - n2) & 15);
                 while (rank--) f &= f - 1u;
                 v = (uint16_t)((kC + (__ffs(f) - 1)) * 8);
             }
+            // bit 0 (free: byte offsets of 8-byte rows) of the first entry of the group's last block of
+            // every lane: the kernel flushes the lane's bin total after that block
+            if (EMIT && (steps >> 2) + 1 == nblk_g && (steps & 3) == 0) v |= 1;
             if (EMIT) eg[(size_t)(steps >> 2) * 128 + (steps & 3)] = v;
             steps++;
         }
@@ -233,14 +279,14 @@ __global__ void __launch_bounds__(512) k_sp_sched(
 // as pieces of kPiece blocks through registers, two pieces ahead of the gathers.  Entries
 // are byte offsets of rows in the staged chunk (LDS [R + UR]).
 constexpr int kPiece = 4;      // entry blocks (256 B) per piece
-constexpr int kMaxG = 128;     // groups per item staged in shared memory (Ks * n* <= 4096)
+constexpr int kMaxG = kUBudget / 32;  // groups per item staged in shared memory (Ks * n* <= kUBudget)
 
 __device__ __forceinline__ double gat(const unsigned char* __restrict__ rb, uint32_t off) {
     return *(const double*)(rb + off);
 }
 __device__ __forceinline__ double gather4(const unsigned char* __restrict__ rb, uint2 v) {
     // fixed order: entries 0, 1, 2, 3 of the block
-    double a = gat(rb, v.x & 0xffff);
+    double a = gat(rb, v.x & 0xfffe);  // bit 0 of entry 0: end-of-group flag
     a += gat(rb, v.x >> 16);
     a += gat(rb, v.y & 0xffff);
     a += gat(rb, v.y >> 16);
@@ -251,30 +297,101 @@ struct Piece {
     uint2 v[kPiece];
 };
 
-__global__ void __launch_bounds__(kStreamT, 2)
+__device__ __forceinline__ uint32_t sm_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            sm_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sm_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(sm_u32(bar))
+                 : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    if (N == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sm_u32(dst)), "l"(src), "n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\n cp.async.wait_all;" ::: "memory");
+}
+
+// One CTA per SM (kStreamT threads).  The chunk of residuals and the group tables of item
+// it + 1 are copied into the second buffer (TMA bulk copy for the chunk, cp.async for the tables)
+// while item it is gathered, so the copies overlap the gathers.
+__global__ void __launch_bounds__(kStreamT, 1)
     k_h1_stream(const double* __restrict__ R, int64_t n, int nch, int Ks, int ns, int nitems, int nslot,
                 const uint2* __restrict__ ent, const uint2* __restrict__ gtab, const uint16_t* __restrict__ dest,
-                const int2* __restrict__ isize, const int2* __restrict__ ibase, double* __restrict__ P,
-                double* __restrict__ rrp, int* status) {
+                const int2* __restrict__ isize, const int2* __restrict__ ibase, const uint32_t* __restrict__ wst,
+                double* __restrict__ P, double* __restrict__ rrp, int* status) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[kStreamT / 32];
-    __shared__ uint2 s_gt[kMaxG];
-    __shared__ __align__(16) uint16_t s_dst[kMaxG * 32];
+    __shared__ __align__(16) uint32_t s_ws[2][kNWK + 4];
+    __shared__ __align__(16) uint16_t s_dst[2][kMaxG * 32];
+    __shared__ __align__(8) uint64_t bars[2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
     const int NU = Ks * ns;
-    double* rs = sm;                      // kC residuals of the chunk, then kPad zero rows
-    const unsigned char* rb = (const unsigned char*)rs;
-    double* U = sm + kC + kPad;           // Ks * ns bin sums
+    // two chunk buffers sm + bf (kC + kPad): kC residuals + kPad zero rows each
+    double* U = sm + 2 * (kC + kPad);                // Ks * ns bin sums
     const int N = gridDim.x, j = blockIdx.x, q = blockIdx.y;
     const int i0 = (int)((int64_t)nitems * j / N), i1 = (int)((int64_t)nitems * (j + 1) / N);
     double* Pj = P + ((size_t)q * N + j) * nslot * NU;
-    for (int a = tid; a < NU; a += blockDim.x) U[a] = 0.0;
-    if (tid < kPad) rs[kC + tid] = 0.0;
     const double* col = R + (size_t)q * n;
-    int cur_lg = i0 / nch, slot = 0, cur_c = -1;
-    for (int item = i0; item < i1; item++) {
-        const int lg = item / nch, c = item - lg * nch;
-        __syncthreads();  // previous item consumed (chunk, group table, bin sums)
+    const bool tma = (((uintptr_t)col) & 15) == 0;   // chunk starts are 16-byte aligned iff the column is
+    for (int a = tid; a < NU; a += blockDim.x) U[a] = 0.0;
+    if (tid < 2 * kPad) sm[(tid / kPad) * (kC + kPad) + kC + (tid % kPad)] = 0.0;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // copies of item it into buffer bf: chunk (TMA, tail row and unaligned columns by plain loads),
+    // group table and destinations (cp.async)
+    auto issue = [&](int it, int bf) {
+        const int lg = it / nch, c = it - lg * nch;
+        const int64_t r0 = (int64_t)c * kC;
+        const int len = (int)min((int64_t)kC, n - r0);
+        double* rs = sm + bf * (kC + kPad);
+        if (tma) {
+            if (tid == 0) {
+                const uint32_t bytes = (uint32_t)((size_t)len * 8) & ~15u;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bars[bf], bytes);
+                if (bytes) bulk_g2s(rs, col + r0, bytes, &bars[bf]);
+                if (len & 1) rs[len - 1] = __ldg(col + r0 + len - 1);
+            }
+        } else {
+            for (int i = tid; i < len; i += blockDim.x) rs[i] = __ldg(col + r0 + i);
+        }
+        const int ng = isize[it].x, gb = ibase[it].x;
+        if (tid < kNWK + 1) cp_async<4>(&s_ws[bf][tid], wst + (size_t)it * (kNWK + 1) + tid);
+        for (int a = tid; a < ng * 4; a += blockDim.x)
+            cp_async<16>((unsigned char*)s_dst[bf] + 16 * a, (const unsigned char*)dest + (size_t)gb * 64 + 16 * a);
+    };
+    int cur_lg = i0 / nch, slot = 0;
+    uint2 va[kStage];   // entry blocks of the warp's current position (prefetched across items)
+    bool pre = false;
+    if (i0 < i1) issue(i0, 0);
+    for (int it = i0; it < i1; it++) {
+        const int lg = it / nch, c = it - lg * nch;
+        const int bf = (it - i0) & 1;
+        cp_async_commit_wait_all();                          // this thread's table copies of item it
+        if (tma) mbar_wait(&bars[bf], (uint32_t)(((it - i0) >> 1) & 1));
+        __syncthreads();  // item it's data visible; item it - 1 consumed (buffer bf ^ 1 is free)
         if (lg != cur_lg) {  // flush the bin sums of the previous learner group
             for (int a = tid; a < NU; a += blockDim.x) {
                 Pj[(size_t)slot * NU + a] = U[a];
@@ -282,88 +399,74 @@ __global__ void __launch_bounds__(kStreamT, 2)
             }
             slot++;
             cur_lg = lg;
+            __syncthreads();
         }
-        const int2 isz = isize[item], ib = ibase[item];
-        const int ng = isz.x, gb = ib.x;
-        for (int g = tid; g < ng; g += blockDim.x) s_gt[g] = gtab[gb + g];
-        for (int a = tid; a < ng * 16; a += blockDim.x) ((uint32_t*)s_dst)[a] = ((const uint32_t*)dest)[(size_t)gb * 16 + a];
-        if (c != cur_c) {
-            const int64_t r0 = (int64_t)c * kC;
-            const int len = (int)min((int64_t)kC, n - r0);
-            double sq = 0.0;  // r^T r of the chunk (I8 / the SSE identity), by the items of learner group 0
-            if ((((uintptr_t)(col + r0)) & 15) == 0) {
-                const int h = len >> 1;
-                const double2* src = (const double2*)(col + r0);
-                for (int i = tid; i < h; i += blockDim.x) {
-                    const double2 v = __ldg(src + i);
-                    ((double2*)rs)[i] = v;
-                    sq += v.x * v.x;
-                    sq += v.y * v.y;
-                }
-                if ((len & 1) && tid == 0) {
-                    const double v = __ldg(col + r0 + len - 1);
-                    rs[len - 1] = v;
-                    sq += v * v;
-                }
-            } else {
-                for (int i = tid; i < len; i += blockDim.x) {
-                    const double v = __ldg(col + r0 + i);
-                    rs[i] = v;
-                    sq += v * v;
-                }
-            }
-            if (lg == 0) {  // block-uniform: one writer per chunk, fixed order
-                if (!isfinite(sq)) cwb_dev_fail(status, CWB_ENONFINITE);
-                sq = warp_sum(sq);
-                if (lane == 0) red[w] = sq;
-                __syncthreads();
-                if (tid == 0) {
-                    double t = 0.0;
-                    for (int u = 0; u < nw; u++) t += red[u];
-                    rrp[(size_t)q * nch + c] = t;
-                }
-            }
-            cur_c = c;
+        if (it + 1 < i1) issue(it + 1, bf ^ 1);
+        // this warp's block range in item it + 1, read early: its first blocks are loaded before the
+        // end-of-item barrier so that their latency overlaps the wait
+        uint32_t nws = 0, nwe = 0;
+        if (it + 1 < i1) {
+            nws = __ldg(wst + (size_t)(it + 1) * (kNWK + 1) + w);
+            nwe = __ldg(wst + (size_t)(it + 1) * (kNWK + 1) + w + 1);
         }
-        __syncthreads();
-        // this warp's pieces (group g, first block b0), groups w, w + nw, ...; loads two pieces ahead
-        int lg_ = w, lb_ = 0;  // next piece to load
-        auto load = [&](Piece& pc) {
-            if (lg_ < ng) {
-                const uint2 gt = s_gt[lg_];
-                const uint2* e = ent + ((size_t)gt.x + lb_) * 32 + lane;
-                const int nb = (int)gt.y - lb_;
+        const double* rs = sm + bf * (kC + kPad);
+        const unsigned char* rb = (const unsigned char*)rs;
+        if (lg == 0) {  // r^T r of the chunk (I8 / the SSE identity): one writer per chunk, fixed order
+            const int len = (int)min((int64_t)kC, n - (int64_t)c * kC);
+            double sq = 0.0;
+            for (int i = tid; i < len; i += blockDim.x) sq = fma(rs[i], rs[i], sq);
+            if (!isfinite(sq)) cwb_dev_fail(status, CWB_ENONFINITE);
+            sq = warp_sum(sq);
+            if (lane == 0) red[w] = sq;
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int u = 0; u < nw; u++) t += red[u];
+                rrp[(size_t)q * nch + c] = t;
+            }
+        }
+        // this warp's entry blocks [ws[w], ws[w+1]) (warp-major plan layout): its groups in dealing order,
+        // bit 0 of a lane's first entry marks the last block of a group; loads run 4 blocks ahead
+        const uint16_t* dss = s_dst[bf];
+        const uint32_t bend = s_ws[bf][w + 1];
+        uint32_t blk = s_ws[bf][w];
+        auto gsn = [&](int jr) { return jr * kNWK + ((jr & 1) ? kNWK - 1 - w : w); };
+        int jr = 0, g = gsn(0);
+        double a0 = 0.0, a1 = 0.0;
+        auto loadS = [&](uint2 (&v)[kStage], uint32_t b) {
 #pragma unroll
-                for (int u = 0; u < kPiece; u++)
-                    if (u < nb) pc.v[u] = __ldg(e + u * 32);
-                lb_ += kPiece;
-                if (lb_ >= (int)gt.y) { lg_ += nw; lb_ = 0; }
+            for (int u = 0; u < kStage; u++)
+                if (b + u < bend) v[u] = __ldg(ent + (size_t)(b + u) * 32 + lane);
+        };
+        auto procS = [&](const uint2 (&v)[kStage], uint32_t b) {
+#pragma unroll
+            for (int u = 0; u < kStage; u++) {
+                if (b + u >= bend) break;
+                if (u & 1) a1 += gather4(rb, v[u]);
+                else a0 += gather4(rb, v[u]);
+                if (v[u].x & 1u) {  // end of group (warp-uniform): the lane's bin total
+                    const uint16_t dst = dss[g * 32 + lane];
+                    if (dst != 0xffff) U[dst] += a0 + a1;
+                    a0 = a1 = 0.0;
+                    g = gsn(++jr);
+                }
             }
         };
-        Piece p0, p1, p2;
-        load(p0);
-        load(p1);
-        int cg = w, cb = 0;
-        double a0 = 0.0, a1 = 0.0;
-        while (cg < ng) {
-            load(p2);
-            const uint2 gt = s_gt[cg];
-            const int nb = (int)gt.y - cb;
+        uint2 vb[kStage];
+        if (!pre) loadS(va, blk);
+        for (; blk < bend; blk += 2 * kStage) {
+            loadS(vb, blk + kStage);
+            procS(va, blk);
+            if (blk + kStage >= bend) break;
+            loadS(va, blk + 2 * kStage);
+            procS(vb, blk + kStage);
+        }
+        pre = false;
+        if (it + 1 < i1) {  // first blocks of item it + 1
 #pragma unroll
-            for (int u = 0; u < kPiece; u += 2) {
-                if (u < nb) a0 += gather4(rb, p0.v[u]);
-                if (u + 1 < nb) a1 += gather4(rb, p0.v[u + 1]);
-            }
-            cb += kPiece;
-            if (cb >= (int)gt.y) {  // group complete: lane's bin total
-                const uint16_t dst = s_dst[cg * 32 + lane];
-                if (dst != 0xffff) U[dst] += a0 + a1;
-                a0 = a1 = 0.0;
-                cg += nw;
-                cb = 0;
-            }
-            p0 = p1;
-            p1 = p2;
+            for (int u = 0; u < kStage; u++)
+                if (nws + u < nwe) va[u] = __ldg(ent + (size_t)(nws + u) * 32 + lane);
+            pre = true;
         }
     }
     __syncthreads();
@@ -387,24 +490,35 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     double* __restrict__ sse_out) {
     extern __shared__ double u[];  // [ns][B]
     __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4], V[CWB_MAX_D][4];
-    __shared__ int s_j[2 * 148 + 1], s_slot[2 * 148 + 1], s_nj;
+    __shared__ int s_j[148 + 1], s_slot[148 + 1], s_nj;
     __shared__ bool last;
     const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
     const int lg = k / Ks, NU = Ks * ns, a0 = (k - lg * Ks) * ns;
-    // the CTAs whose item range meets [lg nch, (lg+1) nch), and their slot for lg
-    if (tid == 0) {
+    // the CTAs whose item range meets [lg nch, (lg+1) nch), and their slot for lg (warp 0, a lane per CTA)
+    if (w == 0) {
         const int64_t it0 = (int64_t)lg * nch, it1 = it0 + nch;
-        int jlo = (int)(it0 * N / nitems), m = 0;
+        int jlo = (int)(it0 * N / nitems);
         while (jlo > 0 && (int64_t)nitems * jlo / N > it0) jlo--;
-        for (int jj = jlo; jj < N && m < 2 * 148 + 1; jj++) {
-            const int64_t b0 = (int64_t)nitems * jj / N, b1 = (int64_t)nitems * (jj + 1) / N;
-            if (b0 >= it1) break;
-            if (b1 <= it0 || b0 == b1) continue;
-            s_j[m] = jj;
-            s_slot[m] = lg - (int)(b0 / nch);
-            m++;
+        int m = 0;
+        for (int base = jlo;; base += 32) {
+            const int jj = base + lane;
+            int64_t b0 = 0, b1 = 0;
+            if (jj < N) {
+                b0 = (int64_t)nitems * jj / N;
+                b1 = (int64_t)nitems * (jj + 1) / N;
+            }
+            const bool ov = jj < N && b0 < it1 && b1 > it0 && b0 != b1;
+            const bool stop = jj >= N || b0 >= it1;
+            const unsigned bal = __ballot_sync(0xffffffffu, ov);
+            if (ov && m + __popc(bal & ((1u << lane) - 1u)) < 148 + 1) {
+                const int pos = m + __popc(bal & ((1u << lane) - 1u));
+                s_j[pos] = jj;
+                s_slot[pos] = lg - (int)(b0 / nch);
+            }
+            m = min(148 + 1, m + __popc(bal));
+            if (__any_sync(0xffffffffu, stop)) break;
         }
-        s_nj = m;
+        if (lane == 0) s_nj = m;
     }
     __syncthreads();
     const int nj = s_nj;
@@ -501,7 +615,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
 void cwb_stream_release(cwb_ctx* c, cudaStream_t s) {
     cwb_stream_plan& p = c->sp;
     cwb_release(p.ent, s); cwb_release(p.gtab, s); cwb_release(p.dest, s); cwb_release(p.isize, s);
-    cwb_release(p.ibase, s); cwb_release(p.part, s);
+    cwb_release(p.ibase, s); cwb_release(p.part, s); cwb_release(p.wst, s);
     p = cwb_stream_plan();
 }
 
@@ -514,7 +628,7 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
     if (ns > kUBudget) return CWB_EUNSUPPORTED;  // <= kMaxG groups of 32 tasks per item
     // learner group size: bin sums within the shared-memory budget, and at least 2 x 148 items
     const int nch0 = (int)((n + kC - 1) / kC);
-    const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / (2 * 148))));
+    const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / 148)));
     if ((int64_t)Ks * ns > 0xfffe) return CWB_EUNSUPPORTED;
     const int nch = (int)((n + kC - 1) / kC), nlg = (K + Ks - 1) / Ks, nitems = nlg * nch;
     int NTP = 32;
@@ -571,6 +685,7 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
     ok = cwb_alloc((void**)&p.ent, (size_t)std::max(1ll, nbt) * 256, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&p.gtab, sizeof(uint2) * (size_t)std::max(1ll, ngt), s) == cudaSuccess;
     ok &= cwb_alloc((void**)&p.dest, sizeof(uint16_t) * 32 * (size_t)std::max(1ll, ngt), s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&p.wst, sizeof(uint32_t) * (kNWK + 1) * (size_t)nitems, s) == cudaSuccess;
     if (!ok) {
         cleanup(); cwb_release(isize, s); cwb_release(ibase, s);
         cwb_stream_release(c, s);
@@ -582,7 +697,8 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
     else
         k_sp_sched<uint32_t, true><<<nitems, 512, 0, s>>>(tasks, cnt, cst, (const uint32_t*)c->perm, n, ns, nch, Ks,
                                                           NTP, isize, ibase, gsteps, (uint16_t*)p.ent, p.gtab, p.dest);
-    c->launches += 1;
+    k_sp_wstart<<<nitems, 32, 0, s>>>(isize, ibase, gsteps, NTP, p.wst);  // kNWK <= 32
+    c->launches += 2;
     cleanup();
     p.isize = isize;
     p.ibase = ibase;
@@ -606,7 +722,7 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
     if (rc) return rc;
     cwb_stream_plan& p = c->sp;
     const int K = c->K, ns = c->n_star, d = c->d;
-    const int N = std::max(1, std::min(p.nitems, 2 * 148));
+    const int N = std::max(1, std::min(p.nitems, 148));
     // learner groups met by one CTA's item range
     const int per = (p.nitems + N - 1) / N;
     const int nslot = std::min(p.nlg, (per + p.nch - 1) / p.nch + 1);
@@ -625,10 +741,10 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
     double* th = rrp + 4 * p.nch;
     double* de = th + (size_t)K * d * 4;
     unsigned* ticket = (unsigned*)(p.part + part + extra - 1);
-    const size_t smem = sizeof(double) * ((size_t)kC + kPad + (size_t)p.Ks * ns);
+    const size_t smem = sizeof(double) * (2 * ((size_t)kC + kPad) + (size_t)p.Ks * ns);
     cudaFuncSetAttribute(k_h1_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_h1_stream<<<dim3(N, B), kStreamT, smem, s>>>(R, c->n, p.nch, p.Ks, ns, p.nitems, nslot, (const uint2*)p.ent,
-                                                    p.gtab, p.dest, p.isize, p.ibase, p.part, rrp, c->d_status);
+                                                    p.gtab, p.dest, p.isize, p.ibase, p.wst, p.part, rrp, c->d_status);
     const size_t fsm = sizeof(double) * (size_t)ns * B;
     cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
     k_fit_narrow<<<K, 1024, fsm, s>>>(p.part, K, ns, p.Ks, p.nch, p.nitems, N, nslot, B, d, c->W, c->ZT, c->lwin,
