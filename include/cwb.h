@@ -203,10 +203,11 @@ int cwb_train_acwb(cwb_ctx* ctx, const double* Y, int32_t B, double nu, double g
  * cwb_train, except: offset_out[b] = log(p / (1 - p)) with p = mean(y_b) (Alg. 1 line 2,
  * argmin_c R_emp(c)); the pseudo residuals are r = y - 1 / (1 + exp(-f)), fitted
  * by the base learners with the L2 criterion as for the L2 loss (sse_trace = SSE of that
- * fit); risk_trace[m][b] = mean L(y, f) after the update of iteration m.  General path
- * (per-iteration kernels).  Errors: CWB_EINVAL (arguments; a target value that is not 0
+ * fit); risk_trace[m][b] = mean L(y, f) after the update of iteration m.  The persistent
+ * kernel of cwb_train when it fits (y and f in shared memory), else the per-iteration kernels
+ * (cwb_set_path selects).  Errors: CWB_EINVAL (arguments; a target value that is not 0
  * or 1, reported by cwb_status), CWB_EDEGENERATE (mean(y_b) is 0 or 1, cwb_status),
- * CWB_ENONFINITE, CWB_EUNSUPPORTED (row-sharded context, cwb_set_path(1)). */
+ * CWB_ENONFINITE, CWB_EUNSUPPORTED (row-sharded context, unbinned pool). */
 int cwb_train_bernoulli(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
                         double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
                         cudaStream_t stream);

@@ -351,7 +351,14 @@ int cwb_train_bernoulli(cwb_ctx* c, const double* Y, int32_t B, double nu, int32
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: row-sharded context");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: unbinned pool (cwb_train only)");
-    if (c->path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: general path only");
+    if (c->path != 2) {
+        bool launched = false;
+        int rc = cwb_train_bernoulli_fused(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace,
+                                           s, &launched);
+        if (rc || launched) return rc;
+        if (c->path == 1)
+            return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: fused path needs more shared memory than a CTA has");
+    }
     return cwb_train_bernoulli_general(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace, s);
 }
 

@@ -84,9 +84,10 @@ struct SmemLayout {
     size_t r, U, delta, th, ss, zhat, agg, pc, red, permt, zt, ai, cb, lw, zs, zj, ix, total;
     size_t hh;  // ACC: H = y - h (momentum model), n doubles
     size_t ff, mk;  // HC: F = y - f (primary model, all rows), n doubles; validation mask, n bytes
+    size_t by, bf;  // BERN: targets y and fit f, n x RB doubles each
     __host__ __device__ SmemLayout(int n, int K, int nsp, int d, int W, int n_multi, int RB, int NW, bool pool,
                                    size_t permt_bytes, int ztab, int idx_bytes = 1, bool acc = false,
-                                   bool hc = false) {
+                                   bool hc = false, bool bern = false) {
         size_t o = 0;
         r = o; o = align16(o + sizeof(double) * RB * (size_t)(n + kPadRows));  // r[n..n+15] = 0: padding rows
         U = o; o = align16(o + sizeof(double) * RB * ((size_t)K * nsp + W));  // +W: window overrun pad
@@ -96,10 +97,13 @@ struct SmemLayout {
         zhat = o; o = align16(o + sizeof(double) * RB * (size_t)nsp);
         agg = o; o = align16(o + sizeof(double) * RB * (size_t)K * d);
         pc = o; o = align16(o + sizeof(double) * RB * (n_multi > 0 ? n_multi : 1));
-        red = o; o = align16(o + sizeof(double) * 2 * (RB + (acc ? 1 : 0) + (hc ? 1 : 0)) * (size_t)NW * 32);
+        red = o; o = align16(o + sizeof(double) * 2 * (RB + (acc ? 1 : 0) + (hc ? 1 : 0) + (bern ? RB : 0)) *
+                                 (size_t)NW * 32);
         hh = o; if (acc) o = align16(o + sizeof(double) * (size_t)n);
         ff = o; if (hc) o = align16(o + sizeof(double) * (size_t)n);
         mk = o; if (hc) o = align16(o + (size_t)n);
+        by = o; if (bern) o = align16(o + sizeof(double) * RB * (size_t)n);
+        bf = o; if (bern) o = align16(o + sizeof(double) * RB * (size_t)n);
         permt = o; if (pool) o = align16(o + permt_bytes);
         zt = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * W * d);
         ai = o; if (pool) o = align16(o + sizeof(double) * (size_t)K * d * d);
@@ -176,19 +180,25 @@ __device__ __forceinline__ long long phase_mark(long long* acc, long long t0, bo
 // validation-risk patience counter is below pat0, then CWB on all rows from the primary model;
 // F = y - f in shared memory, fitting columns zero on validation rows while accelerated, the
 // training-row tables (A_tr^-1, C_tr) until the switch, the pool's afterwards.
-template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false, bool HC = false>
+// BERN (CWB with the Bernoulli loss, NEXT-4): y and f of the RB replications in shared memory,
+// offset logit(mean y), pseudo residuals r = y - sigma(f), risk = mean log-loss.
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false, bool HC = false,
+          bool BERN = false>
 __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int T = blockDim.x, NW = T >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     static_assert(!ACC || RB == 2, "ACWB runs its two columns as RB = 2");
     static_assert(!HC || ACC, "HCWB builds on the ACWB layout");
+    static_assert(!BERN || !ACC, "Bernoulli loss: CWB layout");
     const int b0 = ACC ? blockIdx.x : blockIdx.x * RB;  // ACC: the replication; else the first of RB
     const int n = p.n;
     const int K = p.K, ns = p.ns, nsp = p.nsp, d = p.d, KS = K * ns;
     const int W = p.W;
     const SmemLayout L(n, K, nsp, d, W, p.n_multi, RB, NW, POOL, sizeof(PermT) * (size_t)p.permt_cap, p.ztab,
-                       (int)sizeof(IdxT), ACC, HC);
+                       (int)sizeof(IdxT), ACC, HC, BERN);
+    double* Yb = (double*)(smem + L.by);  // BERN only: Yb[i * RB + q]
+    double* Fb = (double*)(smem + L.bf);  // BERN only
     double* Hm = (double*)(smem + L.hh);  // ACC only
     double* Fm = (double*)(smem + L.ff);  // HC only
     uint8_t* mk = (uint8_t*)(smem + L.mk);  // HC only
@@ -262,7 +272,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
     for (int a = tid; a < RB * K * d; a += T) agg[a] = 0.0;
     for (int a = tid; a < RB * kPadRows; a += T) r[n * RB + a] = 0.0;
 
-    const int NRB = RB + (ACC ? 1 : 0) + (HC ? 1 : 0);  // per-thread partial slots (+ F^2, + F^2 on D_val)
+    // per-thread partial slots: r^T r of the RB columns (+ F^2 for ACC, + F^2 on D_val for HC,
+    // + the log-loss of the RB columns for BERN)
+    const int NRB = RB + (ACC ? 1 : 0) + (HC ? 1 : 0) + (BERN ? RB : 0);
     double f0[RB];
     if (HC) {
         // f0 = mean of the training targets (Alg. 3 / Alg. 2 line 2 on D_train); F = H = y - f0 on all
@@ -315,6 +327,55 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             hc_pat = 0;
             hc_sw = p.M;
         }
+        __syncthreads();
+    } else if (BERN) {
+        // Alg. 1 line 2 with the Bernoulli loss: f0 = logit(mean y), y in {0, 1};
+        // r = y - sigma(f0) (line 4); r^T r
+        double part[RB];
+        bool bad = false, nb01 = false;
+#pragma unroll
+        for (int q = 0; q < RB; q++) part[q] = 0.0;
+        for (int i = tid; i < n; i += T) {
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const int bq = b0 + q;
+                const double v = (bq < p.B) ? p.Y[(size_t)bq * n + i] : (double)(i & 1);  // padding column
+                bad |= !isfinite(v);
+                nb01 |= v != 0.0 && v != 1.0;
+                Yb[i * RB + q] = v;
+                part[q] += v;
+            }
+        }
+        if (bad) cwb_dev_fail(p.status, CWB_ENONFINITE);
+        if (nb01) cwb_dev_fail(p.status, CWB_EINVAL);
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+            part[q] = warp_sum(part[q]);
+            if (lane == 0) red[q * 32 + warp] = part[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < RB; q++) {
+            double sy = 0.0;
+            for (int w = 0; w < NW; w++) sy += red[q * 32 + w];
+            const double pb = sy / (double)n;
+            if (!(pb > 0.0 && pb < 1.0) && b0 + q < p.B && tid == 0) cwb_dev_fail(p.status, CWB_EDEGENERATE);
+            f0[q] = log(pb / (1.0 - pb));
+            part[q] = 0.0;
+        }
+        for (int i = tid; i < n; i += T) {
+#pragma unroll
+            for (int q = 0; q < RB; q++) {
+                const double f = f0[q];
+                const double v = Yb[i * RB + q] - 1.0 / (1.0 + exp(-f));
+                Fb[i * RB + q] = f;
+                r[i * RB + q] = v;
+                part[q] += v * v;
+            }
+        }
+        __syncthreads();  // everyone has read red[] for f0
+#pragma unroll
+        for (int q = 0; q < RB; q++) red[(NRB + q) * T + tid] = part[q];  // rr_0 -> parity 1
         __syncthreads();
     } else {
         double part[RB];
@@ -425,13 +486,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         double s0 = 0.0, s1 = 0.0;
         for (int t = lane; t < T; t += 32) {
             s0 += red[((mp + 1) & 1) * NRB * T + q * T + t];
-            s1 += red[(mp & 1) * NRB * T + q * T + t];
+            s1 += red[(mp & 1) * NRB * T + ((BERN ? RB : 0) + q) * T + t];  // BERN: the log-loss slot
         }
         const double rr0 = warp_sum(s0), rr1 = warp_sum(s1);
         if (lane == 0 && b < p.B) {
             if (p.k_trace) p.k_trace[(size_t)mp * p.B + b] = kb;
             if (p.sse_trace) p.sse_trace[(size_t)mp * p.B + b] = rr0 - best_sh[q];
-            if (p.risk_trace) p.risk_trace[(size_t)mp * p.B + b] = rr1 * p.inv2n;
+            if (p.risk_trace) p.risk_trace[(size_t)mp * p.B + b] = BERN ? rr1 * (2.0 * p.inv2n) : rr1 * p.inv2n;
         }
     };
 
@@ -685,9 +746,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             const int parw = m & 1;
             const IdxT* ik0 = idx + (size_t)ks_sh[0] * n;
             const IdxT* ik1 = idx + (size_t)ks_sh[RB - 1] * n;
-            double acc[RB], accF = 0.0;
+            double acc[RB], accF = 0.0, accL[RB];
 #pragma unroll
-            for (int q = 0; q < RB; q++) acc[q] = 0.0;
+            for (int q = 0; q < RB; q++) { acc[q] = 0.0; accL[q] = 0.0; }
             // ACC (Alg. 2, ACWB iteration ma = m + 1): F = r - nu b_k (line 8), H -= eta b_kcor (line 16),
             // next columns r' = (1 - vt1) F + vt1 H (lines 4-6), c' = r' + a1 (c - b_kcor) (line 10)
             const double vt = 2.0 / (double)(m + 2), eta = p.gamma * p.nu / vt;
@@ -703,7 +764,19 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const int i = i0 + e * T;
-                    if (i < n) {
+                    if (i < n && BERN) {
+                        // f += nu b_k* (line 10), r = y - sigma(f) (line 4 of the next iteration), log-loss
+#pragma unroll
+                        for (int q = 0; q < RB; q++) {
+                            const double f = Fb[i * RB + q] + zhat[q * nsp + (q ? j1[e] : j0[e])];
+                            Fb[i * RB + q] = f;
+                            const double y = Yb[i * RB + q];
+                            const double v = y - 1.0 / (1.0 + exp(-f));
+                            r[i * RB + q] = v;
+                            acc[q] = fma(v, v, acc[q]);
+                            accL[q] += (f > 0.0 ? f + log1p(exp(-f)) : log1p(exp(f))) - y * f;
+                        }
+                    } else if (i < n) {
                         if (RB == 1) {
                             const double v = r[i] - zhat[j0[e]];
                             r[i] = v;
@@ -734,6 +807,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
 #pragma unroll
             for (int q = 0; q < RB; q++) red[(parw * NRB + q) * T + tid] = acc[q];
             if (ACC) red[(parw * NRB + RB) * T + tid] = accF;
+            if (BERN)
+#pragma unroll
+                for (int q = 0; q < RB; q++) red[(parw * NRB + RB + q) * T + tid] = accL[q];
         }
         __syncthreads();
         if (timed) tm = phase_mark(&tD, tm, true);
@@ -1093,9 +1169,10 @@ __global__ void k_fused_pack(const int32_t* __restrict__ plan, const int32_t* __
     }
 }
 
-template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false, bool HC = false>
+template <typename IdxT, typename PermT, int RB, bool POOL, int MAXT, int MINB, bool ACC = false, bool HC = false,
+          bool BERN = false>
 int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
-    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB, ACC, HC>;
+    auto kern = k_train_fused<IdxT, PermT, RB, POOL, MAXT, MINB, ACC, HC, BERN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -1;
     const int grid = ACC ? fp.B : (fp.B + RB - 1) / RB;
@@ -1105,7 +1182,15 @@ int launch_t(const FusedParams& fp, int T, size_t smem, cudaStream_t s) {
 
 template <typename IdxT, typename PermT>
 int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cudaStream_t s, bool acc = false,
-               bool hc = false) {
+               bool hc = false, bool bern = false) {
+    if (bern) {  // Bernoulli loss: the CWB shapes of k_train_fused plus y and f in shared memory
+        if (RB == 2) {
+            if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, false, false, true>(fp, T, smem, s);
+            return launch_t<IdxT, PermT, 2, false, 512, 1, false, false, true>(fp, T, smem, s);
+        }
+        if (pool) return launch_t<IdxT, PermT, 1, true, 768, 1, false, false, true>(fp, T, smem, s);
+        return launch_t<IdxT, PermT, 1, false, 768, 1, false, false, true>(fp, T, smem, s);
+    }
     if (hc) {  // HCWB: the ACWB layout plus F, the validation mask and the phase state
         if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, true, true>(fp, T, smem, s);
         return launch_t<IdxT, PermT, 2, false, 512, 1, true, true>(fp, T, smem, s);
@@ -1143,7 +1228,7 @@ struct FusedShape {
 
 // Launch shape for B replications: RB replications per CTA, T threads, pool
 // tables in shared memory or not.  false when the residuals do not fit.
-static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
+static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out, bool bern = false) {
     if ((int64_t)c->K * c->n + 8 > INT32_MAX) return false;
     if ((int64_t)c->K * c->n_star * 16 > 200 * 1024) return false;  // plan kernel shared memory
     const int KS = c->K * c->n_star;
@@ -1152,7 +1237,7 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
     int nc = 0;
     const int nsm = 148;
     if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};  // ~2 replications per SM: one CTA (512 best of 256..768)
-    if (B > nsm) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
+    if (B > nsm && !bern) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
     cands[nc++] = {1, c->n >= 8192 ? 768 : 512, kMaxSmem};
     for (int i = 0; i < nc; i++) {
         FusedShape f;
@@ -1165,7 +1250,8 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out) {
         f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
         f.cap = permt_bound(KS, f.T, f.P);
         for (int pool = 1; pool >= 0; pool--) {
-            SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, 0);
+            SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, 0,
+                         1, false, false, bern);
             if (L.total <= cands[i].lim) {
                 f.pool = pool != 0;
                 f.smem = L.total;
@@ -1310,7 +1396,7 @@ struct HcArgs {  // HCWB extras of a fused launch
 static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, double nu, double gamma, int32_t M,
                               double* offset_out, double* theta_out, double* theta_h_out, int32_t* k_trace,
                               int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s,
-                              bool* launched, const HcArgs* hc = nullptr) {
+                              bool* launched, const HcArgs* hc = nullptr, bool bern = false) {
     *launched = false;
     FusedShape f;
     if (acc) {  // the two columns (r, c) of a replication run as RB = 2 in a 512-thread CTA
@@ -1323,7 +1409,7 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
                        hc != nullptr)
                 .total > kMaxSmem)
             return CWB_OK;
-    } else if (!fused_shape(c, B, &f)) {
+    } else if (!fused_shape(c, B, &f, bern)) {
         return CWB_OK;  // does not fit: caller uses the general path
     }
     int rc = CWB_OK;
@@ -1341,12 +1427,12 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
     const int nm = c->plan_multi;
     const bool hcm = hc != nullptr;
     f.smem = SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, false, 0, 0, c->idx_bytes, acc,
-                        hcm).total;
+                        hcm, bern).total;
     if (f.smem > lim) return CWB_OK;
     int ztab = 0;
     {   // POOL: schedule, B tables, Zs / zj0 and the index vectors all in shared memory, or none
         SmemLayout L1((int)c->n, c->K, c->nsp, c->d, c->W, nm, f.RB, f.T / 32, true, pbytes, 3, c->idx_bytes, acc,
-                      hcm);
+                      hcm, bern);
         if (L1.total <= lim) {
             f.pool = true;
             ztab = 3;
@@ -1373,10 +1459,10 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
         fp.val_risk_trace = hc->val_risk_trace; fp.switch_iter = hc->switch_iter;
     }
     const bool i8 = c->idx_bytes == 1, p16 = f.permt_bytes == 2;
-    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
-    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
-    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
-    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm);
+    if (i8 && p16) rc = launch_sel<uint8_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm, bern);
+    else if (i8) rc = launch_sel<uint8_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm, bern);
+    else if (p16) rc = launch_sel<uint16_t, uint16_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm, bern);
+    else rc = launch_sel<uint16_t, uint32_t>(fp, f.T, f.RB, f.pool, f.smem, s, acc, hcm, bern);
     if (rc) return cwb_set_error(c, CWB_ECUDA, "fused kernel: cannot set shared memory size");
     c->launches++;
     c->fused_smem = f.smem;
@@ -1410,4 +1496,11 @@ int cwb_train_hcwb_fused(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* 
     h.val_risk_trace = val_risk_trace; h.switch_iter = switch_iter;
     return train_fused_common(c, true, Y, B, nu, gamma, M, offset_out, theta_f_out, nullptr, k_trace, kcor_trace,
                               sse_trace, risk_trace, s, launched, &h);
+}
+
+int cwb_train_bernoulli_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                              double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+                              cudaStream_t s, bool* launched) {
+    return train_fused_common(c, false, Y, B, nu, 0.0, M, offset_out, theta_agg_out, nullptr, k_trace, nullptr,
+                              sse_trace, risk_trace, s, launched, nullptr, true);
 }

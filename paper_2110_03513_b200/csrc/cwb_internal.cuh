@@ -178,6 +178,9 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
                            int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
                            int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
                            int32_t* switch_iter, cudaStream_t s);
+int cwb_train_bernoulli_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                              double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+                              cudaStream_t s, bool* launched);
 int cwb_train_bernoulli_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
                                 double* offset_out, double* theta_agg_out, int32_t* k_trace,
                                 double* sse_trace, double* risk_trace, cudaStream_t s);

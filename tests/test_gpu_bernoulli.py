@@ -28,15 +28,18 @@ def host(out):
     return {k: v.cpu().numpy() for k, v in out.items()}
 
 
-@pytest.mark.parametrize("name,reps,M", [("R0", None, None), ("R1", None, None), ("R1", range(37), 60),
-                                         ("R2", range(0, 1024, 97), 80)])
-def test_bernoulli_matches_oracle(name, reps, M):
+@pytest.mark.parametrize("name,reps,M,path", [("R0", None, None, 1), ("R0", None, None, 2), ("R1", None, None, 1),
+                                              ("R1", None, None, 2), ("R1", range(37), 60, 1),
+                                              ("R2", range(0, 1024, 97), 80, 0)])
+def test_bernoulli_matches_oracle(name, reps, M, path):
+    # path 1: the persistent kernel (BERN mode), 2: per-iteration kernels
     ds = S.make(name, reps=reps)
     c = ds.cfg
     M = M or c.M
     Y = S.binary_targets(ds)
     po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
     pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    pg.set_path(path)
     g = host(pg.train_bernoulli(dev(Y), nu=c.nu, M=M))
     pg.status()
     o = po.train_bernoulli(Y, nu=c.nu, M=M, threads=8)
@@ -44,10 +47,12 @@ def test_bernoulli_matches_oracle(name, reps, M):
     pg.close()
 
 
-def test_bernoulli_nu_zero_and_m_zero():
+@pytest.mark.parametrize("path", [1, 2])
+def test_bernoulli_nu_zero_and_m_zero(path):
     ds = S.make("R1", reps=range(3))
     Y = S.binary_targets(ds)
     pg = cwb.Pool(dev(ds.X), gpu_cfg_of(ds.cfg))
+    pg.set_path(path)
     g = host(pg.train_bernoulli(dev(Y), nu=0.0, M=5))
     p = Y.mean(1)
     ent = -(p * np.log(p) + (1 - p) * np.log(1 - p))
@@ -68,8 +73,10 @@ def test_bernoulli_errors_and_determinism():
     for k in a:
         assert (a[k] == b[k]).all(), k
     pg.close()
-    for bad, err in ((np.where(Y > 0, 2.0, 0.0), "CWB_EINVAL"), (np.ones_like(Y), "CWB_EDEGENERATE")):
+    for (bad, err), path in [(b_, p_) for b_ in ((np.where(Y > 0, 2.0, 0.0), "CWB_EINVAL"),
+                                              (np.ones_like(Y), "CWB_EDEGENERATE")) for p_ in (1, 2)]:
         pg = cwb.Pool(dev(ds.X), gpu_cfg_of(ds.cfg))
+        pg.set_path(path)
         with pytest.raises(cwb.CwbError) as e:
             pg.train_bernoulli(dev(bad), M=2)
             pg.status()
