@@ -955,6 +955,170 @@ int orc_train_hcwb(const orc_pool* p, const double* Y, int B, const uint8_t* val
 
 /* -------------------------------------------------------------- predict */
 
+/* ------------------------------------------------------ CV folds (NEXT-4) */
+
+/* Alg. 1 supp. with 0/1 observation weights per replication (binMatMat /
+ * binMatVec with weights; the weights of P:L870): replication b fits on the rows
+ * whose fold differs from fold_of_rep[b] (all rows when fold_of_rep[b] < 0) and the held-out
+ * rows only follow the model.  Per replication, step by step:
+ *   f0 = mean of y over its training rows (line 2 on D_train);
+ *   r = y - f on every row (line 4), fitted with weights w (w_i = 1 on training rows):
+ *   theta_k = (Z_k^T W Z_k + lambda_k D)^-1 Z_k^T W r (lambda of the pool, calibrated on all rows),
+ *   SSE_k = sum_i w_i (r_i - (Z_k theta_k)_i)^2 (lines 5-8), k* = argmin (lowest k, line 9);
+ *   f += nu Z_k* theta* on every row (line 10), theta_agg[k*] += nu theta* (P:L838);
+ *   risk_trace = sum_i w_i (y_i - f_i)^2 / (2 sum w), val_risk_trace = the same over the
+ *   held-out rows (0 when there are none). */
+typedef struct {
+    const orc_pool* p;
+    const double* Y;
+    const int32_t* fold_of_rep;
+    const double* W;    /* F x n weights (fold f held out) */
+    const double* Lf;   /* F x K x d x d Cholesky factors of Z^T W_f Z + lambda D */
+    int B, M, F, tid, nth;
+    double nu;
+    double *offset, *theta_agg, *sse_trace, *risk_trace, *val_risk_trace, *gap_trace, *f_out;
+    int32_t* k_trace;
+} folds_job;
+
+static void folds_one(const folds_job* J, int b, scratch* ws, double* f, double* r, double* theta, const double* ones,
+                      const double* Lall) {
+    const orc_pool* p = J->p;
+    int64_t n = p->n;
+    int d = p->d, K = p->K, B = J->B;
+    const double* y = J->Y + (size_t)b * n;
+    const int fb = J->fold_of_rep[b];
+    const double* w = fb < 0 ? ones : J->W + (size_t)fb * n;
+    const double* L = fb < 0 ? Lall : J->Lf + (size_t)fb * K * d * d;
+    double sw = 0.0, sy = 0.0, sv = 0.0;
+    for (int64_t i = 0; i < n; i++) { sw += w[i]; sy += w[i] * y[i]; }
+    const double f0 = sy / sw;
+    J->offset[b] = f0;
+    for (int64_t i = 0; i < n; i++) f[i] = f0;
+    double* agg = J->theta_agg + (size_t)b * K * d;
+    for (int a = 0; a < K * d; a++) agg[a] = 0.0;
+    for (int m = 0; m < J->M; m++) {
+        for (int64_t i = 0; i < n; i++) r[i] = y[i] - f[i];
+        int32_t ks;
+        double sse, gap;
+        find_best_w(p, r, w, L, ws, &ks, theta, &sse, &gap);
+        const double* Zb = p->Zb + (size_t)ks * p->n_star * d;
+        const int32_t* idx = p->idx + (size_t)ks * n;
+        for (int64_t i = 0; i < n; i++) {
+            const double* zi = (p->mode == ORC_MODE_UNBINNED) ? p->Zx + ((size_t)ks * n + i) * d : Zb + (size_t)idx[i] * d;
+            double v = 0.0;
+            for (int j = 0; j < d; j++) v += zi[j] * theta[j];
+            f[i] = f[i] + J->nu * v;
+        }
+        for (int j = 0; j < d; j++) agg[ks * d + j] += J->nu * theta[j];
+        double rs = 0.0, rv = 0.0;
+        sv = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            double e = y[i] - f[i];
+            rs += w[i] * 0.5 * e * e;
+            rv += (1.0 - w[i]) * 0.5 * e * e;
+            sv += 1.0 - w[i];
+        }
+        J->k_trace[(size_t)m * B + b] = ks;
+        J->sse_trace[(size_t)m * B + b] = sse;
+        J->risk_trace[(size_t)m * B + b] = rs / sw;
+        J->val_risk_trace[(size_t)m * B + b] = sv > 0.0 ? rv / sv : 0.0;
+        if (J->gap_trace) J->gap_trace[(size_t)m * B + b] = gap;
+    }
+    if (J->f_out)
+        for (int64_t i = 0; i < n; i++) J->f_out[(size_t)b * n + i] = f[i];
+}
+
+typedef struct {
+    const folds_job* J;
+    const double* ones;
+    const double* Lall;
+} folds_ctx;
+
+static void* folds_worker(void* arg) {
+    const folds_ctx* X = (const folds_ctx*)arg;
+    const folds_job* J = X->J;
+    scratch w;
+    scratch_init(&w, J->p->d, J->p->n_star);
+    double* f = (double*)malloc(sizeof(double) * J->p->n);
+    double* r = (double*)malloc(sizeof(double) * J->p->n);
+    double* theta = (double*)malloc(sizeof(double) * J->p->d);
+    for (int b = J->tid; b < J->B; b += J->nth) folds_one(J, b, &w, f, r, theta, X->ones, X->Lall);
+    free(f); free(r); free(theta);
+    scratch_free(&w);
+    return NULL;
+}
+
+/* penalised normal matrix of learner k with weights w: Z^T W Z + lambda_k D, Cholesky into L */
+static int weighted_factor(const orc_pool* p, int k, const double* w, double* A, double* L) {
+    int d = p->d;
+    int64_t n = p->n;
+    const double* Zb = p->Zb + (size_t)k * p->n_star * d;
+    const int32_t* idx = p->idx + (size_t)k * n;
+    if (p->mode == ORC_MODE_BINNED) orc_bin_mat_mat(Zb, p->n_star, d, idx, w, n, A);
+    else {
+        const double* rows = (p->mode == ORC_MODE_DENSE) ? Zb : p->Zx + (size_t)k * n * d;
+        orc_dense_ztwz(rows, d, (p->mode == ORC_MODE_DENSE) ? idx : NULL, w, n, A);
+    }
+    for (int a = 0; a < d * d; a++) A[a] += p->lambda[k] * p->D[a];
+    return orc_cholesky(A, d, L);
+}
+
+int orc_train_folds(const orc_pool* p, const double* Y, int B, const uint8_t* fold_of_row, int F,
+                    const int32_t* fold_of_rep, double nu, int M, int n_threads, double* offset, double* theta_agg,
+                    int32_t* k_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                    double* gap_trace, double* f_out) {
+    if (!p || p->K < 1) return ORC_EEMPTY;
+    if (B < 1 || M < 0 || !(nu >= 0.0) || F < 1 || F > 255 || !fold_of_row || !fold_of_rep) return ORC_EINVAL;
+    int64_t n = p->n;
+    int d = p->d, K = p->K;
+    for (int64_t a = 0; a < (int64_t)B * n; a++)
+        if (!isfinite(Y[a])) return ORC_ENONFINITE;
+    for (int b = 0; b < B; b++)
+        if (fold_of_rep[b] >= F || fold_of_rep[b] < -1) return ORC_EINVAL;
+    for (int64_t i = 0; i < n; i++)
+        if (fold_of_row[i] >= F) return ORC_EINVAL;
+    double* W = (double*)malloc(sizeof(double) * (size_t)F * n);
+    double* ones = (double*)malloc(sizeof(double) * n);
+    double* Lf = (double*)malloc(sizeof(double) * (size_t)F * K * d * d);
+    double* Lall = (double*)malloc(sizeof(double) * (size_t)K * d * d);
+    double* A = (double*)malloc(sizeof(double) * d * d);
+    int st = ORC_OK;
+    for (int64_t i = 0; i < n; i++) ones[i] = 1.0;
+    for (int f = 0; f < F && st == ORC_OK; f++) {
+        double cnt = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            W[(size_t)f * n + i] = fold_of_row[i] == f ? 0.0 : 1.0;
+            cnt += W[(size_t)f * n + i];
+        }
+        if (cnt == 0.0) st = ORC_EINVAL;  /* a fold holding out every row */
+        for (int k = 0; k < K && st == ORC_OK; k++)
+            if (weighted_factor(p, k, W + (size_t)f * n, A, Lf + ((size_t)f * K + k) * d * d) != ORC_OK) st = ORC_ECALIB;
+    }
+    for (int k = 0; k < K && st == ORC_OK; k++)
+        if (weighted_factor(p, k, ones, A, Lall + (size_t)k * d * d) != ORC_OK) st = ORC_ECALIB;
+    free(A);
+    if (st == ORC_OK) {
+        if (n_threads < 1) n_threads = 1;
+        if (n_threads > B) n_threads = B;
+        folds_job* jobs = (folds_job*)malloc(sizeof(folds_job) * n_threads);
+        folds_ctx* ctxs = (folds_ctx*)malloc(sizeof(folds_ctx) * n_threads);
+        pthread_t* thr = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
+        for (int t = 0; t < n_threads; t++) {
+            folds_job J = {p, Y, fold_of_rep, W, Lf, B, M, F, t, n_threads, nu, offset, theta_agg, sse_trace,
+                           risk_trace, val_risk_trace, gap_trace, f_out, k_trace};
+            jobs[t] = J;
+            folds_ctx X = {&jobs[t], ones, Lall};
+            ctxs[t] = X;
+        }
+        for (int t = 1; t < n_threads; t++) pthread_create(&thr[t], NULL, folds_worker, &ctxs[t]);
+        folds_worker(&ctxs[0]);
+        for (int t = 1; t < n_threads; t++) pthread_join(thr[t], NULL);
+        free(jobs); free(ctxs); free(thr);
+    }
+    free(W); free(ones); free(Lf); free(Lall);
+    return st;
+}
+
 int orc_predict(const orc_pool* p, const double* Xnew, int64_t m, const double* offset,
                 const double* theta_agg, int B, double* out) {
     int d = p->d, K = p->K, n_star = p->n_star;

@@ -141,6 +141,18 @@ int orc_train_loss(const orc_pool* p, const double* Y, int B, int loss, double n
                    double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
                    double* risk_trace, double* gap_trace, double* f_out);
 
+/* CWB with 0/1 observation weights per replication (cross-validation folds):
+ * replication b fits on the rows with fold_of_row[i] != fold_of_rep[b] (every row when
+ * fold_of_rep[b] = -1) with G = Z^T W Z and s = Z^T W r (binMatMat / binMatVec with weights,
+ * P:L887-904) and the pool's lambda; the held-out rows follow the model.  Outputs as
+ * orc_train; offset = mean of y over the training rows; risk_trace / val_risk_trace = half
+ * mean squared error over the training / held-out rows after iteration m (0 if none held out).
+ * ORC_EINVAL for fold ids >= F, F outside 1..255, a fold holding out every row. */
+int orc_train_folds(const orc_pool* p, const double* Y, int B, const uint8_t* fold_of_row, int F,
+                    const int32_t* fold_of_rep, double nu, int M, int n_threads, double* offset, double* theta_agg,
+                    int32_t* k_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                    double* gap_trace, double* f_out);
+
 /* Accelerated CWB, Algorithm 2, L2 loss, for B target vectors: primary
  * model f, momentum model h, combined model g = (1 - theta_m) f + theta_m h, theta_m =
  * 2/(m+1); pseudo residuals at g; error-corrected residuals c; eta_m = gamma nu / theta_m.

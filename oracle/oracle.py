@@ -95,6 +95,9 @@ def lib():
                                 _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p]
         L.orc_train_loss.argtypes = [C.POINTER(_Pool), _D, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
                                      _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p]
+        L.orc_train_folds.argtypes = [C.POINTER(_Pool), _D, C.c_int, _P(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_int,
+                                      _I, C.c_double, C.c_int, C.c_int, _D, _D, _I, _D, _D, _D, C.c_void_p,
+                                      C.c_void_p]
         L.orc_train_acwb.argtypes = [C.c_void_p, _D, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _D, _D, _D,
                                      _I, _I, _D, _D, _D, _D, _D, _D, _D]
         L.orc_train_hcwb.argtypes = [C.c_void_p, _D, C.c_int, _P(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_double,
@@ -363,6 +366,26 @@ class Pool:
         _chk(lib().orc_train_loss(self._p, Y, B, 1, nu, M, threads, off, agg, kt, st, rt,
                                   gt.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p)), "train_bernoulli")
         return TrainResult(off, agg, kt, st, rt, gt, f)
+
+    def train_folds(self, Y, fold_of_row, F: int, fold_of_rep, nu: float = 0.05, M: int = 200, threads: int = 1):
+        """CWB with per-replication 0/1 observation weights (CV folds): replication b
+        fits on the rows with fold_of_row != fold_of_rep[b]; returns (TrainResult, val_risk_trace)."""
+        Y = _f64(np.atleast_2d(Y))
+        B = Y.shape[0]
+        K, d = self.K, self.d
+        off = np.empty(B)
+        agg = np.empty((B, K, d))
+        kt = np.empty((M, B), dtype=np.int32)
+        st = np.empty((M, B))
+        rt = np.empty((M, B))
+        vt = np.empty((M, B))
+        gt = np.empty((M, B))
+        f = np.empty((B, self.n))
+        _chk(lib().orc_train_folds(self._p, Y, B, np.ascontiguousarray(fold_of_row, dtype=np.uint8), F,
+                                   np.ascontiguousarray(fold_of_rep, dtype=np.int32), nu, M, threads, off, agg, kt,
+                                   st, rt, vt, gt.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p)),
+             "train_folds")
+        return TrainResult(off, agg, kt, st, rt, gt, f), vt
 
     def train_acwb(self, Y, nu: float = 0.05, gamma: float = 0.0034, M: int = 200,
                    threads: int = 1) -> AcwbResult:

@@ -742,3 +742,78 @@ def test_bernoulli_errors():
         p.train_bernoulli(np.where(y > 0, 2.0, 0.0), M=2)        # y not in {0, 1}
     with pytest.raises(O.OracleError):
         p.train_bernoulli(np.ones_like(y), M=2)                   # mean(y) = 1
+
+
+# -------------------------------------------- CV folds: per-replication observation weights (NEXT-4)
+# Alg. 1 supp. with 0/1 weights per replication (binMatMat / binMatVec with weights).
+
+def _folds_data(seed=21, K=3, n=360, F=4):
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(0, 1, (K, n))
+    Y = np.stack([np.sin(5 * X[0]) + 0.4 * X[1] + 0.3 * rng.standard_normal(n) for _ in range(F + 1)])
+    fold = (rng.permutation(n) % F).astype(np.uint8)
+    return O.Pool(X, O.Config(n_knots=6), O.MODE_BINNED), X, Y, fold
+
+
+def test_folds_without_holdout_equal_plain_cwb():
+    p, X, Y, fold = _folds_data()
+    res, vr = p.train_folds(Y, fold, 4, np.full(Y.shape[0], -1), nu=0.1, M=30)
+    ref = p.train(Y, nu=0.1, M=30)
+    assert (res.k_trace == ref.k_trace).all()
+    assert np.abs(res.theta_agg - ref.theta_agg).max() <= 1e-12 * np.abs(ref.theta_agg).max()
+    assert np.abs(res.risk_trace - ref.risk_trace).max() <= 1e-12 * ref.risk_trace.max()
+    assert (vr == 0).all()
+
+
+def test_folds_held_out_targets_do_not_enter_the_fit():
+    p, X, Y, fold = _folds_data()
+    reps = np.array([0, 1, 2, 3, 0])
+    a, va = p.train_folds(Y, fold, 4, reps, nu=0.1, M=25)
+    Y2 = Y.copy()
+    for b, f in enumerate(reps):
+        Y2[b, fold == f] += 100.0 * (b + 1)  # change only the held-out rows
+    b_, vb = p.train_folds(Y2, fold, 4, reps, nu=0.1, M=25)
+    assert (a.k_trace == b_.k_trace).all() and (a.theta_agg == b_.theta_agg).all()
+    assert (a.offset == b_.offset).all() and (a.sse_trace == b_.sse_trace).all()
+    assert (np.abs(vb - va) > 1.0).all()  # the held-out risk sees them
+
+
+def test_folds_first_fit_is_penalised_weighted_least_squares():
+    # iteration 1: theta = (Z^T W Z + lambda D)^-1 Z^T W (y - f0), f0 = training mean; solved here
+    # with numpy on the expanded design of the selected learner
+    p, X, Y, fold = _folds_data(seed=4)
+    res, _ = p.train_folds(Y[:1], fold, 4, np.array([2]), nu=1.0, M=1)
+    k = int(res.k_trace[0, 0])
+    w = (fold != 2).astype(float)
+    y = Y[0]
+    f0 = (w * y).sum() / w.sum()
+    assert abs(res.offset[0] - f0) <= 1e-13 * abs(f0)
+    Z = p.Zb[k][p.idx[k]]
+    A = Z.T @ (w[:, None] * Z) + p.lam[k] * O.penalty(p.d)
+    th = np.linalg.solve(A, Z.T @ (w * (y - f0)))
+    assert np.abs(res.theta_agg[0, k] - th).max() <= 1e-10 * np.abs(th).max()
+    sse = (w * (y - f0 - Z @ th) ** 2).sum()
+    assert abs(res.sse_trace[0, 0] - sse) <= 1e-10 * sse
+
+
+def test_folds_risk_traces_match_the_final_fit():
+    p, X, Y, fold = _folds_data(seed=9)
+    reps = np.array([0, 1, 2, 3, -1])
+    res, vr = p.train_folds(Y, fold, 4, reps, nu=0.1, M=15, threads=3)
+    for b, f in enumerate(reps):
+        w = np.ones(Y.shape[1]) if f < 0 else (fold != f).astype(float)
+        e2 = 0.5 * (Y[b] - res.f[b]) ** 2
+        assert abs(res.risk_trace[-1, b] - (w * e2).sum() / w.sum()) <= 1e-12 * res.risk_trace[-1, b]
+        ho = (1 - w)
+        ref = (ho * e2).sum() / ho.sum() if ho.sum() else 0.0
+        assert abs(vr[-1, b] - ref) <= 1e-12 * max(ref, 1e-300)
+    pred = p.predict(X, res.offset, res.theta_agg)
+    assert np.abs(pred - res.f).max() <= 1e-12 * np.abs(res.f).max()
+
+
+def test_folds_errors():
+    p, X, Y, fold = _folds_data()
+    with pytest.raises(O.OracleError):
+        p.train_folds(Y[:1], fold, 4, np.array([4]), M=2)        # fold id >= F
+    with pytest.raises(O.OracleError):
+        p.train_folds(Y[:1], np.zeros_like(fold), 1, np.array([0]), M=2)  # fold 0 holds out every row
