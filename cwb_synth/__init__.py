@@ -153,3 +153,9 @@ def binary_targets(ds: Dataset, scale: float = 2.0) -> np.ndarray:
         u = np.random.default_rng(np.random.SeedSequence([SEED, 9, ds.cfg.cfg_id, int(b)])).uniform(size=z.size)
         out[c] = (u < 1.0 / (1.0 + np.exp(-z))).astype(np.float64)
     return out
+
+
+def cv_folds(n: int, F: int = 5, seed: int = 0) -> np.ndarray:
+    """Seeded assignment of the n rows to F cross-validation folds of (nearly) equal size: uint8[n]."""
+    rng = np.random.default_rng(np.random.SeedSequence([SEED, 11, seed]))
+    return (rng.permutation(n) % F).astype(np.uint8)

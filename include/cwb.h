@@ -212,6 +212,22 @@ int cwb_train_bernoulli(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int
                         double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
                         cudaStream_t stream);
 
+/* CWB with per-replication cross-validation folds (0/1 observation weights, SURVEY NEXT-4;
+ * binMatMat / binMatVec with weights P:L887-904, the weights of P:L870).  fold_of_row[n]
+ * (device, uint8, values < F) assigns every row to one of F folds; replication b (fold_of_rep[b],
+ * device int32, -1 = no hold-out) fits on the rows of the other folds: offset = mean of its
+ * training targets, s = Z^T W r, theta = (Z^T W Z + lambda D)^-1 s with the pool's lambda,
+ * SSE over its training rows; the model is updated on every row.  Outputs as cwb_train;
+ * risk_trace[m][b] = sum over training rows of (y - f)^2 / (2 n_train), val_risk_trace[m][b] the
+ * same over the held-out rows (0 when none).  Per-iteration kernels.  Errors: CWB_EINVAL
+ * (arguments; fold ids out of range or a replication without training rows, via cwb_status),
+ * CWB_ECALIB (a fold's training rows leave Z^T W Z + lambda D singular), CWB_EUNSUPPORTED
+ * (row-sharded context, unbinned pool). */
+int cwb_train_folds(cwb_ctx* ctx, const double* Y, int32_t B, const uint8_t* fold_of_row, int32_t F,
+                    const int32_t* fold_of_rep, double nu, int32_t M, double* offset_out, double* theta_agg_out,
+                    int32_t* k_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
+                    cudaStream_t stream);
+
 /* Hybrid CWB, Algorithm 3 ("HCWB"), L2 loss.  val_mask[n] (device, uint8):
  * 1 = validation row (D_val), 0 = training row (D_train); the split is the caller's
  * (seeded) draw.  Per replication: ACWB (as cwb_train_acwb, momentum gamma) fitted on the

@@ -162,7 +162,7 @@ void cwb_free(cwb_ctx* c) {
     if (c->ev_plan) cudaStreamWaitEvent(s, c->ev_plan, 0);  // a plan still building on the side stream
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
-                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->ws.bern, c->plan, c->permt,
+                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->ws.bern, c->ws.fold, c->plan, c->permt,
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
     cwb_stream_release(c, s);
@@ -360,6 +360,20 @@ int cwb_train_bernoulli(cwb_ctx* c, const double* Y, int32_t B, double nu, int32
             return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: fused path needs more shared memory than a CTA has");
     }
     return cwb_train_bernoulli_general(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace, s);
+}
+
+int cwb_train_folds(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* fold_of_row, int32_t F,
+                    const int32_t* fold_of_rep, double nu, int32_t M, double* offset_out, double* theta_agg_out,
+                    int32_t* k_trace, double* sse_trace, double* risk_trace, double* val_risk_trace, cudaStream_t s) {
+    if (!c || !Y || !fold_of_row || !fold_of_rep || !theta_agg_out || B < 1 || M < 0 || F < 1 || F > 255 ||
+        !(nu >= 0.0) || !isfinite(nu))
+        return cwb_set_error(c, CWB_EINVAL, "cwb_train_folds: invalid argument");
+    if (c->status) return c->status;
+    c->stream = s;
+    if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: row-sharded context");
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: unbinned pool (cwb_train only)");
+    return cwb_train_folds_general(c, Y, B, fold_of_row, F, fold_of_rep, nu, M, offset_out, theta_agg_out, k_trace,
+                                   sse_trace, risk_trace, val_risk_trace, s);
 }
 
 int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gamma, int32_t M,

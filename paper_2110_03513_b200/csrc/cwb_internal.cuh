@@ -41,6 +41,8 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     double* pack = nullptr;    // row sharding: [K][d][Bp] partial s, then [Bp] partial r^T r
     double* bern = nullptr;    // Bernoulli loss: F, Yt (n x Bp each), row-block partials
     size_t bern_bytes = 0;
+    double* fold = nullptr;    // CV folds: per-fold tables, column statistics, partials, masks
+    size_t fold_bytes = 0;
 };
 
 struct cwb_stream_plan {  // streaming binMatVec gather plan (cwb_stream.cu), built on first use
@@ -184,6 +186,10 @@ int cwb_train_bernoulli_fused(cwb_ctx* c, const double* Y, int32_t B, double nu,
 int cwb_train_bernoulli_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
                                 double* offset_out, double* theta_agg_out, int32_t* k_trace,
                                 double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_train_folds_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* fold_of_row, int32_t F,
+                            const int32_t* fold_of_rep, double nu, int32_t M, double* offset_out,
+                            double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+                            double* val_risk_trace, cudaStream_t s);
 int cwb_launch_masked_pool(cwb_ctx* c, const uint8_t* mask, uint32_t* cnt_tr, double* G_tr, double* Ainv_tr,
                            cudaStream_t s, double* Cb_tr = nullptr);
 int cwb_find_best_general(cwb_ctx* ctx, const double* R, int32_t B, int32_t* k_out,

@@ -96,10 +96,12 @@ __global__ void k_tr_in(const double* __restrict__ Y, int64_t n, int B, int Bp,
 
 // H1: one warp per (learner, bin), lane = replication column; rows of the bin
 // in increasing order (the order of the paper's loop over i).
+// (fold != NULL: CV folds, rows of column b's own fold colfold[b] >= 0 count as 0)
 template <typename PermT>
 __global__ void k_h1(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
                      const int32_t* __restrict__ off, const PermT* __restrict__ perm,
-                     double* __restrict__ U) {
+                     double* __restrict__ U, const uint8_t* __restrict__ fold = nullptr,
+                     const int32_t* __restrict__ colfold = nullptr) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
     if (g >= (int64_t)K * ns) return;
@@ -110,6 +112,16 @@ __global__ void k_h1(const double* __restrict__ Rt, int64_t n, int Bp, int K, in
     const double* col = Rt + b;
     double acc = 0.0;
     int32_t q = a0;
+    if (fold) {  // weighted binMatVec (P:L898-904 with 0/1 weights)
+        const int fb = colfold[b];
+        for (; q < a1; q++) {
+            const uint32_t i = pk[q];
+            const double v = col[(size_t)i * Bp];
+            acc += fold[i] == fb ? 0.0 : v;
+        }
+        U[(size_t)g * Bp + b] = acc;
+        return;
+    }
     for (; q + 4 <= a1; q += 4) {
         const uint32_t i0 = pk[q], i1 = pk[q + 1], i2 = pk[q + 2], i3 = pk[q + 3];
         const double v0 = col[(size_t)i0 * Bp], v1 = col[(size_t)i1 * Bp];
@@ -129,7 +141,9 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
                        const double* __restrict__ G, double* __restrict__ theta,
                        double* __restrict__ delta, const double* __restrict__ Ainv2 = nullptr,
                        const double* __restrict__ G2 = nullptr, const int32_t* __restrict__ phase = nullptr,
-                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0, int Bu = 0) {
+                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0, int Bu = 0,
+                       const double* __restrict__ Aset = nullptr, const double* __restrict__ Gset = nullptr,
+                       const int32_t* __restrict__ colset = nullptr) {
     __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
     const int k = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -156,7 +170,10 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
     if (smode == 1) return;  // block-uniform
     __syncthreads();
     const bool set2 = phase && b < 2 * Bph && phase[b >= Bph ? b - Bph : b] != 0;
-    const double* Ai = (set2 ? Ainv2 : Ainv) + (size_t)k * d * d;
+    // CV folds: column b uses fold colset[b]'s tables (colset[b] < 0: the pool's)
+    const int cs = colset ? colset[b] : -1;
+    const int K_ = gridDim.x;
+    const double* Ai = (cs >= 0 ? Aset + (size_t)cs * K_ * d * d : (set2 ? Ainv2 : Ainv)) + (size_t)k * d * d;
     for (int j = w; j < d; j += nw) {
         double t = 0.0;
         for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][lane];
@@ -164,7 +181,7 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
         theta[((size_t)k * d + j) * Bp + b] = t;
     }
     __syncthreads();
-    const double* Gk = (set2 ? G2 : G) + (size_t)k * d * d;
+    const double* Gk = (cs >= 0 ? Gset + (size_t)cs * K_ * d * d : (set2 ? G2 : G)) + (size_t)k * d * d;
     for (int j = w; j < d; j += nw) {
         double gt = 0.0;
         for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++)
@@ -714,6 +731,107 @@ __global__ void k_bern_rr(const double* __restrict__ part, int nblk, int B, int 
     if (risk_trace && m >= 0) risk_trace[(size_t)m * B + b] = l / (double)n;
 }
 
+// ---------------------------------------------------------------- CV folds
+// CWB with 0/1 observation weights per replication: column b fits on the rows
+// whose fold differs from colfold[b] (colfold[b] = -1: every row).
+
+// per column (one block): f0 = mean of y over the training rows, rr = their sum of (y - f0)^2,
+// training / held-out row counts; argument checks (CWB_EINVAL)
+__global__ void k_fold_stats(const double* __restrict__ Y, int64_t n, const uint8_t* __restrict__ fold, int F,
+                             const int32_t* __restrict__ colfold, double* __restrict__ f0, double* __restrict__ rr,
+                             double* __restrict__ ntr, double* __restrict__ nho, double* offset_out, int* status) {
+    __shared__ double red[3][32];
+    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int fb = colfold[b];
+    if (fb >= F || fb < -1) cwb_dev_fail(status, CWB_EINVAL);
+    const double* y = Y + (size_t)b * n;
+    double sy = 0.0, c = 0.0;
+    bool bad = false, badf = false;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = y[i];
+        bad |= !isfinite(v);
+        badf |= fold[i] >= F;
+        if (fold[i] != fb) { sy += v; c += 1.0; }
+    }
+    if (bad) cwb_dev_fail(status, CWB_ENONFINITE);
+    if (badf) cwb_dev_fail(status, CWB_EINVAL);
+    sy = warp_sum(sy);
+    c = warp_sum(c);
+    if (lane == 0) { red[0][w] = sy; red[1][w] = c; }
+    __syncthreads();
+    double ts = 0.0, tc = 0.0;
+    for (int q = 0; q < nw; q++) { ts += red[0][q]; tc += red[1][q]; }
+    if (tc == 0.0) { if (threadIdx.x == 0) cwb_dev_fail(status, CWB_EINVAL); return; }
+    const double m = ts / tc;
+    double s2 = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (fold[i] != fb) { const double e = y[i] - m; s2 += e * e; }
+    s2 = warp_sum(s2);
+    if (lane == 0) red[2][w] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < nw; q++) t += red[2][q];
+        f0[b] = m;
+        rr[b] = t;
+        ntr[b] = tc;
+        nho[b] = (double)n - tc;
+        if (offset_out) offset_out[b] = m;
+    }
+}
+
+__global__ void k_fold_mask(const uint8_t* __restrict__ fold, int64_t n, int f, uint8_t* __restrict__ mask) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        mask[i] = fold[i] == f ? 1 : 0;
+}
+
+// r -= zhat[idx_k*(i)] on every row; partials of r^2 over the training and the held-out rows
+template <typename IdxT>
+__global__ void k_h6_fold(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* __restrict__ kstar,
+                          const IdxT* __restrict__ idx, const double* __restrict__ zhat,
+                          const uint8_t* __restrict__ fold, const int32_t* __restrict__ colfold, int B,
+                          double* __restrict__ part, int nblk) {
+    __shared__ double red[2][8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const int ks = kstar[b];
+    const int fb = b < B ? colfold[b] : -1;
+    const IdxT* ik = idx + (size_t)ks * n;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6;
+    const int64_t r1 = min(n, r0 + kRowsH6);
+    double at = 0.0, ah = 0.0;
+    for (int64_t i = r0 + w; i < r1; i += 8) {
+        const double v = Rt[(size_t)i * Bp + b] - zhat[(size_t)ik[i] * Bp + b];
+        Rt[(size_t)i * Bp + b] = v;
+        if (fold[i] == fb) ah += v * v;
+        else at += v * v;
+    }
+    red[0][w][lane] = at;
+    red[1][w][lane] = ah;
+    __syncthreads();
+    if (w < 2) {
+        double t = 0.0;
+        for (int q = 0; q < 8; q++) t += red[w][q][lane];
+        part[((size_t)w * nblk + blockIdx.x) * Bp + b] = t;
+    }
+}
+
+// rr[b] = training r^T r; risk_trace = rr / (2 n_train), val_risk_trace = held-out / (2 n_held) (0: none)
+__global__ void k_rr_fold(const double* __restrict__ part, int nblk, int B, int Bp, const double* __restrict__ ntr,
+                          const double* __restrict__ nho, int m, double* __restrict__ rr, double* risk_trace,
+                          double* val_risk_trace) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double st = 0.0, sh = 0.0;
+    for (int q = 0; q < nblk; q++) {
+        st += part[(size_t)q * Bp + b];
+        sh += part[((size_t)nblk + q) * Bp + b];
+    }
+    rr[b] = st;
+    if (risk_trace) risk_trace[(size_t)m * B + b] = st / (2.0 * ntr[b]);
+    if (val_risk_trace) val_risk_trace[(size_t)m * B + b] = nho[b] > 0.0 ? sh / (2.0 * nho[b]) : 0.0;
+}
+
 // ---------------------------------------------------------------- narrow path
 // binMatVec sums for a few residual vectors (B <= 4), e.g. one
 // findBestBaselearner on a single residual: HBM-bound on the index vector.  A CTA
@@ -897,6 +1015,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     cwb_release(w.acwb, s);
     cwb_release(w.pack, s);
     cwb_release(w.bern, s);
+    cwb_release(w.fold, s);
     w = cwb_train_ws();
     const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
     bool ok = true;
@@ -1153,6 +1272,82 @@ int cwb_train_bernoulli_general(cwb_ctx* c, const double* Y, int32_t B, double n
         c->launches += 3;
     }
     return cwb_check_launch(c, "Bernoulli train kernels");
+}
+
+// CWB with per-replication CV folds on the general path (kernels above).
+int cwb_train_folds_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* fold_of_row, int32_t F,
+                            const int32_t* fold_of_rep, double nu, int32_t M, double* offset_out,
+                            double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace,
+                            double* val_risk_trace, cudaStream_t s) {
+    int rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp, K = c->K, ns = c->n_star, d = c->d;
+    const int nblk = w.n_part;
+    // per fold: G_f, A_f^-1 (K x d x d each); per column: f0, training / held-out counts;
+    // partials 2 x nblk x Bp; column folds (padded); training-row bin counts; a fold mask (n bytes)
+    const size_t dbl = 2 * (size_t)F * K * d * d + 3 * (size_t)Bp + 2 * (size_t)nblk * Bp;
+    const size_t need = sizeof(double) * dbl + sizeof(int32_t) * Bp + sizeof(uint32_t) * (size_t)K * ns +
+                        (size_t)c->n + 16;
+    if (w.fold_bytes < need) {
+        cwb_release(w.fold, s);
+        w.fold = nullptr;
+        w.fold_bytes = 0;
+        if (cwb_alloc((void**)&w.fold, need, s) != cudaSuccess)
+            return cwb_set_error(c, CWB_ENOMEM, "CV-fold workspace allocation failed");
+        w.fold_bytes = need;
+    }
+    double* Gs = w.fold;
+    double* As = Gs + (size_t)F * K * d * d;
+    double* f0 = As + (size_t)F * K * d * d;
+    double* ntr = f0 + Bp;
+    double* nho = ntr + Bp;
+    double* part = nho + Bp;
+    int32_t* colfold = (int32_t*)(part + 2 * (size_t)nblk * Bp);
+    uint32_t* cnt_tr = (uint32_t*)(colfold + Bp);
+    uint8_t* mask = (uint8_t*)(cnt_tr + (size_t)K * ns);
+    k_fill_int<<<(Bp + 127) / 128, 128, 0, s>>>(colfold, Bp, -1);
+    CWB_CUDA_TRY(c, cudaMemcpyAsync(colfold, fold_of_rep, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, s));
+    // argument checks first (a replication without training rows is CWB_EINVAL, not a singular table)
+    k_fold_stats<<<B, 256, 0, s>>>(Y, c->n, fold_of_row, F, colfold, f0, w.rr, ntr, nho, offset_out, c->d_status);
+    const int gx = (int)std::min<int64_t>(1184, (c->n + 255) / 256);
+    for (int f = 0; f < F; f++) {  // training-row tables of fold f (binMatMat with 0/1 weights)
+        k_fold_mask<<<gx, 256, 0, s>>>(fold_of_row, c->n, f, mask);
+        rc = cwb_launch_masked_pool(c, mask, cnt_tr, Gs + (size_t)f * K * d * d, As + (size_t)f * K * d * d, s);
+        if (rc) return rc;
+        c->launches += 1;
+    }
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, f0, nullptr, w.Rt);
+    const size_t nagg = (size_t)B * K * d;
+    k_zero<<<(unsigned)min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_agg_out, nagg);
+    c->launches += 4;
+    for (int m = 0; m < M; m++) {
+        const int wpb = 8;
+        dim3 grid((unsigned)(((int64_t)K * ns + wpb - 1) / wpb), Bp / 32);
+        if (c->perm_bytes == 2)
+            k_h1<uint16_t><<<grid, wpb * 32, 0, s>>>(w.Rt, c->n, Bp, K, ns, c->off, (const uint16_t*)c->perm, w.U,
+                                                    fold_of_row, colfold);
+        else
+            k_h1<uint32_t><<<grid, wpb * 32, 0, s>>>(w.Rt, c->n, Bp, K, ns, c->off, (const uint32_t*)c->perm, w.U,
+                                                    fold_of_row, colfold);
+        k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+                                                w.delta, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, As, Gs, colfold);
+        k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, K, d, B, Bp, nu, m, w.kstar, theta_agg_out,
+                                              k_trace, sse_trace, nullptr, nullptr, nullptr);
+        k_zhat<<<dim3((ns + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, ns, d, B, Bp, nu, B, nu,
+                                                           w.zhat);
+        dim3 g6(nblk, Bp / 32);
+        if (c->idx_bytes == 1)
+            k_h6_fold<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, fold_of_row,
+                                                  colfold, B, part, nblk);
+        else
+            k_h6_fold<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat,
+                                                   fold_of_row, colfold, B, part, nblk);
+        k_rr_fold<<<(B + 127) / 128, 128, 0, s>>>(part, nblk, B, Bp, ntr, nho, m, w.rr, risk_trace, val_risk_trace);
+        c->launches += 6;
+    }
+    return cwb_check_launch(c, "CV-fold train kernels");
 }
 
 // ------------------------------------------------------------ row sharding

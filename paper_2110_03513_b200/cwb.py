@@ -21,7 +21,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 # the exported symbols declared in include/cwb.h
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
-           "cwb_set_path", "cwb_set_narrow", "cwb_find_best", "cwb_train", "cwb_train_bernoulli", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
+           "cwb_set_path", "cwb_set_narrow", "cwb_find_best", "cwb_train", "cwb_train_bernoulli", "cwb_train_folds", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
            "cwb_launch_count", "cwb_set_phase_timing", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
            "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_get_rows"]
 
@@ -88,6 +88,7 @@ def load() -> C.CDLL:
     L.cwb_find_best.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp]
     L.cwb_train.argtypes = [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_train_bernoulli.argtypes = [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.cwb_train_folds.argtypes = [_vp, _vp, _i32, _vp, _i32, _vp, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_train_acwb.argtypes = [_vp, _vp, _i32, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_train_hcwb.argtypes = [_vp, _vp, _i32, _vp, _f64, _f64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp]
@@ -286,6 +287,26 @@ def cwb_train_bernoulli(ctx, Y, nu: float = 0.05, M: int = 200, traces: bool = T
     return out
 
 
+def cwb_train_folds(ctx, Y, fold_of_row, F: int, fold_of_rep, nu: float = 0.05, M: int = 200):
+    """CWB with per-replication CV folds for Y[B][n]; fold_of_row uint8[n], fold_of_rep int32[B] (device)."""
+    import torch
+    Y = _dev_f64(Y, "Y")
+    if fold_of_row.dtype != torch.uint8 or fold_of_rep.dtype != torch.int32:
+        raise TypeError("fold_of_row must be uint8 and fold_of_rep int32")
+    ns, d, K, n = cwb_get_dims(ctx)
+    B = Y.shape[0]
+    f = dict(dtype=torch.float64, device=Y.device)
+    out = dict(offset=torch.empty(B, **f), theta_agg=torch.empty((B, K, d), **f),
+               k_trace=torch.empty((M, B), dtype=torch.int32, device=Y.device),
+               sse_trace=torch.empty((M, B), **f), risk_trace=torch.empty((M, B), **f),
+               val_risk_trace=torch.empty((M, B), **f))
+    _chk(load().cwb_train_folds(ctx, _ptr(Y), B, _ptr(fold_of_row.contiguous()), F, _ptr(fold_of_rep.contiguous()),
+                                float(nu), M, _ptr(out["offset"]), _ptr(out["theta_agg"]), _ptr(out["k_trace"]),
+                                _ptr(out["sse_trace"]), _ptr(out["risk_trace"]), _ptr(out["val_risk_trace"]),
+                                _stream(Y)), ctx)
+    return out
+
+
 def cwb_train_acwb(ctx, Y, nu: float = 0.05, gamma: float = 0.0034, M: int = 200, traces: bool = True):
     """Accelerated CWB (Alg. 2) for Y[B][n].  Returns a dict of device tensors."""
     import torch
@@ -450,6 +471,9 @@ class Pool:
 
     def train_bernoulli(self, Y, nu=0.05, M=200, traces=True):
         return cwb_train_bernoulli(self.ctx, Y, nu, M, traces)
+
+    def train_folds(self, Y, fold_of_row, F, fold_of_rep, nu=0.05, M=200):
+        return cwb_train_folds(self.ctx, Y, fold_of_row, F, fold_of_rep, nu, M)
 
     def train_acwb(self, Y, nu=0.05, gamma=0.0034, M=200, traces=True):
         return cwb_train_acwb(self.ctx, Y, nu, gamma, M, traces)
