@@ -488,12 +488,22 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     const double* __restrict__ G, const double* __restrict__ rrp, double* __restrict__ theta, double* __restrict__ delta,
     unsigned* __restrict__ ticket, int32_t* __restrict__ k_out, double* __restrict__ theta_out,
     double* __restrict__ sse_out) {
-    extern __shared__ double u[];  // [ns][B]
+    extern __shared__ double u[];  // [ns][B], then this learner's ZT [W][d], A^-1 [d][d], G [d][d]
     __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4], V[CWB_MAX_D][4];
-    __shared__ int s_j[148 + 1], s_slot[148 + 1], s_nj;
+    __shared__ int s_j[148 + 1], s_slot[148 + 1], s_nj, s_lw[2 * CWB_MAX_D];
     __shared__ bool last;
     const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
     const int lg = k / Ks, NU = Ks * ns, a0 = (k - lg * Ks) * ns;
+    double* zts = u + (((size_t)ns * B + 1) & ~(size_t)1);
+    double* ais = zts + (size_t)W * d;
+    double* gks = ais + (size_t)d * d;
+    // the learner's tables are copied to shared memory (cp.async) while the partials are combined
+    for (int a = tid; a < W * d; a += blockDim.x) cp_async<8>(zts + a, ZT + (size_t)k * W * d + a);
+    for (int a = tid; a < d * d; a += blockDim.x) {
+        cp_async<8>(ais + a, Ainv + (size_t)k * d * d + a);
+        cp_async<8>(gks + a, G + (size_t)k * d * d + a);
+    }
+    if (tid < 2 * d) s_lw[tid] = lwin[(size_t)k * d * 2 + tid];
     // the CTAs whose item range meets [lg nch, (lg+1) nch), and their slot for lg (warp 0, a lane per CTA)
     if (w == 0) {
         const int64_t it0 = (int64_t)lg * nch, it1 = it0 + nch;
@@ -537,13 +547,14 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
         for (; m < nj; m++) v += pq[((size_t)s_j[m] * nslot + s_slot[m]) * NU];
         u[e] = v;
     }
+    cp_async_commit_wait_all();
     __syncthreads();
     // s_j = sum over the design-point window of basis j of Zb[l][j] u(l)   (ZT: window-major basis)
     for (int j = w; j < d; j += nw) {
-        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+        const int lb = s_lw[2 * j], le = s_lw[2 * j + 1];
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int x = lane; x < le - lb; x += 32) {
-            const double z = ZT[((size_t)k * W + x) * d + j];
+            const double z = zts[(size_t)x * d + j];
 #pragma unroll
             for (int q = 0; q < 4; q++)
                 if (q < B) acc[q] += z * u[(lb + x) * B + q];
@@ -557,7 +568,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     __syncthreads();
     const int jq = tid / B, qq = tid - jq * B;
     if (tid < d * B) {  // theta = A^-1 s (cached inverse)
-        const double* Ai = Ainv + ((size_t)k * d + jq) * d;
+        const double* Ai = ais + (size_t)jq * d;
         double t = 0.0;
         for (int jp = 0; jp < d; jp++) t += Ai[jp] * S[jp][qq];
         Th[jq][qq] = t;
@@ -565,7 +576,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     }
     __syncthreads();
     if (tid < d * B) {  // theta_j (2 s_j - (G theta)_j), G banded (|j - j'| <= 3)
-        const double* Gk = G + ((size_t)k * d + jq) * d;
+        const double* Gk = gks + (size_t)jq * d;
         double gt = 0.0;
         for (int jp = max(0, jq - (CWB_SPW - 1)); jp <= min(d - 1, jq + CWB_SPW - 1); jp++) gt += Gk[jp] * Th[jp][qq];
         V[jq][qq] = Th[jq][qq] * (2.0 * S[jq][qq] - gt);
@@ -745,7 +756,7 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
     cudaFuncSetAttribute(k_h1_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_h1_stream<<<dim3(N, B), kStreamT, smem, s>>>(R, c->n, p.nch, p.Ks, ns, p.nitems, nslot, (const uint2*)p.ent,
                                                     p.gtab, p.dest, p.isize, p.ibase, p.wst, p.part, rrp, c->d_status);
-    const size_t fsm = sizeof(double) * (size_t)ns * B;
+    const size_t fsm = sizeof(double) * ((((size_t)ns * B + 1) & ~(size_t)1) + (size_t)c->W * d + 2 * (size_t)d * d);
     cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
     k_fit_narrow<<<K, 1024, fsm, s>>>(p.part, K, ns, p.Ks, p.nch, p.nitems, N, nslot, B, d, c->W, c->ZT, c->lwin,
                                       c->Ainv, c->G, rrp, th, de, ticket, k_out, theta_out, sse_out);
