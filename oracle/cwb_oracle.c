@@ -386,6 +386,7 @@ int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int m
 
 typedef struct {
     double *s, *theta, *fz, *A;
+    double* sse_all;  /* K: SSE of every learner (tie-following mode only) */
 } scratch;
 
 static void scratch_init(scratch* w, int d, int n_star) {
@@ -393,9 +394,10 @@ static void scratch_init(scratch* w, int d, int n_star) {
     w->theta = (double*)malloc(sizeof(double) * d);
     w->fz = (double*)malloc(sizeof(double) * (n_star > 0 ? n_star : 1));
     w->A = (double*)malloc(sizeof(double) * d * d);
+    w->sse_all = NULL;
 }
 
-static void scratch_free(scratch* w) { free(w->s); free(w->theta); free(w->fz); free(w->A); }
+static void scratch_free(scratch* w) { free(w->s); free(w->theta); free(w->fz); free(w->A); free(w->sse_all); }
 
 /* Fit learner k to r (supp. eq. pen-regr): theta = (G + lambda D)^-1 Z^T r,
  * and its SSE = sum_i (r_i - Z(i) theta)^2 (unpenalised, reading G12). */
@@ -479,6 +481,9 @@ typedef struct {
     double *offset, *theta_agg, *sse_trace, *risk_trace, *gap_trace, *f_out;
     int32_t* k_trace;
     int loss; /* ORC_LOSS_L2 or ORC_LOSS_BERNOULLI */
+    const int32_t* follow; /* [M][B] learner sequence to follow at verified near-ties (NULL: none) */
+    double tie_rtol;
+    int32_t* followed;     /* [B] number of iterations at which the followed learner was taken */
 } train_job;
 
 /* Bernoulli loss of the logistic model, y in {0, 1}:
@@ -513,7 +518,17 @@ static void train_one(const train_job* J, int b, scratch* w, double* f, double* 
         /* lines 5-9: fit every learner, SSE, argmin */
         int32_t ks;
         double sse, gap;
-        find_best_ws(p, r, w, &ks, theta, &sse, NULL, &gap);
+        find_best_ws(p, r, w, &ks, theta, &sse, J->follow ? w->sse_all : NULL, &gap);
+        if (J->follow) {  /* tie-following: take the given learner when its SSE is
+                             within tie_rtol of the minimum -- several results are correct at a near-tie */
+            const int32_t kf = J->follow[(size_t)m * B + b];
+            if (kf != ks && kf >= 0 && kf < K && w->sse_all[kf] - sse <= J->tie_rtol * fabs(sse)) {
+                sse = w->sse_all[kf];
+                ks = kf;
+                fit_one(p, ks, r, w, theta);
+                J->followed[b]++;
+            }
+        }
         /* line 10: f += nu b_{k*}(x, theta) */
         const double* Zb = p->Zb + (size_t)ks * p->n_star * d;
         const int32_t* idx = p->idx + (size_t)ks * n;
@@ -549,6 +564,7 @@ static void* train_worker(void* arg) {
     int64_t n = J->p->n;
     scratch w;
     scratch_init(&w, J->p->d, J->p->n_star);
+    if (J->follow) w.sse_all = (double*)malloc(sizeof(double) * J->p->K);
     double* f = (double*)malloc(sizeof(double) * n);
     double* r = (double*)malloc(sizeof(double) * n);
     double* theta = (double*)malloc(sizeof(double) * J->p->d);
@@ -560,25 +576,36 @@ static void* train_worker(void* arg) {
 
 static int train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
                       double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
-                      double* risk_trace, double* gap_trace, double* f_out);
+                      double* risk_trace, double* gap_trace, double* f_out, const int32_t* follow,
+                      double tie_rtol, int32_t* followed);
 
 int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n_threads,
               double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
               double* risk_trace, double* gap_trace, double* f_out) {
     return train_loss(p, Y, B, ORC_LOSS_L2, nu, M, n_threads, offset, theta_agg, k_trace, sse_trace, risk_trace,
-                      gap_trace, f_out);
+                      gap_trace, f_out, NULL, 0.0, NULL);
+}
+
+int orc_train_follow(const orc_pool* p, const double* Y, int B, double nu, int M, int n_threads,
+                     const int32_t* follow, double tie_rtol, double* offset, double* theta_agg, int32_t* k_trace,
+                     double* sse_trace, double* risk_trace, double* gap_trace, double* f_out, int32_t* followed) {
+    if (!follow || !followed || !(tie_rtol >= 0.0)) return ORC_EINVAL;
+    for (int b = 0; b < B; b++) followed[b] = 0;
+    return train_loss(p, Y, B, ORC_LOSS_L2, nu, M, n_threads, offset, theta_agg, k_trace, sse_trace, risk_trace,
+                      gap_trace, f_out, follow, tie_rtol, followed);
 }
 
 int orc_train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
                    double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
                    double* risk_trace, double* gap_trace, double* f_out) {
     return train_loss(p, Y, B, loss, nu, M, n_threads, offset, theta_agg, k_trace, sse_trace, risk_trace,
-                      gap_trace, f_out);
+                      gap_trace, f_out, NULL, 0.0, NULL);
 }
 
 static int train_loss(const orc_pool* p, const double* Y, int B, int loss, double nu, int M, int n_threads,
                       double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
-                      double* risk_trace, double* gap_trace, double* f_out) {
+                      double* risk_trace, double* gap_trace, double* f_out, const int32_t* follow,
+                      double tie_rtol, int32_t* followed) {
     if (!p || p->K < 1) return ORC_EEMPTY;
     if (B < 1 || M < 0 || !(nu >= 0.0) || (loss != ORC_LOSS_L2 && loss != ORC_LOSS_BERNOULLI)) return ORC_EINVAL;
     for (int64_t a = 0; a < (int64_t)B * p->n; a++)
@@ -598,7 +625,7 @@ static int train_loss(const orc_pool* p, const double* Y, int B, int loss, doubl
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
     for (int t = 0; t < n_threads; t++) {
         train_job J = {p, Y, B, M, t, n_threads, nu, offset, theta_agg, sse_trace,
-                       risk_trace, gap_trace, f_out, k_trace, loss};
+                       risk_trace, gap_trace, f_out, k_trace, loss, follow, tie_rtol, followed};
         jobs[t] = J;
     }
     for (int t = 1; t < n_threads; t++) pthread_create(&th[t], NULL, train_worker, &jobs[t]);

@@ -130,6 +130,14 @@ int orc_train(const orc_pool* p, const double* Y, int B, double nu, int M, int n
               double* offset, double* theta_agg, int32_t* k_trace, double* sse_trace,
               double* risk_trace, double* gap_trace, double* f_out);
 
+/* orc_train (L2) in tie-following mode: at iteration m, replication b takes
+ * the learner follow[m][b] instead of its own argmin when that learner's SSE exceeds the minimum
+ * by at most tie_rtol * SSE_min (a near-tie: several selections are correct); followed[b] counts
+ * those iterations.  Any other difference is kept (the comparator then reports it). */
+int orc_train_follow(const orc_pool* p, const double* Y, int B, double nu, int M, int n_threads,
+                     const int32_t* follow, double tie_rtol, double* offset, double* theta_agg, int32_t* k_trace,
+                     double* sse_trace, double* risk_trace, double* gap_trace, double* f_out, int32_t* followed);
+
 /* orc_train with a loss: ORC_LOSS_L2 (as orc_train) or ORC_LOSS_BERNOULLI, y in {0, 1}:
  * L(y, f) = log(1 + exp(f)) - y f, pseudo residuals r = y - 1/(1 + exp(-f))
  * (P:L833), offset log(p/(1-p)) with p = mean(y) (Alg. 1 line 2),

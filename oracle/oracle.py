@@ -98,6 +98,8 @@ def lib():
         L.orc_train_folds.argtypes = [C.POINTER(_Pool), _D, C.c_int, _P(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_int,
                                       _I, C.c_double, C.c_int, C.c_int, _D, _D, _I, _D, _D, _D, C.c_void_p,
                                       C.c_void_p]
+        L.orc_train_follow.argtypes = [C.POINTER(_Pool), _D, C.c_int, C.c_double, C.c_int, C.c_int, _I, C.c_double,
+                                       _D, _D, _I, _D, _D, C.c_void_p, C.c_void_p, _I]
         L.orc_train_acwb.argtypes = [C.c_void_p, _D, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _D, _D, _D,
                                      _I, _I, _D, _D, _D, _D, _D, _D, _D]
         L.orc_train_hcwb.argtypes = [C.c_void_p, _D, C.c_int, _P(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_double,
@@ -349,6 +351,25 @@ class Pool:
         _chk(lib().orc_train(self._p, Y, B, nu, M, threads, off, agg, kt, st, rt,
                              gt.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p)), "train")
         return TrainResult(off, agg, kt, st, rt, gt, f)
+
+    def train_follow(self, Y, follow, tie_rtol: float = 1e-10, nu: float = 0.05, M: int = 200, threads: int = 1):
+        """Alg. 1 supp. in tie-following mode: at a near-tie (SSE within tie_rtol of the minimum) the
+        learner follow[m][b] is taken.  Returns (TrainResult, followed[B])."""
+        Y = _f64(np.atleast_2d(Y))
+        B = Y.shape[0]
+        K, d = self.K, self.d
+        off = np.empty(B)
+        agg = np.empty((B, K, d))
+        kt = np.empty((M, B), dtype=np.int32)
+        st = np.empty((M, B))
+        rt = np.empty((M, B))
+        gt = np.empty((M, B))
+        f = np.empty((B, self.n))
+        fol = np.zeros(B, dtype=np.int32)
+        _chk(lib().orc_train_follow(self._p, Y, B, nu, M, threads, np.ascontiguousarray(follow, dtype=np.int32),
+                                    tie_rtol, off, agg, kt, st, rt, gt.ctypes.data_as(C.c_void_p),
+                                    f.ctypes.data_as(C.c_void_p), fol), "train_follow")
+        return TrainResult(off, agg, kt, st, rt, gt, f), fol
 
     def train_bernoulli(self, Y, nu: float = 0.05, M: int = 200, threads: int = 1) -> TrainResult:
         """Alg. 1 supp. with the Bernoulli loss, y in {0, 1}, for B

@@ -359,3 +359,29 @@ def test_fit_host_matches_device_api():
     g = _gpu_train(pg, ds.Y, c, 0)
     for k in g:
         assert (h[k] == g[k]).all(), k
+
+
+@pytest.mark.parametrize("name,path", [("R1", 1), ("R1", 2), ("R0", 1)])
+def test_train_parity_tie_following(name, path):
+    # every replication, every iteration: the oracle follows the GPU's choice only at verified near-ties
+    # (SSE within TIE_RTOL of its minimum), so the learner sequences must be identical and all traces
+    # and parameters must agree everywhere
+    from parity_util import TIE_RTOL
+    ds = S.make(name)
+    c = ds.cfg
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    pg.set_path(path)
+    out = pg.train(dev(ds.Y), nu=c.nu, M=c.M)
+    pg.status()
+    g = {k: host(v) for k, v in out.items()}
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    o, followed = po.train_follow(ds.Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=c.nu, M=c.M, threads=8)
+    assert (o.k_trace == g["k_trace"]).all(), "a non-tie selection differs"
+    for key, ref in (("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
+        ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())
+        assert ok, f"{key}: {e}"
+    ok, e = close(g["theta_agg"], o.theta_agg, RTOL, scale=np.abs(o.theta_agg).max())
+    assert ok, e
+    ok, e = close(g["offset"], o.offset, 1e-12)
+    assert ok, e
+    pg.close()

@@ -817,3 +817,34 @@ def test_folds_errors():
         p.train_folds(Y[:1], fold, 4, np.array([4]), M=2)        # fold id >= F
     with pytest.raises(O.OracleError):
         p.train_folds(Y[:1], np.zeros_like(fold), 1, np.array([0]), M=2)  # fold 0 holds out every row
+
+
+# ------------------------------------------------------- tie-following mode
+
+def test_follow_own_sequence_is_identity_and_non_ties_are_not_followed():
+    p, X, y = _acwb_pool(seed=7)
+    Y = np.stack([y, -y, 0.5 * y])
+    ref = p.train(Y, nu=0.1, M=40)
+    res, fol = p.train_follow(Y, ref.k_trace, tie_rtol=1e-10, nu=0.1, M=40)
+    assert (fol == 0).all() and (res.k_trace == ref.k_trace).all() and (res.theta_agg == ref.theta_agg).all()
+    # a sequence that differs where the SSE gap is large: not followed, the own choice is kept
+    bad = (ref.k_trace + 1) % p.K
+    res2, fol2 = p.train_follow(Y, bad, tie_rtol=1e-10, nu=0.1, M=40)
+    assert (fol2 == 0).all() and (res2.k_trace == ref.k_trace).all()
+
+
+def test_follow_takes_a_tie():
+    # two identical learners (columns 0 and 1): every selection of learner 0 is an exact tie with 1
+    rng = np.random.default_rng(2)
+    x = rng.uniform(0, 1, 400)
+    X = np.stack([x, x, rng.uniform(0, 1, 400)])
+    p = O.Pool(X, O.Config(n_knots=6), O.MODE_BINNED)
+    y = np.sin(6 * x) + 0.2 * rng.standard_normal(400)
+    ref = p.train(y, nu=0.1, M=20)
+    assert (ref.k_trace[:, 0] != 1).all()  # lowest index wins the exact ties
+    follow = np.where(ref.k_trace == 0, 1, ref.k_trace)
+    res, fol = p.train_follow(y, follow, tie_rtol=0.0, nu=0.1, M=20)
+    assert fol[0] == (ref.k_trace == 0).sum() > 0
+    assert (res.k_trace == follow).all()
+    # the fitted model is the same (learners 0 and 1 are the same function)
+    assert np.abs(res.f - ref.f).max() <= 1e-12 * np.abs(ref.f).max()
