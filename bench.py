@@ -132,33 +132,49 @@ def dist_env():
     return w.size, w.rank, w.local_rank
 
 
-def oracle_sample(cfg, seconds_target=12.0, threads=None):
-    """Time the oracle (binned mode = the paper's Algorithm, as it stands) on a bounded sample."""
+def oracle_sample(cfg, seconds_target=12.0, threads=None, algo="cwb", unbinned=False):
+    """Time the oracle as it stands (binned mode = the paper's Algorithm binMatVec; unbinned mode for
+    --unbinned) on a bounded sample of the workload, running the same algorithm as the GPU arm."""
     from oracle import oracle as O
     threads = threads or os.cpu_count() or 1
     c = cfg
     oc = O.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots,
                   degree=c.degree, df=c.df)
+    mode = O.MODE_UNBINNED if unbinned else O.MODE_BINNED
+    fits = 2 if algo in ("acwb", "hcwb") else 1  # evaluations per iteration as in the GPU arm (HCWB: upper bound)
+
+    def run(pool, ds, M, th):
+        Y = S.binary_targets(ds) if algo == "bernoulli" else ds.Y
+        if algo == "acwb":
+            return pool.train_acwb(Y, nu=c.nu, gamma=0.0034, M=M, threads=th)
+        if algo == "hcwb":
+            return pool.train_hcwb(Y, S.validation_mask(c.n), nu=c.nu, gamma=0.037, pat0=5, M=M, threads=th)
+        if algo == "bernoulli":
+            return pool.train_bernoulli(Y, nu=c.nu, M=M, threads=th)
+        return pool.train(Y, nu=c.nu, M=M, threads=th)
+
     # probe: one replication, a few iterations
     ds = S.make(c, reps=range(min(c.B, threads)))
     t0 = time.perf_counter()
-    pool = O.Pool(ds.X, oc, O.MODE_BINNED)
+    pool = O.Pool(ds.X, oc, mode)
     t_init = time.perf_counter() - t0
     M_probe = max(1, min(c.M, 5))
+    ds1 = S.make(c, reps=range(1))
     t0 = time.perf_counter()
-    pool.train(ds.Y[:1], nu=c.nu, M=M_probe, threads=1)
+    run(pool, ds1, M_probe, 1)
     per_rep_iter = (time.perf_counter() - t0) / M_probe
     reps = int(max(1, min(c.B, seconds_target * threads / max(per_rep_iter * c.M, 1e-9))))
     reps = max(min(reps, c.B), 1)
     ds = S.make(c, reps=range(reps))
     t0 = time.perf_counter()
-    pool = O.Pool(ds.X, oc, O.MODE_BINNED)
-    pool.train(ds.Y, nu=c.nu, M=c.M, threads=threads)
+    pool = O.Pool(ds.X, oc, mode)
+    run(pool, ds, c.M, threads)
     dt = time.perf_counter() - t0
-    evals = c.K * c.n * reps * c.M
+    evals = fits * c.K * c.n * reps * c.M
+    kind = "unbinned mode" if unbinned else "binned mode (Algorithm binMatVec, P:L898-904)"
     return {"value": evals / dt, "unit": UNIT, "cores": min(threads, reps), "kind": "oracle",
-            "sample": f"{c.name}: {reps} of {c.B} replications x M={c.M} iterations, oracle binned mode "
-                      f"(Algorithm binMatVec, P:L898-904), pool build included; {dt:.2f} s",
+            "sample": f"{c.name}: {reps} of {c.B} replications x M={c.M} iterations, oracle {algo}, {kind}, "
+                      f"pool build included; {dt:.2f} s",
             "seconds": dt, "init_s": t_init}
 
 
@@ -169,7 +185,8 @@ def run_reference(args, cfg):
     threads = os.cpu_count() or 1
     res = []
     for i in range(args.warmup + args.steps):
-        r = oracle_sample(cfg, seconds_target=args.ref_seconds, threads=threads)
+        r = oracle_sample(cfg, seconds_target=args.ref_seconds, threads=threads, algo=args.algo,
+                          unbinned=args.unbinned)
         if i >= args.warmup:
             res.append(r)
     v = float(np.mean([r["value"] for r in res]))
@@ -178,7 +195,8 @@ def run_reference(args, cfg):
             "ms_per_step": float(np.mean([r["seconds"] for r in res]) * 1e3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper Sec. 4.1.1 generator, seeded)",
-            "config": workload_config(cfg, None, None),
+            "config": dict(workload_config(cfg, None, None), algo=args.algo,
+                           learners="unbinned" if args.unbinned else "binned"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": res[0]["cores"], "kind": "oracle",
                              "sample": res[0]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -453,7 +471,8 @@ def main():
         }
         if not args.no_cpu_baseline and ws == 1:
             try:
-                line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg).items()
+                line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, algo=args.algo,
+                                                                        unbinned=args.unbinned).items()
                                         if k in ("value", "unit", "cores", "kind", "sample")}
             except Exception as e:  # keep the GPU line even if the host leg fails
                 line["cpu_baseline"] = {"error": str(e)}
