@@ -3,6 +3,7 @@
 // arithmetic step of the method runs in the kernels of cwb_init.cu,
 // cwb_fused.cu and cwb_iter.cu.  There is no CPU fallback.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -167,6 +168,7 @@ void cwb_free(cwb_ctx* c) {
     for (void* p : bufs) cwb_release(p, s);
     cwb_stream_release(c, s);
     cwb_nb_release(c, s);
+    cwb_release(c->h1c, s);
     if (c->ev_plan) cudaEventDestroy(c->ev_plan);
     if (c->ev_csr) cudaEventDestroy(c->ev_csr);
     if (c->s2) cudaStreamDestroy(c->s2);
@@ -197,6 +199,7 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     c->df = cfg.df; c->df_kind = cfg.df_kind;
     c->batch_hint = cfg.batch_hint > 0 && !cfg.unbinned ? cfg.batch_hint : 0;
     c->nb = cfg.unbinned != 0;
+    if (const char* e = getenv("CWB_H1_CHUNKING")) c->h1_chunking = atoi(e);  // A/B measurement switch
     if (c->nb) c->path = 2;  // per-iteration kernels only
     c->idx_bytes = ns <= 256 ? 1 : 2;
     c->perm_bytes = n <= 65536 ? 2 : 4;

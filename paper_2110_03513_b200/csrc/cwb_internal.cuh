@@ -68,6 +68,9 @@ struct cwb_ctx {
     int32_t perm_bytes = 2;  // 2: uint16 row ids, 4: uint32
     int32_t path = 0;        // 0 auto, 1 fused, 2 general
     int32_t narrow_mode = 0; // narrow findBest H1: 0 stream plan (fallback histograms), 1 histograms
+    int32_t h1_chunking = 1; // general-path H1 swept in L2-sized row chunks when a tile exceeds L2 (CWB_H1_CHUNKING=0 off)
+    uint32_t* h1c = nullptr; // chunked H1: [K][nch][n*] row counts, then starts
+    int32_t h1c_nch = 0;
     cudaStream_t stream = 0;
     int status = CWB_OK;
     std::string err;

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "cwb_internal.cuh"
 
@@ -130,6 +131,67 @@ __global__ void k_h1(const double* __restrict__ Rt, int64_t n, int Bp, int K, in
     }
     for (; q < a1; q++) acc += col[(size_t)pk[q] * Bp];
     U[(size_t)g * Bp + b] = acc;
+}
+
+// H1 over a chunk of rows [c CR, (c+1) CR): when a 32-column tile of the residual block
+// (n x 256 bytes) exceeds L2, the bins are swept chunk by chunk (one launch per chunk) so that
+// the K learners' gathers of a chunk hit L2.  The rows of bin l inside chunk c are a contiguous
+// piece of the bin's ascending row list: perm[k][cst[(k nch + c) ns + l] ...] with ccnt rows.
+// U += the chunk's sums (chunk 0 writes), so every bin sum is added in chunk order.
+__global__ void k_h1_chunk_count(const void* __restrict__ idx, int idx_bytes, int64_t n, int ns, int64_t CR,
+                                 int nch, uint32_t* __restrict__ cnt) {
+    extern __shared__ uint32_t h[];
+    const int c = blockIdx.x, k = blockIdx.y;
+    for (int l = threadIdx.x; l < ns; l += blockDim.x) h[l] = 0;
+    __syncthreads();
+    const int64_t r0 = (int64_t)c * CR, r1 = min(n, r0 + CR);
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const uint32_t l = idx_bytes == 1 ? ((const uint8_t*)idx)[(size_t)k * n + i]
+                                          : ((const uint16_t*)idx)[(size_t)k * n + i];
+        atomicAdd(&h[l], 1u);
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < ns; l += blockDim.x) cnt[((size_t)k * nch + c) * ns + l] = h[l];
+}
+
+__global__ void k_h1_chunk_start(uint32_t* __restrict__ cnt_cst, const int32_t* __restrict__ off, int K, int ns,
+                                 int nch) {
+    // in place: cnt -> (start, count) pairs packed as start in the first K nch ns words' twin array
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)K * ns) return;
+    const int k = (int)(g / ns), l = (int)(g - (int64_t)k * ns);
+    uint32_t run = (uint32_t)off[(size_t)k * (ns + 1) + l];
+    uint32_t* cst = cnt_cst + (size_t)K * nch * ns;
+    for (int c = 0; c < nch; c++) {
+        const size_t e = ((size_t)k * nch + c) * ns + l;
+        cst[e] = run;
+        run += cnt_cst[e];
+    }
+}
+
+template <typename PermT>
+__global__ void k_h1c(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns, int nch, int c,
+                      const uint32_t* __restrict__ ccnt, const PermT* __restrict__ perm, double* __restrict__ U) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+    if (g >= (int64_t)K * ns) return;
+    const int k = (int)(g / ns), l = (int)(g - (int64_t)k * ns);
+    const int b = blockIdx.y * 32 + lane;
+    const size_t e = ((size_t)k * nch + c) * ns + l;
+    const uint32_t cnt = ccnt[e], a0 = ccnt[(size_t)K * nch * ns + e], a1 = a0 + cnt;
+    const PermT* pk = perm + (size_t)k * n;
+    const double* col = Rt + b;
+    double acc = 0.0;
+    uint32_t q = a0;
+    for (; q + 4 <= a1; q += 4) {
+        const uint32_t i0 = pk[q], i1 = pk[q + 1], i2 = pk[q + 2], i3 = pk[q + 3];
+        const double v0 = col[(size_t)i0 * Bp], v1 = col[(size_t)i1 * Bp];
+        const double v2 = col[(size_t)i2 * Bp], v3 = col[(size_t)i3 * Bp];
+        acc += v0; acc += v1; acc += v2; acc += v3;
+    }
+    for (; q < a1; q++) acc += col[(size_t)pk[q] * Bp];
+    double* up = U + (size_t)g * Bp + b;
+    *up = c == 0 ? acc : *up + acc;
 }
 
 // H2-H4 for one learner (blockIdx.x) and 32 replications (blockIdx.y)
@@ -1041,10 +1103,44 @@ static void launch_h1(const double* Rt, int64_t n, int Bp, int K, int ns, const 
     k_h1<PermT><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, off, (const PermT*)perm, U);
 }
 
+// rows per chunk of the chunked H1: a 32-column tile of one chunk (rows x 256 B) well inside L2
+static constexpr int64_t kH1ChunkBytes = 40ll << 20;  // R4 sweep: 24 MB 934, 40 MB 913, 64 MB 921, 96 MB 985 ms/step
+
 static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_t* off,
                const void* perm, int perm_bytes, double* U, cudaStream_t s) {
-    if (perm_bytes == 2) launch_h1<uint16_t>(Rt, c->n, Bp, K, ns, off, perm, U, s);
-    else launch_h1<uint32_t>(Rt, c->n, Bp, K, ns, off, perm, U, s);
+    const int64_t n = c->n;
+    const bool chunked = n * 256 > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off;
+    if (chunked) {
+        static const int64_t chunk_bytes =
+            getenv("CWB_H1_CHUNK_MB") ? (int64_t)atoi(getenv("CWB_H1_CHUNK_MB")) << 20 : kH1ChunkBytes;
+        const int64_t CR = chunk_bytes / 256;
+        const int nch = (int)((n + CR - 1) / CR);
+        if (!c->h1c || c->h1c_nch != nch) {  // per (learner, chunk, bin) row counts and starts, once per pool
+            cwb_release(c->h1c, s);
+            c->h1c = nullptr;
+            if (cwb_alloc((void**)&c->h1c, 2 * sizeof(uint32_t) * (size_t)K * nch * ns, s) != cudaSuccess) {
+                cwb_set_error(c, CWB_ENOMEM, "chunked H1 tables");
+                return;
+            }
+            c->h1c_nch = nch;
+            k_h1_chunk_count<<<dim3(nch, K), 1024, sizeof(uint32_t) * ns, s>>>(c->idx, c->idx_bytes, n, ns, CR, nch,
+                                                                             c->h1c);
+            k_h1_chunk_start<<<(unsigned)(((int64_t)K * ns + 255) / 256), 256, 0, s>>>(c->h1c, c->off, K, ns, nch);
+            c->launches += 2;
+        }
+        const int wpb = 8;
+        dim3 grid((unsigned)(((int64_t)K * ns + wpb - 1) / wpb), Bp / 32);
+        for (int ch = 0; ch < nch; ch++) {
+            if (perm_bytes == 2)
+                k_h1c<uint16_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint16_t*)perm, U);
+            else
+                k_h1c<uint32_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint32_t*)perm, U);
+        }
+        c->launches += nch;
+        return;
+    }
+    if (perm_bytes == 2) launch_h1<uint16_t>(Rt, n, Bp, K, ns, off, perm, U, s);
+    else launch_h1<uint32_t>(Rt, n, Bp, K, ns, off, perm, U, s);
     c->launches++;
 }
 

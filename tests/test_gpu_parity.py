@@ -385,3 +385,35 @@ def test_train_parity_tie_following(name, path):
     ok, e = close(g["offset"], o.offset, 1e-12)
     assert ok, e
     pg.close()
+
+
+@pytest.mark.slow
+def test_general_h1_chunked_equals_unchunked_r4():
+    # the row-chunked H1 (32-column tile of R beyond L2) against the one-sweep H1 on R4
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.getcwd())
+import cwb_synth as S
+from parity_util import gpu_cfg_of
+from paper_2110_03513_b200 import cwb
+ds = S.make("R4", reps=range(6))
+pg = cwb.Pool(torch.as_tensor(ds.X, device="cuda"), gpu_cfg_of(ds.cfg))
+out = pg.train(torch.as_tensor(ds.Y, device="cuda"), nu=0.05, M=30)
+pg.status()
+torch.cuda.synchronize()
+np.savez(sys.argv[1], **{k: v.cpu().numpy() for k, v in out.items()})
+'''
+    res = []
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for mode in ("0", "1"):
+        path = f"/tmp/h1chunk_{mode}.npz"
+        env = dict(os.environ, CWB_H1_CHUNKING=mode, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, cwd=root)
+        res.append(np.load(path))
+    a, b = res
+    assert (a["k_trace"] == b["k_trace"]).mean() >= 0.99
+    same = (a["k_trace"] == b["k_trace"]).all(0)
+    assert np.abs(a["theta_agg"][same] - b["theta_agg"][same]).max() <= 1e-11 * np.abs(a["theta_agg"]).max()
