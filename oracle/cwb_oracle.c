@@ -330,6 +330,7 @@ int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int m
     int d = orc_basis_dim(cfg->degree, cfg->n_knots);
     orc_pool* p = (orc_pool*)calloc(1, sizeof(orc_pool));
     p->K = K; p->n = n; p->n_star = n_star; p->d = d; p->mode = mode;
+    p->degree = cfg->degree; p->n_knots = cfg->n_knots;
     p->lo = (double*)malloc(sizeof(double) * K);
     p->hi = (double*)malloc(sizeof(double) * K);
     p->z = (double*)malloc(sizeof(double) * K * n_star);
@@ -1149,6 +1150,29 @@ int orc_train_folds(const orc_pool* p, const double* Y, int B, const uint8_t* fo
 int orc_predict(const orc_pool* p, const double* Xnew, int64_t m, const double* offset,
                 const double* theta_agg, int B, double* out) {
     int d = p->d, K = p->K, n_star = p->n_star;
+    if (p->mode == ORC_MODE_UNBINNED) {
+        /* unbinned learners: the basis at x itself, x clamped to the training range
+         * [min, max] of the learner (reading U2: the binned pool's end-bin rule) */
+        double* zr = (double*)malloc(sizeof(double) * d);
+        for (int64_t i = 0; i < m; i++)
+            for (int k = 0; k < K; k++)
+                if (!isfinite(Xnew[(size_t)k * m + i])) { free(zr); return ORC_ENONFINITE; }
+        for (int bb = 0; bb < B; bb++)
+            for (int64_t i = 0; i < m; i++) {
+                double v = offset[bb];
+                for (int k = 0; k < K; k++) {
+                    double x = Xnew[(size_t)k * m + i];
+                    if (x < p->lo[k]) x = p->lo[k];
+                    if (x > p->hi[k]) x = p->hi[k];
+                    orc_bspline_basis(&x, 1, p->lo[k], p->hi[k], p->degree, p->n_knots, zr);
+                    const double* th = theta_agg + ((size_t)bb * K + k) * d;
+                    for (int j = 0; j < d; j++) v += zr[j] * th[j];
+                }
+                out[(size_t)bb * m + i] = v;
+            }
+        free(zr);
+        return ORC_OK;
+    }
     int32_t* lix = (int32_t*)malloc(sizeof(int32_t) * (size_t)K * (m > 0 ? m : 1));
     for (int k = 0; k < K; k++) {
         const double* bnd = p->bnd + (size_t)k * (n_star - 1);

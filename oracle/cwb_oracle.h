@@ -108,6 +108,7 @@ typedef struct {
     double* D;      /* d x d */
     double* lambda; /* K */
     double* L;      /* K x d x d   Cholesky of G + lambda D (binned mode cache) */
+    int degree, n_knots;  /* of the basis (unbinned prediction evaluates it at new x) */
 } orc_pool;
 
 int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int mode, orc_pool** out);

@@ -60,7 +60,7 @@ class _Pool(C.Structure):
                 ("idx", C.POINTER(C.c_int32)), ("Zb", C.POINTER(C.c_double)),
                 ("Zx", C.POINTER(C.c_double)), ("G", C.POINTER(C.c_double)),
                 ("D", C.POINTER(C.c_double)), ("lam", C.POINTER(C.c_double)),
-                ("L", C.POINTER(C.c_double))]
+                ("L", C.POINTER(C.c_double)), ("degree", C.c_int), ("n_knots", C.c_int)]
 
 
 def lib():

@@ -848,3 +848,22 @@ def test_follow_takes_a_tie():
     assert (res.k_trace == follow).all()
     # the fitted model is the same (learners 0 and 1 are the same function)
     assert np.abs(res.f - ref.f).max() <= 1e-12 * np.abs(ref.f).max()
+
+
+def test_unbinned_predict_reproduces_the_fit_and_clamps():
+    # unbinned pool (basis at x itself): prediction at the training x equals the accumulated fit;
+    # values outside [min, max] take the boundary's basis (reading U2)
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-2, 3, (3, 250))
+    y = np.sin(2 * X[0]) + X[1] + 0.2 * rng.standard_normal(250)
+    p = O.Pool(X, O.Config(n_knots=6), O.MODE_UNBINNED)
+    res = p.train(y, nu=0.2, M=30)
+    pred = p.predict(X, res.offset, res.theta_agg)
+    assert np.abs(pred - res.f).max() <= 1e-12 * np.abs(res.f).max()
+    Xo = X[:, :5].copy()
+    Xo[:, 0] = X.min(1) - 10.0
+    Xo[:, 1] = X.max(1) + 10.0
+    Xc = Xo.copy()
+    Xc[:, 0] = X.min(1)
+    Xc[:, 1] = X.max(1)
+    assert np.abs(p.predict(Xo, res.offset, res.theta_agg) - p.predict(Xc, res.offset, res.theta_agg)).max() == 0.0
