@@ -67,8 +67,9 @@ typedef struct {
                              learners on the raw feature values, the
                              baseline binning is compared against: per row 4 non-zero
                              cubic B-spline values at the knot span of x.  Degree 3 only;
-                             cwb_train (L2) and cwb_find_best on the per-iteration kernels;
-                             the other training calls and cwb_predict return CWB_EUNSUPPORTED. */
+                             cwb_train (L2), cwb_find_best and cwb_predict (basis at x clamped
+                             to the training range); the other training calls return
+                             CWB_EUNSUPPORTED. */
 } cwb_config;
 
 /* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5, no batch hint,

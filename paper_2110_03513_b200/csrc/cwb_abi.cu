@@ -479,8 +479,8 @@ int cwb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offset,
     if (!c || !Xnew || !offset || !theta_agg || !out || m < 1 || B < 1)
         return cwb_set_error(c, CWB_EINVAL, "cwb_predict: invalid argument");
     if (c->status) return c->status;
-    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_predict: unbinned pool");
     c->stream = s;
+    if (c->nb) return cwb_nb_predict(c, Xnew, m, offset, theta_agg, B, out, s);
     return cwb_predict_impl(c, Xnew, m, offset, theta_agg, B, out, s);
 }
 

@@ -210,6 +210,8 @@ int cwb_nb_h12(cwb_ctx* c, const double* Rt, int Bp, double* Sg, cudaStream_t s)
 void cwb_nb_h6(cwb_ctx* c, double* Rt, int Bp, const int32_t* kstar, const double* theta, double nu,
                int rows_per_blk, int nblk, double* part, cudaStream_t s);
 void cwb_nb_release(cwb_ctx* c, cudaStream_t s);
+int cwb_nb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offset, const double* theta_agg,
+                   int32_t B, double* out, cudaStream_t s);
 int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
                      const double* theta_agg, int32_t B, double* out, cudaStream_t s);
 

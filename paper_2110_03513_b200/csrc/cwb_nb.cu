@@ -212,7 +212,42 @@ __global__ void k_h6_nb(double* __restrict__ Rt, int64_t n, int Bp, int d, const
     }
 }
 
+// prediction with unbinned learners: out[b][i] = offset[b] + sum_k sum_t B_{s+t}(x) theta_agg[b][k][s+t],
+// x = Xnew[k][i] clamped to [lo_k, hi_k] (reading U2)
+__global__ void k_pred_nb(const double* __restrict__ Xnew, int64_t m, int K, int d, int S,
+                          const double* __restrict__ lo, const double* __restrict__ hi,
+                          const double* __restrict__ offset, const double* __restrict__ agg, double* __restrict__ out,
+                          int* status) {
+    const int b = blockIdx.y;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = offset[b];
+        for (int k = 0; k < K; k++) {
+            double x = Xnew[(size_t)k * m + i];
+            if (!isfinite(x)) cwb_dev_fail(status, CWB_ENONFINITE);
+            const double l = lo[k], h = (hi[k] - l) / (double)S;
+            x = fmin(fmax(x, l), hi[k]);
+            int s = (int)floor((x - l) / h);
+            s = max(0, min(S - 1, s));
+            double bv[4];
+            cubic4((x - (l + (double)s * h)) / h, bv);
+            const double* th = agg + ((size_t)b * K + k) * d + s;
+#pragma unroll
+            for (int t = 0; t < 4; t++) v += bv[t] * th[t];
+        }
+        out[(size_t)b * m + i] = v;
+    }
+}
+
 }  // namespace
+
+int cwb_nb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offset, const double* theta_agg,
+                   int32_t B, double* out, cudaStream_t s) {
+    const unsigned gx = (unsigned)std::min<int64_t>(1184, (m + 255) / 256);
+    k_pred_nb<<<dim3(gx, B), 256, 0, s>>>(Xnew, m, c->K, c->d, c->nb_spans, c->lo, c->hi, offset, theta_agg, out,
+                                          c->d_status);
+    c->launches += 1;
+    return cwb_check_launch(c, "unbinned predict kernel");
+}
 
 // ===================================================================== host
 

@@ -76,11 +76,24 @@ def test_unbinned_unsupported_calls():
         with pytest.raises(cwb.CwbError) as e:
             call()
         assert e.value.name == "CWB_EUNSUPPORTED"
-    out = pg.train(Y, M=3)
-    with pytest.raises(cwb.CwbError) as e:
-        pg.predict(dev(ds.X), out["offset"], out["theta_agg"])
-    assert e.value.name == "CWB_EUNSUPPORTED"
     pg.close()
     with pytest.raises(cwb.CwbError) as e:
         cwb.Pool(dev(ds.X), cwb.Config(n_star_rule=2, n_star_fixed=21, n_knots=4, degree=2, unbinned=1))
     assert e.value.name == "CWB_EUNSUPPORTED"
+
+
+def test_unbinned_predict_matches_oracle():
+    ds = S.make("R1", reps=range(6))
+    c = ds.cfg
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_UNBINNED)
+    pg = cwb.Pool(dev(ds.X), gcfg(c))
+    out = pg.train(dev(ds.Y), nu=c.nu, M=40)
+    pg.status()
+    off, agg = out["offset"], out["theta_agg"]
+    rng = np.random.default_rng(3)
+    Xn = ds.X[:, rng.choice(c.n, 300)] + rng.normal(0, 0.5, (c.K, 300))  # includes values outside the range
+    g = pg.predict(dev(Xn), off, agg).cpu().numpy()
+    o = po.predict(Xn, off.cpu().numpy(), agg.cpu().numpy())
+    ok, e = close(g, o, 1e-12, scale=np.abs(o).max())
+    assert ok, e
+    pg.close()
