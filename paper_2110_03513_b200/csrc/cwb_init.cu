@@ -430,7 +430,8 @@ __global__ void k_lambda(const double* __restrict__ Gall, int d, double target, 
     __syncwarp();
     const double trG = warp_sum(i < d ? Gs[i][i] : 0.0);
     const double trD = warp_sum(i < d ? Dm[i][i] : 0.0);
-    double t = log(fmax(trG, 1e-300) / fmax(trD, 1e-300));
+    const double t0 = log(fmax(trG, 1e-300) / fmax(trD, 1e-300));
+    double t = t0;
     double tlo = -INFINITY, thi = INFINITY;  // f(tlo) > 0 > f(thi)
     bool done = false, fail = false;
     int it = 0;
@@ -439,16 +440,20 @@ __global__ void k_lambda(const double* __restrict__ Gall, int d, double target, 
 #ifdef CWB_DEBUG_LAMBDA
         if (i == 0) printf("k=%d it=%d t=%.17g f=%.3e fp=%.3e ok=%d\n", k, it, t, e.f, e.fp, (int)e.ok);
 #endif
-        if (!e.ok || !isfinite(e.f)) {  // A not numerically SPD at this lambda: move up
-            tlo = t;
-            t = isfinite(thi) ? 0.5 * (t + thi) : t + 4.0;
-            if (t > 120.0) { fail = true; break; }
+        if (!e.ok || !isfinite(e.f)) {
+            // A not numerically SPD: above the start the penalty dominates (lambda too high, its
+            // null space meets G's small directions), below it G's rank deficiency does (too low)
+            if (t > t0) { thi = t; t = isfinite(tlo) ? 0.5 * (t + tlo) : t - 4.0; }
+            else { tlo = t; t = isfinite(thi) ? 0.5 * (t + thi) : t + 4.0; }
+            if (t > 120.0 || t < -120.0) { fail = true; break; }
             continue;
         }
         if (fabs(e.f) <= 1e-13 * target) { done = true; break; }
         if (e.f > 0.0) tlo = t; else thi = t;
         double tn = t - e.f / e.fp;
-        const bool inside = isfinite(tn) && tn > tlo && tn < thi;
+        if (!isfinite(tn)) tn = e.f > 0.0 ? t + 4.0 : t - 4.0;
+        tn = fmin(fmax(tn, t - 6.0), t + 6.0);  // at most a factor e^6 in lambda per step (flat df when G is rank-deficient)
+        const bool inside = tn > tlo && tn < thi;
         if (!inside) {
             if (isfinite(tlo) && isfinite(thi)) tn = 0.5 * (tlo + thi);
             else tn = (e.f > 0.0) ? t + 4.0 : t - 4.0;

@@ -417,3 +417,25 @@ np.savez(sys.argv[1], **{k: v.cpu().numpy() for k, v in out.items()})
     assert (a["k_trace"] == b["k_trace"]).mean() >= 0.99
     same = (a["k_trace"] == b["k_trace"]).all(0)
     assert np.abs(a["theta_agg"][same] - b["theta_agg"][same]).max() <= 1e-11 * np.abs(a["theta_agg"]).max()
+
+
+@pytest.mark.parametrize("name,reps", [("R1", range(64)), ("R2", range(0, 1024, 128))])
+def test_train_parity_fourth_root_bins(name, reps):
+    # n* = ceil(n^(1/4)) (the paper's second bin rule; n* < d leaves Z^T Z rank-deficient)
+    from parity_util import TIE_RTOL
+    import dataclasses
+    ds = S.make(name, reps=reps)
+    c = dataclasses.replace(ds.cfg, n_star_rule=1)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    assert pg.n_star == O.n_star(c.n, 1)
+    out = pg.train(dev(ds.Y), nu=c.nu, M=c.M)
+    pg.status()
+    g = {k: host(v) for k, v in out.items()}
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    o, followed = po.train_follow(ds.Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=c.nu, M=c.M, threads=8)
+    assert (o.k_trace == g["k_trace"]).all()
+    ok, e = close(g["theta_agg"], o.theta_agg, RTOL, scale=np.abs(o.theta_agg).max())
+    assert ok, e
+    ok, e = close(g["risk_trace"], o.risk_trace, RTOL, scale=np.abs(o.risk_trace).max())
+    assert ok, e
+    pg.close()
