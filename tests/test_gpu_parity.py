@@ -439,3 +439,20 @@ def test_train_parity_fourth_root_bins(name, reps):
     ok, e = close(g["risk_trace"], o.risk_trace, RTOL, scale=np.abs(o.risk_trace).max())
     assert ok, e
     pg.close()
+
+
+@pytest.mark.parametrize("ns", [5, 6, 7, 9, 12, 16, 23, 24, 30, 64, 300])
+@pytest.mark.parametrize("df", [2.5, 4.0, 5.0])
+def test_lambda_calibration_sweep(ns, df):
+    # df -> lambda on the definition from rank-deficient (n* < d) to well-determined G
+    if df >= ns:
+        pytest.skip("df target above the rank")
+    rng = np.random.default_rng(ns)
+    n = 2000
+    X = np.stack([rng.uniform(-1, 2, n), rng.standard_normal(n), rng.exponential(1.0, n)])
+    ocfg = O.Config(n_star_rule=2, n_star_fixed=ns, n_knots=20, df=df)
+    po = O.Pool(X, ocfg, O.MODE_BINNED)
+    pg = cwb.Pool(dev(X), cwb.Config(n_star_rule=2, n_star_fixed=ns, n_knots=20, df=df))
+    lam = pg.lam()
+    assert np.abs(lam - po.lam).max() <= 1e-9 * np.abs(po.lam).max(), (lam, po.lam)
+    pg.close()
