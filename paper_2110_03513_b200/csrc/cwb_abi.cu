@@ -434,25 +434,11 @@ int cwb_fit_host(const double* X, int64_t n, int32_t K, const cwb_config* cfg, c
     if (risk_trace) ok &= cwb_alloc((void**)&dR, 8 * mb, s) == cudaSuccess;
     int rc = ok ? CWB_OK : cwb_set_error(nullptr, CWB_ENOMEM, "cwb_fit_host: allocation failed");
     cwb_ctx* c = nullptr;
-    // the targets are copied on a second stream while the pool is built from X (cwb_init needs only X)
-    cudaStream_t sy = nullptr;
-    cudaEvent_t ev_alloc = nullptr, ev_y = nullptr;
-    const bool split = rc == CWB_OK && cudaStreamCreateWithFlags(&sy, cudaStreamNonBlocking) == cudaSuccess &&
-                       cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming) == cudaSuccess &&
-                       cudaEventCreateWithFlags(&ev_y, cudaEventDisableTiming) == cudaSuccess;
     if (rc == CWB_OK) {
         cudaMemcpyAsync(dX, X, 8 * (size_t)K * n, cudaMemcpyHostToDevice, s);
-        if (split) {
-            cudaEventRecord(ev_alloc, s);  // dY is allocated stream-ordered on s
-            cudaStreamWaitEvent(sy, ev_alloc, 0);
-            cudaMemcpyAsync(dY, Y, 8 * (size_t)B * n, cudaMemcpyHostToDevice, sy);
-            cudaEventRecord(ev_y, sy);
-        } else {
-            cudaMemcpyAsync(dY, Y, 8 * (size_t)B * n, cudaMemcpyHostToDevice, s);
-        }
+        cudaMemcpyAsync(dY, Y, 8 * (size_t)B * n, cudaMemcpyHostToDevice, s);
         rc = cwb_init(&c, dX, n, K, cfg, s);
     }
-    if (split) cudaStreamWaitEvent(s, ev_y, 0);
     if (rc == CWB_OK) rc = cwb_train(c, dY, B, nu, M, dOff, dAgg, dK, dS, dR, s);
     if (rc == CWB_OK) {
         if (offset_out) cudaMemcpyAsync(offset_out, dOff, 8 * (size_t)B, cudaMemcpyDeviceToHost, s);
@@ -468,9 +454,6 @@ int cwb_fit_host(const double* X, int64_t n, int32_t K, const cwb_config* cfg, c
     cwb_release(dK, s); cwb_release(dS, s); cwb_release(dR, s);
     if (rc == CWB_OK && cudaStreamSynchronize(s) != cudaSuccess)
         rc = cwb_set_error(nullptr, CWB_ECUDA, "cwb_fit_host: synchronisation failed");
-    if (ev_alloc) cudaEventDestroy(ev_alloc);
-    if (ev_y) cudaEventDestroy(ev_y);
-    if (sy) cudaStreamDestroy(sy);
     return rc;
 }
 
