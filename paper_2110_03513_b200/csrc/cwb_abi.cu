@@ -25,6 +25,17 @@ int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32
                         double* lo, double* hi, double* z, double* bnd, void* idx, int32_t idx_bytes,
                         cudaStream_t s);
 
+int cwb_num_sms() {
+    static int sms = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1)
+            v = 148;
+        return std::min(v, CWB_MAX_SMS);
+    }();
+    return sms;
+}
+
 int cwb_set_error(cwb_ctx* ctx, int code, const std::string& msg) {
     if (ctx) {
         // argument / unsupported-configuration rejections leave the context usable (include/cwb.h)

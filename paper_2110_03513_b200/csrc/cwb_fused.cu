@@ -1235,7 +1235,7 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out, bool bern = fa
     struct Cand { int RB, T; size_t lim; };
     Cand cands[4];
     int nc = 0;
-    const int nsm = 148;
+    const int nsm = cwb_num_sms();
     if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};  // ~2 replications per SM: one CTA (512 best of 256..768)
     if (B > nsm && !bern) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
     cands[nc++] = {1, c->n >= 8192 ? 768 : 512, kMaxSmem};

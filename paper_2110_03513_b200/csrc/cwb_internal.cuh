@@ -215,6 +215,10 @@ int cwb_nb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offs
 int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offset,
                      const double* theta_agg, int32_t B, double* out, cudaStream_t s);
 
+// Streaming multiprocessors of the current device (B200: 148), queried once; grids are sized by it.
+int cwb_num_sms();
+constexpr int CWB_MAX_SMS = 256;  // bound for per-SM tables in shared memory
+
 // Warp reductions with a fixed butterfly order (deterministic).
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -203,7 +203,7 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
                        const double* __restrict__ G, double* __restrict__ theta,
                        double* __restrict__ delta, const double* __restrict__ Ainv2 = nullptr,
                        const double* __restrict__ G2 = nullptr, const int32_t* __restrict__ phase = nullptr,
-                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0, int Bu = 0,
+                       int Bph = 0, double* __restrict__ Sg = nullptr, int smode = 0,
                        const double* __restrict__ Aset = nullptr, const double* __restrict__ Gset = nullptr,
                        const int32_t* __restrict__ colset = nullptr) {
     __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
@@ -212,10 +212,7 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
     const int b = blockIdx.y * 32 + lane;
     const int32_t* j0 = zj0 + (size_t)k * ns;
     const double* zs = Zs + (size_t)k * ns * CWB_SPW;
-    // U columns: stride Bu (narrow findBest: only the B real columns are stored), else Bp
-    const int bu = Bu ? Bu : Bp;
-    const bool uval = b < bu;
-    const double* u = U + (size_t)k * ns * bu + (uval ? b : 0);
+    const double* u = U + (size_t)k * ns * Bp + b;
     for (int j = w; j < d; j += nw) {
         double s;
         if (smode == 2) {
@@ -223,8 +220,7 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
         } else {
             const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
             s = 0.0;
-            if (uval)
-                for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * bu];
+            for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * Bp];
             if (smode == 1) Sg[((size_t)k * d + j) * Bp + b] = s;
         }
         S[j][lane] = s;
@@ -1220,7 +1216,7 @@ static int find_best_narrow(cwb_ctx* c, const double* R, int32_t B, int32_t* k_o
     int nc = 16384;  // rows staged per chunk, within ~110 KB (two CTAs per SM) if possible
     while (nc > 512 && hist + nbuf * per_row * nc > 110 * 1024) nc >>= 1;
     while (nc > 512 && hist + nbuf * per_row * nc > 200 * 1024) nc >>= 1;
-    int nranges = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + groups - 1) / groups, (c->n + nc - 1) / nc));
+    int nranges = (int)std::max<int64_t>(1, std::min<int64_t>((2 * cwb_num_sms() + groups - 1) / groups, (c->n + nc - 1) / nc));
     const int64_t rpc = ((c->n + nranges - 1) / nranges + 15) / 16 * 16;  // 16-row aligned range starts
     nranges = (int)((c->n + rpc - 1) / rpc);
     const size_t need = sizeof(double) * (size_t)nranges * K * ns * B;
@@ -1428,7 +1424,7 @@ int cwb_train_folds_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_
             k_h1<uint32_t><<<grid, wpb * 32, 0, s>>>(w.Rt, c->n, Bp, K, ns, c->off, (const uint32_t*)c->perm, w.U,
                                                     fold_of_row, colfold);
         k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
-                                                w.delta, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, As, Gs, colfold);
+                                                w.delta, nullptr, nullptr, nullptr, 0, nullptr, 0, As, Gs, colfold);
         k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, K, d, B, Bp, nu, m, w.kstar, theta_agg_out,
                                               k_trace, sse_trace, nullptr, nullptr, nullptr);
         k_zhat<<<dim3((ns + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, ns, d, B, Bp, nu, B, nu,

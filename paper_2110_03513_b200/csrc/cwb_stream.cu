@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     double* __restrict__ sse_out) {
     extern __shared__ double u[];  // [ns][B], then this learner's ZT [W][d], A^-1 [d][d], G [d][d]
     __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4], V[CWB_MAX_D][4];
-    __shared__ int s_j[148 + 1], s_slot[148 + 1], s_nj, s_lw[2 * CWB_MAX_D];
+    __shared__ int s_j[CWB_MAX_SMS + 1], s_slot[CWB_MAX_SMS + 1], s_nj, s_lw[2 * CWB_MAX_D];
     __shared__ bool last;
     const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
     const int lg = k / Ks, NU = Ks * ns, a0 = (k - lg * Ks) * ns;
@@ -520,12 +520,12 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
             const bool ov = jj < N && b0 < it1 && b1 > it0 && b0 != b1;
             const bool stop = jj >= N || b0 >= it1;
             const unsigned bal = __ballot_sync(0xffffffffu, ov);
-            if (ov && m + __popc(bal & ((1u << lane) - 1u)) < 148 + 1) {
+            if (ov && m + __popc(bal & ((1u << lane) - 1u)) < CWB_MAX_SMS + 1) {
                 const int pos = m + __popc(bal & ((1u << lane) - 1u));
                 s_j[pos] = jj;
                 s_slot[pos] = lg - (int)(b0 / nch);
             }
-            m = min(148 + 1, m + __popc(bal));
+            m = min(CWB_MAX_SMS + 1, m + __popc(bal));
             if (__any_sync(0xffffffffu, stop)) break;
         }
         if (lane == 0) s_nj = m;
@@ -637,9 +637,9 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
     const int K = c->K, ns = c->n_star;
     const int64_t n = c->n;
     if (ns > kUBudget) return CWB_EUNSUPPORTED;  // <= kMaxG groups of 32 tasks per item
-    // learner group size: bin sums within the shared-memory budget, and at least 2 x 148 items
+    // learner group size: bin sums within the shared-memory budget, and at least one item per SM
     const int nch0 = (int)((n + kC - 1) / kC);
-    const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / 148)));
+    const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / cwb_num_sms())));
     if ((int64_t)Ks * ns > 0xfffe) return CWB_EUNSUPPORTED;
     const int nch = (int)((n + kC - 1) / kC), nlg = (K + Ks - 1) / Ks, nitems = nlg * nch;
     int NTP = 32;
@@ -733,7 +733,7 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
     if (rc) return rc;
     cwb_stream_plan& p = c->sp;
     const int K = c->K, ns = c->n_star, d = c->d;
-    const int N = std::max(1, std::min(p.nitems, 148));
+    const int N = std::max(1, std::min(p.nitems, cwb_num_sms()));
     // learner groups met by one CTA's item range
     const int per = (p.nitems + N - 1) / N;
     const int nslot = std::min(p.nlg, (per + p.nch - 1) / p.nch + 1);
