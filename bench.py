@@ -221,8 +221,9 @@ def main():
     ap.add_argument("--algo", default="cwb", choices=["cwb", "acwb", "hcwb", "bernoulli"],
                     help="cwb: Alg. 1 supp. (default, the headline); acwb: Alg. 2; hcwb: Alg. 3; "
                          "bernoulli: Alg. 1 with the Bernoulli loss on seeded 0/1 targets")
-    ap.add_argument("--shard", default="replications", choices=["replications", "rows"],
-                    help="multi-GPU sharding: replications (weak, default) or rows (strong, NCCL per iteration)")
+    ap.add_argument("--shard", default="replications", choices=["replications", "rows", "learners"],
+                    help="multi-GPU sharding: replications (weak, default), rows or learners (strong, one "
+                         "collective per iteration)")
     ap.add_argument("--unbinned", action="store_true",
                     help="unbinned learners on the raw x (SURVEY NEXT-3): the baseline binning is compared to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,11 +247,13 @@ def main():
     from paper_2110_03513_b200 import cwb
 
     rows = args.shard == "rows"
-    if rows and args.algo != "cwb":
-        raise SystemExit("--shard rows supports --algo cwb only")
+    strong = args.shard in ("rows", "learners")
+    if strong and args.algo != "cwb":
+        raise SystemExit("--shard rows / learners support --algo cwb only")
     # replications: this rank's block (weak scaling), rank r owns [r*B, (r+1)*B);
-    # rows: the workload's B replications on every rank, this rank's row block of them
-    reps = range(cfg.B) if rows else D.replication_block(cfg.B, rank)
+    # rows: the workload's B replications on every rank, this rank's row block of them;
+    # learners: the workload's B replications and rows on every rank, this rank's block of learners
+    reps = range(cfg.B) if strong else D.replication_block(cfg.B, rank)
     ds = S.make(cfg, reps=reps)
     blk = D.row_block(cfg.n, rank, ws) if rows else range(cfg.n)
     X = torch.as_tensor(ds.X, device=devname)
@@ -258,17 +261,20 @@ def main():
     Y_host = np.ascontiguousarray(Ysrc[:, blk.start:blk.stop])
     Y = torch.as_tensor(Y_host, device=devname)
     gcfg = cwb.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots,
-                      degree=cfg.degree, df=cfg.df, batch_hint=0 if rows or args.unbinned else cfg.B,
+                      degree=cfg.degree, df=cfg.df, batch_hint=0 if strong or args.unbinned else cfg.B,
                       unbinned=int(args.unbinned))
     comm = None
-    if rows:  # libcwb's own NCCL communicator, id from rank 0 over the torch process group
+    if strong:  # libcwb's own NCCL communicator, id from rank 0 over the torch process group
         uid = D.nccl_unique_id(w, torch.device(devname)) if ws > 1 else cwb.cwb_comm_unique_id()
         comm = cwb.Comm(rank, ws, unique_id=uid)
 
     def new_pool(Xsrc):
         p_ = cwb.Pool(Xsrc, gcfg)
         if comm is not None:
-            p_.attach(comm)
+            if rows:
+                p_.attach(comm)
+            else:
+                p_.attach_learners(comm)
         return p_
     B, K, n, M = cfg.B, cfg.K, cfg.n, cfg.M
     stream = torch.cuda.current_stream()
@@ -336,7 +342,7 @@ def main():
         evals_rank = int(K * n * (2 * sw + (M - sw)).sum())
     else:
         evals_rank = K * n * B * M
-    evals = evals_rank if rows else evals_rank * ws
+    evals = evals_rank if strong else evals_rank * ws
     value = evals / (ms_per_step * 1e-3)
 
     # ---- end-to-end through the host-pointer C-ABI call (pinned host buffers)
@@ -359,7 +365,7 @@ def main():
         if rc:
             raise cwb.CwbError(rc, lib.cwb_last_error(None).decode())
 
-    if args.algo != "cwb" or rows:
+    if args.algo != "cwb" or strong:
         Xd = torch.empty_like(X)
         Yd = torch.empty_like(Y)
         host_out = {}
@@ -395,7 +401,7 @@ def main():
         e_ms.append(e0.elapsed_time(e1))
     e2e_ms = D.max_over_ranks(float(np.mean(e_ms)), w, devname)
     h2d = ds.X.nbytes + Y_host.nbytes
-    d2h = sum(v.numel() * v.element_size() for v in (outh if args.algo == "cwb" and not rows else host_out).values())
+    d2h = sum(v.numel() * v.element_size() for v in (outh if args.algo == "cwb" and not strong else host_out).values())
 
     # ---- kernel-only time of one k_train_fused launch (plan cached: one launch per call),
     #      CUDA events on the launching stream, for the roofline
@@ -438,16 +444,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if rows else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper Sec. 4.1.1 generator, seeded; OpenML sets not available)",
             "config": dict(workload_config(cfg, n_star, d), algo=args.algo, shard=args.shard,
                            learners="unbinned" if args.unbinned else "binned",
-                           parallelism=(f"rows{ws}" if rows else f"replications{ws}")),
+                           parallelism=(f"{args.shard}{ws}")),
             "iters_per_s": M / (ms_per_step * 1e-3),
             "phase_ms": {"init": float(np.mean(init_ms)), "train": float(np.mean(train_ms))},
             "roofline": {"bound": "alu",
                          "kernel": ("general path, unbinned learners" if args.unbinned else
                                     "general path, row-sharded" if rows else
+                                    "general path, learner-sharded" if strong else
                                     "k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
                          else f"{args.algo} per-iteration kernels (general path)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
@@ -464,7 +471,7 @@ def main():
             "e2e": {"value": evals / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                     "api": ("cwb_fit_host (pinned host buffers, copies + init + train + sync)"
-                            if args.algo == "cwb" and not rows
+                            if args.algo == "cwb" and not strong
                             else f"pinned H2D of X, Y + cwb_init + cwb_train_{args.algo} + D2H of all outputs")},
             "clocks": clk.summary(),
             "gpu_launches": int(sum(launches)),

@@ -320,6 +320,16 @@ void cwb_comm_free(cwb_comm* comm);
  * above.  Once per context, before its first cwb_train / cwb_find_best. */
 int cwb_attach_comm(cwb_ctx* ctx, cwb_comm* comm);
 
+/* Learner sharding (the alternative to row sharding): ctx keeps every row and
+ * learner (a context built from all of X on every rank), and this rank fits the learners
+ * [K rank / world, K (rank+1) / world) in each findBestBaselearner; per iteration one
+ * all-reduce (sum) of world x B x (d + 2) doubles gathers every rank's best (delta, k, theta),
+ * every rank takes the best over ranks in rank order (the lowest k on ties, as unsharded) and
+ * applies the update to its full residuals (replicated, O(n B)).  Results are bitwise those of
+ * the unsharded per-iteration kernels.  cwb_train and cwb_find_best only (the other training
+ * calls return CWB_EUNSUPPORTED).  Errors: CWB_EINVAL (world > K, already attached). */
+int cwb_attach_comm_learners(cwb_ctx* ctx, cwb_comm* comm);
+
 /* Host outputs: first row of this context's block and its row count
  * (0 and n when not sharded), rank and world (0 and 1 when not sharded). */
 int cwb_get_rows(const cwb_ctx* ctx, int64_t* row_begin, int64_t* n_rows, int32_t* rank, int32_t* world);

@@ -174,7 +174,7 @@ void cwb_free(cwb_ctx* c) {
     if (c->ev_plan) cudaStreamWaitEvent(s, c->ev_plan, 0);  // a plan still building on the side stream
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
-                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->ws.bern, c->ws.fold, c->plan, c->permt,
+                    c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->ws.bern, c->ws.fold, c->ws.lbuf, c->plan, c->permt,
                     c->Cb, c->ZT};
     for (void* p : bufs) cwb_release(p, s);
     cwb_stream_release(c, s);
@@ -364,6 +364,7 @@ int cwb_train_bernoulli(cwb_ctx* c, const double* Y, int32_t B, double nu, int32
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: row-sharded context");
+    if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: learner-sharded context");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: unbinned pool (cwb_train only)");
     if (c->path != 2) {
         bool launched = false;
@@ -385,6 +386,7 @@ int cwb_train_folds(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* fold_
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: row-sharded context");
+    if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: learner-sharded context");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: unbinned pool (cwb_train only)");
     return cwb_train_folds_general(c, Y, B, fold_of_row, F, fold_of_rep, nu, M, offset_out, theta_agg_out, k_trace,
                                    sse_trace, risk_trace, val_risk_trace, s);
@@ -399,6 +401,7 @@ int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gam
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: row-sharded context");
+    if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: learner-sharded context");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: unbinned pool (cwb_train only)");
     if (c->path != 2) {
         bool launched = false;
@@ -422,6 +425,7 @@ int cwb_train_hcwb(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_ma
     if (c->status) return c->status;
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: row-sharded context");
+    if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: learner-sharded context");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: unbinned pool (cwb_train only)");
     return cwb_train_hcwb_general(c, Y, B, val_mask, nu, gamma, pat0, M, offset_out, theta_f_out, k_trace, kcor_trace,
                                   sse_trace, risk_trace, val_risk_trace, switch_iter, s);

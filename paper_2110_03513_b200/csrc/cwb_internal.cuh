@@ -43,6 +43,8 @@ struct cwb_train_ws {  // workspace of the general (per-iteration kernels) path
     size_t bern_bytes = 0;
     double* fold = nullptr;    // CV folds: per-fold tables, column statistics, partials, masks
     size_t fold_bytes = 0;
+    double* lbuf = nullptr;    // learner sharding: [world][Bp][d + 2] candidates
+    size_t lbuf_bytes = 0;
 };
 
 struct cwb_stream_plan {  // streaming binMatVec gather plan (cwb_stream.cu), built on first use
@@ -117,6 +119,9 @@ struct cwb_ctx {
     int32_t plan_T = 0, plan_rb = 0, plan_permt_bytes = 2;
     size_t plan_cap = 0;
 
+    // learner sharding (cwb_attach_comm_learners): this rank fits the learners [lk0, lk1)
+    bool lshard = false;
+    int32_t lk0 = 0, lk1 = 0;
     // row sharding (cwb_attach_comm): n is then the local row count
     bool rows = false;
     int32_t rank = 0, world = 1;

@@ -890,6 +890,55 @@ __global__ void k_rr_fold(const double* __restrict__ part, int nblk, int B, int 
     if (val_risk_trace) val_risk_trace[(size_t)m * B + b] = nho[b] > 0.0 ? sh / (2.0 * nho[b]) : 0.0;
 }
 
+// ---------------------------------------------------------------- learner sharding
+// (include/cwb.h cwb_attach_comm_learners, SURVEY 8(e) alternative): rank r fits the learners
+// [k0, k1); per replication its best (delta, k, theta) goes to slot r of buf[world][Bp][d + 2]
+// (zeros elsewhere), a sum all-reduce gathers the slots, and every rank takes the best over the
+// slots in rank order (= k order: strict > keeps the lowest k on ties), then the H5 bookkeeping.
+__global__ void k_lshard_pack(const double* __restrict__ delta, const double* __restrict__ theta, int k0, int k1,
+                              int d, int B, int Bp, int rank, double* __restrict__ buf) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    int ks = k0;
+    double best = delta[(size_t)k0 * Bp + b];
+    for (int k = k0 + 1; k < k1; k++) {
+        const double v = delta[(size_t)k * Bp + b];
+        if (v > best) { best = v; ks = k; }
+    }
+    double* o = buf + ((size_t)rank * Bp + b) * (d + 2);
+    o[0] = best;
+    o[1] = (double)ks;
+    for (int j = 0; j < d; j++) o[2 + j] = theta[((size_t)ks * d + j) * Bp + b];
+}
+
+__global__ void k_lshard_pick(const double* __restrict__ buf, int world, const double* __restrict__ rr, int K, int d,
+                              int B, int Bp, double nu, int m, int32_t* __restrict__ kstar, double* __restrict__ theta,
+                              double* __restrict__ agg, int32_t* k_trace, double* sse_trace, int32_t* k_out,
+                              double* theta_out, double* sse_out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= Bp) return;
+    if (b >= B) { kstar[b] = 0; return; }
+    int rb = 0;
+    double best = buf[(size_t)b * (d + 2)];
+    for (int r = 1; r < world; r++) {
+        const double v = buf[((size_t)r * Bp + b) * (d + 2)];
+        if (v > best) { best = v; rb = r; }
+    }
+    const double* o = buf + ((size_t)rb * Bp + b) * (d + 2);
+    const int ks = (int)o[1];
+    kstar[b] = ks;
+    for (int j = 0; j < d; j++) theta[((size_t)ks * d + j) * Bp + b] = o[2 + j];
+    const double sse = rr[b] - best;
+    if (agg)
+        for (int j = 0; j < d; j++) agg[((size_t)b * K + ks) * d + j] += nu * o[2 + j];
+    if (k_trace) k_trace[(size_t)m * B + b] = ks;
+    if (sse_trace) sse_trace[(size_t)m * B + b] = sse;
+    if (k_out) k_out[b] = ks;
+    if (sse_out) sse_out[b] = sse;
+    if (theta_out)
+        for (int j = 0; j < d; j++) theta_out[(size_t)b * d + j] = o[2 + j];
+}
+
 // ---------------------------------------------------------------- narrow path
 // binMatVec sums for a few residual vectors (B <= 4), e.g. one
 // findBestBaselearner on a single residual: HBM-bound on the index vector.  A CTA
@@ -1074,6 +1123,7 @@ static int ensure_ws(cwb_ctx* c, int32_t B, cudaStream_t s, bool need_rt = true)
     cwb_release(w.pack, s);
     cwb_release(w.bern, s);
     cwb_release(w.fold, s);
+    cwb_release(w.lbuf, s);
     w = cwb_train_ws();
     const size_t n = (size_t)c->n, K = c->K, ns = c->n_star, d = c->d;
     bool ok = true;
@@ -1172,6 +1222,38 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
                            cudaStream_t s) {
     cwb_train_ws& w = c->ws;
     const int Bp = w.Bp;
+    if (c->lshard) {  // learner sharding: H1-H4 on this rank's learners, one all-reduce of the candidates
+        const int k0 = c->lk0, kl = c->lk1 - c->lk0, ns = c->n_star, d = c->d;
+        const int world = c->world, rank = c->rank;
+        const size_t cnt = (size_t)world * Bp * (d + 2);
+        if (w.lbuf_bytes < cnt * sizeof(double)) {
+            cwb_release(w.lbuf, s);
+            w.lbuf = nullptr;
+            w.lbuf_bytes = 0;
+            if (cwb_alloc((void**)&w.lbuf, cnt * sizeof(double), s) != cudaSuccess) {
+                cwb_set_error(c, CWB_ENOMEM, "learner-sharding buffer");
+                return;
+            }
+            w.lbuf_bytes = cnt * sizeof(double);
+        }
+        const void* pk = (const char*)c->perm + (size_t)c->perm_bytes * k0 * c->n;
+        if (c->perm_bytes == 2)
+            launch_h1<uint16_t>(w.Rt, c->n, Bp, kl, ns, c->off + (size_t)k0 * (ns + 1), pk, w.U + (size_t)k0 * ns * Bp, s);
+        else
+            launch_h1<uint32_t>(w.Rt, c->n, Bp, kl, ns, c->off + (size_t)k0 * (ns + 1), pk, w.U + (size_t)k0 * ns * Bp, s);
+        k_h234<<<dim3(kl, Bp / 32), 256, 0, s>>>(w.U + (size_t)k0 * ns * Bp, Bp, ns, d, c->zj0 + (size_t)k0 * ns,
+                                                 c->Zs + (size_t)k0 * ns * CWB_SPW, c->lwin + (size_t)k0 * d * 2,
+                                                 c->Ainv + (size_t)k0 * d * d, c->G + (size_t)k0 * d * d,
+                                                 w.theta + (size_t)k0 * d * Bp, w.delta + (size_t)k0 * Bp);
+        cudaMemsetAsync(w.lbuf, 0, cnt * sizeof(double), s);
+        k_lshard_pack<<<(B + 127) / 128, 128, 0, s>>>(w.delta, w.theta, k0, k0 + kl, d, B, Bp, rank, w.lbuf);
+        c->launches += 3;
+        if (cwb_rows_allreduce(c, w.lbuf, (int64_t)cnt, s)) return;
+        k_lshard_pick<<<(Bp + 127) / 128, 128, 0, s>>>(w.lbuf, world, w.rr, c->K, d, B, Bp, nu, m, w.kstar, w.theta,
+                                                       agg, k_trace, sse_trace, k_out, theta_out, sse_out);
+        c->launches += 1;
+        return;
+    }
     if (c->nb) {  // unbinned learners: s = Z^T r by the 4-tap scatter (cwb_nb.cu), then H3-H4 from s
         cwb_nb_h12(c, w.Rt, Bp, w.pack, s);
         k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin, c->Ainv,
@@ -1274,6 +1356,7 @@ int cwb_find_best_general(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out
     k_tr_in<<<gt, dim3(32, 8), 0, s>>>(R, c->n, B, w.Bp, nullptr, nullptr, w.Rt);
     c->launches += 1;
     find_best_iter(c, B, 0.0, 0, nullptr, nullptr, nullptr, k_out, theta_out, sse_out, s);
+    if (c->status) return c->status;
     return cwb_check_launch(c, "find_best kernels");
 }
 
@@ -1310,6 +1393,7 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
             k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
         k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
         c->launches += 3;
+        if (c->status) return c->status;  // e.g. a failed collective of learner sharding
     }
     return cwb_check_launch(c, "general train kernels");
 }

@@ -180,11 +180,28 @@ void cwb_comm_free(cwb_comm* m) {
     delete m;
 }
 
+int cwb_attach_comm_learners(cwb_ctx* c, cwb_comm* m) {
+    if (!c) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_attach_comm_learners: NULL context");
+    if (c->status) return c->status;
+    if (!m) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm_learners: NULL communicator");
+    if (c->rows || c->lshard) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm_learners: context already attached");
+    if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_attach_comm_learners: unbinned pool");
+    if (m->world > c->K) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm_learners: world > K");
+    c->lk0 = (int32_t)((int64_t)c->K * m->rank / m->world);
+    c->lk1 = (int32_t)((int64_t)c->K * (m->rank + 1) / m->world);
+    c->lshard = true;
+    c->rank = m->rank;
+    c->world = m->world;
+    c->comm = m;
+    c->path = 2;  // per-iteration kernels
+    return CWB_OK;
+}
+
 int cwb_attach_comm(cwb_ctx* c, cwb_comm* m) {
     if (!c) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_attach_comm: NULL context");
     if (c->status) return c->status;
     if (!m) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: NULL communicator");
-    if (c->rows) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: context already attached");
+    if (c->rows || c->lshard) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: context already attached");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_attach_comm: unbinned pool");
     if (m->world > c->n) return cwb_set_error(c, CWB_EINVAL, "cwb_attach_comm: world > n");
     const int rc = restrict_rows(c, m->rank, m->world);

@@ -23,7 +23,7 @@ SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "c
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
            "cwb_set_path", "cwb_set_narrow", "cwb_find_best", "cwb_train", "cwb_train_bernoulli", "cwb_train_folds", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
            "cwb_launch_count", "cwb_set_phase_timing", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
-           "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_get_rows"]
+           "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_attach_comm_learners", "cwb_get_rows"]
 
 
 class CwbError(RuntimeError):
@@ -106,6 +106,7 @@ def load() -> C.CDLL:
     L.cwb_comm_free.argtypes = [_vp]
     L.cwb_comm_free.restype = None
     L.cwb_attach_comm.argtypes = [_vp, _vp]
+    L.cwb_attach_comm_learners.argtypes = [_vp, _vp]
     L.cwb_get_rows.argtypes = [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)]
     _lib = L
     return L
@@ -501,6 +502,10 @@ class Pool:
 
     def launches(self):
         return cwb_launch_count(self.ctx)
+
+    def attach_learners(self, comm: Comm):
+        _chk(load().cwb_attach_comm_learners(self.ctx, comm.h), self.ctx)
+        self._comm = comm  # the communicator must outlive the context
 
     def attach(self, comm: Comm):
         cwb_attach_comm(self.ctx, comm)
