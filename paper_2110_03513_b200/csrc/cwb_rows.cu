@@ -107,9 +107,14 @@ int restrict_rows(cwb_ctx* c, int32_t rank, int32_t world) {
     c->perm_bytes = pb;
     // the general-path workspace is sized by n: drop it
     cwb_train_ws& w = c->ws;
-    void* bufs[] = {w.Rt, w.U, w.theta, w.delta, w.rr, w.zhat, w.kstar, w.part, w.narrow, w.colpart, w.acwb, w.pack};
+    void* bufs[] = {w.Rt, w.U, w.theta, w.delta, w.rr, w.zhat, w.kstar, w.part, w.narrow, w.colpart, w.acwb, w.pack,
+                    w.bern, w.fold, w.lbuf};
     for (void* p : bufs) cwb_release(p, s);
     w = cwb_train_ws();
+    cwb_stream_release(c, s);  // the streaming findBest plan and the chunked-H1 tables index the full rows
+    cwb_release(c->h1c, s);
+    c->h1c = nullptr;
+    c->h1c_nch = 0;
     c->n_glob = n;
     c->row0 = r0;
     c->n = nl;
