@@ -72,6 +72,11 @@ void cwb_release(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+void cwb_pool_release(cwb_ctx* c, void* p, cudaStream_t s) {
+    const char* a = (const char*)c->arena;
+    if (p && !(a && (const char*)p >= a && (const char*)p < a + c->arena_bytes)) cudaFreeAsync(p, s);
+}
+
 static const char* status_name(int c) {
     switch (c) {
         case CWB_OK: return "ok";
@@ -176,13 +181,14 @@ void cwb_free(cwb_ctx* c) {
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
                     c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->ws.bern, c->ws.fold, c->ws.lbuf, c->plan, c->permt,
                     c->Cb, c->ZT};
-    for (void* p : bufs) cwb_release(p, s);
+    for (void* p : bufs) cwb_pool_release(c, p, s);
+    cwb_release(c->arena, s);
     cwb_stream_release(c, s);
     cwb_nb_release(c, s);
     cwb_release(c->h1c, s);
     if (c->ev_plan) cudaEventDestroy(c->ev_plan);
     if (c->ev_csr) cudaEventDestroy(c->ev_csr);
-    if (c->s2) cudaStreamDestroy(c->s2);
+    // c->s2 is the device's shared side stream: not destroyed
     delete c;
 }
 
@@ -216,28 +222,31 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     c->perm_bytes = n <= 65536 ? 2 : 4;
     c->stream = s;
     const size_t Ks = K, nn = n, nss = ns, dd = d;
-    bool ok = true;
-    ok &= cwb_alloc((void**)&c->d_status, sizeof(int), s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->lo, 8 * Ks, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->hi, 8 * Ks, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->z, 8 * Ks * nss, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->bnd, 8 * Ks * (nss - 1), s) == cudaSuccess;
-    ok &= cwb_alloc(&c->idx, (size_t)c->idx_bytes * Ks * nn + 16, s) == cudaSuccess;  // +16: bulk-copy slack
-    ok &= cwb_alloc((void**)&c->cnt, 4 * Ks * nss, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->off, 4 * Ks * (nss + 1), s) == cudaSuccess;
-    ok &= cwb_alloc(&c->perm, (size_t)c->perm_bytes * (Ks * nn + 8), s) == cudaSuccess;  // +8: vector-load padding
-    ok &= cwb_alloc((void**)&c->Zb, 8 * Ks * nss * dd, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->zj0, 4 * Ks * nss, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->Zs, 8 * Ks * nss * CWB_SPW, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->lwin, 4 * Ks * dd * 2, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->G, 8 * Ks * dd * dd, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->Ainv, 8 * Ks * dd * dd, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->lambda, 8 * Ks, s) == cudaSuccess;
     c->nsp = (int32_t)((ns + 1) / 2 * 2);
     // design points in the support of one B-spline ((degree+1) knot intervals), +2 for rounding
     c->W = (int32_t)std::min<int64_t>(ns, ((int64_t)(cfg.degree + 1) * (ns - 1)) / (cfg.n_knots + 1) + 2);
-    ok &= cwb_alloc((void**)&c->Cb, 8 * Ks * dd * 4, s) == cudaSuccess;
-    ok &= cwb_alloc((void**)&c->ZT, 8 * Ks * (size_t)c->W * dd, s) == cudaSuccess;
+    // the pool's buffers are carved from one allocation (one host call instead of 18)
+    struct Part { void** p; size_t bytes; };
+    const Part parts[] = {
+        {(void**)&c->d_status, sizeof(int)}, {(void**)&c->lo, 8 * Ks}, {(void**)&c->hi, 8 * Ks},
+        {(void**)&c->z, 8 * Ks * nss}, {(void**)&c->bnd, 8 * Ks * (nss - 1)},
+        {&c->idx, (size_t)c->idx_bytes * Ks * nn + 16},  // +16: bulk-copy slack
+        {(void**)&c->cnt, 4 * Ks * nss}, {(void**)&c->off, 4 * Ks * (nss + 1)},
+        {&c->perm, (size_t)c->perm_bytes * (Ks * nn + 8)},  // +8: vector-load padding
+        {(void**)&c->Zb, 8 * Ks * nss * dd}, {(void**)&c->zj0, 4 * Ks * nss}, {(void**)&c->Zs, 8 * Ks * nss * CWB_SPW},
+        {(void**)&c->lwin, 4 * Ks * dd * 2}, {(void**)&c->G, 8 * Ks * dd * dd}, {(void**)&c->Ainv, 8 * Ks * dd * dd},
+        {(void**)&c->lambda, 8 * Ks}, {(void**)&c->Cb, 8 * Ks * dd * 4}, {(void**)&c->ZT, 8 * Ks * (size_t)c->W * dd}};
+    size_t total = 0;
+    for (const Part& q : parts) total += (q.bytes + 255) & ~(size_t)255;
+    bool ok = cwb_alloc(&c->arena, total, s) == cudaSuccess;
+    if (ok) {
+        c->arena_bytes = total;
+        char* base = (char*)c->arena;
+        for (const Part& q : parts) {
+            *q.p = base;
+            base += (q.bytes + 255) & ~(size_t)255;
+        }
+    }
     if (!ok) {
         cwb_free(c);
         return cwb_set_error(nullptr, CWB_ENOMEM, "cwb_init: device allocation failed");

@@ -1376,7 +1376,15 @@ int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
     if (c->batch_hint <= 0) return CWB_OK;
     FusedShape f;
     if (!fused_shape(c, c->batch_hint, &f)) return CWB_OK;
-    if (!c->s2 && cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess) return CWB_OK;
+    if (!c->s2) {  // one side stream per device, shared by the contexts (created once, never destroyed)
+        static cudaStream_t side[16] = {};
+        static std::mutex mu;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return CWB_OK;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!side[dev] && cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking) != cudaSuccess) return CWB_OK;
+        c->s2 = side[dev];
+    }
     if (!c->ev_csr && cudaEventCreateWithFlags(&c->ev_csr, cudaEventDisableTiming) != cudaSuccess) return CWB_OK;
     CWB_CUDA_TRY(c, cudaEventRecord(c->ev_csr, s));
     CWB_CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_csr, 0));

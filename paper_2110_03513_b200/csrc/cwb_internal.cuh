@@ -78,7 +78,9 @@ struct cwb_ctx {
     std::string err;
     int64_t launches = 0;
 
-    // device buffers (pool, built once by cwb_init)
+    // device buffers (pool, built once by cwb_init; carved from one arena allocation)
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
     int* d_status = nullptr;
     double* lo = nullptr;     // K
     double* hi = nullptr;     // K
@@ -158,6 +160,7 @@ int cwb_set_error(cwb_ctx* ctx, int code, const std::string& msg);
 int cwb_check_launch(cwb_ctx* ctx, const char* what);
 cudaError_t cwb_alloc(void** p, size_t bytes, cudaStream_t s);
 void cwb_release(void* p, cudaStream_t s);
+void cwb_pool_release(cwb_ctx* c, void* p, cudaStream_t s);  // no-op for buffers carved from c->arena
 
 // Kernel entry points used across translation units (host launchers).
 int cwb_launch_init(cwb_ctx* ctx, const double* X, cudaStream_t s);

@@ -98,9 +98,9 @@ int restrict_rows(cwb_ctx* c, int32_t rank, int32_t world) {
         cwb_release(idx, s); cwb_release(perm, s); cwb_release(off, s);
         return rc;
     }
-    cwb_release(c->idx, s);
-    cwb_release(c->perm, s);
-    cwb_release(c->off, s);
+    cwb_pool_release(c, c->idx, s);
+    cwb_pool_release(c, c->perm, s);
+    cwb_pool_release(c, c->off, s);
     c->idx = idx;
     c->perm = perm;
     c->off = off;
