@@ -431,14 +431,19 @@ def main():
         achieved = ops / (kernel_ms * 1e-3)
         peak = fp64_peak_ops(peaks)
         traffic = None
+        smem_wf = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(cfg.name)
+                tj = json.load(open(tp))
+                if args.algo == "cwb" and not strong and not args.unbinned and args.path != 2:
+                    traffic = tj.get(cfg.name)
+                    smem_wf = tj.get("smem_wavefronts", {}).get(cfg.name)
             except Exception:
                 traffic = None
         rb = 2 if B > 148 else 1  # replications per CTA
         sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        n_sms = torch.cuda.get_device_properties(devname).multi_processor_count
         ctas_per_sm = -(-(-(-B // rb)) // 148)
         h1_floor_ms = K * n * ctas_per_sm * M / (GATHER_LANE_LOADS_PER_CLK[rb] * sm_hz) * 1e3
         line = {
@@ -459,6 +464,9 @@ def main():
                          else f"{args.algo} per-iteration kernels (general path)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         # the binding on-chip unit: shared-memory load wavefronts of one launch (ncu) over
+                         # the pipe's 1 wavefront / clock / SM during the measured launch time
+                         "smem_pipe_frac": (smem_wf / (kernel_ms * 1e-3 * sm_hz * n_sms) if smem_wf else None),
                          "kernel_ms": kernel_ms, "launches_per_call": int(k_launches),
                          "note": ("achieved = algorithmic fp64 add/FMA operations of one launch (FMA counted "
                                   "once; DESIGN.md Sec. 7) / its CUDA-event duration; peak = 148 SM x 64 fp64 "
