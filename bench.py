@@ -461,7 +461,8 @@ def main():
                                     "general path, row-sharded" if rows else
                                     "general path, learner-sharded" if strong else
                                     "k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
-                         else f"{args.algo} per-iteration kernels (general path)",
+                         else (f"k_train_fused ({args.algo} mode)" if k_launches == 1
+                               else f"{args.algo} per-iteration kernels (general path)"),
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          # the binding on-chip unit: shared-memory load wavefronts of one launch (ncu) over

@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
 #pragma unroll
             for (int q = 0; q < RB; q++) {
                 const double f = f0[q];
-                const double v = Yb[i * RB + q] - 1.0 / (1.0 + exp(-f));
+                double lo;
+                const double v = bern_resid(Yb[i * RB + q], f, &lo);
                 Fb[i * RB + q] = f;
                 r[i * RB + q] = v;
                 part[q] += v * v;
@@ -771,10 +772,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                             const double f = Fb[i * RB + q] + zhat[q * nsp + (q ? j1[e] : j0[e])];
                             Fb[i * RB + q] = f;
                             const double y = Yb[i * RB + q];
-                            const double v = y - 1.0 / (1.0 + exp(-f));
+                            double lo;
+                            const double v = bern_resid(y, f, &lo);
                             r[i * RB + q] = v;
                             acc[q] = fma(v, v, acc[q]);
-                            accL[q] += (f > 0.0 ? f + log1p(exp(-f)) : log1p(exp(f))) - y * f;
+                            accL[q] += lo;
                         }
                     } else if (i < n) {
                         if (RB == 1) {

@@ -234,6 +234,66 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// 1 / t for t in [1, 3): fp32 reciprocal estimate and two Newton steps (branch-free, ~1 ulp).
+__device__ __forceinline__ double cwb_rcp_1_3(double t) {
+    double y = (double)__frcp_rn((float)t);
+    y = fma(y, fma(-t, y, 1.0), y);
+    return fma(y, fma(-t, y, 1.0), y);
+}
+
+// Bernoulli loss L(y, f) = log(1 + exp(f)) - y f and pseudo residual r = y - sigma(f) (P:L833,
+// S:L311) from ONE exponential e = exp(-|f|) in [0, 1]:
+//   sigma(f) = (f >= 0 ? 1 : e) / (1 + e),   L = max(f, 0) + log1p(e) - y f.
+// Branch-free fp64 so that the rows of a thread overlap (the library exp / log1p / division have
+// special-case branches): e^-a by Cody-Waite reduction a = k ln2 - r, |r| <= ln2/2, and the
+// degree-13 Taylor polynomial of e^r (truncation < 1e-17); log1p(e) = k2 ln2 + 2 atanh(s) +
+// (e - (t - 1)) / t with t = 1 + e = 2^k2 m, s = (m - 1) / (m + 1), |s| <= 0.172, atanh by its
+// series to s^23.  Agrees with the library functions to a few ulp (reading B1).
+__device__ __forceinline__ double bern_resid(double y, double f, double* loss) {
+    const double a = fmin(fabs(f), 708.0);  // e^-708 ~ 3e-308: below 1 ulp of 1 + e
+    const double k = rint(a * 1.4426950408889634);
+    double r = fma(k, 6.93147180369123816490e-01, -a);  // ln2 hi (21 trailing zero bits: k ln2hi exact)
+    r = fma(k, 1.90821492927058770002e-10, r);          // ln2 lo
+    double p = 1.0 / 6227020800.0;                      // 1/13!
+    p = fma(p, r, 1.0 / 479001600.0);
+    p = fma(p, r, 1.0 / 39916800.0);
+    p = fma(p, r, 1.0 / 3628800.0);
+    p = fma(p, r, 1.0 / 362880.0);
+    p = fma(p, r, 1.0 / 40320.0);
+    p = fma(p, r, 1.0 / 5040.0);
+    p = fma(p, r, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const double e = p * __hiloint2double((1023 - (int)k) << 20, 0);  // e^r 2^-k
+    const double t = 1.0 + e, inv = cwb_rcp_1_3(t);
+    const double corr = e - (t - 1.0);  // exact rounding error of t
+    const bool hi = t > 1.4142135623730951;
+    const double m = hi ? 0.5 * t : t, fm = m - 1.0;  // exact
+    const double s = fm * cwb_rcp_1_3(m + 1.0), s2 = s * s;
+    double q = 1.0 / 23.0;
+    q = fma(q, s2, 1.0 / 21.0);
+    q = fma(q, s2, 1.0 / 19.0);
+    q = fma(q, s2, 1.0 / 17.0);
+    q = fma(q, s2, 1.0 / 15.0);
+    q = fma(q, s2, 1.0 / 13.0);
+    q = fma(q, s2, 1.0 / 11.0);
+    q = fma(q, s2, 1.0 / 9.0);
+    q = fma(q, s2, 1.0 / 7.0);
+    q = fma(q, s2, 1.0 / 5.0);
+    q = fma(q, s2, 1.0 / 3.0);
+    const double s3q = s * s2 * q;
+    const double kl = hi ? 1.0 : 0.0;
+    // log1p(e): (k2 ln2hi + 2s) + (2 s^3 q + k2 ln2lo + corr / t)
+    const double l = fma(kl, 6.93147180369123816490e-01, 2.0 * s) +
+                     fma(kl, 1.90821492927058770002e-10, fma(corr, inv, 2.0 * s3q));
+    *loss = (f > 0.0 ? f + l : l) - y * f;
+    return y - (f >= 0.0 ? inv : e * inv);
+}
+
 template <typename T>
 __device__ __forceinline__ uint32_t ld_u(const T* p, int64_t i) {
     return (uint32_t)p[i];

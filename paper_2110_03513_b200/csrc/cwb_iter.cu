@@ -759,10 +759,11 @@ __global__ void k_bern_update(double* __restrict__ Rt, double* __restrict__ F, c
             F[e] = f;
         }
         const double y = Yt[e];
-        const double r = y - 1.0 / (1.0 + exp(-f));
+        double lo;
+        const double r = bern_resid(y, f, &lo);
         Rt[e] = r;
         a2 += r * r;
-        al += (f > 0.0 ? f + log1p(exp(-f)) : log1p(exp(f))) - y * f;
+        al += lo;
     }
     red[0][w][lane] = a2;
     red[1][w][lane] = al;

@@ -82,3 +82,25 @@ def test_bernoulli_errors_and_determinism():
             pg.status()
         assert e.value.name == err
         pg.close()
+
+
+@pytest.mark.parametrize("path", [1, 2])
+def test_bernoulli_skewed_classes(path):
+    # class shares 0.3 % .. 99.7 %: |f| up to ~6 at the offset and beyond it as the fit sharpens,
+    # so exp(-|f|) spans many binades and sigma saturates (csrc bern_resid, reading B1)
+    ds = S.make("R1", reps=range(8))
+    c = ds.cfg
+    Y = S.binary_targets(ds)
+    rng = np.random.default_rng(20211007)
+    for b, share in enumerate((0.003, 0.01, 0.05, 0.2, 0.8, 0.95, 0.99, 0.997)):
+        y = np.zeros(c.n)
+        y[rng.choice(c.n, max(1, int(round(share * c.n))), replace=False)] = 1.0
+        Y[b] = y
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    pg = cwb.Pool(dev(ds.X), gpu_cfg_of(c))
+    pg.set_path(path)
+    g = host(pg.train_bernoulli(dev(Y), nu=0.3, M=60))
+    pg.status()
+    o = po.train_bernoulli(Y, nu=0.3, M=60, threads=8)
+    assert_train_parity(g, o, c.n, tag=f"skewed bernoulli path {path}")
+    pg.close()

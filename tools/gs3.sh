@@ -1,10 +1,8 @@
-TAG=r1f
+TAG=r1g
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 python __graft_entry__.py build > gpurun_out/${TAG}_build.log 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.log
-timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_R1.json 2> gpurun_out/${TAG}_bench_R1.err; echo "bench rc=$?" >> gpurun_out/${TAG}_bench_R1.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_ref_R1.json 2>&1
-BENCH_ALLOW_SHORT=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_R1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1
-BENCH_ALLOW_SHORT=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_train_fused -s 2 -c 1 -o gpurun_out/${TAG}_fused_R1 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full.log 2>&1
+for a in acwb hcwb bernoulli; do
+  timeout 300 python bench.py --algo $a --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_$a.json 2>&1
+  BENCH_ALLOW_SHORT=1 timeout 600 ncu --set full --clock-control none -k regex:k_train_fused -s 1 -c 1 -o /tmp/${TAG}_fused_$a python bench.py --algo $a --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_$a.log 2>&1
+  python tools/ncu_brief.py /tmp/${TAG}_fused_$a.ncu-rep > gpurun_out/${TAG}_ncu_$a.txt 2>&1
+done
