@@ -1194,10 +1194,18 @@ int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cud
         return launch_t<IdxT, PermT, 1, false, 768, 1, false, false, true>(fp, T, smem, s);
     }
     if (hc) {  // HCWB: the ACWB layout plus F, the validation mask and the phase state
+        if (T <= 256) {
+            if (pool) return launch_t<IdxT, PermT, 2, true, 256, 2, true, true>(fp, T, smem, s);
+            return launch_t<IdxT, PermT, 2, false, 256, 2, true, true>(fp, T, smem, s);
+        }
         if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, true, true>(fp, T, smem, s);
         return launch_t<IdxT, PermT, 2, false, 512, 1, true, true>(fp, T, smem, s);
     }
-    if (acc) {  // ACWB: two columns of one replication, 512 threads
+    if (acc) {  // ACWB: two columns of one replication; 512 threads, or 256 with two CTAs per SM
+        if (T <= 256) {
+            if (pool) return launch_t<IdxT, PermT, 2, true, 256, 2, true>(fp, T, smem, s);
+            return launch_t<IdxT, PermT, 2, false, 256, 2, true>(fp, T, smem, s);
+        }
         if (pool) return launch_t<IdxT, PermT, 2, true, 512, 1, true>(fp, T, smem, s);
         return launch_t<IdxT, PermT, 2, false, 512, 1, true>(fp, T, smem, s);
     }
@@ -1409,16 +1417,28 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
                               bool* launched, const HcArgs* hc = nullptr, bool bern = false) {
     *launched = false;
     FusedShape f;
-    if (acc) {  // the two columns (r, c) of a replication run as RB = 2 in a 512-thread CTA
+    if (acc) {  // the two columns (r, c) of a replication run as RB = 2
         if ((int64_t)c->K * c->n + 8 > INT32_MAX || (int64_t)c->K * c->n_star * 16 > 200 * 1024) return CWB_OK;
         f.RB = 2;
-        f.T = 512;
         f.permt_bytes = 16 * (c->n + kPadRows) <= 65535 ? 2 : 4;
+        // HCWB with more replications than SMs: 256-thread CTAs, two per SM, when both fit in shared
+        // memory (R1: 3.24 -> 2.98 ms; ACWB measured slower that way, 2.33 -> 2.48 ms, and keeps
+        // 512).  CWB_ACC_T=256|512 overrides.
+        const char* ev = getenv("CWB_ACC_T");
+        const int want = ev ? atoi(ev) : (hc != nullptr && B > cwb_num_sms() ? 256 : 512);
+        f.T = 0;
+        for (int T : {256, 512}) {
+            if (T < want) continue;
+            const size_t lim = T == 256 ? kTwoCtaSmem : kMaxSmem;
+            if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * T, 2, T / 32, false, 0, 0, c->idx_bytes, true,
+                           hc != nullptr)
+                    .total <= lim) {
+                f.T = T;
+                break;
+            }
+        }
+        if (!f.T) return CWB_OK;
         f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
-        if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, 2, f.T / 32, false, 0, 0, c->idx_bytes, true,
-                       hc != nullptr)
-                .total > kMaxSmem)
-            return CWB_OK;
     } else if (!fused_shape(c, B, &f, bern)) {
         return CWB_OK;  // does not fit: caller uses the general path
     }
@@ -1431,7 +1451,7 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
     if (rc) return rc;
     if (c->fused_T != f.T) return CWB_OK;  // plan failed on the device: cwb_status reports it
     CWB_CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_plan, 0));  // the plan may come from the side stream
-    const size_t lim = (f.RB == 1 && f.T <= 384) ? kTwoCtaSmem : kMaxSmem;
+    const size_t lim = ((f.RB == 1 || acc) && f.T <= 384) ? kTwoCtaSmem : kMaxSmem;
     const size_t pbytes = ((size_t)(c->permt_entries + kSlackEntries) * f.permt_bytes + 15) / 16 * 16;  // < plan_cap
     f.pool = false;
     const int nm = c->plan_multi;
