@@ -281,6 +281,14 @@ int orc_df_to_lambda(const double* G, const double* D, int d, double target, int
                      double* lambda_out) {
     if (!(target > 0.0) || target > (double)d) return ORC_ECALIB;
     double v;
+    if (d <= 2) {
+        /* no second differences (Delta has d - 2 = 0 rows): D = 0 and df(lambda) =
+         * rank(Z^T Z) for every lambda -- the target is met by any lambda or by none (the
+         * degree-1, no-knot learner of S:L383 with df = 2) */
+        if (orc_df(G, D, d, 1.0, kind, &v) != ORC_OK || fabs(v - target) > 1e-9) return ORC_ECALIB;
+        *lambda_out = 1.0;
+        return ORC_OK;
+    }
     double hi = 1.0;
     for (;;) {
         if (orc_df(G, D, d, hi, kind, &v) != ORC_OK) return ORC_ECALIB;

@@ -258,15 +258,16 @@ __global__ void k_basis(const double* __restrict__ z, const double* lo_, const d
             if (q < W4) zrow[j] = v;
         }
         zj0[(size_t)k * ns + l] = w0;
-        sj0[l] = w0;
+        sj0[l] = j0 < 0 ? 0 : j0;  // first non-zero basis (w0 is clamped to d - 4 for degree < 3)
     }
     __syncthreads();
-    // design-point window of basis j: l with j - 3 <= zj0[l] <= j (zj0 non-decreasing)
+    // design-point window of basis j: l with j - deg <= j0(l) <= j (j0 non-decreasing), i.e. the
+    // deg + 1 knot intervals of its support
     for (int j = threadIdx.x; j < d; j += blockDim.x) {
-        int a = 0, b = ns;  // first l with zj0[l] >= j - (W4-1)
-        while (a < b) { int m = (a + b) >> 1; if (sj0[m] >= j - (W4 - 1)) b = m; else a = m + 1; }
+        int a = 0, b = ns;  // first l with j0[l] >= j - deg
+        while (a < b) { int m = (a + b) >> 1; if (sj0[m] >= j - deg) b = m; else a = m + 1; }
         int lb = a;
-        a = lb; b = ns;     // first l with zj0[l] > j
+        a = lb; b = ns;     // first l with j0[l] > j
         while (a < b) { int m = (a + b) >> 1; if (sj0[m] > j) b = m; else a = m + 1; }
         lwin[((size_t)k * d + j) * 2 + 0] = lb;
         lwin[((size_t)k * d + j) * 2 + 1] = a;

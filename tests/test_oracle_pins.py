@@ -867,3 +867,15 @@ def test_unbinned_predict_reproduces_the_fit_and_clamps():
     Xc[:, 0] = X.min(1)
     Xc[:, 1] = X.max(1)
     assert np.abs(p.predict(Xo, res.offset, res.theta_agg) - p.predict(Xc, res.offset, res.theta_agg)).max() == 0.0
+
+
+def test_no_penalty_learner_calibration():
+    # d = 2 (degree 1, no inner knots): Delta has no rows, D = 0, df(lambda) = rank(Z^T Z)
+    # = 2 for every lambda: df = 2 is met (any lambda; the oracle reports 1), df = 1.5 is not
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-1, 4, (3, 500))
+    p = O.Pool(X, O.Config(n_star_rule=2, n_star_fixed=3, degree=1, n_knots=0, df=2.0), O.MODE_BINNED)
+    assert (p.lam == 1.0).all()
+    with pytest.raises(O.OracleError) as e:
+        O.Pool(X, O.Config(n_star_rule=2, n_star_fixed=3, degree=1, n_knots=0, df=1.5), O.MODE_BINNED)
+    assert e.value.name == "ECALIB"
