@@ -140,6 +140,14 @@ int cwb_get_dims(const cwb_ctx* ctx, int32_t* n_star, int32_t* d, int32_t* K, in
 /* Host output lambda[K] (synchronises). */
 int cwb_get_lambda(cwb_ctx* ctx, double* lambda_out);
 
+/* Host output n_star_k[K] (synchronises): the bins of every learner, min(n*, number of
+ * distinct values of its feature; -0.0 and +0.0 are one value).  S:L143 / SURVEY 8(c)
+ * step 1 clamp n* to the distinct values; learner k's design points are those of
+ * n*_k bins over [min, max], stored in the first n*_k slots of its z[n*] row
+ * (the slots after are padding: z = max, no row binned there).  CWB_EINVAL: NULL
+ * output. */
+int cwb_get_n_star_k(cwb_ctx* ctx, int32_t* n_star_k_out);
+
 /* Device copies of the pool for inspection (each pointer may be NULL):
  * z[K][n*], idx[K][n] (uint16 regardless of the internal width),
  * Zb[K][n*][d], G[K][d][d], Ainv[K][d][d].  Synchronises. */

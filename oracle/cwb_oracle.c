@@ -71,6 +71,22 @@ int orc_build_bins(const double* x, int64_t n, int n_star, double* z, double* bn
     return ORC_OK;
 }
 
+static int cmp_double(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+int64_t orc_count_distinct(const double* x, int64_t n) {
+    double* t = (double*)malloc(sizeof(double) * (size_t)n);
+    if (!t) return -1;
+    memcpy(t, x, sizeof(double) * (size_t)n);
+    qsort(t, (size_t)n, sizeof(double), cmp_double);
+    int64_t c = n > 0 ? 1 : 0;
+    for (int64_t i = 1; i < n; i++) c += t[i] != t[i - 1];  /* -0.0 == +0.0 */
+    free(t);
+    return c;
+}
+
 /* ----------------------------------------------------------------- basis */
 
 /* "20 knots and degree 3" -> 20 inner knots, d = n_knots + degree + 1
@@ -323,7 +339,7 @@ int orc_df_to_lambda(const double* G, const double* D, int d, double target, int
 void orc_pool_free(orc_pool* p) {
     if (!p) return;
     free(p->lo); free(p->hi); free(p->z); free(p->bnd); free(p->idx); free(p->Zb);
-    free(p->Zx); free(p->G); free(p->D); free(p->lambda); free(p->L);
+    free(p->Zx); free(p->G); free(p->D); free(p->lambda); free(p->L); free(p->nsk);
     free(p);
 }
 
@@ -349,9 +365,10 @@ int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int m
     p->D = (double*)malloc(sizeof(double) * d * d);
     p->lambda = (double*)malloc(sizeof(double) * K);
     p->L = (double*)malloc(sizeof(double) * K * d * d);
+    p->nsk = (int32_t*)malloc(sizeof(int32_t) * K);
     if (mode == ORC_MODE_UNBINNED) p->Zx = (double*)malloc(sizeof(double) * (size_t)K * n * d);
     if (!p->lo || !p->hi || !p->z || !p->bnd || !p->idx || !p->Zb || !p->G || !p->D || !p->lambda ||
-        !p->L || (mode == ORC_MODE_UNBINNED && !p->Zx)) {
+        !p->L || !p->nsk || (mode == ORC_MODE_UNBINNED && !p->Zx)) {
         orc_pool_free(p);
         return ORC_ENOMEM;
     }
@@ -360,10 +377,25 @@ int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int m
     for (int k = 0; k < K && st == ORC_OK; k++) {
         const double* x = X + (size_t)k * n;
         double* z = p->z + (size_t)k * n_star;
-        st = orc_build_bins(x, n, n_star, z, p->bnd + (size_t)k * (n_star - 1), p->idx + (size_t)k * n);
+        /* n* clamped to the count of distinct values, per learner;
+         * the learner's bins are those of n* = nsk, stored in the first nsk slots */
+        const int64_t nd = orc_count_distinct(x, n);
+        if (nd < 0) { st = ORC_ENOMEM; break; }
+        const int nsk = nd < n_star ? (int)nd : n_star;
+        if (nsk < 2) {  /* a constant feature (1 distinct value) */
+            for (int64_t i = 0; i < n; i++)
+                if (!isfinite(x[i])) { st = ORC_ENONFINITE; break; }
+            if (st == ORC_OK) st = ORC_EDEGENERATE;
+            break;
+        }
+        p->nsk[k] = nsk;
+        double* bk = p->bnd + (size_t)k * (n_star - 1);
+        st = orc_build_bins(x, n, nsk, z, bk, p->idx + (size_t)k * n);
         if (st != ORC_OK) break;
         p->lo[k] = z[0];
-        p->hi[k] = z[n_star - 1];
+        p->hi[k] = z[nsk - 1];
+        for (int l = nsk; l < n_star; l++) z[l] = p->hi[k];
+        for (int l = nsk - 1; l < n_star - 1; l++) bk[l] = INFINITY;
         double* Zb = p->Zb + (size_t)k * n_star * d;
         st = orc_bspline_basis(z, n_star, p->lo[k], p->hi[k], cfg->degree, cfg->n_knots, Zb);
         if (st != ORC_OK) break;

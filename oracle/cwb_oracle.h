@@ -109,7 +109,13 @@ typedef struct {
     double* lambda; /* K */
     double* L;      /* K x d x d   Cholesky of G + lambda D (binned mode cache) */
     int degree, n_knots;  /* of the basis (unbinned prediction evaluates it at new x) */
+    int32_t* nsk;   /* K: effective bins of learner k = min(n_star, #distinct x values) (S:L143,
+                     * reading N1); design points l >= nsk[k] are padding (z = hi, bnd = +inf,
+                     * never hit by a row) */
 } orc_pool;
+
+/* Number of distinct values of x (n >= 1), -0.0 and +0.0 counted once: sort a copy, count runs. */
+int64_t orc_count_distinct(const double* x, int64_t n);
 
 int orc_pool_new(const double* X, int64_t n, int K, const orc_config* cfg, int mode, orc_pool** out);
 void orc_pool_free(orc_pool* p);

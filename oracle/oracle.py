@@ -60,7 +60,8 @@ class _Pool(C.Structure):
                 ("idx", C.POINTER(C.c_int32)), ("Zb", C.POINTER(C.c_double)),
                 ("Zx", C.POINTER(C.c_double)), ("G", C.POINTER(C.c_double)),
                 ("D", C.POINTER(C.c_double)), ("lam", C.POINTER(C.c_double)),
-                ("L", C.POINTER(C.c_double)), ("degree", C.c_int), ("n_knots", C.c_int)]
+                ("L", C.POINTER(C.c_double)), ("degree", C.c_int), ("n_knots", C.c_int),
+                ("nsk", C.POINTER(C.c_int32))]
 
 
 def lib():
@@ -317,6 +318,7 @@ class Pool:
         self.G = arr(s.G, (K, d, d))
         self.D = arr(s.D, (d, d))
         self.lam = arr(s.lam, (K,))
+        self.nsk = arr(s.nsk, (K,), np.int32)  # effective bins per learner (S:L143 clamp, reading N1)
 
     def __del__(self):
         p = getattr(self, "_p", None)

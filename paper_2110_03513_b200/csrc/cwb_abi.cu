@@ -23,7 +23,7 @@ int cwb_bin_mat_mat_impl(const double* Zb, int32_t ns, int32_t d, const void* id
                          const double* w, int64_t n, double* out, cudaStream_t s);
 int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32_t K, int32_t ns,
                         double* lo, double* hi, double* z, double* bnd, void* idx, int32_t idx_bytes,
-                        cudaStream_t s);
+                        cudaStream_t s, int32_t* nsk = nullptr);
 
 int cwb_num_sms() {
     static int sms = [] {
@@ -180,7 +180,7 @@ void cwb_free(cwb_ctx* c) {
     void* bufs[] = {c->d_status, c->lo, c->hi, c->z, c->bnd, c->idx, c->cnt, c->off, c->perm, c->Zb,
                     c->zj0, c->Zs, c->lwin, c->G, c->Ainv, c->lambda, c->ws.Rt, c->ws.U,
                     c->ws.theta, c->ws.delta, c->ws.rr, c->ws.zhat, c->ws.kstar, c->ws.part, c->ws.narrow, c->ws.colpart, c->ws.acwb, c->ws.pack, c->ws.bern, c->ws.fold, c->ws.lbuf, c->plan, c->permt,
-                    c->Cb, c->ZT};
+                    c->Cb, c->ZT, c->nsk};
     for (void* p : bufs) cwb_pool_release(c, p, s);
     cwb_release(c->arena, s);
     cwb_stream_release(c, s);
@@ -235,7 +235,8 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
         {&c->perm, (size_t)c->perm_bytes * (Ks * nn + 8)},  // +8: vector-load padding
         {(void**)&c->Zb, 8 * Ks * nss * dd}, {(void**)&c->zj0, 4 * Ks * nss}, {(void**)&c->Zs, 8 * Ks * nss * CWB_SPW},
         {(void**)&c->lwin, 4 * Ks * dd * 2}, {(void**)&c->G, 8 * Ks * dd * dd}, {(void**)&c->Ainv, 8 * Ks * dd * dd},
-        {(void**)&c->lambda, 8 * Ks}, {(void**)&c->Cb, 8 * Ks * dd * 4}, {(void**)&c->ZT, 8 * Ks * (size_t)c->W * dd}};
+        {(void**)&c->lambda, 8 * Ks}, {(void**)&c->Cb, 8 * Ks * dd * 4}, {(void**)&c->ZT, 8 * Ks * (size_t)c->W * dd},
+        {(void**)&c->nsk, 4 * Ks}};
     size_t total = 0;
     for (const Part& q : parts) total += (q.bytes + 255) & ~(size_t)255;
     bool ok = cwb_alloc(&c->arena, total, s) == cudaSuccess;
@@ -294,6 +295,14 @@ int cwb_get_lambda(cwb_ctx* c, double* lambda_out) {
     if (rc) return rc;
     if (!lambda_out) return cwb_set_error(c, CWB_EINVAL, "cwb_get_lambda: NULL output");
     CWB_CUDA_TRY(c, cudaMemcpy(lambda_out, c->lambda, sizeof(double) * c->K, cudaMemcpyDeviceToHost));
+    return CWB_OK;
+}
+
+int cwb_get_n_star_k(cwb_ctx* c, int32_t* out) {
+    int rc = cwb_status(c);
+    if (rc) return rc;
+    if (!out) return cwb_set_error(c, CWB_EINVAL, "cwb_get_n_star_k: NULL output");
+    CWB_CUDA_TRY(c, cudaMemcpy(out, c->nsk, sizeof(int32_t) * c->K, cudaMemcpyDeviceToHost));
     return CWB_OK;
 }
 

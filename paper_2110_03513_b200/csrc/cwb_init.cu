@@ -64,18 +64,77 @@ __device__ __forceinline__ double design_point(double lo, double hi, int l, int 
     return __dadd_rn(lo, __dmul_rn(t, __dsub_rn(hi, lo)));
 }
 
+// ------------------------------------------- I1b distinct values (n* clamp)
+// S:L143 (reading N1): the bins of learner k are those of
+// n*_k = min(n*, #distinct values of x_k).  One CTA per learner inserts the values
+// into an open-addressing hash set of H = 2^m >= 2 (n* + T) slots (shared memory, or
+// the global scratch `gtab` when it does not fit) and stops as soon as n* distinct
+// values are seen -- a continuous feature exits after its first few thousand rows.
+// The T threads see the stop flag at their next row, so at most n* + T - 1 keys are
+// ever inserted: the load factor stays <= 1/2 and every probe sequence ends.
+// Keys are the value bits with -0.0 folded into +0.0; empty = all ones (a NaN: the
+// values are finite, k_minmax has checked).  The count is exact below n*.
+constexpr unsigned long long kEmptyKey = ~0ull;
+
+__global__ void k_distinct(const double* __restrict__ X, int64_t n, int ns, int hbits,
+                           unsigned long long* __restrict__ gtab, int32_t* __restrict__ nsk, const int* status) {
+    extern __shared__ unsigned long long htab_s[];
+    __shared__ int s_count;
+    __shared__ volatile int s_full;
+    if (status && *status) return;
+    const int k = blockIdx.x;
+    const uint32_t H = 1u << hbits, mask = H - 1u;
+    unsigned long long* tab = gtab ? gtab + (size_t)k * H : htab_s;
+    for (uint32_t e = threadIdx.x; e < H; e += blockDim.x) tab[e] = kEmptyKey;
+    if (threadIdx.x == 0) { s_count = 0; s_full = 0; }
+    __syncthreads();
+    const double* x = X + (size_t)k * n;
+    for (int64_t i = threadIdx.x; i < n && !s_full; i += blockDim.x) {
+        const double v = x[i];
+        const unsigned long long key = (unsigned long long)__double_as_longlong(v == 0.0 ? 0.0 : v);
+        uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - hbits));
+        for (uint32_t probe = 0;; probe++) {
+            if (probe >= H) {  // unreachable at load <= 1/2; never spin
+                cwb_dev_fail(const_cast<int*>(status), CWB_ECUDA);
+                s_full = 1;
+                break;
+            }
+            unsigned long long cur = gtab ? __ldcg(tab + h) : tab[h];
+            if (cur == key) break;
+            if (cur == kEmptyKey) {
+                cur = atomicCAS(tab + h, kEmptyKey, key);
+                if (cur == kEmptyKey) {
+                    if (atomicAdd(&s_count, 1) + 1 >= ns) s_full = 1;
+                    break;
+                }
+                if (cur == key) break;
+            }
+            h = (h + 1u) & mask;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) nsk[k] = s_count < ns ? s_count : ns;
+}
+
 // ---------------------------------------------------------- I2 design points
-__global__ void k_design(const double* lo_, const double* hi_, int ns, double* z, double* bnd,
+// nsk (NULL: n* for every learner): the design points of n*_k = nsk[k]; the slots
+// l >= n*_k are padding, z = hi and bnd = +inf (no row is binned there).
+__global__ void k_design(const double* lo_, const double* hi_, int ns, const int32_t* nsk, double* z, double* bnd,
                          const int* status) {
     if (status && *status) return;
     const int k = blockIdx.x;
     const double lo = lo_[k], hi = hi_[k];
+    const int nk = nsk ? nsk[k] : ns;
     for (int l = threadIdx.x; l < ns; l += blockDim.x) {
-        double zl = design_point(lo, hi, l, ns);
+        double zl = l < nk ? design_point(lo, hi, l, nk) : hi;
         z[(size_t)k * ns + l] = zl;
         if (l < ns - 1) {
-            double zr = design_point(lo, hi, l + 1, ns);
-            bnd[(size_t)k * (ns - 1) + l] = __dadd_rn(zl, __ddiv_rn(__dsub_rn(zr, zl), 2.0));
+            double b = INFINITY;
+            if (l < nk - 1) {
+                double zr = design_point(lo, hi, l + 1, nk);
+                b = __dadd_rn(zl, __ddiv_rn(__dsub_rn(zr, zl), 2.0));
+            }
+            bnd[(size_t)k * (ns - 1) + l] = b;
         }
     }
 }
@@ -213,8 +272,8 @@ __device__ __forceinline__ double knot(double lo, double h, int q, int deg) {
 }
 
 __global__ void k_basis(const double* __restrict__ z, const double* lo_, const double* hi_, int ns,
-                        int deg, int nk, int d, double* Zb, int32_t* zj0, double* Zs,
-                        int32_t* lwin, const int* status) {
+                        const int32_t* __restrict__ nsk, int deg, int nk, int d, double* Zb, int32_t* zj0,
+                        double* Zs, int32_t* lwin, const int* status) {
     extern __shared__ int32_t sj0[];
     if (status && *status) return;
     const int k = blockIdx.x;
@@ -258,7 +317,9 @@ __global__ void k_basis(const double* __restrict__ z, const double* lo_, const d
             if (q < W4) zrow[j] = v;
         }
         zj0[(size_t)k * ns + l] = w0;
-        sj0[l] = j0 < 0 ? 0 : j0;  // first non-zero basis (w0 is clamped to d - 4 for degree < 3)
+        // first non-zero basis (w0 is clamped to d - 4 for degree < 3); padding design points
+        // (l >= n*_k) are in no basis window
+        sj0[l] = (nsk && l >= nsk[k]) ? (1 << 30) : (j0 < 0 ? 0 : j0);
     }
     __syncthreads();
     // design-point window of basis j: l with j - deg <= j0(l) <= j (j0 non-decreasing), i.e. the
@@ -603,9 +664,23 @@ int cwb_launch_csr(cwb_ctx* ctx, const void* idx, int32_t idx_bytes, int64_t n, 
 
 int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32_t K, int32_t ns,
                         double* lo, double* hi, double* z, double* bnd, void* idx, int32_t idx_bytes,
-                        cudaStream_t s) {
+                        cudaStream_t s, int32_t* nsk) {
     k_minmax<<<K, 512, 0, s>>>(x, n, lo, hi, st);
-    k_design<<<K, 256, 0, s>>>(lo, hi, ns, z, bnd, st);
+    unsigned long long* gtab = nullptr;
+    if (nsk) {  // per-learner n* clamp
+        const int T = 1024;
+        int hbits = 1;
+        while ((1ll << hbits) < 2ll * (ns + T)) hbits++;
+        const size_t hbytes = sizeof(unsigned long long) << hbits;
+        const bool in_smem = hbytes <= 128 * 1024;
+        if (!in_smem && cwb_alloc((void**)&gtab, hbytes * (size_t)K, s) != cudaSuccess)
+            return cwb_set_error(ctx, CWB_ENOMEM, "cwb_init: distinct-value table allocation failed");
+        if (in_smem) cudaFuncSetAttribute(k_distinct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hbytes);
+        k_distinct<<<K, T, in_smem ? hbytes : 0, s>>>(x, n, ns, hbits, gtab, nsk, st);
+        if (gtab) cwb_release(gtab, s);
+        if (ctx) ctx->launches++;
+    }
+    k_design<<<K, 256, 0, s>>>(lo, hi, ns, nsk, z, bnd, st);
     int gx = (int)((n + 255) / 256);
     if (gx > 1184) gx = 1184;
     dim3 grid(gx, K);
@@ -626,7 +701,7 @@ int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32
 int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
     const int K = c->K, ns = c->n_star, d = c->d;
     int rc = cwb_launch_bin_only(c, c->d_status, X, c->n, K, ns, c->lo, c->hi, c->z, c->bnd, c->idx,
-                                 c->idx_bytes, s);
+                                 c->idx_bytes, s, c->nsk);
     if (rc) return rc;
     rc = cwb_launch_csr(c, c->idx, c->idx_bytes, c->n, K, ns, c->cnt, c->off, c->perm,
                         c->perm_bytes, s);
@@ -635,7 +710,7 @@ int cwb_launch_init(cwb_ctx* c, const double* X, cudaStream_t s) {
         rc = cwb_fused_plan(c, s);
         if (rc) return rc;
     }
-    k_basis<<<K, 128, sizeof(int32_t) * ns, s>>>(c->z, c->lo, c->hi, ns, c->degree, c->n_knots, d,
+    k_basis<<<K, 128, sizeof(int32_t) * ns, s>>>(c->z, c->lo, c->hi, ns, c->nsk, c->degree, c->n_knots, d,
                                                  c->Zb, c->zj0, c->Zs, c->lwin, c->d_status);
     if (c->nb) {  // unbinned learners: G = Z^T Z on the raw x (cwb_nb.cu)
         rc = cwb_nb_init(c, X, s);

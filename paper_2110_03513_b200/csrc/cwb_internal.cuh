@@ -93,7 +93,9 @@ struct cwb_ctx {
     double* Zb = nullptr;     // K x n* x d  dense basis at the design points
     int32_t* zj0 = nullptr;   // K x n*      first non-zero basis index of design point l
     double* Zs = nullptr;     // K x n* x 4  its non-zero values
-    int32_t* lwin = nullptr;  // K x d x 2   design points l with zj0[l] <= j <= zj0[l]+3
+    int32_t* lwin = nullptr;  // K x d x 2   design points l where basis j can be non-zero
+    int32_t* nsk = nullptr;   // K  effective bins min(n*, #distinct x) (reading N1);
+                              //    design points l >= nsk[k] are padding (z = hi, bnd = +inf)
     double* G = nullptr;      // K x d x d   Zb^T diag(cnt) Zb
     double* Ainv = nullptr;   // K x d x d   (G + lambda D)^-1
     double* lambda = nullptr; // K

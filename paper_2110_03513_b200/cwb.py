@@ -20,7 +20,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 
 # the exported symbols declared in include/cwb.h
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
-           "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_pool",
+           "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_n_star_k", "cwb_get_pool",
            "cwb_set_path", "cwb_set_narrow", "cwb_find_best", "cwb_train", "cwb_train_bernoulli", "cwb_train_folds", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
            "cwb_launch_count", "cwb_set_phase_timing", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
            "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_attach_comm_learners", "cwb_get_rows"]
@@ -82,6 +82,7 @@ def load() -> C.CDLL:
     L.cwb_last_error.restype = C.c_char_p
     L.cwb_get_dims.argtypes = [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i64)]
     L.cwb_get_lambda.argtypes = [_vp, _vp]
+    L.cwb_get_n_star_k.argtypes = [_vp, _vp]
     L.cwb_get_pool.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_set_path.argtypes = [_vp, _i32]
     L.cwb_set_narrow.argtypes = [_vp, _i32]
@@ -214,6 +215,14 @@ def cwb_get_lambda(ctx):
     ns, d, K, n = cwb_get_dims(ctx)
     out = np.empty(K, dtype=np.float64)
     _chk(load().cwb_get_lambda(ctx, out.ctypes.data_as(C.c_void_p)), ctx)
+    return out
+
+
+def cwb_get_n_star_k(ctx):
+    import numpy as np
+    ns, d, K, n = cwb_get_dims(ctx)
+    out = np.empty(K, dtype=np.int32)
+    _chk(load().cwb_get_n_star_k(ctx, out.ctypes.data_as(C.c_void_p)), ctx)
     return out
 
 
@@ -493,6 +502,9 @@ class Pool:
 
     def lam(self):
         return cwb_get_lambda(self.ctx)
+
+    def n_star_k(self):
+        return cwb_get_n_star_k(self.ctx)
 
     def pool(self):
         return cwb_get_pool(self.ctx)

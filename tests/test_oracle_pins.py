@@ -879,3 +879,54 @@ def test_no_penalty_learner_calibration():
     with pytest.raises(O.OracleError) as e:
         O.Pool(X, O.Config(n_star_rule=2, n_star_fixed=3, degree=1, n_knots=0, df=1.5), O.MODE_BINNED)
     assert e.value.name == "ECALIB"
+
+
+# ------------------------------------------------- n* clamp (reading N1)
+
+def test_n_star_clamped_to_distinct_values():
+    # brute force: nsk = min(n*, #distinct), -0.0 and +0.0 one value; rows only in the first nsk bins
+    rng = np.random.default_rng(21)
+    n = 900  # n* = 30
+    X = np.stack([rng.integers(0, 7, n).astype(float),            # 7 distinct
+                  rng.choice([-1.5, -0.0, 0.0, 2.25], n),        # 3 distinct (-0 == +0)
+                  rng.standard_normal(n),                        # n distinct
+                  np.repeat(np.arange(30.0), 30)])               # exactly n* distinct
+    p = O.Pool(X, O.Config(n_knots=6, df=2.5), O.MODE_BINNED)  # 3 bins: rank 3, df in (2, 3]
+    assert p.n_star == 30
+    assert p.nsk.tolist() == [7, 3, 30, 30]
+    for k in range(4):
+        assert p.idx[k].max() < p.nsk[k]
+        # the learner's bins are those of n* = nsk: its design points at the distinct values
+        z, bnd = np.empty(p.nsk[k]), np.empty(p.nsk[k] - 1)
+        idx = np.empty(n, np.int32)
+        O.lib().orc_build_bins(np.ascontiguousarray(X[k]), n, int(p.nsk[k]), z, bnd, idx)
+        assert (p.z[k, :p.nsk[k]] == z).all() and (p.idx[k] == idx).all()
+        assert (p.z[k, p.nsk[k]:] == p.hi[k]).all()
+    # 3 distinct values -> 3 equidistant design points over [-1.5, 2.25]: -1.5, 0.375, 2.25
+    assert np.allclose(p.z[1, :3], [-1.5, 0.375, 2.25], rtol=0, atol=1e-15)
+
+
+def test_clamped_binning_equals_unbinned_on_equidistant_values():
+    # with n* = #distinct values, equally spaced, the binned fit equals the unbinned fit.
+    # The values are the design points themselves (the P:L859 formula, a linspace differs by
+    # 1 ulp); n = 1600 gives n* = 40 > 9 and 13 distinct values, so the clamp decides n*.
+    rng = np.random.default_rng(22)
+    n = 1600
+
+    def grid(lo, hi, m):
+        g = np.array([lo + (l / (m - 1)) * (hi - lo) for l in range(m)])
+        g[-1] = hi
+        return g
+    X = np.stack([rng.choice(grid(-2.0, 3.0, 9), n), rng.choice(grid(0.5, 7.25, 13), n)])
+    X[0, :9], X[1, :13] = grid(-2.0, 3.0, 9), grid(0.5, 7.25, 13)  # every value present
+    Y = np.stack([np.sin(X[0]) + 0.1 * X[1] ** 2 + 0.2 * rng.standard_normal(n) for _ in range(3)])
+    cfg = O.Config(n_knots=4)
+    pb = O.Pool(X, cfg, O.MODE_BINNED)
+    pu = O.Pool(X, cfg, O.MODE_UNBINNED)
+    assert pb.nsk.tolist() == [9, 13]
+    assert np.allclose(pb.lam, pu.lam, rtol=1e-9)
+    rb = pb.train(Y, nu=0.1, M=50)
+    ru = pu.train(Y, nu=0.1, M=50)
+    assert (rb.k_trace == ru.k_trace).all()
+    assert np.allclose(rb.theta_agg, ru.theta_agg, rtol=1e-9, atol=1e-12)
+    assert np.allclose(rb.f, ru.f, rtol=1e-10, atol=1e-12)
