@@ -1,8 +1,9 @@
 // cwb_init.cu -- one-off pool construction on the device (I1-I7).
 //
-//   I1 k_minmax   per-learner min / max of x
+//   I1 k_minmax_part / _fin   per-learner min / max of x (HBM-bound, all SMs)
+//   I1b k_distinct  n*_k = min(n*, #distinct values)                S:L143 (reading N1)
 //   I2 k_design   design points z and bin boundaries
-//   I3 k_bin      index vector (binary search on the boundaries)
+//   I3 k_bin      index vector (nearest design point, then exact boundary comparisons)
 //   I4 k_csr      bin inversion: rows of every bin, ascending      (binning as a hash map)
 //   I5 k_basis    cubic B-spline basis at the design points
 //   I6 k_gram     G = Zb^T diag(cnt) Zb  (binMatMat, w = 1)
@@ -17,42 +18,83 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "cwb_internal.cuh"
 
 namespace {
 
 // ---------------------------------------------------------------- I1 min/max
-__global__ void k_minmax(const double* __restrict__ X, int64_t n, double* lo, double* hi,
-                         int* status) {
-    const int k = blockIdx.x;
+// HBM-bound: blocks of every learner reduce contiguous row ranges (4 loads in flight per
+// thread), k_minmax_fin combines the partials and records ENONFINITE / EDEGENERATE.
+constexpr int kMMT = 256;
+
+__global__ void __launch_bounds__(kMMT) k_minmax_part(const double* __restrict__ X, int64_t n, int nb,
+                                                      double* __restrict__ part) {
+    const int k = blockIdx.y, b = blockIdx.x;
     const double* x = X + (size_t)k * n;
+    const int64_t per = (n + nb - 1) / nb, r0 = min(n, (int64_t)b * per), r1 = min(n, r0 + per);
     double mn = INFINITY, mx = -INFINITY;
     bool bad = false;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        double v = x[i];
+    int64_t i = r0 + threadIdx.x;
+    for (; i + 3 * kMMT < r1; i += 4 * kMMT) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldcs(x + i + u * kMMT);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            bad |= !isfinite(v[u]);
+            mn = fmin(mn, v[u]);
+            mx = fmax(mx, v[u]);
+        }
+    }
+    for (; i < r1; i += kMMT) {
+        const double v = __ldcs(x + i);
         bad |= !isfinite(v);
         mn = fmin(mn, v);
         mx = fmax(mx, v);
     }
-    __shared__ double smn[32], smx[32];
+    __shared__ double smn[kMMT / 32], smx[kMMT / 32];
     __shared__ int sbad;
     if (threadIdx.x == 0) sbad = 0;
     __syncthreads();
-    if (bad) atomicOr(&sbad, 1);
+    if (bad) sbad = 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) { smn[w] = mn; smx[w] = mx; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int i = 1; i < nw; i++) { mn = fmin(mn, smn[i]); mx = fmax(mx, smx[i]); }
+        for (int q = 1; q < kMMT / 32; q++) { mn = fmin(mn, smn[q]); mx = fmax(mx, smx[q]); }
+        double* o = part + ((size_t)k * nb + b) * 3;
+        o[0] = mn;
+        o[1] = mx;
+        o[2] = sbad ? 1.0 : 0.0;
+    }
+}
+
+__global__ void k_minmax_fin(const double* __restrict__ part, int nb, double* lo, double* hi, int* status) {
+    const int k = blockIdx.x, lane = threadIdx.x;
+    double mn = INFINITY, mx = -INFINITY, bad = 0.0;
+    for (int b = lane; b < nb; b += 32) {
+        const double* q = part + ((size_t)k * nb + b) * 3;
+        mn = fmin(mn, q[0]);
+        mx = fmax(mx, q[1]);
+        bad = fmax(bad, q[2]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        bad = fmax(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    }
+    if (lane == 0) {
         lo[k] = mn;
         hi[k] = mx;
-        if (sbad) cwb_dev_fail(status, CWB_ENONFINITE);
+        if (bad != 0.0) cwb_dev_fail(status, CWB_ENONFINITE);
         else if (!(mn < mx)) cwb_dev_fail(status, CWB_EDEGENERATE);
     }
 }
@@ -140,10 +182,15 @@ __global__ void k_design(const double* lo_, const double* hi_, int ns, const int
 }
 
 // ------------------------------------------------------------ I3 index vector
-// idx(x) = smallest l with x <= bnd_l, else n*-1 (P:L861 closed-right bins).
+// idx(x) = smallest l with x <= bnd_l, else n*-1 (P:L861 closed-right bins).  The search
+// starts at the nearest design point by arithmetic, g = round((x - lo) (n*_k - 1) / (hi - lo)),
+// and walks to the exact answer by comparisons with bnd (non-decreasing): down while
+// x <= bnd_{g-1}, up while x > bnd_g -- the same index as a binary search over bnd, in one or
+// two shared-memory loads instead of log2 n*.  Padding boundaries (l >= n*_k - 1) are +inf.
 template <typename IdxT, bool SMEM>
 __global__ void k_bin(const double* __restrict__ X, int64_t n, int ns, const double* __restrict__ bnd,
-                      IdxT* __restrict__ idx, const int* status) {
+                      const double* __restrict__ lo_, const double* __restrict__ hi_,
+                      const int32_t* __restrict__ nsk, IdxT* __restrict__ idx, const int* status) {
     extern __shared__ double sb[];
     if (status && *status) return;
     const int k = blockIdx.y;
@@ -153,19 +200,29 @@ __global__ void k_bin(const double* __restrict__ X, int64_t n, int ns, const dou
         __syncthreads();
     }
     const double* bs = SMEM ? sb : bk;
+    const int nk = nsk ? nsk[k] : ns;
+    const double lo = lo_[k], scale = (double)(nk - 1) / (hi_[k] - lo);
     const double* x = X + (size_t)k * n;
     IdxT* out = idx + (size_t)k * n;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double v = x[i];
-        int a = 0, b = ns - 1;
-        while (a < b) {
-            int mid = a + ((b - a) >> 1);
-            if (v <= bs[mid]) b = mid;
-            else a = mid + 1;
-        }
-        out[i] = (IdxT)a;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x, r0 = min(n, (int64_t)blockIdx.x * per),
+                  r1 = min(n, r0 + per);
+    auto bin = [&](double v) {
+        const double t = (v - lo) * scale + 0.5;
+        int g = t >= 0.0 ? (t < (double)(nk - 1) ? (int)t : nk - 1) : 0;
+        while (g > 0 && v <= bs[g - 1]) g--;
+        while (g < ns - 1 && v > bs[g]) g++;
+        return (IdxT)g;
+    };
+    const int T = blockDim.x;
+    int64_t i = r0 + threadIdx.x;
+    for (; i + 3 * T < r1; i += 4 * T) {  // four loads in flight per thread
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldcs(x + i + u * T);
+#pragma unroll
+        for (int u = 0; u < 4; u++) out[i + u * T] = bin(v[u]);
     }
+    for (; i < r1; i += T) out[i] = bin(__ldcs(x + i));
 }
 
 // --------------------------------------------------------- I4 bin inversion
@@ -638,9 +695,228 @@ static int smem_csr_warps(int ns, int max_warps) {
     return w;
 }
 
+namespace {
+// ------------------------------------------- I4 bin inversion, chunked (large n)
+// The same stable counting sort as k_csr spread over (chunk, learner) CTAs: chunk c of
+// learner k holds rows [c C, (c+1) C).  k_csrc_count: per-chunk bin counts; k_csrc_scan:
+// per learner the bin totals, the offsets off[l] and the first slot of every (chunk, bin),
+// off[l] + rows of bin l in the chunks before; k_csrc_scatter: the chunk's rows sorted by
+// bin in shared memory (per-warp histograms + __match_any_sync ranks: stable), then
+// written out run by run (consecutive threads, consecutive slots).  The output is
+// bit-identical to k_csr's (a stable sort is unique).
+constexpr int kCsrC = 16384;  // rows per chunk
+constexpr int kCsrT = 512;
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kCsrT) k_csrc_count(const IdxT* __restrict__ idx, int64_t n, int ns, int nch,
+                                                      uint32_t* __restrict__ ccnt, const int* status) {
+    extern __shared__ uint32_t hc2[];
+    if (status && *status) return;
+    const int c = blockIdx.x, k = blockIdx.y;
+    for (int l = threadIdx.x; l < ns; l += kCsrT) hc2[l] = 0;
+    __syncthreads();
+    const IdxT* id = idx + (size_t)k * n;
+    const int64_t r0 = (int64_t)c * kCsrC, r1 = min(n, r0 + kCsrC);
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kCsrT) atomicAdd(&hc2[id[i]], 1u);
+    __syncthreads();
+    uint32_t* o = ccnt + ((size_t)k * nch + c) * ns;
+    for (int l = threadIdx.x; l < ns; l += kCsrT) o[l] = hc2[l];
+}
+
+__global__ void __launch_bounds__(1024) k_csrc_scan(uint32_t* __restrict__ ccnt, int64_t n, int ns, int nch,
+                                                    uint32_t* __restrict__ cnt_out, int32_t* __restrict__ off_out,
+                                                    const int* status) {
+    extern __shared__ uint32_t tot2[];
+    __shared__ uint32_t wsum[32];
+    if (status && *status) return;
+    const int k = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nthr = blockDim.x;
+    uint32_t* cc = ccnt + (size_t)k * nch * ns;
+    for (int l = threadIdx.x; l < ns; l += nthr) {  // chunk-exclusive prefix per bin, totals
+        uint32_t run = 0;
+        for (int c = 0; c < nch; c++) {
+            const uint32_t v = cc[(size_t)c * ns + l];
+            cc[(size_t)c * ns + l] = run;
+            run += v;
+        }
+        tot2[l] = run;
+        cnt_out[(size_t)k * ns + l] = run;
+    }
+    __syncthreads();
+    const int per = (ns + nthr - 1) / nthr;  // exclusive scan of the totals: off[l]
+    const int b0 = threadIdx.x * per, b1 = min(ns, b0 + per);
+    uint32_t local = 0;
+    for (int b = b0; b < b1; b++) local += tot2[b];
+    uint32_t inc = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t v = lane < (nthr >> 5) ? wsum[lane] : 0u;
+        uint32_t sc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, sc, o);
+            if (lane >= o) sc += t;
+        }
+        wsum[lane] = sc - v;
+    }
+    __syncthreads();
+    uint32_t base = wsum[w] + inc - local;
+    int32_t* off = off_out + (size_t)k * (ns + 1);
+    for (int b = b0; b < b1; b++) {
+        const uint32_t c = tot2[b];
+        tot2[b] = base;
+        off[b] = (int32_t)base;
+        base += c;
+    }
+    if (threadIdx.x == 0) off[ns] = (int32_t)n;
+    __syncthreads();
+    for (int l = threadIdx.x; l < ns; l += nthr)
+        for (int c = 0; c < nch; c++) cc[(size_t)c * ns + l] += tot2[l];
+}
+
+// shared memory: hist [nw][ns], lofs [ns], gst [ns], srow [C] (PermT), sbin [C] (u16)
+template <typename IdxT, typename PermT>
+__global__ void __launch_bounds__(kCsrT) k_csrc_scatter(const IdxT* __restrict__ idx, int64_t n, int ns, int nch,
+                                                        int nw_use, const uint32_t* __restrict__ cst,
+                                                        PermT* __restrict__ perm_out, const int* status) {
+    extern __shared__ uint32_t sm2[];
+    __shared__ uint32_t wsum[32];
+    if (status && *status) return;
+    const int c = blockIdx.x, k = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* hist = sm2;
+    uint32_t* lofs = hist + (size_t)nw_use * ns;
+    uint32_t* gst = lofs + ns;
+    PermT* srow = reinterpret_cast<PermT*>(gst + ns);
+    uint16_t* sbin = reinterpret_cast<uint16_t*>(srow + kCsrC);
+    const IdxT* id = idx + (size_t)k * n;
+    const int64_t r0 = (int64_t)c * kCsrC, r1 = min(n, r0 + kCsrC);
+    const int rows = (int)(r1 - r0);
+    for (int a = threadIdx.x; a < nw_use * ns; a += kCsrT) hist[a] = 0;
+    const uint32_t* cs = cst + ((size_t)k * nch + c) * ns;
+    for (int l = threadIdx.x; l < ns; l += kCsrT) gst[l] = cs[l];
+    __syncthreads();
+    const int L = (rows + nw_use - 1) / nw_use;
+    const int q0 = w * L, q1 = min(rows, q0 + L);
+    if (w < nw_use)
+        for (int q = q0 + lane; q < q1; q += 32) atomicAdd(&hist[(size_t)w * ns + id[r0 + q]], 1u);
+    __syncthreads();
+    // per bin: exclusive prefix over warps (hist -> warp base within the bin), bin totals in lofs
+    for (int b = threadIdx.x; b < ns; b += kCsrT) {
+        uint32_t run = 0;
+        for (int q = 0; q < nw_use; q++) {
+            const uint32_t v = hist[(size_t)q * ns + b];
+            hist[(size_t)q * ns + b] = run;
+            run += v;
+        }
+        lofs[b] = run;
+    }
+    __syncthreads();
+    {   // exclusive scan of the bin totals: local offsets of the bins in the chunk's sorted order
+        const int per = (ns + kCsrT - 1) / kCsrT;
+        const int b0 = threadIdx.x * per, b1 = min(ns, b0 + per);
+        uint32_t local = 0;
+        for (int b = b0; b < b1; b++) local += lofs[b];
+        uint32_t inc = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const uint32_t v = lane < kCsrT / 32 ? wsum[lane] : 0u;  // wsum has 32 slots
+            uint32_t sc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, sc, o);
+                if (lane >= o) sc += t;
+            }
+            wsum[lane] = sc - v;
+        }
+        __syncthreads();
+        uint32_t base = wsum[w] + inc - local;
+        for (int b = b0; b < b1; b++) {
+            const uint32_t t = lofs[b];
+            lofs[b] = base;
+            base += t;
+        }
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < nw_use * ns; a += kCsrT) hist[a] += lofs[a % ns];
+    __syncthreads();
+    if (w < nw_use) {  // stable local slots: warps own contiguous row ranges, lanes ranked by match_any
+        uint32_t* mybase = hist + (size_t)w * ns;
+        for (int s0 = q0; s0 < q1; s0 += 32) {
+            const int q = s0 + lane;
+            const bool valid = q < q1;
+            const uint32_t b = valid ? (uint32_t)id[r0 + q] : 0xffffffffu;
+            const uint32_t mask = __match_any_sync(0xffffffffu, b);
+            const uint32_t lt = mask & ((1u << lane) - 1u);
+            if (valid) {
+                const uint32_t slot = mybase[b] + __popc(lt);
+                srow[slot] = (PermT)(r0 + q);
+                sbin[slot] = (uint16_t)b;
+            }
+            __syncwarp();
+            if (valid && lt == 0) mybase[b] += __popc(mask);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    PermT* perm = perm_out + (size_t)k * n;
+    for (int t = threadIdx.x; t < rows; t += kCsrT) {
+        const uint32_t b = sbin[t];
+        perm[gst[b] + (uint32_t)t - lofs[b]] = srow[t];
+    }
+}
+}  // namespace
+
 int cwb_launch_csr(cwb_ctx* ctx, const void* idx, int32_t idx_bytes, int64_t n, int32_t K,
                    int32_t ns, uint32_t* cnt, int32_t* off, void* perm, int32_t perm_bytes,
                    cudaStream_t s) {
+    const int* st0 = ctx ? ctx->d_status : nullptr;
+    static const bool chunked_ok = [] {  // CWB_CSR_CHUNKED=0: always the one-CTA-per-learner k_csr
+        const char* e = getenv("CWB_CSR_CHUNKED");
+        return !(e && e[0] == '0');
+    }();
+    if (chunked_ok && n > 4 * (int64_t)kCsrC && ns <= 65535) {  // chunked: (chunk, learner) CTAs over all SMs
+        const int nch = (int)((n + kCsrC - 1) / kCsrC);
+        const size_t fixed = (size_t)kCsrC * (perm_bytes + 2) + 2 * sizeof(uint32_t) * ns;
+        int nw = kCsrT / 32;
+        while (nw > 1 && fixed + sizeof(uint32_t) * (size_t)nw * ns > 220 * 1024) nw >>= 1;
+        const size_t ssm = fixed + sizeof(uint32_t) * (size_t)nw * ns;
+        if (ssm <= 220 * 1024) {
+            uint32_t* ccnt = nullptr;
+            if (cwb_alloc((void**)&ccnt, sizeof(uint32_t) * (size_t)K * nch * ns, s) != cudaSuccess)
+                return cwb_set_error(ctx, CWB_ENOMEM, "bin inversion scratch allocation failed");
+            const dim3 g(nch, K);
+            if (idx_bytes == 1)
+                k_csrc_count<uint8_t><<<g, kCsrT, sizeof(uint32_t) * ns, s>>>((const uint8_t*)idx, n, ns, nch, ccnt, st0);
+            else
+                k_csrc_count<uint16_t><<<g, kCsrT, sizeof(uint32_t) * ns, s>>>((const uint16_t*)idx, n, ns, nch, ccnt, st0);
+            k_csrc_scan<<<K, 1024, sizeof(uint32_t) * ns, s>>>(ccnt, n, ns, nch, cnt, off, st0);
+#define CSRC_CASE(IT, PT)                                                                                  \
+            {                                                                                              \
+                auto kern = k_csrc_scatter<IT, PT>;                                                        \
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);         \
+                kern<<<g, kCsrT, ssm, s>>>((const IT*)idx, n, ns, nch, nw, ccnt, (PT*)perm, st0);          \
+            }
+            if (idx_bytes == 1 && perm_bytes == 2) CSRC_CASE(uint8_t, uint16_t)
+            else if (idx_bytes == 1) CSRC_CASE(uint8_t, uint32_t)
+            else if (perm_bytes == 2) CSRC_CASE(uint16_t, uint16_t)
+            else CSRC_CASE(uint16_t, uint32_t)
+#undef CSRC_CASE
+            cwb_release(ccnt, s);
+            if (ctx) ctx->launches += 3;
+            return cwb_check_launch(ctx, "chunked bin inversion");
+        }
+    }
     const int threads = 1024;
     int nw = smem_csr_warps(ns, threads / 32);
     size_t smem = (size_t)(nw + 1) * ns * sizeof(uint32_t);
@@ -665,7 +941,16 @@ int cwb_launch_csr(cwb_ctx* ctx, const void* idx, int32_t idx_bytes, int64_t n, 
 int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32_t K, int32_t ns,
                         double* lo, double* hi, double* z, double* bnd, void* idx, int32_t idx_bytes,
                         cudaStream_t s, int32_t* nsk) {
-    k_minmax<<<K, 512, 0, s>>>(x, n, lo, hi, st);
+    // I1: ~8 blocks of 256 threads per SM over all learners
+    const int nsm = cwb_num_sms();
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * kMMT - 1) / (4 * kMMT),
+                                                              (8LL * nsm + K - 1) / K));
+    double* mmp = nullptr;
+    if (cwb_alloc((void**)&mmp, sizeof(double) * 3 * (size_t)nb * K, s) != cudaSuccess)
+        return cwb_set_error(ctx, CWB_ENOMEM, "min/max scratch allocation failed");
+    k_minmax_part<<<dim3(nb, K), kMMT, 0, s>>>(x, n, nb, mmp);
+    k_minmax_fin<<<K, 32, 0, s>>>(mmp, nb, lo, hi, st);
+    cwb_release(mmp, s);
     unsigned long long* gtab = nullptr;
     if (nsk) {  // per-learner n* clamp
         const int T = 1024;
@@ -681,20 +966,21 @@ int cwb_launch_bin_only(cwb_ctx* ctx, int* st, const double* x, int64_t n, int32
         if (ctx) ctx->launches++;
     }
     k_design<<<K, 256, 0, s>>>(lo, hi, ns, nsk, z, bnd, st);
-    int gx = (int)((n + 255) / 256);
-    if (gx > 1184) gx = 1184;
+    // I3: contiguous row ranges, ~4 waves of 256-thread blocks over all learners (each block
+    // stages the learner's boundaries once)
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (32LL * nsm + K - 1) / K));
     dim3 grid(gx, K);
     size_t smem = sizeof(double) * (size_t)(ns > 1 ? ns - 1 : 1);
     const bool use_smem = smem <= 48 * 1024;
     if (!use_smem) smem = 0;
     if (idx_bytes == 1) {
-        if (use_smem) k_bin<uint8_t, true><<<grid, 256, smem, s>>>(x, n, ns, bnd, (uint8_t*)idx, st);
-        else k_bin<uint8_t, false><<<grid, 256, 0, s>>>(x, n, ns, bnd, (uint8_t*)idx, st);
+        if (use_smem) k_bin<uint8_t, true><<<grid, 256, smem, s>>>(x, n, ns, bnd, lo, hi, nsk, (uint8_t*)idx, st);
+        else k_bin<uint8_t, false><<<grid, 256, 0, s>>>(x, n, ns, bnd, lo, hi, nsk, (uint8_t*)idx, st);
     } else {
-        if (use_smem) k_bin<uint16_t, true><<<grid, 256, smem, s>>>(x, n, ns, bnd, (uint16_t*)idx, st);
-        else k_bin<uint16_t, false><<<grid, 256, 0, s>>>(x, n, ns, bnd, (uint16_t*)idx, st);
+        if (use_smem) k_bin<uint16_t, true><<<grid, 256, smem, s>>>(x, n, ns, bnd, lo, hi, nsk, (uint16_t*)idx, st);
+        else k_bin<uint16_t, false><<<grid, 256, 0, s>>>(x, n, ns, bnd, lo, hi, nsk, (uint16_t*)idx, st);
     }
-    if (ctx) ctx->launches += 3;
+    if (ctx) ctx->launches += 4;
     return cwb_check_launch(ctx, "binning kernels");
 }
 
