@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(kStreamT, 1)
     double* Pj = P + ((size_t)q * N + j) * nslot * NU;
     const double* col = R + (size_t)q * n;
     const bool tma = (((uintptr_t)col) & 15) == 0;   // chunk starts are 16-byte aligned iff the column is
+    // programmatic dependent launch: k_fit_narrow may start its prologue on SMs this grid frees
+    // (it waits for this grid's completion before it reads P and rrp)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int a = tid; a < NU; a += blockDim.x) U[a] = 0.0;
     if (tid < 2 * kPad) sm[(tid / kPad) * (kC + kPad) + kC + (tid % kPad)] = 0.0;
     if (tid == 0) {
@@ -532,6 +535,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     }
     __syncthreads();
     const int nj = s_nj;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_h1_stream complete: P and rrp visible
     for (int e = tid; e < ns * B; e += blockDim.x) {  // u_k(l) for column q, partials added in CTA order
         const int l = e / B, q = e - l * B;
         const double* pq = P + (size_t)q * N * nslot * NU + a0 + l;
@@ -758,8 +762,22 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
                                                     p.gtab, p.dest, p.isize, p.ibase, p.wst, p.part, rrp, c->d_status);
     const size_t fsm = sizeof(double) * ((((size_t)ns * B + 1) & ~(size_t)1) + (size_t)c->W * d + 2 * (size_t)d * d);
     cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    k_fit_narrow<<<K, 1024, fsm, s>>>(p.part, K, ns, p.Ks, p.nch, p.nitems, N, nslot, B, d, c->W, c->ZT, c->lwin,
-                                      c->Ainv, c->G, rrp, th, de, ticket, k_out, theta_out, sse_out);
+    {   // launched as a programmatic dependent of k_h1_stream (prologue overlaps its tail)
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(K);
+        lc.blockDim = dim3(1024);
+        lc.dynamicSmemBytes = fsm;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        CWB_CUDA_TRY(c, cudaLaunchKernelEx(&lc, k_fit_narrow, (const double*)p.part, K, ns, p.Ks, p.nch, p.nitems, N,
+                                           nslot, B, d, (int)c->W, (const double*)c->ZT, (const int32_t*)c->lwin,
+                                           (const double*)c->Ainv, (const double*)c->G, (const double*)rrp, th, de,
+                                           ticket, k_out, theta_out, sse_out));
+    }
     c->launches += 2;
     return cwb_check_launch(c, "stream find_best kernels");
 }

@@ -1,4 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_csr.py -q -x > gpurun_out/s62_pytest.log 2>&1 || { tail -30 gpurun_out/s62_pytest.log; exit 1; }
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_clamp.py tests/test_gpu_stream.py tests/test_gpu_rows.py -q -x >> gpurun_out/s62_pytest.log 2>&1; tail -3 gpurun_out/s62_pytest.log
-timeout 300 python tools/init_timing.py R4 5 > gpurun_out/s62_init.log 2>&1; timeout 300 python tools/init_timing.py R3 5 >> gpurun_out/s62_init.log 2>&1; timeout 300 python tools/init_timing.py R2 10 >> gpurun_out/s62_init.log 2>&1; cat gpurun_out/s62_init.log
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/s62_init_R4.csv python tools/init_timing.py R4 1 > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_gpu_stream.py tests/test_gpu_clamp.py tests/test_gpu_degree.py -q -x > gpurun_out/s63_pytest.log 2>&1; tail -3 gpurun_out/s63_pytest.log
+for c in R2 R3 R4; do timeout 120 python tools/findbest_timing.py $c 1 3 0 >> gpurun_out/s63_fb.log 2>&1; done; cat gpurun_out/s63_fb.log
