@@ -508,17 +508,17 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     }
     if (tid < 2 * d) s_lw[tid] = lwin[(size_t)k * d * 2 + tid];
     // the CTAs whose item range meets [lg nch, (lg+1) nch), and their slot for lg (warp 0, a lane per CTA)
-    if (w == 0) {
-        const int64_t it0 = (int64_t)lg * nch, it1 = it0 + nch;
-        int jlo = (int)(it0 * N / nitems);
-        while (jlo > 0 && (int64_t)nitems * jlo / N > it0) jlo--;
+    if (w == 0) {  // (32-bit divisions: nitems * (N + 1) < 2^31 is checked on the host)
+        const int it0 = lg * nch, it1 = it0 + nch;
+        int jlo = it0 * N / nitems;
+        while (jlo > 0 && nitems * jlo / N > it0) jlo--;
         int m = 0;
         for (int base = jlo;; base += 32) {
             const int jj = base + lane;
-            int64_t b0 = 0, b1 = 0;
+            int b0 = 0, b1 = 0;
             if (jj < N) {
-                b0 = (int64_t)nitems * jj / N;
-                b1 = (int64_t)nitems * (jj + 1) / N;
+                b0 = nitems * jj / N;
+                b1 = nitems * (jj + 1) / N;
             }
             const bool ov = jj < N && b0 < it1 && b1 > it0 && b0 != b1;
             const bool stop = jj >= N || b0 >= it1;
@@ -733,6 +733,7 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
                          double* sse_out, cudaStream_t s) {
     if (c->rows || B < 1 || B > 4 || (size_t)c->n_star * B * sizeof(double) > 96 * 1024 ||
         c->n_star > kUBudget) return CWB_EUNSUPPORTED;
+    if ((int64_t)c->K * ((c->n + kC - 1) / kC) * (CWB_MAX_SMS + 1) >= INT32_MAX) return CWB_EUNSUPPORTED;  // item math in int32
     int rc = stream_plan(c, s);
     if (rc) return rc;
     cwb_stream_plan& p = c->sp;

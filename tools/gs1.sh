@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_stream.py tests/test_gpu_clamp.py tests/test_gpu_degree.py -q -x > gpurun_out/s63_pytest.log 2>&1; tail -3 gpurun_out/s63_pytest.log
-for c in R2 R3 R4; do timeout 120 python tools/findbest_timing.py $c 1 3 0 >> gpurun_out/s63_fb.log 2>&1; done; cat gpurun_out/s63_fb.log
+timeout 600 python -m pytest tests/test_gpu_stream.py -q -x > gpurun_out/s65_pytest.log 2>&1; tail -2 gpurun_out/s65_pytest.log
+for c in R2 R3 R4; do timeout 120 python tools/findbest_timing.py $c 1 3 0 >> gpurun_out/s65_fb.log 2>&1; done; cat gpurun_out/s65_fb.log
