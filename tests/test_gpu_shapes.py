@@ -93,3 +93,27 @@ def test_fused_variants_equal_general(seed, n, K, ns, B, algo):
     assert ok, e
     ok, e = close(a["risk_trace"][:, same], b["risk_trace"][:, same], RTOL)
     assert ok, e
+
+
+@pytest.mark.parametrize("seed,n,K,ns,B", [(7, 3000, 300, 40, 5), (8, 2500, 600, 50, 3), (9, 1500, 130, 39, 200)])
+def test_many_learners_vs_oracle(seed, n, K, ns, B):
+    # K beyond the persistent kernel's shared memory: the auto path (per-iteration kernels or
+    # the fused layout where it still fits) against the oracle, selection over hundreds of learners
+    X, Y = data(seed, n, K, B)
+    oc, gc = cfgs(ns)
+    pg = cwb.Pool(dev(X), gc)
+    g = host(pg.train(dev(Y), nu=0.1, M=30))
+    pg.status()
+    po = O.Pool(X, oc, O.MODE_BINNED)
+    o, _ = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=30, threads=8)
+    assert (o.k_trace == g["k_trace"]).all()
+    for key, ref in (("theta_agg", o.theta_agg), ("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
+        ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())
+        assert ok, f"{key} {e}"
+    # findBest on two columns through the narrow path
+    R = Y[:2] - Y[:2].mean(1, keepdims=True)
+    k, th, sse = (t.cpu().numpy() for t in pg.find_best(dev(R)))
+    for b in range(2):
+        ko, tho, sseo, _, gap = po.find_best(R[b])
+        assert k[b] == ko or gap / sseo <= TIE_RTOL
+    pg.close()
