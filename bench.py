@@ -203,6 +203,40 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def findbest_b1(devname, peaks, name="R3", calls=15):
+    """SURVEY Sec. 8(d) target: one findBestBaselearner (cwb_find_best) on ONE residual column at R3
+    (u16 index vectors) against the HBM roofline of its algorithmic bytes K*n*2 + n*8.  L2 is flushed
+    (256 MiB write) before every call and each call is timed alone with CUDA events; median."""
+    import torch
+    from paper_2110_03513_b200 import cwb
+    c = S.CONFIGS[name]
+    ds = S.make(c, reps=[0])
+    X = torch.as_tensor(ds.X, device=devname)
+    R = torch.as_tensor(ds.Y - ds.Y.mean(1, keepdims=True), device=devname)
+    pool = cwb.Pool(X, cwb.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots,
+                                  degree=c.degree, df=c.df))
+    buf = torch.empty(256 << 20, dtype=torch.uint8, device=devname)
+    for _ in range(3):
+        pool.find_best(R)
+    ts = []
+    for i in range(calls):
+        buf.fill_(i & 255)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pool.find_best(R)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    pool.status()
+    pool.close()
+    us = float(np.median(ts))
+    alg = c.K * c.n * (1 if pool.n_star <= 256 else 2) + c.n * 8
+    peak = float(peaks.get("hbm_gbs", 6548.2))
+    return {"workload": name, "B": 1, "us": us, "alg_bytes": alg, "achieved_gbs": alg / us * 1e-3,
+            "peak_gbs": peak, "frac": alg / us * 1e-3 / peak, "target_frac": 0.6,
+            "kernels": "k_h1_stream + k_fit_narrow", "l2": "flushed before every call"}
+
+
 def workload_config(c, n_star, d):
     return {"workload": c.name, "n": c.n, "K": c.K, "B_per_gpu": c.B, "M": c.M, "nu": c.nu,
             "n_star": n_star, "d": d, "df": c.df, "degree": c.degree, "n_knots": c.n_knots,
@@ -227,6 +261,8 @@ def main():
     ap.add_argument("--unbinned", action="store_true",
                     help="unbinned learners on the raw x (SURVEY NEXT-3): the baseline binning is compared to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-findbest", action="store_true",
+                    help="skip the auxiliary B = 1 findBest measurement at R3 (SURVEY Sec. 8(d) target)")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_SHORT"), \
@@ -485,6 +521,11 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": int(sum(launches)),
         }
+        if args.algo == "cwb" and not strong and not args.unbinned and ws == 1 and not args.no_findbest:
+            try:  # after the timed region: does not touch the step measurement
+                line["findbest_b1"] = findbest_b1(devname, peaks)
+            except Exception as e:
+                line["findbest_b1"] = {"error": str(e)}
         if not args.no_cpu_baseline and ws == 1:
             try:
                 line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, algo=args.algo,
