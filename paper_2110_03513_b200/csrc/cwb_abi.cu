@@ -186,8 +186,12 @@ void cwb_free(cwb_ctx* c) {
     cwb_stream_release(c, s);
     cwb_nb_release(c, s);
     cwb_release(c->h1c, s);
-    if (c->ev_plan) cudaEventDestroy(c->ev_plan);
+    if (c->ev_plan) {
+        cudaEventSynchronize(c->ev_plan);  // the header copy into the pinned slot has landed
+        cudaEventDestroy(c->ev_plan);
+    }
     if (c->ev_csr) cudaEventDestroy(c->ev_csr);
+    cwb_release_header_slot(c->h_hdr);
     // c->s2 is the device's shared side stream: not destroyed
     delete c;
 }

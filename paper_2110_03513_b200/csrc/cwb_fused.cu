@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "cwb_internal.cuh"
 
@@ -1279,17 +1280,30 @@ size_t cwb_fused_smem_bytes(const cwb_ctx* c) {
 }
 
 // (Re)builds the H1 task plan for the shape of a B-replication launch.
-// Pinned host slots for the plan headers (read back without a synchronous copy).
+// Pinned host slots for the plan headers (read back without a synchronous copy).  A slot belongs
+// to one context from its first plan until cwb_free (cwb_release_header_slot); slots come from
+// pinned chunks of 256, allocated on demand, so live contexts never share one.
+namespace {
+std::mutex g_hdr_mu;
+std::vector<int32_t*> g_hdr_free;
+}  // namespace
+
 static int32_t* pinned_header_slot() {
-    static std::once_flag once;
-    static int32_t* pool = nullptr;
-    static std::atomic<unsigned> next{0};
-    std::call_once(once, [] {
+    std::lock_guard<std::mutex> lock(g_hdr_mu);
+    if (g_hdr_free.empty()) {
         void* p = nullptr;
-        if (cudaHostAlloc(&p, sizeof(int32_t) * 16 * 256, cudaHostAllocDefault) == cudaSuccess) pool = (int32_t*)p;
-    });
-    if (!pool) return nullptr;
-    return pool + 16 * (next.fetch_add(1) % 256);
+        if (cudaHostAlloc(&p, sizeof(int32_t) * 16 * 256, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+        for (int i = 255; i >= 0; i--) g_hdr_free.push_back((int32_t*)p + 16 * i);
+    }
+    int32_t* slot = g_hdr_free.back();
+    g_hdr_free.pop_back();
+    return slot;
+}
+
+void cwb_release_header_slot(int32_t* slot) {
+    if (!slot) return;
+    std::lock_guard<std::mutex> lock(g_hdr_mu);
+    g_hdr_free.push_back(slot);
 }
 
 // Launches the H1 plan for launch shape f on stream s (allocations stream-ordered on s):

@@ -227,6 +227,8 @@ int cwb_predict_impl(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* 
 
 // Streaming multiprocessors of the current device (B200: 148), queried once; grids are sized by it.
 int cwb_num_sms();
+// Returns a context's pinned plan-header slot to the pool (cwb_free).
+void cwb_release_header_slot(int32_t* slot);
 constexpr int CWB_MAX_SMS = 256;  // bound for per-SM tables in shared memory
 
 // Warp reductions with a fixed butterfly order (deterministic).

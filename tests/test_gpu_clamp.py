@@ -89,6 +89,12 @@ def test_train_on_tied_features_matches_oracle(path):
     for key, ref in (("theta_agg", o.theta_agg), ("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
         ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())
         assert ok, f"{key} {e}"
+    # prediction on new points (tied values, values between and outside the training levels)
+    Xn = np.concatenate([X[:, :300], X[:, :300] + 0.37, X[:, :50] * 3.0 - 2.0], axis=1)
+    pred = pg.predict(dev(Xn), dev(g["offset"]), dev(g["theta_agg"])).cpu().numpy()
+    opred = po.predict(Xn, g["offset"], g["theta_agg"])
+    ok, e = close(pred, opred, RTOL, scale=np.abs(opred).max())
+    assert ok, f"predict {e}"
     # streaming findBest on one column
     R = Y[:1] - Y[:1].mean(1, keepdims=True)
     pg.set_narrow(0)

@@ -68,6 +68,12 @@ def test_learner_config_matches_oracle(degree, n_knots, ns, df):
         for key, ref in (("theta_agg", o.theta_agg), ("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
             ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())
             assert ok, f"path {path} {key} {e}"
+        if path == 2:  # prediction on new points, in and outside the training range
+            Xn = np.concatenate([X[:, :200] * 0.9 + 0.05, X[:, :40] * 2.5], axis=1)
+            pred = pg.predict(dev(Xn), dev(g["offset"]), dev(g["theta_agg"])).cpu().numpy()
+            opred = po.predict(Xn, g["offset"], g["theta_agg"])
+            ok, e = close(pred, opred, RTOL, scale=np.abs(opred).max())
+            assert ok, f"predict {e}"
     # streaming findBest, one column
     R = Y[:1] - Y[:1].mean(1, keepdims=True)
     pg.set_narrow(0)
