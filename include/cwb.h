@@ -116,14 +116,18 @@ int cwb_bin_mat_vec(const double* Zb, int32_t n_star, int32_t d, const void* idx
  * ---------------------------------------------------------------------- */
 
 /* Builds the pool of K binned P-spline learners from X[K][n] (feature-major):
- * per learner min/max, design points, index vector, the bin
- * inversion (rows sorted by bin), basis at the design points Zb,
- * G = binMatMat, lambda with df(lambda) = cfg->df via the
- * Demmler-Reinsch orthogonalisation (supp. P:L319) and the cached inverse of
- * G + lambda D.  cfg == NULL uses the defaults.  The context owns
- * all its device buffers (stream-ordered allocations on `stream`).
- * Errors: CWB_EINVAL (n < 2, K < 1, d > 32, degree not in 1..3),
- * CWB_EEMPTY (K == 0); device-side errors via cwb_status(). */
+ * per learner min/max, the number of bins min(n*, distinct values),
+ * design points, index vector, the bin inversion (rows sorted by
+ * bin), basis at the design points Zb, G = binMatMat, lambda
+ * with df(lambda) = cfg->df (supp. P:L314-319; solved by safeguarded Newton on
+ * the definition tr((G + lambda D)^-1 G)) and the cached
+ * inverse of G + lambda D.  cfg == NULL uses the defaults.  The
+ * context owns all its device buffers (stream-ordered allocations on `stream`).
+ * Errors: CWB_EINVAL (n < 2, K < 1, d > 32, degree not in 1..3, n* < 2),
+ * CWB_EUNSUPPORTED (n* > 12288 bins per learner: the pool kernels keep per-bin
+ * tables in shared memory; cwb_bin alone accepts up to 65536), CWB_EEMPTY
+ * (K == 0); device-side errors (constant feature, non-finite x, unreachable
+ * df) via cwb_status(). */
 int cwb_init(cwb_ctx** ctx, const double* X, int64_t n, int32_t K, const cwb_config* cfg,
              cudaStream_t stream);
 

@@ -208,6 +208,8 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     const int64_t ns = n_star_of(n, cfg);
     const int d = cfg.n_knots + cfg.degree + 1;
     if (ns < 2 || ns > 65536) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: n* out of range");
+    if (ns > CWB_POOL_MAX_NSTAR)  // per-bin tables of the pool kernels live in shared memory
+        return cwb_set_error(nullptr, CWB_EUNSUPPORTED, "cwb_init: n* > 12288 bins per learner");
     if (cfg.degree < 1 || cfg.degree > 3 || cfg.n_knots < 0 || d > CWB_MAX_D)
         return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: need degree 1..3 and d <= 32");
     if (cfg.df_kind != 1 && cfg.df_kind != 2) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: df_kind");

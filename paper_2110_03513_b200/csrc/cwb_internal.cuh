@@ -13,6 +13,7 @@
 
 #define CWB_MAX_D 32      // basis dimension d <= 32: one warp lane per coefficient
 #define CWB_SPW 4         // non-zero B-spline values per design point (degree <= 3)
+#define CWB_POOL_MAX_NSTAR 12288  // bins per learner of a pool: per-bin u32 tables in 48 KB of shared memory
 #define CWB_FUSED_THREADS 256
 
 // Device-side error recording: first error wins.

@@ -85,3 +85,22 @@ def test_learner_config_matches_oracle(degree, n_knots, ns, df):
         assert close(sse[0], sseo, RTOL)[0]
         assert close(th[0], tho, RTOL, scale=np.abs(tho).max())[0]
     pg.close()
+
+
+def test_bin_count_limit():
+    # the largest pool n* (12288) trains and matches the oracle's findBest; one more bin is rejected
+    rng = np.random.default_rng(31)
+    n = 40000
+    X = np.stack([rng.uniform(-1, 1, n), rng.standard_normal(n)])
+    Y = np.sin(3 * X[:1]) + 0.2 * rng.standard_normal((1, n))
+    pg = cwb.Pool(dev(X), cwb.Config(n_star_rule=2, n_star_fixed=12288, n_knots=20))
+    po = O.Pool(X, O.Config(n_star_rule=2, n_star_fixed=12288, n_knots=20), O.MODE_BINNED)
+    assert (pg.n_star_k() == po.nsk).all()
+    R = Y - Y.mean(1, keepdims=True)
+    k, th, sse = (t.cpu().numpy() for t in pg.find_best(dev(R)))
+    ko, tho, sseo, _, gap = po.find_best(R[0])
+    assert k[0] == ko and close(sse[0], sseo, RTOL)[0]
+    pg.close()
+    with pytest.raises(cwb.CwbError) as e:
+        cwb.Pool(dev(X), cwb.Config(n_star_rule=2, n_star_fixed=12289, n_knots=20))
+    assert e.value.name == "CWB_EUNSUPPORTED"
