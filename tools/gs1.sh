@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_degree.py tests/test_gpu_parity.py -q -x -k "limit or pool or bin" > gpurun_out/s78_pytest.log 2>&1; tail -3 gpurun_out/s78_pytest.log
+timeout 600 python -m pytest tests/test_gpu_edges.py -q > gpurun_out/s80_pytest.log 2>&1; tail -30 gpurun_out/s80_pytest.log
