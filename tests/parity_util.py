@@ -37,16 +37,21 @@ def close(a, b, rtol=RTOL, scale=None):
 
 
 def compare_traces(gpu_k, orc_k, orc_gap, orc_sse):
-    """Returns (first_divergence[B] (M if none), list of (m, b) verified ties)."""
+    """Returns (first_divergence[B] (M if none), list of (m, b) verified ties).  The SSE gap is
+    measured relative to the best SSE with the agreement rules' absolute floor of 1e-12 of the
+    targets' scale ("absolute floor 1e-12 ||y||^2"; the largest SSE of the batch stands
+    for ||r||^2): two learners that both fit the residual exactly (SSE ~ 0, e.g. two training rows
+    and three coefficients) are a tie whatever rounding noise separates them."""
     M, B = orc_k.shape
     first = np.full(B, M, dtype=np.int64)
     ties = []
+    floor = 1e-12 * float(np.abs(orc_sse).max()) if orc_sse.size else 0.0
     for b in range(B):
         bad = np.nonzero(gpu_k[:, b] != orc_k[:, b])[0]
         if len(bad) == 0:
             continue
         m = int(bad[0])
-        rel = orc_gap[m, b] / max(abs(orc_sse[m, b]), 1e-300)
+        rel = orc_gap[m, b] / max(abs(orc_sse[m, b]), floor, 1e-300)
         assert rel <= TIE_RTOL, (
             f"replication {b} iteration {m}: gpu k={gpu_k[m, b]} oracle k={orc_k[m, b]} "
             f"but the oracle's SSE gap is {rel:.3e} relative (not a tie)")
@@ -55,12 +60,14 @@ def compare_traces(gpu_k, orc_k, orc_gap, orc_sse):
     return first, ties
 
 
-def assert_train_parity(g, o, n, tag=""):
-    """g: dict of numpy arrays from the GPU; o: oracle TrainResult."""
+def assert_train_parity(g, o, n, tag="", min_full=0.9):
+    """g: dict of numpy arrays from the GPU; o: oracle TrainResult.  min_full: share of the
+    replications that must follow the oracle over all iterations (every divergence is a verified
+    tie either way; tiny problems with exact fits may tie on purpose)."""
     M, B = o.k_trace.shape
     first, ties = compare_traces(g["k_trace"], o.k_trace, o.gap_trace, o.sse_trace)
     full = first == M
-    assert full.mean() >= 0.9, f"{tag}: too many tie divergences {ties}"
+    assert full.mean() >= min_full, f"{tag}: too many tie divergences {ties}"
     ok, e = close(g["offset"], o.offset, 1e-12)
     assert ok, f"{tag}: offset rel err {e}"
     for b in range(B):

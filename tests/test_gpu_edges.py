@@ -87,3 +87,42 @@ def test_edge_shapes_all_entry_points(n, K, B, ns, dg, nk, df, path):
         # a forced fused path may refuse the shape first (EUNSUPPORTED) -- never accept it
         assert e.value.name == "CWB_" + oracle_err or (path == 1 and e.value.name == "CWB_EUNSUPPORTED")
     pg.close()
+
+
+@pytest.mark.parametrize("n,K,B,ns,dg,nk,df", CASES)
+def test_edge_shapes_folds_and_unbinned(n, K, B, ns, dg, nk, df):
+    rng = np.random.default_rng(n + K + B + 1)
+    X = rng.uniform(-1, 2, (K, n))
+    Y = np.cos(2 * X[0])[None, :] + 0.3 * rng.standard_normal((B, n))
+    ocfg = O.Config(n_star_rule=2, n_star_fixed=ns, degree=dg, n_knots=nk, df=df)
+    gcfg = cwb.Config(n_star_rule=2, n_star_fixed=ns, degree=dg, n_knots=nk, df=df)
+    po = O.Pool(X, ocfg, O.MODE_BINNED)
+    # CV folds (F = 2): replications cycle through no hold-out, fold 0, fold 1
+    F = 2
+    fold = S.cv_folds(n, F)
+    frep = (np.arange(B) % (F + 1) - 1).astype(np.int32)
+    try:
+        o, ov = po.train_folds(Y, fold, F, frep, nu=0.2, M=10)
+        oracle_err = None
+    except O.OracleError as e:
+        oracle_err = e.name
+    pg = cwb.Pool(dev(X), gcfg)
+    if oracle_err is None:
+        g = host(pg.train_folds(dev(Y), dev(fold, torch.uint8), F, dev(frep, torch.int32), nu=0.2, M=10))
+        pg.status()
+        assert_train_parity(g, o, n, tag="folds", min_full=0.0)  # 2 training rows: exact fits tie
+    else:
+        with pytest.raises(cwb.CwbError) as e:
+            pg.train_folds(dev(Y), dev(fold, torch.uint8), F, dev(frep, torch.int32), nu=0.2, M=10)
+            pg.status()
+        assert e.value.name == "CWB_" + oracle_err
+    pg.close()
+    if dg != 3:
+        return  # unbinned learners are cubic (include/cwb.h)
+    pu = O.Pool(X, ocfg, O.MODE_UNBINNED)
+    gu = cwb.Config(n_star_rule=2, n_star_fixed=ns, degree=dg, n_knots=nk, df=df, unbinned=1)
+    pg = cwb.Pool(dev(X), gu)
+    g = host(pg.train(dev(Y), nu=0.2, M=10))
+    pg.status()
+    assert_train_parity(g, pu.train(Y, nu=0.2, M=10), n, tag="unbinned")
+    pg.close()
