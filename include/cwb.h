@@ -157,18 +157,21 @@ int cwb_get_n_star_k(cwb_ctx* ctx, int32_t* n_star_k_out);
  * Zb[K][n*][d], G[K][d][d], Ainv[K][d][d].  Synchronises. */
 int cwb_get_pool(cwb_ctx* ctx, double* z, uint16_t* idx, double* Zb, double* G, double* Ainv);
 
-/* Implementation selector for cwb_train (tests use it to cover both):
- * 0 = auto, 1 = fused persistent kernel (one CTA per replication, residual
- * vector resident in shared memory; needs n*8 + K*n**8 bytes to fit), 2 =
- * general per-iteration kernels. */
+/* Implementation selector for cwb_train and its variants (tests use it to cover
+ * both): 0 = auto, 1 = fused persistent kernel (one CTA per one or two
+ * replications, residuals resident in shared memory; CWB_EUNSUPPORTED from the
+ * training call when its layout does not fit), 2 = general per-iteration kernels.
+ * Errors: CWB_EINVAL (path not 0..2), CWB_EUNSUPPORTED (1 on a row-sharded context). */
 int cwb_set_path(cwb_ctx* ctx, int32_t path);
 
 /* H1 implementation of cwb_find_best for B <= 4 columns (tests and benchmarks
  * compare them): 0 = streaming gather plan (built on the first call, which
- * synchronises the stream; per chunk of 8192 rows the bins of every learner
+ * synchronises the stream; per chunk of 8176 rows the bins of every learner
  * inverted into a gather schedule, binMatVec P:L898-902), falling back to 1
- * when n* > 12288; 1 = per-warp histograms with __match_any_sync grouping.
- * Errors: CWB_EINVAL (mode not 0 or 1). */
+ * when n* > 6144 (the bin sums of a learner group live in 48 KB of shared
+ * memory) or on a row-sharded context; 1 = per-warp histograms with
+ * __match_any_sync grouping, falling back to the per-iteration kernels where
+ * they do not fit.  Errors: CWB_EINVAL (mode not 0 or 1). */
 int cwb_set_narrow(cwb_ctx* ctx, int32_t mode);
 
 /* findBestBaselearner (Alg. 1 supp. lines 5-9) for B
