@@ -1,3 +1,4 @@
+# bench + ncu brief of the fused kernel in ACWB / HCWB / Bernoulli modes -> gpurun_out/r1g_*
 TAG=r1g
 mkdir -p gpurun_out
 python __graft_entry__.py build > gpurun_out/${TAG}_build.log 2>&1

@@ -1,6 +1,6 @@
 # round-end validation on one B200 (run under gpurun from the repo root): tests, smoke, bench (plain and
 # torchrun N=1), reference arm, launch list and an ncu capture of the top kernel -> gpurun_out/${TAG}_*
-# usage: /usr/local/graft/bin/gpurun --timeout 3000 -- 'TAG=r1z bash tools/gs1.sh'
+# usage: /usr/local/graft/bin/gpurun --timeout 3000 -- 'TAG=r1z bash tools/round_validation.sh'
 TAG=${TAG:-r1z}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_gpu_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_gpu_pytest.log
