@@ -9,7 +9,7 @@
 // rows of one bin into a register:
 //
 //   plan (built once, lazily, on the first narrow findBest):
-//     rows are cut into chunks of C = 8192 (a chunk of r is 64 KB of shared memory);
+//     rows are cut into chunks of C = 8176 (a chunk of r is ~64 KB of shared memory);
 //     learners into groups of Ks (the group's bin sums, Ks * n* doubles, stay in
 //     shared memory across chunks).  For every item (learner group, chunk) the
 //     non-empty bins of the group's learners are tasks; tasks are sorted by row count
