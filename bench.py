@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the B200 binned-CWB engine (arXiv 2110.03513).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config R1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config R3] [--impl ours|reference]
 
 One STEP = the whole hot path on one batch: cwb_init (binning, bin inversion,
 basis, G, df->lambda, cached inverse) + cwb_train (M boosting iterations for
@@ -18,6 +18,19 @@ B replications, no collective on the data path); with --shard rows the rows
 are (strong scaling: the B replications of the workload on n rows split over
 the ranks, one NCCL all-reduce of (K d + 1) x B doubles per iteration issued
 by libcwb).
+
+Default workload: R3 (n = 200,000, K = 66, B = 512, M = 200), the largest rung
+of the ladder that runs on one GPU (P:L1047 scale); R1 and
+the others by --config.
+
+Roofline: for the dominant kernel of the step (k_train_fused
+when the whole run is one persistent launch, else the binMatVec phase H1 of the
+per-iteration path, timed with CUDA events that libcwb records around it),
+roofline time = max(bytes_alg / HBM, adds_alg / DADD) with bytes_alg =
+K n ceil(log2 n* / 8) + n B 8 (H1 reads the index vectors and the residuals;
++ n B 8 for the residual write of a whole iteration) and adds_alg = K n B;
+frac = roofline time / kernel time.  HBM = MEASURED_PEAKS.json's copy bandwidth,
+DADD = the measured issue rate in profiles/peaks_fp64.json (tools/peaks.py).
 
 --impl reference times the CPU oracle (oracle/, plain fp64 C) on a bounded
 sample of the same workload on the host cores (rank 0 only).
@@ -60,17 +73,51 @@ def alg_ops_per_rep_iter(c, n_star, d, unbinned=False):
 GATHER_LANE_LOADS_PER_CLK = {2: 7.1, 1: 12.7}
 
 
-def fp64_peak_ops(peaks):
-    mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    return 148 * 64 * mhz * 1e6      # 148 SMs x 64 FP64 lanes/clk (B200), one add or FMA each
-
-
 def load_peaks():
+    """MEASURED_PEAKS.json (driver-written: HBM copy GB/s, clocks) + profiles/peaks_fp64.json
+    (tools/peaks.py on this pool's B200: DADD / DFMA issue rate, L2 / HBM read, DGEMM)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        return json.load(open(p)), "measured"
+        peaks, src = json.load(open(p)), "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+        peaks, src = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+    try:
+        f = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64.json")))
+        m = {r["what"]: r for r in f["measurements"]}
+        peaks["dadd_tops"] = m["dadd"]["ops_per_s"] / 1e12
+        peaks["dfma_tops"] = m["dfma"]["ops_per_s"] / 1e12
+        peaks["l2_read_gbs"] = m["l2_read"]["gb_per_s"]
+        peaks["hbm_read_gbs"] = m["hbm_read"]["gb_per_s"]
+        peaks["dgemm_tflops"] = m["dgemm_cublas"]["tflops"]
+        peaks["fp64_src"] = "measured (profiles/peaks_fp64.json)"
+    except Exception:  # datasheet product, said so in the line
+        peaks["dadd_tops"] = 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e-6
+        peaks["fp64_src"] = "datasheet (148 SM x 64 lanes x clock): profiles/peaks_fp64.json missing"
+    return peaks, src
+
+
+def idx_bytes_of(n_star):
+    return 1 if n_star <= 256 else 2   # ceil(log2 n* / 8)
+
+
+def sec8d_roofline(K, n, B, n_star, peaks, kernel_s, units, what, bytes_extra=0):
+    """roofline time = max(bytes_alg / HBM, adds_alg / DADD) of `units` launches-worth of
+    work (H1 of one iteration: K n idx bytes + n B 8 residual bytes, K n B adds); frac = that / kernel time."""
+    bytes_alg = units * (K * n * idx_bytes_of(n_star) + n * B * 8 + bytes_extra)
+    adds_alg = units * K * n * B
+    hbm = float(peaks["hbm_gbs"]) * 1e9
+    dadd = float(peaks["dadd_tops"]) * 1e12
+    t_hbm, t_dadd = bytes_alg / hbm, adds_alg / dadd
+    bound = "hbm" if t_hbm >= t_dadd else "alu"
+    if bound == "hbm":
+        achieved, peak, unit = bytes_alg / kernel_s / 1e9, hbm / 1e9, "GB/s"
+    else:
+        achieved, peak, unit = adds_alg / kernel_s / 1e12, dadd / 1e12, "Tadd/s"
+    return {"bound": bound, "kernel": what, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": max(t_hbm, t_dadd) / kernel_s,
+            "terms": {"bytes_alg": bytes_alg, "adds_alg": adds_alg, "t_hbm_ms": t_hbm * 1e3,
+                      "t_dadd_ms": t_dadd * 1e3, "t_kernel_ms": kernel_s * 1e3,
+                      "hbm_gbs": hbm / 1e9, "dadd_tops": dadd / 1e12}}
 
 
 class ClockSampler:
@@ -132,6 +179,9 @@ def dist_env():
     return w.size, w.rank, w.local_rank
 
 
+_ORACLE_PLAN = {}
+
+
 def oracle_sample(cfg, seconds_target=12.0, threads=None, algo="cwb", unbinned=False):
     """Time the oracle as it stands (binned mode = the paper's Algorithm binMatVec; unbinned mode for
     --unbinned) on a bounded sample of the workload, running the same algorithm as the GPU arm."""
@@ -153,28 +203,35 @@ def oracle_sample(cfg, seconds_target=12.0, threads=None, algo="cwb", unbinned=F
             return pool.train_bernoulli(Y, nu=c.nu, M=M, threads=th)
         return pool.train(Y, nu=c.nu, M=M, threads=th)
 
-    # probe: one replication, a few iterations
-    ds = S.make(c, reps=range(min(c.B, threads)))
+    # probe (first call only): one replication, a few iterations, on a pool built once; sizes the sample so that
+    # its training part takes about seconds_target on `threads` cores (at least one replication per core
+    # is free: the replications run in parallel)
+    key = (c.name, algo, unbinned, threads, seconds_target)
+    if key not in _ORACLE_PLAN:
+        ds1 = S.make(c, reps=range(1))
+        t0 = time.perf_counter()
+        pool = O.Pool(ds1.X, oc, mode)
+        t_init = time.perf_counter() - t0
+        M_probe = max(1, min(c.M, 5))
+        t0 = time.perf_counter()
+        run(pool, ds1, M_probe, 1)
+        per_rep_iter = (time.perf_counter() - t0) / M_probe
+        del pool
+        reps = int(max(1, seconds_target * threads / max(per_rep_iter * c.M, 1e-9)))
+        reps = max(min(reps, c.B), min(threads, c.B), 1)
+        _ORACLE_PLAN[key] = (reps, S.make(c, reps=range(reps)))
+    reps, ds = _ORACLE_PLAN[key]
+    # one step: pool build (the GPU arm's cwb_init) + M iterations of the sampled replications
     t0 = time.perf_counter()
     pool = O.Pool(ds.X, oc, mode)
     t_init = time.perf_counter() - t0
-    M_probe = max(1, min(c.M, 5))
-    ds1 = S.make(c, reps=range(1))
-    t0 = time.perf_counter()
-    run(pool, ds1, M_probe, 1)
-    per_rep_iter = (time.perf_counter() - t0) / M_probe
-    reps = int(max(1, min(c.B, seconds_target * threads / max(per_rep_iter * c.M, 1e-9))))
-    reps = max(min(reps, c.B), 1)
-    ds = S.make(c, reps=range(reps))
-    t0 = time.perf_counter()
-    pool = O.Pool(ds.X, oc, mode)
     run(pool, ds, c.M, threads)
     dt = time.perf_counter() - t0
     evals = fits * c.K * c.n * reps * c.M
     kind = "unbinned mode" if unbinned else "binned mode (Algorithm binMatVec, P:L898-904)"
     return {"value": evals / dt, "unit": UNIT, "cores": min(threads, reps), "kind": "oracle",
             "sample": f"{c.name}: {reps} of {c.B} replications x M={c.M} iterations, oracle {algo}, {kind}, "
-                      f"pool build included; {dt:.2f} s",
+                      f"pool build included ({t_init:.2f} s); {dt:.2f} s",
             "seconds": dt, "init_s": t_init}
 
 
@@ -182,6 +239,7 @@ def run_reference(args, cfg):
     ws, rank, local = dist_env()
     if rank != 0:
         return
+    from oracle import oracle as O
     threads = os.cpu_count() or 1
     res = []
     for i in range(args.warmup + args.steps):
@@ -195,8 +253,9 @@ def run_reference(args, cfg):
             "ms_per_step": float(np.mean([r["seconds"] for r in res]) * 1e3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (paper Sec. 4.1.1 generator, seeded)",
-            "config": dict(workload_config(cfg, None, None), algo=args.algo,
-                           learners="unbinned" if args.unbinned else "binned"),
+            "config": dict(workload_config(cfg, O.n_star(cfg.n, cfg.n_star_rule, cfg.n_star_fixed),
+                                           cfg.n_knots + cfg.degree + 1), algo=args.algo, shard="replications",
+                           learners="unbinned" if args.unbinned else "binned", parallelism=f"replications{args.gpus}"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": res[0]["cores"], "kind": "oracle",
                              "sample": res[0]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -249,7 +308,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="R1")
+    ap.add_argument("--config", default="R3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 fused, 2 general")
     ap.add_argument("--algo", default="cwb", choices=["cwb", "acwb", "hcwb", "bernoulli"],
@@ -263,7 +322,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-findbest", action="store_true",
                     help="skip the auxiliary B = 1 findBest measurement at R3 (SURVEY Sec. 8(d) target)")
-    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0,
+                    help="training seconds of one reference-arm step (the sample of replications is sized to it)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_SHORT"), \
         "timing rules: at least 3 warm-up steps"
@@ -279,6 +339,8 @@ def main():
     ws, rank, local = w.size, w.rank, w.local_rank
     torch.cuda.set_device(local)
     devname = f"cuda:{local}"
+    if ws > 1:  # NCCL's communicator lines (stderr) let a scaling run verify nranks and the transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     D.init_process_group(w, "nccl", torch.device(devname))
     from paper_2110_03513_b200 import cwb
 
@@ -439,49 +501,88 @@ def main():
     h2d = ds.X.nbytes + Y_host.nbytes
     d2h = sum(v.numel() * v.element_size() for v in (outh if args.algo == "cwb" and not strong else host_out).values())
 
-    # ---- kernel-only time of one k_train_fused launch (plan cached: one launch per call),
-    #      CUDA events on the launching stream, for the roofline
+    # ---- kernel-only time of the dominant kernel, CUDA events on the launching stream, same launch
+    #      configuration as the step: the whole k_train_fused launch when cwb_train is one persistent launch
+    #      (plan cached), else the binMatVec phase H1 of the per-iteration path (libcwb brackets its launches
+    #      with events: cwb_set_h1_timing / cwb_get_h1_time)
     kpool = new_pool(X)
     if args.path:
         kpool.set_path(args.path)
     kouts = train(kpool)
     kpool.status()
-    k_ms = []
+    k_ms, h1_ms, h1_n = [], 0.0, 0
     for i in range(max(3, min(args.steps, 10))):
         flush.fill_(float(i))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = kpool.launches()
+        kpool.set_h1_timing(True)
         e0.record(stream)
         kouts = train(kpool, kouts)
         e1.record(stream)
         e1.synchronize()
+        t_, n_ = kpool.h1_time()
+        h1_ms += t_
+        h1_n += n_
         k_ms.append(e0.elapsed_time(e1))
         k_launches = kpool.launches() - l0
+    kpool.set_h1_timing(False)
     kpool.close()
     kernel_ms = float(np.mean(k_ms))
     if rank == 0:
         peaks, src = load_peaks()
-        import dataclasses
-        ops = alg_ops_per_rep_iter(dataclasses.replace(cfg, n=len(blk)), n_star, d, args.unbinned) * B * M * (
-            1 if args.algo in ("cwb", "bernoulli") else 2)  # this rank's rows
-        achieved = ops / (kernel_ms * 1e-3)
-        peak = fp64_peak_ops(peaks)
+        n_loc = len(blk)
+        fits = 1 if args.algo in ("cwb", "bernoulli") else 2
+        sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        n_sms = torch.cuda.get_device_properties(devname).multi_processor_count
+        if k_launches == 1:   # one persistent launch: M iterations of H1-H6 on chip
+            roof = sec8d_roofline(K, n_loc, B * fits, n_star, peaks, kernel_ms * 1e-3, M,
+                                  f"k_train_fused ({args.algo} mode)" if args.algo != "cwb" else "k_train_fused",
+                                  bytes_extra=n_loc * B * fits * 8)
+            roof["units"] = f"{M} iterations per launch (bytes_alg per iteration = K n idx + 2 n B 8)"
+        elif h1_n > 0:        # per-iteration kernels: the binMatVec phase H1 dominates the iteration
+            roof = sec8d_roofline(K, n_loc, B * fits, n_star, peaks, h1_ms / h1_n * 1e-3, 1,
+                                  "H1 binMatVec (k_h1, or the k_h1c row-chunk launches) of one iteration")
+            roof["units"] = f"one H1 phase (mean of {h1_n} timed phases); bytes_alg = K n idx + n B 8"
+            roof["h1_share_of_train"] = (h1_ms / (len(k_ms))) / kernel_ms
+            # the binding on-chip unit: each (learner, row, column) add reads 8 B of the residual block
+            # from L2 (the 32-column tile of R fits L2 at R3; chunked at R4)
+            l2b = 8.0 * K * n_loc * B * fits
+            l2 = float(peaks.get("l2_read_gbs", 0.0))
+            roof["l2_gather"] = {"bytes_per_phase": l2b, "achieved_gbs": l2b / (h1_ms / h1_n * 1e-3) / 1e9,
+                                 "peak_gbs": l2 or None, "frac": (l2b / (h1_ms / h1_n * 1e-3) / 1e9 / l2) if l2 else None,
+                                 "note": "measured L2-resident read bandwidth, profiles/peaks_fp64.json"}
+        else:
+            roof = sec8d_roofline(K, n_loc, B * fits, n_star, peaks, kernel_ms * 1e-3, M,
+                                  f"{args.algo} per-iteration kernels (whole cwb_train call)",
+                                  bytes_extra=n_loc * B * fits * 8)
+        # iteration level: M x max(bytes/HBM, adds/DADD) against the measured cwb_train time
+        it = sec8d_roofline(K, n_loc, B * fits, n_star, peaks, kernel_ms * 1e-3, M, "cwb_train (all kernels)",
+                            bytes_extra=n_loc * B * fits * 8)
+        roof["train_frac"] = it["frac"]
+        roof["train_ms"] = kernel_ms
+        roof["launches_per_call"] = int(k_launches)
+        roof["peak_src"] = {"hbm": f"MEASURED_PEAKS.json hbm_gbs ({src})", "dadd": peaks.get("fp64_src")}
         traffic = None
         smem_wf = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
                 tj = json.load(open(tp))
-                if args.algo == "cwb" and not strong and not args.unbinned and args.path != 2:
-                    traffic = tj.get(cfg.name)
-                    smem_wf = tj.get("smem_wavefronts", {}).get(cfg.name)
+                if args.algo == "cwb" and not strong and not args.unbinned:  # ncu --set full of the same kernel
+                    key = cfg.name if k_launches == 1 else cfg.name + "_h1"
+                    traffic = tj.get(key)
+                    smem_wf = tj.get("smem_wavefronts", {}).get(key)
             except Exception:
                 traffic = None
-        rb = 2 if B > 148 else 1  # replications per CTA
-        sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-        n_sms = torch.cuda.get_device_properties(devname).multi_processor_count
-        ctas_per_sm = -(-(-(-B // rb)) // 148)
-        h1_floor_ms = K * n * ctas_per_sm * M / (GATHER_LANE_LOADS_PER_CLK[rb] * sm_hz) * 1e3
+        roof["traffic"] = traffic
+        if k_launches == 1:
+            rb = 2 if B > n_sms else 1  # replications per CTA
+            ctas_per_sm = -(-(-(-B // rb)) // n_sms)
+            roof["smem_pipe_frac"] = smem_wf / (kernel_ms * 1e-3 * sm_hz * n_sms) if smem_wf else None
+            roof["smem_gather_ceiling"] = {
+                "h1_floor_ms": K * n * ctas_per_sm * M / (GATHER_LANE_LOADS_PER_CLK[rb] * sm_hz) * 1e3,
+                "note": ("time H1 alone would take at the measured conflict-free shared-memory gather rate "
+                         "(profiles/ubench_smem_gather.txt); the binding on-chip ceiling of this kernel")}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -492,27 +593,7 @@ def main():
                            parallelism=(f"{args.shard}{ws}")),
             "iters_per_s": M / (ms_per_step * 1e-3),
             "phase_ms": {"init": float(np.mean(init_ms)), "train": float(np.mean(train_ms))},
-            "roofline": {"bound": "alu",
-                         "kernel": ("general path, unbinned learners" if args.unbinned else
-                                    "general path, row-sharded" if rows else
-                                    "general path, learner-sharded" if strong else
-                                    "k_train_fused" if args.path != 2 else "general path") if args.algo == "cwb"
-                         else (f"k_train_fused ({args.algo} mode)" if k_launches == 1
-                               else f"{args.algo} per-iteration kernels (general path)"),
-                         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         # the binding on-chip unit: shared-memory load wavefronts of one launch (ncu) over
-                         # the pipe's 1 wavefront / clock / SM during the measured launch time
-                         "smem_pipe_frac": (smem_wf / (kernel_ms * 1e-3 * sm_hz * n_sms) if smem_wf else None),
-                         "kernel_ms": kernel_ms, "launches_per_call": int(k_launches),
-                         "note": ("achieved = algorithmic fp64 add/FMA operations of one launch (FMA counted "
-                                  "once; DESIGN.md Sec. 7) / its CUDA-event duration; peak = 148 SM x 64 fp64 "
-                                  f"lanes x {peaks.get('sm_max_mhz', 1965)} MHz ({src} clock)"),
-                         "smem_gather_ceiling": {
-                             "h1_floor_ms": h1_floor_ms,
-                             "note": ("time H1 alone would take at the measured conflict-free shared-memory "
-                                      "gather rate (profiles/ubench_smem_gather.txt); the binding on-chip "
-                                      "ceiling of this kernel")}},
+            "roofline": roof,
             "e2e": {"value": evals / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                     "api": ("cwb_fit_host (pinned host buffers, copies + init + train + sync)"
@@ -522,10 +603,11 @@ def main():
             "gpu_launches": int(sum(launches)),
         }
         if args.algo == "cwb" and not strong and not args.unbinned and ws == 1 and not args.no_findbest:
-            try:  # after the timed region: does not touch the step measurement
-                line["findbest_b1"] = findbest_b1(devname, peaks)
-            except Exception as e:
-                line["findbest_b1"] = {"error": str(e)}
+            for fb_cfg in ("R3", "R4"):
+                try:  # after the timed region: does not touch the step measurement
+                    line[f"findbest_b1_{fb_cfg}"] = findbest_b1(devname, peaks, fb_cfg)
+                except Exception as e:
+                    line[f"findbest_b1_{fb_cfg}"] = {"error": str(e)}
         if not args.no_cpu_baseline and ws == 1:
             try:
                 line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, algo=args.algo,

@@ -89,7 +89,10 @@ def make_X(cfg: SynthConfig) -> tuple[np.ndarray, np.random.SeedSequence]:
     n, K = cfg.n, cfg.K
     X = np.empty((K, n), dtype=np.float64)
     if cfg.grid_r0:
-        grid = np.linspace(-1.0, 1.0, n)
+        # the design points of [-1, 1] by the P:L859 formula itself, lo + (l / (n - 1)) (hi - lo) with the
+        # last point set to hi (a linspace grid differs from it by 1 ulp in places)
+        grid = -1.0 + (np.arange(n, dtype=np.float64) / float(n - 1)) * 2.0
+        grid[-1] = 1.0
         X[0] = grid
         X[1] = grid[g.permutation(n)]
         for j in range(2, K):

@@ -161,7 +161,8 @@ int cwb_get_pool(cwb_ctx* ctx, double* z, uint16_t* idx, double* Zb, double* G, 
  * both): 0 = auto, 1 = fused persistent kernel (one CTA per one or two
  * replications, residuals resident in shared memory; CWB_EUNSUPPORTED from the
  * training call when its layout does not fit), 2 = general per-iteration kernels.
- * Errors: CWB_EINVAL (path not 0..2), CWB_EUNSUPPORTED (1 on a row-sharded context). */
+ * Errors: CWB_EINVAL (path not 0..2), CWB_EUNSUPPORTED (1 on a row-sharded context; 0 or 1
+ * on a learner-sharded context, which runs the per-iteration kernels only). */
 int cwb_set_path(cwb_ctx* ctx, int32_t path);
 
 /* H1 implementation of cwb_find_best for B <= 4 columns (tests and benchmarks
@@ -256,7 +257,9 @@ int cwb_train_folds(cwb_ctx* ctx, const double* Y, int32_t B, const uint8_t* fol
  * kcor_trace (-1 after the switch), sse_trace (SSE of the primary fit on its rows),
  * risk_trace (risk of f on all rows), val_risk_trace; switch_iter[B] = first CWB
  * iteration (M if none).  Trace pointers may be NULL.  Paper defaults gamma = 0.037,
- * pat0 = 5.  Errors: CWB_EINVAL (pat0 < 1, ...), CWB_ECALIB. */
+ * pat0 = 5.  Errors: CWB_EINVAL (pat0 < 1, val_mask without a training
+ * row or without a validation row -- reported by cwb_status, the check runs on the device),
+ * CWB_ECALIB. */
 int cwb_train_hcwb(cwb_ctx* ctx, const double* Y, int32_t B, const uint8_t* val_mask, double nu, double gamma,
                    int32_t pat0, int32_t M, double* offset_out, double* theta_f_out, int32_t* k_trace,
                    int32_t* kcor_trace, double* sse_trace, double* risk_trace, double* val_risk_trace,
@@ -282,6 +285,17 @@ int cwb_predict(cwb_ctx* ctx, const double* Xnew, int64_t m, const double* offse
  * selection criterion, C: argmax + parameters, D: residual update), summed over
  * the M iterations.  NULL switches it off (default). */
 int cwb_set_phase_timing(cwb_ctx* ctx, int64_t* cycles4);
+
+/* Profiling hook of the per-iteration (general) path: with on != 0 every later
+ * binMatVec phase H1 (k_h1, or the k_h1c row-chunk launches) is
+ * bracketed by a pair of CUDA events recorded on the call's stream (the context
+ * owns them).  cwb_get_h1_time synchronises on the last pair, returns the summed
+ * elapsed time of every bracketed phase since the last call (*ms_total) and their
+ * number (*n_phases, may be NULL), and starts a new tally.  bench.py uses it for the
+ * roofline of the dominant kernel of the R3/R4 steps.  Errors: CWB_EINVAL (NULL),
+ * CWB_ECUDA. */
+int cwb_set_h1_timing(cwb_ctx* ctx, int32_t on);
+int cwb_get_h1_time(cwb_ctx* ctx, double* ms_total, int32_t* n_phases);
 
 /* ------------------------------------------------------------- row sharding
  * The rows of the data are partitioned over `world` ranks (one process and GPU

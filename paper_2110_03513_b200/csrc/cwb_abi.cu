@@ -156,7 +156,7 @@ int cwb_bin(const double* x, int64_t n, int32_t n_star, double* z_out, double* b
 
 int cwb_bin_mat_mat(const double* Zb, int32_t n_star, int32_t d, const void* idx, int32_t idx_bytes,
                     const double* w, int64_t n, double* out, cudaStream_t s) {
-    if (!Zb || !idx || !out || n < 1 || n_star < 1 || d < 1 || (idx_bytes != 1 && idx_bytes != 2))
+    if (!Zb || !idx || !out || n < 1 || n > INT32_MAX || n_star < 1 || d < 1 || (idx_bytes != 1 && idx_bytes != 2))
         return cwb_set_error(nullptr, CWB_EINVAL, "cwb_bin_mat_mat: invalid argument");
     int rc = cwb_bin_mat_mat_impl(Zb, n_star, d, idx, idx_bytes, w, n, out, s);
     if (rc) return cwb_set_error(nullptr, rc, std::string("cwb_bin_mat_mat: ") + status_name(rc));
@@ -165,7 +165,7 @@ int cwb_bin_mat_mat(const double* Zb, int32_t n_star, int32_t d, const void* idx
 
 int cwb_bin_mat_vec(const double* Zb, int32_t n_star, int32_t d, const void* idx, int32_t idx_bytes,
                     const double* w, const double* R, int64_t n, int32_t B, double* out, cudaStream_t s) {
-    if (!Zb || !idx || !R || !out || n < 1 || n_star < 1 || d < 1 || B < 1 ||
+    if (!Zb || !idx || !R || !out || n < 1 || n > INT32_MAX || n_star < 1 || d < 1 || B < 1 ||
         (idx_bytes != 1 && idx_bytes != 2))
         return cwb_set_error(nullptr, CWB_EINVAL, "cwb_bin_mat_vec: invalid argument");
     int rc = cwb_bin_mat_vec_impl(Zb, n_star, d, idx, idx_bytes, w, R, n, B, out, s);
@@ -191,6 +191,7 @@ void cwb_free(cwb_ctx* c) {
         cudaEventDestroy(c->ev_plan);
     }
     if (c->ev_csr) cudaEventDestroy(c->ev_csr);
+    for (cudaEvent_t e : c->h1_ev) cudaEventDestroy(e);
     cwb_release_header_slot(c->h_hdr);
     // c->s2 is the device's shared side stream: not destroyed
     delete c;
@@ -347,6 +348,9 @@ int cwb_set_narrow(cwb_ctx* c, int32_t mode) {
 int cwb_set_path(cwb_ctx* c, int32_t path) {
     if (!c || path < 0 || path > 2) return cwb_set_error(c, CWB_EINVAL, "cwb_set_path: invalid argument");
     if (c->rows && path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_set_path: row-sharded context");
+    // learner sharding runs on the per-iteration kernels only (the fused and stream paths fit all K learners)
+    if (c->lshard && path != 2)
+        return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_set_path: learner-sharded context (path 2 only)");
     c->path = path;
     return CWB_OK;
 }
@@ -486,8 +490,8 @@ int cwb_fit_host(const double* X, int64_t n, int32_t K, const cwb_config* cfg, c
         if (sse_trace) cudaMemcpyAsync(sse_trace, dS, 8 * mb, cudaMemcpyDeviceToHost, s);
         if (risk_trace) cudaMemcpyAsync(risk_trace, dR, 8 * mb, cudaMemcpyDeviceToHost, s);
         rc = cwb_status(c);
-        if (rc) g_err = c->err;
     }
+    if (rc && c) g_err = c->err;  // the context's message outlives cwb_free
     if (c) cwb_free(c);
     cwb_release(dX, s); cwb_release(dY, s); cwb_release(dOff, s); cwb_release(dAgg, s);
     cwb_release(dK, s); cwb_release(dS, s); cwb_release(dR, s);
@@ -507,6 +511,33 @@ int cwb_predict(cwb_ctx* c, const double* Xnew, int64_t m, const double* offset,
 }
 
 int64_t cwb_launch_count(const cwb_ctx* c) { return c ? c->launches : 0; }
+
+int cwb_set_h1_timing(cwb_ctx* c, int32_t on) {
+    if (!c) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_set_h1_timing: NULL context");
+    c->h1_timing = on != 0;
+    c->h1_ev_used = 0;
+    return CWB_OK;
+}
+
+int cwb_get_h1_time(cwb_ctx* c, double* ms_total, int32_t* n_phases) {
+    if (!c || !ms_total) return cwb_set_error(c, CWB_EINVAL, "cwb_get_h1_time: invalid argument");
+    double t = 0.0;
+    const int np = c->h1_ev_used / 2;
+    if (np) {
+        if (cudaEventSynchronize(c->h1_ev[2 * np - 1]) != cudaSuccess)
+            return cwb_set_error(c, CWB_ECUDA, "cwb_get_h1_time: event synchronisation failed");
+        for (int i = 0; i < np; i++) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, c->h1_ev[2 * i], c->h1_ev[2 * i + 1]) != cudaSuccess)
+                return cwb_set_error(c, CWB_ECUDA, "cwb_get_h1_time: elapsed time");
+            t += ms;
+        }
+    }
+    *ms_total = t;
+    if (n_phases) *n_phases = np;
+    c->h1_ev_used = 0;
+    return CWB_OK;
+}
 
 int cwb_set_phase_timing(cwb_ctx* c, int64_t* cycles4) {
     if (!c) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_set_phase_timing: NULL context");

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/cwb.h"
 
@@ -115,6 +116,10 @@ struct cwb_ctx {
     bool fused_pool = false;
     size_t fused_smem = 0;
     long long* timing = nullptr;  // optional device buffer: fused-kernel phase cycles (cwb_set_timing)
+    // optional CUDA-event timing of the general path's H1 launches (cwb_set_h1_timing / cwb_get_h1_time)
+    bool h1_timing = false;
+    std::vector<cudaEvent_t> h1_ev;
+    int32_t h1_ev_used = 0;
     // plan pre-built during cwb_init on a side stream (cwb_config.batch_hint)
     int32_t batch_hint = 0;
     cudaStream_t s2 = nullptr;

@@ -499,7 +499,8 @@ __global__ void k_fill_int(int32_t* __restrict__ p, int cnt, int v) {
     if (b < cnt) p[b] = v;
 }
 
-__global__ void k_mask_count(const uint8_t* __restrict__ mask, int64_t n, double* __restrict__ cnt) {
+__global__ void k_mask_count(const uint8_t* __restrict__ mask, int64_t n, double* __restrict__ cnt,
+                             int* __restrict__ status) {
     __shared__ double red[32];
     double v = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v += mask[i] ? 1.0 : 0.0;
@@ -511,6 +512,9 @@ __global__ void k_mask_count(const uint8_t* __restrict__ mask, int64_t n, double
         for (int q = 0; q < (int)(blockDim.x >> 5); q++) t += red[q];
         cnt[0] = (double)n - t;  // training rows
         cnt[1] = t;              // validation rows
+        // HCWB needs both sets: the training fits divide by the training rows, the patience rule by the
+        // validation rows (Alg. 3)
+        if (t == 0.0 || t == (double)n) cwb_dev_fail(status, CWB_EINVAL);
     }
 }
 
@@ -1217,6 +1221,21 @@ static int column_stats(cwb_ctx* c, const double* Y, int B, bool center, double*
     return CWB_OK;
 }
 
+// next (start, stop) event pair of the H1 timing hook, NULL when it is off
+static cudaEvent_t* cwb_h1_events(cwb_ctx* c) {
+    if (!c->h1_timing) return nullptr;
+    if ((size_t)c->h1_ev_used + 2 > c->h1_ev.size()) {
+        for (int i = 0; i < 64; i++) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+            c->h1_ev.push_back(e);
+        }
+    }
+    cudaEvent_t* p = c->h1_ev.data() + c->h1_ev_used;
+    c->h1_ev_used += 2;
+    return p;
+}
+
 // one findBestBaselearner on the residual columns of ws.Rt
 static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg, int32_t* k_trace,
                            double* sse_trace, int32_t* k_out, double* theta_out, double* sse_out,
@@ -1260,7 +1279,10 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
         k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin, c->Ainv,
                                                     c->G, w.theta, w.delta, nullptr, nullptr, nullptr, 0, w.pack, 2);
     } else {
+        cudaEvent_t* ev = cwb_h1_events(c);  // profiling hook (bench.py's roofline): H1 bracketed by events
+        if (ev) cudaEventRecord(ev[0], s);
         h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
+        if (ev) cudaEventRecord(ev[1], s);
         k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
                                                     c->Ainv, c->G, w.theta, w.delta);
     }
@@ -1662,6 +1684,16 @@ __global__ void k_fill(double* p, int64_t cnt, double v) {
 }
 }  // namespace
 
+// caller-supplied index vectors of the standalone binMatVec / binMatMat calls: every idx(i) < n* (ADVICE r1:
+// the bin inversion would otherwise count and scatter outside its arrays)
+template <typename IdxT>
+__global__ void k_idx_check(const IdxT* __restrict__ idx, int64_t n, int ns, int* bad) {
+    int b = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b |= (int)idx[i] >= ns;
+    if (__syncthreads_or(b) && threadIdx.x == 0) *bad = 1;
+}
+
 // U[l][b] = sum_{i: idx(i) = l} w_i R[b][i]  (binMatVec's u), rows in increasing order
 static int binned_sums(const void* idx, int32_t idx_bytes, const double* w, const double* R, int64_t n,
                        int32_t B, int32_t ns, double* U, int Bp, cudaStream_t s) {
@@ -1675,6 +1707,17 @@ static int binned_sums(const void* idx, int32_t idx_bytes, const double* w, cons
     ok &= cwb_alloc(&perm, (size_t)perm_bytes * n, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&Rt, sizeof(double) * (size_t)n * Bp, s) == cudaSuccess;
     int rc = ok ? CWB_OK : CWB_ENOMEM;
+    if (rc == CWB_OK) {  // validate the index vector (one flag, read back: these are stand-alone calls)
+        int* bad = reinterpret_cast<int*>(cnt);
+        int hbad = 0;
+        cudaMemsetAsync(bad, 0, sizeof(int), s);
+        const unsigned g = (unsigned)std::min<int64_t>(1184, (n + 255) / 256);
+        if (idx_bytes == 1) k_idx_check<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)idx, n, ns, bad);
+        else k_idx_check<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)idx, n, ns, bad);
+        if (cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) rc = CWB_ECUDA;
+        else if (hbad) rc = CWB_EINVAL;
+    }
     if (rc == CWB_OK) rc = cwb_launch_csr(nullptr, idx, idx_bytes, n, 1, ns, cnt, off, perm, perm_bytes, s);
     if (rc == CWB_OK) {
         dim3 gt((unsigned)((n + 31) / 32), Bp / 32);
@@ -1822,6 +1865,7 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
     uint32_t* cnt_tr = (uint32_t*)(Cb_tr + (size_t)K * d * 4);
     int32_t* phase = (int32_t*)(cnt_tr + (size_t)K * ns);
     int32_t* pat = phase + Bq;
+    k_mask_count<<<1, 1024, 0, s>>>(val_mask, c->n, cnt, c->d_status);
     rc = cwb_launch_masked_pool(c, val_mask, cnt_tr, G_tr, Ainv_tr, s, Cb_tr);
     if (rc) return rc;
     if (c->path != 2) {  // the whole run in one persistent kernel when it fits (cwb_fused.cu, HC mode)
@@ -1832,7 +1876,6 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
         if (rc || launched) return rc;
         if (c->path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: fused path does not fit");
     }
-    k_mask_count<<<1, 1024, 0, s>>>(val_mask, c->n, cnt);
     cudaMemsetAsync(phase, 0, sizeof(int32_t) * 2 * Bq, s);
     // f0 = mean of the training targets (Alg. 2 line 2 on D_train); rr = sum over training rows
     rc = column_stats(c, Y, B, true, off_ws, w.rr, offset_out, s, val_mask, 0, cnt);

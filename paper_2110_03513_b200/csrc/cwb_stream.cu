@@ -734,6 +734,19 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
     if (c->rows || B < 1 || B > 4 || (size_t)c->n_star * B * sizeof(double) > 96 * 1024 ||
         c->n_star > kUBudget) return CWB_EUNSUPPORTED;
     if ((int64_t)c->K * ((c->n + kC - 1) / kC) * (CWB_MAX_SMS + 1) >= INT32_MAX) return CWB_EUNSUPPORTED;  // item math in int32
+    {   // k_fit_narrow stages the bin sums, the window-major basis and two d x d tables in shared memory:
+        // larger pools take the other findBest paths
+        const size_t fsm0 = sizeof(double) * ((((size_t)c->n_star * B + 1) & ~(size_t)1) + (size_t)c->W * c->d +
+                                              2 * (size_t)c->d * c->d);
+        cudaFuncAttributes fa;
+        int optin = 0, dev = 0;
+        if (cudaFuncGetAttributes(&fa, k_fit_narrow) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return CWB_EUNSUPPORTED;
+        }
+        if (fsm0 + fa.sharedSizeBytes > (size_t)optin) return CWB_EUNSUPPORTED;
+    }
     int rc = stream_plan(c, s);
     if (rc) return rc;
     cwb_stream_plan& p = c->sp;
@@ -762,7 +775,7 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
     k_h1_stream<<<dim3(N, B), kStreamT, smem, s>>>(R, c->n, p.nch, p.Ks, ns, p.nitems, nslot, (const uint2*)p.ent,
                                                     p.gtab, p.dest, p.isize, p.ibase, p.wst, p.part, rrp, c->d_status);
     const size_t fsm = sizeof(double) * ((((size_t)ns * B + 1) & ~(size_t)1) + (size_t)c->W * d + 2 * (size_t)d * d);
-    cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
     {   // launched as a programmatic dependent of k_h1_stream (prologue overlaps its tail)
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(K);

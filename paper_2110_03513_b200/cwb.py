@@ -22,7 +22,7 @@ CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB",
 SYMBOLS = ["cwb_default_config", "cwb_version", "cwb_bin", "cwb_bin_mat_mat", "cwb_bin_mat_vec",
            "cwb_init", "cwb_status", "cwb_last_error", "cwb_get_dims", "cwb_get_lambda", "cwb_get_n_star_k", "cwb_get_pool",
            "cwb_set_path", "cwb_set_narrow", "cwb_find_best", "cwb_train", "cwb_train_bernoulli", "cwb_train_folds", "cwb_train_acwb", "cwb_train_hcwb", "cwb_fit_host", "cwb_predict",
-           "cwb_launch_count", "cwb_set_phase_timing", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
+           "cwb_launch_count", "cwb_set_phase_timing", "cwb_set_h1_timing", "cwb_get_h1_time", "cwb_free", "cwb_comm_unique_id", "cwb_comm_init",
            "cwb_comm_init_fn", "cwb_comm_free", "cwb_attach_comm", "cwb_attach_comm_learners", "cwb_get_rows"]
 
 
@@ -97,6 +97,8 @@ def load() -> C.CDLL:
                                _vp, _vp, _vp, _vp, _vp, _vp]
     L.cwb_predict.argtypes = [_vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp]
     L.cwb_set_phase_timing.argtypes = [_vp, _vp]
+    L.cwb_set_h1_timing.argtypes = [_vp, _i32]
+    L.cwb_get_h1_time.argtypes = [_vp, C.POINTER(_f64), C.POINTER(_i32)]
     L.cwb_launch_count.argtypes = [_vp]
     L.cwb_launch_count.restype = C.c_int64
     L.cwb_free.argtypes = [_vp]
@@ -399,6 +401,17 @@ def cwb_set_phase_timing(ctx, cycles4=None) -> None:
     _chk(load().cwb_set_phase_timing(ctx, _ptr(cycles4)), ctx)
 
 
+def cwb_set_h1_timing(ctx, on: bool) -> None:
+    _chk(load().cwb_set_h1_timing(ctx, int(bool(on))), ctx)
+
+
+def cwb_get_h1_time(ctx):
+    """(summed milliseconds, number of bracketed H1 phases) since the last call; synchronises."""
+    ms, np_ = _f64(0.0), _i32(0)
+    _chk(load().cwb_get_h1_time(ctx, C.byref(ms), C.byref(np_)), ctx)
+    return float(ms.value), int(np_.value)
+
+
 def cwb_free(ctx) -> None:
     if ctx:
         load().cwb_free(ctx)
@@ -514,6 +527,12 @@ class Pool:
 
     def launches(self):
         return cwb_launch_count(self.ctx)
+
+    def set_h1_timing(self, on=True):
+        cwb_set_h1_timing(self.ctx, on)
+
+    def h1_time(self):
+        return cwb_get_h1_time(self.ctx)
 
     def attach_learners(self, comm: Comm):
         _chk(load().cwb_attach_comm_learners(self.ctx, comm.h), self.ctx)

@@ -12,7 +12,9 @@
 import numpy as np
 
 RTOL = 1e-9
-TIE_RTOL = 1e-10
+# north_star / SURVEY 8(c) G11: selected-learner sequences are identical except at SSE ties within
+# 1e-12 relative (the oracle's best and second-best)
+TIE_RTOL = 1e-12
 
 
 def cfg_of(c):
@@ -81,3 +83,26 @@ def assert_train_parity(g, o, n, tag="", min_full=0.9):
         ok, e = close(g["theta_agg"][full], o.theta_agg[full], RTOL, scale=np.abs(o.theta_agg[full]).max())
         assert ok, f"{tag}: theta_agg rel err {e}"
     return first, ties
+
+
+def follow_parity(g, po, Y, nu, M, tag="", threads=8, report=True):
+    """Tie-following comparison: the oracle runs Alg. 1 on the target vectors Y
+    (rows = the GPU's replications, in the order of g's columns) and takes the GPU's learner only at a
+    verified near tie (its SSE within TIE_RTOL relative of the oracle's minimum); every selected-learner
+    index must then match bit for bit and the SSE / risk traces, theta_agg and the offsets agree within
+    the tolerances.  g: dict of numpy arrays of exactly these replications.  Returns followed[B] (the
+    number of iterations at which the oracle took the GPU's choice at a tie), printed when report."""
+    o, followed = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=nu, M=M, threads=threads)
+    bad = np.argwhere(o.k_trace != g["k_trace"])
+    assert len(bad) == 0, f"{tag}: non-tie selections differ at (m, b) = {bad[:5].tolist()}"
+    for key, ref in (("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
+        ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())
+        assert ok, f"{tag}: {key} rel err {e}"
+    ok, e = close(g["theta_agg"], o.theta_agg, RTOL, scale=np.abs(o.theta_agg).max())
+    assert ok, f"{tag}: theta_agg rel err {e}"
+    ok, e = close(g["offset"], o.offset, 1e-12)
+    assert ok, f"{tag}: offset rel err {e}"
+    if report:
+        print(f"[parity] {tag}: {g['k_trace'].shape[1]} replications x {M} iterations identical; "
+              f"ties followed: {int(followed.sum())} (tie rule {TIE_RTOL:g} relative)")
+    return followed

@@ -22,11 +22,12 @@ def run_bench(*args, timeout=600):
 
 
 def test_reference_arm_line():
-    d = run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-seconds", "0.5")
+    d = run_bench("--impl", "reference", "--config", "R1", "--steps", "1", "--warmup", "0", "--ref-seconds", "0.5")
     for k in BASE + ["impl", "cpu_baseline"]:
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["config"]["workload"] == "R1"
+    assert d["config"]["n_star"] == 37 and d["config"]["d"] == 24 and d["config"]["parallelism"] == "replications1"
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
@@ -41,11 +42,13 @@ def test_gpu_arm_line():
     for k in BASE + ["roofline", "clocks", "gpu_launches"]:
         assert k in d, k
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
-    assert d["scaling"] == "weak" and d["dtype"] == "f64" and d["config"]["workload"] == "R1"
+    assert d["scaling"] == "weak" and d["dtype"] == "f64" and d["config"]["workload"] == "R3"  # the default
     r = d["roofline"]
-    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "terms"):
         assert k in r, k
     assert 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+    t = r["terms"]  # frac = max(bytes/HBM, adds/DADD) / kernel time
+    assert abs(r["frac"] - max(t["t_hbm_ms"], t["t_dadd_ms"]) / t["t_kernel_ms"]) < 1e-9
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])

@@ -80,7 +80,8 @@ def check(name, reps, gamma=0.0034, nu=None, M=None, path=0):
 
 
 @pytest.mark.parametrize("path", [1, 2])  # 1: fused kernel (ACC mode), 2: general per-iteration kernels
-@pytest.mark.parametrize("name,reps", [("R0", range(8)), ("R1", range(32)), ("R2", [0, 1, 2, 3, 700, 1023])])
+@pytest.mark.parametrize("name,reps", [("R0", range(8)), ("R1", range(32)), ("R1", range(256)),
+                                       ("R2", [0, 1, 2, 3, 700, 1023])])
 def test_acwb_parity(name, reps, path):
     if name == "R2" and path == 1:
         pytest.skip("R2 residuals do not fit the ACWB fused kernel (two columns + momentum model)")

@@ -63,7 +63,8 @@ def test_learner_config_matches_oracle(degree, n_knots, ns, df):
         pg.set_path(path)
         g = host(pg.train(dev(Y), nu=0.1, M=40))
         pg.status()
-        o, _ = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=40, threads=6)
+        o, fol = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=40, threads=6)
+        print(f"[parity] ties followed: {int(fol.sum())} over {fol.size} replications (tie rule {TIE_RTOL:g})")
         assert (o.k_trace == g["k_trace"]).all(), f"path {path}"
         for key, ref in (("theta_agg", o.theta_agg), ("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
             ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())

@@ -76,14 +76,15 @@ def check(name, reps, nu=None, gamma=0.037, pat0=5, M=None, frac=0.3, path=0):
 
 
 @pytest.mark.parametrize("path", [1, 2])  # 1: fused persistent kernel (HC mode), 2: per-iteration kernels
-def test_hcwb_parity_r1_switches(path):
+@pytest.mark.parametrize("B", [24, 256])  # 256: the bench shape (fused: two 256-thread CTAs per SM)
+def test_hcwb_parity_r1_switches(path, B):
     # strong momentum so that replications switch at different iterations inside one launch
-    g, ro = check("R1", list(range(24)), nu=0.1, gamma=0.5, pat0=3, M=200, path=path)
-    assert (ro.switch_iter < 200).sum() >= 12 and len(set(ro.switch_iter.tolist())) > 3
+    g, ro = check("R1", list(range(B)), nu=0.1, gamma=0.5, pat0=3, M=200, path=path)
+    assert (ro.switch_iter < 200).sum() >= B // 2 and len(set(ro.switch_iter.tolist())) > 3
 
 
 @pytest.mark.parametrize("name,reps,path", [("R0", range(8), 1), ("R0", range(8), 2), ("R1", range(16), 1),
-                                            ("R1", range(16), 2), ("R2", [0, 5, 1000], 0)])
+                                            ("R1", range(16), 2), ("R1", range(256), 1), ("R2", [0, 5, 1000], 0)])
 def test_hcwb_parity_paper_defaults(name, reps, path):
     check(name, list(reps), path=path)
 

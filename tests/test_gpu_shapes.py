@@ -52,7 +52,8 @@ def test_fused_cwb_shapes_vs_oracle(seed, n, K, ns, B):
     g = host(pg.train(dev(Y), nu=0.1, M=60))
     pg.status()
     po = O.Pool(X, oc, O.MODE_BINNED)
-    o, _ = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=60, threads=8)
+    o, fol = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=60, threads=8)
+    print(f"[parity] ties followed: {int(fol.sum())} over {fol.size} replications (tie rule {TIE_RTOL:g})")
     assert (o.k_trace == g["k_trace"]).all()
     for key, ref in (("theta_agg", o.theta_agg), ("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
         ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())
@@ -105,7 +106,8 @@ def test_many_learners_vs_oracle(seed, n, K, ns, B):
     g = host(pg.train(dev(Y), nu=0.1, M=30))
     pg.status()
     po = O.Pool(X, oc, O.MODE_BINNED)
-    o, _ = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=30, threads=8)
+    o, fol = po.train_follow(Y, g["k_trace"], tie_rtol=TIE_RTOL, nu=0.1, M=30, threads=8)
+    print(f"[parity] ties followed: {int(fol.sum())} over {fol.size} replications (tie rule {TIE_RTOL:g})")
     assert (o.k_trace == g["k_trace"]).all()
     for key, ref in (("theta_agg", o.theta_agg), ("sse_trace", o.sse_trace), ("risk_trace", o.risk_trace)):
         ok, e = close(g[key], ref, RTOL, scale=np.abs(ref).max())

@@ -15,7 +15,7 @@ pytestmark = [pytest.mark.gpu,
 
 import cwb_synth as S  # noqa: E402
 from oracle import oracle as O  # noqa: E402
-from parity_util import RTOL, cfg_of, close, gpu_cfg_of  # noqa: E402
+from parity_util import RTOL, TIE_RTOL, cfg_of, close, gpu_cfg_of  # noqa: E402
 
 from paper_2110_03513_b200 import cwb  # noqa: E402
 
@@ -37,7 +37,7 @@ def _check(po, pg, R):
     for b in range(R.shape[0]):
         ko, tho, sseo, sall, gap = po.find_best(R[b])
         if k[b] != ko:
-            assert gap / sseo <= 1e-10, (b, k[b], ko)
+            assert gap / sseo <= TIE_RTOL, (b, k[b], ko)
             continue
         ok, e = close(th[b], tho, RTOL, scale=np.abs(tho).max())
         assert ok, e

@@ -10,7 +10,7 @@ pytestmark = [pytest.mark.gpu,
 
 import cwb_synth as S  # noqa: E402
 from oracle import oracle as O  # noqa: E402
-from parity_util import RTOL, assert_train_parity, cfg_of, close  # noqa: E402
+from parity_util import RTOL, TIE_RTOL, assert_train_parity, cfg_of, close  # noqa: E402
 
 from paper_2110_03513_b200 import cwb  # noqa: E402
 
@@ -58,7 +58,7 @@ def test_unbinned_find_best_matches_oracle(name, B):
     for b in range(B):
         ko, tho, sseo, sall, gap = po.find_best(R[b])
         if k[b] != ko:
-            assert gap / sseo <= 1e-10
+            assert gap / sseo <= TIE_RTOL
             continue
         ok, e = close(th[b], tho, RTOL, scale=np.abs(tho).max())
         assert ok, e

@@ -519,11 +519,34 @@ def test_acwb_first_iteration_is_cwb_first_iteration():
     assert np.allclose(a.theta_h[0, k], 0.5 * c.theta_agg[0, k], rtol=1e-13, atol=0)
 
 
-def test_acwb_eta_sequence_spec_example():
-    # gamma = 0.0034, nu = 0.05, m = 3: theta_3 = 0.5, eta_3 = 3.4e-4.  With K = 1 every
-    # correction learner is learner 0, so theta_h^[3] - theta_h^[2] = eta_3 theta_cor^[3]; rather than
-    # reading eta directly, check theta_h against the K = 1 matrix recurrence below (exact same etas).
-    assert np.isclose(0.0034 * 0.05 / (2.0 / 4.0), 3.4e-4, rtol=1e-15)
+def test_acwb_eta_sequence_read_off_the_oracle():
+    # eta_m = gamma nu / vartheta_m with vartheta_m = 2 / (m + 1) (Alg. 2 lines 3 and 15); S:L393's
+    # example: gamma = 0.0034, nu = 0.05, m = 3 -> vartheta_3 = 0.5, eta_3 = 3.4e-4.  Read eta off the oracle:
+    # one learner on a design-point grid (binned = exact, n* = n) and a LINEAR target: linear functions are in
+    # the penalty's null space (D . linear = 0), so the smoother reproduces every residual exactly, the
+    # error correction c - b_cor vanishes and theta_cor^[m] = theta^[m], the primary fit of iteration m.  Then
+    #   theta_h^[m] - theta_h^[m-1] = eta_m theta^[m],   theta^[m] = (theta_f^[m] - theta_g^[m]) / nu,
+    #   theta_g^[m] = (1 - vartheta_m) theta_f^[m-1] + vartheta_m theta_h^[m-1]   (lines 3, 8)
+    # from runs of M = m - 1 and M = m iterations.
+    n = 41
+    x = -1.0 + (np.arange(n) / (n - 1.0)) * 2.0
+    x[-1] = 1.0
+    y = 3.0 + 2.0 * x
+    pool = O.Pool(x[None], O.Config(n_star_rule=2, n_star_fixed=n, n_knots=4), O.MODE_BINNED)
+    gamma, nu = 0.0034, 0.05
+    runs = [pool.train_acwb(y[None], nu=nu, gamma=gamma, M=M) for M in range(0, 6)]
+    for m in range(1, 6):
+        a, b = runs[m - 1], runs[m]
+        vt = 2.0 / (m + 1)
+        th_g = (1.0 - vt) * a.theta_f[0, 0] + vt * a.theta_h[0, 0]
+        th = (b.theta_f[0, 0] - th_g) / nu
+        dh = b.theta_h[0, 0] - a.theta_h[0, 0]
+        j = int(np.argmax(np.abs(th)))
+        eta = dh[j] / th[j]
+        assert np.allclose(dh, eta * th, rtol=1e-9, atol=1e-12 * np.abs(dh).max()), m
+        assert np.isclose(eta, gamma * nu / vt, rtol=1e-9), (m, eta)
+        if m == 3:
+            assert np.isclose(eta, 3.4e-4, rtol=1e-9)
 
 
 def test_acwb_aggregation_invariants():
