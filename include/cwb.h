@@ -158,11 +158,20 @@ int cwb_get_n_star_k(cwb_ctx* ctx, int32_t* n_star_k_out);
 int cwb_get_pool(cwb_ctx* ctx, double* z, uint16_t* idx, double* Zb, double* G, double* Ainv);
 
 /* Implementation selector for cwb_train and its variants (tests use it to cover
- * both): 0 = auto, 1 = fused persistent kernel (one CTA per one or two
- * replications, residuals resident in shared memory; CWB_EUNSUPPORTED from the
- * training call when its layout does not fit), 2 = general per-iteration kernels.
- * Errors: CWB_EINVAL (path not 0..2), CWB_EUNSUPPORTED (1 on a row-sharded context; 0 or 1
- * on a learner-sharded context, which runs the per-iteration kernels only). */
+ * all): 0 = auto (1 when it fits, else 2; never 3), 1 = fused persistent kernel (one
+ * CTA per one or two replications, residuals resident in shared memory;
+ * CWB_EUNSUPPORTED from the training call when its layout does not fit), 2 = general
+ * per-iteration kernels, 3 = cross-Gram formulation (cwb_train only, L2 loss; SURVEY
+ * Sec. 7.3 item 3): s_k = Z_k^T r is updated by s_k -= nu (Z_k^T Z_k*) theta* and r^T r
+ * by its exact expansion (Alg. 1 supp. line 8, carried through the linear map
+ * Z^T), so after one binMatVec pass for the initial residuals an iteration costs
+ * O(K d^2) per replication instead of O(n); the cross Gram Z^T Z (K d x K d, built
+ * once per pool by binMatVec over the gathered basis rows) is kept in the context.
+ * The same iterates as paths 1/2 up to rounding; the residuals themselves are never
+ * formed (the outputs do not need them).
+ * Errors: CWB_EINVAL (path not 0..3), CWB_EUNSUPPORTED (1 on a row-sharded context; 0 or 1
+ * on a learner-sharded context, which runs the per-iteration kernels only; 3 on a sharded or
+ * unbinned pool; the training variants other than cwb_train return it for path 3). */
 int cwb_set_path(cwb_ctx* ctx, int32_t path);
 
 /* H1 implementation of cwb_find_best for B <= 4 columns (tests and benchmarks

@@ -186,6 +186,7 @@ void cwb_free(cwb_ctx* c) {
     cwb_stream_release(c, s);
     cwb_nb_release(c, s);
     cwb_release(c->h1c, s);
+    cwb_release(c->xg, s);
     if (c->ev_plan) {
         cudaEventSynchronize(c->ev_plan);  // the header copy into the pinned slot has landed
         cudaEventDestroy(c->ev_plan);
@@ -346,8 +347,10 @@ int cwb_set_narrow(cwb_ctx* c, int32_t mode) {
 }
 
 int cwb_set_path(cwb_ctx* c, int32_t path) {
-    if (!c || path < 0 || path > 2) return cwb_set_error(c, CWB_EINVAL, "cwb_set_path: invalid argument");
+    if (!c || path < 0 || path > 3) return cwb_set_error(c, CWB_EINVAL, "cwb_set_path: invalid argument");
     if (c->rows && path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_set_path: row-sharded context");
+    if (path == 3 && (c->rows || c->lshard || c->nb))
+        return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_set_path: the cross-Gram path needs an unsharded binned pool");
     // learner sharding runs on the per-iteration kernels only (the fused and stream paths fit all K learners)
     if (c->lshard && path != 2)
         return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_set_path: learner-sharded context (path 2 only)");
@@ -373,6 +376,8 @@ int cwb_train(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, doub
     c->stream = s;
     if (c->rows)
         return cwb_train_rows(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace, s);
+    if (c->path == 3)
+        return cwb_train_gram(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace, risk_trace, s);
     if (c->path != 2) {
         bool launched = false;
         int rc = cwb_train_fused(c, Y, B, nu, M, offset_out, theta_agg_out, k_trace, sse_trace,
@@ -393,6 +398,7 @@ int cwb_train_bernoulli(cwb_ctx* c, const double* Y, int32_t B, double nu, int32
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: row-sharded context");
     if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: learner-sharded context");
+    if (c->path == 3) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: the cross-Gram path (3) is cwb_train only");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_bernoulli: unbinned pool (cwb_train only)");
     if (c->path != 2) {
         bool launched = false;
@@ -415,6 +421,7 @@ int cwb_train_folds(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* fold_
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: row-sharded context");
     if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: learner-sharded context");
+    if (c->path == 3) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: the cross-Gram path (3) is cwb_train only");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_folds: unbinned pool (cwb_train only)");
     return cwb_train_folds_general(c, Y, B, fold_of_row, F, fold_of_rep, nu, M, offset_out, theta_agg_out, k_trace,
                                    sse_trace, risk_trace, val_risk_trace, s);
@@ -430,6 +437,7 @@ int cwb_train_acwb(cwb_ctx* c, const double* Y, int32_t B, double nu, double gam
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: row-sharded context");
     if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: learner-sharded context");
+    if (c->path == 3) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: the cross-Gram path (3) is cwb_train only");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_acwb: unbinned pool (cwb_train only)");
     if (c->path != 2) {
         bool launched = false;
@@ -454,6 +462,7 @@ int cwb_train_hcwb(cwb_ctx* c, const double* Y, int32_t B, const uint8_t* val_ma
     c->stream = s;
     if (c->rows) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: row-sharded context");
     if (c->lshard) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: learner-sharded context");
+    if (c->path == 3) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: the cross-Gram path (3) is cwb_train only");
     if (c->nb) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: unbinned pool (cwb_train only)");
     return cwb_train_hcwb_general(c, Y, B, val_mask, nu, gamma, pat0, M, offset_out, theta_f_out, k_trace, kcor_trace,
                                   sse_trace, risk_trace, val_risk_trace, switch_iter, s);

@@ -75,6 +75,10 @@ struct cwb_ctx {
     int32_t h1_chunking = 1; // general-path H1 swept in L2-sized row chunks when a tile exceeds L2 (CWB_H1_CHUNKING=0 off)
     uint32_t* h1c = nullptr; // chunked H1: [K][nch][n*] row counts, then starts
     int32_t h1c_nch = 0;
+    // cross-Gram path (cwb_set_path 3): xg[(k d + a) * xg_ld + k' d + b] = (Z_k^T Z_k')[a][b],
+    // built on the first path-3 train call of the pool
+    double* xg = nullptr;
+    int32_t xg_ld = 0;
     cudaStream_t stream = 0;
     int status = CWB_OK;
     std::string err;
@@ -183,6 +187,9 @@ int cwb_fused_plan(cwb_ctx* ctx, cudaStream_t s);
 int cwb_train_general(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
                       double* offset_out, double* theta_agg_out, int32_t* k_trace,
                       double* sse_trace, double* risk_trace, cudaStream_t s);
+int cwb_train_gram(cwb_ctx* ctx, const double* Y, int32_t B, double nu, int32_t M,
+                   double* offset_out, double* theta_agg_out, int32_t* k_trace,
+                   double* sse_trace, double* risk_trace, cudaStream_t s);
 int cwb_train_acwb_fused(cwb_ctx* c, const double* Y, int32_t B, double nu, double gamma, int32_t M,
                          double* offset_out, double* theta_f_out, double* theta_h_out, int32_t* k_trace,
                          int32_t* kcor_trace, double* sse_trace, double* risk_trace, cudaStream_t s,

@@ -1874,7 +1874,11 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
                                   k_trace, kcor_trace, sse_trace, risk_trace, val_risk_trace, switch_iter, s,
                                   &launched);
         if (rc || launched) return rc;
-        if (c->path == 1) return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: fused path does not fit");
+        if (c->path == 1) {  // a device-side error (e.g. the mask check above) stopped the plan: report it first
+            const int st = cwb_status(c);
+            if (st) return st;
+            return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train_hcwb: fused path does not fit");
+        }
     }
     cudaMemsetAsync(phase, 0, sizeof(int32_t) * 2 * Bq, s);
     // f0 = mean of the training targets (Alg. 2 line 2 on D_train); rr = sum over training rows
@@ -1931,4 +1935,187 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
         c->launches += 8;
     }
     return cwb_check_launch(c, "HCWB kernels");
+}
+
+// ===================================================================== cross-Gram path (cwb_set_path 3)
+// SURVEY Sec. 7.3 item 3, an exact reformulation of Alg. 1 supp. for the L2 loss with fixed weights.  With
+// Z_k the n x d design of learner k (row i = Zb_k[idx_k(i)]) and s_k = Z_k^T r:
+//   r^[m] = r^[m-1] - nu Z_k* theta*
+//   => s_k^[m] = s_k^[m-1] - nu (Z_k^T Z_k*) theta*,   r^T r ^[m] = r^T r - 2 nu theta*^T s_k* + nu^2 theta*^T G_k* theta*
+// so after one binMatVec pass for s^[0] (H1 + H2 on the initial residuals) every iteration costs O(K d^2) per
+// replication instead of O(n).  theta_k = A_k^-1 s_k, delta_k = |C_k^T theta_k|^2, SSE_k = r^T r - delta_k and
+// the argmin are those of the direct path (H3-H5).  The cross Gram Z^T Z (K d x K d) is itself binMatVec-shaped:
+// with P = [Z_1 ... Z_K] (n x K d, gathered basis rows), (Z_k^T Z)[a][.] = sum_l Zb_k[l][a] U_k[l][.],
+// U_k[l][.] = sum_{i: idx_k(i) = l} P[i][.] -- H1 and the H2 projection on the K d "columns" of P.
+namespace {
+
+// P[i][k d + a] = Zb_k[idx_k(i)][a] (4 non-zeros per learner block; columns >= K d are 0)
+template <typename IdxT>
+__global__ void k_gram_P(const IdxT* __restrict__ idx, int64_t n, int K, int ns, int d, int ld,
+                         const int32_t* __restrict__ zj0, const double* __restrict__ Zs, double* __restrict__ P) {
+    const int64_t tot = n * ld;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / ld;
+        const int col = (int)(e - i * ld);
+        double v = 0.0;
+        if (col < K * d) {
+            const int k = col / d, a = col - k * d;
+            const int l = (int)idx[(size_t)k * n + i];
+            const int t = a - zj0[(size_t)k * ns + l];
+            if (t >= 0 && t < CWB_SPW) v = Zs[((size_t)k * ns + l) * CWB_SPW + t];
+        }
+        P[e] = v;
+    }
+}
+
+// One CTA per replication b, all M iterations.  Shared: s (K d), theta of every learner (K d), delta (K).
+// s0: [K d][Bp] (k_h234 smode 1 layout), rr0: [Bp].  Per iteration (4 barriers):
+//   A  warp per learner: theta_k = A_k^-1 s_k (lane j), c = C_k^T theta_k (3 shuffles), delta_k = |c|^2
+//   B  warp 0: k* = argmax delta (lowest k on ties), SSE, theta_agg, t1 = theta*^T s_k*, t2 = theta*^T G_k* theta*,
+//      r^T r update, traces
+//   C  every thread: s[q] -= nu sum_b xg[(k* d + b) ld + q] theta*[b]   (rows of the symmetric cross Gram)
+__global__ void __launch_bounds__(256) k_gram_train(
+    const double* __restrict__ s0, int Bp, const double* __restrict__ rr0, const double* __restrict__ xg, int ld,
+    const double* __restrict__ Ainv, const double* __restrict__ Cb, const double* __restrict__ G, int K, int d,
+    int64_t n, double nu, int M, int B, double* __restrict__ agg, int32_t* __restrict__ k_trace,
+    double* __restrict__ sse_trace, double* __restrict__ risk_trace) {
+    extern __shared__ double gsm[];
+    const int Kd = K * d;
+    double* s = gsm;             // K d
+    double* th = s + Kd;         // K d
+    double* de = th + Kd;        // K
+    __shared__ double s_rr;
+    __shared__ int s_k;
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    for (int q = tid; q < Kd; q += blockDim.x) s[q] = s0[(size_t)q * Bp + b];
+    if (tid == 0) s_rr = rr0[b];
+    double* ag = agg + (size_t)b * Kd;
+    for (int q = tid; q < Kd; q += blockDim.x) ag[q] = 0.0;
+    __syncthreads();
+    for (int m = 0; m < M; m++) {
+        // A: H3 and H4 of every learner
+        for (int k = w; k < K; k += nw) {
+            const double* Ai = Ainv + (size_t)k * d * d;
+            const double* sk = s + k * d;
+            double t = 0.0;
+            if (lane < d)
+                for (int jp = 0; jp < d; jp++) t += Ai[(size_t)jp * d + lane] * sk[jp];  // A^-1 symmetric
+            // c_j = sum_{i<4} C[j+i][j] theta[j+i]
+            double c = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const double tj = __shfl_down_sync(0xffffffffu, t, i);
+                if (lane + i < d && lane < d) c += Cb[((size_t)k * d + lane) * 4 + i] * tj;
+            }
+            const double dl = warp_sum(lane < d ? c * c : 0.0);
+            if (lane < d) th[k * d + lane] = t;
+            if (lane == 0) de[k] = dl;
+        }
+        __syncthreads();
+        // B: H5 and the scalar updates
+        if (w == 0) {
+            int kb = -1;
+            double best = -1.0;
+            for (int k = lane; k < K; k += 32) {  // ascending k per lane: strict > keeps the lowest
+                const double v = de[k];
+                if (kb < 0 || v > best) { best = v; kb = k; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
+                if (ok >= 0 && (kb < 0 || ob > best || (ob == best && ok < kb))) { best = ob; kb = ok; }
+            }
+            const int ks = kb;
+            const double tj = lane < d ? th[ks * d + lane] : 0.0;
+            double g = 0.0;
+            if (lane < d) {
+                const double* Gk = G + (size_t)ks * d * d + (size_t)lane * d;
+                for (int jp = 0; jp < d; jp++) g += Gk[jp] * th[ks * d + jp];
+            }
+            const double t1 = warp_sum(tj * (lane < d ? s[ks * d + lane] : 0.0));
+            const double t2 = warp_sum(tj * g);
+            if (lane < d) ag[ks * d + lane] += nu * tj;
+            if (lane == 0) {
+                const double rr = s_rr;
+                const double rrn = rr - 2.0 * nu * t1 + nu * nu * t2;
+                if (k_trace) k_trace[(size_t)m * B + b] = ks;
+                if (sse_trace) sse_trace[(size_t)m * B + b] = rr - best;
+                if (risk_trace) risk_trace[(size_t)m * B + b] = rrn / (2.0 * (double)n);
+                s_rr = rrn;
+                s_k = ks;
+            }
+        }
+        __syncthreads();
+        // C: s -= nu (Z^T Z_k*) theta*
+        {
+            const int ks = s_k;
+            const double* xr = xg + (size_t)ks * d * ld;
+            const double* t = th + ks * d;
+            for (int q = tid; q < Kd; q += blockDim.x) {
+                double u = 0.0;
+                for (int bb = 0; bb < d; bb++) u += xr[(size_t)bb * ld + q] * t[bb];
+                s[q] -= nu * u;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+// builds c->xg (the cross Gram of the pool's K learners) once per pool
+static int gram_build(cwb_ctx* c, cudaStream_t s) {
+    if (c->xg) return CWB_OK;
+    const int K = c->K, d = c->d, ns = c->n_star;
+    const int ld = (K * d + 31) / 32 * 32;
+    const int64_t n = c->n;
+    double *P = nullptr, *U = nullptr, *xg = nullptr;
+    bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)n * ld, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&U, sizeof(double) * (size_t)K * ns * ld, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
+    if (!ok) {
+        cwb_release(P, s); cwb_release(U, s); cwb_release(xg, s);
+        return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
+    }
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (n * ld + 255) / 256);
+    if (c->idx_bytes == 1)
+        k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
+    else
+        k_gram_P<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
+    h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s);   // U_k[l][.] = sum over bin l of P rows
+    k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr, nullptr,
+                                             nullptr, nullptr, nullptr, 0, xg, 1);  // projection Zb_k^T U_k
+    c->launches += 2;
+    cwb_release(P, s);
+    cwb_release(U, s);
+    c->xg = xg;
+    c->xg_ld = ld;
+    return cwb_check_launch(c, "cross-Gram kernels");
+}
+
+int cwb_train_gram(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
+                   double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace, cudaStream_t s) {
+    const int K = c->K, d = c->d;
+    int rc = gram_build(c, s);
+    if (rc) return rc;
+    rc = ensure_ws(c, B, s);
+    if (rc) return rc;
+    cwb_train_ws& w = c->ws;
+    const int Bp = w.Bp;
+    double* off_ws = w.rr + Bp;
+    rc = column_stats(c, Y, B, true, off_ws, w.rr, offset_out, s);   // f0 = mean(y), r^T r (Alg. 1 lines 2-4)
+    if (rc) return rc;
+    dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
+    k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
+    // s^[0] = Z^T r^[0]: H1 + H2 of the initial residuals, into w.theta ([K d][Bp], k_h234 smode 1)
+    h1(c, w.Rt, Bp, K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr,
+                                             nullptr, nullptr, nullptr, nullptr, 0, w.theta, 1);
+    const size_t smem = sizeof(double) * (2 * (size_t)K * d + K);
+    CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_gram_train, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gram_train<<<B, 256, smem, s>>>(w.theta, Bp, w.rr, c->xg, c->xg_ld, c->Ainv, c->Cb, c->G, K, d, c->n, nu, M,
+                                       B, theta_agg_out, k_trace, sse_trace, risk_trace);
+    c->launches += 4;
+    return cwb_check_launch(c, "cross-Gram train kernels");
 }
