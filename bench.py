@@ -401,6 +401,8 @@ def main():
             pool.set_path(args.path)
         b.record(stream)
         outs = train(pool, outs)
+        if ws > 1 and not strong and args.algo == "cwb":  # one all-gather of the results
+            D.gather_results(outs, w)
         c_.record(stream)
         launches.append(pool.launches())
         pool.close()

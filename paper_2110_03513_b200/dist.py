@@ -88,6 +88,32 @@ def gather_rows(t, w: World):
     return torch.cat(parts, 0)
 
 
+def gather_results(out: dict, w: World) -> dict:
+    """Replication sharding's one collective: every rank's training outputs of its block
+    of replications -- offset [B], theta_agg [B, K, d], k/sse/risk traces [M, B] -- packed into one
+    [B, 1 + K d + 3 M] float64 tensor and all-gathered in rank order (one NCCL all-gather on the GPU).
+    Returns the same keys with the replication axis of all ranks (rank r's block at [r B, (r+1) B))."""
+    import torch
+    off, agg = out["offset"], out["theta_agg"]
+    B, K, d = agg.shape
+    tr = [out[k] for k in ("k_trace", "sse_trace", "risk_trace")]
+    M = tr[0].shape[0]
+    pack = torch.cat([off.reshape(B, 1).to(torch.float64), agg.reshape(B, K * d)] +
+                     [t.t().to(torch.float64) for t in tr], 1).contiguous()
+    if w.size > 1:
+        import torch.distributed as dist
+        full = torch.empty((w.size * B, pack.shape[1]), dtype=pack.dtype, device=pack.device)
+        dist.all_gather_into_tensor(full, pack)
+    else:
+        full = pack
+    Bt = full.shape[0]
+    o = 1 + K * d
+    return {"offset": full[:, 0].contiguous(), "theta_agg": full[:, 1:o].reshape(Bt, K, d),
+            "k_trace": full[:, o:o + M].t().to(torch.int32).contiguous(),
+            "sse_trace": full[:, o + M:o + 2 * M].t().contiguous(),
+            "risk_trace": full[:, o + 2 * M:o + 3 * M].t().contiguous()}
+
+
 def row_block(n: int, rank: int, world: int) -> range:
     """Rows [floor(n r / W), floor(n (r+1) / W)) of rank r: the block libcwb keeps after an
     attach (cwb_rows.cu restrict_rows uses the same formula)."""

@@ -39,6 +39,13 @@ def _worker(rank, size, port, q):
         res = pool.train(ds.Y, nu=cfg.nu, M=cfg.M)
         kt = D.gather_rows(torch.as_tensor(np.ascontiguousarray(res.k_trace.T)), w)      # [B_total, M]
         agg = D.gather_rows(torch.as_tensor(res.theta_agg), w)                          # [B_total, K, d]
+        # the packed one-collective gather bench.py runs at the end of every sharded step
+        full = D.gather_results({"offset": torch.as_tensor(res.offset), "theta_agg": torch.as_tensor(res.theta_agg),
+                                 "k_trace": torch.as_tensor(res.k_trace), "sse_trace": torch.as_tensor(res.sse_trace),
+                                 "risk_trace": torch.as_tensor(res.risk_trace)}, w)
+        assert (full["theta_agg"].numpy() == agg.numpy()).all()
+        assert (full["k_trace"].numpy().T == kt.numpy()).all() and full["k_trace"].dtype == torch.int32
+        assert full["sse_trace"].shape == (cfg.M, 4 * size) and full["offset"].shape == (4 * size,)
         tmax = D.max_over_ranks(float(10 + w.rank), w)
         D.barrier(w)
         strong = [list(D.split_replications(7, size, r)) for r in range(size)]
