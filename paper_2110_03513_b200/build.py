@@ -23,23 +23,26 @@ def deps() -> list[str]:
         os.path.join(ROOT, "include", "cwb.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+LIB_JITTER = os.path.join(HERE, "libcwb_jitter.so")
+JITTER_SEED = 0x5EED
+
+
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compiles every csrc/*.cu to an object in parallel (objects of unchanged sources are
-    reused), then links libcwb.so."""
-    if force or not up_to_date():
+def _build(lib: str, odir: str, extra: list[str], force: bool, verbose: bool) -> str:
+    """Compiles every csrc/*.cu to an object in parallel (objects of unchanged sources are reused), then
+    links `lib`."""
+    if force or not up_to_date(lib):
         from concurrent.futures import ThreadPoolExecutor
-        odir = os.path.join(HERE, "build")
         os.makedirs(odir, exist_ok=True)
         hdrs = [p for p in deps() if not p.endswith(".cu")]
         newest_hdr = max(os.path.getmtime(p) for p in hdrs)
-        comp = [f for f in FLAGS if f not in ("-shared", "-ldl")]
+        comp = [f for f in FLAGS if f not in ("-shared", "-ldl")] + extra
 
         def obj(src):
             o = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
@@ -55,9 +58,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
         with ThreadPoolExecutor(max_workers=len(sources())) as ex:
             objs = list(ex.map(obj, sources()))
-        cmd = [NVCC, "-shared", "-ldl", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp", *objs]
+        cmd = [NVCC, "-shared", "-ldl", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib + ".tmp", *objs]
         subprocess.run(cmd, check=True)
-        os.replace(LIB + ".tmp", LIB)
+        os.replace(lib + ".tmp", lib)
+    return lib
+
+
+def build(force: bool = False, verbose: bool = False, jitter: bool = True) -> str:
+    """libcwb.so, and (jitter=True) libcwb_jitter.so: the same sources with -DCWB_JITTER, the schedule-
+    perturbation build of tests/test_gpu_jitter.py (race hunting; compute-sanitizer is closed on the pool)."""
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = [(LIB, os.path.join(HERE, "build"), [])]
+    if jitter:
+        jobs.append((LIB_JITTER, os.path.join(HERE, "build", "jitter"), [f"-DCWB_JITTER={JITTER_SEED}"]))
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        list(ex.map(lambda j: _build(j[0], j[1], j[2], force, verbose), jobs))
     return LIB
 
 

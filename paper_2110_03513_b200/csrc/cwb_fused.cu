@@ -506,6 +506,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         } else if (m > 0 && warp < RB) {
             bookkeeping(m - 1, warp);
         }
+        CWB_JIT(m * 8 + 0);
         // ---- A / H1: each lane sums its task, 4 steps per offset load ------------------
         for (int rd = 0; rd < rounds; rd++) {
             const int steps = __ldg(wl + rd * NW + warp);  // warp-uniform
@@ -555,6 +556,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
         __syncthreads();
         if (timed) tm = phase_mark(&tA, tm, true);
+        CWB_JIT(m * 8 + 1);
         // ---- B / H2-H4, one warp per learner, lane j = coefficient j:
         //      s = Zb^T u (window of basis j), theta = (G + lambda D)^-1 s (cached inverse,
         //      P:L846), c = C^T theta, delta = |c|^2 = 2 theta^T s - theta^T G theta ------
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
         __syncthreads();
         if (timed) tm = phase_mark(&tB, tm, true);
+        CWB_JIT(m * 8 + 2);
         // ---- C / H5: job (q, slice): k* = argmax delta (lowest k on ties) for
         //      replication q, then zhat = nu Zb_k* theta_k* on design points slice*32 + lane ------
         {
@@ -659,6 +662,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
         __syncthreads();
         if (timed) tm = phase_mark(&tC, tm, true);
+        CWB_JIT(m * 8 + 3);
         // ---- D / H6: r_i -= zhat[idx_k*(i)], per-thread r^T r partials -------------
         if (HC) {
             // D1: models after iteration m (phase hc_ph): ACWB F = (1-vt) F + vt H - nu b_k (= y - (g + nu b_k)),
@@ -688,6 +692,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             red[(parw * NRB + RB) * T + tid] = accA;
             red[(parw * NRB + RB + 1) * T + tid] = accV;
             __syncthreads();
+            CWB_JIT(m * 8 + 4);
             // decide (Alg. 3 line 6): risk traces, patience counter, one-way switch to CWB
             if (warp == 0) {
                 double sa = 0.0, sv = 0.0;
@@ -715,6 +720,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 }
             }
             __syncthreads();
+            CWB_JIT(m * 8 + 5);
             const bool accel1 = hc_ph == 0;
             if (accel && !accel1) {  // switched: the pool's tables from now on
                 if (POOL) {
@@ -816,6 +822,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
         __syncthreads();
         if (timed) tm = phase_mark(&tD, tm, true);
+        CWB_JIT(m * 8 + 6);
     }
     if (HC) {
         if (p.M > 0 && warp == 0) bookkeeping_hc(p.M - 1);

@@ -244,6 +244,27 @@ int cwb_num_sms();
 void cwb_release_header_slot(int32_t* slot);
 constexpr int CWB_MAX_SMS = 256;  // bound for per-SM tables in shared memory
 
+// Schedule perturbation for race hunting (compute-sanitizer is closed on this GPU pool): the jitter build
+// (libcwb_jitter.so, -DCWB_JITTER=<seed>) delays about a quarter of the warps at every marked point by a
+// pseudo-random 0-2 us, keyed by (block, warp, salt, seed).  Every kernel here is deterministic, so any
+// output that differs from the normal build's bytes exposes a missing barrier / ordering bug
+// (tests/test_gpu_jitter.py).  In the normal build the marks compile to nothing.
+#ifdef CWB_JITTER
+__device__ __forceinline__ void cwb_jitter(unsigned salt) {
+    unsigned h = (blockIdx.x * 0x9E3779B1u) ^ (blockIdx.y * 0x85EBCA77u) ^ ((threadIdx.x >> 5) * 0xC2B2AE3Du) ^
+                 (salt * 0x27D4EB2Fu) ^ (unsigned)(CWB_JITTER);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    if ((h & 3u) == 0u) __nanosleep((h >> 21) & 2047u);
+}
+#define CWB_JIT(salt) cwb_jitter((unsigned)(salt))
+#else
+#define CWB_JIT(salt) ((void)0)
+#endif
+
 // Warp reductions with a fixed butterfly order (deterministic).
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -1939,14 +1939,17 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
 
 // ===================================================================== cross-Gram path (cwb_set_path 3)
 // SURVEY Sec. 7.3 item 3, an exact reformulation of Alg. 1 supp. for the L2 loss with fixed weights.  With
-// Z_k the n x d design of learner k (row i = Zb_k[idx_k(i)]) and s_k = Z_k^T r:
-//   r^[m] = r^[m-1] - nu Z_k* theta*            (P:L293)
-//   => s_k^[m] = s_k^[m-1] - nu (Z_k^T Z_k*) theta*,   r^T r ^[m] = r^T r - 2 nu theta*^T s_k* + nu^2 theta*^T G_k* theta*
-// so after one binMatVec pass for s^[0] (H1 + H2 on the initial residuals) every iteration costs O(K d^2) per
-// replication instead of O(n).  theta_k = A_k^-1 s_k, delta_k = |C_k^T theta_k|^2, SSE_k = r^T r - delta_k and
-// the argmin are those of the direct path (H3-H5).  The cross Gram Z^T Z (K d x K d) is itself binMatVec-shaped:
-// with P = [Z_1 ... Z_K] (n x K d, gathered basis rows), (Z_k^T Z)[a][.] = sum_l Zb_k[l][a] U_k[l][.],
-// U_k[l][.] = sum_{i: idx_k(i) = l} P[i][.] -- H1 and the H2 projection on the K d "columns" of P.
+// Z_k the n x d design of learner k (row i = Zb_k[idx_k(i)]), s_k = Z_k^T r and the
+// cached fit theta_k = A_k^-1 s_k (A_k = G_k + lambda_k D):
+//   r^[m] = r^[m-1] - nu Z_k* theta*                                   (P:L293)
+//   => theta_k^[m] = theta_k^[m-1] - nu W_k,k* theta*,   W_k,k' = A_k^-1 (Z_k^T Z_k')
+//      r^T r ^[m] = r^T r - 2 nu theta*^T s_k* + nu^2 theta*^T G_k* theta* = r^T r - nu delta* - nu (1 - nu) theta*^T G_k* theta*
+// (delta = 2 theta^T s - theta^T G theta), so after one binMatVec pass for theta^[0] (H1-H3 on the
+// initial residuals) an iteration costs O(K d^2) per replication instead of O(n).  delta_k = |C_k^T theta_k|^2,
+// SSE_k = r^T r - delta_k and the argmin are those of the direct path (H4, H5).  The cross Gram Z^T Z
+// (K d x K d) is itself binMatVec-shaped: with P = [Z_1 ... Z_K] (n x K d, gathered basis rows),
+// (Z_k^T Z)[a][.] = sum_l Zb_k[l][a] U_k[l][.], U_k[l][.] = sum_{i: idx_k(i) = l} P[i][.] -- H1 and the H2
+// projection on the K d "columns" of P.
 namespace {
 
 // P[i][k d + a] = Zb_k[idx_k(i)][a] (4 non-zeros per learner block; columns >= K d are 0)
@@ -1968,50 +1971,62 @@ __global__ void k_gram_P(const IdxT* __restrict__ idx, int64_t n, int K, int ns,
     }
 }
 
-// One CTA per replication b, all M iterations.  Shared: s (K d), theta of every learner (K d), delta (K).
-// s0: [K d][Bp] (k_h234 smode 1 layout), rr0: [Bp].  Per iteration (4 barriers):
-//   A  warp per learner: theta_k = A_k^-1 s_k (lane j), c = C_k^T theta_k (3 shuffles), delta_k = |c|^2
-//   B  warp 0: k* = argmax delta (lowest k on ties), SSE, theta_agg, t1 = theta*^T s_k*, t2 = theta*^T G_k* theta*,
-//      r^T r update, traces
-//   C  every thread: s[q] -= nu sum_b xg[(k* d + b) ld + q] theta*[b]   (rows of the symmetric cross Gram)
+// Wt[(k' d + b) ld + k d + a] = (A_k^-1 Z_k^T Z_k')[a][b] = sum_c A_k^-1[a][c] xg[(k' d + b) ld + k d + c]
+// (xg symmetric): row (k', b) of Wt is what an iteration with k* = k' reads, contiguous in (k, a)
+__global__ void k_gram_w(const double* __restrict__ xg, const double* __restrict__ Ainv, int K, int d, int ld,
+                         double* __restrict__ Wt) {
+    const int row = blockIdx.x;  // k' d + b
+    const double* xr = xg + (size_t)row * ld;
+    for (int q = threadIdx.x; q < ld; q += blockDim.x) {
+        double v = 0.0;
+        if (q < K * d) {
+            const int k = q / d, a = q - k * d;
+            const double* Ai = Ainv + ((size_t)k * d + a) * d;
+            for (int c = 0; c < d; c++) v += Ai[c] * xr[k * d + c];
+        }
+        Wt[(size_t)row * ld + q] = v;
+    }
+}
+
+// One CTA per replication b, all M iterations.  Shared: theta of every learner (K d), delta (K), theta* (d);
+// C (the band factor of G + 2 lambda D, K d 4) is read through L1.  th0: [K d][Bp] (k_h234 layout), rr0: [Bp].  Per iteration:
+//   A  warp per learner: c = C_k^T theta_k (the band, 3 shuffles), delta_k = |c|^2                   (H4)
+//   B  warp 0: k* = argmax delta (lowest k on ties), SSE, theta_agg[k*] += nu theta* (P:L838),
+//      t2 = theta*^T G_k* theta*, r^T r -= nu delta* + nu (1 - nu) t2, traces
+//   C  every thread: theta[q] -= nu sum_b Wt[(k* d + b) ld + q] theta*[b]
 __global__ void __launch_bounds__(256) k_gram_train(
-    const double* __restrict__ s0, int Bp, const double* __restrict__ rr0, const double* __restrict__ xg, int ld,
-    const double* __restrict__ Ainv, const double* __restrict__ Cb, const double* __restrict__ G, int K, int d,
-    int64_t n, double nu, int M, int B, double* __restrict__ agg, int32_t* __restrict__ k_trace,
-    double* __restrict__ sse_trace, double* __restrict__ risk_trace) {
+    const double* __restrict__ th0, int Bp, const double* __restrict__ rr0, const double* __restrict__ Wt, int ld,
+    const double* __restrict__ Cb, const double* __restrict__ G, int K, int d, int64_t n, double nu, int M, int B,
+    double* __restrict__ agg, int32_t* __restrict__ k_trace, double* __restrict__ sse_trace,
+    double* __restrict__ risk_trace) {
     extern __shared__ double gsm[];
     const int Kd = K * d;
-    double* s = gsm;             // K d
-    double* th = s + Kd;         // K d
-    double* de = th + Kd;        // K
-    __shared__ double s_rr;
+    double* th = gsm;              // K d
+    double* de = th + Kd;          // K   (the band factor stays in global memory: L1-resident, shared by all CTAs)
+    __shared__ double s_rr, s_ts[CWB_MAX_D];
     __shared__ int s_k;
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
-    for (int q = tid; q < Kd; q += blockDim.x) s[q] = s0[(size_t)q * Bp + b];
+    for (int q = tid; q < Kd; q += blockDim.x) th[q] = th0[(size_t)q * Bp + b];
     if (tid == 0) s_rr = rr0[b];
     double* ag = agg + (size_t)b * Kd;
     for (int q = tid; q < Kd; q += blockDim.x) ag[q] = 0.0;
     __syncthreads();
     for (int m = 0; m < M; m++) {
-        // A: H3 and H4 of every learner
+        CWB_JIT(m * 4 + 0);
+        // A: delta_k = |C_k^T theta_k|^2, c_j = sum_{i<4} C[j+i][j] theta[j+i]
         for (int k = w; k < K; k += nw) {
-            const double* Ai = Ainv + (size_t)k * d * d;
-            const double* sk = s + k * d;
-            double t = 0.0;
-            if (lane < d)
-                for (int jp = 0; jp < d; jp++) t += Ai[(size_t)jp * d + lane] * sk[jp];  // A^-1 symmetric
-            // c_j = sum_{i<4} C[j+i][j] theta[j+i]
+            const double t = lane < d ? th[k * d + lane] : 0.0;
             double c = 0.0;
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 const double tj = __shfl_down_sync(0xffffffffu, t, i);
-                if (lane + i < d && lane < d) c += Cb[((size_t)k * d + lane) * 4 + i] * tj;
+                if (lane + i < d && lane < d) c += __ldg(Cb + (k * d + lane) * 4 + i) * tj;
             }
             const double dl = warp_sum(lane < d ? c * c : 0.0);
-            if (lane < d) th[k * d + lane] = t;
             if (lane == 0) de[k] = dl;
         }
         __syncthreads();
+        CWB_JIT(m * 4 + 1);
         // B: H5 and the scalar updates
         if (w == 0) {
             int kb = -1;
@@ -2030,15 +2045,16 @@ __global__ void __launch_bounds__(256) k_gram_train(
             const double tj = lane < d ? th[ks * d + lane] : 0.0;
             double g = 0.0;
             if (lane < d) {
-                const double* Gk = G + (size_t)ks * d * d + (size_t)lane * d;
-                for (int jp = 0; jp < d; jp++) g += Gk[jp] * th[ks * d + jp];
+                const double* Gk = G + ((size_t)ks * d + lane) * d;
+                for (int jp = max(0, lane - (CWB_SPW - 1)); jp <= min(d - 1, lane + CWB_SPW - 1); jp++)
+                    g += Gk[jp] * th[ks * d + jp];   // G banded (|j - j'| <= 3)
+                s_ts[lane] = tj;
+                ag[ks * d + lane] += nu * tj;
             }
-            const double t1 = warp_sum(tj * (lane < d ? s[ks * d + lane] : 0.0));
             const double t2 = warp_sum(tj * g);
-            if (lane < d) ag[ks * d + lane] += nu * tj;
             if (lane == 0) {
                 const double rr = s_rr;
-                const double rrn = rr - 2.0 * nu * t1 + nu * nu * t2;
+                const double rrn = rr - nu * best - nu * (1.0 - nu) * t2;
                 if (k_trace) k_trace[(size_t)m * B + b] = ks;
                 if (sse_trace) sse_trace[(size_t)m * B + b] = rr - best;
                 if (risk_trace) risk_trace[(size_t)m * B + b] = rrn / (2.0 * (double)n);
@@ -2047,15 +2063,20 @@ __global__ void __launch_bounds__(256) k_gram_train(
             }
         }
         __syncthreads();
-        // C: s -= nu (Z^T Z_k*) theta*
+        CWB_JIT(m * 4 + 2);
+        // C: theta_k -= nu W_k,k* theta*
         {
             const int ks = s_k;
-            const double* xr = xg + (size_t)ks * d * ld;
-            const double* t = th + ks * d;
+            const double* wr = Wt + (size_t)ks * d * ld;
             for (int q = tid; q < Kd; q += blockDim.x) {
-                double u = 0.0;
-                for (int bb = 0; bb < d; bb++) u += xr[(size_t)bb * ld + q] * t[bb];
-                s[q] -= nu * u;
+                double u0 = 0.0, u1 = 0.0;
+                int bb = 0;
+                for (; bb + 1 < d; bb += 2) {
+                    u0 += wr[(size_t)bb * ld + q] * s_ts[bb];
+                    u1 += wr[(size_t)(bb + 1) * ld + q] * s_ts[bb + 1];
+                }
+                if (bb < d) u0 += wr[(size_t)bb * ld + q] * s_ts[bb];
+                th[q] -= nu * (u0 + u1);
             }
         }
         __syncthreads();
@@ -2064,18 +2085,19 @@ __global__ void __launch_bounds__(256) k_gram_train(
 
 }  // namespace
 
-// builds c->xg (the cross Gram of the pool's K learners) once per pool
+// builds the cross Gram of the pool's K learners and Wt = (A^-1 Z^T Z)^T rows once per pool (c->xg)
 static int gram_build(cwb_ctx* c, cudaStream_t s) {
     if (c->xg) return CWB_OK;
     const int K = c->K, d = c->d, ns = c->n_star;
     const int ld = (K * d + 31) / 32 * 32;
     const int64_t n = c->n;
-    double *P = nullptr, *U = nullptr, *xg = nullptr;
+    double *P = nullptr, *U = nullptr, *xg = nullptr, *Wt = nullptr;
     bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)n * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&U, sizeof(double) * (size_t)K * ns * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
+    ok &= cwb_alloc((void**)&Wt, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
     if (!ok) {
-        cwb_release(P, s); cwb_release(U, s); cwb_release(xg, s);
+        cwb_release(P, s); cwb_release(U, s); cwb_release(xg, s); cwb_release(Wt, s);
         return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
     }
     const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (n * ld + 255) / 256);
@@ -2086,10 +2108,12 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
     h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s);   // U_k[l][.] = sum over bin l of P rows
     k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, 0, xg, 1);  // projection Zb_k^T U_k
-    c->launches += 2;
+    k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
+    c->launches += 3;
     cwb_release(P, s);
     cwb_release(U, s);
-    c->xg = xg;
+    cwb_release(xg, s);
+    c->xg = Wt;
     c->xg_ld = ld;
     return cwb_check_launch(c, "cross-Gram kernels");
 }
@@ -2108,14 +2132,14 @@ int cwb_train_gram(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
     if (rc) return rc;
     dim3 gt((unsigned)((c->n + 31) / 32), Bp / 32);
     k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
-    // s^[0] = Z^T r^[0]: H1 + H2 of the initial residuals, into w.theta ([K d][Bp], k_h234 smode 1)
+    // theta^[0] = A^-1 Z^T r^[0]: H1-H3 of the initial residuals (k_h234 also writes delta, unused here)
     h1(c, w.Rt, Bp, K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
-    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr,
-                                             nullptr, nullptr, nullptr, nullptr, 0, w.theta, 1);
-    const size_t smem = sizeof(double) * (2 * (size_t)K * d + K);
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+                                             w.delta);
+    const size_t smem = sizeof(double) * ((size_t)K * d + K);
     CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_gram_train, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_gram_train<<<B, 256, smem, s>>>(w.theta, Bp, w.rr, c->xg, c->xg_ld, c->Ainv, c->Cb, c->G, K, d, c->n, nu, M,
-                                       B, theta_agg_out, k_trace, sse_trace, risk_trace);
+    k_gram_train<<<B, 256, smem, s>>>(w.theta, Bp, w.rr, c->xg, c->xg_ld, c->Cb, c->G, K, d, c->n, nu, M, B,
+                                       theta_agg_out, k_trace, sse_trace, risk_trace);
     c->launches += 4;
     return cwb_check_launch(c, "cross-Gram train kernels");
 }

@@ -394,7 +394,9 @@ __global__ void __launch_bounds__(kStreamT, 1)
         const int bf = (it - i0) & 1;
         cp_async_commit_wait_all();                          // this thread's table copies of item it
         if (tma) mbar_wait(&bars[bf], (uint32_t)(((it - i0) >> 1) & 1));
+        CWB_JIT(it * 4 + 0);
         __syncthreads();  // item it's data visible; item it - 1 consumed (buffer bf ^ 1 is free)
+        CWB_JIT(it * 4 + 1);
         if (lg != cur_lg) {  // flush the bin sums of the previous learner group
             for (int a = tid; a < NU; a += blockDim.x) {
                 Pj[(size_t)slot * NU + a] = U[a];
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(kStreamT, 1)
             cur_lg = lg;
             __syncthreads();
         }
+        CWB_JIT(it * 4 + 2);
         if (it + 1 < i1) issue(it + 1, bf ^ 1);
         // this warp's block range in item it + 1, read early: its first blocks are loaded before the
         // end-of-item barrier so that their latency overlaps the wait
@@ -536,6 +539,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     __syncthreads();
     const int nj = s_nj;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_h1_stream complete: P and rrp visible
+    CWB_JIT(k * 4 + 0);
     for (int e = tid; e < ns * B; e += blockDim.x) {  // u_k(l) for column q, partials added in CTA order
         const int l = e / B, q = e - l * B;
         const double* pq = P + (size_t)q * N * nslot * NU + a0 + l;
@@ -591,6 +595,7 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
         for (int j = 0; j < d; j++) v += V[j][tid];
         delta[(size_t)k * 4 + tid] = v;
     }
+    CWB_JIT(k * 4 + 1);
     __threadfence();
     __syncthreads();
     if (tid == 0) last = atomicAdd(ticket, 1u) == (unsigned)(K - 1);

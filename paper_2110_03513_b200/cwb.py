@@ -13,7 +13,8 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcwb.so")
+# CWB_LIB selects another in-tree build of the same sources (tests: libcwb_jitter.so)
+LIB_PATH = os.environ.get("CWB_LIB") or os.path.join(HERE, "libcwb.so")
 
 CODES = {0: "CWB_OK", -1: "CWB_EINVAL", -2: "CWB_EDEGENERATE", -3: "CWB_ECALIB", -4: "CWB_ENONFINITE",
          -5: "CWB_EEMPTY", -6: "CWB_ECUDA", -7: "CWB_ENCCL", -8: "CWB_ENOMEM", -9: "CWB_EUNSUPPORTED"}
