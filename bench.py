@@ -86,7 +86,8 @@ def load_peaks():
         m = {r["what"]: r for r in f["measurements"]}
         peaks["dadd_tops"] = m["dadd"]["ops_per_s"] / 1e12
         peaks["dfma_tops"] = m["dfma"]["ops_per_s"] / 1e12
-        peaks["l2_read_gbs"] = m["l2_read"]["gb_per_s"]
+        peaks["l2_read_gbs"] = max([m["l2_read"]["gb_per_s"]] + [r["gb_per_s"] for k, r in m.items()
+                                                                 if k.startswith("l2_read8_")])
         peaks["hbm_read_gbs"] = m["hbm_read"]["gb_per_s"]
         peaks["dgemm_tflops"] = m["dgemm_cublas"]["tflops"]
         peaks["fp64_src"] = "measured (profiles/peaks_fp64.json)"
@@ -296,6 +297,65 @@ def findbest_b1(devname, peaks, name="R3", calls=15):
             "kernels": "k_h1_stream + k_fit_narrow", "l2": "flushed before every call"}
 
 
+def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
+    """The cross-Gram formulation (cwb_set_path 3), timed like the headline step (fresh pool:
+    cwb_init + cwb_train with the cross-Gram build, CUDA events, L2 flushed between steps) and reported
+    separately -- never mixed into the direct path's numbers.  Phases from pools with the cross Gram cached:
+    theta^[0] (one binMatVec pass, M = 0) and the M iterations (k_gram_train)."""
+    import torch
+    from paper_2110_03513_b200 import cwb
+    K, n, B, M = cfg.K, cfg.n, cfg.B, cfg.M
+
+    def ev(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    def step():
+        p = cwb.Pool(X, gcfg)
+        p.set_path(3)
+        p.train(Y, nu=cfg.nu, M=M)
+        p.close()
+    for i in range(args.warmup):
+        step()
+    ts = []
+    for i in range(max(3, min(args.steps, 10))):
+        flush.fill_(float(i))
+        ts.append(ev(step))
+    ms = float(np.mean(ts))
+    p = cwb.Pool(X, gcfg)
+    t_init = ev(lambda: None)
+    p.set_path(3)
+    t_first0 = ev(lambda: p.train(Y, nu=cfg.nu, M=0))          # cross Gram + W + theta^[0]
+    t_m0 = min(ev(lambda: p.train(Y, nu=cfg.nu, M=0)) for _ in range(3))   # theta^[0] only
+    t_mm = min(ev(lambda: p.train(Y, nu=cfg.nu, M=M)) for _ in range(3))
+    p.status()
+    ld = (K * p.d + 31) // 32 * 32
+    p.close()
+    t_x = t_first0 - t_m0
+    t_it = t_mm - t_m0
+    # dominant phase = the cross-Gram build: binMatVec of the K learners over the ld gathered basis columns
+    # (K n ld adds, the gather of 8 B per add from L2 as the direct path's H1)
+    adds_x = K * n * ld
+    dadd = float(peaks["dadd_tops"]) * 1e12
+    l2 = float(peaks.get("l2_read_gbs", 0.0)) * 1e9
+    return {"path": "cross-Gram (cwb_set_path 3): s_k -= nu Z_k^T Z_k* theta*, exact reformulation of Alg. 1 for "
+                    "L2 loss; parity tests/test_gpu_gram.py (R0-R3 vs the oracle, tie rule 1e-12)",
+            "ms_per_step": ms, "value": K * n * B * M / (ms * 1e-3), "unit": UNIT,
+            "speedup_vs_direct": direct_ms / ms,
+            "phases_ms": {"xgram_build": t_x, "theta0_binmatvec": t_m0, "iterations": t_it,
+                          "iteration_us": t_it / max(M, 1) * 1e3},
+            "roofline": {"kernel": "cross-Gram build (H1 + H2 over the gathered basis columns of all learners)",
+                         "bound": "alu", "adds": adds_x, "achieved": adds_x / (t_x * 1e-3) / 1e12,
+                         "peak": dadd / 1e12, "unit": "Tadd/s", "frac": adds_x / (t_x * 1e-3) / dadd,
+                         "l2_gather_frac": (8.0 * adds_x / (t_x * 1e-3) / l2) if l2 else None,
+                         "note": "time from the difference of a fresh and a cached pool (M = 0); the K d of "
+                                 f"{ld} columns are 1/6 non-zero (4 B-spline values per learner block)"}}
+
+
 def workload_config(c, n_star, d):
     return {"workload": c.name, "n": c.n, "K": c.K, "B_per_gpu": c.B, "M": c.M, "nu": c.nu,
             "n_star": n_star, "d": d, "df": c.df, "degree": c.degree, "n_knots": c.n_knots,
@@ -320,6 +380,7 @@ def main():
     ap.add_argument("--unbinned", action="store_true",
                     help="unbinned learners on the raw x (SURVEY NEXT-3): the baseline binning is compared to")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gram", action="store_true", help="skip the separately reported cross-Gram path (path 3)")
     ap.add_argument("--no-findbest", action="store_true",
                     help="skip the auxiliary B = 1 findBest measurement at R3 (SURVEY Sec. 8(d) target)")
     ap.add_argument("--ref-seconds", type=float, default=4.0,
@@ -610,6 +671,11 @@ def main():
                     line[f"findbest_b1_{fb_cfg}"] = findbest_b1(devname, peaks, fb_cfg)
                 except Exception as e:
                     line[f"findbest_b1_{fb_cfg}"] = {"error": str(e)}
+        if args.algo == "cwb" and not strong and not args.unbinned and ws == 1 and not args.no_gram:
+            try:  # after the timed region: the separately reported cross-Gram path (cwb_set_path 3)
+                line["gram"] = gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, ms_per_step)
+            except Exception as e:
+                line["gram"] = {"error": str(e)}
         if not args.no_cpu_baseline and ws == 1:
             try:
                 line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, algo=args.algo,

@@ -225,6 +225,7 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     c->batch_hint = cfg.batch_hint > 0 && !cfg.unbinned ? cfg.batch_hint : 0;
     c->nb = cfg.unbinned != 0;
     if (const char* e = getenv("CWB_H1_CHUNKING")) c->h1_chunking = atoi(e);  // A/B measurement switch
+    if (const char* e = getenv("CWB_H1_WIDE")) c->h1_wide = atoi(e) != 0;       // A/B: k_h1w vs k_h1
     if (c->nb) c->path = 2;  // per-iteration kernels only
     c->idx_bytes = ns <= 256 ? 1 : 2;
     c->perm_bytes = n <= 65536 ? 2 : 4;

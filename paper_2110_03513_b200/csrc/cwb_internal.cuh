@@ -73,6 +73,7 @@ struct cwb_ctx {
     int32_t path = 0;        // 0 auto, 1 fused, 2 general
     int32_t narrow_mode = 0; // narrow findBest H1: 0 stream plan (fallback histograms), 1 histograms
     int32_t h1_chunking = 1; // general-path H1 swept in L2-sized row chunks when a tile exceeds L2 (CWB_H1_CHUNKING=0 off)
+    bool h1_wide = true;     // H1 with two replication columns per lane (k_h1w) when Bp % 64 == 0 (CWB_H1_WIDE=0: off)
     uint32_t* h1c = nullptr; // chunked H1: [K][nch][n*] row counts, then starts
     int32_t h1c_nch = 0;
     // cross-Gram path (cwb_set_path 3): xg[(k d + a) * xg_ld + k' d + b] = (Z_k^T Z_k')[a][b],

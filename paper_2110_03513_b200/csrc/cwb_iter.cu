@@ -194,6 +194,62 @@ __global__ void k_h1c(const double* __restrict__ Rt, int64_t n, int Bp, int K, i
     *up = c == 0 ? acc : *up + acc;
 }
 
+// H1, two replication columns per lane (64 per warp, 16-byte gathers): one warp per (learner, bin) as k_h1,
+// rows of the bin in increasing order and one accumulator per column, so every sum is added in exactly
+// k_h1's order (bitwise the same U).  The bin's row ids are loaded 32 at a time, one per lane (coalesced),
+// and broadcast with a shuffle; the row address is one IMAD.WIDE (row * row stride + column base).
+// CHUNK: the rows of chunk c only (k_h1c's tables); U += the chunk sums (chunk 0 writes).
+template <typename PermT, bool CHUNK>
+__global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
+                                             const int32_t* __restrict__ off, const uint32_t* __restrict__ ccnt,
+                                             int nch, int c, const PermT* __restrict__ perm, double* __restrict__ U) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x >> 5) + w;
+    if (g >= K * ns) return;
+    const int k = g / ns, l = g - k * ns;
+    const int b = blockIdx.y * 64 + 2 * lane;
+    uint32_t q, a1;
+    if (CHUNK) {
+        const size_t e = ((size_t)k * nch + c) * ns + l;
+        q = ccnt[(size_t)K * nch * ns + e];
+        a1 = q + ccnt[e];
+    } else {
+        q = (uint32_t)off[(size_t)k * (ns + 1) + l];
+        a1 = (uint32_t)off[(size_t)k * (ns + 1) + l + 1];
+    }
+    const PermT* pk = perm + (size_t)k * n;
+    const unsigned long long base = (unsigned long long)(Rt + b);
+    const uint32_t stride = (uint32_t)Bp * 8u;
+    double ax = 0.0, ay = 0.0;
+    for (; q < a1; q += 32) {
+        const int cnt = (int)min(32u, a1 - q);
+        const uint32_t mine = lane < cnt ? (uint32_t)pk[q + lane] : 0u;
+        int j = 0;
+        for (; j + 4 <= cnt; j += 4) {
+            const uint32_t i0 = __shfl_sync(0xffffffffu, mine, j), i1 = __shfl_sync(0xffffffffu, mine, j + 1);
+            const uint32_t i2 = __shfl_sync(0xffffffffu, mine, j + 2), i3 = __shfl_sync(0xffffffffu, mine, j + 3);
+            const double2 v0 = __ldg((const double2*)(base + (unsigned long long)i0 * stride));
+            const double2 v1 = __ldg((const double2*)(base + (unsigned long long)i1 * stride));
+            const double2 v2 = __ldg((const double2*)(base + (unsigned long long)i2 * stride));
+            const double2 v3 = __ldg((const double2*)(base + (unsigned long long)i3 * stride));
+            ax += v0.x; ay += v0.y; ax += v1.x; ay += v1.y;
+            ax += v2.x; ay += v2.y; ax += v3.x; ay += v3.y;
+        }
+        for (; j < cnt; j++) {
+            const uint32_t i0 = __shfl_sync(0xffffffffu, mine, j);
+            const double2 v0 = __ldg((const double2*)(base + (unsigned long long)i0 * stride));
+            ax += v0.x; ay += v0.y;
+        }
+    }
+    double2* up = reinterpret_cast<double2*>(U + (size_t)g * Bp + b);
+    if (CHUNK && c != 0) {
+        const double2 o = *up;
+        *up = make_double2(o.x + ax, o.y + ay);
+    } else {
+        *up = make_double2(ax, ay);
+    }
+}
+
 // H2-H4 for one learner (blockIdx.x) and 32 replications (blockIdx.y)
 // (HCWB: column b uses Ainv2 / G2 when phase[b mod Bph] != 0)
 // (row sharding: smode 1 writes s to Sg[k][d][Bp] and stops, smode 2 reads the summed s from Sg)
@@ -1160,11 +1216,13 @@ static constexpr int64_t kH1ChunkBytes = 40ll << 20;  // R4 sweep: 24 MB 934, 40
 static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_t* off,
                const void* perm, int perm_bytes, double* U, cudaStream_t s) {
     const int64_t n = c->n;
-    const bool chunked = n * 256 > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off;
+    const bool wide = c->h1_wide && Bp % 64 == 0;
+    const int64_t tile_row = wide ? 512 : 256;  // bytes of one row of the column tile a wave of warps gathers
+    const bool chunked = n * tile_row > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off;
     if (chunked) {
         static const int64_t chunk_bytes =
             getenv("CWB_H1_CHUNK_MB") ? (int64_t)atoi(getenv("CWB_H1_CHUNK_MB")) << 20 : kH1ChunkBytes;
-        const int64_t CR = chunk_bytes / 256;
+        const int64_t CR = chunk_bytes / tile_row;
         const int nch = (int)((n + CR - 1) / CR);
         if (!c->h1c || c->h1c_nch != nch) {  // per (learner, chunk, bin) row counts and starts, once per pool
             cwb_release(c->h1c, s);
@@ -1182,16 +1240,34 @@ static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_
         const int wpb = 8;
         dim3 grid((unsigned)(((int64_t)K * ns + wpb - 1) / wpb), Bp / 32);
         for (int ch = 0; ch < nch; ch++) {
-            if (perm_bytes == 2)
+            if (wide) {
+                dim3 gw(grid.x, Bp / 64);
+                if (perm_bytes == 2)
+                    k_h1w<uint16_t, true><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, nullptr, c->h1c, nch, ch,
+                                                            (const uint16_t*)perm, U);
+                else
+                    k_h1w<uint32_t, true><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, nullptr, c->h1c, nch, ch,
+                                                            (const uint32_t*)perm, U);
+            } else if (perm_bytes == 2) {
                 k_h1c<uint16_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint16_t*)perm, U);
-            else
+            } else {
                 k_h1c<uint32_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint32_t*)perm, U);
+            }
         }
         c->launches += nch;
         return;
     }
-    if (perm_bytes == 2) launch_h1<uint16_t>(Rt, n, Bp, K, ns, off, perm, U, s);
-    else launch_h1<uint32_t>(Rt, n, Bp, K, ns, off, perm, U, s);
+    if (wide && (int64_t)K * ns < INT32_MAX) {
+        dim3 gw((unsigned)(((int64_t)K * ns + 7) / 8), Bp / 64);
+        if (perm_bytes == 2)
+            k_h1w<uint16_t, false><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, off, nullptr, 0, 0, (const uint16_t*)perm, U);
+        else
+            k_h1w<uint32_t, false><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, off, nullptr, 0, 0, (const uint32_t*)perm, U);
+    } else if (perm_bytes == 2) {
+        launch_h1<uint16_t>(Rt, n, Bp, K, ns, off, perm, U, s);
+    } else {
+        launch_h1<uint32_t>(Rt, n, Bp, K, ns, off, perm, U, s);
+    }
     c->launches++;
 }
 

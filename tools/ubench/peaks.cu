@@ -59,6 +59,23 @@ __global__ void k_read(const double2* __restrict__ p, size_t n2, int passes, dou
     if (s0 + s1 == 12345.678) out[0] = s0;
 }
 
+// L2-resident gather-like read: every thread streams 8 independent 16-byte loads per step over a buffer that
+// fits L2 (the access width of the wide H1 kernel); best of a few buffer sizes
+__global__ void k_read8(const double2* __restrict__ p, size_t n2, int passes, double* out) {
+    double s0 = 0, s1 = 0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t per = n2 / 8;  // 8 independent streams
+    for (int ps = 0; ps < passes; ps++)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per; i += stride) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) v[u] = __ldcg(p + i + u * per);
+#pragma unroll
+            for (int u = 0; u < 8; u++) { s0 += v[u].x; s1 += v[u].y; }
+        }
+    if (s0 + s1 == 12345.678) out[0] = s0;
+}
+
 // ---------------------------------------------------------------- shared-memory loads
 __global__ void k_lds(double* out, int iters, long long* cyc) {
     __shared__ __align__(16) double2 sm[2048];
@@ -221,6 +238,26 @@ int main() {
     }
     CK(cudaGetLastError());
 
+    // L2-resident reads, 8 x 16-byte loads in flight per thread
+    for (size_t mb : {24, 48, 64, 96}) {
+        const size_t bytes = mb << 20;
+        double2* p; CK(cudaMalloc(&p, bytes));
+        CK(cudaMemset(p, 0, bytes));
+        float best = 1e30f;
+        for (int T : {256, 512})
+            for (int occ : {4, 8}) {
+                for (int rep = 0; rep < 4; rep++) {
+                    cudaEventRecord(e0);
+                    k_read8<<<sms * occ, T>>>(p, bytes / 16, 20, out);
+                    cudaEventRecord(e1);
+                    CK(cudaEventSynchronize(e1));
+                    if (rep) best = fminf(best, time_ms(e0, e1));
+                }
+            }
+        printf("{\"what\": \"l2_read8_%zuMB\", \"gb_per_s\": %.1f, \"bytes\": %zu, \"passes\": 20, \"ms\": %.3f}\n", mb,
+               (double)bytes * 20 / (best * 1e-3) / 1e9, bytes, best);
+        cudaFree(p);
+    }
     // shared memory LDS.128
     {
         const int iters = 1 << 14;
