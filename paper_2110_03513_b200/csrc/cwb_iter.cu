@@ -221,10 +221,22 @@ __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int6
     const unsigned long long base = (unsigned long long)(Rt + b);
     const uint32_t stride = (uint32_t)Bp * 8u;
     double ax = 0.0, ay = 0.0;
+    uint32_t mine = q + lane < a1 ? (uint32_t)pk[q + lane] : 0u;
     for (; q < a1; q += 32) {
         const int cnt = (int)min(32u, a1 - q);
-        const uint32_t mine = lane < cnt ? (uint32_t)pk[q + lane] : 0u;
+        // the next 32 row ids load while these 32 rows are gathered
+        const uint32_t nxt = q + 32 + lane < a1 ? (uint32_t)pk[q + 32 + lane] : 0u;
         int j = 0;
+        for (; j + 8 <= cnt; j += 8) {
+            uint32_t ii[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) ii[u] = __shfl_sync(0xffffffffu, mine, j + u);
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) v[u] = __ldg((const double2*)(base + (unsigned long long)ii[u] * stride));
+#pragma unroll
+            for (int u = 0; u < 8; u++) { ax += v[u].x; ay += v[u].y; }
+        }
         for (; j + 4 <= cnt; j += 4) {
             const uint32_t i0 = __shfl_sync(0xffffffffu, mine, j), i1 = __shfl_sync(0xffffffffu, mine, j + 1);
             const uint32_t i2 = __shfl_sync(0xffffffffu, mine, j + 2), i3 = __shfl_sync(0xffffffffu, mine, j + 3);
@@ -240,6 +252,7 @@ __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int6
             const double2 v0 = __ldg((const double2*)(base + (unsigned long long)i0 * stride));
             ax += v0.x; ay += v0.y;
         }
+        mine = nxt;
     }
     double2* up = reinterpret_cast<double2*>(U + (size_t)g * Bp + b);
     if (CHUNK && c != 0) {
@@ -311,30 +324,53 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
 }
 
 // H5: argmax over learners per replication; theta_agg update; logs
-__global__ void k_h5(const double* __restrict__ delta, const double* __restrict__ theta,
+// H5: block (32 columns, 8 warps); warp w scans the learners k = w, w + 8, ... (strict > keeps the lowest k
+// of its sequence), the 8 candidates are merged with ties to the lower k -- argmax delta = argmin SSE, lowest k
+// on ties; then theta_agg[k*] += nu theta* with the warps over the coefficients
+__global__ void __launch_bounds__(256) k_h5(const double* __restrict__ delta, const double* __restrict__ theta,
                      const double* __restrict__ rr, int K, int d, int B, int Bp, double nu, int m,
                      int32_t* __restrict__ kstar, double* __restrict__ agg, int32_t* k_trace,
                      double* sse_trace, int32_t* k_out, double* theta_out, double* sse_out) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= Bp) return;
-    if (b >= B) { kstar[b] = 0; return; }
-    int ks = 0;
-    double best = delta[b];
-    for (int k = 1; k < K; k++) {
-        double v = delta[(size_t)k * Bp + b];
-        if (v > best) { best = v; ks = k; }
+    __shared__ double sb[8][33];
+    __shared__ int sk[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.x * 32 + lane;
+    int ks = -1;
+    double best = 0.0;
+    for (int k = w; k < K; k += 8) {
+        const double v = delta[(size_t)k * Bp + b];
+        if (ks < 0 || v > best) { best = v; ks = k; }
     }
-    kstar[b] = ks;
-    const double sse = rr[b] - best;
-    if (agg)
-        for (int j = 0; j < d; j++)
-            agg[((size_t)b * K + ks) * d + j] += nu * theta[((size_t)ks * d + j) * Bp + b];
-    if (k_trace) k_trace[(size_t)m * B + b] = ks;
-    if (sse_trace) sse_trace[(size_t)m * B + b] = sse;
-    if (k_out) k_out[b] = ks;
-    if (sse_out) sse_out[b] = sse;
-    if (theta_out)
-        for (int j = 0; j < d; j++) theta_out[(size_t)b * d + j] = theta[((size_t)ks * d + j) * Bp + b];
+    sb[w][lane] = best;
+    sk[w][lane] = ks;
+    __syncthreads();
+    if (w == 0) {
+        for (int x = 1; x < 8; x++) {
+            const int kx = sk[x][lane];
+            const double vx = sb[x][lane];
+            if (kx >= 0 && (ks < 0 || vx > best || (vx == best && kx < ks))) { best = vx; ks = kx; }
+        }
+        if (b >= B) ks = 0;
+        sk[0][lane] = ks;
+        if (b < B) {
+            kstar[b] = ks;
+            const double sse = rr[b] - best;
+            if (k_trace) k_trace[(size_t)m * B + b] = ks;
+            if (sse_trace) sse_trace[(size_t)m * B + b] = sse;
+            if (k_out) k_out[b] = ks;
+            if (sse_out) sse_out[b] = sse;
+        } else {
+            kstar[b] = 0;
+        }
+    }
+    __syncthreads();
+    if (b >= B) return;
+    const int kb = sk[0][lane];
+    for (int j = w; j < d; j += 8) {
+        const double t = theta[((size_t)kb * d + j) * Bp + b];
+        if (agg) agg[((size_t)b * K + kb) * d + j] += nu * t;
+        if (theta_out) theta_out[(size_t)b * d + j] = t;
+    }
 }
 
 // nu * Zb_{k*} theta* at the design points, per (design point, replication)
@@ -385,14 +421,80 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
     }
 }
 
-__global__ void k_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n, int m,
-                     double* __restrict__ rr, double* risk_trace) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    double s = 0.0;
-    for (int q = 0; q < nblk; q++) s += part[(size_t)q * Bp + b];
-    rr[b] = s;
-    if (risk_trace) risk_trace[(size_t)m * B + b] = s / (2.0 * (double)n);
+// r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
+// q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
+// H6 with two replication columns per lane (64 per block, 16-byte accesses): the same rows per warp
+// (r0 + w + 8 j) and the same per-thread sums as k_h6, so the row-block partials are bitwise those of k_h6
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_h6w(double* __restrict__ Rt, int64_t n, int Bp,
+                                             const int32_t* __restrict__ kstar, const IdxT* __restrict__ idx,
+                                             const double* __restrict__ zhat, double* __restrict__ part) {
+    __shared__ double red[8][65];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 64 + 2 * lane;
+    const IdxT* ik0 = idx + (size_t)kstar[b] * n;
+    const IdxT* ik1 = idx + (size_t)kstar[b + 1] * n;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6;
+    const int64_t r1 = min(n, r0 + kRowsH6);
+    double a0 = 0.0, a1 = 0.0;
+    int64_t i = r0 + w;
+    for (; i + 24 < r1; i += 32) {  // four rows in flight per warp
+        double2 v[4];
+        uint32_t l0[4], l1[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            v[u] = *reinterpret_cast<const double2*>(Rt + (size_t)(i + 8 * u) * Bp + b);
+            l0[u] = ik0[i + 8 * u];
+            l1[u] = ik1[i + 8 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const double x = v[u].x - zhat[(size_t)l0[u] * Bp + b];
+            const double y = v[u].y - zhat[(size_t)l1[u] * Bp + b + 1];
+            *reinterpret_cast<double2*>(Rt + (size_t)(i + 8 * u) * Bp + b) = make_double2(x, y);
+            a0 += x * x;
+            a1 += y * y;
+        }
+    }
+    for (; i < r1; i += 8) {
+        const double2 v = *reinterpret_cast<const double2*>(Rt + (size_t)i * Bp + b);
+        const double x = v.x - zhat[(size_t)ik0[i] * Bp + b];
+        const double y = v.y - zhat[(size_t)ik1[i] * Bp + b + 1];
+        *reinterpret_cast<double2*>(Rt + (size_t)i * Bp + b) = make_double2(x, y);
+        a0 += x * x;
+        a1 += y * y;
+    }
+    red[w][2 * lane] = a0;
+    red[w][2 * lane + 1] = a1;
+    __syncthreads();
+    if (w < 2) {
+        const int c = w * 32 + lane;
+        double s = 0.0;
+        for (int q = 0; q < 8; q++) s += red[q][c];
+        part[(size_t)blockIdx.x * Bp + blockIdx.y * 64 + c] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n,
+                                            int m, double* __restrict__ rr, double* risk_trace) {
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.x * 32 + lane;
+    double s0 = 0.0, s1 = 0.0;
+    int q = w;
+    for (; q + 8 < nblk; q += 16) {
+        s0 += part[(size_t)q * Bp + b];
+        s1 += part[(size_t)(q + 8) * Bp + b];
+    }
+    if (q < nblk) s0 += part[(size_t)q * Bp + b];
+    red[w][lane] = s0 + s1;
+    __syncthreads();
+    if (w == 0 && b < B) {
+        double s = 0.0;
+        for (int x = 0; x < 8; x++) s += red[x][lane];
+        rr[b] = s;
+        if (risk_trace) risk_trace[(size_t)m * B + b] = s / (2.0 * (double)n);
+    }
 }
 
 // row sharding: f0[b] = (sum over all ranks' rows) / n, as k_center_fin mode 0
@@ -1362,7 +1464,7 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
         k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
                                                     c->Ainv, c->G, w.theta, w.delta);
     }
-    k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
+    k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
                                           agg, k_trace, sse_trace, k_out, theta_out, sse_out);
     c->launches += 2;
 }
@@ -1430,7 +1532,7 @@ static int find_best_narrow(cwb_ctx* c, const double* R, int32_t B, int32_t* k_o
     }
     k_h234<<<dim3(K, w.Bp / 32), 256, 0, s>>>(w.U, w.Bp, ns, c->d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
                                               w.delta);
-    k_h5<<<(w.Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, K, c->d, B, w.Bp, 0.0, 0, w.kstar, nullptr,
+    k_h5<<<w.Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, K, c->d, B, w.Bp, 0.0, 0, w.kstar, nullptr,
                                             nullptr, nullptr, k_out, theta_out, sse_out);
     c->launches += 2;
     return cwb_check_launch(c, "narrow find_best kernels");
@@ -1480,17 +1582,24 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
         dim3 g6(nblk, Bp / 32);
         if (c->nb) {
             cwb_nb_h6(c, w.Rt, Bp, w.kstar, w.theta, nu, kRowsH6, nblk, w.part, s);
-            k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+            k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
             c->launches += 1;
             continue;
         }
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
                                                                   c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
-        if (c->idx_bytes == 1)
+        if (Bp % 64 == 0) {
+            const dim3 g6w(nblk, Bp / 64);
+            if (c->idx_bytes == 1)
+                k_h6w<uint8_t><<<g6w, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
+            else
+                k_h6w<uint16_t><<<g6w, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
+        } else if (c->idx_bytes == 1) {
             k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-        else
+        } else {
             k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+        }
+        k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
         c->launches += 3;
         if (c->status) return c->status;  // e.g. a failed collective of learner sharding
     }
@@ -1608,7 +1717,7 @@ int cwb_train_folds_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_
                                                     fold_of_row, colfold);
         k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
                                                 w.delta, nullptr, nullptr, nullptr, 0, nullptr, 0, As, Gs, colfold);
-        k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, K, d, B, Bp, nu, m, w.kstar, theta_agg_out,
+        k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, K, d, B, Bp, nu, m, w.kstar, theta_agg_out,
                                               k_trace, sse_trace, nullptr, nullptr, nullptr);
         k_zhat<<<dim3((ns + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, ns, d, B, Bp, nu, B, nu,
                                                            w.zhat);
@@ -1671,7 +1780,7 @@ static int find_best_rows_iter(cwb_ctx* c, int32_t B, double nu, int m, double* 
     }
     k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
                                             w.delta, nullptr, nullptr, nullptr, 0, w.pack, 2);
-    k_h5<<<(Bp + 127) / 128, 128, 0, s>>>(w.delta, w.theta, rr_g, K, d, B, Bp, nu, m, w.kstar, agg, k_trace,
+    k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, rr_g, K, d, B, Bp, nu, m, w.kstar, agg, k_trace,
                                           sse_trace, k_out, theta_out, sse_out);
     c->launches += 2;
     return CWB_OK;
@@ -1731,7 +1840,7 @@ int cwb_train_rows(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
             k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
         else
             k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        k_rr<<<(B + 127) / 128, 128, 0, s>>>(w.part, nblk, B, Bp, c->n, m, rr_g, nullptr);  // local r^T r
+        k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, rr_g, nullptr);  // local r^T r
         c->launches += 3;
     }
     if (M > 0 && risk_trace) {  // the last iteration's risk needs one more sum

@@ -440,6 +440,41 @@ np.savez(sys.argv[1], **{k: v.cpu().numpy() for k, v in out.items()})
     assert np.abs(a["theta_agg"][same] - b["theta_agg"][same]).max() <= 1e-11 * np.abs(a["theta_agg"]).max()
 
 
+@pytest.mark.parametrize("name,B", [("R2", 128), ("R3", 128), ("R4", 64)])
+def test_wide_h1_bitwise_equals_one_column_per_lane(name, B):
+    # k_h1w / k_h6w (two replication columns per lane) add every bin sum and every row-block partial in exactly
+    # the order of k_h1 / k_h6: the general path's outputs are bitwise the same with CWB_H1_WIDE=0 and 1
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.getcwd())
+import cwb_synth as S
+from parity_util import gpu_cfg_of
+from paper_2110_03513_b200 import cwb
+ds = S.make(sys.argv[2], reps=range(int(sys.argv[3])))
+pg = cwb.Pool(torch.as_tensor(ds.X, device="cuda"), gpu_cfg_of(ds.cfg))
+pg.set_path(2)
+out = pg.train(torch.as_tensor(ds.Y, device="cuda"), nu=0.05, M=12)
+pg.status()
+torch.cuda.synchronize()
+np.savez(sys.argv[1], **{k: v.cpu().numpy() for k, v in out.items()})
+'''
+    res = []
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for mode in ("0", "1"):
+        path = f"/tmp/h1wide_{name}_{mode}.npz"
+        # one sweep in both runs (the row-chunked H1 adds chunk sums: another, equally valid, order)
+        env = dict(os.environ, CWB_H1_WIDE=mode, CWB_H1_CHUNKING="0",
+                   PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
+        subprocess.run([sys.executable, "-c", code, path, name, str(B)], check=True, env=env, cwd=root)
+        res.append(np.load(path))
+    a, b = res
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
+
+
 @pytest.mark.parametrize("name,reps", [("R1", range(64)), ("R2", range(0, 1024, 128))])
 def test_train_parity_fourth_root_bins(name, reps):
     # n* = ceil(n^(1/4)) (P:L445, the paper's second bin rule; n* < d leaves Z^T Z rank-deficient)
