@@ -423,6 +423,8 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
 
 // r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
 // q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
+// r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
+// q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
 // H6 with two replication columns per lane (64 per block, 16-byte accesses): the same rows per warp
 // (r0 + w + 8 j) and the same per-thread sums as k_h6, so the row-block partials are bitwise those of k_h6
 template <typename IdxT>
@@ -1588,17 +1590,10 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
         }
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
                                                                   c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
-        if (Bp % 64 == 0) {
-            const dim3 g6w(nblk, Bp / 64);
-            if (c->idx_bytes == 1)
-                k_h6w<uint8_t><<<g6w, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-            else
-                k_h6w<uint16_t><<<g6w, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        } else if (c->idx_bytes == 1) {
+        if (c->idx_bytes == 1)
             k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-        } else {
+        else
             k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        }
         k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
         c->launches += 3;
         if (c->status) return c->status;  // e.g. a failed collective of learner sharding

@@ -442,8 +442,8 @@ np.savez(sys.argv[1], **{k: v.cpu().numpy() for k, v in out.items()})
 
 @pytest.mark.parametrize("name,B", [("R2", 128), ("R3", 128), ("R4", 64)])
 def test_wide_h1_bitwise_equals_one_column_per_lane(name, B):
-    # k_h1w / k_h6w (two replication columns per lane) add every bin sum and every row-block partial in exactly
-    # the order of k_h1 / k_h6: the general path's outputs are bitwise the same with CWB_H1_WIDE=0 and 1
+    # k_h1w (two replication columns per lane) adds every bin sum in exactly the order of k_h1: the general
+    # path's outputs are bitwise the same with CWB_H1_WIDE=0 and 1
     import os
     import subprocess
     import sys
