@@ -423,60 +423,6 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
 
 // r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
 // q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
-// r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
-// q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
-// H6 with two replication columns per lane (64 per block, 16-byte accesses): the same rows per warp
-// (r0 + w + 8 j) and the same per-thread sums as k_h6, so the row-block partials are bitwise those of k_h6
-template <typename IdxT>
-__global__ void __launch_bounds__(256) k_h6w(double* __restrict__ Rt, int64_t n, int Bp,
-                                             const int32_t* __restrict__ kstar, const IdxT* __restrict__ idx,
-                                             const double* __restrict__ zhat, double* __restrict__ part) {
-    __shared__ double red[8][65];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int b = blockIdx.y * 64 + 2 * lane;
-    const IdxT* ik0 = idx + (size_t)kstar[b] * n;
-    const IdxT* ik1 = idx + (size_t)kstar[b + 1] * n;
-    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6;
-    const int64_t r1 = min(n, r0 + kRowsH6);
-    double a0 = 0.0, a1 = 0.0;
-    int64_t i = r0 + w;
-    for (; i + 24 < r1; i += 32) {  // four rows in flight per warp
-        double2 v[4];
-        uint32_t l0[4], l1[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            v[u] = *reinterpret_cast<const double2*>(Rt + (size_t)(i + 8 * u) * Bp + b);
-            l0[u] = ik0[i + 8 * u];
-            l1[u] = ik1[i + 8 * u];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const double x = v[u].x - zhat[(size_t)l0[u] * Bp + b];
-            const double y = v[u].y - zhat[(size_t)l1[u] * Bp + b + 1];
-            *reinterpret_cast<double2*>(Rt + (size_t)(i + 8 * u) * Bp + b) = make_double2(x, y);
-            a0 += x * x;
-            a1 += y * y;
-        }
-    }
-    for (; i < r1; i += 8) {
-        const double2 v = *reinterpret_cast<const double2*>(Rt + (size_t)i * Bp + b);
-        const double x = v.x - zhat[(size_t)ik0[i] * Bp + b];
-        const double y = v.y - zhat[(size_t)ik1[i] * Bp + b + 1];
-        *reinterpret_cast<double2*>(Rt + (size_t)i * Bp + b) = make_double2(x, y);
-        a0 += x * x;
-        a1 += y * y;
-    }
-    red[w][2 * lane] = a0;
-    red[w][2 * lane + 1] = a1;
-    __syncthreads();
-    if (w < 2) {
-        const int c = w * 32 + lane;
-        double s = 0.0;
-        for (int q = 0; q < 8; q++) s += red[q][c];
-        part[(size_t)blockIdx.x * Bp + blockIdx.y * 64 + c] = s;
-    }
-}
-
 __global__ void __launch_bounds__(256) k_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n,
                                             int m, double* __restrict__ rr, double* risk_trace) {
     __shared__ double red[8][33];
