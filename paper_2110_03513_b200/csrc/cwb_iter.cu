@@ -199,14 +199,19 @@ __global__ void k_h1c(const double* __restrict__ Rt, int64_t n, int Bp, int K, i
 // k_h1's order (bitwise the same U).  The bin's row ids are loaded 32 at a time, one per lane (coalesced),
 // and broadcast with a shuffle; the row address is one IMAD.WIDE (row * row stride + column base).
 // CHUNK: the rows of chunk c only (k_h1c's tables); U += the chunk sums (chunk 0 writes).
+// tri_d > 0 (the cross-Gram build): the columns are the K d basis columns of all learners and only the blocks
+// k' >= k of the symmetric cross Gram are needed -- a warp whose 64-column tile ends before learner k's own
+// columns (k tri_d) exits (the lower blocks are filled by symmetry afterwards)
 template <typename PermT, bool CHUNK>
 __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
                                              const int32_t* __restrict__ off, const uint32_t* __restrict__ ccnt,
-                                             int nch, int c, const PermT* __restrict__ perm, double* __restrict__ U) {
+                                             int nch, int c, const PermT* __restrict__ perm, double* __restrict__ U,
+                                             int tri_d = 0) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x * (blockDim.x >> 5) + w;
     if (g >= K * ns) return;
     const int k = g / ns, l = g - k * ns;
+    if (tri_d && (int)blockIdx.y * 64 + 64 <= k * tri_d) return;
     const int b = blockIdx.y * 64 + 2 * lane;
     uint32_t q, a1;
     if (CHUNK) {
@@ -1264,7 +1269,7 @@ static void launch_h1(const double* Rt, int64_t n, int Bp, int K, int ns, const 
 static constexpr int64_t kH1ChunkBytes = 40ll << 20;  // R4 sweep: 24 MB 934, 40 MB 913, 64 MB 921, 96 MB 985 ms/step
 
 static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_t* off,
-               const void* perm, int perm_bytes, double* U, cudaStream_t s) {
+               const void* perm, int perm_bytes, double* U, cudaStream_t s, int tri_d = 0) {
     const int64_t n = c->n;
     const bool wide = c->h1_wide && Bp % 64 == 0;
     const int64_t tile_row = wide ? 512 : 256;  // bytes of one row of the column tile a wave of warps gathers
@@ -1294,10 +1299,10 @@ static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_
                 dim3 gw(grid.x, Bp / 64);
                 if (perm_bytes == 2)
                     k_h1w<uint16_t, true><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, nullptr, c->h1c, nch, ch,
-                                                            (const uint16_t*)perm, U);
+                                                            (const uint16_t*)perm, U, tri_d);
                 else
                     k_h1w<uint32_t, true><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, nullptr, c->h1c, nch, ch,
-                                                            (const uint32_t*)perm, U);
+                                                            (const uint32_t*)perm, U, tri_d);
             } else if (perm_bytes == 2) {
                 k_h1c<uint16_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint16_t*)perm, U);
             } else {
@@ -1310,9 +1315,11 @@ static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_
     if (wide && (int64_t)K * ns < INT32_MAX) {
         dim3 gw((unsigned)(((int64_t)K * ns + 7) / 8), Bp / 64);
         if (perm_bytes == 2)
-            k_h1w<uint16_t, false><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, off, nullptr, 0, 0, (const uint16_t*)perm, U);
+            k_h1w<uint16_t, false><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, off, nullptr, 0, 0, (const uint16_t*)perm, U,
+                                                     tri_d);
         else
-            k_h1w<uint32_t, false><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, off, nullptr, 0, 0, (const uint32_t*)perm, U);
+            k_h1w<uint32_t, false><<<gw, 256, 0, s>>>(Rt, n, Bp, K, ns, off, nullptr, 0, 0, (const uint32_t*)perm, U,
+                                                     tri_d);
     } else if (perm_bytes == 2) {
         launch_h1<uint16_t>(Rt, n, Bp, K, ns, off, perm, U, s);
     } else {
@@ -2211,11 +2218,17 @@ __global__ void __launch_bounds__(256) k_gram_train(
 
 }  // namespace
 
+// lower blocks of the symmetric cross Gram from the upper ones: xg[(k,a)][(k',b)] = xg[(k',b)][(k,a)], k' < k
+__global__ void k_gram_sym(double* __restrict__ xg, int K, int d, int ld) {
+    const int row = blockIdx.x, k = row / d;  // row = k d + a
+    for (int q = threadIdx.x; q < k * d; q += blockDim.x) xg[(size_t)row * ld + q] = xg[(size_t)q * ld + row];
+}
+
 // builds the cross Gram of the pool's K learners and Wt = (A^-1 Z^T Z)^T rows once per pool (c->xg)
 static int gram_build(cwb_ctx* c, cudaStream_t s) {
     if (c->xg) return CWB_OK;
     const int K = c->K, d = c->d, ns = c->n_star;
-    const int ld = (K * d + 31) / 32 * 32;
+    const int ld = (K * d + 63) / 64 * 64;  // whole 64-column tiles: the wide H1
     const int64_t n = c->n;
     double *P = nullptr, *U = nullptr, *xg = nullptr, *Wt = nullptr;
     bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)n * ld, s) == cudaSuccess;
@@ -2231,11 +2244,12 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
         k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
     else
         k_gram_P<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
-    h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s);   // U_k[l][.] = sum over bin l of P rows
+    h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s, d);  // U_k[l][.] = sum over bin l of P rows, k' >= k
     k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, 0, xg, 1);  // projection Zb_k^T U_k
+    k_gram_sym<<<K * d, 256, 0, s>>>(xg, K, d, ld);
     k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
-    c->launches += 3;
+    c->launches += 4;
     cwb_release(P, s);
     cwb_release(U, s);
     cwb_release(xg, s);

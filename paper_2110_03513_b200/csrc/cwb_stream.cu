@@ -781,6 +781,11 @@ int cwb_find_best_stream(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out,
                                                     p.gtab, p.dest, p.isize, p.ibase, p.wst, p.part, rrp, c->d_status);
     const size_t fsm = sizeof(double) * ((((size_t)ns * B + 1) & ~(size_t)1) + (size_t)c->W * d + 2 * (size_t)d * d);
     CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_fit_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    static const int no_fit = getenv("CWB_STREAM_NOFIT") ? atoi(getenv("CWB_STREAM_NOFIT")) : 0;
+    if (no_fit) {  // timing experiment only (tools/findbest_timing.py): the stream kernel alone, outputs invalid
+        c->launches += 1;
+        return cwb_check_launch(c, "stream kernel");
+    }
     {   // launched as a programmatic dependent of k_h1_stream (prologue overlaps its tail)
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(K);
