@@ -426,6 +426,48 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
     }
 }
 
+// H6 with the column block's nu Zb_k* theta* table staged in shared memory (ns x 32 doubles, conflict-free
+// gathers: lane b reads column b of the row of its own bin), kRowsH6S rows per block so the staging is
+// amortised; warp w takes the rows r0 + w + 32 j, per-thread sums of squares, then the 32 warp sums in warp order.
+constexpr int kRowsH6S = 4096;
+template <typename IdxT>
+__global__ void __launch_bounds__(1024) k_h6s(double* __restrict__ Rt, int64_t n, int Bp, int ns,
+                                              const int32_t* __restrict__ kstar, const IdxT* __restrict__ idx,
+                                              const double* __restrict__ zhat, double* __restrict__ part) {
+    extern __shared__ double zs[];  // [ns][32]
+    __shared__ double red[32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    for (int e = threadIdx.x; e < ns * 32; e += blockDim.x) zs[e] = zhat[(size_t)(e >> 5) * Bp + blockIdx.y * 32 + (e & 31)];
+    const IdxT* ik = idx + (size_t)kstar[b] * n;
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6S;
+    const int64_t r1 = min(n, r0 + kRowsH6S);
+    double acc = 0.0;
+    int64_t i = r0 + w;
+    for (; i + 32 < r1; i += 64) {
+        const uint32_t l0 = ik[i], l1 = ik[i + 32];
+        const double v0 = Rt[(size_t)i * Bp + b] - zs[l0 * 32 + lane];
+        const double v1 = Rt[(size_t)(i + 32) * Bp + b] - zs[l1 * 32 + lane];
+        Rt[(size_t)i * Bp + b] = v0;
+        Rt[(size_t)(i + 32) * Bp + b] = v1;
+        acc += v0 * v0;
+        acc += v1 * v1;
+    }
+    if (i < r1) {
+        const double v0 = Rt[(size_t)i * Bp + b] - zs[(uint32_t)ik[i] * 32 + lane];
+        Rt[(size_t)i * Bp + b] = v0;
+        acc += v0 * v0;
+    }
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) {
+        double t = 0.0;
+        for (int q = 0; q < 32; q++) t += red[q][lane];
+        part[(size_t)blockIdx.x * Bp + b] = t;
+    }
+}
+
 // r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
 // q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
 __global__ void __launch_bounds__(256) k_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n,
@@ -1532,6 +1574,16 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
     k_zero<<<(unsigned)min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_agg_out, nagg);
     c->launches += 3;
     const int nblk = w.n_part;
+    // H6 with the staged nu Zb theta table (k_h6s) for n >= 32 row blocks of kRowsH6S; CWB_H6_STAGED=0: k_h6
+    static const bool h6s_env = !(getenv("CWB_H6_STAGED") && getenv("CWB_H6_STAGED")[0] == '0');
+    const bool h6s = h6s_env && c->n >= 32 * (int64_t)kRowsH6S;
+    if (h6s) {
+        const size_t zsm = sizeof(double) * 32 * (size_t)c->n_star;
+        if (zsm <= 160 * 1024) {
+            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_h6s<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
+            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_h6s<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
+        }
+    }
     for (int m = 0; m < M; m++) {
         find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
         dim3 g6(nblk, Bp / 32);
@@ -1543,11 +1595,23 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
         }
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
                                                                   c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
-        if (c->idx_bytes == 1)
-            k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-        else
-            k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+        const size_t zsm = sizeof(double) * 32 * (size_t)c->n_star;
+        if (h6s && zsm <= 160 * 1024) {  // staged table: large n, moderate n*
+            const int nb6 = (int)((c->n + kRowsH6S - 1) / kRowsH6S);
+            if (c->idx_bytes == 1)
+                k_h6s<uint8_t><<<dim3(nb6, Bp / 32), 1024, zsm, s>>>(w.Rt, c->n, Bp, c->n_star, w.kstar,
+                                                                    (const uint8_t*)c->idx, w.zhat, w.part);
+            else
+                k_h6s<uint16_t><<<dim3(nb6, Bp / 32), 1024, zsm, s>>>(w.Rt, c->n, Bp, c->n_star, w.kstar,
+                                                                     (const uint16_t*)c->idx, w.zhat, w.part);
+            k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nb6, B, Bp, c->n, m, w.rr, risk_trace);
+        } else {
+            if (c->idx_bytes == 1)
+                k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
+            else
+                k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
+            k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+        }
         c->launches += 3;
         if (c->status) return c->status;  // e.g. a failed collective of learner sharding
     }
@@ -2218,66 +2282,6 @@ __global__ void __launch_bounds__(256) k_gram_train(
 
 }  // namespace
 
-// Compact basis rows for the cross-Gram build: Pz[i][k][t] = the t-th non-zero of Zb_k[idx_k(i)] (t < 4),
-// Pj[i][k] = its first basis index j0 (the design point's knot span)
-template <typename IdxT>
-__global__ void k_gram_pc(const IdxT* __restrict__ idx, int64_t n, int K, int ns, const int32_t* __restrict__ zj0,
-                          const double* __restrict__ Zs, double4* __restrict__ Pz, uint8_t* __restrict__ Pj) {
-    const int64_t tot = n * K;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / K;
-        const int k = (int)(e - i * K);
-        const int l = (int)idx[(size_t)k * n + i];
-        const double* z = Zs + ((size_t)k * ns + l) * CWB_SPW;
-        Pz[e] = make_double4(z[0], z[1], z[2], z[3]);
-        Pj[e] = (uint8_t)zj0[(size_t)k * ns + l];
-    }
-}
-
-// U_k[l][k' d + b] = sum over the rows i of bin l of learner k of Zb_k'[idx_k'(i)][b], for k' >= k (the upper
-// blocks of the symmetric cross Gram): one warp per (k, l) accumulates the bin's row in shared memory -- lane
-// (k' offset, t) adds the t-th non-zero of learner k' at column k' d + j0 + t (distinct addresses within a
-// warp step: no races), rows in ascending order (the bin's row list, coalesced and shuffled as k_h1w) --
-// then writes it.  Work per (row, learner k): 4 (K - k) adds, against the dense gather's K d.
-template <typename PermT>
-__global__ void __launch_bounds__(128) k_gram_u(const double4* __restrict__ Pz, const uint8_t* __restrict__ Pj,
-                                                int K, int ns, int d, int ld, const int32_t* __restrict__ off,
-                                                const PermT* __restrict__ perm, int64_t n, double* __restrict__ U) {
-    extern __shared__ double gu[];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = blockIdx.x * (blockDim.x >> 5) + w;
-    if (g >= K * ns) return;  // warp-uniform
-    double* u = gu + (size_t)w * ld;
-    const int k = g / ns, l = g - k * ns;
-    const int c0 = k * d;  // first column this warp owns
-    for (int q = c0 + lane; q < ld; q += 32) u[q] = 0.0;
-    __syncwarp();
-    uint32_t q = (uint32_t)off[(size_t)k * (ns + 1) + l];
-    const uint32_t a1 = (uint32_t)off[(size_t)k * (ns + 1) + l + 1];
-    const PermT* pk = perm + (size_t)k * n;
-    const int kb = lane >> 2, t = lane & 3;  // 8 learners x 4 non-zeros per warp step
-    uint32_t mine = q + lane < a1 ? (uint32_t)pk[q + lane] : 0u;
-    for (; q < a1; q += 32) {
-        const int cnt = (int)min(32u, a1 - q);
-        const uint32_t nxt = q + 32 + lane < a1 ? (uint32_t)pk[q + 32 + lane] : 0u;
-        for (int j = 0; j < cnt; j++) {
-            const uint32_t i = __shfl_sync(0xffffffffu, mine, j);
-            const double* zr = reinterpret_cast<const double*>(Pz + (size_t)i * K);
-            const uint8_t* jr = Pj + (size_t)i * K;
-            for (int kp = k + kb; kp < K; kp += 8) {
-                const double v = __ldg(zr + (size_t)kp * 4 + t);
-                const int col = (int)__ldg(jr + kp) + t;
-                if (col < d) u[kp * d + col] += v;
-            }
-            __syncwarp();
-        }
-        mine = nxt;
-    }
-    __syncwarp();
-    double* ur = U + (size_t)g * ld;
-    for (int q2 = c0 + lane; q2 < ld; q2 += 32) ur[q2] = u[q2];
-}
-
 // lower blocks of the symmetric cross Gram from the upper ones: xg[(k,a)][(k',b)] = xg[(k',b)][(k,a)], k' < k
 __global__ void k_gram_sym(double* __restrict__ xg, int K, int d, int ld) {
     const int row = blockIdx.x, k = row / d;  // row = k d + a
@@ -2290,54 +2294,27 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
     const int K = c->K, d = c->d, ns = c->n_star;
     const int ld = (K * d + 63) / 64 * 64;  // whole 64-column tiles: the wide H1
     const int64_t n = c->n;
-    // compact (4 non-zeros + span) basis rows when one warp's shared-memory row fits, else the dense gather
-    static const int dense_env = getenv("CWB_GRAM_DENSE") ? atoi(getenv("CWB_GRAM_DENSE")) : 0;
-    const bool compact = !dense_env && (size_t)ld * sizeof(double) * 4 <= 160 * 1024 && d <= 255;
     double *P = nullptr, *U = nullptr, *xg = nullptr, *Wt = nullptr;
-    uint8_t* Pj = nullptr;
-    bool ok = compact ? cwb_alloc((void**)&P, sizeof(double) * 4 * (size_t)n * K, s) == cudaSuccess &&
-                        cwb_alloc((void**)&Pj, (size_t)n * K, s) == cudaSuccess
-                      : cwb_alloc((void**)&P, sizeof(double) * (size_t)n * ld, s) == cudaSuccess;
+    bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)n * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&U, sizeof(double) * (size_t)K * ns * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&Wt, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
     if (!ok) {
-        cwb_release(P, s); cwb_release(Pj, s); cwb_release(U, s); cwb_release(xg, s); cwb_release(Wt, s);
+        cwb_release(P, s); cwb_release(U, s); cwb_release(xg, s); cwb_release(Wt, s);
         return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
     }
-    if (compact) {
-        const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (n * K + 255) / 256);
-        if (c->idx_bytes == 1)
-            k_gram_pc<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, c->zj0, c->Zs, (double4*)P, Pj);
-        else
-            k_gram_pc<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, K, ns, c->zj0, c->Zs, (double4*)P, Pj);
-        const size_t sm = sizeof(double) * 4 * (size_t)ld;
-        const unsigned gb = (unsigned)(((int64_t)K * ns + 3) / 4);
-        if (c->perm_bytes == 2) {
-            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_gram_u<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_gram_u<uint16_t><<<gb, 128, sm, s>>>((const double4*)P, Pj, K, ns, d, ld, c->off, (const uint16_t*)c->perm,
-                                                   n, U);
-        } else {
-            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_gram_u<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_gram_u<uint32_t><<<gb, 128, sm, s>>>((const double4*)P, Pj, K, ns, d, ld, c->off, (const uint32_t*)c->perm,
-                                                   n, U);
-        }
-        c->launches += 2;
-    } else {
-        const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (n * ld + 255) / 256);
-        if (c->idx_bytes == 1)
-            k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
-        else
-            k_gram_P<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
-        h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s, d);  // U_k[l][.] = sum over bin l of P rows, k' >= k
-    }
+    const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (n * ld + 255) / 256);
+    if (c->idx_bytes == 1)
+        k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
+    else
+        k_gram_P<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
+    h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s, d);  // U_k[l][.] = sum over bin l of P rows, k' >= k
     k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, 0, xg, 1);  // projection Zb_k^T U_k
     k_gram_sym<<<K * d, 256, 0, s>>>(xg, K, d, ld);
     k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
-    c->launches += 3;
+    c->launches += 4;
     cwb_release(P, s);
-    cwb_release(Pj, s);
     cwb_release(U, s);
     cwb_release(xg, s);
     c->xg = Wt;

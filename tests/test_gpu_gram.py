@@ -118,35 +118,3 @@ def test_gram_edge_cases_and_errors():
         pg.status()
     assert e.value.name == "CWB_ENONFINITE"
 
-
-@pytest.mark.parametrize("name,B", [("R1", 64), ("R2", 64)])
-def test_gram_compact_build_equals_dense_build(name, B):
-    # the cross Gram from the compact basis rows (4 non-zeros + span per learner) adds the same non-zero terms in
-    # the same row order as the dense gather (whose extra terms are exact zeros): the same outputs bit for bit
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import os, sys, numpy as np, torch
-sys.path.insert(0, os.getcwd())
-import cwb_synth as S
-from parity_util import gpu_cfg_of
-from paper_2110_03513_b200 import cwb
-ds = S.make(sys.argv[2], reps=range(int(sys.argv[3])))
-pg = cwb.Pool(torch.as_tensor(ds.X, device="cuda"), gpu_cfg_of(ds.cfg))
-pg.set_path(3)
-out = pg.train(torch.as_tensor(ds.Y, device="cuda"), nu=0.05, M=50)
-pg.status()
-torch.cuda.synchronize()
-np.savez(sys.argv[1], **{k: v.cpu().numpy() for k, v in out.items()})
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = []
-    for mode in ("1", "0"):
-        path = f"/tmp/gram_dense_{name}_{mode}.npz"
-        env = dict(os.environ, CWB_GRAM_DENSE=mode, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]))
-        subprocess.run([sys.executable, "-c", code, path, name, str(B)], check=True, env=env, cwd=root)
-        res.append(np.load(path))
-    a, b = res
-    for k in a.files:
-        assert np.array_equal(a[k], b[k]), k
