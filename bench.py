@@ -333,13 +333,14 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
     t_m0 = min(ev(lambda: p.train(Y, nu=cfg.nu, M=0)) for _ in range(3))   # theta^[0] only
     t_mm = min(ev(lambda: p.train(Y, nu=cfg.nu, M=M)) for _ in range(3))
     p.status()
-    ld = (K * p.d + 31) // 32 * 32
+    p_d = p.d
     p.close()
     t_x = t_first0 - t_m0
     t_it = t_mm - t_m0
-    # dominant phase = the cross-Gram build: binMatVec of the K learners over the ld gathered basis columns
-    # (K n ld adds, the gather of 8 B per add from L2 as the direct path's H1)
-    adds_x = K * n * ld
+    # dominant phase = the cross-Gram build: binMatVec of learner k over the gathered basis columns of the
+    # 64-column tiles that hold learners k' >= k (the upper blocks of the symmetric Z^T Z), 8 B gathered per add
+    ld = (K * p_d + 63) // 64 * 64
+    adds_x = n * sum(ld - 64 * ((k * p_d) // 64) for k in range(K))
     dadd = float(peaks["dadd_tops"]) * 1e12
     l2 = float(peaks.get("l2_read_gbs", 0.0)) * 1e9
     return {"path": "cross-Gram (cwb_set_path 3): s_k -= nu Z_k^T Z_k* theta*, exact reformulation of Alg. 1 for "
@@ -352,8 +353,8 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
                          "bound": "alu", "adds": adds_x, "achieved": adds_x / (t_x * 1e-3) / 1e12,
                          "peak": dadd / 1e12, "unit": "Tadd/s", "frac": adds_x / (t_x * 1e-3) / dadd,
                          "l2_gather_frac": (8.0 * adds_x / (t_x * 1e-3) / l2) if l2 else None,
-                         "note": "time from the difference of a fresh and a cached pool (M = 0); the K d of "
-                                 f"{ld} columns are 1/6 non-zero (4 B-spline values per learner block)"}}
+                         "note": "time from the difference of a fresh and a cached pool (M = 0); of the "
+                                 f"{ld} gathered columns 1/6 are non-zero (4 B-spline values per learner block)"}}
 
 
 def workload_config(c, n_star, d):

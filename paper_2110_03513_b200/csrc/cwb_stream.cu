@@ -36,7 +36,10 @@
 
 namespace {
 
-constexpr int kC = 8176;        // rows per chunk: byte offsets of rows and pad rows (C..C+15) fit u16
+#ifndef CWB_STREAM_KC
+#define CWB_STREAM_KC 8176
+#endif
+constexpr int kC = CWB_STREAM_KC;  // rows per chunk: byte offsets of rows and pad rows (C..C+15) fit u16
 constexpr int kPad = 16;        // zero padding rows after the chunk
 constexpr int kUBudget = 6144;  // doubles of bin sums per CTA (48 KB): Ks * n* <= kUBudget
 constexpr int kStreamT = 1024;  // threads of the stream kernel (one CTA per SM)

@@ -73,6 +73,19 @@ def test_gram_r3_full_launch():
     pg.close()
 
 
+@pytest.mark.slow
+def test_gram_r4_full_launch():
+    # the R4 launch (B = 64, n = 1,000,000, K = 84, n* = 1000), replications 0-3, all 200 iterations
+    ds, pg, g = gram_train("R4")
+    c = ds.cfg
+    reps = [0, 1, 2, 3]
+    sub = {k: (v[:, reps] if v.ndim == 2 and k != "theta_agg" else v[reps]) for k, v in g.items()}
+    po = O.Pool(ds.X, cfg_of(c), O.MODE_BINNED)
+    fol = follow_parity(sub, po, ds.Y[reps], c.nu, c.M, "R4 gram B=64", threads=len(reps))
+    assert fol.sum() <= 2
+    pg.close()
+
+
 def test_gram_equals_direct_path_and_deterministic():
     ds = S.make("R1", reps=range(64))
     c = ds.cfg
