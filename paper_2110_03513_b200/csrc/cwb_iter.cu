@@ -2345,6 +2345,13 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
 int cwb_train_gram(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M, double* offset_out,
                    double* theta_agg_out, int32_t* k_trace, double* sse_trace, double* risk_trace, cudaStream_t s) {
     const int K = c->K, d = c->d;
+    {   // k_gram_train keeps theta of every learner (K d doubles) and delta (K) of its replication in shared memory
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (sizeof(double) * ((size_t)K * d + K) + 1024 > (size_t)optin)
+            return cwb_set_error(c, CWB_EUNSUPPORTED, "cwb_train (path 3): K d too large for the cross-Gram kernel");
+    }
     int rc = gram_build(c, s);
     if (rc) return rc;
     rc = ensure_ws(c, B, s);
