@@ -14,3 +14,5 @@ BENCH_ALLOW_SHORT=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-con
 python tools/launches_summary.py gpurun_out/${TAG}_launches_R3.csv > gpurun_out/${TAG}_launches_R3_summary.txt 2>&1
 timeout 300 python tools/prof_iter.py R3 1 > gpurun_out/${TAG}_prof_plain.log 2>&1 && timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_h1w -s 2 -c 1 -o gpurun_out/${TAG}_h1w python tools/prof_iter.py R3 1 > gpurun_out/${TAG}_ncu.log 2>&1
 python tools/ncu_brief.py gpurun_out/${TAG}_h1w.ncu-rep > gpurun_out/${TAG}_ncu_h1w_R3.txt 2>&1
+# DRAM bytes of the H1 phase of one R3 iteration (its row-chunk launches), for roofline.traffic (profiles/traffic.json)
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_h1w -c 6 --csv --log-file gpurun_out/${TAG}_h1w_traffic.csv python tools/prof_iter.py R3 1 > /dev/null 2>&1
