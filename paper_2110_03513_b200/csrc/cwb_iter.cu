@@ -202,20 +202,7 @@ __global__ void k_h1c(const double* __restrict__ Rt, int64_t n, int Bp, int K, i
 // tri_d > 0 (the cross-Gram build): the columns are the K d basis columns of all learners and only the blocks
 // k' >= k of the symmetric cross Gram are needed -- a warp whose 64-column tile ends before learner k's own
 // columns (k tri_d) exits (the lower blocks are filled by symmetry afterwards)
-// residual-row loads of the wide H1: 0 = ld.global.nc (L1 allocate), 1 = ld.global.cg (L2 only),
-// 2 = ld.global.nc.L1::no_allocate (CWB_H1_LD selects; an A/B switch)
-template <int LDM>
-__device__ __forceinline__ double2 ld_row(const double2* p) {
-    if (LDM == 1) return __ldcg(p);
-    if (LDM == 2) {
-        double2 v;
-        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-        return v;
-    }
-    return __ldg(p);
-}
-
-template <typename PermT, bool CHUNK, int LDM = 0>
+template <typename PermT, bool CHUNK>
 __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
                                              const int32_t* __restrict__ off, const uint32_t* __restrict__ ccnt,
                                              int nch, int c, const PermT* __restrict__ perm, double* __restrict__ U,
@@ -251,23 +238,23 @@ __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int6
             for (int u = 0; u < 8; u++) ii[u] = __shfl_sync(0xffffffffu, mine, j + u);
             double2 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) v[u] = ld_row<LDM>((const double2*)(base + (unsigned long long)ii[u] * stride));
+            for (int u = 0; u < 8; u++) v[u] = __ldg((const double2*)(base + (unsigned long long)ii[u] * stride));
 #pragma unroll
             for (int u = 0; u < 8; u++) { ax += v[u].x; ay += v[u].y; }
         }
         for (; j + 4 <= cnt; j += 4) {
             const uint32_t i0 = __shfl_sync(0xffffffffu, mine, j), i1 = __shfl_sync(0xffffffffu, mine, j + 1);
             const uint32_t i2 = __shfl_sync(0xffffffffu, mine, j + 2), i3 = __shfl_sync(0xffffffffu, mine, j + 3);
-            const double2 v0 = ld_row<LDM>((const double2*)(base + (unsigned long long)i0 * stride));
-            const double2 v1 = ld_row<LDM>((const double2*)(base + (unsigned long long)i1 * stride));
-            const double2 v2 = ld_row<LDM>((const double2*)(base + (unsigned long long)i2 * stride));
-            const double2 v3 = ld_row<LDM>((const double2*)(base + (unsigned long long)i3 * stride));
+            const double2 v0 = __ldg((const double2*)(base + (unsigned long long)i0 * stride));
+            const double2 v1 = __ldg((const double2*)(base + (unsigned long long)i1 * stride));
+            const double2 v2 = __ldg((const double2*)(base + (unsigned long long)i2 * stride));
+            const double2 v3 = __ldg((const double2*)(base + (unsigned long long)i3 * stride));
             ax += v0.x; ay += v0.y; ax += v1.x; ay += v1.y;
             ax += v2.x; ay += v2.y; ax += v3.x; ay += v3.y;
         }
         for (; j < cnt; j++) {
             const uint32_t i0 = __shfl_sync(0xffffffffu, mine, j);
-            const double2 v0 = ld_row<LDM>((const double2*)(base + (unsigned long long)i0 * stride));
+            const double2 v0 = __ldg((const double2*)(base + (unsigned long long)i0 * stride));
             ax += v0.x; ay += v0.y;
         }
         mine = nxt;
@@ -1323,26 +1310,19 @@ static void launch_h1(const double* Rt, int64_t n, int Bp, int K, int ns, const 
 // rows per chunk of the chunked H1: a 32-column tile of one chunk (rows x 256 B) well inside L2
 static constexpr int64_t kH1ChunkBytes = 40ll << 20;  // R4 sweep: 24 MB 934, 40 MB 913, 64 MB 921, 96 MB 985 ms/step
 
-#define H1W_ONE(CH, LDM, GRID, OFF, CC, NCH, CHI)                                                              \
-    do {                                                                                                   \
-        if (perm_bytes == 2)                                                                               \
-            k_h1w<uint16_t, CH, LDM><<<GRID, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,             \
-                                                          (const uint16_t*)perm, U, tri_d);                \
-        else                                                                                               \
-            k_h1w<uint32_t, CH, LDM><<<GRID, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,             \
-                                                          (const uint32_t*)perm, U, tri_d);                \
-    } while (0)
 #define H1W_LAUNCH(CH, GRID, OFF, CC, NCH, CHI)                                                            \
     do {                                                                                                   \
-        if (h1_ld == 1) H1W_ONE(CH, 1, GRID, OFF, CC, NCH, CHI);                                           \
-        else if (h1_ld == 2) H1W_ONE(CH, 2, GRID, OFF, CC, NCH, CHI);                                      \
-        else H1W_ONE(CH, 0, GRID, OFF, CC, NCH, CHI);                                                      \
+        if (perm_bytes == 2)                                                                               \
+            k_h1w<uint16_t, CH><<<GRID, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,                  \
+                                                     (const uint16_t*)perm, U, tri_d);                     \
+        else                                                                                               \
+            k_h1w<uint32_t, CH><<<GRID, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,                  \
+                                                     (const uint32_t*)perm, U, tri_d);                     \
     } while (0)
 
 static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_t* off,
                const void* perm, int perm_bytes, double* U, cudaStream_t s, int tri_d = 0) {
     const int64_t n = c->n;
-    static const int h1_ld = getenv("CWB_H1_LD") ? atoi(getenv("CWB_H1_LD")) : 0;
     const bool wide = c->h1_wide && Bp % 64 == 0;
     const int64_t tile_row = wide ? 512 : 256;  // bytes of one row of the column tile a wave of warps gathers
     const bool chunked = n * tile_row > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off;
