@@ -327,7 +327,6 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
         ts.append(ev(step))
     ms = float(np.mean(ts))
     p = cwb.Pool(X, gcfg)
-    t_init = ev(lambda: None)
     p.set_path(3)
     t_first0 = ev(lambda: p.train(Y, nu=cfg.nu, M=0))          # cross Gram + W + theta^[0]
     t_m0 = min(ev(lambda: p.train(Y, nu=cfg.nu, M=0)) for _ in range(3))   # theta^[0] only
