@@ -378,6 +378,54 @@ __global__ void __launch_bounds__(256) k_h5(const double* __restrict__ delta, co
     }
 }
 
+// H2-H4 for one learner and 32 replications with the learner's bin sums staged in shared memory first
+// (u[ns][32], dynamic): every bin sum is read from global memory once instead of once per basis window it
+// falls in (4x for cubic B-splines).  Same arithmetic and order as k_h234 (plain mode): bitwise equal.
+__global__ void __launch_bounds__(256) k_h234s(const double* __restrict__ U, int Bp, int ns, int d,
+                                               const int32_t* __restrict__ zj0, const double* __restrict__ Zs,
+                                               const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
+                                               const double* __restrict__ G, double* __restrict__ theta,
+                                               double* __restrict__ delta) {
+    extern __shared__ double us[];  // [ns][32]
+    __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
+    const int k = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int b = blockIdx.y * 32 + lane;
+    const int32_t* j0 = zj0 + (size_t)k * ns;
+    const double* zs = Zs + (size_t)k * ns * CWB_SPW;
+    const double* u = U + (size_t)k * ns * Bp + blockIdx.y * 32;
+    for (int l = w; l < ns; l += nw) us[l * 32 + lane] = u[(size_t)l * Bp + lane];
+    __syncthreads();
+    for (int j = w; j < d; j += nw) {
+        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+        double s = 0.0;
+        for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * us[l * 32 + lane];
+        S[j][lane] = s;
+    }
+    __syncthreads();
+    const double* Ai = Ainv + (size_t)k * d * d;
+    for (int j = w; j < d; j += nw) {
+        double t = 0.0;
+        for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][lane];
+        Th[j][lane] = t;
+        theta[((size_t)k * d + j) * Bp + b] = t;
+    }
+    __syncthreads();
+    const double* Gk = G + (size_t)k * d * d;
+    for (int j = w; j < d; j += nw) {
+        double gt = 0.0;
+        for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++)
+            gt += Gk[j * d + jp] * Th[jp][lane];
+        V[j][lane] = Th[j][lane] * (2.0 * S[j][lane] - gt);
+    }
+    __syncthreads();
+    if (w == 0) {
+        double v = 0.0;
+        for (int j = 0; j < d; j++) v += V[j][lane];
+        delta[(size_t)k * Bp + b] = v;
+    }
+}
+
 // nu * Zb_{k*} theta* at the design points, per (design point, replication)
 // columns b < B_nu are scaled by nu, columns B_nu <= b < B by nu2
 __global__ void k_zhat(const int32_t* __restrict__ kstar, const double* __restrict__ theta,
@@ -1458,8 +1506,19 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
         if (ev) cudaEventRecord(ev[0], s);
         h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
         if (ev) cudaEventRecord(ev[1], s);
-        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
-                                                    c->Ainv, c->G, w.theta, w.delta);
+        const size_t usm = sizeof(double) * 32 * (size_t)c->n_star;
+        if (usm <= 160 * 1024 && c->n_star >= 64) {  // bin sums staged once per block (large n* only)
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_h234s, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+                attr = true;
+            }
+            k_h234s<<<dim3(c->K, Bp / 32), 256, usm, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
+                                                           c->Ainv, c->G, w.theta, w.delta);
+        } else {
+            k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
+                                                        c->Ainv, c->G, w.theta, w.delta);
+        }
     }
     k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
                                           agg, k_trace, sse_trace, k_out, theta_out, sse_out);

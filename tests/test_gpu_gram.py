@@ -131,3 +131,33 @@ def test_gram_edge_cases_and_errors():
         pg.status()
     assert e.value.name == "CWB_ENONFINITE"
 
+
+
+@pytest.mark.slow
+def test_gram_equals_direct_path_r3_all_replications():
+    # every replication of the R3 bench launch (B = 512, 200 iterations): the cross-Gram path and the direct
+    # per-iteration path (itself oracle-checked on replications 0-7, 255, 511) select the same learners except
+    # where the two runs' SSE gap is a tie within 1e-12; traces and parameters agree to rounding
+    ds = S.make("R3")
+    c = ds.cfg
+    gc = gpu_cfg_of(c)
+    gc.batch_hint = c.B
+    pg = cwb.Pool(dev(ds.X), gc)
+    res = {}
+    for p in (2, 3):
+        pg.set_path(p)
+        out = pg.train(dev(ds.Y), nu=c.nu, M=c.M)
+        pg.status()
+        res[p] = {k: v.cpu().numpy() for k, v in out.items()}
+    a, b = res[2], res[3]
+    same = (a["k_trace"] == b["k_trace"]).all(0)
+    print(f"[parity] R3 gram vs direct: {int(same.sum())} of {c.B} replications identical over {c.M} iterations")
+    for r in np.nonzero(~same)[0]:   # a divergence must start at a near tie of the direct run's SSEs
+        m = int(np.nonzero(a["k_trace"][:, r] != b["k_trace"][:, r])[0][0])
+        assert abs(a["sse_trace"][m, r] - b["sse_trace"][m, r]) <= 1e-12 * abs(a["sse_trace"][m, r]) * 10, (r, m)
+    assert same.mean() >= 0.99
+    ok, e = close(b["theta_agg"][same], a["theta_agg"][same], 1e-9, scale=np.abs(a["theta_agg"]).max())
+    assert ok, e
+    ok, e = close(b["risk_trace"][:, same], a["risk_trace"][:, same], 1e-10)
+    assert ok, e
+    pg.close()
