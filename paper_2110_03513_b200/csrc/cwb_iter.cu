@@ -378,54 +378,6 @@ __global__ void __launch_bounds__(256) k_h5(const double* __restrict__ delta, co
     }
 }
 
-// H2-H4 for one learner and 32 replications with the learner's bin sums staged in shared memory first
-// (u[ns][32], dynamic): every bin sum is read from global memory once instead of once per basis window it
-// falls in (4x for cubic B-splines).  Same arithmetic and order as k_h234 (plain mode): bitwise equal.
-__global__ void __launch_bounds__(256) k_h234s(const double* __restrict__ U, int Bp, int ns, int d,
-                                               const int32_t* __restrict__ zj0, const double* __restrict__ Zs,
-                                               const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
-                                               const double* __restrict__ G, double* __restrict__ theta,
-                                               double* __restrict__ delta) {
-    extern __shared__ double us[];  // [ns][32]
-    __shared__ double S[CWB_MAX_D][33], Th[CWB_MAX_D][33], V[CWB_MAX_D][33];
-    const int k = blockIdx.x;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int b = blockIdx.y * 32 + lane;
-    const int32_t* j0 = zj0 + (size_t)k * ns;
-    const double* zs = Zs + (size_t)k * ns * CWB_SPW;
-    const double* u = U + (size_t)k * ns * Bp + blockIdx.y * 32;
-    for (int l = w; l < ns; l += nw) us[l * 32 + lane] = u[(size_t)l * Bp + lane];
-    __syncthreads();
-    for (int j = w; j < d; j += nw) {
-        const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
-        double s = 0.0;
-        for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * us[l * 32 + lane];
-        S[j][lane] = s;
-    }
-    __syncthreads();
-    const double* Ai = Ainv + (size_t)k * d * d;
-    for (int j = w; j < d; j += nw) {
-        double t = 0.0;
-        for (int jp = 0; jp < d; jp++) t += Ai[j * d + jp] * S[jp][lane];
-        Th[j][lane] = t;
-        theta[((size_t)k * d + j) * Bp + b] = t;
-    }
-    __syncthreads();
-    const double* Gk = G + (size_t)k * d * d;
-    for (int j = w; j < d; j += nw) {
-        double gt = 0.0;
-        for (int jp = max(0, j - (CWB_SPW - 1)); jp <= min(d - 1, j + CWB_SPW - 1); jp++)
-            gt += Gk[j * d + jp] * Th[jp][lane];
-        V[j][lane] = Th[j][lane] * (2.0 * S[j][lane] - gt);
-    }
-    __syncthreads();
-    if (w == 0) {
-        double v = 0.0;
-        for (int j = 0; j < d; j++) v += V[j][lane];
-        delta[(size_t)k * Bp + b] = v;
-    }
-}
-
 // nu * Zb_{k*} theta* at the design points, per (design point, replication)
 // columns b < B_nu are scaled by nu, columns B_nu <= b < B by nu2
 __global__ void k_zhat(const int32_t* __restrict__ kstar, const double* __restrict__ theta,
@@ -471,48 +423,6 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
         double s = 0.0;
         for (int q = 0; q < 8; q++) s += red[q][lane];
         part[(size_t)blockIdx.x * Bp + b] = s;
-    }
-}
-
-// H6 with the column block's nu Zb_k* theta* table staged in shared memory (ns x 32 doubles, conflict-free
-// gathers: lane b reads column b of the row of its own bin), kRowsH6S rows per block so the staging is
-// amortised; warp w takes the rows r0 + w + 32 j, per-thread sums of squares, then the 32 warp sums in warp order.
-constexpr int kRowsH6S = 4096;
-template <typename IdxT>
-__global__ void __launch_bounds__(1024) k_h6s(double* __restrict__ Rt, int64_t n, int Bp, int ns,
-                                              const int32_t* __restrict__ kstar, const IdxT* __restrict__ idx,
-                                              const double* __restrict__ zhat, double* __restrict__ part) {
-    extern __shared__ double zs[];  // [ns][32]
-    __shared__ double red[32][33];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int b = blockIdx.y * 32 + lane;
-    for (int e = threadIdx.x; e < ns * 32; e += blockDim.x) zs[e] = zhat[(size_t)(e >> 5) * Bp + blockIdx.y * 32 + (e & 31)];
-    const IdxT* ik = idx + (size_t)kstar[b] * n;
-    __syncthreads();
-    const int64_t r0 = (int64_t)blockIdx.x * kRowsH6S;
-    const int64_t r1 = min(n, r0 + kRowsH6S);
-    double acc = 0.0;
-    int64_t i = r0 + w;
-    for (; i + 32 < r1; i += 64) {
-        const uint32_t l0 = ik[i], l1 = ik[i + 32];
-        const double v0 = Rt[(size_t)i * Bp + b] - zs[l0 * 32 + lane];
-        const double v1 = Rt[(size_t)(i + 32) * Bp + b] - zs[l1 * 32 + lane];
-        Rt[(size_t)i * Bp + b] = v0;
-        Rt[(size_t)(i + 32) * Bp + b] = v1;
-        acc += v0 * v0;
-        acc += v1 * v1;
-    }
-    if (i < r1) {
-        const double v0 = Rt[(size_t)i * Bp + b] - zs[(uint32_t)ik[i] * 32 + lane];
-        Rt[(size_t)i * Bp + b] = v0;
-        acc += v0 * v0;
-    }
-    red[w][lane] = acc;
-    __syncthreads();
-    if (w == 0) {
-        double t = 0.0;
-        for (int q = 0; q < 32; q++) t += red[q][lane];
-        part[(size_t)blockIdx.x * Bp + b] = t;
     }
 }
 
@@ -1506,19 +1416,8 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
         if (ev) cudaEventRecord(ev[0], s);
         h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
         if (ev) cudaEventRecord(ev[1], s);
-        const size_t usm = sizeof(double) * 32 * (size_t)c->n_star;
-        if (usm <= 160 * 1024 && c->n_star >= 64) {  // bin sums staged once per block (large n* only)
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_h234s, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-                attr = true;
-            }
-            k_h234s<<<dim3(c->K, Bp / 32), 256, usm, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
-                                                           c->Ainv, c->G, w.theta, w.delta);
-        } else {
-            k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
-                                                        c->Ainv, c->G, w.theta, w.delta);
-        }
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
+                                                    c->Ainv, c->G, w.theta, w.delta);
     }
     k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
                                           agg, k_trace, sse_trace, k_out, theta_out, sse_out);
@@ -1633,16 +1532,6 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
     k_zero<<<(unsigned)min((size_t)1184, (nagg + 255) / 256 + 1), 256, 0, s>>>(theta_agg_out, nagg);
     c->launches += 3;
     const int nblk = w.n_part;
-    // H6 with the staged nu Zb theta table (k_h6s) for n >= 32 row blocks of kRowsH6S; CWB_H6_STAGED=0: k_h6
-    static const bool h6s_env = !(getenv("CWB_H6_STAGED") && getenv("CWB_H6_STAGED")[0] == '0');
-    const bool h6s = h6s_env && c->n >= 32 * (int64_t)kRowsH6S;
-    if (h6s) {
-        const size_t zsm = sizeof(double) * 32 * (size_t)c->n_star;
-        if (zsm <= 160 * 1024) {
-            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_h6s<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
-            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_h6s<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm));
-        }
-    }
     for (int m = 0; m < M; m++) {
         find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
         dim3 g6(nblk, Bp / 32);
@@ -1654,23 +1543,11 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
         }
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
                                                                   c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
-        const size_t zsm = sizeof(double) * 32 * (size_t)c->n_star;
-        if (h6s && zsm <= 160 * 1024) {  // staged table: large n, moderate n*
-            const int nb6 = (int)((c->n + kRowsH6S - 1) / kRowsH6S);
-            if (c->idx_bytes == 1)
-                k_h6s<uint8_t><<<dim3(nb6, Bp / 32), 1024, zsm, s>>>(w.Rt, c->n, Bp, c->n_star, w.kstar,
-                                                                    (const uint8_t*)c->idx, w.zhat, w.part);
-            else
-                k_h6s<uint16_t><<<dim3(nb6, Bp / 32), 1024, zsm, s>>>(w.Rt, c->n, Bp, c->n_star, w.kstar,
-                                                                     (const uint16_t*)c->idx, w.zhat, w.part);
-            k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nb6, B, Bp, c->n, m, w.rr, risk_trace);
-        } else {
-            if (c->idx_bytes == 1)
-                k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-            else
-                k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-            k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
-        }
+        if (c->idx_bytes == 1)
+            k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
+        else
+            k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
+        k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
         c->launches += 3;
         if (c->status) return c->status;  // e.g. a failed collective of learner sharding
     }
