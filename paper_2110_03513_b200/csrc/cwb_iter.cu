@@ -2239,7 +2239,7 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
         cwb_release(P, s); cwb_release(U, s); cwb_release(xg, s); cwb_release(Wt, s);
         return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
     }
-    const unsigned g = (unsigned)std::min<int64_t>(148 * 16, (n * ld + 255) / 256);
+    const unsigned g = (unsigned)std::min<int64_t>((int64_t)cwb_num_sms() * 16, (n * ld + 255) / 256);
     if (c->idx_bytes == 1)
         k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
     else
