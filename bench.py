@@ -113,7 +113,7 @@ def sec8d_roofline(K, n, B, n_star, peaks, kernel_s, units, what, bytes_extra=0)
     if bound == "hbm":
         achieved, peak, unit = bytes_alg / kernel_s / 1e9, hbm / 1e9, "GB/s"
     else:
-        achieved, peak, unit = adds_alg / kernel_s / 1e12, dadd / 1e12, "Tadd/s"
+        achieved, peak, unit = adds_alg / kernel_s / 1e12, dadd / 1e12, "TFLOP/s"  # one fp64 add = one flop
     return {"bound": bound, "kernel": what, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": max(t_hbm, t_dadd) / kernel_s,
             "terms": {"bytes_alg": bytes_alg, "adds_alg": adds_alg, "t_hbm_ms": t_hbm * 1e3,
@@ -350,7 +350,7 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
                           "iteration_us": t_it / max(M, 1) * 1e3},
             "roofline": {"kernel": "cross-Gram build (H1 + H2 over the gathered basis columns of all learners)",
                          "bound": "alu", "adds": adds_x, "achieved": adds_x / (t_x * 1e-3) / 1e12,
-                         "peak": dadd / 1e12, "unit": "Tadd/s", "frac": adds_x / (t_x * 1e-3) / dadd,
+                         "peak": dadd / 1e12, "unit": "TFLOP/s", "frac": adds_x / (t_x * 1e-3) / dadd,
                          "l2_gather_frac": (8.0 * adds_x / (t_x * 1e-3) / l2) if l2 else None,
                          "note": "time from the difference of a fresh and a cached pool (M = 0); of the "
                                  f"{ld} gathered columns 1/6 are non-zero (4 B-spline values per learner block)"}}
