@@ -1278,43 +1278,62 @@ static constexpr int64_t kH1ChunkBytes = 40ll << 20;  // R4 sweep: 24 MB 934, 40
                                                      (const uint32_t*)perm, U, tri_d);                     \
     } while (0)
 
+// Row chunking of the general-path H1: when a column tile of the gathered matrix (n rows x tile_row bytes) exceeds
+// L2, the bins are swept in row chunks of kH1ChunkBytes (per (learner, chunk, bin) row counts and starts, built
+// once per pool and chunk size).  Returns the rows per chunk (0: one sweep) and sets *nch_out.
+static int64_t h1_chunk_plan(cwb_ctx* c, int64_t tile_row, const int32_t* off, int K, int ns, int* nch_out,
+                             cudaStream_t s) {
+    const int64_t n = c->n;
+    *nch_out = 1;
+    if (!(n * tile_row > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off)) return 0;
+    static const int64_t chunk_bytes =
+        getenv("CWB_H1_CHUNK_MB") ? (int64_t)atoi(getenv("CWB_H1_CHUNK_MB")) << 20 : kH1ChunkBytes;
+    const int64_t CR = chunk_bytes / tile_row;
+    const int nch = (int)((n + CR - 1) / CR);
+    if (!c->h1c || c->h1c_nch != nch) {  // per (learner, chunk, bin) row counts and starts, once per pool
+        cwb_release(c->h1c, s);
+        c->h1c = nullptr;
+        if (cwb_alloc((void**)&c->h1c, 2 * sizeof(uint32_t) * (size_t)K * nch * ns, s) != cudaSuccess) {
+            cwb_set_error(c, CWB_ENOMEM, "chunked H1 tables");
+            return -1;
+        }
+        c->h1c_nch = nch;
+        k_h1_chunk_count<<<dim3(nch, K), 1024, sizeof(uint32_t) * ns, s>>>(c->idx, c->idx_bytes, n, ns, CR, nch,
+                                                                         c->h1c);
+        k_h1_chunk_start<<<(unsigned)(((int64_t)K * ns + 255) / 256), 256, 0, s>>>(c->h1c, c->off, K, ns, nch);
+        c->launches += 2;
+    }
+    *nch_out = nch;
+    return CR;
+}
+
+// one row chunk ch of the chunked H1 (U += the chunk's bin sums; chunk 0 writes)
+static void h1_chunk(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const void* perm, int perm_bytes,
+                     double* U, int nch, int ch, cudaStream_t s, int tri_d = 0) {
+    const int64_t n = c->n;
+    const int wpb = 8;
+    dim3 grid((unsigned)(((int64_t)K * ns + wpb - 1) / wpb), Bp / 32);
+    if (c->h1_wide && Bp % 64 == 0) {
+        dim3 gw(grid.x, Bp / 64);
+        H1W_LAUNCH(true, gw, nullptr, c->h1c, nch, ch);
+    } else if (perm_bytes == 2) {
+        k_h1c<uint16_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint16_t*)perm, U);
+    } else {
+        k_h1c<uint32_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint32_t*)perm, U);
+    }
+    c->launches++;
+}
+
 static void h1(cwb_ctx* c, const double* Rt, int Bp, int K, int ns, const int32_t* off,
                const void* perm, int perm_bytes, double* U, cudaStream_t s, int tri_d = 0) {
     const int64_t n = c->n;
     const bool wide = c->h1_wide && Bp % 64 == 0;
     const int64_t tile_row = wide ? 512 : 256;  // bytes of one row of the column tile a wave of warps gathers
-    const bool chunked = n * tile_row > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off;
-    if (chunked) {
-        static const int64_t chunk_bytes =
-            getenv("CWB_H1_CHUNK_MB") ? (int64_t)atoi(getenv("CWB_H1_CHUNK_MB")) << 20 : kH1ChunkBytes;
-        const int64_t CR = chunk_bytes / tile_row;
-        const int nch = (int)((n + CR - 1) / CR);
-        if (!c->h1c || c->h1c_nch != nch) {  // per (learner, chunk, bin) row counts and starts, once per pool
-            cwb_release(c->h1c, s);
-            c->h1c = nullptr;
-            if (cwb_alloc((void**)&c->h1c, 2 * sizeof(uint32_t) * (size_t)K * nch * ns, s) != cudaSuccess) {
-                cwb_set_error(c, CWB_ENOMEM, "chunked H1 tables");
-                return;
-            }
-            c->h1c_nch = nch;
-            k_h1_chunk_count<<<dim3(nch, K), 1024, sizeof(uint32_t) * ns, s>>>(c->idx, c->idx_bytes, n, ns, CR, nch,
-                                                                             c->h1c);
-            k_h1_chunk_start<<<(unsigned)(((int64_t)K * ns + 255) / 256), 256, 0, s>>>(c->h1c, c->off, K, ns, nch);
-            c->launches += 2;
-        }
-        const int wpb = 8;
-        dim3 grid((unsigned)(((int64_t)K * ns + wpb - 1) / wpb), Bp / 32);
-        for (int ch = 0; ch < nch; ch++) {
-            if (wide) {
-                dim3 gw(grid.x, Bp / 64);
-                H1W_LAUNCH(true, gw, nullptr, c->h1c, nch, ch);
-            } else if (perm_bytes == 2) {
-                k_h1c<uint16_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint16_t*)perm, U);
-            } else {
-                k_h1c<uint32_t><<<grid, wpb * 32, 0, s>>>(Rt, n, Bp, K, ns, nch, ch, c->h1c, (const uint32_t*)perm, U);
-            }
-        }
-        c->launches += nch;
+    int nch = 1;
+    const int64_t CR = h1_chunk_plan(c, tile_row, off, K, ns, &nch, s);
+    if (CR < 0) return;
+    if (CR > 0) {
+        for (int ch = 0; ch < nch; ch++) h1_chunk(c, Rt, Bp, K, ns, perm, perm_bytes, U, nch, ch, s, tri_d);
         return;
     }
     if (wide && (int64_t)K * ns < INT32_MAX) {
@@ -2085,13 +2104,14 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
 // projection on the K d "columns" of P.
 namespace {
 
-// P[i][k d + a] = Zb_k[idx_k(i)][a] (4 non-zeros per learner block; columns >= K d are 0)
+// P[i - r0][k d + a] = Zb_k[idx_k(i)][a] for the rows i in [r0, r1) (4 non-zeros per learner block; columns
+// >= K d are 0)
 template <typename IdxT>
-__global__ void k_gram_P(const IdxT* __restrict__ idx, int64_t n, int K, int ns, int d, int ld,
+__global__ void k_gram_P(const IdxT* __restrict__ idx, int64_t n, int64_t r0, int64_t r1, int K, int ns, int d, int ld,
                          const int32_t* __restrict__ zj0, const double* __restrict__ Zs, double* __restrict__ P) {
-    const int64_t tot = n * ld;
+    const int64_t tot = (r1 - r0) * ld;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / ld;
+        const int64_t i = r0 + e / ld;
         const int col = (int)(e - i * ld);
         double v = 0.0;
         if (col < K * d) {
@@ -2230,8 +2250,13 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
     const int K = c->K, d = c->d, ns = c->n_star;
     const int ld = (K * d + 63) / 64 * 64;  // whole 64-column tiles: the wide H1
     const int64_t n = c->n;
+    // the gathered basis P is built one H1 row chunk at a time (n x ld would be 16 GB at R4)
+    int nch = 1;
+    const int64_t CR = h1_chunk_plan(c, c->h1_wide ? 512 : 256, c->off, K, ns, &nch, s);
+    if (CR < 0) return c->status ? c->status : CWB_ENOMEM;
+    const int64_t prow = CR > 0 ? CR : n;
     double *P = nullptr, *U = nullptr, *xg = nullptr, *Wt = nullptr;
-    bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)n * ld, s) == cudaSuccess;
+    bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)prow * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&U, sizeof(double) * (size_t)K * ns * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&Wt, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
@@ -2239,17 +2264,24 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
         cwb_release(P, s); cwb_release(U, s); cwb_release(xg, s); cwb_release(Wt, s);
         return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
     }
-    const unsigned g = (unsigned)std::min<int64_t>((int64_t)cwb_num_sms() * 16, (n * ld + 255) / 256);
-    if (c->idx_bytes == 1)
-        k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
-    else
-        k_gram_P<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, K, ns, d, ld, c->zj0, c->Zs, P);
-    h1(c, P, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s, d);  // U_k[l][.] = sum over bin l of P rows, k' >= k
+    for (int ch = 0; ch < nch; ch++) {
+        const int64_t r0 = (int64_t)ch * prow, r1 = std::min(n, r0 + prow);
+        const unsigned g = (unsigned)std::min<int64_t>((int64_t)cwb_num_sms() * 16, ((r1 - r0) * ld + 255) / 256);
+        if (c->idx_bytes == 1)
+            k_gram_P<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)c->idx, n, r0, r1, K, ns, d, ld, c->zj0, c->Zs, P);
+        else
+            k_gram_P<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)c->idx, n, r0, r1, K, ns, d, ld, c->zj0, c->Zs, P);
+        c->launches++;
+        // U_k[l][.] = sum over bin l of P rows (k' >= k); the kernels index rows globally: P's base shifted by r0
+        const double* Pv = P - r0 * (int64_t)ld;
+        if (CR > 0) h1_chunk(c, Pv, ld, K, ns, c->perm, c->perm_bytes, U, nch, ch, s, d);
+        else h1(c, Pv, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s, d);
+    }
     k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, 0, xg, 1);  // projection Zb_k^T U_k
     k_gram_sym<<<K * d, 256, 0, s>>>(xg, K, d, ld);
     k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
-    c->launches += 4;
+    c->launches += 3;
     cwb_release(P, s);
     cwb_release(U, s);
     cwb_release(xg, s);
