@@ -2111,8 +2111,8 @@ __global__ void k_gram_P(const IdxT* __restrict__ idx, int64_t n, int64_t r0, in
                          const int32_t* __restrict__ zj0, const double* __restrict__ Zs, double* __restrict__ P) {
     const int64_t tot = (r1 - r0) * ld;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = r0 + e / ld;
-        const int col = (int)(e - i * ld);
+        const int64_t il = e / ld, i = r0 + il;
+        const int col = (int)(e - il * ld);
         double v = 0.0;
         if (col < K * d) {
             const int k = col / d, a = col - k * d;
