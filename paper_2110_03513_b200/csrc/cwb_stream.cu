@@ -41,7 +41,7 @@ namespace {
 #endif
 constexpr int kC = CWB_STREAM_KC;  // rows per chunk: byte offsets of rows and pad rows (C..C+15) fit u16
 constexpr int kPad = 16;        // zero padding rows after the chunk
-constexpr int kUBudget = 6144;  // doubles of bin sums per CTA (48 KB): Ks * n* <= kUBudget
+constexpr int kUBudget = 7168;  // doubles of bin sums per CTA (56 KB): Ks * n* <= kUBudget
 constexpr int kStreamT = 1024;  // threads of the stream kernel (one CTA per SM)
 constexpr int kNWK = kStreamT / 32;  // kernel warps: the plan deals groups to them
 constexpr int kStage = 4;        // entry blocks per register stage (two stages in flight per warp)
@@ -649,9 +649,18 @@ static int stream_plan(cwb_ctx* c, cudaStream_t s) {
     const int K = c->K, ns = c->n_star;
     const int64_t n = c->n;
     if (ns > kUBudget) return CWB_EUNSUPPORTED;  // <= kMaxG groups of 32 tasks per item
-    // learner group size: bin sums within the shared-memory budget, and at least one item per SM
+    // learner group size Ks: bin sums within the shared-memory budget; among those, the one with the smallest
+    // makespan estimate: the CTAs take contiguous item ranges, so the busiest CTA runs ceil(items / SMs) items of
+    // Ks learners each plus a fixed per-item cost (chunk staging, barrier; ~3 learners' worth), larger Ks on ties
     const int nch0 = (int)((n + kC - 1) / kC);
-    const int Ks = std::max(1, std::min<int>(std::min(K, kUBudget / ns), (int)((int64_t)K * nch0 / cwb_num_sms())));
+    const int nsm = cwb_num_sms();
+    int Ks = 1;
+    int64_t best = INT64_MAX;
+    for (int ks = 1; ks <= std::min(K, kUBudget / ns); ks++) {
+        const int64_t items = (int64_t)((K + ks - 1) / ks) * nch0;
+        const int64_t cost = ((items + nsm - 1) / nsm) * (ks + 3);
+        if (cost <= best) { best = cost; Ks = ks; }
+    }
     if ((int64_t)Ks * ns > 0xfffe) return CWB_EUNSUPPORTED;
     const int nch = (int)((n + kC - 1) / kC), nlg = (K + Ks - 1) / Ks, nitems = nlg * nch;
     int NTP = 32;
