@@ -263,6 +263,57 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def r1_rung(devname, peaks, steps=20, warmup=5):
+    """The R1 rung (n = 1,331, K = 10, B = 256, M = 200: the latency-bound rung, one persistent k_train_fused
+    launch per cwb_train) measured like the headline step (fresh pool per step, L2 flushed between steps, CUDA
+    events), with the SURVEY 8(d) roofline of its kernel -- an extra key of the default line."""
+    import torch
+    from paper_2110_03513_b200 import cwb
+    c = S.CONFIGS["R1"]
+    ds = S.make(c)
+    X = torch.as_tensor(ds.X, device=devname)
+    Y = torch.as_tensor(ds.Y, device=devname)
+    cfg = cwb.Config(n_star_rule=c.n_star_rule, n_star_fixed=c.n_star_fixed, n_knots=c.n_knots, degree=c.degree,
+                     df=c.df, batch_hint=c.B)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=devname)
+
+    def ev(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    def step():
+        p = cwb.Pool(X, cfg)
+        p.train(Y, nu=c.nu, M=c.M)
+        p.close()
+    for _ in range(warmup):
+        step()
+    ts = []
+    for i in range(steps):
+        flush.fill_(i & 255)
+        ts.append(ev(step))
+    p = cwb.Pool(X, cfg)
+    p.train(Y, nu=c.nu, M=c.M)
+    ks = []
+    for i in range(10):
+        flush.fill_(i & 255)
+        l0 = p.launches()
+        ks.append(ev(lambda: p.train(Y, nu=c.nu, M=c.M)))
+        nl = p.launches() - l0
+    p.status()
+    n_star = p.n_star
+    p.close()
+    ms, kms = float(np.mean(ts)), float(np.mean(ks))
+    roof = sec8d_roofline(c.K, c.n, c.B, n_star, peaks, kms * 1e-3, c.M, "k_train_fused", bytes_extra=c.n * c.B * 8)
+    return {"workload": "R1", "ms_per_step": ms, "value": c.K * c.n * c.B * c.M / (ms * 1e-3), "unit": UNIT,
+            "iters_per_s": c.M / (ms * 1e-3), "kernel_ms": kms, "launches_per_call": int(nl),
+            "roofline": {k: roof[k] for k in ("bound", "kernel", "achieved", "peak", "unit", "frac", "terms")}}
+
+
 def findbest_b1(devname, peaks, name="R3", calls=15):
     """SURVEY Sec. 8(d) target: one findBestBaselearner (cwb_find_best) on ONE residual column at R3
     (u16 index vectors) against the HBM roofline of its algorithmic bytes K*n*2 + n*8.  L2 is flushed
@@ -666,6 +717,11 @@ def main():
             "gpu_launches": int(sum(launches)),
         }
         if args.algo == "cwb" and not strong and not args.unbinned and ws == 1 and not args.no_findbest:
+            if cfg.name != "R1":
+                try:
+                    line["r1"] = r1_rung(devname, peaks)
+                except Exception as e:
+                    line["r1"] = {"error": str(e)}
             for fb_cfg in ("R3", "R4"):
                 try:  # after the timed region: does not touch the step measurement
                     line[f"findbest_b1_{fb_cfg}"] = findbest_b1(devname, peaks, fb_cfg)
