@@ -294,7 +294,18 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
         } else {
             const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
             s = 0.0;
-            for (int l = lb; l < le; l++) s += zs[l * CWB_SPW + (j - j0[l])] * u[(size_t)l * Bp];
+            int l = lb;
+            for (; l + 4 <= le; l += 4) {  // four bins' loads in flight, the sum in the same order
+                double zq[4], uq[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    zq[q] = zs[(l + q) * CWB_SPW + (j - j0[l + q])];
+                    uq[q] = u[(size_t)(l + q) * Bp];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; q++) s = fma(zq[q], uq[q], s);
+            }
+            for (; l < le; l++) s = fma(zs[l * CWB_SPW + (j - j0[l])], u[(size_t)l * Bp], s);
             if (smode == 1) Sg[((size_t)k * d + j) * Bp + b] = s;
         }
         S[j][lane] = s;
@@ -412,7 +423,23 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
     const int64_t r0 = (int64_t)blockIdx.x * kRowsH6;
     const int64_t r1 = min(n, r0 + kRowsH6);
     double acc = 0.0;
-    for (int64_t i = r0 + w; i < r1; i += 8) {
+    int64_t i = r0 + w;
+    for (; i + 24 < r1; i += 32) {  // four rows in flight (the idx -> zhat gathers are dependent loads)
+        uint32_t l[4];
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            l[u] = ik[i + 8 * u];
+            x[u] = Rt[(size_t)(i + 8 * u) * Bp + b];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const double v = x[u] - zhat[(size_t)l[u] * Bp + b];
+            Rt[(size_t)(i + 8 * u) * Bp + b] = v;
+            acc += v * v;
+        }
+    }
+    for (; i < r1; i += 8) {
         double v = Rt[(size_t)i * Bp + b] - zhat[(size_t)ik[i] * Bp + b];
         Rt[(size_t)i * Bp + b] = v;
         acc += v * v;
