@@ -2251,11 +2251,17 @@ __global__ void __launch_bounds__(256) k_gram_train(
             for (int q = tid; q < Kd; q += blockDim.x) {
                 double u0 = 0.0, u1 = 0.0;
                 int bb = 0;
-                for (; bb + 1 < d; bb += 2) {
-                    u0 += wr[(size_t)bb * ld + q] * s_ts[bb];
-                    u1 += wr[(size_t)(bb + 1) * ld + q] * s_ts[bb + 1];
+                for (; bb + 8 <= d; bb += 8) {  // eight row loads of W^T in flight
+                    double w8[8];
+#pragma unroll
+                    for (int x = 0; x < 8; x++) w8[x] = __ldg(wr + (size_t)(bb + x) * ld + q);
+#pragma unroll
+                    for (int x = 0; x < 8; x += 2) {
+                        u0 = fma(w8[x], s_ts[bb + x], u0);
+                        u1 = fma(w8[x + 1], s_ts[bb + x + 1], u1);
+                    }
                 }
-                if (bb < d) u0 += wr[(size_t)bb * ld + q] * s_ts[bb];
+                for (; bb < d; bb++) u0 = fma(__ldg(wr + (size_t)bb * ld + q), s_ts[bb], u0);
                 th[q] -= nu * (u0 + u1);
             }
         }
