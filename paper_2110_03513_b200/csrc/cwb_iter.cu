@@ -202,69 +202,6 @@ __global__ void k_h1c(const double* __restrict__ Rt, int64_t n, int Bp, int K, i
 // tri_d > 0 (the cross-Gram build): the columns are the K d basis columns of all learners and only the blocks
 // k' >= k of the symmetric cross Gram are needed -- a warp whose 64-column tile ends before learner k's own
 // columns (k tri_d) exits (the lower blocks are filled by symmetry afterwards)
-// H1 with four replication columns per lane (128 per warp) and one 256-bit gather per row and lane
-// (ld.global.nc.v4.f64, LDG.E.256 on sm_100a); the same per-column order as k_h1w / k_h1.  CWB_H1_X4=1 (A/B).
-template <typename PermT, bool CHUNK>
-__global__ void __launch_bounds__(256) k_h1x(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
-                                             const int32_t* __restrict__ off, const uint32_t* __restrict__ ccnt,
-                                             int nch, int c, const PermT* __restrict__ perm, double* __restrict__ U,
-                                             int tri_d = 0) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = blockIdx.x * (blockDim.x >> 5) + w;
-    if (g >= K * ns) return;
-    const int k = g / ns, l = g - k * ns;
-    if (tri_d && (int)blockIdx.y * 128 + 128 <= k * tri_d) return;
-    const int b = blockIdx.y * 128 + 4 * lane;
-    uint32_t q, a1;
-    if (CHUNK) {
-        const size_t e = ((size_t)k * nch + c) * ns + l;
-        q = ccnt[(size_t)K * nch * ns + e];
-        a1 = q + ccnt[e];
-    } else {
-        q = (uint32_t)off[(size_t)k * (ns + 1) + l];
-        a1 = (uint32_t)off[(size_t)k * (ns + 1) + l + 1];
-    }
-    const PermT* pk = perm + (size_t)k * n;
-    const unsigned long long base = (unsigned long long)(Rt + b);
-    const uint32_t stride = (uint32_t)Bp * 8u;
-    double a0 = 0.0, a1c = 0.0, a2 = 0.0, a3 = 0.0;
-    uint32_t mine = q + lane < a1 ? (uint32_t)pk[q + lane] : 0u;
-    for (; q < a1; q += 32) {
-        const int cnt = (int)min(32u, a1 - q);
-        const uint32_t nxt = q + 32 + lane < a1 ? (uint32_t)pk[q + 32 + lane] : 0u;
-        int j = 0;
-        for (; j + 4 <= cnt; j += 4) {
-            double v[4][4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t i = __shfl_sync(0xffffffffu, mine, j + u);
-                const double* rp = (const double*)(base + (unsigned long long)i * stride);
-                asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-                             : "=d"(v[u][0]), "=d"(v[u][1]), "=d"(v[u][2]), "=d"(v[u][3]) : "l"(rp));
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) { a0 += v[u][0]; a1c += v[u][1]; a2 += v[u][2]; a3 += v[u][3]; }
-        }
-        for (; j < cnt; j++) {
-            const uint32_t i = __shfl_sync(0xffffffffu, mine, j);
-            const double* rp = (const double*)(base + (unsigned long long)i * stride);
-            double x0, x1, x2, x3;
-            asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3) : "l"(rp));
-            a0 += x0; a1c += x1; a2 += x2; a3 += x3;
-        }
-        mine = nxt;
-    }
-    double2* up = reinterpret_cast<double2*>(U + (size_t)g * Bp + b);
-    if (CHUNK && c != 0) {
-        const double2 o0 = up[0], o1 = up[1];
-        up[0] = make_double2(o0.x + a0, o0.y + a1c);
-        up[1] = make_double2(o1.x + a2, o1.y + a3);
-    } else {
-        up[0] = make_double2(a0, a1c);
-        up[1] = make_double2(a2, a3);
-    }
-}
-
 template <typename PermT, bool CHUNK>
 __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int64_t n, int Bp, int K, int ns,
                                              const int32_t* __restrict__ off, const uint32_t* __restrict__ ccnt,
@@ -1360,22 +1297,13 @@ static constexpr int64_t kH1ChunkBytes = 40ll << 20;  // R4 sweep: 24 MB 934, 40
 
 #define H1W_LAUNCH(CH, GRID, OFF, CC, NCH, CHI)                                                            \
     do {                                                                                                   \
-        if (h1x4 && Bp % 128 == 0) {                                                                       \
-            dim3 gx(GRID.x, Bp / 128);                                                                     \
-            if (perm_bytes == 2)                                                                           \
-                k_h1x<uint16_t, CH><<<gx, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,                \
-                                                       (const uint16_t*)perm, U, tri_d);                   \
-            else                                                                                           \
-                k_h1x<uint32_t, CH><<<gx, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,                \
-                                                       (const uint32_t*)perm, U, tri_d);                   \
-        } else if (perm_bytes == 2)                                                                        \
+        if (perm_bytes == 2)                                                                               \
             k_h1w<uint16_t, CH><<<GRID, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,                  \
                                                      (const uint16_t*)perm, U, tri_d);                     \
         else                                                                                               \
             k_h1w<uint32_t, CH><<<GRID, 256, 0, s>>>(Rt, n, Bp, K, ns, OFF, CC, NCH, CHI,                  \
                                                      (const uint32_t*)perm, U, tri_d);                     \
     } while (0)
-static const bool h1x4 = getenv("CWB_H1_X4") && getenv("CWB_H1_X4")[0] == '1';
 
 // Row chunking of the general-path H1: when a column tile of the gathered matrix (n rows x tile_row bytes) exceeds
 // L2, the bins are swept in row chunks of kH1ChunkBytes (per (learner, chunk, bin) row counts and starts, built
