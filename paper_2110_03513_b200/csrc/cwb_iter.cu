@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <numeric>
 
 #include "cwb_internal.cuh"
 
@@ -295,7 +296,19 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
             const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
             s = 0.0;
             int l = lb;
-            for (; l + 4 <= le; l += 4) {  // four bins' loads in flight, the sum in the same order
+            // sixteen bins' loads in flight (the window is ~4 n* / (n_knots + 1) bins: ~85 at R3), the FMA
+            // chain in bin order as before (bitwise the same s)
+            for (; l + 16 <= le; l += 16) {
+                double zq[16], uq[16];
+#pragma unroll
+                for (int q = 0; q < 16; q++) {
+                    zq[q] = zs[(l + q) * CWB_SPW + (j - j0[l + q])];
+                    uq[q] = u[(size_t)(l + q) * Bp];
+                }
+#pragma unroll
+                for (int q = 0; q < 16; q++) s = fma(zq[q], uq[q], s);
+            }
+            for (; l + 4 <= le; l += 4) {
                 double zq[4], uq[4];
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
@@ -453,25 +466,95 @@ __global__ void k_h6(double* __restrict__ Rt, int64_t n, int Bp, const int32_t* 
     }
 }
 
-// r^T r of every column from the row-block partials: block (32 columns, 8 warps), warp w adds the blocks
-// q = w, w + 8, ... in ascending order, then the 8 warp sums in warp order (fixed order: deterministic)
-__global__ void __launch_bounds__(256) k_rr(const double* __restrict__ part, int nblk, int B, int Bp, int64_t n,
-                                            int m, double* __restrict__ rr, double* risk_trace) {
-    __shared__ double red[8][33];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int b = blockIdx.x * 32 + lane;
-    double s0 = 0.0, s1 = 0.0;
-    int q = w;
-    for (; q + 8 < nblk; q += 16) {
-        s0 += part[(size_t)q * Bp + b];
-        s1 += part[(size_t)(q + 8) * Bp + b];
+// H6 with the block's CB columns of zhat staged in shared memory ([ns][CB]): k_h6's zhat gathers (a
+// different design-point row per replication) made the L1 the busiest unit (79 %, DRAM 58 %, ncu R3).  Here
+// the 16 lanes of a half-warp read 16 distinct columns of the staged table (conflict-free) and the residual
+// rows stream at HBM rate.  One 1024-thread block per SM; a warp-step covers 32 / CB rows, eight steps in
+// flight; r^T r partials per block in fixed order (rows ascending per thread, warps ascending, then the row
+// halves of a column for CB = 16).
+constexpr int kH6sThreads = 1024;
+template <typename IdxT, int CB>
+__global__ void __launch_bounds__(kH6sThreads, 1) k_h6s(double* __restrict__ Rt, int64_t n, int Bp,
+                                                       const int32_t* __restrict__ kstar,
+                                                       const IdxT* __restrict__ idx, const double* __restrict__ zhat,
+                                                       int ns, int64_t rpb, double* __restrict__ part) {
+    extern __shared__ double zs[];
+    __shared__ double red[kH6sThreads / 32][33];
+    constexpr int RW = 32 / CB, U = 8;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int cc = lane % CB, rs = lane / CB;
+    const int b = blockIdx.y * CB + cc;
+    for (int e = tid; e < ns * CB; e += kH6sThreads) {
+        const int l = e / CB;
+        zs[e] = zhat[(size_t)l * Bp + blockIdx.y * CB + (e - l * CB)];
     }
-    if (q < nblk) s0 += part[(size_t)q * Bp + b];
-    red[w][lane] = s0 + s1;
+    const IdxT* ik = idx + (size_t)kstar[b] * n;
+    const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(n, r0 + rpb);
+    const int64_t stride = (int64_t)(kH6sThreads / 32) * RW;  // rows per block-step
+    __syncthreads();
+    double acc = 0.0;
+    int64_t i = r0 + w * RW + rs;
+    for (; i + (U - 1) * stride < r1; i += U * stride) {
+        uint32_t l[U];
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            l[u] = ik[i + u * stride];
+            x[u] = Rt[(size_t)(i + u * stride) * Bp + b];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const double v = x[u] - zs[l[u] * CB + cc];
+            Rt[(size_t)(i + u * stride) * Bp + b] = v;
+            acc += v * v;
+        }
+    }
+    for (; i < r1; i += stride) {
+        const double v = Rt[(size_t)i * Bp + b] - zs[(uint32_t)ik[i] * CB + cc];
+        Rt[(size_t)i * Bp + b] = v;
+        acc += v * v;
+    }
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) {
+        double t = 0.0;
+        for (int q = 0; q < kH6sThreads / 32; q++) t += red[q][lane];
+        if (CB == 16) t += __shfl_down_sync(0xffffffffu, t, 16);  // row half 1 of column cc after half 0
+        if (lane < CB) part[(size_t)blockIdx.x * Bp + b] = t;
+    }
+}
+
+// r^T r of every column from the row-block partials: block (32 columns, 32 warps), warp w adds the blocks
+// q = w + 32 (8 t + u) into accumulator u (eight loads in flight), the eight accumulators in u order, then the
+// 32 warp sums in warp order (fixed order: deterministic)
+constexpr int kRrThreads = 1024;
+__global__ void __launch_bounds__(kRrThreads, 1) k_rr(const double* __restrict__ part, int nblk, int B, int Bp,
+                                                   int64_t n, int m, double* __restrict__ rr, double* risk_trace) {
+    __shared__ double red[kRrThreads / 32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = kRrThreads / 32;
+    const int b = blockIdx.x * 32 + lane;
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) a[u] = 0.0;
+    int q = w;
+    for (; q + 7 * nw < nblk; q += 8 * nw) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = part[(size_t)(q + u * nw) * Bp + b];
+#pragma unroll
+        for (int u = 0; u < 8; u++) a[u] += v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+        if (q + u * nw < nblk) a[u] += part[(size_t)(q + u * nw) * Bp + b];
+    double t = a[0];
+#pragma unroll
+    for (int u = 1; u < 8; u++) t += a[u];
+    red[w][lane] = t;
     __syncthreads();
     if (w == 0 && b < B) {
         double s = 0.0;
-        for (int x = 0; x < 8; x++) s += red[x][lane];
+        for (int x = 0; x < nw; x++) s += red[x][lane];
         rr[b] = s;
         if (risk_trace) risk_trace[(size_t)m * B + b] = s / (2.0 * (double)n);
     }
@@ -1562,6 +1645,44 @@ int cwb_find_best_general(cwb_ctx* c, const double* R, int32_t B, int32_t* k_out
     return cwb_check_launch(c, "find_best kernels");
 }
 
+// H6 launch: k_h6s when a block's zhat columns fit in shared memory (CB = 32, else 16), else k_h6.  The grid
+// has X row blocks per column block with X * (Bp / CB) a multiple of the SM count (whole waves of one block per
+// SM).  Returns the number of row-block partials written to part (k_rr's nblk).  CWB_H6=0 forces k_h6 (A/B).
+template <typename IdxT>
+static int launch_h6_t(cwb_ctx* c, double* Rt, int Bp, const int32_t* kstar, const double* zhat, double* part,
+                       int nblk_max, cudaStream_t s) {
+    static const int mode = getenv("CWB_H6") ? atoi(getenv("CWB_H6")) : 1;
+    const int ns = c->n_star;
+    int cb = 0;
+    if (mode && (size_t)ns * 32 * sizeof(double) <= 160 * 1024) cb = 32;
+    else if (mode && (size_t)ns * 16 * sizeof(double) <= 160 * 1024) cb = 16;
+    if (cb) {
+        const int Y = Bp / cb, nsm = cwb_num_sms();
+        const int X = std::max(1, std::min(nblk_max, nsm / std::gcd(nsm, Y)));
+        const int64_t rpb = (c->n + X - 1) / X;
+        const size_t smem = sizeof(double) * (size_t)ns * cb;
+        if (cb == 32) {
+            static bool attr = false;
+            if (!attr) { cudaFuncSetAttribute(k_h6s<IdxT, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); attr = true; }
+            k_h6s<IdxT, 32><<<dim3(X, Y), kH6sThreads, smem, s>>>(Rt, c->n, Bp, kstar, (const IdxT*)c->idx, zhat, ns,
+                                                                 rpb, part);
+        } else {
+            static bool attr = false;
+            if (!attr) { cudaFuncSetAttribute(k_h6s<IdxT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); attr = true; }
+            k_h6s<IdxT, 16><<<dim3(X, Y), kH6sThreads, smem, s>>>(Rt, c->n, Bp, kstar, (const IdxT*)c->idx, zhat, ns,
+                                                                 rpb, part);
+        }
+        return X;
+    }
+    k_h6<IdxT><<<dim3(nblk_max, Bp / 32), 256, 0, s>>>(Rt, c->n, Bp, kstar, (const IdxT*)c->idx, zhat, part);
+    return nblk_max;
+}
+static int launch_h6(cwb_ctx* c, double* Rt, int Bp, const int32_t* kstar, const double* zhat, double* part,
+                     int nblk_max, cudaStream_t s) {
+    return c->idx_bytes == 1 ? launch_h6_t<uint8_t>(c, Rt, Bp, kstar, zhat, part, nblk_max, s)
+                             : launch_h6_t<uint16_t>(c, Rt, Bp, kstar, zhat, part, nblk_max, s);
+}
+
 int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
                       double* offset_out, double* theta_agg_out, int32_t* k_trace,
                       double* sse_trace, double* risk_trace, cudaStream_t s) {
@@ -1580,20 +1701,16 @@ int cwb_train_general(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t
     const int nblk = w.n_part;
     for (int m = 0; m < M; m++) {
         find_best_iter(c, B, nu, m, theta_agg_out, k_trace, sse_trace, nullptr, nullptr, nullptr, s);
-        dim3 g6(nblk, Bp / 32);
         if (c->nb) {
             cwb_nb_h6(c, w.Rt, Bp, w.kstar, w.theta, nu, kRowsH6, nblk, w.part, s);
-            k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+            k_rr<<<Bp / 32, kRrThreads, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
             c->launches += 1;
             continue;
         }
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs,
                                                                   c->n_star, c->d, B, Bp, nu, B, nu, w.zhat);
-        if (c->idx_bytes == 1)
-            k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-        else
-            k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, w.rr, risk_trace);
+        const int nb6 = launch_h6(c, w.Rt, Bp, w.kstar, w.zhat, w.part, nblk, s);
+        k_rr<<<Bp / 32, kRrThreads, 0, s>>>(w.part, nb6, B, Bp, c->n, m, w.rr, risk_trace);
         c->launches += 3;
         if (c->status) return c->status;  // e.g. a failed collective of learner sharding
     }
@@ -1829,12 +1946,8 @@ int cwb_train_rows(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
         if (rc) return rc;
         k_zhat<<<dim3((c->n_star + 7) / 8, Bp / 32), 256, 0, s>>>(w.kstar, w.theta, c->zj0, c->Zs, c->n_star,
                                                                   c->d, B, Bp, nu, B, nu, w.zhat);
-        dim3 g6(nblk, Bp / 32);
-        if (c->idx_bytes == 1)
-            k_h6<uint8_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint8_t*)c->idx, w.zhat, w.part);
-        else
-            k_h6<uint16_t><<<g6, 256, 0, s>>>(w.Rt, c->n, Bp, w.kstar, (const uint16_t*)c->idx, w.zhat, w.part);
-        k_rr<<<Bp / 32, 256, 0, s>>>(w.part, nblk, B, Bp, c->n, m, rr_g, nullptr);  // local r^T r
+        const int nb6 = launch_h6(c, w.Rt, Bp, w.kstar, w.zhat, w.part, nblk, s);
+        k_rr<<<Bp / 32, kRrThreads, 0, s>>>(w.part, nb6, B, Bp, c->n, m, rr_g, nullptr);  // local r^T r
         c->launches += 3;
     }
     if (M > 0 && risk_trace) {  // the last iteration's risk needs one more sum

@@ -45,6 +45,7 @@ constexpr int kUBudget = 7168;  // doubles of bin sums per CTA (56 KB): Ks * n* 
 constexpr int kStreamT = 1024;  // threads of the stream kernel (one CTA per SM)
 constexpr int kNWK = kStreamT / 32;  // kernel warps: the plan deals groups to them
 constexpr int kStage = 4;        // entry blocks per register stage (two stages in flight per warp)
+constexpr int kFitSplitMax = 8;  // threads per bin sum in k_fit_narrow's combine
 
 // ---------------------------------------------------------------- plan kernels
 // bin counts of every (learner, chunk): cnt[(k * nch + c) * ns + l]
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(kStreamT, 1)
 //   delta = 2 theta^T s - theta^T G theta, SSE = r^T r - delta
 // and the last block to finish (atomic ticket) takes argmin SSE over k, lowest k on ties
 // (P:L292), for every column.
-__global__ void __launch_bounds__(1024) k_fit_narrow(
+__global__ void __launch_bounds__(1024, 1) k_fit_narrow(
     const double* __restrict__ P, int K, int ns, int Ks, int nch, int nitems, int N, int nslot, int B, int d, int W,
     const double* __restrict__ ZT, const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
     const double* __restrict__ G, const double* __restrict__ rrp, double* __restrict__ theta, double* __restrict__ delta,
@@ -501,6 +502,8 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     __shared__ double S[CWB_MAX_D][4], Th[CWB_MAX_D][4], V[CWB_MAX_D][4];
     __shared__ int s_j[CWB_MAX_SMS + 1], s_slot[CWB_MAX_SMS + 1], s_nj, s_lw[2 * CWB_MAX_D];
     __shared__ bool last;
+    __shared__ double hsum[1024];  // slice sums of the split combine (NE * split <= blockDim.x)
+    __shared__ long long s_off[CWB_MAX_SMS + 1];  // offset of each contributing CTA's partial (doubles)
     const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
     const int lg = k / Ks, NU = Ks * ns, a0 = (k - lg * Ks) * ns;
     double* zts = u + (((size_t)ns * B + 1) & ~(size_t)1);
@@ -541,25 +544,47 @@ __global__ void __launch_bounds__(1024) k_fit_narrow(
     }
     __syncthreads();
     const int nj = s_nj;
+    for (int m = tid; m < nj; m += blockDim.x) s_off[m] = ((long long)s_j[m] * nslot + s_slot[m]) * NU;
+    __syncthreads();
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_h1_stream complete: P and rrp visible
     CWB_JIT(k * 4 + 0);
-    for (int e = tid; e < ns * B; e += blockDim.x) {  // u_k(l) for column q, partials added in CTA order
+    // u_k(l) for column q: the CTA partials added in CTA order.  When ns * B is below the block size, each
+    // element's partials are cut into `split` consecutive slices summed by different threads (sixteen loads in
+    // flight each) and the slice sums are added in slice order: one or two L2 round trips instead of nj / 8
+    const int NE = ns * B;
+    const int split = max(1, min(kFitSplitMax, (int)blockDim.x / NE));
+    const int per = (nj + split - 1) / split;
+    for (int e2 = tid; e2 < NE * split; e2 += blockDim.x) {
+        const int h = e2 / NE, e = e2 - h * NE;
         const int l = e / B, q = e - l * B;
         const double* pq = P + (size_t)q * N * nslot * NU + a0 + l;
+        const int m1 = min(nj, (h + 1) * per);
         double v = 0.0;
-        int m = 0;
-        for (; m + 8 <= nj; m += 8) {
-            double t[8];
+        int m = h * per;
+        for (; m + 16 <= m1; m += 16) {
+            long long o[16];
+            double t[16];
 #pragma unroll
-            for (int x = 0; x < 8; x++) t[x] = pq[((size_t)s_j[m + x] * nslot + s_slot[m + x]) * NU];
+            for (int x = 0; x < 16; x++) o[x] = s_off[m + x];
 #pragma unroll
-            for (int x = 0; x < 8; x++) v += t[x];
+            for (int x = 0; x < 16; x++) t[x] = __ldcg(pq + o[x]);
+#pragma unroll
+            for (int x = 0; x < 16; x++) v += t[x];
         }
-        for (; m < nj; m++) v += pq[((size_t)s_j[m] * nslot + s_slot[m]) * NU];
-        u[e] = v;
+        for (; m < m1; m++) v += pq[s_off[m]];
+        if (split == 1) u[e] = v;
+        else hsum[e2] = v;
     }
     cp_async_commit_wait_all();
     __syncthreads();
+    if (split > 1) {
+        for (int e = tid; e < NE; e += blockDim.x) {
+            double v = hsum[e];
+            for (int h = 1; h < split; h++) v += hsum[h * NE + e];
+            u[e] = v;
+        }
+        __syncthreads();
+    }
     // s_j = sum over the design-point window of basis j of Zb[l][j] u(l)   (ZT: window-major basis)
     for (int j = w; j < d; j += nw) {
         const int lb = s_lw[2 * j], le = s_lw[2 * j + 1];
