@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(256) k_h1w(const double* __restrict__ Rt, int6
 // H2-H4 for one learner (blockIdx.x) and 32 replications (blockIdx.y)
 // (HCWB: column b uses Ainv2 / G2 when phase[b mod Bph] != 0)
 // (row sharding: smode 1 writes s to Sg[k][d][Bp] and stops, smode 2 reads the summed s from Sg)
-__global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
-                       const int32_t* __restrict__ zj0, const double* __restrict__ Zs,
+__global__ void __launch_bounds__(256, 3) k_h234(const double* __restrict__ U, int Bp, int ns, int d,
+                       const double* __restrict__ ZT, int W,
                        const int32_t* __restrict__ lwin, const double* __restrict__ Ainv,
                        const double* __restrict__ G, double* __restrict__ theta,
                        double* __restrict__ delta, const double* __restrict__ Ainv2 = nullptr,
@@ -285,8 +285,7 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
     const int k = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int b = blockIdx.y * 32 + lane;
-    const int32_t* j0 = zj0 + (size_t)k * ns;
-    const double* zs = Zs + (size_t)k * ns * CWB_SPW;
+    const double* ztk = ZT + (size_t)k * W * d;  // window-major basis: ZT[k][x][j] = Zb_k[lb_j + x][j]
     const double* u = U + (size_t)k * ns * Bp + b;
     for (int j = w; j < d; j += nw) {
         double s;
@@ -294,31 +293,24 @@ __global__ void k_h234(const double* __restrict__ U, int Bp, int ns, int d,
             s = Sg[((size_t)k * d + j) * Bp + b];
         } else {
             const int lb = lwin[((size_t)k * d + j) * 2], le = lwin[((size_t)k * d + j) * 2 + 1];
+            const double* zt = ztk + j;
+            const double* up = u + (size_t)lb * Bp;
+            const int len = le - lb;
             s = 0.0;
-            int l = lb;
+            int x = 0;
             // sixteen bins' loads in flight (the window is ~4 n* / (n_knots + 1) bins: ~85 at R3), the FMA
-            // chain in bin order as before (bitwise the same s)
-            for (; l + 16 <= le; l += 16) {
+            // chain in bin order
+            for (; x + 16 <= len; x += 16) {
                 double zq[16], uq[16];
 #pragma unroll
                 for (int q = 0; q < 16; q++) {
-                    zq[q] = zs[(l + q) * CWB_SPW + (j - j0[l + q])];
-                    uq[q] = u[(size_t)(l + q) * Bp];
+                    zq[q] = zt[(x + q) * d];
+                    uq[q] = up[(size_t)(x + q) * Bp];
                 }
 #pragma unroll
                 for (int q = 0; q < 16; q++) s = fma(zq[q], uq[q], s);
             }
-            for (; l + 4 <= le; l += 4) {
-                double zq[4], uq[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    zq[q] = zs[(l + q) * CWB_SPW + (j - j0[l + q])];
-                    uq[q] = u[(size_t)(l + q) * Bp];
-                }
-#pragma unroll
-                for (int q = 0; q < 4; q++) s = fma(zq[q], uq[q], s);
-            }
-            for (; l < le; l++) s = fma(zs[l * CWB_SPW + (j - j0[l])], u[(size_t)l * Bp], s);
+            for (; x < len; x++) s = fma(zt[x * d], up[(size_t)x * Bp], s);
             if (smode == 1) Sg[((size_t)k * d + j) * Bp + b] = s;
         }
         S[j][lane] = s;
@@ -1523,8 +1515,8 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
             launch_h1<uint16_t>(w.Rt, c->n, Bp, kl, ns, c->off + (size_t)k0 * (ns + 1), pk, w.U + (size_t)k0 * ns * Bp, s);
         else
             launch_h1<uint32_t>(w.Rt, c->n, Bp, kl, ns, c->off + (size_t)k0 * (ns + 1), pk, w.U + (size_t)k0 * ns * Bp, s);
-        k_h234<<<dim3(kl, Bp / 32), 256, 0, s>>>(w.U + (size_t)k0 * ns * Bp, Bp, ns, d, c->zj0 + (size_t)k0 * ns,
-                                                 c->Zs + (size_t)k0 * ns * CWB_SPW, c->lwin + (size_t)k0 * d * 2,
+        k_h234<<<dim3(kl, Bp / 32), 256, 0, s>>>(w.U + (size_t)k0 * ns * Bp, Bp, ns, d, c->ZT + (size_t)k0 * c->W * d,
+                                                 c->W, c->lwin + (size_t)k0 * d * 2,
                                                  c->Ainv + (size_t)k0 * d * d, c->G + (size_t)k0 * d * d,
                                                  w.theta + (size_t)k0 * d * Bp, w.delta + (size_t)k0 * Bp);
         cudaMemsetAsync(w.lbuf, 0, cnt * sizeof(double), s);
@@ -1538,14 +1530,14 @@ static void find_best_iter(cwb_ctx* c, int32_t B, double nu, int m, double* agg,
     }
     if (c->nb) {  // unbinned learners: s = Z^T r by the 4-tap scatter (cwb_nb.cu), then H3-H4 from s
         cwb_nb_h12(c, w.Rt, Bp, w.pack, s);
-        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin, c->Ainv,
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->ZT, c->W, c->lwin, c->Ainv,
                                                     c->G, w.theta, w.delta, nullptr, nullptr, nullptr, 0, w.pack, 2);
     } else {
         cudaEvent_t* ev = cwb_h1_events(c);  // profiling hook (bench.py's roofline): H1 bracketed by events
         if (ev) cudaEventRecord(ev[0], s);
         h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
         if (ev) cudaEventRecord(ev[1], s);
-        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin,
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->ZT, c->W, c->lwin,
                                                     c->Ainv, c->G, w.theta, w.delta);
     }
     k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, m, w.kstar,
@@ -1614,7 +1606,7 @@ static int find_best_narrow(cwb_ctx* c, const double* R, int32_t B, int32_t* k_o
             w.narrow, nranges, K, ns, B, w.Bp, w.U);
         c->launches += 2;
     }
-    k_h234<<<dim3(K, w.Bp / 32), 256, 0, s>>>(w.U, w.Bp, ns, c->d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+    k_h234<<<dim3(K, w.Bp / 32), 256, 0, s>>>(w.U, w.Bp, ns, c->d, c->ZT, c->W, c->lwin, c->Ainv, c->G, w.theta,
                                               w.delta);
     k_h5<<<w.Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, K, c->d, B, w.Bp, 0.0, 0, w.kstar, nullptr,
                                             nullptr, nullptr, k_out, theta_out, sse_out);
@@ -1826,7 +1818,7 @@ int cwb_train_folds_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_
         else
             k_h1<uint32_t><<<grid, wpb * 32, 0, s>>>(w.Rt, c->n, Bp, K, ns, c->off, (const uint32_t*)c->perm, w.U,
                                                     fold_of_row, colfold);
-        k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+        k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->ZT, c->W, c->lwin, c->Ainv, c->G, w.theta,
                                                 w.delta, nullptr, nullptr, nullptr, 0, nullptr, 0, As, Gs, colfold);
         k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, w.rr, K, d, B, Bp, nu, m, w.kstar, theta_agg_out,
                                               k_trace, sse_trace, nullptr, nullptr, nullptr);
@@ -1878,7 +1870,7 @@ static int find_best_rows_iter(cwb_ctx* c, int32_t B, double nu, int m, double* 
     const int Bp = w.Bp, K = c->K, d = c->d;
     double* rr_g = w.pack + (size_t)K * d * Bp;
     h1(c, w.Rt, Bp, K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
-    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->ZT, c->W, c->lwin, c->Ainv, c->G, w.theta,
                                             w.delta, nullptr, nullptr, nullptr, 0, w.pack, 1);
     c->launches += 1;
     int rc = cwb_check_launch(c, "row-sharded s kernels");
@@ -1889,7 +1881,7 @@ static int find_best_rows_iter(cwb_ctx* c, int32_t B, double nu, int m, double* 
         k_risk<<<(B + 127) / 128, 128, 0, s>>>(rr_g, B, c->n_glob, risk_prev);
         c->launches += 1;
     }
-    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->ZT, c->W, c->lwin, c->Ainv, c->G, w.theta,
                                             w.delta, nullptr, nullptr, nullptr, 0, w.pack, 2);
     k_h5<<<Bp / 32, 256, 0, s>>>(w.delta, w.theta, rr_g, K, d, B, Bp, nu, m, w.kstar, agg, k_trace,
                                           sse_trace, k_out, theta_out, sse_out);
@@ -2100,7 +2092,7 @@ int cwb_train_acwb_general(cwb_ctx* c, const double* Y, int32_t B, double nu, do
         const double vt1 = 2.0 / (double)(m + 2);             // next iteration's combination
         const double a1 = (double)(m + 1) / (double)(m + 2);  // next iteration's correction weight
         h1(c, w.Rt, Bp, c->K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);  // lines 7 and 14: binMatVec
-        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G,
+        k_h234<<<dim3(c->K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, c->d, c->ZT, c->W, c->lwin, c->Ainv, c->G,
                                                     w.theta, w.delta);
         k_acwb_select<<<(B + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, c->K, c->d, B, Bp, nu, vt, eta, m - 1,
                                                       w.kstar, theta_f_out, theta_h_out, k_trace, kcor_trace,
@@ -2202,7 +2194,7 @@ int cwb_train_hcwb_general(cwb_ctx* c, const double* Y, int32_t B, const uint8_t
         const double vt1 = 2.0 / (double)(m + 3);
         const double a1 = (double)(m + 2) / (double)(m + 3);
         h1(c, w.Rt, Bp, K, ns, c->off, c->perm, c->perm_bytes, w.U, s);
-        k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->zj0, c->Zs, c->lwin, Ainv_tr, G_tr, w.theta, w.delta,
+        k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, ns, d, c->ZT, c->W, c->lwin, Ainv_tr, G_tr, w.theta, w.delta,
                                                 c->Ainv, c->G, phase, B);
         k_hcwb_select<<<(B + 127) / 128, 128, 0, s>>>(w.delta, w.theta, w.rr, phase, K, d, B, Bp, nu, vt, eta, m,
                                                       w.kstar, theta_f_out, th, k_trace, kcor_trace, sse_trace);
@@ -2423,7 +2415,7 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
         if (CR > 0) h1_chunk(c, Pv, ld, K, ns, c->perm, c->perm_bytes, U, nch, ch, s, d);
         else h1(c, Pv, ld, K, ns, c->off, c->perm, c->perm_bytes, U, s, d);
     }
-    k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, nullptr, nullptr,
+    k_h234<<<dim3(K, ld / 32), 256, 0, s>>>(U, ld, ns, d, c->ZT, c->W, c->lwin, c->Ainv, c->G, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, 0, xg, 1);  // projection Zb_k^T U_k
     k_gram_sym<<<K * d, 256, 0, s>>>(xg, K, d, ld);
     k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
@@ -2459,7 +2451,7 @@ int cwb_train_gram(cwb_ctx* c, const double* Y, int32_t B, double nu, int32_t M,
     k_tr_in<<<gt, dim3(32, 8), 0, s>>>(Y, c->n, B, Bp, off_ws, nullptr, w.Rt);
     // theta^[0] = A^-1 Z^T r^[0]: H1-H3 of the initial residuals (k_h234 also writes delta, unused here)
     h1(c, w.Rt, Bp, K, c->n_star, c->off, c->perm, c->perm_bytes, w.U, s);
-    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->zj0, c->Zs, c->lwin, c->Ainv, c->G, w.theta,
+    k_h234<<<dim3(K, Bp / 32), 256, 0, s>>>(w.U, Bp, c->n_star, d, c->ZT, c->W, c->lwin, c->Ainv, c->G, w.theta,
                                              w.delta);
     const size_t smem = sizeof(double) * ((size_t)K * d + K);
     CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_gram_train, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
