@@ -129,6 +129,15 @@ __host__ __device__ __forceinline__ size_t plan_ints(int KS, int T) {
     const size_t R = plan_rounds_max(KS, T);
     return 8 + R * T + 2 * R * (T / 32) + 3 * (size_t)KS;
 }
+// task cut: bins longer than piece_factor() x the mean bin size are cut into pieces.  Any cut bin costs the
+// combine pass and its barrier in every iteration, which outweighs the shorter critical task: R1 (B = 256) per
+// iteration 9,565 cycles at 1.6 vs 9,073 at 4.0 (CWB; ACWB 10,900 -> 9,975, HCWB 24,832 -> 23,155, Bernoulli
+// 16,027 -> 15,401; profiles/r2h_piece_factor.txt).  4x still cuts outlier bins (heavy ties).  CWB_PFAC
+// overrides it for experiments.
+static double piece_factor() {
+    static const double f = getenv("CWB_PFAC") ? atof(getenv("CWB_PFAC")) : 4.0;
+    return f;
+}
 __host__ __device__ __forceinline__ size_t permt_bound(int KS, int T, int P) {
     return (size_t)plan_rounds_max(KS, T) * T * (size_t)((P + 3) / 4 * 4);
 }
@@ -1264,8 +1273,8 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out, bool bern = fa
         const int64_t stride = 8 * f.RB;
         f.permt_bytes = stride * (c->n + kPadRows) <= 65535 ? 2 : 4;
         // task size: balance the K*n rows over T threads, but do not cut bins of up to
-        // 1.6x the mean bin size (a cut bin costs a combine pass)
-        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
+        // piece_factor() x the mean bin size (a cut bin costs a combine pass)
+        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(piece_factor() * c->n / c->n_star)));
         f.cap = permt_bound(KS, f.T, f.P);
         for (int pool = 1; pool >= 0; pool--) {
             SmemLayout L((int)c->n, c->K, c->nsp, c->d, c->W, 2 * f.T, f.RB, f.T / 32, pool != 0, f.cap * f.permt_bytes, 0,
@@ -1459,7 +1468,7 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
             }
         }
         if (!f.T) return CWB_OK;
-        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(1.6 * c->n / c->n_star)));
+        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(piece_factor() * c->n / c->n_star)));
     } else if (!fused_shape(c, B, &f, bern)) {
         return CWB_OK;  // does not fit: caller uses the general path
     }
