@@ -1263,9 +1263,11 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out, bool bern = fa
     Cand cands[4];
     int nc = 0;
     const int nsm = cwb_num_sms();
-    if (B > nsm) cands[nc++] = {2, 512, kMaxSmem};  // ~2 replications per SM: one CTA (512 best of 256..768)
+    static const int t2 = getenv("CWB_FT2") ? atoi(getenv("CWB_FT2")) : 512;  // experiments only
+    static const int t1 = getenv("CWB_FT1") ? atoi(getenv("CWB_FT1")) : 0;
+    if (B > nsm) cands[nc++] = {2, t2, kMaxSmem};  // ~2 replications per SM: one CTA (512 best of 256..768)
     if (B > nsm && !bern) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
-    cands[nc++] = {1, c->n >= 8192 ? 768 : 512, kMaxSmem};
+    cands[nc++] = {1, t1 ? t1 : (c->n >= 8192 ? 768 : 512), kMaxSmem};
     for (int i = 0; i < nc; i++) {
         FusedShape f;
         f.RB = cands[i].RB;
