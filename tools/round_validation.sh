@@ -16,3 +16,6 @@ timeout 300 python tools/prof_iter.py R3 1 > gpurun_out/${TAG}_prof_plain.log 2>
 python tools/ncu_brief.py gpurun_out/${TAG}_h1w.ncu-rep > gpurun_out/${TAG}_ncu_h1w_R3.txt 2>&1
 # DRAM bytes of the H1 phase of one R3 iteration (its row-chunk launches), for roofline.traffic (profiles/traffic.json)
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_h1w -c 6 --csv --log-file gpurun_out/${TAG}_h1w_traffic.csv python tools/prof_iter.py R3 1 > /dev/null 2>&1
+# R1 variants of the fused kernel (ACWB, HCWB, Bernoulli) and the findBest B = 1 split
+for a in acwb hcwb bernoulli; do timeout 600 python bench.py --config R1 --algo $a --steps 10 --warmup 3 --no-gram --no-cpu-baseline --no-findbest > gpurun_out/${TAG}_bench_R1_$a.json 2> gpurun_out/${TAG}_bench_R1_$a.err; done
+for cfg in R3 R4; do timeout 300 python tools/findbest_timing.py $cfg 1 20 0 1 >> gpurun_out/${TAG}_findbest.log 2>&1; CWB_STREAM_NOFIT=1 timeout 300 python tools/findbest_timing.py $cfg 1 20 0 1 | sed 's/^/NOFIT /' >> gpurun_out/${TAG}_findbest.log 2>&1; done
