@@ -76,6 +76,7 @@ struct cwb_ctx {
     bool h1_wide = true;     // H1 with two replication columns per lane (k_h1w) when Bp % 64 == 0 (CWB_H1_WIDE=0: off)
     uint32_t* h1c = nullptr; // chunked H1: [K][nch][n*] row counts, then starts
     int32_t h1c_nch = 0;
+    int64_t h1c_cr = 0;  // rows per chunk of the cached tables
     // cross-Gram path (cwb_set_path 3): xg[(k d + a) * xg_ld + k' d + b] = (Z_k^T Z_k')[a][b],
     // built on the first path-3 train call of the pool
     double* xg = nullptr;

@@ -1390,9 +1390,13 @@ static int64_t h1_chunk_plan(cwb_ctx* c, int64_t tile_row, const int32_t* off, i
     if (!(n * tile_row > 80ll * 1000 * 1000 && c->h1_chunking && !c->rows && off == c->off)) return 0;
     static const int64_t chunk_bytes =
         getenv("CWB_H1_CHUNK_MB") ? (int64_t)atoi(getenv("CWB_H1_CHUNK_MB")) << 20 : kH1ChunkBytes;
-    const int64_t CR = chunk_bytes / tile_row;
-    const int nch = (int)((n + CR - 1) / CR);
-    if (!c->h1c || c->h1c_nch != nch) {  // per (learner, chunk, bin) row counts and starts, once per pool
+    // equal chunks of at most chunk_bytes (R3: 3 x 66,667 rows = 34 MB instead of 2 x 81,920 + 36,160): the
+    // measured sweep favours ~34 MB at R3 (profiles/r2h_h1_chunk.txt); the cached tables are keyed on the
+    // rows per chunk
+    const int64_t CR0 = std::max<int64_t>(1, chunk_bytes / tile_row);
+    const int nch = (int)((n + CR0 - 1) / CR0);
+    const int64_t CR = (n + nch - 1) / nch;
+    if (!c->h1c || c->h1c_nch != nch || c->h1c_cr != CR) {  // per (learner, chunk, bin) counts / starts, once per pool
         cwb_release(c->h1c, s);
         c->h1c = nullptr;
         if (cwb_alloc((void**)&c->h1c, 2 * sizeof(uint32_t) * (size_t)K * nch * ns, s) != cudaSuccess) {
@@ -1400,6 +1404,7 @@ static int64_t h1_chunk_plan(cwb_ctx* c, int64_t tile_row, const int32_t* off, i
             return -1;
         }
         c->h1c_nch = nch;
+        c->h1c_cr = CR;
         k_h1_chunk_count<<<dim3(nch, K), 1024, sizeof(uint32_t) * ns, s>>>(c->idx, c->idx_bytes, n, ns, CR, nch,
                                                                          c->h1c);
         k_h1_chunk_start<<<(unsigned)(((int64_t)K * ns + 255) / 256), 256, 0, s>>>(c->h1c, c->off, K, ns, nch);
