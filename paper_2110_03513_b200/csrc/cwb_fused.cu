@@ -563,6 +563,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 }
             }
         }
+#ifdef CWB_PHASE_DEBUG
+        __shared__ long long dbg_endA[32], dbg_endB[32];
+        if (lane == 0) dbg_endA[warp] = clock64();
+#endif
         __syncthreads();
         if (timed) tm = phase_mark(&tA, tm, true);
         CWB_JIT(m * 8 + 1);
@@ -570,6 +574,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         //      s = Zb^T u (window of basis j), theta = (G + lambda D)^-1 s (cached inverse,
         //      P:L846), c = C^T theta, delta = |c|^2 = 2 theta^T s - theta^T G theta ------
         for (int k = warp; k < K; k += NW) {
+#ifdef CWB_PHASE_DEBUG
+            long long dt0 = 0;
+            const bool dbgw = timed || (blockIdx.x == 0 && warp == 0 && lane == 0);
+            if (dbgw) { if (__double_as_longlong(U[k * nsp * RB]) == 0x7ff8deadbeefll) dt0 = 1; dt0 += clock64(); }
+#endif
             double sv[RB];
 #pragma unroll
             for (int q = 0; q < RB; q++) sv[q] = 0.0;
@@ -590,6 +599,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                     }
                 }
             }
+#ifdef CWB_PHASE_DEBUG
+            long long dts = 0;
+            if (dbgw) { if (__double_as_longlong(sv[0]) == 0x7ff8deadbeefll) dts = 1; dts += clock64(); }
+#endif
 #pragma unroll
             for (int q = 0; q < RB; q++) sS[q * 32 + lane] = sv[q];  // lanes >= d store 0
             __syncwarp();
@@ -616,6 +629,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                     for (int q = 0; q < RB; q++) t0[q] = fma(a0, sS[q * 32 + jp], t0[q]);
                 }
             }
+#ifdef CWB_PHASE_DEBUG
+            long long dtt = 0;
+            if (dbgw) { if (__double_as_longlong(t0[0] + t1[0]) == 0x7ff8deadbeefll) dtt = 1; dtt += clock64(); }
+#endif
             double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
             if (lane < d) {
                 const double* cbj = Cbc + ((size_t)k * d + lane) * 4;
@@ -631,9 +648,35 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 const double v = warp_sum(c * c);
                 thall[(k * RB + q) * 32 + lane] = th;
                 if (lane == 0) delta[k * RB + q] = v;
+#ifdef CWB_PHASE_DEBUG
+                if (dbgw && q == RB - 1) {
+                    long long dte = 0;
+                    if (__double_as_longlong(v) == 0x7ff8deadbeefll) dte = 1;
+                    dte += clock64();
+                    if (timed) { p.timing[60] += dts - dt0; p.timing[61] += dtt - dts; p.timing[62] += dte - dtt; }
+                }
+#endif
             }
         }
+#ifdef CWB_PHASE_DEBUG
+        if (lane == 0) dbg_endB[warp] = clock64();
+#endif
         __syncthreads();
+#ifdef CWB_PHASE_DEBUG
+        if (timed) {  // CTA 0: A-phase spread over warps, B after the last A warp, which warp ends A last
+            long long mn = dbg_endA[0], mx = dbg_endA[0], mb = dbg_endB[0];
+            int wl = 0;
+            for (int x = 1; x < NW; x++) {
+                mn = min(mn, dbg_endA[x]);
+                if (dbg_endA[x] > mx) { mx = dbg_endA[x]; wl = x; }
+                mb = max(mb, dbg_endB[x]);
+            }
+            p.timing[4] += mx - mn;
+            p.timing[5] += mb - mx;
+            p.timing[8 + wl] += 1;
+            for (int x = 0; x < NW; x++) p.timing[40 + x] += dbg_endA[x] - mn;
+        }
+#endif
         if (timed) tm = phase_mark(&tB, tm, true);
         CWB_JIT(m * 8 + 2);
         // ---- C / H5: job (q, slice): k* = argmax delta (lowest k on ties) for
