@@ -376,7 +376,10 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
     for i in range(max(3, min(args.steps, 10))):
         flush.fill_(float(i))
         ts.append(ev(step))
-    ms = float(np.mean(ts))
+    # median: a fresh pool re-allocates the row-chunk basis buffer (1.3 GB at R3), and one of a few steps can
+    # take an allocator stall (seen once under torchrun: 0.6 s); the mean is reported beside it
+    ms = float(np.median(ts))
+    ms_mean = float(np.mean(ts))
     p = cwb.Pool(X, gcfg)
     p.set_path(3)
     t_first0 = ev(lambda: p.train(Y, nu=cfg.nu, M=0))          # cross Gram + W + theta^[0]
@@ -395,7 +398,8 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
     l2 = float(peaks.get("l2_read_gbs", 0.0)) * 1e9
     return {"path": "cross-Gram (cwb_set_path 3): s_k -= nu Z_k^T Z_k* theta*, exact reformulation of Alg. 1 for "
                     "L2 loss; parity tests/test_gpu_gram.py (R0-R3 vs the oracle, tie rule 1e-12)",
-            "ms_per_step": ms, "value": K * n * B * M / (ms * 1e-3), "unit": UNIT,
+            "ms_per_step": ms, "ms_per_step_mean": ms_mean, "steps_timed": len(ts),
+            "value": K * n * B * M / (ms * 1e-3), "unit": UNIT,
             "speedup_vs_direct": direct_ms / ms,
             "phases_ms": {"xgram_build": t_x, "theta0_binmatvec": t_m0, "iterations": t_it,
                           "iteration_us": t_it / max(M, 1) * 1e3},
