@@ -41,6 +41,7 @@
 namespace {
 
 constexpr int kDiscard = INT32_MIN;
+constexpr int kAregD = 24;  // basis dimension of the register-resident A^-1 columns (the default d)
 constexpr int kPadRows = 16;  // zero rows after the n residual rows, one per bank group
 constexpr int kSlackEntries = 256;  // schedule entries after the last block (2 groups of 4 x 32 lanes)
 
@@ -507,6 +508,16 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
         }
     };
 
+    // CWB with two replications per 384-thread CTA (register budget 170): when every learner has its own warp
+    // and d = 24, lane j of learner k's warp keeps column j of A_k^-1 in registers for phase B (the per-iteration
+    // A^-1 stream from shared memory was phase B's bound at R1)
+    constexpr bool AREG_T = (MAXT == 384 && RB == 2 && !ACC && !HC && !BERN);
+    const bool areg = AREG_T && K <= NW && d == kAregD;
+    double Areg[AREG_T ? kAregD : 1];
+#pragma unroll
+    for (int jp = 0; jp < (AREG_T ? kAregD : 1); jp++)
+        Areg[jp] = (AREG_T && areg && warp < K && lane < d) ? Ac[((size_t)warp * d + jp) * d + lane] : 0.0;
+
     for (int m = 0; m < p.M; m++) {
         if (HC) {
             if (m > 0 && warp == 0) bookkeeping_hc(m - 1);
@@ -609,7 +620,19 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
             double t0[RB], t1[RB];
 #pragma unroll
             for (int q = 0; q < RB; q++) { t0[q] = 0.0; t1[q] = 0.0; }
-            if (lane < d) {
+            if (AREG_T && areg) {
+                if (lane < d) {  // same products and order as the loop below (even jp -> t0, odd -> t1)
+#pragma unroll
+                    for (int jp = 0; jp < (AREG_T ? kAregD : 2); jp += 2) {
+#pragma unroll
+                        for (int q = 0; q < RB; q++) {
+                            const double2 s2 = *reinterpret_cast<const double2*>(sS + q * 32 + jp);
+                            t0[q] = fma(Areg[jp], s2.x, t0[q]);
+                            t1[q] = fma(Areg[jp + 1], s2.y, t1[q]);
+                        }
+                    }
+                }
+            } else if (lane < d) {
                 const double* Ak = Ac + (size_t)k * d * d + lane;  // A^-1 symmetric: column j = row j
                 int jp = 0;
 #pragma unroll 4
@@ -1270,6 +1293,10 @@ int launch_sel(const FusedParams& fp, int T, int RB, bool pool, size_t smem, cud
         return launch_t<IdxT, PermT, 2, false, 512, 1, true>(fp, T, smem, s);
     }
     if (RB == 2) {
+        if (T == 384) {  // register-resident A^-1 columns (AREG_T)
+            if (pool) return launch_t<IdxT, PermT, 2, true, 384, 1>(fp, T, smem, s);
+            return launch_t<IdxT, PermT, 2, false, 384, 1>(fp, T, smem, s);
+        }
         if (T > 512) {
             if (pool) return launch_t<IdxT, PermT, 2, true, 768, 1>(fp, T, smem, s);
             return launch_t<IdxT, PermT, 2, false, 768, 1>(fp, T, smem, s);
@@ -1306,7 +1333,9 @@ static bool fused_shape(const cwb_ctx* c, int B, FusedShape* out, bool bern = fa
     Cand cands[4];
     int nc = 0;
     const int nsm = cwb_num_sms();
-    static const int t2 = getenv("CWB_FT2") ? atoi(getenv("CWB_FT2")) : 512;  // experiments only
+    // 384 threads (the register-resident A^-1 instance) when every learner gets its own warp at d = 24, else 512
+    static const int t2env = getenv("CWB_FT2") ? atoi(getenv("CWB_FT2")) : 0;  // experiments only
+    const int t2 = t2env ? t2env : ((!bern && c->K <= 12 && c->d == kAregD) ? 384 : 512);
     static const int t1 = getenv("CWB_FT1") ? atoi(getenv("CWB_FT1")) : 0;
     if (B > nsm) cands[nc++] = {2, t2, kMaxSmem};  // ~2 replications per SM: one CTA (512 best of 256..768)
     if (B > nsm && !bern) cands[nc++] = {1, std::min(384, std::max(256, 32 * c->K)), kTwoCtaSmem};
