@@ -476,7 +476,8 @@ def main():
     Y = torch.as_tensor(Y_host, device=devname)
     gcfg = cwb.Config(n_star_rule=cfg.n_star_rule, n_star_fixed=cfg.n_star_fixed, n_knots=cfg.n_knots,
                       degree=cfg.degree, df=cfg.df, batch_hint=0 if strong or args.unbinned else cfg.B,
-                      unbinned=int(args.unbinned))
+                      unbinned=int(args.unbinned),
+                      train_hint={"cwb": 0, "acwb": 1, "hcwb": 2, "bernoulli": 3}[args.algo])
     comm = None
     if strong:  # libcwb's own NCCL communicator, id from rank 0 over the torch process group
         uid = D.nccl_unique_id(w, torch.device(devname)) if ws > 1 else cwb.cwb_comm_unique_id()

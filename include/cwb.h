@@ -70,10 +70,15 @@ typedef struct {
                              cwb_train (L2), cwb_find_best and cwb_predict (basis at x clamped
                              to the training range); the other training calls return
                              CWB_EUNSUPPORTED. */
+    int32_t train_hint;   /* the training call batch_hint is for, which fixes the shape (threads per
+                             CTA, replications per CTA) of the plan cwb_init pre-builds: 0 cwb_train
+                             (default), 1 cwb_train_acwb, 2 cwb_train_hcwb, 3 cwb_train_bernoulli.
+                             Any call still works on any context; a call whose shape differs from
+                             the pre-built plan rebuilds it first.  Out of range: CWB_EINVAL.     */
 } cwb_config;
 
-/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5, no batch hint,
- * binned learners. */
+/* Fills *cfg with the paper's defaults: sqrt rule, degree 3, 20 knots, df1 = 5, no batch hint
+ * (train_hint 0), binned learners. */
 void cwb_default_config(cwb_config* cfg);
 
 /* Library ABI version (major*100 + minor). */

@@ -120,6 +120,7 @@ void cwb_default_config(cwb_config* cfg) {
     cfg->df_kind = 1;
     cfg->batch_hint = 0;
     cfg->unbinned = 0;
+    cfg->train_hint = 0;
 }
 
 int cwb_version(void) { return 100; }
@@ -219,10 +220,12 @@ int cwb_init(cwb_ctx** out, const double* X, int64_t n, int32_t K, const cwb_con
     if (cfg.unbinned != 0 && cfg.unbinned != 1) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: unbinned");
     if (cfg.unbinned && (cfg.degree != 3 || cfg.n_knots + 1 > 255))
         return cwb_set_error(nullptr, CWB_EUNSUPPORTED, "cwb_init: unbinned learners need degree 3");
+    if (cfg.train_hint < 0 || cfg.train_hint > 3) return cwb_set_error(nullptr, CWB_EINVAL, "cwb_init: train_hint");
     cwb_ctx* c = new cwb_ctx();
     c->n = n; c->K = K; c->n_star = (int32_t)ns; c->d = d; c->degree = cfg.degree; c->n_knots = cfg.n_knots;
     c->df = cfg.df; c->df_kind = cfg.df_kind;
     c->batch_hint = cfg.batch_hint > 0 && !cfg.unbinned ? cfg.batch_hint : 0;
+    c->train_hint = cfg.train_hint;
     c->nb = cfg.unbinned != 0;
     if (const char* e = getenv("CWB_H1_CHUNKING")) c->h1_chunking = atoi(e);  // A/B measurement switch
     if (const char* e = getenv("CWB_H1_WIDE")) c->h1_wide = atoi(e) != 0;       // A/B: k_h1w vs k_h1

@@ -710,15 +710,27 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                 const int q = job % RB, sl = job / RB;
                 double best = -INFINITY;
                 int kb = 0;
-                for (int k = lane; k < K; k += 32) {
-                    const double v = delta[k * RB + q];
-                    if (v > best) { best = v; kb = k; }
-                }
+                if (K <= 16) {
+                    // every lane scans the K deltas in k order (broadcast loads, strict >: the lowest k of
+                    // the maximum), the same result as the lane-strided scan + shuffle tree below without
+                    // its five dependent shuffle rounds
+                    double dv[16];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
-                    if (ob > best || (ob == best && ok < kb)) { best = ob; kb = ok; }
+                    for (int k = 0; k < 16; k++) dv[k] = k < K ? delta[k * RB + q] : -INFINITY;
+#pragma unroll
+                    for (int k = 0; k < 16; k++)
+                        if (dv[k] > best) { best = dv[k]; kb = k; }
+                } else {
+                    for (int k = lane; k < K; k += 32) {
+                        const double v = delta[k * RB + q];
+                        if (v > best) { best = v; kb = k; }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                        const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
+                        if (ob > best || (ob == best && ok < kb)) { best = ob; kb = ok; }
+                    }
                 }
                 const int l = sl * 32 + lane;
                 if (l < ns) {
@@ -844,28 +856,57 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                     j0[e] = i < n ? (uint32_t)ik0[i] : 0u;
                     j1[e] = (RB == 2 && i < n) ? (uint32_t)ik1[i] : 0u;
                 }
+                if (!BERN && !ACC) {
+                    // plain CWB: the four rows' r and zhat loads are issued before the first store (the
+                    // compiler cannot reorder loads past the r stores itself); same arithmetic and order
+                    double2 rv[4];
+                    double z0[4], z1[4];
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const int i = i0 + e * T;
-                    if (i < n && BERN) {
-                        // f += nu b_k* (line 10), r = y - sigma(f) (line 4 of the next iteration), log-loss
-#pragma unroll
-                        for (int q = 0; q < RB; q++) {
-                            const double f = Fb[i * RB + q] + zhat[q * nsp + (q ? j1[e] : j0[e])];
-                            Fb[i * RB + q] = f;
-                            const double y = Yb[i * RB + q];
-                            double lo;
-                            const double v = bern_resid(y, f, &lo);
-                            r[i * RB + q] = v;
-                            acc[q] = fma(v, v, acc[q]);
-                            accL[q] += lo;
+                    for (int e = 0; e < 4; e++) {
+                        const int i = i0 + e * T;
+                        if (i < n) {
+                            if (RB == 1) rv[e].x = r[i];
+                            else rv[e] = *reinterpret_cast<const double2*>(r + 2 * i);
+                            z0[e] = zhat[j0[e]];
+                            z1[e] = RB == 2 ? zhat[nsp + j1[e]] : 0.0;
                         }
-                    } else if (i < n) {
-                        if (RB == 1) {
-                            const double v = r[i] - zhat[j0[e]];
-                            r[i] = v;
-                            acc[0] = fma(v, v, acc[0]);
-                        } else if (ACC) {
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int i = i0 + e * T;
+                        if (i < n) {
+                            if (RB == 1) {
+                                const double v = rv[e].x - z0[e];
+                                r[i] = v;
+                                acc[0] = fma(v, v, acc[0]);
+                            } else {
+                                double2 v = rv[e];
+                                v.x -= z0[e];
+                                v.y -= z1[e];
+                                *reinterpret_cast<double2*>(r + 2 * i) = v;
+                                acc[0] = fma(v.x, v.x, acc[0]);
+                                acc[RB - 1] = fma(v.y, v.y, acc[RB - 1]);
+                            }
+                        }
+                    }
+                } else {  // Bernoulli (RB = 1, 2) or ACWB (RB = 2)
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int i = i0 + e * T;
+                        if (i < n && BERN) {
+                            // f += nu b_k* (line 10), r = y - sigma(f) (line 4 of the next iteration), log-loss
+#pragma unroll
+                            for (int q = 0; q < RB; q++) {
+                                const double f = Fb[i * RB + q] + zhat[q * nsp + (q ? j1[e] : j0[e])];
+                                Fb[i * RB + q] = f;
+                                const double y = Yb[i * RB + q];
+                                double lo;
+                                const double v = bern_resid(y, f, &lo);
+                                r[i * RB + q] = v;
+                                acc[q] = fma(v, v, acc[q]);
+                                accL[q] += lo;
+                            }
+                        } else if (i < n && ACC) {
                             const double2 v = *reinterpret_cast<double2*>(r + 2 * i);
                             const double bc = zhat[nsp + j1[e]];
                             const double F = v.x - zhat[j0[e]];
@@ -877,13 +918,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_train_fused(FusedParams p) {
                             accF = fma(F, F, accF);
                             acc[0] = fma(rn, rn, acc[0]);
                             acc[RB - 1] = fma(cn, cn, acc[RB - 1]);
-                        } else {
-                            double2 v = *reinterpret_cast<double2*>(r + 2 * i);
-                            v.x -= zhat[j0[e]];
-                            v.y -= zhat[nsp + j1[e]];
-                            *reinterpret_cast<double2*>(r + 2 * i) = v;
-                            acc[0] = fma(v.x, v.x, acc[0]);
-                            acc[RB - 1] = fma(v.y, v.y, acc[RB - 1]);
                         }
                     }
                 }
@@ -1483,13 +1517,44 @@ static int fused_plan_finish(cwb_ctx* c) {
     return CWB_OK;
 }
 
+// Shape (replications and threads per CTA, task size) of a fused launch of B replications for the
+// CWB (acc = false), ACWB / HCWB (acc, hc) or Bernoulli (bern) kernel; false when it does not fit.
+static bool train_shape(const cwb_ctx* c, int B, bool acc, bool hc, bool bern, FusedShape* out) {
+    if (!acc) return fused_shape(c, B, out, bern);
+    FusedShape f;  // the two columns (r, c) of a replication run as RB = 2
+    if ((int64_t)c->K * c->n + 8 > INT32_MAX || (int64_t)c->K * c->n_star * 16 > 200 * 1024) return false;
+    f.RB = 2;
+    f.permt_bytes = 16 * (c->n + kPadRows) <= 65535 ? 2 : 4;
+    // HCWB with more replications than SMs: 256-thread CTAs, two per SM, when both fit in shared
+    // memory (R1: 3.24 -> 2.98 ms; ACWB measured slower that way, 2.33 -> 2.48 ms, and keeps
+    // 512).  CWB_ACC_T=256|512 overrides.
+    const char* ev = getenv("CWB_ACC_T");
+    const int want = ev ? atoi(ev) : (hc && B > cwb_num_sms() ? 256 : 512);
+    f.T = 0;
+    for (int T : {256, 512}) {
+        if (T < want) continue;
+        const size_t lim = T == 256 ? kTwoCtaSmem : kMaxSmem;
+        if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * T, 2, T / 32, false, 0, 0, c->idx_bytes, true,
+                       hc)
+                .total <= lim) {
+            f.T = T;
+            break;
+        }
+    }
+    if (!f.T) return false;
+    f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(piece_factor() * c->n / c->n_star)));
+    *out = f;
+    return true;
+}
+
 // Pre-builds the plan for the expected batch (cwb_config.batch_hint) on a side stream that
 // starts right after the bin inversion, so it overlaps the basis / binMatMat / df->lambda
 // kernels of cwb_init.  Called by cwb_launch_init after k_csr.
 int cwb_fused_plan(cwb_ctx* c, cudaStream_t s) {
     if (c->batch_hint <= 0) return CWB_OK;
-    FusedShape f;
-    if (!fused_shape(c, c->batch_hint, &f)) return CWB_OK;
+    FusedShape f;  // the shape of the training call the hint names (cwb_config.train_hint)
+    const int th = c->train_hint;
+    if (!train_shape(c, c->batch_hint, th == 1 || th == 2, th == 2, th == 3, &f)) return CWB_OK;
     if (!c->s2) {  // one side stream per device, shared by the contexts (created once, never destroyed)
         static cudaStream_t side[16] = {};
         static std::mutex mu;
@@ -1521,31 +1586,7 @@ static int train_fused_common(cwb_ctx* c, bool acc, const double* Y, int32_t B, 
                               bool* launched, const HcArgs* hc = nullptr, bool bern = false) {
     *launched = false;
     FusedShape f;
-    if (acc) {  // the two columns (r, c) of a replication run as RB = 2
-        if ((int64_t)c->K * c->n + 8 > INT32_MAX || (int64_t)c->K * c->n_star * 16 > 200 * 1024) return CWB_OK;
-        f.RB = 2;
-        f.permt_bytes = 16 * (c->n + kPadRows) <= 65535 ? 2 : 4;
-        // HCWB with more replications than SMs: 256-thread CTAs, two per SM, when both fit in shared
-        // memory (R1: 3.24 -> 2.98 ms; ACWB measured slower that way, 2.33 -> 2.48 ms, and keeps
-        // 512).  CWB_ACC_T=256|512 overrides.
-        const char* ev = getenv("CWB_ACC_T");
-        const int want = ev ? atoi(ev) : (hc != nullptr && B > cwb_num_sms() ? 256 : 512);
-        f.T = 0;
-        for (int T : {256, 512}) {
-            if (T < want) continue;
-            const size_t lim = T == 256 ? kTwoCtaSmem : kMaxSmem;
-            if (SmemLayout((int)c->n, c->K, c->nsp, c->d, c->W, 2 * T, 2, T / 32, false, 0, 0, c->idx_bytes, true,
-                           hc != nullptr)
-                    .total <= lim) {
-                f.T = T;
-                break;
-            }
-        }
-        if (!f.T) return CWB_OK;
-        f.P = std::max(4, (int)std::max((c->K * c->n + f.T - 1) / f.T, (int64_t)(piece_factor() * c->n / c->n_star)));
-    } else if (!fused_shape(c, B, &f, bern)) {
-        return CWB_OK;  // does not fit: caller uses the general path
-    }
+    if (!train_shape(c, B, acc, hc != nullptr, bern, &f)) return CWB_OK;  // does not fit: general path
     int rc = CWB_OK;
     const bool have = (c->plan_pending && c->plan_T == f.T && c->plan_rb == f.RB) ||
                       (!c->plan_pending && c->fused_T == f.T && c->fused_rb == f.RB && c->plan);

@@ -128,6 +128,7 @@ struct cwb_ctx {
     int32_t h1_ev_used = 0;
     // plan pre-built during cwb_init on a side stream (cwb_config.batch_hint)
     int32_t batch_hint = 0;
+    int32_t train_hint = 0;  // cwb_config.train_hint: 0 CWB, 1 ACWB, 2 HCWB, 3 Bernoulli
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev_csr = nullptr, ev_plan = nullptr;
     int32_t* h_hdr = nullptr;  // pinned: plan header [0..7], device status [8]

@@ -37,7 +37,7 @@ class CwbError(RuntimeError):
 class cwb_config(C.Structure):
     _fields_ = [("n_star_rule", C.c_int32), ("n_star_fixed", C.c_int32), ("degree", C.c_int32),
                 ("n_knots", C.c_int32), ("df", C.c_double), ("df_kind", C.c_int32), ("batch_hint", C.c_int32),
-                ("unbinned", C.c_int32)]
+                ("unbinned", C.c_int32), ("train_hint", C.c_int32)]
 
 
 @dataclass
@@ -50,10 +50,11 @@ class Config:
     df_kind: int = 1
     batch_hint: int = 0  # expected B of the train calls: lets cwb_init pre-build the fused plan
     unbinned: int = 0    # 1: learners on the raw x (no binning), SURVEY NEXT-3
+    train_hint: int = 0  # the training call batch_hint is for: 0 cwb, 1 acwb, 2 hcwb, 3 bernoulli
 
     def c(self) -> cwb_config:
         return cwb_config(self.n_star_rule, self.n_star_fixed, self.degree, self.n_knots, self.df,
-                          self.df_kind, self.batch_hint, self.unbinned)
+                          self.df_kind, self.batch_hint, self.unbinned, self.train_hint)
 
 
 _lib = None

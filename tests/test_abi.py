@@ -44,6 +44,11 @@ def test_host_side_validation_without_gpu():
     cfg = cwb.cwb_config()
     lib.cwb_default_config(ctypes.byref(cfg))
     assert (cfg.n_star_rule, cfg.degree, cfg.n_knots, cfg.df, cfg.df_kind) == (0, 3, 20, 5.0, 1)
+    assert (cfg.batch_hint, cfg.unbinned, cfg.train_hint) == (0, 0, 0)
+    bad = cwb.cwb_config()
+    lib.cwb_default_config(ctypes.byref(bad))
+    bad.train_hint = 4  # out of range: rejected on the host before any device work
+    assert lib.cwb_init(ctypes.byref(h), ctypes.c_void_p(16), 10, 3, ctypes.byref(bad), None) == -1
     assert lib.cwb_version() >= 100
     assert b"empty" in lib.cwb_last_error(None) or lib.cwb_last_error(None)
 

@@ -125,3 +125,30 @@ def test_acwb_gamma_zero_and_edge_cases():
 @pytest.mark.slow
 def test_acwb_r3_sampled():
     check("R3", [0, 1], M=60)
+
+
+@pytest.mark.parametrize("algo", ["acwb", "bernoulli"])
+def test_train_hint_prebuilds_the_plan(algo):
+    """cwb_config.train_hint: cwb_init pre-builds the fused plan in the shape of the named training call, which
+    then launches only its training kernel; the results are bitwise those of a context built without the hint
+    (the plan is a pure function of the pool and the launch shape)."""
+    ds = S.make("R1", reps=range(256))
+    c = ds.cfg
+    Y = S.binary_targets(ds) if algo == "bernoulli" else ds.Y
+    outs, nl = [], []
+    for hint in (0, 1 if algo == "acwb" else 3):
+        gc = gpu_cfg_of(c)
+        gc.batch_hint, gc.train_hint = 256, hint
+        pg = cwb.Pool(dev(ds.X), gc)
+        pg.status()
+        l0 = pg.launches
+        if algo == "acwb":
+            out = pg.train_acwb(dev(Y), nu=c.nu, gamma=0.0034, M=20)
+        else:
+            out = pg.train_bernoulli(dev(Y), nu=c.nu, M=20)
+        pg.status()
+        nl.append(pg.launches - l0)
+        outs.append({k: host(v) for k, v in out.items()})
+    assert nl[1] < nl[0], nl  # with the hint: no plan rebuild inside the training call
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k
