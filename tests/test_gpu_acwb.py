@@ -141,13 +141,13 @@ def test_train_hint_prebuilds_the_plan(algo):
         gc.batch_hint, gc.train_hint = 256, hint
         pg = cwb.Pool(dev(ds.X), gc)
         pg.status()
-        l0 = pg.launches
+        l0 = pg.launches()
         if algo == "acwb":
             out = pg.train_acwb(dev(Y), nu=c.nu, gamma=0.0034, M=20)
         else:
             out = pg.train_bernoulli(dev(Y), nu=c.nu, M=20)
         pg.status()
-        nl.append(pg.launches - l0)
+        nl.append(pg.launches() - l0)
         outs.append({k: host(v) for k, v in out.items()})
     assert nl[1] < nl[0], nl  # with the hint: no plan rebuild inside the training call
     for k in outs[0]:
