@@ -2381,6 +2381,137 @@ __global__ void __launch_bounds__(256) k_gram_train(
 
 }  // namespace
 
+// idxT[i][k] = idx_k(i) as uint16, row-major with Kp (a multiple of 32) learners per row: the bins of one row
+// of all learners are contiguous (one or a few sectors), tile transpose through shared memory
+template <typename IdxT>
+__global__ void k_idx_rowmajor(const IdxT* __restrict__ idx, int64_t n, int K, int Kp, uint16_t* __restrict__ idxT) {
+    __shared__ uint16_t tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int k0 = blockIdx.y * 32;
+    for (int m = threadIdx.y; m < 32; m += blockDim.y) {
+        const int k = k0 + m;
+        const int64_t i = i0 + threadIdx.x;
+        tile[m][threadIdx.x] = (k < K && i < n) ? (uint16_t)idx[(size_t)k * n + i] : (uint16_t)0;
+    }
+    __syncthreads();
+    for (int m = threadIdx.y; m < 32; m += blockDim.y) {
+        const int64_t i = i0 + m;
+        if (i < n) idxT[(size_t)i * Kp + k0 + threadIdx.x] = tile[threadIdx.x][m];
+    }
+}
+
+// idxP[slot(k, k')][j] = idx_k'(perm_k[j]) for the learners k of the launch (blockIdx.y -> k = kb0 + y) and every
+// k' >= k; slot(k, k') = sum_{k'' in [kb0, k)} (K - k'') + k' - k.  A warp takes 32 consecutive positions j: it
+// reads the 32 rows' learner chunks from idxT (lanes over k', contiguous) into a shared tile and writes them
+// back with lanes over j (contiguous in idxP).
+template <typename PermT>
+__global__ void __launch_bounds__(256) k_gram_pregather(const uint16_t* __restrict__ idxT, const PermT* __restrict__ perm,
+                                                         int64_t n, int K, int Kp, int kb0,
+                                                         uint16_t* __restrict__ idxP) {
+    __shared__ uint16_t tile[8][32][34];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int k = kb0 + blockIdx.y;
+    size_t slot0 = 0;
+    for (int kk = kb0; kk < k; kk++) slot0 += (size_t)(K - kk);
+    const PermT* pk = perm + (size_t)k * n;
+    const int64_t ntile = (n + 31) / 32;
+    for (int64_t t = (int64_t)blockIdx.x * 8 + w; t < ntile; t += (int64_t)gridDim.x * 8) {
+        const int64_t j0 = t * 32;
+        const int64_t jm = j0 + lane;
+        const size_t irow = jm < n ? (size_t)pk[jm] : 0;
+        for (int c0 = k & ~31; c0 < K; c0 += 32) {
+#pragma unroll 8
+            for (int r = 0; r < 32; r++) {
+                const size_t ir = __shfl_sync(0xffffffffu, irow, r);
+                tile[w][lane][r] = idxT[ir * Kp + c0 + lane];
+            }
+            __syncwarp();
+            for (int q = 0; q < 32; q++) {
+                const int kp = c0 + q;
+                if (kp < k || kp >= K) continue;  // warp-uniform
+                if (jm < n) idxP[(slot0 + (size_t)(kp - k)) * n + jm] = tile[w][q][lane];
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Cross-Gram block of a pair of learners through their joint bin counts -- binMatMat's "counts times
+// design-point products" (G_k = Zb_k^T diag(c) Zb_k with c the bin counts) for two index vectors:
+//   (Z_k^T Z_k')[a][b] = sum_{l, l'} C[l][l'] Zb_k[l][a] Zb_k'[l'][b],   C[l][l'] = #{i : idx_k(i) = l, idx_k'(i) = l'}
+// (rows of one (l, l') cell have identical basis rows in both learners).  One CTA per pair k <= k',
+// bins of k in tiles of TL: the tile's rows are contiguous in the bin inversion perm_k; their idx_k' values are
+// counted into C[tile][n*] (u32 shared-memory atomics: integer, order-free), then
+//   V[l][b] = sum_{l' in window of b} C[l][l'] Zb_k'[l'][b]      (window-major basis ZT, lwin)
+//   acc[a][b] += sum_{l in tile, in window of a} Zb_k[l][a] V[l][b]   (thread (a, b), tiles ascending: fixed order)
+// The idx_k' values of the tile's rows are read from idxP: for every pair slot of the launch, idx_k' permuted into
+// the bin order of k (idxP[slot][j] = idx_k'(perm_k[j]), k_gram_pregather), so the counting pass is a coalesced
+// stream (a per-row gather of 2-byte values from idx_k' costs a 32-byte sector each and, at R4, thrashes L2).
+__global__ void __launch_bounds__(1024, 1) k_gram_joint(const uint16_t* __restrict__ idxP, int kb0,
+                                                         const int32_t* __restrict__ off, int64_t n, int K, int ns,
+                                                         int d, int TL, const double* __restrict__ ZT, int W,
+                                                         const int32_t* __restrict__ lwin, double* __restrict__ xg,
+                                                         int ld) {
+    extern __shared__ __align__(16) unsigned char gsm[];
+    const int hs = ns | 1;  // odd row stride: the lanes of stage 1 (consecutive bins of k) hit distinct banks
+    uint32_t* hist = reinterpret_cast<uint32_t*>(gsm);                                          // [TL][hs]
+    double* V = reinterpret_cast<double*>(gsm + (((size_t)TL * hs * 4 + 15) & ~(size_t)15));    // [TL][d]
+    int k = kb0, kp = 0;
+    {   // slot of the launch -> (k, k'), k' >= k (row k of the upper triangle holds K - k pairs), k from kb0
+        int rem = blockIdx.x;
+        while (rem >= K - k) { rem -= K - k; k++; }
+        kp = k + rem;
+    }
+    const uint16_t* ip = idxP + (size_t)blockIdx.x * n;
+    const int32_t* ok = off + (size_t)k * (ns + 1);
+    const double* ztk = ZT + (size_t)k * W * d;
+    const double* ztp = ZT + (size_t)kp * W * d;
+    const int32_t* lwk = lwin + (size_t)k * d * 2;
+    const int32_t* lwp = lwin + (size_t)kp * d * 2;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const bool own = tid < d * d;  // d <= CWB_MAX_D = 32: d^2 <= blockDim
+    const int a = tid / d, b = tid - a * d;
+    int lba = 0, lea = 0;
+    if (own) { lba = lwk[a * 2]; lea = lwk[a * 2 + 1]; }
+    double acc = 0.0;
+    for (int t0 = 0; t0 < ns; t0 += TL) {
+        const int t1 = min(ns, t0 + TL);
+        const int tlc = t1 - t0;
+        for (int e = tid; e < tlc * hs; e += blockDim.x) hist[e] = 0u;
+        __syncthreads();
+        for (int l = t0 + w; l < t1; l += nw) {  // a warp per bin of k, four gathers in flight per lane
+            const int j1 = ok[l + 1];
+            uint32_t* hl = hist + (size_t)(l - t0) * hs;
+            int j = ok[l] + lane;
+            for (; j + 96 < j1; j += 128) {
+                const int c0 = ip[j], c1 = ip[j + 32], c2 = ip[j + 64], c3 = ip[j + 96];
+                atomicAdd(&hl[c0], 1u);
+                atomicAdd(&hl[c1], 1u);
+                atomicAdd(&hl[c2], 1u);
+                atomicAdd(&hl[c3], 1u);
+            }
+            for (; j < j1; j += 32) atomicAdd(&hl[ip[j]], 1u);
+        }
+        __syncthreads();
+        for (int e = tid; e < tlc * d; e += blockDim.x) {  // lanes: consecutive bins of k, one basis b of k'
+            const int bb = e / tlc, tl = e - bb * tlc;
+            const int lb = lwp[bb * 2], len = lwp[bb * 2 + 1] - lb;
+            const uint32_t* hl = hist + (size_t)tl * hs + lb;
+            const double* zt = ztp + bb;
+            double sacc = 0.0;
+            for (int x = 0; x < len; x++) sacc = fma((double)hl[x], zt[x * d], sacc);
+            V[tl * d + bb] = sacc;
+        }
+        __syncthreads();
+        if (own) {
+            const int l0 = max(lba, t0), l1 = min(lea, t1);
+            for (int l = l0; l < l1; l++) acc = fma(ztk[(l - lba) * d + a], V[(l - t0) * d + b], acc);
+        }
+        __syncthreads();
+    }
+    if (own) xg[((size_t)k * d + a) * ld + (size_t)kp * d + b] = acc;
+}
+
 // lower blocks of the symmetric cross Gram from the upper ones: xg[(k,a)][(k',b)] = xg[(k',b)][(k,a)], k' < k
 __global__ void k_gram_sym(double* __restrict__ xg, int K, int d, int ld) {
     const int row = blockIdx.x, k = row / d;  // row = k d + a
@@ -2393,12 +2524,79 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
     const int K = c->K, d = c->d, ns = c->n_star;
     const int ld = (K * d + 63) / 64 * 64;  // whole 64-column tiles: the wide H1
     const int64_t n = c->n;
+    double *P = nullptr, *U = nullptr, *xg = nullptr, *Wt = nullptr;
+    // joint-bin-count build (k_gram_joint) when a tile of the count table fits shared memory; CWB_GRAM_JOINT=0
+    // keeps the gathered-basis build below (the A/B and the fallback for very large n*)
+    static const int joint_on = getenv("CWB_GRAM_JOINT") ? atoi(getenv("CWB_GRAM_JOINT")) : 1;
+    {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const size_t per_bin = (size_t)(ns | 1) * 4 + (size_t)d * 8;
+        const size_t budget = (size_t)std::max(0, optin - 2048);
+        int TL = (int)std::min<size_t>((size_t)ns, budget > 64 ? (budget - 64) / per_bin : 0);
+        if (joint_on && TL >= 1 && d * d <= 1024) {
+            const int ntile = (ns + TL - 1) / TL;
+            TL = (ns + ntile - 1) / ntile;
+            const size_t smem = (((size_t)TL * (ns | 1) * 4 + 15) & ~(size_t)15) + (size_t)TL * d * 8;
+            bool ok2 = cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
+            ok2 &= cwb_alloc((void**)&Wt, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
+            if (!ok2) {
+                cwb_release(xg, s); cwb_release(Wt, s);
+                return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
+            }
+            CWB_CUDA_TRY(c, cudaMemsetAsync(xg, 0, sizeof(double) * (size_t)K * d * ld, s));
+            // idx row-major (all learners' bins of a row adjacent), then per batch of learners k: the permuted
+            // index rows of its pairs (at most ~1 GiB at a time) and one CTA per pair
+            const int Kp = (K + 31) / 32 * 32;
+            const size_t slot_cap = std::max<size_t>((size_t)K, ((size_t)1 << 30) / ((size_t)n * 2));
+            uint16_t *idxT = nullptr, *idxP = nullptr;
+            const size_t slots_all = (size_t)K * (K + 1) / 2;
+            ok2 = cwb_alloc((void**)&idxT, sizeof(uint16_t) * (size_t)n * Kp, s) == cudaSuccess;
+            ok2 &= cwb_alloc((void**)&idxP, sizeof(uint16_t) * (size_t)n * std::min(slot_cap, slots_all), s) == cudaSuccess;
+            if (!ok2) {
+                cwb_release(idxT, s); cwb_release(idxP, s); cwb_release(xg, s); cwb_release(Wt, s);
+                return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
+            }
+            {
+                dim3 g((unsigned)((n + 31) / 32), (unsigned)(Kp / 32));
+                if (c->idx_bytes == 1) k_idx_rowmajor<uint8_t><<<g, dim3(32, 8), 0, s>>>((const uint8_t*)c->idx, n, K, Kp, idxT);
+                else k_idx_rowmajor<uint16_t><<<g, dim3(32, 8), 0, s>>>((const uint16_t*)c->idx, n, K, Kp, idxT);
+                c->launches++;
+            }
+            CWB_CUDA_TRY(c, cudaFuncSetAttribute(k_gram_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            for (int kb0 = 0; kb0 < K;) {
+                int kb1 = kb0;
+                size_t slots = 0;
+                while (kb1 < K && (kb1 == kb0 || slots + (size_t)(K - kb1) <= slot_cap)) slots += (size_t)(K - kb1++);
+                const unsigned gx = (unsigned)std::min<int64_t>(((n + 31) / 32 + 7) / 8, (int64_t)cwb_num_sms() * 8);
+                dim3 gp(gx, (unsigned)(kb1 - kb0));
+                if (c->perm_bytes == 2)
+                    k_gram_pregather<uint16_t><<<gp, 256, 0, s>>>(idxT, (const uint16_t*)c->perm, n, K, Kp, kb0, idxP);
+                else
+                    k_gram_pregather<uint32_t><<<gp, 256, 0, s>>>(idxT, (const uint32_t*)c->perm, n, K, Kp, kb0, idxP);
+                k_gram_joint<<<(unsigned)slots, 1024, smem, s>>>(idxP, kb0, c->off, n, K, ns, d, TL, c->ZT, c->W,
+                                                                 c->lwin, xg, ld);
+                c->launches += 2;
+                kb0 = kb1;
+            }
+            CWB_CUDA_TRY(c, cudaGetLastError());
+            cwb_release(idxT, s);
+            cwb_release(idxP, s);
+            k_gram_sym<<<K * d, 256, 0, s>>>(xg, K, d, ld);
+            k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
+            c->launches += 3;
+            cwb_release(xg, s);
+            c->xg = Wt;
+            c->xg_ld = ld;
+            return cwb_check_launch(c, "cross-Gram kernels (joint bin counts)");
+        }
+    }
     // the gathered basis P is built one H1 row chunk at a time (n x ld would be 16 GB at R4)
     int nch = 1;
     const int64_t CR = h1_chunk_plan(c, c->h1_wide ? 512 : 256, c->off, K, ns, &nch, s);
     if (CR < 0) return c->status ? c->status : CWB_ENOMEM;
     const int64_t prow = CR > 0 ? CR : n;
-    double *P = nullptr, *U = nullptr, *xg = nullptr, *Wt = nullptr;
     bool ok = cwb_alloc((void**)&P, sizeof(double) * (size_t)prow * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&U, sizeof(double) * (size_t)K * ns * ld, s) == cudaSuccess;
     ok &= cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
