@@ -2450,12 +2450,16 @@ __global__ void __launch_bounds__(256) k_gram_pregather(const uint16_t* __restri
 __global__ void __launch_bounds__(1024, 1) k_gram_joint(const uint16_t* __restrict__ idxP, int kb0,
                                                          const int32_t* __restrict__ off, int64_t n, int K, int ns,
                                                          int d, int TL, const double* __restrict__ ZT, int W,
-                                                         const int32_t* __restrict__ lwin, double* __restrict__ xg,
-                                                         int ld) {
+                                                         const int32_t* __restrict__ lwin,
+                                                         const double* __restrict__ Zb, const double* __restrict__ G,
+                                                         double* __restrict__ xg, int ld) {
     extern __shared__ __align__(16) unsigned char gsm[];
     const int hs = ns | 1;  // odd row stride: the lanes of stage 1 (consecutive bins of k) hit distinct banks
     uint32_t* hist = reinterpret_cast<uint32_t*>(gsm);                                          // [TL][hs]
     double* V = reinterpret_cast<double*>(gsm + (((size_t)TL * hs * 4 + 15) & ~(size_t)15));    // [TL][d]
+    double* zks = V + (size_t)TL * d;             // [TL][d]  Zb_k rows of the tile
+    double* zps = zks + (size_t)TL * d;           // [W][d]   window-major basis of k' (read every tile)
+    int32_t* oks = reinterpret_cast<int32_t*>(zps + (size_t)W * d);                              // [TL + 1] bin starts
     int k = kb0, kp = 0;
     {   // slot of the launch -> (k, k'), k' >= k (row k of the upper triangle holds K - k pairs), k from kb0
         int rem = blockIdx.x;
@@ -2464,49 +2468,78 @@ __global__ void __launch_bounds__(1024, 1) k_gram_joint(const uint16_t* __restri
     }
     const uint16_t* ip = idxP + (size_t)blockIdx.x * n;
     const int32_t* ok = off + (size_t)k * (ns + 1);
-    const double* ztk = ZT + (size_t)k * W * d;
     const double* ztp = ZT + (size_t)kp * W * d;
-    const int32_t* lwk = lwin + (size_t)k * d * 2;
+    const double* zbk = Zb + (size_t)k * ns * d;
     const int32_t* lwp = lwin + (size_t)kp * d * 2;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    const int tid = threadIdx.x;
     const bool own = tid < d * d;  // d <= CWB_MAX_D = 32: d^2 <= blockDim
     const int a = tid / d, b = tid - a * d;
-    int lba = 0, lea = 0;
-    if (own) { lba = lwk[a * 2]; lea = lwk[a * 2 + 1]; }
+    if (kp == k) {  // Z_k^T Z_k = G_k (binMatMat, I6): already in the pool
+        if (own) xg[((size_t)k * d + a) * ld + (size_t)kp * d + b] = G[(size_t)k * d * d + tid];
+        return;
+    }
+    for (int e = tid; e < W * d; e += blockDim.x) zps[e] = ztp[e];
     double acc = 0.0;
     for (int t0 = 0; t0 < ns; t0 += TL) {
         const int t1 = min(ns, t0 + TL);
         const int tlc = t1 - t0;
         for (int e = tid; e < tlc * hs; e += blockDim.x) hist[e] = 0u;
+        for (int e = tid; e <= tlc; e += blockDim.x) oks[e] = ok[t0 + e];
+        for (int e = tid; e < tlc * d; e += blockDim.x) zks[e] = zbk[(size_t)t0 * d + e];
         __syncthreads();
-        for (int l = t0 + w; l < t1; l += nw) {  // a warp per bin of k, four gathers in flight per lane
-            const int j1 = ok[l + 1];
-            uint32_t* hl = hist + (size_t)(l - t0) * hs;
-            int j = ok[l] + lane;
-            for (; j + 96 < j1; j += 128) {
-                const int c0 = ip[j], c1 = ip[j + 32], c2 = ip[j + 64], c3 = ip[j + 96];
-                atomicAdd(&hl[c0], 1u);
-                atomicAdd(&hl[c1], 1u);
-                atomicAdd(&hl[c2], 1u);
-                atomicAdd(&hl[c3], 1u);
+        // the tile's rows are contiguous in the bin order of k: threads stride over aligned groups of 8 rows (one
+        // 16-byte load each, four in flight: a tile costs one or two DRAM round trips), balanced whatever the bin
+        // sizes; each thread's bin pointer only moves forward.  Groups may start up to 7 rows before the tile /
+        // end after it (masked; idxP is allocated with 16 bytes of slack on both sides).
+        {
+            const int jb = oks[0], je = oks[tlc];
+            const int sh = (int)(((16 - ((uintptr_t)ip & 15)) & 15) >> 1);  // rows to the first 16-byte boundary
+            const int g0 = (jb - sh + 8) / 8 - 1, g1 = (je - sh + 7) / 8;   // groups [g0, g1) cover [jb, je)
+            int l = 0;
+            for (int g = g0 + tid; g < g1; g += 4 * 1024) {
+                uint4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (g + u * 1024 < g1) v[u] = *reinterpret_cast<const uint4*>(ip + sh + 8 * (int64_t)(g + u * 1024));
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if (g + u * 1024 >= g1) break;
+                    const int r0 = sh + 8 * (g + u * 1024);
+                    const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                    while (r0 >= oks[l + 1]) l++;  // (r0 < jb on the first group: l stays 0)
+                    if (r0 >= jb && r0 + 7 < min(je, oks[l + 1])) {  // the whole group inside one bin of the tile
+                        uint32_t* hl = hist + (size_t)l * hs;
+#pragma unroll
+                        for (int e = 0; e < 8; e++)
+                            atomicAdd(&hl[(e & 1) ? (wv[e >> 1] >> 16) : (wv[e >> 1] & 0xffffu)], 1u);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; e++) {
+                            const int jj = r0 + e;
+                            if (jj < jb || jj >= je) continue;
+                            const uint32_t cv = (e & 1) ? (wv[e >> 1] >> 16) : (wv[e >> 1] & 0xffffu);
+                            while (jj >= oks[l + 1]) l++;
+                            atomicAdd(&hist[(size_t)l * hs + cv], 1u);
+                        }
+                    }
+                }
             }
-            for (; j < j1; j += 32) atomicAdd(&hl[ip[j]], 1u);
         }
         __syncthreads();
         for (int e = tid; e < tlc * d; e += blockDim.x) {  // lanes: consecutive bins of k, one basis b of k'
             const int bb = e / tlc, tl = e - bb * tlc;
             const int lb = lwp[bb * 2], len = lwp[bb * 2 + 1] - lb;
             const uint32_t* hl = hist + (size_t)tl * hs + lb;
-            const double* zt = ztp + bb;
+            const double* zt = zps + bb;
             double sacc = 0.0;
-            for (int x = 0; x < len; x++) sacc = fma((double)hl[x], zt[x * d], sacc);
+            // u32 -> double by the 2^52 bit pattern and one subtraction (exact; the FP64 pipe instead of I2F.F64)
+            for (int x = 0; x < len; x++)
+                sacc = fma(__hiloint2double(0x43300000, (int)hl[x]) - 4503599627370496.0, zt[x * d], sacc);
             V[tl * d + bb] = sacc;
         }
         __syncthreads();
-        if (own) {
-            const int l0 = max(lba, t0), l1 = min(lea, t1);
-            for (int l = l0; l < l1; l++) acc = fma(ztk[(l - lba) * d + a], V[(l - t0) * d + b], acc);
-        }
+        if (own)  // Zb_k[l][a] is 0 outside the window of a: the whole tile in bin order
+            for (int tl = 0; tl < tlc; tl++) acc = fma(zks[tl * d + a], V[tl * d + b], acc);
         __syncthreads();
     }
     if (own) xg[((size_t)k * d + a) * ld + (size_t)kp * d + b] = acc;
@@ -2532,13 +2565,16 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        const size_t per_bin = (size_t)(ns | 1) * 4 + (size_t)d * 8;
-        const size_t budget = (size_t)std::max(0, optin - 2048);
+        const size_t per_bin = (size_t)(ns | 1) * 4 + (size_t)d * 16 + 4;
+        const size_t budget = (size_t)std::max<int64_t>(0, (int64_t)optin - 2048 - (int64_t)c->W * d * 8);
         int TL = (int)std::min<size_t>((size_t)ns, budget > 64 ? (budget - 64) / per_bin : 0);
         if (joint_on && TL >= 1 && d * d <= 1024) {
-            const int ntile = (ns + TL - 1) / TL;
-            TL = (ns + ntile - 1) / ntile;
-            const size_t smem = (((size_t)TL * (ns | 1) * 4 + 15) & ~(size_t)15) + (size_t)TL * d * 8;
+            // whole rounds of the 1024 threads in the (bin, basis) contraction; then equal tiles
+            const int q = std::max(1, 1024 / d);
+            if (TL >= q && TL < ns) TL = TL / q * q;
+            else if (TL < ns) TL = (ns + (ns + TL - 1) / TL - 1) / ((ns + TL - 1) / TL);
+            const size_t smem = (((size_t)TL * (ns | 1) * 4 + 15) & ~(size_t)15) + (size_t)TL * d * 16 +
+                                (size_t)c->W * d * 8 + (size_t)(TL + 1) * 4 + 16;
             bool ok2 = cwb_alloc((void**)&xg, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
             ok2 &= cwb_alloc((void**)&Wt, sizeof(double) * (size_t)K * d * ld, s) == cudaSuccess;
             if (!ok2) {
@@ -2553,9 +2589,11 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
             uint16_t *idxT = nullptr, *idxP = nullptr;
             const size_t slots_all = (size_t)K * (K + 1) / 2;
             ok2 = cwb_alloc((void**)&idxT, sizeof(uint16_t) * (size_t)n * Kp, s) == cudaSuccess;
-            ok2 &= cwb_alloc((void**)&idxP, sizeof(uint16_t) * (size_t)n * std::min(slot_cap, slots_all), s) == cudaSuccess;
+            uint16_t* idxP_base = nullptr;  // 16 bytes of slack before and after the slots (k_gram_joint's aligned loads)
+            ok2 &= cwb_alloc((void**)&idxP_base, sizeof(uint16_t) * ((size_t)n * std::min(slot_cap, slots_all) + 16), s) == cudaSuccess;
+            idxP = idxP_base ? idxP_base + 8 : nullptr;
             if (!ok2) {
-                cwb_release(idxT, s); cwb_release(idxP, s); cwb_release(xg, s); cwb_release(Wt, s);
+                cwb_release(idxT, s); cwb_release(idxP_base, s); cwb_release(xg, s); cwb_release(Wt, s);
                 return cwb_set_error(c, CWB_ENOMEM, "cross-Gram workspace allocation failed");
             }
             {
@@ -2576,13 +2614,13 @@ static int gram_build(cwb_ctx* c, cudaStream_t s) {
                 else
                     k_gram_pregather<uint32_t><<<gp, 256, 0, s>>>(idxT, (const uint32_t*)c->perm, n, K, Kp, kb0, idxP);
                 k_gram_joint<<<(unsigned)slots, 1024, smem, s>>>(idxP, kb0, c->off, n, K, ns, d, TL, c->ZT, c->W,
-                                                                 c->lwin, xg, ld);
+                                                                 c->lwin, c->Zb, c->G, xg, ld);
                 c->launches += 2;
                 kb0 = kb1;
             }
             CWB_CUDA_TRY(c, cudaGetLastError());
             cwb_release(idxT, s);
-            cwb_release(idxP, s);
+            cwb_release(idxP_base, s);
             k_gram_sym<<<K * d, 256, 0, s>>>(xg, K, d, ld);
             k_gram_w<<<K * d, 256, 0, s>>>(xg, c->Ainv, K, d, ld, Wt);
             c->launches += 3;

@@ -132,6 +132,33 @@ def test_gram_edge_cases_and_errors():
     assert e.value.name == "CWB_ENONFINITE"
 
 
+@pytest.mark.parametrize("seed,n,K,degree,n_knots,ns_fixed", [
+    (11, 1237, 5, 3, 20, 0),     # odd n (the pairs' index rows start at every 2-byte alignment), sqrt rule
+    (12, 4001, 7, 2, 6, 300),    # u16 bins, degree 2, few knots (wide windows), several bin tiles per pair
+    (13, 997, 4, 1, 9, 40),      # degree 1
+    (14, 70001, 3, 3, 20, 0),    # 32-bit row ids, n* = 265
+])
+def test_gram_joint_build_edge_shapes(seed, n, K, degree, n_knots, ns_fixed):
+    """The cross-Gram blocks come from the joint bin counts of learner pairs (k_gram_joint): ragged n,
+    clamped learners (a feature with few distinct values: n*_k < n*), both index widths and row-id widths,
+    B-spline degrees 1-3 -- path 3 against the oracle's Alg. 1, tie rule 1e-12."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((K, n))
+    X[1] = rng.integers(0, 7, n).astype(np.float64)          # 7 distinct values: clamped n*_k
+    X[K - 1] = np.round(X[0] * 3.0) / 3.0 + 0.01 * X[K - 1]   # strongly dependent on learner 0: dense count cells
+    B, M, nu = 6, 40, 0.1
+    Y = np.sin(X[0]) + 0.5 * X[2] ** 2 + 0.3 * rng.standard_normal((B, n))
+    kw = dict(n_star_rule=2 if ns_fixed else 0, n_star_fixed=ns_fixed, n_knots=n_knots, degree=degree, df=4.0)
+    pg = cwb.Pool(dev(X), cwb.Config(**kw))
+    pg.set_path(3)
+    out = pg.train(dev(Y), nu=nu, M=M)
+    pg.status()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    po = O.Pool(X, O.Config(**kw), O.MODE_BINNED)
+    fol = follow_parity(g, po, Y, nu, M, f"gram joint n={n} K={K} deg={degree}")
+    assert fol.sum() <= 1
+    pg.close()
+
 
 @pytest.mark.slow
 def test_gram_equals_direct_path_r3_all_replications():
