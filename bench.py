@@ -390,12 +390,18 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
     p.close()
     t_x = t_first0 - t_m0
     t_it = t_mm - t_m0
-    # dominant phase = the cross-Gram build: binMatVec of learner k over the gathered basis columns of the
-    # 64-column tiles that hold learners k' >= k (the upper blocks of the symmetric Z^T Z), 8 B gathered per add
-    ld = (K * p_d + 63) // 64 * 64
-    adds_x = n * sum(ld - 64 * ((k * p_d) // 64) for k in range(K))
-    dadd = float(peaks["dadd_tops"]) * 1e12
-    l2 = float(peaks.get("l2_read_gbs", 0.0)) * 1e9
+    # dominant phase = the cross-Gram build through the joint bin counts of the K (K - 1) / 2 learner pairs
+    # (k_idx_rowmajor, k_gram_pregather, k_gram_joint): per pair n integer increments
+    # (u32 shared-memory atomics) and 6 n bytes of index traffic (the permuted index row read from the
+    # row-major copy, written once, streamed once by the count pass); the contraction is O(n* d W) per pair
+    pairs = K * (K - 1) // 2
+    counts = pairs * n
+    bytes_x = 6.0 * pairs * n
+    n_sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    atoms_rate = 8.54 * n_sms * sm_hz   # measured u32 ATOMS.ADD rate, random of 1000 bins (profiles/r2h_ubench_atoms.txt)
+    hbm = float(peaks["hbm_gbs"]) * 1e9
+    t_atoms, t_hbm = counts / atoms_rate, bytes_x / hbm
     return {"path": "cross-Gram (cwb_set_path 3): s_k -= nu Z_k^T Z_k* theta*, exact reformulation of Alg. 1 for "
                     "L2 loss; parity tests/test_gpu_gram.py (R0-R3 vs the oracle, tie rule 1e-12)",
             "ms_per_step": ms, "ms_per_step_mean": ms_mean, "steps_timed": len(ts),
@@ -403,12 +409,13 @@ def gram_path(X, Y, cfg, gcfg, flush, stream, peaks, args, direct_ms):
             "speedup_vs_direct": direct_ms / ms,
             "phases_ms": {"xgram_build": t_x, "theta0_binmatvec": t_m0, "iterations": t_it,
                           "iteration_us": t_it / max(M, 1) * 1e3},
-            "roofline": {"kernel": "cross-Gram build (H1 + H2 over the gathered basis columns of all learners)",
-                         "bound": "alu", "adds": adds_x, "achieved": adds_x / (t_x * 1e-3) / 1e12,
-                         "peak": dadd / 1e12, "unit": "TFLOP/s", "frac": adds_x / (t_x * 1e-3) / dadd,
-                         "l2_gather_frac": (8.0 * adds_x / (t_x * 1e-3) / l2) if l2 else None,
-                         "note": "time from the difference of a fresh and a cached pool (M = 0); of the "
-                                 f"{ld} gathered columns 1/6 are non-zero (4 B-spline values per learner block)"}}
+            "roofline": {"kernel": "cross-Gram build (k_gram_pregather + k_gram_joint: joint bin counts of learner pairs)",
+                         "bound": "hbm" if t_hbm >= t_atoms else "alu", "counts": counts, "bytes": bytes_x,
+                         "t_atoms_ms": t_atoms * 1e3, "t_hbm_ms": t_hbm * 1e3, "t_kernel_ms": t_x,
+                         "achieved": bytes_x / (t_x * 1e-3) / 1e9, "peak": hbm / 1e9, "unit": "GB/s",
+                         "frac": max(t_atoms, t_hbm) / (t_x * 1e-3),
+                         "note": "time from the difference of a fresh and a cached pool (M = 0); roofline time = "
+                                 "max(index bytes / HBM, increments / measured u32 shared-atomic rate)"}}
 
 
 def workload_config(c, n_star, d):
