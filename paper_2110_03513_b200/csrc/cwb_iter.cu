@@ -2420,11 +2420,14 @@ __global__ void __launch_bounds__(256) k_gram_pregather(const uint16_t* __restri
         const int64_t jm = j0 + lane;
         const size_t irow = jm < n ? (size_t)pk[jm] : 0;
         for (int c0 = k & ~31; c0 < K; c0 += 32) {
-#pragma unroll 8
+            uint16_t vals[32];  // all 32 row loads in flight before the tile stores
+#pragma unroll
             for (int r = 0; r < 32; r++) {
                 const size_t ir = __shfl_sync(0xffffffffu, irow, r);
-                tile[w][lane][r] = idxT[ir * Kp + c0 + lane];
+                vals[r] = idxT[ir * Kp + c0 + lane];
             }
+#pragma unroll
+            for (int r = 0; r < 32; r++) tile[w][lane][r] = vals[r];
             __syncwarp();
             for (int q = 0; q < 32; q++) {
                 const int kp = c0 + q;
