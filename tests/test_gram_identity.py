@@ -56,3 +56,24 @@ def test_cross_gram_recurrence_reproduces_alg1(name, reps, M):
     assert np.allclose(sse, ref.sse_trace, rtol=1e-9, atol=1e-12 * np.abs(ref.sse_trace).max())
     assert np.allclose(risk, ref.risk_trace, rtol=1e-9)
     assert np.allclose(agg, ref.theta_agg, rtol=1e-9, atol=1e-12 * np.abs(ref.theta_agg).max())
+
+
+def test_cross_gram_block_from_joint_bin_counts():
+    """The identity behind the cross-Gram build (k_gram_joint), independent of the CUDA code: rows of one cell
+    (l, l') of a pair of binned learners have identical basis rows in both, so
+        Z_k^T Z_k' = Zb_k^T C Zb_k',   C[l][l'] = #{i : idx_k(i) = l, idx_k'(i) = l'}
+    -- binMatMat's counts-times-design-point-products (G_k = Zb_k^T diag(c) Zb_k) for two index
+    vectors; for k' = k, C is diag(bin counts) and the block is G_k."""
+    ds = S.make("R1", reps=[0])
+    pool = O.Pool(ds.X, O.Config(), O.MODE_BINNED)
+    K, ns = pool.K, pool.n_star
+    for k in range(K):
+        for kp in (k, (k + 1) % K, (k + 3) % K):
+            Cn = np.zeros((ns, ns))
+            np.add.at(Cn, (pool.idx[k].astype(np.int64), pool.idx[kp].astype(np.int64)), 1.0)
+            assert Cn.sum() == pool.n
+            blk = pool.Zb[k].T @ Cn @ pool.Zb[kp]
+            ref = pool.Zb[k][pool.idx[k]].T @ pool.Zb[kp][pool.idx[kp]]
+            assert np.allclose(blk, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+            if kp == k:
+                assert np.allclose(blk, pool.G[k], rtol=1e-12, atol=1e-12 * np.abs(ref).max())
