@@ -2418,22 +2418,22 @@ __global__ void __launch_bounds__(256) k_gram_pregather(const uint16_t* __restri
     for (int64_t t = (int64_t)blockIdx.x * 8 + w; t < ntile; t += (int64_t)gridDim.x * 8) {
         const int64_t j0 = t * 32;
         const int64_t jm = j0 + lane;
-        const size_t irow = jm < n ? (size_t)pk[jm] : 0;
-        for (int c0 = k & ~31; c0 < K; c0 += 32) {
+        const uint32_t irow = jm < n ? (uint32_t)pk[jm] : 0u;  // row ids fit 32 bits (off is int32)
+        // learner chunks start at k (not at a multiple of 32): no lanes spent on learners k' < k
+        for (int c0 = k; c0 < K; c0 += 32) {
+            const int cl = min(c0 + lane, Kp - 1);  // (columns >= K are padding; never written out)
             uint16_t vals[32];  // all 32 row loads in flight before the tile stores
 #pragma unroll
             for (int r = 0; r < 32; r++) {
-                const size_t ir = __shfl_sync(0xffffffffu, irow, r);
-                vals[r] = idxT[ir * Kp + c0 + lane];
+                const uint32_t ir = __shfl_sync(0xffffffffu, irow, r);
+                vals[r] = idxT[(size_t)ir * Kp + cl];
             }
 #pragma unroll
             for (int r = 0; r < 32; r++) tile[w][lane][r] = vals[r];
             __syncwarp();
-            for (int q = 0; q < 32; q++) {
-                const int kp = c0 + q;
-                if (kp < k || kp >= K) continue;  // warp-uniform
-                if (jm < n) idxP[(slot0 + (size_t)(kp - k)) * n + jm] = tile[w][q][lane];
-            }
+            const int qn = min(32, K - c0);
+            for (int q = 0; q < qn; q++)
+                if (jm < n) idxP[(slot0 + (size_t)(c0 + q - k)) * n + jm] = tile[w][q][lane];
             __syncwarp();
         }
     }
